@@ -1,0 +1,422 @@
+#!/usr/bin/env python3
+"""bench.py — CPI hot path on B200: frames -> Gamma (Eq. 1) -> refocused plane stack.
+
+One *step* = one pass of the whole hot path over one batch:
+  N frames resident in HBM -> expand + marginals (KB1) -> S_ab on tcgen05 kind::i8 with
+  the fused exact normalisation (KB2) -> fp32 Gamma -> refocus into a P-plane stack
+  (KB5a/KB5/KB6).
+Workload at N=1 (BASELINE.json configs[1] + configs[3]): SwissSPAD2 256x512 frames,
+rho_a = left 256x256 half, rho_b = right 256x256 half, 10^4
+Bernoulli(0.05) frames per step, 64 refocus planes alpha = linspace(0.5, 2, 64).
+Metric: frames/s into Gamma (whole step), with the correlation-only frames/s, planes/s and
+the two kernels' roofline fractions alongside.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cb200|reference]
+Multi-GPU: launched by torch.distributed.run; frames shard across ranks (weak scaling:
+10^4 frames per rank), NCCL all-reduce + reduce-scatter of the sums, refocus of each
+rank's Gamma rows, all-reduce of the planes (paper_2407_20692_b200.parallel).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import synth  # noqa: E402
+
+METRIC = "frames/s into Gamma (and % int8 TC peak); refocused planes/s (% HBM BW)"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="cb200", choices=["cb200", "reference"])
+    p.add_argument("--frames", type=int, default=10_000, help="frames per step per rank")
+    p.add_argument("--planes", type=int, default=64, help="refocus planes per step")
+    p.add_argument("--occupancy", type=float, default=0.05, help="Bernoulli f of the synthetic bits")
+    p.add_argument("--variant", default="tc", choices=["tc", "popc"])
+    p.add_argument("--roi", default="full", choices=["full", "128", "tiny"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-rows", type=int, default=8, help="oracle sample: A pixels (rows of S_ab)")
+    p.add_argument("--cpu-pixels", type=int, default=8, help="oracle sample: refocused output pixels")
+    return p.parse_args()
+
+
+def rois(name):
+    if name == "full":
+        return synth.ROI_FULL_A, synth.ROI_FULL_B
+    if name == "128":
+        return synth.ROI_128_A, synth.ROI_128_B
+    return synth.ROI_TINY_A, synth.ROI_TINY_B
+
+
+def load_peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks ----------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 0]
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(power) if power else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------ roofline helpers -------
+def refocus_span_bytes(dims, alphas, row_range=None):
+    """Algorithmic bytes of refocus stage 1 per plane: 4 B x the Gamma entries inside the
+    separable stencil span, (sum_u |J_u|) * (sum_v |M_v|), J_u = [min j0, max j0 + 1] over
+    the outputs x that use column u (and M_v likewise) — SURVEY §8(d) 'per unit of work'."""
+    Wa, Ha, Wb, Hb = dims
+
+    def axis(W, Wb_, alpha):
+        c, cb = (W - 1) / 2.0, (Wb_ - 1) / 2.0
+        x = np.arange(W, dtype=np.float64)[None, :]
+        u = np.arange(Wb_, dtype=np.float64)[:, None]
+        cc = (alpha * (x - c)) + ((1.0 - alpha) * (u - cb)) + c
+        ok = (cc >= 0) & (cc <= W - 1)
+        j0 = np.minimum(np.floor(cc), W - 2)
+        lo = np.where(ok, j0, np.inf).min(1)
+        hi = np.where(ok, j0 + 1, -np.inf).max(1)
+        span = np.where(hi >= lo, hi - lo + 1, 0)
+        return span
+
+    total = 0.0
+    for a in alphas:
+        sx = axis(Wa, Wb, a).sum()
+        sy = axis(Ha, Hb, a)
+        total += 4.0 * sx * sy.sum()
+    return total
+
+
+# ------------------------------------------------------------------ CPU baseline ----------
+def cpu_baseline(frames_np, roi_a, roi_b, alphas, n_rows, n_pix, step_planes):
+    """The oracle as it stands, on a bounded sample of the same workload (rank 0, N=1)."""
+    import oracle
+    oracle.build()
+    cores = os.cpu_count() or 1
+    n = frames_np.shape[0]
+    p_a = roi_a[2] * roi_a[3]
+    rows = np.linspace(0, p_a - 1, n_rows).astype(np.int64)
+    t0 = time.perf_counter()
+    s_a = oracle.marginals(frames_np, roi_a)
+    s_b = oracle.marginals(frames_np, roi_b)
+    s_ab = oracle.pair_sums(frames_np, roi_a, roi_b, rows=rows, threads=cores)
+    g = oracle.gamma(s_ab, s_a[rows], s_b, n)
+    t_corr = time.perf_counter() - t0
+    # refocus sample: n_pix output pixels of one plane, on a Gamma whose sampled rows are
+    # the oracle's own; the rest is filled with the same rows (cost is data-independent)
+    Wa, Ha, Wb, Hb = roi_a[2], roi_a[3], roi_b[2], roi_b[3]
+    G = np.empty((p_a, Wb * Hb), dtype=np.float32)
+    G[:] = g[np.arange(p_a) % n_rows].astype(np.float32)
+    rng = np.random.default_rng(0)
+    pix = np.stack([rng.integers(0, Wa, n_pix), rng.integers(0, Ha, n_pix)], 1)
+    alpha = float(alphas[len(alphas) // 3])
+    t0 = time.perf_counter()
+    oracle.refocus(G, (Wa, Ha, Wb, Hb), [alpha], pixels=pix, threads=cores)
+    t_ref = time.perf_counter() - t0
+    # the marginals are O(N P) and already complete; pair sums scale with rows
+    est_step = t_corr * (p_a / n_rows) + t_ref * (Wa * Ha / n_pix) * step_planes
+    return {"value": n / est_step, "unit": "frames/s", "cores": cores, "kind": "oracle",
+            "sample": (f"{n_rows} of {p_a} A pixels x all {Wb*Hb} B pixels x all {n} frames "
+                       f"({t_corr:.1f} s) + {n_pix} of {Wa*Ha} output pixels of 1 of {step_planes} "
+                       f"planes ({t_ref:.1f} s); step time extrapolated linearly by rows/pixels/planes"),
+            "extrapolated_step_s": est_step}
+
+
+# ------------------------------------------------------------------ reference arm ---------
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    roi_a, roi_b = rois(args.roi)
+    alphas = synth.alpha_grid(args.planes)
+    frames = synth.bernoulli_frames(args.frames, args.occupancy, seed=synth.SEED_ARMS)
+    vals = []
+    last = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(frames, roi_a, roi_b, alphas, max(1, args.cpu_rows // 2),
+                         max(1, args.cpu_pixels // 2), args.planes)
+        if i >= args.warmup:
+            vals.append(r["value"])
+            last = r
+    v = float(np.median(vals))
+    last["value"] = v
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "frames/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "int64/f64", "data": "synthetic",
+           "config": {"workload": f"configs[1]+configs[3]: {args.frames} frames, RoI {roi_a}/{roi_b}, "
+                                  f"{args.planes} planes", "frames_per_step": args.frames,
+                      "planes_per_step": args.planes},
+           "cpu_baseline": last,
+           "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+# ------------------------------------------------------------------ main arm --------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torch.distributed.run (one rank per GPU)")
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2407_20692_b200 import Context
+    from paper_2407_20692_b200._lib import KC_GEMM, KC_EXPAND, KC_STAGE1, KC_STAGE2, KC_COORDS, KC_FINALIZE
+    from paper_2407_20692_b200 import parallel
+
+    roi_a, roi_b = rois(args.roi)
+    p_a, p_b = roi_a[2] * roi_a[3], roi_b[2] * roi_b[3]
+    Wa, Ha, Wb, Hb = roi_a[2], roi_a[3], roi_b[2], roi_b[3]
+    alphas = synth.alpha_grid(args.planes)
+    n = args.frames
+    # this rank's slice of the global frame sequence (weak scaling: n frames per rank)
+    frames_np = synth.bernoulli_frames(n, args.occupancy, seed=synth.SEED_ARMS, frame0=rank * n)
+    frames_host = torch.from_numpy(frames_np).pin_memory()
+    frames_dev = frames_host.to(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    keep = world > 1
+    ctx = Context(roi_a, roi_b, n, device=local, variant=args.variant, keep_counts=keep)
+    gamma = ctx.new_gamma() if world == 1 else None
+    planes = ctx.new_planes(args.planes)
+    planes_host = torch.empty(planes.shape, dtype=torch.float32).pin_memory()
+    if world > 1:
+        row0, rows = parallel.row_shard(Wa, Ha, rank, world)
+        s_ab = torch.empty((p_a, p_b), dtype=torch.int32, device=dev)
+        s_a = torch.empty(p_a, dtype=torch.int32, device=dev)
+        s_b = torch.empty(p_b, dtype=torch.int32, device=dev)
+        gamma_rows = torch.empty((rows, p_b), dtype=torch.float32, device=dev)
+        marg = torch.empty(p_a + p_b + 1, dtype=torch.int64, device=dev)
+        s_ab_rows = torch.empty((rows, p_b), dtype=torch.int32, device=dev)
+
+    def step(src):
+        """one pass of a1..a6; src = device frames (resident) or pinned host frames (e2e)"""
+        if world == 1:
+            ctx.load_frames(src)
+            ctx.correlate(gamma)
+            ctx.refocus(alphas, gamma, planes)
+            return
+        ctx.reset()
+        ctx.load_frames(src)
+        ctx.correlate(None)
+        ctx.get_counts(s_ab, s_a, s_b)
+        marg[:p_a].copy_(s_a)
+        marg[p_a:p_a + p_b].copy_(s_b)
+        marg[-1].fill_(n)
+        dist.all_reduce(marg)
+        dist.reduce_scatter_tensor(s_ab_rows, s_ab)
+        ctx.finalize_counts(s_ab_rows, row0, marg[:p_a].to(torch.int32), marg[p_a:p_a + p_b].to(torch.int32),
+                            n * world, gamma_rows)
+        ctx.refocus(alphas, gamma_rows, planes, row0=row0, rows=rows)
+        dist.all_reduce(planes)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step(frames_dev)
+    barrier()
+
+    clocks = ClockSampler(local)
+    ctx.set_timing(True)
+    launches0 = ctx.launch_count()
+    clocks.start()
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(frames_dev)
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    launches = ctx.launch_count() - launches0
+    t_ms = ev0.elapsed_time(ev1)
+    kt = {k: ctx.kernel_time_ms(c) for k, c in (("gemm", KC_GEMM), ("expand", KC_EXPAND), ("stage1", KC_STAGE1),
+                                                 ("stage2", KC_STAGE2), ("coords", KC_COORDS),
+                                                 ("finalize", KC_FINALIZE))}
+    ctx.set_timing(False)
+    if world > 1:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    ms_step = t_ms / args.steps
+    value = n * world / (ms_step / 1e3)
+
+    # ---- end to end through the public API with host buffers --------------------------
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(1):
+            step(frames_host)
+            planes_host.copy_(planes, non_blocking=True)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(frames_host)
+            planes_host.copy_(planes, non_blocking=True)
+        e1.record(stream)
+        barrier()
+        te = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([te], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": n * world / (te / args.steps / 1e3), "unit": "frames/s",
+               "h2d_bytes_per_step": int(frames_np.nbytes), "d2h_bytes_per_step": int(planes.numel() * 4),
+               "ms_per_step": te / args.steps}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peaks, peak_src = load_peaks()
+    int8_sustained = 2.0 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])   # TOPS, i8 = 2 x bf16
+    int8_burst = 2.0 * peaks["bf16_tflops"]
+    hbm = peaks["hbm_gbs"]
+    gemm_ms, gemm_n = kt["gemm"]
+    ops = 2.0 * p_a * p_b * n                         # algorithmic: one AND/MAC per pair per frame
+    gemm_tops = ops / (gemm_ms / gemm_n / 1e3) / 1e12 if gemm_n else None
+    s1_ms, s1_n = kt["stage1"]
+    rows_here = p_a if world == 1 else p_a // world
+    span = refocus_span_bytes((Wa, Ha, Wb, Hb), alphas) * rows_here / p_a   # per step
+    s1_gbs = span / (s1_ms / (s1_n / args.planes) / 1e3) / 1e9 if s1_n else None
+    corr_ms = (kt["expand"][0] + gemm_ms) / args.steps
+    ref_ms = (kt["coords"][0] + s1_ms + kt["stage2"][0]) / args.steps
+    roof_gemm = {"kernel": "gemm_i8_tc (KB2)" if args.variant == "tc" else "gemm_popc (KB3)",
+                 "bound": "tensor", "achieved": gemm_tops, "peak": int8_sustained, "unit": "TOPS",
+                 "frac": gemm_tops / int8_sustained if gemm_tops else None,
+                 "frac_of_burst": gemm_tops / int8_burst if gemm_tops else None,
+                 "peak_note": f"int8 dense = 2 x {peak_src} bf16 ({peaks['bf16_tflops']} burst, "
+                              f"{peaks.get('bf16_tflops_sustained')} sustained); sustained used",
+                 "ops_per_launch": ops, "ms_per_launch": gemm_ms / gemm_n if gemm_n else None,
+                 "traffic": None}
+    roof_s1 = {"kernel": "refocus_stage1 (KB5)", "bound": "hbm", "achieved": s1_gbs, "peak": hbm,
+               "unit": "GB/s", "frac": s1_gbs / hbm if s1_gbs else None,
+               "bytes_per_step": span, "ms_per_step": s1_ms / args.steps, "traffic": None,
+               "peak_note": f"{peak_src} HBM copy bandwidth"}
+    dominant = roof_s1 if (s1_ms > gemm_ms) else roof_gemm
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(frames_np, roi_a, roi_b, alphas, args.cpu_rows, args.cpu_pixels, args.planes)
+    out = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8 x u8 -> s32 (S_ab), f64 -> f32 (Gamma), f32/f64 (refocus)",
+        "data": "synthetic",
+        "config": {"workload": (f"configs[1] (+configs[3] stack): SwissSPAD2 256x512 frames, rho_a {roi_a}, "
+                                f"rho_b {roi_b}, {n} Bernoulli({args.occupancy}) frames per rank per step "
+                                f"-> Gamma {p_a}x{p_b} -> {args.planes}-plane refocus stack"),
+                   "frames_per_step_per_rank": n, "planes_per_step": args.planes,
+                   "alphas": "linspace(0.5, 2.0, P)", "variant": args.variant,
+                   "parallelism": f"frame-sharded x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (Gamma 17 GB, operands 1.3 GB) - no flush needed"},
+        "gpu_launches": launches,
+        "roofline": dominant,
+        "rooflines": [roof_gemm, roof_s1],
+        "stages_ms_per_step": {"expand": kt["expand"][0] / args.steps, "gemm": gemm_ms / args.steps,
+                               "refocus_coords": kt["coords"][0] / args.steps,
+                               "refocus_stage1": s1_ms / args.steps, "refocus_stage2": kt["stage2"][0] / args.steps,
+                               "finalize": kt["finalize"][0] / args.steps},
+        "correlation_frames_per_s": n * world / (corr_ms / 1e3) if corr_ms else None,
+        "planes_per_s": args.planes / (ref_ms / 1e3) if ref_ms else None,
+        "clocks": clk,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "paper_context": "paper: 20x (correlation) / 500x (refocus) OpenCL-GPU vs CPU on RTX 2080 Ti vs "
+                         "i7-9700K (PAPER.md:38, 52, 279-292); no absolute timings in the text",
+    }
+    print(json.dumps(out))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,202 @@
+/*
+ * cpi.h — C ABI of the B200 (sm_100a) Correlation Plenoptic Imaging hot path.
+ *
+ * The hot path (BASELINE.json north_star):
+ *   binary SwissSPAD2 frames --(cpi_load_frames)--> device
+ *     --(cpi_correlate)--> on-device int8 expansion + single-pixel sums S_a, S_b
+ *                          + pair sums S_ab = A^T B on tcgen05 kind::i8 tensor cores
+ *                          + fused exact normalisation into fp32 Gamma
+ *     --(cpi_finalize)-->  Gamma from kept counts when not fused
+ *     --(cpi_refocus)-->   stack of refocused planes.
+ *
+ * Citations: P:NNN = PAPER.md line (arXiv 2407.20692), S:NNN = SPEC.md line.
+ *
+ * Conventions shared by every entry point
+ *   - Every function returns cpi_status (0 = CPI_OK, < 0 = error).  None throws, none
+ *     exits, none prints.  On error the context keeps a message (cpi_last_error) and is
+ *     left in the state it had before the call, except for CPI_ERR_CUDA (sticky device
+ *     errors: destroy the context).
+ *   - Calls are stream-ordered and asynchronous on `stream` (a cudaStream_t passed as
+ *     void*; NULL = legacy default stream).  Kernel faults surface at a later call or at
+ *     stream synchronisation as CPI_ERR_CUDA.
+ *   - Ownership: the caller owns every buffer it passes (inputs and outputs, device or
+ *     host); the library owns its workspaces (expanded operands, counts, refocus
+ *     scratch) until cpi_destroy.  Device pointers must be allocated on cfg.device.
+ *   - Pixel indexing inside a RoI: p = m * width + j, j horizontal (fastest), m
+ *     vertical, 0-based (P:69 uses 1-based j,k).  Gamma is row-major
+ *     [P_a][P_b]: Gamma_jkmn of Eq. (1) is gamma[(m*W_a + j) * P_b + (n*W_b + k)].
+ */
+#ifndef CPI_H_
+#define CPI_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t cpi_status;
+
+/* Status codes (names mirror SPEC's errors where one exists). */
+#define CPI_OK                      0
+#define CPI_ERR_INVALID_ARG        (-1)  /* NULL pointer, negative size, bad enum */
+#define CPI_ERR_LAYOUT             (-2)  /* frame width/height not positive multiples of 8 */
+#define CPI_ERR_ROI_OUT_OF_BOUNDS  (-3)  /* RoI not fully inside the frame */
+#define CPI_ERR_SIZE_MISMATCH      (-4)  /* byte count not a whole number of frames */
+#define CPI_ERR_CAPACITY           (-5)  /* more frames than cfg.max_frames in one batch */
+#define CPI_ERR_ZERO_FRAMES        (-6)  /* finalize / Gamma requested with N_TOT = 0 */
+#define CPI_ERR_DEGENERATE_ALPHA   (-7)  /* alpha = 0 or non-finite under the default map */
+#define CPI_ERR_EMPTY_ANGULAR_GRID (-8)  /* n_planes < 1 or empty B lattice */
+#define CPI_ERR_STATE              (-9)  /* call out of order (e.g. correlate before load) */
+#define CPI_ERR_CUDA               (-10) /* CUDA runtime/driver failure or no sm_100 device */
+#define CPI_ERR_OOM                (-11) /* device allocation failure */
+#define CPI_ERR_UNSUPPORTED        (-12) /* feature not available for this configuration */
+
+/* Frame layout.  bit_order: column c of a row is bit (c % 8) of
+ * byte c/8 (CPI_LSB_FIRST, declared convention S:110) or bit 7 - c % 8 (CPI_MSB_FIRST). */
+#define CPI_LSB_FIRST 0
+#define CPI_MSB_FIRST 1
+
+/* Where cpi_load_frames' pointer lives. */
+#define CPI_HOST   0   /* host memory (pinned gives async H2D; pageable is staged by CUDA) */
+#define CPI_DEVICE 1   /* device memory on cfg.device, used in place (not copied): it must
+                          stay valid and unmodified until the next cpi_correlate completes */
+
+/* cpi_config.flags */
+#define CPI_VARIANT_TC    0u  /* S_ab on tcgen05 kind::i8 tensor cores (default) */
+#define CPI_VARIANT_POPC  1u  /* S_ab as popcount(a AND b) on CUDA cores */
+#define CPI_KEEP_COUNTS   2u  /* keep int32 S_ab [P_a][P_b] in a library workspace: needed for
+                                 multi-batch accumulation, cpi_get_counts of S_ab,
+                                 and cpi_finalize from counts.  Costs 4*P_a*P_b bytes. */
+
+/* Boundary policy of refocusing. */
+#define CPI_SKIP_RENORMALIZE 0  /* sample counts only if 0 <= c_A <= W-1 on both axes; mean */
+#define CPI_CLAMP            1  /* c_A clamped into [0, W-1]; every sample counts */
+
+typedef struct {
+    int32_t x0, y0, width, height;   /* 0-based inclusive top-left, size in px */
+} cpi_roi;
+
+typedef struct {
+    int32_t width_px, height_px, bit_order;   /* SwissSPAD2: 512, 256, CPI_LSB_FIRST */
+} cpi_layout;
+
+typedef struct {
+    cpi_layout layout;
+    cpi_roi roi_a, roi_b;   /* spatial arm rho_a (image A) and angular arm rho_b (image B),
+                               P:68-69: A = left half, B = right half for the paper's data */
+    int64_t max_frames;     /* capacity of one cpi_load_frames batch (>= 1) */
+    int32_t device;         /* CUDA device ordinal; must be compute capability 10.0 */
+    uint32_t flags;         /* CPI_VARIANT_* | CPI_KEEP_COUNTS */
+} cpi_config;
+
+typedef struct {
+    const double *alphas;   /* HOST array of n_planes refocusing parameters alpha (finite, != 0) */
+    int32_t n_planes;       /* >= 1 */
+    int32_t boundary;       /* CPI_SKIP_RENORMALIZE | CPI_CLAMP */
+    const float *gamma_dev; /* DEVICE Gamma rows [row0, row0 + rows) of [P_a][P_b], row-major,
+                               leading dimension P_b (e.g. cpi_correlate's output) */
+    int64_t row0, rows;     /* multiples of roi_a.width; a single GPU passes 0, P_a.  A row
+                               shard yields that shard's additive share of every plane. */
+} cpi_refocus_spec;
+
+typedef struct cpi_ctx cpi_ctx;   /* opaque, owned by the library */
+
+/* Create a context on cfg->device: validates the layout and RoIs, allocates
+ * the expanded-operand workspaces for max_frames, the marginals and (CPI_KEEP_COUNTS) the
+ * counts, and encodes the TMA descriptors.  *out is set only on success.
+ * Errors: INVALID_ARG, LAYOUT, ROI_OUT_OF_BOUNDS, CUDA (no sm_100 device), OOM. */
+cpi_status cpi_create(const cpi_config *cfg, cpi_ctx **out);
+
+/* Release every library-owned resource.  NULL is a no-op.  Synchronises the device. */
+void cpi_destroy(cpi_ctx *ctx);
+
+/* Message for the last error on ctx (never NULL; "" when none).  ctx may be NULL (then
+ * the message of the last failed cpi_create on this thread). */
+const char *cpi_last_error(const cpi_ctx *ctx);
+
+/* Static name of a status code. */
+const char *cpi_status_string(cpi_status s);
+
+/* Load one batch of n_frames whole packed frames (frame-major, row-major, 1 bpp,
+ * layout.width_px/8 bytes per row: "Input Dataset") as the input of the
+ * next cpi_correlate.  where = CPI_HOST copies asynchronously on `stream`; CPI_DEVICE
+ * uses the pointer in place.  Errors: INVALID_ARG, CAPACITY (n_frames > max_frames),
+ * CUDA.  n_frames = 0 is allowed (the next correlate adds nothing). */
+cpi_status cpi_load_frames(cpi_ctx *ctx, const void *packed, int64_t n_frames, int32_t where,
+                           void *stream);
+
+/* Accumulate the loaded batch into the context's sums (Eq. (1) numerators):
+ *   S_a[p] += sum_i A^i_p,  S_b[q] += sum_i B^i_q,  N_TOT += n_frames,
+ *   S_ab[p][q] += sum_i A^i_p B^i_q   (int32, exact; N_TOT < 2^31)
+ * on the device: bits are expanded to K-major uint8 operands ("bit-unpacking") and
+ * S_ab runs on tcgen05 kind::i8 (CPI_VARIANT_TC) or popcount(AND) (CPI_VARIANT_POPC).
+ * If gamma_dev != NULL the GEMM epilogue also writes Gamma for the accumulated totals
+ * (fused normalisation, see cpi_finalize for the formula) into gamma_dev [P_a][P_b].
+ * Without CPI_KEEP_COUNTS only one correlate per cpi_reset is allowed (nothing to
+ * accumulate into) and gamma_dev must be non-NULL.
+ * Errors: STATE (nothing loaded; second batch without KEEP_COUNTS; no output at all),
+ * CUDA. */
+cpi_status cpi_correlate(cpi_ctx *ctx, float *gamma_dev, void *stream);
+
+/* Gamma of Eq. (1) from the accumulated sums:
+ *   Gamma[p][q] = (N*S_ab[p][q] - S_a[p]*S_b[q]) / N^2   (= (1/N) S_ab - (S_a/N)(S_b/N))
+ * with the numerator formed exactly (fp64 FMA of exact integers) and one rounding to fp32.
+ * If the last cpi_correlate already wrote Gamma for the current totals and gamma_dev is
+ * NULL or that same buffer, nothing is launched.  Otherwise needs CPI_KEEP_COUNTS.
+ * *n_tot (optional) receives N_TOT.  Errors: ZERO_FRAMES, STATE, INVALID_ARG, CUDA. */
+cpi_status cpi_finalize(cpi_ctx *ctx, float *gamma_dev, int64_t *n_tot, void *stream);
+
+/* Stateless finalisation of an externally reduced row shard (frame-sharded multi-GPU:
+ * SURVEY §8(e), after an all-reduce of S_a/S_b/N and a reduce-scatter of S_ab rows):
+ *   gamma_rows[r][q] = Gamma(s_ab_rows[r][q], s_a[row0 + r], s_b[q], n_tot)
+ * s_ab_rows: device int32 [rows][P_b]; s_a: device int32 [P_a]; s_b: device int32 [P_b];
+ * gamma_rows: device fp32 [rows][P_b].  Errors: INVALID_ARG, ZERO_FRAMES, CUDA. */
+cpi_status cpi_finalize_counts(cpi_ctx *ctx, const int32_t *s_ab_rows, int64_t row0, int64_t rows,
+                               const int32_t *s_a, const int32_t *s_b, int64_t n_tot,
+                               float *gamma_rows, void *stream);
+
+/* Copy the accumulated sums to caller device buffers (audit / bit-exact tests / multi-GPU
+ * reduction).  Any pointer may be NULL.  s_ab_dev (int32 [P_a][P_b]) needs
+ * CPI_KEEP_COUNTS.  *n_tot receives N_TOT.  Errors: STATE, CUDA. */
+cpi_status cpi_get_counts(cpi_ctx *ctx, int32_t *s_ab_dev, int32_t *s_a_dev, int32_t *s_b_dev,
+                          int64_t *n_tot, void *stream);
+
+/* Zero the accumulated sums (start a new acquisition). */
+cpi_status cpi_reset(cpi_ctx *ctx, void *stream);
+
+/* Refocus Gamma into a stack of planes ("Refocusing"):
+ * for plane alpha and output pixel (x, y) of the A lattice,
+ *   R(x,y) = (1/count) * sum over B lattice (u, v) of the multilinear interpolation of
+ *            Gamma at A coordinates
+ *              c_x = alpha*(x - c_ax) + (1 - alpha)*(u - c_bx) + c_ax
+ *              c_y = alpha*(y - c_ay) + (1 - alpha)*(v - c_by) + c_ay
+ *            and B coordinates (u, v)  (SPEC default map S:274, centres c = (W-1)/2),
+ *   samples outside [0, W_a-1] x [0, H_a-1] skipped (CPI_SKIP_RENORMALIZE) or clamped,
+ *   count = number of samples used, R = 0 when count = 0.
+ * The B coordinates are integers, so the 16-corner interpolation is the bilinear one on
+ * the A axes; the kernels evaluate it separably (stage 1 over x, stage 2 over y), fp64
+ * coordinates, fp32 taps summed in fp64.
+ * planes_dev: device fp32 [n_planes][H_a][W_a].  Needs W_a, H_a >= 2.
+ * Errors: INVALID_ARG, DEGENERATE_ALPHA, EMPTY_ANGULAR_GRID, UNSUPPORTED, OOM, CUDA. */
+cpi_status cpi_refocus(cpi_ctx *ctx, const cpi_refocus_spec *spec, float *planes_dev,
+                       void *stream);
+
+/* Number of kernels this context has launched so far (for launch accounting). */
+int64_t cpi_launch_count(const cpi_ctx *ctx);
+
+/* Per-kernel timing: when enabled, the library records CUDA events around its main
+ * kernels on the launching stream; cpi_kernel_time_ms returns the accumulated device time
+ * of one kernel class since the last reset (0 = GEMM, 1 = expand, 2 = refocus stage 1,
+ * 3 = refocus stage 2, 4 = finalize, 5 = refocus coords) and its launch count.
+ * Enabling timing synchronises each timed launch's end event lazily (at query time). */
+cpi_status cpi_set_timing(cpi_ctx *ctx, int32_t enable);
+cpi_status cpi_kernel_time_ms(cpi_ctx *ctx, int32_t kernel_class, double *ms, int64_t *launches);
+
+/* ABI version (major * 100 + minor). */
+int32_t cpi_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CPI_H_ */

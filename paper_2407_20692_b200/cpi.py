@@ -1,0 +1,188 @@
+"""Python binding of the CPI C ABI (include/cpi.h) — argument marshalling only.
+
+Every step of the hot path runs in libcpi.so's CUDA kernels; this module only converts
+torch tensors / numpy arrays into pointers, picks the current torch CUDA stream, and turns
+status codes into exceptions.  torch supplies device memory and streams (plumbing).
+Names follow the C functions: load_frames / correlate / finalize / refocus / get_counts.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import CpiError
+
+FRAME_W, FRAME_H = 512, 256   # SwissSPAD2 frame
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class Context:
+    """One CPI accumulation context on one GPU (cpi_create ... cpi_destroy)."""
+
+    def __init__(self, roi_a, roi_b, max_frames: int, *, width: int = FRAME_W, height: int = FRAME_H,
+                 bit_order: int = _lib.CPI_LSB_FIRST, device: int = 0, variant: str = "tc",
+                 keep_counts: bool = False):
+        self._lib = _lib.load()
+        flags = (_lib.CPI_VARIANT_POPC if variant == "popc" else _lib.CPI_VARIANT_TC)
+        if variant not in ("tc", "popc"):
+            raise ValueError("variant must be 'tc' or 'popc'")
+        if keep_counts:
+            flags |= _lib.CPI_KEEP_COUNTS
+        cfg = _lib.Config(_lib.Layout(width, height, bit_order), _lib.Roi(*roi_a), _lib.Roi(*roi_b),
+                          int(max_frames), int(device), flags)
+        h = ctypes.c_void_p()
+        st = self._lib.cpi_create(ctypes.byref(cfg), ctypes.byref(h))
+        if st != 0:
+            raise CpiError(st, self._lib.cpi_last_error(None).decode())
+        self._h = h
+        self.roi_a, self.roi_b = tuple(roi_a), tuple(roi_b)
+        self.p_a = roi_a[2] * roi_a[3]
+        self.p_b = roi_b[2] * roi_b[3]
+        self.device = device
+        self.width, self.height = width, height
+        self.frame_bytes = (width // 8) * height
+        self.max_frames = int(max_frames)
+        self.variant = variant
+        self.keep_counts = keep_counts
+        self._keep = []   # host buffers that must outlive an async copy
+
+    # -- helpers ----------------------------------------------------------------------
+    def _check(self, st: int):
+        if st != 0:
+            raise CpiError(st, self._lib.cpi_last_error(self._h).decode())
+
+    def _stream(self, stream=None):
+        torch = _torch()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        return ctypes.c_void_p(s.cuda_stream)
+
+    @staticmethod
+    def _ptr(t) -> ctypes.c_void_p:
+        if t is None:
+            return ctypes.c_void_p(0)
+        if isinstance(t, np.ndarray):
+            return ctypes.c_void_p(t.ctypes.data)
+        return ctypes.c_void_p(t.data_ptr())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.cpi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- C ABI -------------------------------------------------------------------------
+    def load_frames(self, frames, n_frames: Optional[int] = None, stream=None):
+        """cpi_load_frames.  frames: packed uint8 [N][H][W/8] as a numpy array / CPU tensor
+        (host copy, pinned = async) or a CUDA tensor (used in place)."""
+        torch = _torch()
+        if isinstance(frames, np.ndarray):
+            nbytes = frames.nbytes
+            where = _lib.CPI_HOST
+            self._keep = [frames]
+        else:
+            nbytes = frames.numel() * frames.element_size()
+            where = _lib.CPI_DEVICE if frames.is_cuda else _lib.CPI_HOST
+            if not frames.is_contiguous():
+                raise ValueError("frames must be contiguous")
+            self._keep = [frames]
+        if n_frames is None:
+            if nbytes % self.frame_bytes:
+                raise CpiError(-4, f"{nbytes} bytes is not a whole number of {self.frame_bytes}-byte frames")
+            n_frames = nbytes // self.frame_bytes
+        self._check(self._lib.cpi_load_frames(self._h, self._ptr(frames), int(n_frames), where,
+                                              self._stream(stream)))
+        return n_frames
+
+    def correlate(self, gamma=None, stream=None):
+        """cpi_correlate: accumulate the loaded batch; write Gamma [P_a][P_b] fp32 if given."""
+        if gamma is not None:
+            self._check_gamma(gamma)
+        self._check(self._lib.cpi_correlate(self._h, self._ptr(gamma), self._stream(stream)))
+        return gamma
+
+    def finalize(self, gamma=None, stream=None) -> int:
+        """cpi_finalize: Gamma from the accumulated sums; returns N_TOT."""
+        if gamma is not None:
+            self._check_gamma(gamma)
+        n = ctypes.c_int64(0)
+        self._check(self._lib.cpi_finalize(self._h, self._ptr(gamma), ctypes.byref(n), self._stream(stream)))
+        return n.value
+
+    def finalize_counts(self, s_ab_rows, row0: int, s_a, s_b, n_tot: int, gamma_rows, stream=None):
+        """cpi_finalize_counts: stateless Gamma of an externally reduced row shard."""
+        rows = s_ab_rows.shape[0]
+        self._check(self._lib.cpi_finalize_counts(self._h, self._ptr(s_ab_rows), int(row0), int(rows),
+                                                  self._ptr(s_a), self._ptr(s_b), int(n_tot),
+                                                  self._ptr(gamma_rows), self._stream(stream)))
+        return gamma_rows
+
+    def get_counts(self, s_ab=None, s_a=None, s_b=None, stream=None) -> int:
+        """cpi_get_counts into caller CUDA int32 tensors; returns N_TOT."""
+        n = ctypes.c_int64(0)
+        self._check(self._lib.cpi_get_counts(self._h, self._ptr(s_ab), self._ptr(s_a), self._ptr(s_b),
+                                             ctypes.byref(n), self._stream(stream)))
+        return n.value
+
+    def reset(self, stream=None):
+        self._check(self._lib.cpi_reset(self._h, self._stream(stream)))
+
+    def refocus(self, alphas: Sequence[float], gamma, planes, row0: int = 0, rows: Optional[int] = None,
+                boundary: int = _lib.CPI_SKIP_RENORMALIZE, stream=None):
+        """cpi_refocus: planes [n_planes][H_a][W_a] fp32 from Gamma rows [row0, row0+rows)
+        (gamma points at row row0, leading dimension P_b)."""
+        al = np.ascontiguousarray(alphas, dtype=np.float64).ravel()
+        if rows is None:
+            rows = self.p_a - row0
+        spec = _lib.RefocusSpec(al.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), al.size, int(boundary),
+                                self._ptr(gamma), int(row0), int(rows))
+        self._check(self._lib.cpi_refocus(self._h, ctypes.byref(spec), self._ptr(planes), self._stream(stream)))
+        return planes
+
+    def launch_count(self) -> int:
+        return int(self._lib.cpi_launch_count(self._h))
+
+    def set_timing(self, enable: bool):
+        self._check(self._lib.cpi_set_timing(self._h, int(bool(enable))))
+
+    def kernel_time_ms(self, cls: int):
+        ms = ctypes.c_double(0)
+        n = ctypes.c_int64(0)
+        self._check(self._lib.cpi_kernel_time_ms(self._h, int(cls), ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
+
+    # -- conveniences -------------------------------------------------------------------
+    def _check_gamma(self, g):
+        torch = _torch()
+        if not (g.is_cuda and g.dtype == torch.float32 and g.is_contiguous() and g.numel() >= self.p_a * self.p_b):
+            raise ValueError("gamma must be a contiguous CUDA float32 tensor with P_a*P_b elements")
+
+    def new_gamma(self):
+        torch = _torch()
+        return torch.empty((self.p_a, self.p_b), dtype=torch.float32, device=f"cuda:{self.device}")
+
+    def new_planes(self, n_planes: int):
+        torch = _torch()
+        return torch.empty((n_planes, self.roi_a[3], self.roi_a[2]), dtype=torch.float32,
+                           device=f"cuda:{self.device}")
+
+
+def abi_version() -> int:
+    return int(_lib.load().cpi_abi_version())

@@ -1,0 +1,535 @@
+// cpi_abi.cu — the C ABI of include/cpi.h: context, validation, workspaces, TMA
+// descriptors, launch sequencing and timing.  All compute runs in the kernels of
+// expand.cu / gemm_tc.cu / gemm_popc.cu / refocus.cu; nothing here touches pixel data.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "../../include/cpi.h"
+#include "kernels.h"
+
+namespace {
+
+constexpr int64_t kKAlign = 128;   // frames per GEMM K block (bytes of one swizzle row)
+
+enum KernelClass { KC_GEMM = 0, KC_EXPAND = 1, KC_STAGE1 = 2, KC_STAGE2 = 3, KC_FINALIZE = 4,
+                   KC_COORDS = 5, KC_COUNT = 6 };
+
+thread_local std::string g_create_error;
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+}  // namespace
+
+struct cpi_ctx {
+    cpi_config cfg{};
+    int dev = 0;
+    int num_sms = 148;
+    bool popc = false, keep = false;
+    int64_t p_a = 0, p_b = 0;
+    int64_t rows_a = 0, rows_b = 0;        // padded operand rows
+    int64_t k_cap = 0;                     // frames capacity rounded to 128
+    int64_t ld_op = 0;                     // operand leading dimension (bytes or 32-bit words)
+    int64_t frame_bytes = 0;
+    uint8_t* frames_dev = nullptr;         // staging for host loads
+    const uint8_t* frames_cur = nullptr;
+    int64_t n_cur = 0;
+    bool loaded = false;
+    void* op_a = nullptr;
+    void* op_b = nullptr;
+    int32_t* s_a = nullptr;
+    int32_t* s_b = nullptr;
+    int32_t* counts = nullptr;
+    int64_t n_tot = 0;
+    int64_t batches = 0;
+    float* gamma_current = nullptr;        // Gamma buffer written for the current totals
+    CUtensorMap tm_a{}, tm_b{};
+    // refocus workspaces
+    cpi::AxisTables xs{}, ys{};
+    double* T = nullptr;
+    // accounting
+    int64_t launches = 0;
+    bool timing = false;
+    struct Timed { int cls; cudaEvent_t a, b; };
+    std::vector<Timed> timed;
+    std::vector<cudaEvent_t> event_pool;
+    double acc_ms[KC_COUNT] = {};
+    int64_t acc_n[KC_COUNT] = {};
+    std::string err;
+};
+
+namespace {
+
+cpi_status fail(cpi_ctx* c, cpi_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf; else g_create_error = buf;
+    return s;
+}
+
+cpi_status cuda_fail(cpi_ctx* c, cudaError_t e, const char* where) {
+    return fail(c, e == cudaErrorMemoryAllocation ? CPI_ERR_OOM : CPI_ERR_CUDA, "%s: %s (%s)", where,
+                cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define CK(c, call)                                                   \
+    do {                                                              \
+        cudaError_t e_ = (call);                                      \
+        if (e_ != cudaSuccess) return cuda_fail((c), e_, #call);      \
+    } while (0)
+
+cudaEvent_t take_event(cpi_ctx* c) {
+    if (!c->event_pool.empty()) {
+        cudaEvent_t e = c->event_pool.back();
+        c->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct TimedScope {
+    cpi_ctx* c; int cls; cudaStream_t st; cudaEvent_t a = nullptr;
+    TimedScope(cpi_ctx* c_, int cls_, cudaStream_t st_) : c(c_), cls(cls_), st(st_) {
+        if (c->timing) { a = take_event(c); cudaEventRecord(a, st); }
+    }
+    ~TimedScope() {
+        if (c->timing) {
+            cudaEvent_t b = take_event(c);
+            cudaEventRecord(b, st);
+            c->timed.push_back({cls, a, b});
+        }
+    }
+};
+
+void drain_timing(cpi_ctx* c) {
+    for (auto& t : c->timed) {
+        cudaEventSynchronize(t.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, t.a, t.b);
+        c->acc_ms[t.cls] += ms;
+        c->acc_n[t.cls] += 1;
+        c->event_pool.push_back(t.a);
+        c->event_pool.push_back(t.b);
+    }
+    c->timed.clear();
+}
+
+bool roi_ok(const cpi_roi& r, const cpi_layout& l) {
+    return r.width >= 1 && r.height >= 1 && r.x0 >= 0 && r.y0 >= 0 &&
+           static_cast<int64_t>(r.x0) + r.width <= l.width_px &&
+           static_cast<int64_t>(r.y0) + r.height <= l.height_px;
+}
+
+EncodeTiledFn get_encode() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+cpi_status make_tmap(cpi_ctx* c, CUtensorMap* m, void* base, int64_t rows, int64_t cols,
+                     uint32_t box_rows) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return fail(c, CPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols)};   // bytes between rows
+    const cuuint32_t box[2] = {128u, box_rows};
+    const cuuint32_t estr[2] = {1u, 1u};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(c, CPI_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+    return CPI_OK;
+}
+
+void free_all(cpi_ctx* c) {
+    cudaFree(c->frames_dev);
+    cudaFree(c->op_a);
+    cudaFree(c->op_b);
+    cudaFree(c->s_a);
+    cudaFree(c->s_b);
+    cudaFree(c->counts);
+    cudaFree(c->xs.i0); cudaFree(c->xs.t); cudaFree(c->xs.cnt); cudaFree(c->xs.lo); cudaFree(c->xs.hi);
+    cudaFree(c->ys.i0); cudaFree(c->ys.t); cudaFree(c->ys.cnt); cudaFree(c->ys.lo); cudaFree(c->ys.hi);
+    cudaFree(c->T);
+    for (auto& t : c->timed) { c->event_pool.push_back(t.a); c->event_pool.push_back(t.b); }
+    for (auto e : c->event_pool) cudaEventDestroy(e);
+}
+
+cpi_status alloc_axis(cpi_ctx* c, cpi::AxisTables& t, int W, int Wb) {
+    CK(c, cudaMalloc(&t.i0, sizeof(int32_t) * W * Wb));
+    CK(c, cudaMalloc(&t.t, sizeof(double) * W * Wb));
+    CK(c, cudaMalloc(&t.cnt, sizeof(int32_t) * W));
+    CK(c, cudaMalloc(&t.lo, sizeof(int32_t) * Wb));
+    CK(c, cudaMalloc(&t.hi, sizeof(int32_t) * Wb));
+    return CPI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t cpi_abi_version(void) { return 100; }
+
+const char* cpi_status_string(cpi_status s) {
+    switch (s) {
+        case CPI_OK: return "CPI_OK";
+        case CPI_ERR_INVALID_ARG: return "CPI_ERR_INVALID_ARG";
+        case CPI_ERR_LAYOUT: return "CPI_ERR_LAYOUT";
+        case CPI_ERR_ROI_OUT_OF_BOUNDS: return "CPI_ERR_ROI_OUT_OF_BOUNDS";
+        case CPI_ERR_SIZE_MISMATCH: return "CPI_ERR_SIZE_MISMATCH";
+        case CPI_ERR_CAPACITY: return "CPI_ERR_CAPACITY";
+        case CPI_ERR_ZERO_FRAMES: return "CPI_ERR_ZERO_FRAMES";
+        case CPI_ERR_DEGENERATE_ALPHA: return "CPI_ERR_DEGENERATE_ALPHA";
+        case CPI_ERR_EMPTY_ANGULAR_GRID: return "CPI_ERR_EMPTY_ANGULAR_GRID";
+        case CPI_ERR_STATE: return "CPI_ERR_STATE";
+        case CPI_ERR_CUDA: return "CPI_ERR_CUDA";
+        case CPI_ERR_OOM: return "CPI_ERR_OOM";
+        case CPI_ERR_UNSUPPORTED: return "CPI_ERR_UNSUPPORTED";
+        default: return "CPI_ERR_UNKNOWN";
+    }
+}
+
+const char* cpi_last_error(const cpi_ctx* c) {
+    return c ? c->err.c_str() : g_create_error.c_str();
+}
+
+cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
+    g_create_error.clear();
+    if (!cfg || !out) return fail(nullptr, CPI_ERR_INVALID_ARG, "cfg and out must be non-NULL");
+    const cpi_layout& L = cfg->layout;
+    if (L.width_px <= 0 || L.height_px <= 0 || L.width_px % 8 || L.height_px % 8)
+        return fail(nullptr, CPI_ERR_LAYOUT, "frame %dx%d: width and height must be positive multiples of 8",
+                    L.width_px, L.height_px);
+    if (L.bit_order != CPI_LSB_FIRST && L.bit_order != CPI_MSB_FIRST)
+        return fail(nullptr, CPI_ERR_INVALID_ARG, "bit_order must be CPI_LSB_FIRST or CPI_MSB_FIRST");
+    if (!roi_ok(cfg->roi_a, L) || !roi_ok(cfg->roi_b, L))
+        return fail(nullptr, CPI_ERR_ROI_OUT_OF_BOUNDS, "RoI outside the %dx%d frame", L.width_px, L.height_px);
+    if (cfg->roi_a.width > 512 || cfg->roi_b.width > 512)
+        return fail(nullptr, CPI_ERR_UNSUPPORTED, "RoI wider than 512 px");
+    if (cfg->max_frames < 1) return fail(nullptr, CPI_ERR_INVALID_ARG, "max_frames must be >= 1");
+    if (cfg->max_frames >= (int64_t(1) << 31) - kKAlign)
+        return fail(nullptr, CPI_ERR_INVALID_ARG, "max_frames must be < 2^31 (int32 sums)");
+    if (cfg->flags & ~(CPI_VARIANT_POPC | CPI_KEEP_COUNTS))
+        return fail(nullptr, CPI_ERR_INVALID_ARG, "unknown flags 0x%x", cfg->flags);
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(nullptr, CPI_ERR_CUDA, "no CUDA device visible");
+    if (cfg->device < 0 || cfg->device >= ndev)
+        return fail(nullptr, CPI_ERR_INVALID_ARG, "device %d out of range (%d devices)", cfg->device, ndev);
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess)
+        return fail(nullptr, CPI_ERR_CUDA, "cudaGetDeviceProperties failed");
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(nullptr, CPI_ERR_CUDA, "device %d is sm_%d%d; this library is built for sm_100a (B200)",
+                    cfg->device, prop.major, prop.minor);
+    if (cudaSetDevice(cfg->device) != cudaSuccess) return fail(nullptr, CPI_ERR_CUDA, "cudaSetDevice failed");
+
+    cpi_ctx* c = new cpi_ctx();
+    c->cfg = *cfg;
+    c->dev = cfg->device;
+    c->num_sms = prop.multiProcessorCount;
+    c->popc = (cfg->flags & CPI_VARIANT_POPC) != 0;
+    c->keep = (cfg->flags & CPI_KEEP_COUNTS) != 0;
+    c->p_a = int64_t(cfg->roi_a.width) * cfg->roi_a.height;
+    c->p_b = int64_t(cfg->roi_b.width) * cfg->roi_b.height;
+    c->k_cap = round_up(cfg->max_frames, kKAlign);
+    c->frame_bytes = int64_t(L.width_px / 8) * L.height_px;
+    if (c->popc) {
+        c->rows_a = round_up(c->p_a, cpi::gemm_popc_block());
+        c->rows_b = round_up(c->p_b, cpi::gemm_popc_block());
+        c->ld_op = c->k_cap / 32;   // 32-bit words
+    } else {
+        c->rows_a = round_up(c->p_a, cpi::gemm_tc_block_m());
+        c->rows_b = round_up(c->p_b, cpi::gemm_tc_block_n());
+        c->ld_op = c->k_cap;        // bytes
+    }
+    const size_t op_elem = c->popc ? 4 : 1;
+    cudaError_t e = cudaSuccess;
+    auto chk = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
+    chk(cudaMalloc(&c->frames_dev, size_t(c->frame_bytes) * cfg->max_frames));
+    chk(cudaMalloc(&c->op_a, size_t(c->rows_a) * c->ld_op * op_elem));
+    chk(cudaMalloc(&c->op_b, size_t(c->rows_b) * c->ld_op * op_elem));
+    chk(cudaMalloc(&c->s_a, sizeof(int32_t) * c->p_a));
+    chk(cudaMalloc(&c->s_b, sizeof(int32_t) * c->p_b));
+    if (c->keep) chk(cudaMalloc(&c->counts, sizeof(int32_t) * size_t(c->p_a) * c->p_b));
+    if (e == cudaSuccess) chk(cudaMemset(c->op_a, 0, size_t(c->rows_a) * c->ld_op * op_elem));
+    if (e == cudaSuccess) chk(cudaMemset(c->op_b, 0, size_t(c->rows_b) * c->ld_op * op_elem));
+    if (e == cudaSuccess) chk(cudaMemset(c->s_a, 0, sizeof(int32_t) * c->p_a));
+    if (e == cudaSuccess) chk(cudaMemset(c->s_b, 0, sizeof(int32_t) * c->p_b));
+    if (e == cudaSuccess && c->keep) chk(cudaMemset(c->counts, 0, sizeof(int32_t) * size_t(c->p_a) * c->p_b));
+    if (e == cudaSuccess) chk(cudaDeviceSynchronize());
+    if (e != cudaSuccess) {
+        cpi_status s = cuda_fail(nullptr, e, "cpi_create allocation");
+        free_all(c);
+        delete c;
+        return s;
+    }
+    if (!c->popc) {
+        cpi_status s = make_tmap(c, &c->tm_a, c->op_a, c->rows_a, c->ld_op, cpi::gemm_tc_block_m());
+        if (s == CPI_OK) s = make_tmap(c, &c->tm_b, c->op_b, c->rows_b, c->ld_op, cpi::gemm_tc_block_n());
+        if (s != CPI_OK) {
+            g_create_error = c->err;
+            free_all(c);
+            delete c;
+            return s;
+        }
+    }
+    *out = c;
+    return CPI_OK;
+}
+
+void cpi_destroy(cpi_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->dev);
+    cudaDeviceSynchronize();
+    free_all(c);
+    delete c;
+}
+
+cpi_status cpi_load_frames(cpi_ctx* c, const void* packed, int64_t n, int32_t where, void* stream) {
+    if (!c) return CPI_ERR_INVALID_ARG;
+    if (n < 0) return fail(c, CPI_ERR_INVALID_ARG, "n_frames < 0");
+    if (n > c->cfg.max_frames)
+        return fail(c, CPI_ERR_CAPACITY, "%lld frames > max_frames %lld", (long long)n, (long long)c->cfg.max_frames);
+    if (n > 0 && !packed) return fail(c, CPI_ERR_INVALID_ARG, "packed is NULL");
+    if (where != CPI_HOST && where != CPI_DEVICE) return fail(c, CPI_ERR_INVALID_ARG, "where must be CPI_HOST or CPI_DEVICE");
+    CK(c, cudaSetDevice(c->dev));
+    auto st = static_cast<cudaStream_t>(stream);
+    if (where == CPI_HOST) {
+        if (n > 0)
+            CK(c, cudaMemcpyAsync(c->frames_dev, packed, size_t(n) * c->frame_bytes, cudaMemcpyHostToDevice, st));
+        c->frames_cur = c->frames_dev;
+    } else {
+        c->frames_cur = static_cast<const uint8_t*>(packed);
+    }
+    c->n_cur = n;
+    c->loaded = true;
+    return CPI_OK;
+}
+
+cpi_status cpi_correlate(cpi_ctx* c, float* gamma, void* stream) {
+    if (!c) return CPI_ERR_INVALID_ARG;
+    if (!c->loaded) return fail(c, CPI_ERR_STATE, "cpi_correlate before cpi_load_frames");
+    if (!c->keep && c->batches > 0)
+        return fail(c, CPI_ERR_STATE, "second batch needs CPI_KEEP_COUNTS (or cpi_reset)");
+    if (!c->keep && !gamma)
+        return fail(c, CPI_ERR_STATE, "gamma_dev is NULL and CPI_KEEP_COUNTS is off: pair sums would be lost");
+    const int64_t n = c->n_cur;
+    if (gamma && c->n_tot + n == 0) return fail(c, CPI_ERR_ZERO_FRAMES, "Gamma needs N_TOT >= 1");
+    CK(c, cudaSetDevice(c->dev));
+    auto st = static_cast<cudaStream_t>(stream);
+    const cpi_layout& L = c->cfg.layout;
+    const int64_t k_pad = round_up(n, kKAlign);
+    {
+        TimedScope ts(c, KC_EXPAND, st);
+        const cpi::RoiDev ra{c->cfg.roi_a.x0, c->cfg.roi_a.y0, c->cfg.roi_a.width, c->cfg.roi_a.height};
+        const cpi::RoiDev rb{c->cfg.roi_b.x0, c->cfg.roi_b.y0, c->cfg.roi_b.width, c->cfg.roi_b.height};
+        if (n > 0) {
+            cpi::launch_expand(c->frames_cur, n, L.width_px / 8, L.height_px, L.bit_order, ra, c->op_a,
+                               c->ld_op, k_pad, c->s_a, c->popc, st);
+            cpi::launch_expand(c->frames_cur, n, L.width_px / 8, L.height_px, L.bit_order, rb, c->op_b,
+                               c->ld_op, k_pad, c->s_b, c->popc, st);
+            c->launches += 2;
+            CK(c, cudaGetLastError());
+        }
+    }
+    const int64_t n_tot = c->n_tot + n;
+    cpi::Epilogue epi{};
+    epi.s_a = c->s_a;
+    epi.s_b = c->s_b;
+    epi.gamma = gamma;
+    epi.ldg = c->p_b;
+    epi.counts = c->keep ? c->counts : nullptr;
+    epi.ldc = c->p_b;
+    epi.accumulate = c->batches > 0 ? 1 : 0;
+    epi.p_a = static_cast<int>(c->p_a);
+    epi.p_b = static_cast<int>(c->p_b);
+    epi.vec = (c->p_b % 4) == 0;
+    epi.n = static_cast<double>(n_tot > 0 ? n_tot : 1);
+    epi.inv_n2 = 1.0 / (epi.n * epi.n);
+    if (n > 0) {
+        TimedScope ts(c, KC_GEMM, st);
+        cudaError_t e;
+        if (c->popc)
+            e = cpi::launch_gemm_popc(static_cast<const uint32_t*>(c->op_a), static_cast<const uint32_t*>(c->op_b),
+                                      c->ld_op, k_pad / 32, epi, st);
+        else
+            e = cpi::launch_gemm_tc(&c->tm_a, &c->tm_b, static_cast<int>(c->rows_a / cpi::gemm_tc_block_m()),
+                                    static_cast<int>(c->rows_b / cpi::gemm_tc_block_n()),
+                                    static_cast<int>(k_pad / kKAlign), epi, c->num_sms, st);
+        c->launches += 1;
+        if (e != cudaSuccess) return cuda_fail(c, e, "pair-sum GEMM launch");
+    } else if (gamma) {
+        // empty batch: Gamma of the unchanged totals from the kept counts
+        if (!c->keep) return fail(c, CPI_ERR_STATE, "empty batch and no kept counts");
+        TimedScope ts(c, KC_FINALIZE, st);
+        cudaError_t e = cpi::launch_finalize(c->counts, c->p_b, c->p_a, c->p_b, c->s_a, c->s_b,
+                                             static_cast<double>(n_tot), gamma, c->p_b, st);
+        c->launches += 1;
+        if (e != cudaSuccess) return cuda_fail(c, e, "finalize launch");
+    }
+    c->n_tot = n_tot;
+    c->batches += 1;
+    c->loaded = false;
+    c->gamma_current = gamma;
+    return CPI_OK;
+}
+
+cpi_status cpi_finalize(cpi_ctx* c, float* gamma, int64_t* n_tot, void* stream) {
+    if (!c) return CPI_ERR_INVALID_ARG;
+    if (c->n_tot == 0) return fail(c, CPI_ERR_ZERO_FRAMES, "N_TOT = 0");
+    if (n_tot) *n_tot = c->n_tot;
+    if (c->gamma_current && (!gamma || gamma == c->gamma_current)) return CPI_OK;
+    if (!gamma) return fail(c, CPI_ERR_INVALID_ARG, "gamma_dev is NULL and no fused Gamma exists");
+    if (!c->keep) return fail(c, CPI_ERR_STATE, "Gamma from counts needs CPI_KEEP_COUNTS");
+    CK(c, cudaSetDevice(c->dev));
+    auto st = static_cast<cudaStream_t>(stream);
+    TimedScope ts(c, KC_FINALIZE, st);
+    cudaError_t e = cpi::launch_finalize(c->counts, c->p_b, c->p_a, c->p_b, c->s_a, c->s_b,
+                                         static_cast<double>(c->n_tot), gamma, c->p_b, st);
+    c->launches += 1;
+    if (e != cudaSuccess) return cuda_fail(c, e, "finalize launch");
+    c->gamma_current = gamma;
+    return CPI_OK;
+}
+
+cpi_status cpi_finalize_counts(cpi_ctx* c, const int32_t* s_ab_rows, int64_t row0, int64_t rows,
+                               const int32_t* s_a, const int32_t* s_b, int64_t n_tot, float* gamma_rows,
+                               void* stream) {
+    if (!c) return CPI_ERR_INVALID_ARG;
+    if (n_tot <= 0) return fail(c, CPI_ERR_ZERO_FRAMES, "n_tot must be >= 1");
+    if (rows < 0 || row0 < 0 || row0 + rows > c->p_a) return fail(c, CPI_ERR_INVALID_ARG, "row range outside [0, P_a)");
+    if (rows > 0 && (!s_ab_rows || !s_a || !s_b || !gamma_rows))
+        return fail(c, CPI_ERR_INVALID_ARG, "NULL buffer");
+    CK(c, cudaSetDevice(c->dev));
+    auto st = static_cast<cudaStream_t>(stream);
+    TimedScope ts(c, KC_FINALIZE, st);
+    cudaError_t e = cpi::launch_finalize(s_ab_rows, c->p_b, rows, c->p_b, s_a + row0, s_b,
+                                         static_cast<double>(n_tot), gamma_rows, c->p_b, st);
+    c->launches += 1;
+    if (e != cudaSuccess) return cuda_fail(c, e, "finalize launch");
+    return CPI_OK;
+}
+
+cpi_status cpi_get_counts(cpi_ctx* c, int32_t* s_ab, int32_t* s_a, int32_t* s_b, int64_t* n_tot, void* stream) {
+    if (!c) return CPI_ERR_INVALID_ARG;
+    if (s_ab && !c->keep) return fail(c, CPI_ERR_STATE, "S_ab requested but CPI_KEEP_COUNTS is off");
+    CK(c, cudaSetDevice(c->dev));
+    auto st = static_cast<cudaStream_t>(stream);
+    if (s_ab) CK(c, cudaMemcpyAsync(s_ab, c->counts, sizeof(int32_t) * size_t(c->p_a) * c->p_b, cudaMemcpyDeviceToDevice, st));
+    if (s_a) CK(c, cudaMemcpyAsync(s_a, c->s_a, sizeof(int32_t) * c->p_a, cudaMemcpyDeviceToDevice, st));
+    if (s_b) CK(c, cudaMemcpyAsync(s_b, c->s_b, sizeof(int32_t) * c->p_b, cudaMemcpyDeviceToDevice, st));
+    if (n_tot) *n_tot = c->n_tot;
+    return CPI_OK;
+}
+
+cpi_status cpi_reset(cpi_ctx* c, void* stream) {
+    if (!c) return CPI_ERR_INVALID_ARG;
+    CK(c, cudaSetDevice(c->dev));
+    auto st = static_cast<cudaStream_t>(stream);
+    CK(c, cudaMemsetAsync(c->s_a, 0, sizeof(int32_t) * c->p_a, st));
+    CK(c, cudaMemsetAsync(c->s_b, 0, sizeof(int32_t) * c->p_b, st));
+    if (c->keep) CK(c, cudaMemsetAsync(c->counts, 0, sizeof(int32_t) * size_t(c->p_a) * c->p_b, st));
+    c->n_tot = 0;
+    c->batches = 0;
+    c->gamma_current = nullptr;
+    c->loaded = false;
+    return CPI_OK;
+}
+
+cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, void* stream) {
+    if (!c) return CPI_ERR_INVALID_ARG;
+    if (!spec || !planes) return fail(c, CPI_ERR_INVALID_ARG, "spec and planes_dev must be non-NULL");
+    if (spec->n_planes < 1 || !spec->alphas) return fail(c, CPI_ERR_EMPTY_ANGULAR_GRID, "n_planes must be >= 1");
+    if (spec->boundary != CPI_SKIP_RENORMALIZE && spec->boundary != CPI_CLAMP)
+        return fail(c, CPI_ERR_INVALID_ARG, "unknown boundary policy %d", spec->boundary);
+    for (int p = 0; p < spec->n_planes; ++p)
+        if (!(spec->alphas[p] != 0.0) || !std::isfinite(spec->alphas[p]))
+            return fail(c, CPI_ERR_DEGENERATE_ALPHA, "alpha[%d] = %g (must be finite and non-zero)", p, spec->alphas[p]);
+    const int Wa = c->cfg.roi_a.width, Ha = c->cfg.roi_a.height;
+    const int Wb = c->cfg.roi_b.width, Hb = c->cfg.roi_b.height;
+    if (Wa < 2 || Ha < 2) return fail(c, CPI_ERR_UNSUPPORTED, "refocusing needs an A RoI of at least 2x2");
+    if (!spec->gamma_dev) return fail(c, CPI_ERR_INVALID_ARG, "gamma_dev is NULL");
+    if (spec->row0 < 0 || spec->rows <= 0 || spec->row0 % Wa || spec->rows % Wa || spec->row0 + spec->rows > c->p_a)
+        return fail(c, CPI_ERR_INVALID_ARG, "rows [%lld, +%lld) must be whole A rows inside [0, P_a)",
+                    (long long)spec->row0, (long long)spec->rows);
+    CK(c, cudaSetDevice(c->dev));
+    auto st = static_cast<cudaStream_t>(stream);
+    if (!c->T) {
+        cpi_status s = alloc_axis(c, c->xs, Wa, Wb);
+        if (s == CPI_OK) s = alloc_axis(c, c->ys, Ha, Hb);
+        if (s != CPI_OK) return s;
+        CK(c, cudaMalloc(&c->T, sizeof(double) * size_t(Wa) * Ha * Hb));
+    }
+    const int m_base = static_cast<int>(spec->row0 / Wa), m_count = static_cast<int>(spec->rows / Wa);
+    for (int p = 0; p < spec->n_planes; ++p) {
+        const double alpha = spec->alphas[p];
+        {
+            TimedScope ts(c, KC_COORDS, st);
+            cudaError_t e = cpi::launch_refocus_coords(alpha, spec->boundary, Wa, Wb, c->xs, st);
+            if (e == cudaSuccess) e = cpi::launch_refocus_coords(alpha, spec->boundary, Ha, Hb, c->ys, st);
+            c->launches += 2;
+            if (e != cudaSuccess) return cuda_fail(c, e, "refocus coords launch");
+        }
+        {
+            TimedScope ts(c, KC_STAGE1, st);
+            cudaError_t e = cpi::launch_refocus_stage1(spec->gamma_dev, c->p_b, Wa, Ha, Wb, Hb, m_base, m_count,
+                                                       c->xs, c->ys, c->T, st);
+            c->launches += 1;
+            if (e != cudaSuccess) return cuda_fail(c, e, "refocus stage-1 launch");
+        }
+        {
+            TimedScope ts(c, KC_STAGE2, st);
+            cudaError_t e = cpi::launch_refocus_stage2(c->T, Wa, Ha, Hb, m_base, m_count, c->xs, c->ys,
+                                                       planes + int64_t(p) * Ha * Wa, st);
+            c->launches += 1;
+            if (e != cudaSuccess) return cuda_fail(c, e, "refocus stage-2 launch");
+        }
+    }
+    return CPI_OK;
+}
+
+int64_t cpi_launch_count(const cpi_ctx* c) { return c ? c->launches : 0; }
+
+cpi_status cpi_set_timing(cpi_ctx* c, int32_t enable) {
+    if (!c) return CPI_ERR_INVALID_ARG;
+    drain_timing(c);
+    for (int i = 0; i < KC_COUNT; ++i) { c->acc_ms[i] = 0; c->acc_n[i] = 0; }
+    c->timing = enable != 0;
+    return CPI_OK;
+}
+
+cpi_status cpi_kernel_time_ms(cpi_ctx* c, int32_t cls, double* ms, int64_t* launches) {
+    if (!c || cls < 0 || cls >= KC_COUNT) return CPI_ERR_INVALID_ARG;
+    drain_timing(c);
+    if (ms) *ms = c->acc_ms[cls];
+    if (launches) *launches = c->acc_n[cls];
+    return CPI_OK;
+}
+
+}  // extern "C"

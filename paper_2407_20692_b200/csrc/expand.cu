@@ -1,0 +1,101 @@
+// expand.cu — KB1: on-device bit unpacking of SwissSPAD2 frames into GEMM operands,
+// fused with the single-pixel sums S_a / S_b of Eq. (1).
+//
+// PAPER.md:265 (prototype: "bit-unpacking is performed" before the matrix product),
+// PAPER.md:266-267 (bit-packed AND variant; unpack joint with correlation)
+// (frame layout), P:104-109 (single-pixel sums).  SURVEY §8(a) row a2.
+//
+// One CTA = one RoI row m of one arm x 512 consecutive frames.  The row's bytes for 128
+// frames are staged in shared memory; each warp then owns one pixel at a time and every
+// lane produces 4 consecutive frames of it, so a warp stores 128 contiguous bytes of the
+// pixel's K-major operand row (fully coalesced).  Frames in [n, k_pad) are written as
+// zeros, so the GEMM's K tail is inert.  The bit-stream variant (KB3 operand) ballots the
+// same bits into pixel-major 32-bit words (bit f%32 of word f/32 = frame f).
+#include "kernels.h"
+
+namespace cpi {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kSub = 128;       // frames per staged sub-block
+constexpr int kFramesCta = 512; // frames per CTA
+constexpr int kRowStride = 65;  // bytes per staged frame row: odd word stride -> no bank conflicts
+constexpr int kMaxWidth = 512;
+
+template <bool kBits>
+__global__ void __launch_bounds__(kThreads)
+expand_kernel(const uint8_t* __restrict__ frames, int64_t n, int row_bytes, int frame_h, int msb,
+              RoiDev roi, void* __restrict__ op, int64_t ld, int64_t k_pad, int32_t* __restrict__ s) {
+    __shared__ uint8_t sbits[kSub * kRowStride];
+    __shared__ int cnt[kMaxWidth];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int m = blockIdx.y;
+    const int b0 = roi.x0 >> 3;
+    const int nb = ((roi.x0 + roi.w - 1) >> 3) - b0 + 1;
+    for (int j = tid; j < roi.w; j += kThreads) cnt[j] = 0;
+    const int64_t f_begin = static_cast<int64_t>(blockIdx.x) * kFramesCta;
+    const int64_t row_off = static_cast<int64_t>(roi.y0 + m) * row_bytes + b0;
+    for (int sub = 0; sub < kFramesCta / kSub; ++sub) {
+        const int64_t f0 = f_begin + sub * kSub;
+        if (f0 >= k_pad) break;
+        __syncthreads();
+        for (int idx = tid; idx < kSub * nb; idx += kThreads) {
+            const int fl = idx / nb, b = idx - fl * nb;
+            const int64_t f = f0 + fl;
+            sbits[fl * kRowStride + b] =
+                (f < n) ? __ldg(frames + f * frame_h * row_bytes + row_off + b) : uint8_t(0);
+        }
+        __syncthreads();
+        for (int j = warp; j < roi.w; j += kThreads / 32) {
+            const int col = roi.x0 + j;
+            const int b = (col >> 3) - b0;
+            const int sh = msb ? 7 - (col & 7) : (col & 7);
+            const int64_t prow = static_cast<int64_t>(m) * roi.w + j;
+            int c;
+            if constexpr (!kBits) {
+                uint32_t word = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    word |= static_cast<uint32_t>((sbits[(4 * lane + k) * kRowStride + b] >> sh) & 1)
+                            << (8 * k);
+                *reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(op) + prow * ld + f0 + 4 * lane) = word;
+                c = __popc(word);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            } else {
+                c = 0;
+                uint32_t mine = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t bit = (sbits[(32 * q + lane) * kRowStride + b] >> sh) & 1;
+                    const uint32_t w = __ballot_sync(0xffffffffu, bit);
+                    c += __popc(w);
+                    if (lane == q) mine = w;
+                }
+                if (lane < 4)
+                    static_cast<uint32_t*>(op)[prow * ld + (f0 >> 5) + lane] = mine;
+            }
+            if (lane == 0) cnt[j] += c;   // pixel j is owned by this warp only
+        }
+    }
+    __syncthreads();
+    for (int j = tid; j < roi.w; j += kThreads)
+        if (cnt[j]) atomicAdd(s + static_cast<int64_t>(m) * roi.w + j, cnt[j]);
+}
+
+}  // namespace
+
+void launch_expand(const uint8_t* frames, int64_t n, int row_bytes, int frame_h, int msb,
+                   RoiDev roi, void* op, int64_t ld, int64_t k_pad, int32_t* s, bool bitstreams,
+                   cudaStream_t st) {
+    if (k_pad <= 0) return;
+    dim3 grid(static_cast<unsigned>((k_pad + kFramesCta - 1) / kFramesCta), roi.h);
+    if (bitstreams)
+        expand_kernel<true><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
+                                                       ld, k_pad, s);
+    else
+        expand_kernel<false><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
+                                                        ld, k_pad, s);
+}
+
+}  // namespace cpi

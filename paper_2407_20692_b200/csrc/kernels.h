@@ -1,0 +1,70 @@
+// kernels.h — host-side launchers of the CPI device kernels (internal to libcpi).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace cpi {
+
+struct RoiDev {
+    int x0, y0, w, h;
+};
+
+// Epilogue of the pair-sum GEMMs: exact Eq. (1) normalisation and/or int32 counts.
+struct Epilogue {
+    const int32_t* s_a;   // [P_a] totals (including this batch)
+    const int32_t* s_b;   // [P_b]
+    float* gamma;         // [P_a][ldg] or nullptr
+    int64_t ldg;
+    int32_t* counts;      // [P_a][ldc] or nullptr
+    int64_t ldc;
+    int accumulate;       // add the existing counts before storing / normalising
+    int p_a, p_b;         // valid rows / columns
+    int vec;              // 16-byte vector stores allowed (ldg, ldc, p_b multiples of 4)
+    double n;             // N_TOT (all batches)
+    double inv_n2;        // 1 / N_TOT^2
+};
+
+// KB1: expand one RoI of packed frames into a K-major operand (bytes 0/1, or packed
+// pixel-major 32-bit bit streams when `bitstreams`), zero-filling frames [n, k_pad),
+// and accumulate the single-pixel sums into s[P].
+void launch_expand(const uint8_t* frames, int64_t n, int row_bytes, int frame_h, int msb,
+                   RoiDev roi, void* op, int64_t ld, int64_t k_pad, int32_t* s, bool bitstreams,
+                   cudaStream_t st);
+
+// KB2: persistent tcgen05 kind::i8 GEMM  S = A^T B  (A: [M_pad][K] u8, B: [N_pad][K] u8,
+// both K-major) with the fused epilogue.  k_blocks = K / 128.
+cudaError_t launch_gemm_tc(const CUtensorMap* tma_a, const CUtensorMap* tma_b, int m_tiles,
+                           int n_tiles, int k_blocks, const Epilogue& epi, int num_sms,
+                           cudaStream_t st);
+int gemm_tc_block_m();
+int gemm_tc_block_n();
+
+// KB3: popcount(AND) GEMM on CUDA cores over 32-bit bit streams [rows][ldw].
+cudaError_t launch_gemm_popc(const uint32_t* a, const uint32_t* b, int64_t ldw, int64_t kw,
+                             const Epilogue& epi, cudaStream_t st);
+int gemm_popc_block();
+
+// KB4: Gamma rows from int32 counts.
+cudaError_t launch_finalize(const int32_t* counts, int64_t ldc, int64_t rows, int64_t p_b,
+                            const int32_t* s_a_rows, const int32_t* s_b, double n, float* gamma,
+                            int64_t ldg, cudaStream_t st);
+
+// KB5/KB6 refocusing.
+struct AxisTables {           // one axis (x with B-axis u, or y with B-axis v)
+    int32_t* i0;              // [Wb][W]  lower interpolation index, -1 = sample skipped
+    double* t;                // [Wb][W]  interpolation fraction
+    int32_t* cnt;             // [W]      number of used samples per output coordinate
+    int32_t* lo;              // [Wb]     min used i0 over outputs (INT_MAX if none)
+    int32_t* hi;              // [Wb]     max used i0 + 1 over outputs (-1 if none)
+};
+cudaError_t launch_refocus_coords(double alpha, int boundary, int W, int Wb, AxisTables tab,
+                                  cudaStream_t st);
+cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
+                                  int m_base, int m_count, AxisTables xs, AxisTables ys,
+                                  double* T, cudaStream_t st);
+cudaError_t launch_refocus_stage2(const double* T, int Wa, int Ha, int Hb, int m_base,
+                                  int m_count, AxisTables xs, AxisTables ys, float* plane,
+                                  cudaStream_t st);
+
+}  // namespace cpi

@@ -1,0 +1,221 @@
+// refocus.cu — KB5/KB6: refocusing of Gamma into a stack of planes (PAPER.md:114-116,
+// P:269-272; SPEC.md:274 default map).
+//
+// For plane alpha the output pixel (x, y) is the mean, over the B lattice (u, v), of Gamma
+// interpolated at A coordinates c_x(x,u), c_y(y,v) and B coordinates (u, v).  Because the
+// B coordinates are integers the 4D multilinear interpolation reduces exactly to
+// bilinear interpolation over the A axes, and the sum separates:
+//   stage 1 (KB5):  T[x][m][v] = sum_u [(1-t_x) G(m, j0; v, u) + t_x G(m, j0+1; v, u)]
+//   stage 2 (KB6):  R[y][x]    = sum_v [(1-t_y) T[x][m0][v] + t_y T[x][m0+1][v]] / (cnt_x cnt_y)
+// with (j0, t_x) = support of c_x(x,u) and (m0, t_y) of c_y(y,v), and skipped samples
+// removed from both the sums and the counts (skip rule is per axis, so counts factorise).
+// The interpolation coordinates are computed on the device for each plane ("computed
+// on-the-fly in the main refocusing kernel") by KB5a in fp64 with the operation
+// order of the declared convention, so skip / index decisions are exact.
+//
+// Stage 1 streams Gamma from HBM once per plane: a CTA owns one A row m and 8 B rows v,
+// stages 8-column (u) slabs of the rows j it needs into padded shared memory (odd word
+// stride -> conflict-free gathers), and each thread owns one output x.
+#include <climits>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cpi {
+namespace {
+
+constexpr int kVG = 8;     // B rows v per stage-1 CTA
+constexpr int kUC = 8;     // B columns u per staged slab
+constexpr int kPad = 9;    // smem words per staged (v, j) row (odd -> no bank conflicts)
+constexpr int kS1Threads = 256;
+
+// ---- KB5a: per-axis interpolation tables ------------------------------------------
+// Block per B coordinate ub (u or v), threads over the output coordinate x (or y).
+__global__ void coords_kernel(double alpha, int boundary, int W, int Wb, AxisTables tab) {
+    const int ub = blockIdx.x;
+    const double c_a = (W - 1) / 2.0, c_b = (Wb - 1) / 2.0;
+    const double one_minus = __dadd_rn(1.0, -alpha);
+    const double bu = __dmul_rn(one_minus, __dadd_rn(static_cast<double>(ub), -c_b));
+    int lo = INT_MAX, hi = -1;
+    for (int x = threadIdx.x; x < W; x += blockDim.x) {
+        // c = (alpha*(x - c_a)) + ((1 - alpha)*(u - c_b)) + c_a, each op rounded, no FMA
+        double c = __dadd_rn(__dadd_rn(__dmul_rn(alpha, __dadd_rn(static_cast<double>(x), -c_a)), bu), c_a);
+        bool ok;
+        if (boundary == 0) {
+            ok = (c >= 0.0) && (c <= static_cast<double>(W - 1));
+        } else {
+            c = fmin(fmax(c, 0.0), static_cast<double>(W - 1));
+            ok = true;
+        }
+        int i0 = 0;
+        double t = 0.0;
+        if (ok) {
+            double f = floor(c);
+            if (f > static_cast<double>(W - 2)) f = static_cast<double>(W - 2);
+            i0 = static_cast<int>(f);
+            t = __dadd_rn(c, -f);
+            lo = min(lo, i0);
+            hi = max(hi, i0 + 1);
+            atomicAdd(tab.cnt + x, 1);
+        }
+        tab.i0[static_cast<int64_t>(ub) * W + x] = ok ? i0 : -1;
+        tab.t[static_cast<int64_t>(ub) * W + x] = t;
+    }
+    // block min / max
+    __shared__ int slo[32], shi[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if (lane == 0) { slo[warp] = lo; shi[warp] = hi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < nw; ++w) { lo = min(lo, slo[w]); hi = max(hi, shi[w]); }
+        tab.lo[ub] = lo;
+        tab.hi[ub] = hi;
+    }
+}
+
+// ---- KB5: stage 1 -----------------------------------------------------------------
+// grid (ceil(Hb / kVG), m_count, ceil(Wa / 256)); thread = output x.
+__global__ void __launch_bounds__(kS1Threads)
+stage1_kernel(const float* __restrict__ gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
+              int m_base, AxisTables xs, AxisTables ys, double* __restrict__ T) {
+    extern __shared__ float sm[];   // [kVG][nj][kPad]
+    const int v0 = blockIdx.x * kVG;
+    const int m = m_base + blockIdx.y;
+    const int x = blockIdx.z * kS1Threads + threadIdx.x;
+    const int nv = min(kVG, Hb - v0);
+    // which of this CTA's v rows need A row m (stage 2 reads m in [lo_y(v), hi_y(v)])
+    unsigned need = 0;
+    for (int v = 0; v < nv; ++v) {
+        const int lo = __ldg(ys.lo + v0 + v), hi = __ldg(ys.hi + v0 + v);
+        if (m >= lo && m <= hi) need |= 1u << v;
+    }
+    if (!need) return;
+    double acc[kVG];
+#pragma unroll
+    for (int v = 0; v < kVG; ++v) acc[v] = 0.0;
+    const float* g_m = gamma + static_cast<int64_t>(m - m_base) * Wa * ldg;   // row (m, j=0) of the shard
+    for (int u0 = 0; u0 < Wb; u0 += kUC) {
+        const int nu = min(kUC, Wb - u0);
+        int jlo = INT_MAX, jhi = -1;
+        for (int k = 0; k < nu; ++k) {
+            jlo = min(jlo, __ldg(xs.lo + u0 + k));
+            jhi = max(jhi, __ldg(xs.hi + u0 + k));
+        }
+        if (jhi < jlo) continue;              // no x uses these u (block-uniform)
+        const int nj = jhi - jlo + 1;
+        __syncthreads();
+        // stage rows (v, j), columns [u0, u0+nu): Gamma[(m, j)][(v0+v, u)]
+        for (int rr = threadIdx.x; rr < nv * nj; rr += kS1Threads) {
+            const int v = rr / nj, jj = rr - v * nj;
+            const float* src = g_m + static_cast<int64_t>(jlo + jj) * ldg + static_cast<int64_t>(v0 + v) * Wb + u0;
+            float* dst = sm + (v * nj + jj) * kPad;
+            if (nu == kUC && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+                const float4 p0 = __ldg(reinterpret_cast<const float4*>(src));
+                const float4 p1 = __ldg(reinterpret_cast<const float4*>(src) + 1);
+                dst[0] = p0.x; dst[1] = p0.y; dst[2] = p0.z; dst[3] = p0.w;
+                dst[4] = p1.x; dst[5] = p1.y; dst[6] = p1.z; dst[7] = p1.w;
+            } else {
+                for (int k = 0; k < nu; ++k) dst[k] = __ldg(src + k);
+            }
+        }
+        __syncthreads();
+        if (x < Wa) {
+            float part[kVG];
+#pragma unroll
+            for (int v = 0; v < kVG; ++v) part[v] = 0.f;
+            for (int k = 0; k < nu; ++k) {
+                const int64_t ti = static_cast<int64_t>(u0 + k) * Wa + x;
+                const int j0 = __ldg(xs.i0 + ti);
+                if (j0 < 0) continue;
+                const float t = static_cast<float>(__ldg(xs.t + ti));
+                const float w0 = 1.f - t;
+                const float* s0 = sm + (j0 - jlo) * kPad + k;
+#pragma unroll
+                for (int v = 0; v < kVG; ++v) {
+                    if (v < nv) {
+                        const float g0 = s0[v * nj * kPad];
+                        const float g1 = s0[v * nj * kPad + kPad];
+                        part[v] = fmaf(t, g1, fmaf(w0, g0, part[v]));
+                    }
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < kVG; ++v) acc[v] += static_cast<double>(part[v]);
+        }
+    }
+    if (x < Wa) {
+        double* dst = T + (static_cast<int64_t>(x) * Ha + m) * Hb + v0;
+        for (int v = 0; v < nv; ++v)
+            if (need & (1u << v)) dst[v] = acc[v];
+    }
+}
+
+// ---- KB6: stage 2 -----------------------------------------------------------------
+// One warp per output pixel (x, y); lanes stride over v; warp-shuffle fp64 reduction.
+__global__ void stage2_kernel(const double* __restrict__ T, int Wa, int Ha, int Hb, int m_lo,
+                              int m_hi, AxisTables xs, AxisTables ys, float* __restrict__ plane) {
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= static_cast<int64_t>(Wa) * Ha) return;
+    const int x = static_cast<int>(gw % Wa), y = static_cast<int>(gw / Wa);
+    const double* Tx = T + static_cast<int64_t>(x) * Ha * Hb;
+    double sum = 0.0;
+    for (int v = lane; v < Hb; v += 32) {
+        const int64_t ti = static_cast<int64_t>(v) * Ha + y;
+        const int m0 = __ldg(ys.i0 + ti);
+        if (m0 < 0) continue;
+        const double t = __ldg(ys.t + ti);
+        const double t0 = (m0 >= m_lo && m0 < m_hi) ? Tx[static_cast<int64_t>(m0) * Hb + v] : 0.0;
+        const double t1 = (m0 + 1 >= m_lo && m0 + 1 < m_hi) ? Tx[static_cast<int64_t>(m0 + 1) * Hb + v] : 0.0;
+        sum += __dadd_rn(1.0, -t) * t0 + t * t1;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) {
+        const int64_t c = static_cast<int64_t>(__ldg(xs.cnt + x)) * __ldg(ys.cnt + y);
+        plane[static_cast<int64_t>(y) * Wa + x] = c ? static_cast<float>(sum / static_cast<double>(c)) : 0.f;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_refocus_coords(double alpha, int boundary, int W, int Wb, AxisTables tab,
+                                  cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(tab.cnt, 0, sizeof(int32_t) * W, st);
+    if (e != cudaSuccess) return e;
+    int threads = W >= 256 ? 256 : ((W + 31) / 32) * 32;
+    coords_kernel<<<Wb, threads, 0, st>>>(alpha, boundary, W, Wb, tab);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
+                                  int m_base, int m_count, AxisTables xs, AxisTables ys, double* T,
+                                  cudaStream_t st) {
+    const size_t smem = static_cast<size_t>(kVG) * Wa * kPad * sizeof(float);
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        cudaError_t e = cudaFuncSetAttribute(stage1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        attr = smem;
+    }
+    dim3 grid((Hb + kVG - 1) / kVG, m_count, (Wa + kS1Threads - 1) / kS1Threads);
+    stage1_kernel<<<grid, kS1Threads, smem, st>>>(gamma, ldg, Wa, Ha, Wb, Hb, m_base, xs, ys, T);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_refocus_stage2(const double* T, int Wa, int Ha, int Hb, int m_base, int m_count,
+                                  AxisTables xs, AxisTables ys, float* plane, cudaStream_t st) {
+    const int64_t warps = static_cast<int64_t>(Wa) * Ha;
+    const int64_t blocks = (warps * 32 + 255) / 256;
+    stage2_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(T, Wa, Ha, Hb, m_base, m_base + m_count,
+                                                                 xs, ys, plane);
+    return cudaGetLastError();
+}
+
+}  // namespace cpi

@@ -1,0 +1,265 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle on identical seeded inputs.
+
+Bars (BASELINE.json north_star):
+  * S_a, S_b, S_ab: bit-exact (integers).
+  * Gamma (fp32) vs the oracle's exact rational rounded to fp64: |g - G| <= 1e-6 |G|, and
+    G == 0 => g == 0 exactly.
+  * Refocused planes (fp32): |R - R_o| <= 1e-6 * M + 1e-30 with M(x,y) the oracle's
+    refocusing of |Gamma| (mean absolute contribution; M >= |R_o|, = |R_o| when no
+    cancellation), stated per output.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests._util import pack
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "-m gpu selected but no CUDA device: GPU parity cannot run"
+    from paper_2407_20692_b200 import build
+    build.build()
+
+
+def _ctx(roi_a, roi_b, max_frames, **kw):
+    from paper_2407_20692_b200 import Context
+    return Context(roi_a, roi_b, max_frames, **kw)
+
+
+def _gpu_sums(frames, roi_a, roi_b, variant="tc", batches=None, width=512, height=256, gamma=True):
+    n = frames.shape[0]
+    batches = batches or [n]
+    ctx = _ctx(roi_a, roi_b, max(max(batches), 1), variant=variant, keep_counts=True,
+               width=width, height=height)
+    g = ctx.new_gamma() if gamma else None
+    off = 0
+    for b in batches:
+        ctx.load_frames(np.ascontiguousarray(frames[off:off + b]))
+        ctx.correlate(g)
+        off += b
+    s_ab = torch.empty((ctx.p_a, ctx.p_b), dtype=torch.int32, device="cuda")
+    s_a = torch.empty(ctx.p_a, dtype=torch.int32, device="cuda")
+    s_b = torch.empty(ctx.p_b, dtype=torch.int32, device="cuda")
+    n_tot = ctx.get_counts(s_ab, s_a, s_b)
+    torch.cuda.synchronize()
+    out = dict(s_ab=s_ab.cpu().numpy(), s_a=s_a.cpu().numpy(), s_b=s_b.cpu().numpy(), n=n_tot,
+               gamma=g.cpu().numpy() if gamma else None, ctx=ctx)
+    return out
+
+
+def _assert_gamma(g_gpu, g_exact):
+    g_gpu = g_gpu.astype(np.float64)
+    zero = g_exact == 0
+    assert np.all(g_gpu[zero] == 0.0), "exact zeros must stay zero"
+    rel = np.abs(g_gpu - g_exact) / np.where(zero, 1.0, np.abs(g_exact))
+    assert rel.max() <= 1e-6, f"max rel err {rel.max():.3e}"
+
+
+def _check_sums(got, want):
+    np.testing.assert_array_equal(got["s_a"], want["s_a"])
+    np.testing.assert_array_equal(got["s_b"], want["s_b"])
+    np.testing.assert_array_equal(got["s_ab"], want["s_ab"])
+    assert got["n"] == want["n"]
+
+
+@pytest.mark.parametrize("variant", ["tc", "popc"])
+def test_tiny_config_bit_exact(variant):
+    """BASELINE configs[0]: 8x8 rho_a x 4x4 rho_b (non byte-aligned), 1000 frames."""
+    fr = synth.bernoulli_frames(1000, 0.05, seed=synth.SEED_ARMS)
+    want = oracle.correlate(fr, synth.ROI_TINY_A, synth.ROI_TINY_B)
+    got = _gpu_sums(fr, synth.ROI_TINY_A, synth.ROI_TINY_B, variant)
+    _check_sums(got, want)
+    _assert_gamma(got["gamma"], want["gamma"])
+
+
+@pytest.mark.parametrize("variant", ["tc", "popc"])
+@pytest.mark.parametrize("n", [1, 31, 127, 129, 1000, 2600])
+def test_ragged_tiles_and_k_tails(variant, n):
+    """Several M/N tiles with ragged edges (P_a = 1500, P_b = 380) and K tails (N not a
+    multiple of 128): zero padding must be inert."""
+    roi_a, roi_b = (3, 7, 50, 30), (261, 2, 20, 19)
+    fr = synth.bernoulli_frames(n, 0.3, seed=n)
+    want = oracle.correlate(fr, roi_a, roi_b)
+    got = _gpu_sums(fr, roi_a, roi_b, variant)
+    _check_sums(got, want)
+    _assert_gamma(got["gamma"], want["gamma"])
+
+
+def test_chaotic_light_dense_and_identities():
+    """Correlated (speckle) data with exact identities: same RoI on both arms -> S_ab
+    symmetric; Gamma diagonal = f(1-f) (exact rational), checked through the GPU path."""
+    roi = (10, 20, 40, 24)
+    fr = synth.speckle_frames(3000, roi, (300, 20, 40, 24), f=0.3, grain=3, shift_b=(0, 0))
+    want = oracle.correlate(fr, roi, roi)
+    got = _gpu_sums(fr, roi, roi, "tc")
+    _check_sums(got, want)
+    np.testing.assert_array_equal(got["s_ab"], got["s_ab"].T)
+    _assert_gamma(got["gamma"], want["gamma"])
+
+
+def test_multi_batch_accumulation_and_virtual_ranks():
+    """S:235-243 accumulate_chunk: three batches == one batch, bit for bit; and the
+    frame-sharded decomposition: G slices in separate contexts, summed,
+    equal the single-context sums (the multi-GPU contract, emulated on one GPU)."""
+    roi_a, roi_b = (0, 0, 64, 20), (256, 0, 30, 20)
+    fr = synth.bernoulli_frames(3000, 0.1, seed=5)
+    one = _gpu_sums(fr, roi_a, roi_b, "tc")
+    three = _gpu_sums(fr, roi_a, roi_b, "tc", batches=[1000, 1, 1999])
+    _check_sums(three, one)
+    np.testing.assert_array_equal(three["gamma"], one["gamma"])
+    parts = [_gpu_sums(fr[a:b], roi_a, roi_b, "tc", gamma=False) for a, b in [(0, 700), (700, 2048), (2048, 3000)]]
+    np.testing.assert_array_equal(sum(p["s_ab"] for p in parts), one["s_ab"])
+    np.testing.assert_array_equal(sum(p["s_a"] for p in parts), one["s_a"])
+
+
+def test_device_frames_in_place_and_finalize():
+    """CPI_DEVICE frames are used in place; cpi_finalize from kept counts equals the fused
+    epilogue's Gamma bit for bit; cpi_finalize_counts of a row shard equals its rows."""
+    roi_a, roi_b = (5, 5, 33, 17), (300, 1, 12, 12)
+    fr = synth.bernoulli_frames(777, 0.2, seed=9)
+    ctx = _ctx(roi_a, roi_b, 777, keep_counts=True)
+    d = torch.from_numpy(fr).cuda()
+    ctx.load_frames(d)
+    g1 = ctx.new_gamma()
+    ctx.correlate(g1)
+    g2 = ctx.new_gamma()
+    n = ctx.finalize(g2)
+    assert n == 777
+    assert torch.equal(g1, g2)
+    s_ab = torch.empty((ctx.p_a, ctx.p_b), dtype=torch.int32, device="cuda")
+    s_a = torch.empty(ctx.p_a, dtype=torch.int32, device="cuda")
+    s_b = torch.empty(ctx.p_b, dtype=torch.int32, device="cuda")
+    ctx.get_counts(s_ab, s_a, s_b)
+    rows = torch.empty((66, ctx.p_b), dtype=torch.float32, device="cuda")
+    ctx.finalize_counts(s_ab[33:99].contiguous(), 33, s_a, s_b, n, rows)
+    assert torch.equal(rows, g1[33:99])
+
+
+def test_error_paths_on_device():
+    from paper_2407_20692_b200 import CpiError
+    ctx = _ctx((0, 0, 8, 8), (8, 0, 8, 8), 10)
+    with pytest.raises(CpiError, match="STATE"):
+        ctx.correlate(ctx.new_gamma())            # nothing loaded
+    with pytest.raises(CpiError, match="CAPACITY"):
+        ctx.load_frames(np.zeros((11, 256, 64), np.uint8))
+    with pytest.raises(CpiError, match="SIZE_MISMATCH"):
+        ctx.load_frames(np.zeros(16385, np.uint8))
+    ctx.load_frames(np.zeros((0, 256, 64), np.uint8))
+    with pytest.raises(CpiError, match="ZERO_FRAMES"):
+        ctx.correlate(ctx.new_gamma())
+    ctx.load_frames(np.zeros((3, 256, 64), np.uint8))
+    g = ctx.new_gamma()
+    ctx.correlate(g)
+    assert torch.all(g == 0)
+    with pytest.raises(CpiError, match="STATE"):
+        ctx.load_frames(np.zeros((3, 256, 64), np.uint8))
+        ctx.correlate(g)                          # second batch without KEEP_COUNTS
+    planes = ctx.new_planes(1)
+    with pytest.raises(CpiError, match="DEGENERATE_ALPHA"):
+        ctx.refocus([0.0], g, planes)
+    with pytest.raises(CpiError, match="EMPTY_ANGULAR_GRID"):
+        ctx.refocus([], g, planes)
+
+
+# ------------------------------------------------------------------ refocusing ---------
+
+def _refocus_gpu(G, dims, alphas, boundary=0, row0=0, rows=None):
+    Wa, Ha, Wb, Hb = dims
+    ctx = _ctx((0, 0, Wa, Ha), (0, 0, Wb, Hb), 1)
+    g = torch.from_numpy(np.ascontiguousarray(G, dtype=np.float32)).cuda()
+    planes = ctx.new_planes(len(alphas))
+    ctx.refocus(alphas, g[row0:] if row0 else g, planes, row0=row0, rows=rows, boundary=boundary)
+    torch.cuda.synchronize()
+    return planes.cpu().numpy().astype(np.float64)
+
+
+def _assert_planes(R, G, dims, alphas, boundary=0):
+    Ro = oracle.refocus(G, dims, alphas, boundary=boundary)
+    M = oracle.refocus(np.abs(G.astype(np.float64)), dims, alphas, boundary=boundary)
+    err = np.abs(R - Ro)
+    assert np.all(err <= 1e-6 * M + 1e-30), f"max err/M {np.max(err / np.maximum(M, 1e-300)):.3e}"
+
+
+@pytest.mark.parametrize("dims", [(24, 20, 16, 12), (7, 5, 9, 3), (40, 33, 37, 10)])
+@pytest.mark.parametrize("boundary", [0, 1])
+def test_refocus_random_gamma(dims, boundary):
+    Wa, Ha, Wb, Hb = dims
+    G = synth.random_gamma(Wa * Ha, Wb * Hb, seed=sum(dims))
+    alphas = [0.5, 0.75, 1.0, 1.3, 2.0, -0.6]
+    R = _refocus_gpu(G, dims, alphas, boundary)
+    _assert_planes(R, G, dims, alphas, boundary)
+
+
+def test_refocus_integer_shear_and_ramp():
+    """Closed forms through the GPU path: integer shear at alpha=2 reproduces O(2x,2y)
+    (fp32 taps; within 1e-6 rel), the sheared ramp reproduces a + b alpha x' + c alpha y'."""
+    W, H = 33, 21
+    rng = np.random.default_rng(4)
+    O = (rng.random((2 * W - 1, 2 * H - 1)) + 0.5).astype(np.float32)
+    jj, uu = np.meshgrid(np.arange(W), np.arange(W), indexing="ij")
+    mm, vv = np.meshgrid(np.arange(H), np.arange(H), indexing="ij")
+    G = np.ascontiguousarray(O[(jj + uu)[None, :, None, :], (mm + vv)[:, None, :, None]].reshape(H * W, H * W))
+    R = _refocus_gpu(G, (W, H, W, H), [2.0])[0]
+    xs, ys = np.meshgrid(np.arange(W), np.arange(H))
+    _, cnt = oracle.refocus(G, (W, H, W, H), [2.0], return_counts=True)
+    ok = cnt[0] > 0
+    np.testing.assert_allclose(R[ok], O[2 * xs, 2 * ys][ok], rtol=1e-6)
+    assert np.all(R[~ok] == 0)
+    # sheared ramp
+    Wa, Ha, Wb, Hb = 30, 26, 22, 14
+    for alpha in (0.6, 1.4):
+        s = 1 - alpha
+        j = np.arange(Wa) - (Wa - 1) / 2
+        m = np.arange(Ha) - (Ha - 1) / 2
+        u = np.arange(Wb) - (Wb - 1) / 2
+        v = np.arange(Hb) - (Hb - 1) / 2
+        G4 = (0.02 + 0.001 * (j[None, :, None, None] - s * u[None, None, None, :])
+              - 0.0007 * (m[:, None, None, None] - s * v[None, None, :, None]))
+        R = _refocus_gpu(G4.reshape(Ha * Wa, Hb * Wb), (Wa, Ha, Wb, Hb), [alpha])[0]
+        _, cnt = oracle.refocus(G4.reshape(Ha * Wa, Hb * Wb), (Wa, Ha, Wb, Hb), [alpha], return_counts=True)
+        expect = 0.02 + 0.001 * alpha * j[None, :] - 0.0007 * alpha * m[:, None]
+        ok = cnt[0] > 0
+        np.testing.assert_allclose(R[ok], expect[ok], rtol=2e-6, atol=1e-9)
+
+
+def test_refocus_row_shards_sum_to_whole():
+    """Row-sharded refocus: the planes of A-row shards add up to the plane of
+    the whole Gamma (linearity), so an all-reduce of shard planes is the multi-GPU merge."""
+    dims = (20, 16, 12, 10)
+    Wa, Ha, Wb, Hb = dims
+    G = synth.random_gamma(Wa * Ha, Wb * Hb, seed=3)
+    al = [0.7, 1.0, 1.6]
+    whole = _refocus_gpu(G, dims, al)
+    parts = sum(_refocus_gpu(G, dims, al, row0=r0 * Wa, rows=(r1 - r0) * Wa) for r0, r1 in [(0, 5), (5, 11), (11, 16)])
+    np.testing.assert_allclose(parts, whole, rtol=1e-5, atol=1e-7)
+
+
+def test_end_to_end_frames_to_planes_alpha1_ghost():
+    """frames -> GPU Gamma -> GPU planes; alpha = 1 equals the direct ghost image computed
+    from the frames (closed form), and every plane matches the oracle pipeline."""
+    roi_a, roi_b = (0, 0, 32, 24), (256, 0, 20, 16)
+    fr = synth.bernoulli_frames(4000, 0.1, seed=12)
+    ctx = _ctx(roi_a, roi_b, 4000)
+    ctx.load_frames(fr)
+    g = ctx.correlate(ctx.new_gamma())
+    al = [0.5, 1.0, 1.5]
+    planes = ctx.new_planes(3)
+    ctx.refocus(al, g, planes)
+    torch.cuda.synchronize()
+    R = planes.cpu().numpy().astype(np.float64)
+    want = oracle.correlate(fr, roi_a, roi_b)
+    dims = (32, 24, 20, 16)
+    _assert_planes(R, want["gamma"], dims, al)
+    from tests._util import unpack_np
+    A = unpack_np(fr, roi_a).astype(np.int64)
+    nB = unpack_np(fr, roi_b).astype(np.int64).sum(1)
+    n = 4000
+    ghost = (n * (A.T @ nB) - A.sum(0) * nB.sum()) / (n * n * 320.0)
+    M = oracle.refocus(np.abs(want["gamma"]), dims, [1.0])[0].reshape(-1)
+    assert np.all(np.abs(R[1].reshape(-1) - ghost) <= 1e-6 * M + 1e-30)
