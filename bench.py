@@ -273,6 +273,7 @@ def main():
     def step(src):
         """one pass of a1..a6; src = device frames (resident) or pinned host frames (e2e)"""
         if world == 1:
+            ctx.reset()          # a new acquisition: zero S_a, S_b, N (memsets)
             ctx.load_frames(src)
             ctx.correlate(gamma)
             ctx.refocus(alphas, gamma, planes)

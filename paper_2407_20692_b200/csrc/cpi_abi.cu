@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -23,11 +24,6 @@ enum KernelClass { KC_GEMM = 0, KC_EXPAND = 1, KC_STAGE1 = 2, KC_STAGE2 = 3, KC_
                    KC_COORDS = 5, KC_COUNT = 6 };
 
 thread_local std::string g_create_error;
-
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
@@ -59,6 +55,9 @@ struct cpi_ctx {
     // refocus workspaces
     cpi::AxisTables xs{}, ys{};
     double* T = nullptr;
+    int2* xpack = nullptr;                 // packed x-table for the TMA stage 1
+    cpi::Stage1Maps s1maps{};
+    bool use_s1_tma = false;
     // accounting
     int64_t launches = 0;
     bool timing = false;
@@ -137,7 +136,9 @@ bool roi_ok(const cpi_roi& r, const cpi_layout& l) {
            static_cast<int64_t>(r.y0) + r.height <= l.height_px;
 }
 
-EncodeTiledFn get_encode() {
+}  // namespace
+
+cpi::EncodeTiledFn cpi::encode_tiled_fn() {
     static EncodeTiledFn fn = nullptr;
     static std::once_flag once;
     std::call_once(once, [] {
@@ -150,9 +151,11 @@ EncodeTiledFn get_encode() {
     return fn;
 }
 
+namespace {
+
 cpi_status make_tmap(cpi_ctx* c, CUtensorMap* m, void* base, int64_t rows, int64_t cols,
                      uint32_t box_rows) {
-    EncodeTiledFn enc = get_encode();
+    cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
     if (!enc) return fail(c, CPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols)};   // bytes between rows
@@ -175,6 +178,7 @@ void free_all(cpi_ctx* c) {
     cudaFree(c->xs.i0); cudaFree(c->xs.t); cudaFree(c->xs.cnt); cudaFree(c->xs.lo); cudaFree(c->xs.hi);
     cudaFree(c->ys.i0); cudaFree(c->ys.t); cudaFree(c->ys.cnt); cudaFree(c->ys.lo); cudaFree(c->ys.hi);
     cudaFree(c->T);
+    cudaFree(c->xpack);
     for (auto& t : c->timed) { c->event_pool.push_back(t.a); c->event_pool.push_back(t.b); }
     for (auto e : c->event_pool) cudaEventDestroy(e);
 }
@@ -485,6 +489,32 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
         if (s == CPI_OK) s = alloc_axis(c, c->ys, Ha, Hb);
         if (s != CPI_OK) return s;
         CK(c, cudaMalloc(&c->T, sizeof(double) * size_t(Wa) * Ha * Hb));
+        c->use_s1_tma = cpi::stage1_tma_supported(Wa, Wb) && getenv("CPI_STAGE1_SIMPLE") == nullptr;
+        if (c->use_s1_tma) {
+            CK(c, cudaMalloc(&c->xpack, sizeof(int2) * size_t(Wa) * Wb));
+            cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
+            if (!enc) return fail(c, CPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+            const cuuint64_t dims[2] = {cuuint64_t(Wa), cuuint64_t(Wb)};
+            const cuuint64_t strides[1] = {cuuint64_t(Wa) * 8};
+            const cuuint32_t box[2] = {cuuint32_t(Wa), 8u};
+            const cuuint32_t es[2] = {1u, 1u};
+            CUresult r = enc(&c->s1maps.xtab, CU_TENSOR_MAP_DATA_TYPE_INT64, 2, c->xpack, dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return fail(c, CPI_ERR_CUDA, "x-table tensor map failed (%d)", int(r));
+        }
+    }
+    bool tma_now = c->use_s1_tma && (reinterpret_cast<uintptr_t>(spec->gamma_dev) & 15) == 0;
+    if (tma_now) {
+        cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
+        const cuuint64_t dims[4] = {cuuint64_t(Wb), cuuint64_t(Hb), cuuint64_t(Wa), cuuint64_t(spec->rows / Wa)};
+        const cuuint64_t strides[3] = {cuuint64_t(Wb) * 4, cuuint64_t(c->p_b) * 4, cuuint64_t(Wa) * c->p_b * 4};
+        const cuuint32_t box[4] = {8u, 8u, 32u, 1u};
+        const cuuint32_t es[4] = {1u, 1u, 1u, 1u};
+        CUresult r = enc(&c->s1maps.gamma, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(spec->gamma_dev),
+                         dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(c, CPI_ERR_CUDA, "Gamma tensor map failed (%d)", int(r));
     }
     const int m_base = static_cast<int>(spec->row0 / Wa), m_count = static_cast<int>(spec->rows / Wa);
     for (int p = 0; p < spec->n_planes; ++p) {
@@ -498,9 +528,18 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
         }
         {
             TimedScope ts(c, KC_STAGE1, st);
-            cudaError_t e = cpi::launch_refocus_stage1(spec->gamma_dev, c->p_b, Wa, Ha, Wb, Hb, m_base, m_count,
-                                                       c->xs, c->ys, c->T, st);
-            c->launches += 1;
+            cudaError_t e;
+            if (tma_now) {
+                e = cpi::launch_pack_xtable(c->xs, Wa, Wb, c->xpack, st);
+                if (e == cudaSuccess)
+                    e = cpi::launch_refocus_stage1_tma(&c->s1maps, Wa, Ha, Wb, Hb, m_base, m_count, c->xs, c->ys,
+                                                       c->xpack, c->T, c->num_sms, st);
+                c->launches += 2;
+            } else {
+                e = cpi::launch_refocus_stage1(spec->gamma_dev, c->p_b, Wa, Ha, Wb, Hb, m_base, m_count,
+                                               c->xs, c->ys, c->T, st);
+                c->launches += 1;
+            }
             if (e != cudaSuccess) return cuda_fail(c, e, "refocus stage-1 launch");
         }
         {

@@ -63,6 +63,26 @@ cudaError_t launch_refocus_coords(double alpha, int boundary, int W, int Wb, Axi
 cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
                                   int m_base, int m_count, AxisTables xs, AxisTables ys,
                                   double* T, cudaStream_t st);
+// KB5 (TMA variant): warp-specialised, persistent, TMA-fed stage 1.  Needs W_a <= 256,
+// W_b % 4 == 0 and the tensor maps of Gamma (4D: u, v, j, m) and of the packed x-table
+// (2D int64: x, u) made by make_stage1_maps.
+struct Stage1Maps {
+    CUtensorMap gamma;
+    CUtensorMap xtab;
+};
+bool stage1_tma_supported(int Wa, int Wb);
+cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int Wa, int Ha, int Wb, int Hb,
+                                      int m_base, int m_count, AxisTables xs, AxisTables ys,
+                                      const int2* xpack, double* T, int num_sms, cudaStream_t st);
+// x-table packed for the TMA stage 1: int2 {j0 + 1 (0 = skipped), float bits of t}, [Wb][Wa].
+cudaError_t launch_pack_xtable(AxisTables xs, int Wa, int Wb, int2* xpack, cudaStream_t st);
+// driver entry point cuTensorMapEncodeTiled (nullptr if unavailable)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled_fn();
+
 cudaError_t launch_refocus_stage2(const double* T, int Wa, int Ha, int Hb, int m_base,
                                   int m_count, AxisTables xs, AxisTables ys, float* plane,
                                   cudaStream_t st);

@@ -182,6 +182,177 @@ __global__ void stage2_kernel(const double* __restrict__ T, int Wa, int Ha, int 
     }
 }
 
+
+// ---- KB5 (TMA variant) ------------------------------------------------------------
+// Persistent, warp-specialised.  Tile = (A row m, 8 B rows v); the tile's Gamma is
+// streamed in chunks of 8 B columns u: warp 8 (one elected lane) issues, per chunk, TMA
+// boxes of 32 j-rows x 8 v x 8 u of Gamma covering only the j span the chunk's outputs
+// touch, plus the 8 x 256 packed x-table rows, into a 2-stage smem ring (mbarrier
+// full/empty).  Warps 0..7 consume: lane = (vq = lane/8, xl = lane%8), warp = x block;
+// thread owns x = 8*warp + xl + 64*i (i < 4) and v in {vq, vq+4}.  At step k a lane reads
+// column u' = (k + xl) % 8, so the 32 lanes of a warp hit 32 distinct banks for any
+// j0 (smem row of (j, v) = 8 floats; bank = 8 v + u').
+constexpr int kTVG = 8, kTUC = 8, kTJBox = 32, kTMaxJ = 256, kTStages = 2;
+constexpr int kTGBytes = kTMaxJ * kTVG * kTUC * 4;     // 64 KB per stage
+constexpr int kTXBytes = kTUC * 256 * 8;               // 16 KB per stage
+constexpr int kTConsumers = 8;
+constexpr int kTThreads = 32 * (kTConsumers + 1);
+constexpr int kTSmem = kTStages * (kTGBytes + kTXBytes) + 1024 + 128;
+
+struct S1Args {
+    int Wa, Ha, Wb, Hb, m_base, m_count, n_vg, n_chunks;
+    const int32_t *xlo, *xhi, *ylo, *yhi;
+    double* T;
+};
+
+__device__ __forceinline__ bool tile_needed(const S1Args& a, int m, int v0, unsigned* mask) {
+    unsigned need = 0;
+    const int nv = min(kTVG, a.Hb - v0);
+    for (int v = 0; v < nv; ++v) {
+        const int lo = __ldg(a.ylo + v0 + v), hi = __ldg(a.yhi + v0 + v);
+        if (m >= lo && m <= hi) need |= 1u << v;
+    }
+    *mask = need;
+    return need != 0;
+}
+
+__device__ __forceinline__ bool chunk_span(const S1Args& a, int u0, int* jlo, int* jhi) {
+    int lo = INT_MAX, hi = -1;
+    const int nu = min(kTUC, a.Wb - u0);
+    for (int k = 0; k < nu; ++k) {
+        lo = min(lo, __ldg(a.xlo + u0 + k));
+        hi = max(hi, __ldg(a.xhi + u0 + k));
+    }
+    *jlo = lo;
+    *jhi = hi;
+    return hi >= lo;
+}
+
+__global__ void __launch_bounds__(kTThreads, 1)
+stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_x, S1Args a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    float* sg = reinterpret_cast<float*>(smem);
+    int2* sx = reinterpret_cast<int2*>(smem + kTStages * kTGBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTStages * (kTGBytes + kTXBytes));
+    uint64_t* empty = full + kTStages;
+    int* sjlo = reinterpret_cast<int*>(empty + kTStages);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kTConsumers);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int n_tiles = a.m_count * a.n_vg;
+
+    if (warp == kTConsumers) {
+        if (lane == 0) {
+            tma_prefetch_desc(&tm_g);
+            tma_prefetch_desc(&tm_x);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+                const int ml = tile / a.n_vg, vg = tile - ml * a.n_vg;
+                unsigned mask;
+                if (!tile_needed(a, a.m_base + ml, vg * kTVG, &mask)) continue;
+                for (int c = 0; c < a.n_chunks; ++c) {
+                    int jlo, jhi;
+                    if (!chunk_span(a, c * kTUC, &jlo, &jhi)) continue;
+                    const int nb = (jhi - jlo + kTJBox) / kTJBox;
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    sjlo[stage] = jlo;
+                    mbar_expect_tx(&full[stage], nb * kTJBox * kTVG * kTUC * 4 + kTUC * a.Wa * 8);
+                    float* dst = sg + stage * (kTGBytes / 4);
+                    for (int b = 0; b < nb; ++b)
+                        tma_load_4d(dst + b * kTJBox * kTVG * kTUC, &tm_g, &full[stage], c * kTUC, vg * kTVG,
+                                    jlo + b * kTJBox, ml);
+                    tma_load_2d(sx + stage * (kTXBytes / 8), &tm_x, &full[stage], 0, c * kTUC);
+                    if (++stage == kTStages) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+        return;
+    }
+
+    // consumers
+    const int vq = lane >> 3, xl = lane & 7;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int ml = tile / a.n_vg, vg = tile - ml * a.n_vg;
+        const int m = a.m_base + ml, v0 = vg * kTVG;
+        unsigned mask;
+        if (!tile_needed(a, m, v0, &mask)) continue;
+        double acc[4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { acc[i][0] = 0.0; acc[i][1] = 0.0; }
+        for (int c = 0; c < a.n_chunks; ++c) {
+            int jlo, jhi;
+            if (!chunk_span(a, c * kTUC, &jlo, &jhi)) continue;
+            mbar_wait(&full[stage], phase);
+            const float* G = sg + stage * (kTGBytes / 4) - sjlo[stage] * (kTVG * kTUC);
+            const int2* X = sx + stage * (kTXBytes / 8);
+            float part[4][2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { part[i][0] = 0.f; part[i][1] = 0.f; }
+            const int u0 = c * kTUC;
+#pragma unroll
+            for (int k = 0; k < kTUC; ++k) {
+                const int uu = (k + xl) & (kTUC - 1);
+                if (u0 + uu < a.Wb) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int x = warp * 8 + xl + 64 * i;
+                        if (x < a.Wa) {
+                            const int2 e = X[uu * a.Wa + x];
+                            if (e.x) {
+                                const float t = __int_as_float(e.y);
+                                const float w0 = 1.f - t;
+                                const float* gp = G + (e.x - 1) * (kTVG * kTUC) + uu;
+                                const float g0a = gp[vq * kTUC];
+                                const float g1a = gp[kTVG * kTUC + vq * kTUC];
+                                const float g0b = gp[(vq + 4) * kTUC];
+                                const float g1b = gp[kTVG * kTUC + (vq + 4) * kTUC];
+                                part[i][0] = fmaf(t, g1a, fmaf(w0, g0a, part[i][0]));
+                                part[i][1] = fmaf(t, g1b, fmaf(w0, g0b, part[i][1]));
+                            }
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                acc[i][0] += static_cast<double>(part[i][0]);
+                acc[i][1] += static_cast<double>(part[i][1]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == kTStages) { stage = 0; phase ^= 1; }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int x = warp * 8 + xl + 64 * i;
+            if (x >= a.Wa) continue;
+            double* dst = a.T + (static_cast<int64_t>(x) * a.Ha + m) * a.Hb + v0;
+            if (mask & (1u << vq)) dst[vq] = acc[i][0];
+            if (mask & (1u << (vq + 4))) dst[vq + 4] = acc[i][1];
+        }
+    }
+}
+
+__global__ void pack_xtable_kernel(const int32_t* __restrict__ i0, const double* __restrict__ t, int n,
+                                   int2* __restrict__ out) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx < n) {
+        const int j = i0[idx];
+        out[idx] = make_int2(j + 1, __float_as_int(static_cast<float>(t[idx])));
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_refocus_coords(double alpha, int boundary, int W, int Wb, AxisTables tab,
@@ -206,6 +377,34 @@ cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int H
     }
     dim3 grid((Hb + kVG - 1) / kVG, m_count, (Wa + kS1Threads - 1) / kS1Threads);
     stage1_kernel<<<grid, kS1Threads, smem, st>>>(gamma, ldg, Wa, Ha, Wb, Hb, m_base, xs, ys, T);
+    return cudaGetLastError();
+}
+
+bool stage1_tma_supported(int Wa, int Wb) { return Wa <= 256 && Wa >= 2 && (Wb % 4) == 0; }
+
+cudaError_t launch_pack_xtable(AxisTables xs, int Wa, int Wb, int2* xpack, cudaStream_t st) {
+    const int n = Wa * Wb;
+    pack_xtable_kernel<<<(n + 255) / 256, 256, 0, st>>>(xs.i0, xs.t, n, xpack);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int Wa, int Ha, int Wb, int Hb, int m_base,
+                                      int m_count, AxisTables xs, AxisTables ys, const int2* /*xpack*/,
+                                      double* T, int num_sms, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(stage1_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    S1Args a;
+    a.Wa = Wa; a.Ha = Ha; a.Wb = Wb; a.Hb = Hb; a.m_base = m_base; a.m_count = m_count;
+    a.n_vg = (Hb + kTVG - 1) / kTVG;
+    a.n_chunks = (Wb + kTUC - 1) / kTUC;
+    a.xlo = xs.lo; a.xhi = xs.hi; a.ylo = ys.lo; a.yhi = ys.hi; a.T = T;
+    const int tiles = m_count * a.n_vg;
+    const int grid = tiles < num_sms ? tiles : num_sms;
+    stage1_tma_kernel<<<grid, kTThreads, kTSmem, st>>>(maps->gamma, maps->xtab, a);
     return cudaGetLastError();
 }
 
