@@ -193,11 +193,18 @@ __global__ void stage2_kernel(const double* __restrict__ T, int Wa, int Ha, int 
 // column u' = (k + xl) % 8, so the 32 lanes of a warp hit 32 distinct banks for any
 // j0 (smem row of (j, v) = 8 floats; bank = 8 v + u').
 constexpr int kTVG = 8, kTUC = 8, kTJBox = 32, kTMaxJ = 256, kTStages = 2;
-constexpr int kTGBytes = kTMaxJ * kTVG * kTUC * 4;     // 64 KB per stage
-constexpr int kTXBytes = kTUC * 256 * 8;               // 16 KB per stage
+constexpr int kTRow = kTVG * kTUC;                     // floats per staged j row (64)
+constexpr int kTGFloats = kTMaxJ * kTRow;              // 64 KB per stage
+constexpr int kTXEntries = kTUC * 256;                 // 16 KB per stage
+constexpr int kTMaxChunks = 64;                        // W_b <= 512
 constexpr int kTConsumers = 8;
 constexpr int kTThreads = 32 * (kTConsumers + 1);
-constexpr int kTSmem = kTStages * (kTGBytes + kTXBytes) + 1024 + 128;
+// smem map (bytes): [Gamma stages][x-table stages][zero rows 2 x 64 floats][span table][barriers]
+constexpr int kTOffX = kTStages * kTGFloats * 4;
+constexpr int kTOffZ = kTOffX + kTStages * kTXEntries * 8;
+constexpr int kTOffSpan = kTOffZ + 2 * kTRow * 4;
+constexpr int kTOffBar = kTOffSpan + kTMaxChunks * 8;
+constexpr int kTSmem = kTOffBar + 4 * kTStages * 8 + 64;
 
 struct S1Args {
     int Wa, Ha, Wb, Hb, m_base, m_count, n_vg, n_chunks;
@@ -205,38 +212,25 @@ struct S1Args {
     double* T;
 };
 
-__device__ __forceinline__ bool tile_needed(const S1Args& a, int m, int v0, unsigned* mask) {
+__device__ __forceinline__ unsigned tile_mask(const S1Args& a, int m, int v0) {
     unsigned need = 0;
     const int nv = min(kTVG, a.Hb - v0);
     for (int v = 0; v < nv; ++v) {
         const int lo = __ldg(a.ylo + v0 + v), hi = __ldg(a.yhi + v0 + v);
         if (m >= lo && m <= hi) need |= 1u << v;
     }
-    *mask = need;
-    return need != 0;
+    return need;
 }
 
-__device__ __forceinline__ bool chunk_span(const S1Args& a, int u0, int* jlo, int* jhi) {
-    int lo = INT_MAX, hi = -1;
-    const int nu = min(kTUC, a.Wb - u0);
-    for (int k = 0; k < nu; ++k) {
-        lo = min(lo, __ldg(a.xlo + u0 + k));
-        hi = max(hi, __ldg(a.xhi + u0 + k));
-    }
-    *jlo = lo;
-    *jhi = hi;
-    return hi >= lo;
-}
-
+template <bool kFullX>
 __global__ void __launch_bounds__(kTThreads, 1)
 stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_x, S1Args a) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    float* sg = reinterpret_cast<float*>(smem);
-    int2* sx = reinterpret_cast<int2*>(smem + kTStages * kTGBytes);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTStages * (kTGBytes + kTXBytes));
+    extern __shared__ __align__(1024) uint8_t s1_smem[];
+    float* sg = reinterpret_cast<float*>(s1_smem);
+    const int2* sx = reinterpret_cast<const int2*>(s1_smem + kTOffX);
+    int2* span = reinterpret_cast<int2*>(s1_smem + kTOffSpan);
+    uint64_t* full = reinterpret_cast<uint64_t*>(s1_smem + kTOffBar);
     uint64_t* empty = full + kTStages;
-    int* sjlo = reinterpret_cast<int*>(empty + kTStages);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -245,6 +239,16 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
             mbar_init(&empty[s], kTConsumers);
         }
         fence_mbar_init();
+    }
+    if (threadIdx.x < 2 * kTRow) sg[kTOffZ / 4 + threadIdx.x] = 0.f;
+    // j span [lo, hi] of every u chunk (lo > hi: no output uses the chunk)
+    for (int c = threadIdx.x; c < a.n_chunks; c += blockDim.x) {
+        int lo = INT_MAX, hi = -1;
+        for (int k = 0; k < kTUC && c * kTUC + k < a.Wb; ++k) {
+            lo = min(lo, __ldg(a.xlo + c * kTUC + k));
+            hi = max(hi, __ldg(a.xhi + c * kTUC + k));
+        }
+        span[c] = make_int2(lo, hi);
     }
     __syncthreads();
     const int n_tiles = a.m_count * a.n_vg;
@@ -257,20 +261,18 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
                 const int ml = tile / a.n_vg, vg = tile - ml * a.n_vg;
-                unsigned mask;
-                if (!tile_needed(a, a.m_base + ml, vg * kTVG, &mask)) continue;
+                if (!tile_mask(a, a.m_base + ml, vg * kTVG)) continue;
                 for (int c = 0; c < a.n_chunks; ++c) {
-                    int jlo, jhi;
-                    if (!chunk_span(a, c * kTUC, &jlo, &jhi)) continue;
-                    const int nb = (jhi - jlo + kTJBox) / kTJBox;
+                    const int2 sp = span[c];
+                    if (sp.y < sp.x) continue;
+                    const int nb = (sp.y - sp.x + kTJBox) / kTJBox;
                     mbar_wait(&empty[stage], phase ^ 1);
-                    sjlo[stage] = jlo;
-                    mbar_expect_tx(&full[stage], nb * kTJBox * kTVG * kTUC * 4 + kTUC * a.Wa * 8);
-                    float* dst = sg + stage * (kTGBytes / 4);
+                    mbar_expect_tx(&full[stage], nb * kTJBox * kTRow * 4 + kTUC * a.Wa * 8);
+                    float* dst = sg + stage * kTGFloats;
                     for (int b = 0; b < nb; ++b)
-                        tma_load_4d(dst + b * kTJBox * kTVG * kTUC, &tm_g, &full[stage], c * kTUC, vg * kTVG,
-                                    jlo + b * kTJBox, ml);
-                    tma_load_2d(sx + stage * (kTXBytes / 8), &tm_x, &full[stage], 0, c * kTUC);
+                        tma_load_4d(dst + b * kTJBox * kTRow, &tm_g, &full[stage], c * kTUC, vg * kTVG,
+                                    sp.x + b * kTJBox, ml);
+                    tma_load_2d(s1_smem + kTOffX + stage * kTXEntries * 8, &tm_x, &full[stage], 0, c * kTUC);
                     if (++stage == kTStages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -278,49 +280,48 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
         return;
     }
 
-    // consumers
+    // consumers: thread owns x = 8*warp + xl + 64*i (i < 4), v in {vq, vq + 4}
     const int vq = lane >> 3, xl = lane & 7;
+    const int xbase = warp * 8 + xl;
+    const int zero_idx = kTOffZ / 4 + vq * kTUC;     // float index of the zero rows for (v = vq)
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int ml = tile / a.n_vg, vg = tile - ml * a.n_vg;
         const int m = a.m_base + ml, v0 = vg * kTVG;
-        unsigned mask;
-        if (!tile_needed(a, m, v0, &mask)) continue;
+        const unsigned mask = tile_mask(a, m, v0);
+        if (!mask) continue;
         double acc[4][2];
 #pragma unroll
         for (int i = 0; i < 4; ++i) { acc[i][0] = 0.0; acc[i][1] = 0.0; }
         for (int c = 0; c < a.n_chunks; ++c) {
-            int jlo, jhi;
-            if (!chunk_span(a, c * kTUC, &jlo, &jhi)) continue;
+            const int2 sp = span[c];
+            if (sp.y < sp.x) continue;
             mbar_wait(&full[stage], phase);
-            const float* G = sg + stage * (kTGBytes / 4) - sjlo[stage] * (kTVG * kTUC);
-            const int2* X = sx + stage * (kTXBytes / 8);
+            // float index of (j = 0, v = vq, u = 0) in this stage, rebased by the chunk's j_lo
+            const int gbase = stage * kTGFloats - sp.x * kTRow + vq * kTUC;
+            const int xt = stage * kTXEntries + xbase;
             float part[4][2];
 #pragma unroll
             for (int i = 0; i < 4; ++i) { part[i][0] = 0.f; part[i][1] = 0.f; }
-            const int u0 = c * kTUC;
 #pragma unroll
             for (int k = 0; k < kTUC; ++k) {
                 const int uu = (k + xl) & (kTUC - 1);
-                if (u0 + uu < a.Wb) {
+                const int xrow = xt + uu * a.Wa;
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int x = warp * 8 + xl + 64 * i;
-                        if (x < a.Wa) {
-                            const int2 e = X[uu * a.Wa + x];
-                            if (e.x) {
-                                const float t = __int_as_float(e.y);
-                                const float w0 = 1.f - t;
-                                const float* gp = G + (e.x - 1) * (kTVG * kTUC) + uu;
-                                const float g0a = gp[vq * kTUC];
-                                const float g1a = gp[kTVG * kTUC + vq * kTUC];
-                                const float g0b = gp[(vq + 4) * kTUC];
-                                const float g1b = gp[kTVG * kTUC + (vq + 4) * kTUC];
-                                part[i][0] = fmaf(t, g1a, fmaf(w0, g0a, part[i][0]));
-                                part[i][1] = fmaf(t, g1b, fmaf(w0, g0b, part[i][1]));
-                            }
-                        }
+                for (int i = 0; i < 4; ++i) {
+                    if (kFullX || xbase + 64 * i < a.Wa) {
+                        const int2 e = sx[xrow + 64 * i];
+                        const float t = __int_as_float(e.y);
+                        const float w0 = 1.f - t;
+                        // skipped samples (e.x == 0, t == 0) read the two zero rows
+                        const int gi = (e.x ? gbase + (e.x - 1) * kTRow : zero_idx) + uu;
+                        const float g0a = sg[gi];
+                        const float g1a = sg[gi + kTRow];
+                        const float g0b = sg[gi + 4 * kTUC];
+                        const float g1b = sg[gi + kTRow + 4 * kTUC];
+                        part[i][0] = fmaf(t, g1a, fmaf(w0, g0a, part[i][0]));
+                        part[i][1] = fmaf(t, g1b, fmaf(w0, g0b, part[i][1]));
                     }
                 }
             }
@@ -335,8 +336,8 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const int x = warp * 8 + xl + 64 * i;
-            if (x >= a.Wa) continue;
+            const int x = xbase + 64 * i;
+            if (!kFullX && x >= a.Wa) continue;
             double* dst = a.T + (static_cast<int64_t>(x) * a.Ha + m) * a.Hb + v0;
             if (mask & (1u << vq)) dst[vq] = acc[i][0];
             if (mask & (1u << (vq + 4))) dst[vq + 4] = acc[i][1];
@@ -380,7 +381,7 @@ cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int H
     return cudaGetLastError();
 }
 
-bool stage1_tma_supported(int Wa, int Wb) { return Wa <= 256 && Wa >= 2 && (Wb % 4) == 0; }
+bool stage1_tma_supported(int Wa, int Wb) { return Wa <= 256 && Wa >= 2 && (Wb % 4) == 0 && Wb <= 8 * kTMaxChunks; }
 
 cudaError_t launch_pack_xtable(AxisTables xs, int Wa, int Wb, int2* xpack, cudaStream_t st) {
     const int n = Wa * Wb;
@@ -393,7 +394,9 @@ cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int Wa, int Ha, in
                                       double* T, int num_sms, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(stage1_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem);
+        cudaError_t e = cudaFuncSetAttribute(stage1_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(stage1_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
@@ -404,7 +407,10 @@ cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int Wa, int Ha, in
     a.xlo = xs.lo; a.xhi = xs.hi; a.ylo = ys.lo; a.yhi = ys.hi; a.T = T;
     const int tiles = m_count * a.n_vg;
     const int grid = tiles < num_sms ? tiles : num_sms;
-    stage1_tma_kernel<<<grid, kTThreads, kTSmem, st>>>(maps->gamma, maps->xtab, a);
+    if (Wa == 256)
+        stage1_tma_kernel<true><<<grid, kTThreads, kTSmem, st>>>(maps->gamma, maps->xtab, a);
+    else
+        stage1_tma_kernel<false><<<grid, kTThreads, kTSmem, st>>>(maps->gamma, maps->xtab, a);
     return cudaGetLastError();
 }
 
