@@ -1,0 +1,88 @@
+"""Full-size parity at BASELINE configs[1] (rho_a = rho_b = 256x256 halves, 10^4 frames) in
+the launch configuration bench.py times (fused Gamma epilogue, no kept counts), then the
+configs[3] 64-plane stack from that Gamma.
+
+The oracle cannot compute 2^32 x 10^4 pair-frames, so:
+  * Gamma: 16 sampled A rows (tile edges included) x all 65,536 B pixels vs the oracle;
+  * S_ab (kept-counts run): the same rows bit-exact, plus exact closed forms over the whole
+    matrix: row sums = A^T n_B, column sums = B^T n_A, total = n_A . n_B;
+  * S_a, S_b: bit-exact in full;
+  * planes: 3 planes x 24 sampled output pixels vs the oracle on the GPU's own fp32 Gamma
+    (stage-isolated), tolerance 1e-6 M per output.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+ROWS = np.array([0, 1, 127, 128, 255, 256, 4095, 20000, 32767, 32768, 40961, 50000, 65279, 65280, 65534, 65535])
+
+
+@pytest.fixture(scope="module")
+def frames():
+    return synth.bernoulli_frames(10_000, 0.05, seed=synth.SEED_ARMS)
+
+
+@pytest.fixture(scope="module")
+def oracle_rows(frames):
+    return oracle.correlate(frames, synth.ROI_FULL_A, synth.ROI_FULL_B, rows=ROWS, threads=0)
+
+
+def _popc_halves(frames):
+    popc = np.array([bin(b).count("1") for b in range(256)], dtype=np.int64)
+    return popc[frames[:, :, 0:32]].sum(axis=(1, 2)), popc[frames[:, :, 32:64]].sum(axis=(1, 2))
+
+
+def test_fullsize_gamma_bench_configuration(frames, oracle_rows):
+    from paper_2407_20692_b200 import Context
+    ctx = Context(synth.ROI_FULL_A, synth.ROI_FULL_B, 10_000)       # bench: no kept counts
+    ctx.load_frames(torch.from_numpy(frames).cuda())
+    g = ctx.correlate(ctx.new_gamma())
+    got = g[torch.from_numpy(ROWS).cuda()].cpu().numpy().astype(np.float64)
+    want = oracle_rows["gamma"]
+    zero = want == 0
+    assert np.all(got[zero] == 0)
+    rel = np.abs(got - want) / np.where(zero, 1, np.abs(want))
+    assert rel.max() <= 1e-6, rel.max()
+    # configs[3]: the 64-plane stack from this Gamma, sampled pixels of 3 planes
+    alphas = synth.alpha_grid(64)
+    planes = ctx.new_planes(64)
+    ctx.refocus(alphas, g, planes)
+    torch.cuda.synchronize()
+    sel = [0, 21, 63]                     # alpha = 0.5, 1.0, 2.0
+    rng = np.random.default_rng(3)
+    pix = np.stack([rng.integers(0, 256, 24), rng.integers(0, 256, 24)], 1)
+    pix[:4] = [[0, 0], [255, 255], [0, 255], [128, 127]]
+    G = g.cpu().numpy()
+    del g
+    R = oracle.refocus(G, (256, 256, 256, 256), alphas[sel], pixels=pix)
+    M = oracle.refocus(np.abs(G), (256, 256, 256, 256), alphas[sel], pixels=pix)
+    P = planes.cpu().numpy().astype(np.float64)
+    got_p = np.stack([P[s][pix[:, 1], pix[:, 0]] for s in sel])
+    assert np.all(np.abs(got_p - R) <= 1e-6 * M + 1e-30), np.max(np.abs(got_p - R) / np.maximum(M, 1e-300))
+
+
+def test_fullsize_counts_exact(frames, oracle_rows):
+    from paper_2407_20692_b200 import Context
+    ctx = Context(synth.ROI_FULL_A, synth.ROI_FULL_B, 10_000, keep_counts=True)
+    ctx.load_frames(frames)
+    ctx.correlate(None)
+    s_ab = torch.empty((65536, 65536), dtype=torch.int32, device="cuda")
+    s_a = torch.empty(65536, dtype=torch.int32, device="cuda")
+    s_b = torch.empty(65536, dtype=torch.int32, device="cuda")
+    assert ctx.get_counts(s_ab, s_a, s_b) == 10_000
+    np.testing.assert_array_equal(s_ab[torch.from_numpy(ROWS).cuda()].cpu().numpy(), oracle_rows["s_ab"])
+    np.testing.assert_array_equal(s_a.cpu().numpy(), oracle_rows["s_a"])
+    np.testing.assert_array_equal(s_b.cpu().numpy(), oracle_rows["s_b"])
+    n_a, n_b = _popc_halves(frames)
+    A = np.unpackbits(frames[:, :, 0:32], axis=-1, bitorder="little").reshape(10_000, -1)
+    B = np.unpackbits(frames[:, :, 32:64], axis=-1, bitorder="little").reshape(10_000, -1)
+    row = s_ab.sum(dim=1, dtype=torch.int64).cpu().numpy()
+    col = s_ab.sum(dim=0, dtype=torch.int64).cpu().numpy()
+    np.testing.assert_array_equal(row, A.T.astype(np.int64) @ n_b)
+    np.testing.assert_array_equal(col, B.T.astype(np.int64) @ n_a)
+    assert int(row.sum()) == int(n_a @ n_b)
