@@ -55,7 +55,7 @@ struct cpi_ctx {
     // refocus workspaces
     cpi::AxisTables xs{}, ys{};
     double* T = nullptr;
-    int2* xpack = nullptr;                 // packed x-table for the TMA stage 1
+    uint32_t* xpack = nullptr;             // packed x-table for the TMA stage 1
     cpi::Stage1Maps s1maps{};
     bool use_s1_tma = false;
     // accounting
@@ -491,14 +491,14 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
         CK(c, cudaMalloc(&c->T, sizeof(double) * size_t(Wa) * Ha * Hb));
         c->use_s1_tma = cpi::stage1_tma_supported(Wa, Wb) && getenv("CPI_STAGE1_SIMPLE") == nullptr;
         if (c->use_s1_tma) {
-            CK(c, cudaMalloc(&c->xpack, sizeof(int2) * size_t(Wa) * Wb));
+            CK(c, cudaMalloc(&c->xpack, sizeof(uint32_t) * size_t(Wa) * Wb));
             cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
             if (!enc) return fail(c, CPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
             const cuuint64_t dims[2] = {cuuint64_t(Wa), cuuint64_t(Wb)};
-            const cuuint64_t strides[1] = {cuuint64_t(Wa) * 8};
+            const cuuint64_t strides[1] = {cuuint64_t(Wa) * 4};
             const cuuint32_t box[2] = {cuuint32_t(Wa), 8u};
             const cuuint32_t es[2] = {1u, 1u};
-            CUresult r = enc(&c->s1maps.xtab, CU_TENSOR_MAP_DATA_TYPE_INT64, 2, c->xpack, dims, strides, box, es,
+            CUresult r = enc(&c->s1maps.xtab, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, c->xpack, dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) return fail(c, CPI_ERR_CUDA, "x-table tensor map failed (%d)", int(r));
@@ -511,9 +511,16 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
         const cuuint64_t strides[3] = {cuuint64_t(Wb) * 4, cuuint64_t(c->p_b) * 4, cuuint64_t(Wa) * c->p_b * 4};
         const cuuint32_t box[4] = {8u, 8u, 32u, 1u};
         const cuuint32_t es[4] = {1u, 1u, 1u, 1u};
+        // L2 sector promotion of the Gamma stream (tuning knob CPI_S1_L2PROMO = 0/64/128/256)
+        CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+        if (const char* ev = getenv("CPI_S1_L2PROMO")) {
+            const int v = atoi(ev);
+            promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                  : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+        }
         CUresult r = enc(&c->s1maps.gamma, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(spec->gamma_dev),
                          dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                         promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(c, CPI_ERR_CUDA, "Gamma tensor map failed (%d)", int(r));
     }
     const int m_base = static_cast<int>(spec->row0 / Wa), m_count = static_cast<int>(spec->rows / Wa);

@@ -73,9 +73,9 @@ struct Stage1Maps {
 bool stage1_tma_supported(int Wa, int Wb);
 cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int Wa, int Ha, int Wb, int Hb,
                                       int m_base, int m_count, AxisTables xs, AxisTables ys,
-                                      const int2* xpack, double* T, int num_sms, cudaStream_t st);
-// x-table packed for the TMA stage 1: int2 {j0 + 1 (0 = skipped), float bits of t}, [Wb][Wa].
-cudaError_t launch_pack_xtable(AxisTables xs, int Wa, int Wb, int2* xpack, cudaStream_t st);
+                                      const uint32_t* xpack, double* T, int num_sms, cudaStream_t st);
+// x-table packed for the TMA stage 1: uint32 (j0 + 1) << 24 | round(t * 2^23), 0 = skipped, [Wb][Wa].
+cudaError_t launch_pack_xtable(AxisTables xs, int Wa, int Wb, uint32_t* xpack, cudaStream_t st);
 // driver entry point cuTensorMapEncodeTiled (nullptr if unavailable)
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,

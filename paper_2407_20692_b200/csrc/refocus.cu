@@ -192,16 +192,16 @@ __global__ void stage2_kernel(const double* __restrict__ T, int Wa, int Ha, int 
 // thread owns x = 8*warp + xl + 64*i (i < 4) and v in {vq, vq+4}.  At step k a lane reads
 // column u' = (k + xl) % 8, so the 32 lanes of a warp hit 32 distinct banks for any
 // j0 (smem row of (j, v) = 8 floats; bank = 8 v + u').
-constexpr int kTVG = 8, kTUC = 8, kTJBox = 32, kTMaxJ = 256, kTStages = 2;
+constexpr int kTVG = 8, kTUC = 8, kTJBox = 32, kTMaxJ = 256, kTStages = 3;
 constexpr int kTRow = kTVG * kTUC;                     // floats per staged j row (64)
 constexpr int kTGFloats = kTMaxJ * kTRow;              // 64 KB per stage
-constexpr int kTXEntries = kTUC * 256;                 // 16 KB per stage
+constexpr int kTXEntries = kTUC * 256;                 // 8 KB per stage (uint32 entries)
 constexpr int kTMaxChunks = 64;                        // W_b <= 512
 constexpr int kTConsumers = 8;
 constexpr int kTThreads = 32 * (kTConsumers + 1);
 // smem map (bytes): [Gamma stages][x-table stages][zero rows 2 x 64 floats][span table][barriers]
 constexpr int kTOffX = kTStages * kTGFloats * 4;
-constexpr int kTOffZ = kTOffX + kTStages * kTXEntries * 8;
+constexpr int kTOffZ = kTOffX + kTStages * kTXEntries * 4;
 constexpr int kTOffSpan = kTOffZ + 2 * kTRow * 4;
 constexpr int kTOffBar = kTOffSpan + kTMaxChunks * 8;
 constexpr int kTSmem = kTOffBar + 4 * kTStages * 8 + 64;
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kTThreads, 1)
 stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_x, S1Args a) {
     extern __shared__ __align__(1024) uint8_t s1_smem[];
     float* sg = reinterpret_cast<float*>(s1_smem);
-    const int2* sx = reinterpret_cast<const int2*>(s1_smem + kTOffX);
+    const uint32_t* sx = reinterpret_cast<const uint32_t*>(s1_smem + kTOffX);
     int2* span = reinterpret_cast<int2*>(s1_smem + kTOffSpan);
     uint64_t* full = reinterpret_cast<uint64_t*>(s1_smem + kTOffBar);
     uint64_t* empty = full + kTStages;
@@ -267,12 +267,12 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                     if (sp.y < sp.x) continue;
                     const int nb = (sp.y - sp.x + kTJBox) / kTJBox;
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], nb * kTJBox * kTRow * 4 + kTUC * a.Wa * 8);
+                    mbar_expect_tx(&full[stage], nb * kTJBox * kTRow * 4 + kTUC * a.Wa * 4);
                     float* dst = sg + stage * kTGFloats;
                     for (int b = 0; b < nb; ++b)
                         tma_load_4d(dst + b * kTJBox * kTRow, &tm_g, &full[stage], c * kTUC, vg * kTVG,
                                     sp.x + b * kTJBox, ml);
-                    tma_load_2d(s1_smem + kTOffX + stage * kTXEntries * 8, &tm_x, &full[stage], 0, c * kTUC);
+                    tma_load_2d(s1_smem + kTOffX + stage * kTXEntries * 4, &tm_x, &full[stage], 0, c * kTUC);
                     if (++stage == kTStages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -311,11 +311,13 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     if (kFullX || xbase + 64 * i < a.Wa) {
-                        const int2 e = sx[xrow + 64 * i];
-                        const float t = __int_as_float(e.y);
+                        // entry = (j0 + 1) << 24 | round(t * 2^23); 0 = skipped sample
+                        const uint32_t e = sx[xrow + 64 * i];
+                        const int jp1 = static_cast<int>(e >> 24);
+                        const float t = __int_as_float(0x3F800000 + static_cast<int>(e & 0xFFFFFFu)) - 1.f;
                         const float w0 = 1.f - t;
-                        // skipped samples (e.x == 0, t == 0) read the two zero rows
-                        const int gi = (e.x ? gbase + (e.x - 1) * kTRow : zero_idx) + uu;
+                        // skipped samples (t == 0) read the two zero rows
+                        const int gi = (jp1 ? gbase + (jp1 - 1) * kTRow : zero_idx) + uu;
                         const float g0a = sg[gi];
                         const float g1a = sg[gi + kTRow];
                         const float g0b = sg[gi + 4 * kTUC];
@@ -345,12 +347,15 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
     }
 }
 
+// Packed x-table for the TMA stage 1 (W_a <= 256): (j0 + 1) << 24 | round(t * 2^23), 0 for a
+// skipped sample.  t in [0, 1] keeps 2^-23 resolution; t = 0 and t = 1 stay exact.
 __global__ void pack_xtable_kernel(const int32_t* __restrict__ i0, const double* __restrict__ t, int n,
-                                   int2* __restrict__ out) {
+                                   uint32_t* __restrict__ out) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx < n) {
         const int j = i0[idx];
-        out[idx] = make_int2(j + 1, __float_as_int(static_cast<float>(t[idx])));
+        const uint32_t tq = static_cast<uint32_t>(__double2uint_rn(t[idx] * 8388608.0));
+        out[idx] = j < 0 ? 0u : ((static_cast<uint32_t>(j + 1) << 24) | tq);
     }
 }
 
@@ -383,14 +388,14 @@ cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int H
 
 bool stage1_tma_supported(int Wa, int Wb) { return Wa <= 256 && Wa >= 2 && (Wb % 4) == 0 && Wb <= 8 * kTMaxChunks; }
 
-cudaError_t launch_pack_xtable(AxisTables xs, int Wa, int Wb, int2* xpack, cudaStream_t st) {
+cudaError_t launch_pack_xtable(AxisTables xs, int Wa, int Wb, uint32_t* xpack, cudaStream_t st) {
     const int n = Wa * Wb;
     pack_xtable_kernel<<<(n + 255) / 256, 256, 0, st>>>(xs.i0, xs.t, n, xpack);
     return cudaGetLastError();
 }
 
 cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int Wa, int Ha, int Wb, int Hb, int m_base,
-                                      int m_count, AxisTables xs, AxisTables ys, const int2* /*xpack*/,
+                                      int m_count, AxisTables xs, AxisTables ys, const uint32_t* /*xpack*/,
                                       double* T, int num_sms, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
