@@ -33,7 +33,7 @@ struct cpi_ctx {
     cpi_config cfg{};
     int dev = 0;
     int num_sms = 148;
-    bool popc = false, keep = false;
+    bool popc = false, keep = false, pair = true;   // pair: cta_group::2 GEMM
     int64_t p_a = 0, p_b = 0;
     int64_t rows_a = 0, rows_b = 0;        // padded operand rows
     int64_t k_cap = 0;                     // frames capacity rounded to 128
@@ -268,8 +268,9 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
         c->rows_b = round_up(c->p_b, cpi::gemm_popc_block());
         c->ld_op = c->k_cap / 32;   // 32-bit words
     } else {
-        c->rows_a = round_up(c->p_a, cpi::gemm_tc_block_m());
-        c->rows_b = round_up(c->p_b, cpi::gemm_tc_block_n());
+        c->pair = getenv("CPI_GEMM_1CTA") == nullptr;
+        c->rows_a = round_up(c->p_a, c->pair ? cpi::gemm_tc2_block_m() : cpi::gemm_tc_block_m());
+        c->rows_b = round_up(c->p_b, c->pair ? cpi::gemm_tc2_block_n() : cpi::gemm_tc_block_n());
         c->ld_op = c->k_cap;        // bytes
     }
     const size_t op_elem = c->popc ? 4 : 1;
@@ -294,8 +295,10 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
         return s;
     }
     if (!c->popc) {
-        cpi_status s = make_tmap(c, &c->tm_a, c->op_a, c->rows_a, c->ld_op, cpi::gemm_tc_block_m());
-        if (s == CPI_OK) s = make_tmap(c, &c->tm_b, c->op_b, c->rows_b, c->ld_op, cpi::gemm_tc_block_n());
+        const uint32_t box_a = c->pair ? cpi::gemm_tc2_box_rows() : cpi::gemm_tc_block_m();
+        const uint32_t box_b = c->pair ? cpi::gemm_tc2_box_rows() : cpi::gemm_tc_block_n();
+        cpi_status s = make_tmap(c, &c->tm_a, c->op_a, c->rows_a, c->ld_op, box_a);
+        if (s == CPI_OK) s = make_tmap(c, &c->tm_b, c->op_b, c->rows_b, c->ld_op, box_b);
         if (s != CPI_OK) {
             g_create_error = c->err;
             free_all(c);
@@ -382,6 +385,10 @@ cpi_status cpi_correlate(cpi_ctx* c, float* gamma, void* stream) {
         if (c->popc)
             e = cpi::launch_gemm_popc(static_cast<const uint32_t*>(c->op_a), static_cast<const uint32_t*>(c->op_b),
                                       c->ld_op, k_pad / 32, epi, st);
+        else if (c->pair)
+            e = cpi::launch_gemm_tc2(&c->tm_a, &c->tm_b, static_cast<int>(c->rows_a / cpi::gemm_tc2_block_m()),
+                                     static_cast<int>(c->rows_b / cpi::gemm_tc2_block_n()),
+                                     static_cast<int>(k_pad / kKAlign), epi, c->num_sms, st);
         else
             e = cpi::launch_gemm_tc(&c->tm_a, &c->tm_b, static_cast<int>(c->rows_a / cpi::gemm_tc_block_m()),
                                     static_cast<int>(c->rows_b / cpi::gemm_tc_block_n()),

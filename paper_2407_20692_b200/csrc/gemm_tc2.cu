@@ -1,0 +1,232 @@
+// gemm_tc2.cu — KB2 (CTA-pair variant): S_ab = A^T B of Eq. (1) on
+// tcgen05 tensor cores with two SMs per MMA (cta_group::2), fused exact normalisation
+// (P:100-111).
+//
+// A pair of CTAs (cluster of 2) owns a 256 x 256 output tile.  Each CTA TMA-loads its own
+// 128-row half of the A panel and its own 128-row half of the B panel (128 B of K each) into
+// a 6-stage ring; the transaction bytes of both halves are counted on the leader CTA's
+// barrier.  The leader's single MMA thread issues tcgen05.mma.cta_group::2.kind::i8 with
+// M = 256, N = 256, K = 32: the tensor cores of both SMs read A rows from their own smem and
+// the two B halves from both, and each CTA's TMEM receives its 128 rows x 256 columns.
+// Commits are multicast to both CTAs (smem slots free, accumulator full); both CTAs'
+// epilogue warps release an accumulator on the leader's barrier.  Per SM this halves the
+// B-panel L2->SMEM traffic of the 1-CTA kernel (32 KB instead of 48 KB per 512 MMA
+// cycles) and leaves room for 6 stages.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cpi {
+namespace {
+
+constexpr int BM = 256, BN = 256, BK = 128;       // pair tile; BK in bytes
+constexpr int HM = BM / 2, HN = BN / 2;           // per-CTA halves
+constexpr int kStages = 6;
+constexpr int kABytes = HM * BK;                  // 16 KB
+constexpr int kBBytes = HN * BK;                  // 16 KB
+constexpr int kStageBytes = kABytes + kBBytes;    // per CTA
+constexpr int kThreads = 192;
+constexpr int kTmemCols = 512;                    // 2 accumulators x 256 columns
+constexpr int kGroupM = 8;                        // pair-tile rows per raster group
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+
+__device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int& tm, int& tn) {
+    const int group = kGroupM * n_tiles;
+    const int g = t / group;
+    const int first_m = g * kGroupM;
+    const int gm = min(m_tiles - first_m, kGroupM);
+    const int r = t - g * group;
+    tm = first_m + r % gm;
+    tn = r / gm;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                   int m_tiles, int n_tiles, int k_blocks, Epilogue epi) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kStages * kABytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBBytes);
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tma_a);
+        tma_prefetch_desc(&tma_b);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);      // leader: one arrive.expect_tx per stage
+            mbar_init(&empty[s], 1);     // one multicast commit per stage
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);     // one multicast commit per tile
+            mbar_init(&tempty[a], 8);    // 4 epilogue warps x 2 CTAs (leader's copy is used)
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc_2sm(tmem_slot, kTmemCols);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int num_tiles = m_tiles * n_tiles;
+    const int pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = pair; t < num_tiles; t += num_pairs) {
+                int tm, tn;
+                tile_coords(t, m_tiles, n_tiles, tm, tn);
+                for (int kb = 0; kb < k_blocks; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (leader) mbar_expect_tx(&full[stage], 2 * kStageBytes);
+                    tma_load_2d_2sm(sA + stage * kABytes, &tma_a, &full[stage], kb * BK, tm * BM + rank * HM);
+                    tma_load_2d_2sm(sB + stage * kBBytes, &tma_b, &full[stage], kb * BK, tn * BN + rank * HN);
+                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            constexpr uint32_t idesc = idesc_u8_s32(BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int local = 0;
+            for (int t = pair; t < num_tiles; t += num_pairs, ++local) {
+                const int acc = local & 1;
+                const uint32_t acc_phase = (local >> 1) & 1;
+                mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = 0; kb < k_blocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + stage * kABytes);
+                    const uint32_t b0 = smem_u32(sB + stage * kBBytes);
+#pragma unroll
+                    for (int k = 0; k < BK / 32; ++k)
+                        mma_i8_2sm(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), idesc,
+                                   (kb | k) != 0);
+                    mma_commit_2sm(&empty[stage]);
+                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                }
+                mma_commit_2sm(&tfull[acc]);
+            }
+        }
+    } else {
+        // epilogue warps 2..5 of both CTAs -> TMEM lane quadrant (warp % 4) of this CTA
+        const int q = warp & 3;
+        const double n = epi.n, inv_n2 = epi.inv_n2;
+        const uint32_t tempty_leader0 = leader_addr(&tempty[0]), tempty_leader1 = leader_addr(&tempty[1]);
+        int local = 0;
+        for (int t = pair; t < num_tiles; t += num_pairs, ++local) {
+            int tm, tn;
+            tile_coords(t, m_tiles, n_tiles, tm, tn);
+            const int acc = local & 1;
+            const uint32_t acc_phase = (local >> 1) & 1;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int row = tm * BM + rank * HM + 32 * q + lane;
+            const bool row_ok = row < epi.p_a;
+            const double sa = row_ok ? static_cast<double>(__ldg(epi.s_a + row)) : 0.0;
+            const uint32_t taddr = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(taddr + 32 * c, r);
+                tmem_wait_ld();
+                const int col0 = tn * BN + 32 * c;
+                if (row_ok && col0 < epi.p_b) {
+                    const bool full_chunk = epi.vec && col0 + 32 <= epi.p_b;
+                    if (epi.counts) {
+                        int32_t* cp = epi.counts + static_cast<int64_t>(row) * epi.ldc + col0;
+                        if (full_chunk) {
+#pragma unroll
+                            for (int e = 0; e < 32; e += 4) {
+                                int4 v = make_int4(int(r[e]), int(r[e + 1]), int(r[e + 2]), int(r[e + 3]));
+                                if (epi.accumulate) {
+                                    const int4 o = *reinterpret_cast<const int4*>(cp + e);
+                                    v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+                                    r[e] = v.x; r[e + 1] = v.y; r[e + 2] = v.z; r[e + 3] = v.w;
+                                }
+                                *reinterpret_cast<int4*>(cp + e) = v;
+                            }
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 32; ++e) {
+                                if (col0 + e < epi.p_b) {
+                                    const int v = int(r[e]) + (epi.accumulate ? cp[e] : 0);
+                                    r[e] = v;
+                                    cp[e] = v;
+                                }
+                            }
+                        }
+                    }
+                    if (epi.gamma) {
+                        float* gp = epi.gamma + static_cast<int64_t>(row) * epi.ldg + col0;
+                        const int32_t* sbp = epi.s_b + col0;
+                        if (full_chunk) {
+#pragma unroll
+                            for (int e = 0; e < 32; e += 4) {
+                                const int4 sb = __ldg(reinterpret_cast<const int4*>(sbp + e));
+                                float4 g;
+                                g.x = gamma_entry(int(r[e + 0]), sa, double(sb.x), n, inv_n2);
+                                g.y = gamma_entry(int(r[e + 1]), sa, double(sb.y), n, inv_n2);
+                                g.z = gamma_entry(int(r[e + 2]), sa, double(sb.z), n, inv_n2);
+                                g.w = gamma_entry(int(r[e + 3]), sa, double(sb.w), n, inv_n2);
+                                *reinterpret_cast<float4*>(gp + e) = g;
+                            }
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 32; ++e)
+                                if (col0 + e < epi.p_b)
+                                    gp[e] = gamma_entry(int(r[e]), sa, double(__ldg(sbp + e)), n, inv_n2);
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+        }
+    }
+    __syncwarp();
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_2sm(tmem_base, kTmemCols);
+    }
+}
+
+}  // namespace
+
+int gemm_tc2_block_m() { return BM; }
+int gemm_tc2_block_n() { return BN; }
+int gemm_tc2_box_rows() { return HM; }
+
+cudaError_t launch_gemm_tc2(const CUtensorMap* tma_a, const CUtensorMap* tma_b, int m_tiles,
+                            int n_tiles, int k_blocks, const Epilogue& epi, int num_sms,
+                            cudaStream_t st) {
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_i8_tc2_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    const int tiles = m_tiles * n_tiles;
+    int pairs = num_sms / 2;
+    if (tiles < pairs) pairs = tiles;
+    gemm_i8_tc2_kernel<<<2 * pairs, kThreads, kSmemBytes, st>>>(*tma_a, *tma_b, m_tiles, n_tiles,
+                                                                 k_blocks, epi);
+    return cudaGetLastError();
+}
+
+}  // namespace cpi

@@ -39,6 +39,14 @@ cudaError_t launch_gemm_tc(const CUtensorMap* tma_a, const CUtensorMap* tma_b, i
                            cudaStream_t st);
 int gemm_tc_block_m();
 int gemm_tc_block_n();
+// KB2 CTA-pair variant (cta_group::2, M = N = 256 per pair, 6 stages).  Operand maps with
+// 128-row boxes for both A and B; M_pad and N_pad multiples of 256.
+cudaError_t launch_gemm_tc2(const CUtensorMap* tma_a, const CUtensorMap* tma_b, int m_tiles,
+                            int n_tiles, int k_blocks, const Epilogue& epi, int num_sms,
+                            cudaStream_t st);
+int gemm_tc2_block_m();
+int gemm_tc2_block_n();
+int gemm_tc2_box_rows();
 
 // KB3: popcount(AND) GEMM on CUDA cores over 32-bit bit streams [rows][ldw].
 cudaError_t launch_gemm_popc(const uint32_t* a, const uint32_t* b, int64_t ldw, int64_t kw,
