@@ -218,12 +218,93 @@ __host__ __device__ constexpr uint32_t idesc_u8_s32(int M, int N) {
            | (static_cast<uint32_t>(M >> 4) << 24);    // M / 16
 }
 
-// Exact Eq. (1) normalisation of one entry: numerator N*s - sa*sb formed from
-// exact fp64 products of integers (< 2^53), one multiply by 1/N^2, one rounding to fp32.
-__device__ __forceinline__ float gamma_entry(int32_t s, double sa, double sb, double n,
-                                             double inv_n2) {
-    const double num = __fma_rn(static_cast<double>(s), n, -__dmul_rn(sa, sb));
-    return __double2float_rn(__dmul_rn(num, inv_n2));
+// Exact Eq. (1) normalisation of one entry.  The numerator N*s - sa*sb is an
+// exact integer; it is formed
+//   * in int32 when N <= 46340 (|N*s - sa*sb| <= N^2 < 2^31), converted once to fp32 and
+//     multiplied by fp32(1/N^2): three roundings, <= 1.8e-7 relative;
+//   * otherwise from exact fp64 products (all terms < 2^53), one fp64 multiply by 1/N^2 and
+//     one rounding to fp32: <= 6e-8 relative.
+// An exact zero numerator gives +0 on both paths.
+struct GammaScale {
+    int small;          // N <= 46340: int32 path
+    int32_t n_i;        // N
+    float inv_n2_f;     // fp32(1 / N^2)
+    double n_d;         // N
+    double inv_n2_d;    // fp64(1 / N^2)
+};
+constexpr int32_t kGammaInt32MaxN = 46340;
+
+__host__ __device__ inline GammaScale make_gamma_scale(double n) {
+    GammaScale g;
+    g.small = n <= kGammaInt32MaxN ? 1 : 0;
+    g.n_i = g.small ? static_cast<int32_t>(n) : 0;
+    g.n_d = n;
+    g.inv_n2_d = 1.0 / (n * n);
+    g.inv_n2_f = static_cast<float>(g.inv_n2_d);
+    return g;
+}
+template <bool kSmall>
+__device__ __forceinline__ float gamma_entry_t(int32_t s, int32_t sa, int32_t sb, const GammaScale& g) {
+    if constexpr (kSmall) {
+        const int32_t num = g.n_i * s - sa * sb;
+        return __fmul_rn(__int2float_rn(num), g.inv_n2_f);
+    } else {
+        const double num = __fma_rn(static_cast<double>(s), g.n_d,
+                                    -__dmul_rn(static_cast<double>(sa), static_cast<double>(sb)));
+        return __double2float_rn(__dmul_rn(num, g.inv_n2_d));
+    }
+}
+__device__ __forceinline__ float gamma_entry(int32_t s, int32_t sa, int32_t sb, const GammaScale& g) {
+    return g.small ? gamma_entry_t<true>(s, sa, sb, g) : gamma_entry_t<false>(s, sa, sb, g);
+}
+
+// Epilogue of one 32-column chunk of one accumulator row (thread = row): optional int32
+// counts (with accumulation of the previous batches) and Gamma.  r[] holds the TMEM values;
+// sbs points at the chunk's 32 S_b values in shared memory.
+template <bool kSmall>
+__device__ __forceinline__ void epilogue_chunk_vec(uint32_t (&r)[32], int32_t* cp, int accumulate,
+                                                   float* gp, const int32_t* sbs, int32_t sa,
+                                                   const GammaScale& gs) {
+    if (cp) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+            int4 v = make_int4(int(r[e]), int(r[e + 1]), int(r[e + 2]), int(r[e + 3]));
+            if (accumulate) {
+                const int4 o = *reinterpret_cast<const int4*>(cp + e);
+                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+                r[e] = v.x; r[e + 1] = v.y; r[e + 2] = v.z; r[e + 3] = v.w;
+            }
+            *reinterpret_cast<int4*>(cp + e) = v;
+        }
+    }
+    if (gp) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+            const int4 sb = *reinterpret_cast<const int4*>(sbs + e);
+            float4 g;
+            g.x = gamma_entry_t<kSmall>(int(r[e + 0]), sa, sb.x, gs);
+            g.y = gamma_entry_t<kSmall>(int(r[e + 1]), sa, sb.y, gs);
+            g.z = gamma_entry_t<kSmall>(int(r[e + 2]), sa, sb.z, gs);
+            g.w = gamma_entry_t<kSmall>(int(r[e + 3]), sa, sb.w, gs);
+            *reinterpret_cast<float4*>(gp + e) = g;
+        }
+    }
+}
+// Scalar tail version (ragged last chunk or unaligned leading dimension).
+__device__ __forceinline__ void epilogue_chunk_tail(uint32_t (&r)[32], int ncols, int32_t* cp, int accumulate,
+                                                    float* gp, const int32_t* sbs, int32_t sa,
+                                                    const GammaScale& gs) {
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+        if (e < ncols) {
+            int v = int(r[e]);
+            if (cp) {
+                if (accumulate) v += cp[e];
+                cp[e] = v;
+            }
+            if (gp) gp[e] = gamma_entry(v, sa, sbs[e], gs);
+        }
+    }
 }
 
 }  // namespace cpi

@@ -48,7 +48,8 @@ gemm_popc_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
     for (int i = 0; i < 4; ++i) {
         const int64_t row = row0 + ty * 4 + i;
         if (row >= epi.p_a) continue;
-        const double sa = static_cast<double>(epi.s_a[row]);
+        const int32_t sa = epi.s_a[row];
+        const GammaScale gs = make_gamma_scale(epi.n);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int64_t col = col0 + tx * 4 + j;
@@ -61,21 +62,21 @@ gemm_popc_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
             }
             if (epi.gamma)
                 epi.gamma[row * epi.ldg + col] =
-                    gamma_entry(s, sa, static_cast<double>(epi.s_b[col]), epi.n, epi.inv_n2);
+                    gamma_entry(s, sa, epi.s_b[col], gs);
         }
     }
 }
 
 __global__ void finalize_kernel(const int32_t* __restrict__ counts, int64_t ldc, int64_t rows,
                                 int64_t p_b, const int32_t* __restrict__ s_a_rows,
-                                const int32_t* __restrict__ s_b, double n, double inv_n2,
+                                const int32_t* __restrict__ s_b, double n,
                                 float* __restrict__ gamma, int64_t ldg) {
+    const GammaScale gs = make_gamma_scale(n);
     const int64_t total = rows * p_b;
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t r = idx / p_b, q = idx - r * p_b;
-        gamma[r * ldg + q] = gamma_entry(counts[r * ldc + q], static_cast<double>(s_a_rows[r]),
-                                         static_cast<double>(s_b[q]), n, inv_n2);
+        gamma[r * ldg + q] = gamma_entry(counts[r * ldc + q], s_a_rows[r], s_b[q], gs);
     }
 }
 
@@ -98,7 +99,7 @@ cudaError_t launch_finalize(const int32_t* counts, int64_t ldc, int64_t rows, in
     int64_t blocks = (total + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
     finalize_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(counts, ldc, rows, p_b, s_a_rows,
-                                                                   s_b, n, 1.0 / (n * n), gamma, ldg);
+                                                                   s_b, n, gamma, ldg);
     return cudaGetLastError();
 }
 

@@ -22,7 +22,7 @@ struct Epilogue {
     int p_a, p_b;         // valid rows / columns
     int vec;              // 16-byte vector stores allowed (ldg, ldc, p_b multiples of 4)
     double n;             // N_TOT (all batches)
-    double inv_n2;        // 1 / N_TOT^2
+    double inv_n2;        // 1 / N_TOT^2 (kept for reference; kernels use make_gamma_scale(n))
 };
 
 // KB1: expand one RoI of packed frames into a K-major operand (bytes 0/1, or packed

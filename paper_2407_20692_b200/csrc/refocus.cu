@@ -280,10 +280,16 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
         return;
     }
 
-    // consumers: thread owns x = 8*warp + xl + 64*i (i < 4), v in {vq, vq + 4}
-    const int vq = lane >> 3, xl = lane & 7;
-    const int xbase = warp * 8 + xl;
-    const int zero_idx = kTOffZ / 4 + vq * kTUC;     // float index of the zero rows for (v = vq)
+    // consumers: lane = (vq = lane / 16, xl = lane % 16); thread owns x = 16*warp + xl + 128*i
+    // (i < 2) and v = vq + 2*s (s < 4).  At step k the lane reads column u' = (k + xl) % 8 and,
+    // for accumulator slot s, B row v = vq + 2*((s + hi) % 4) with hi = xl / 8, so the 32 lanes
+    // hit 32 distinct banks (bank = 8 v + u') for any j0.
+    const int vq = lane >> 4, xl = lane & 15, hi = xl >> 3;
+    const int xbase = warp * 16 + xl;
+    int voff[4];                                           // float offset of slot s's v row
+#pragma unroll
+    for (int s = 0; s < 4; ++s) voff[s] = (vq + 2 * ((s + hi) & 3)) * kTUC;
+    const int zero_idx = kTOffZ / 4;
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -291,64 +297,68 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
         const int m = a.m_base + ml, v0 = vg * kTVG;
         const unsigned mask = tile_mask(a, m, v0);
         if (!mask) continue;
-        double acc[4][2];
+        double acc[2][4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) { acc[i][0] = 0.0; acc[i][1] = 0.0; }
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int s = 0; s < 4; ++s) acc[i][s] = 0.0;
         for (int c = 0; c < a.n_chunks; ++c) {
             const int2 sp = span[c];
             if (sp.y < sp.x) continue;
             mbar_wait(&full[stage], phase);
-            // float index of (j = 0, v = vq, u = 0) in this stage, rebased by the chunk's j_lo
-            const int gbase = stage * kTGFloats - sp.x * kTRow + vq * kTUC;
+            // float index of (j = 0, v = 0, u = 0) in this stage, rebased by the chunk's j_lo
+            const int gbase = stage * kTGFloats - sp.x * kTRow;
             const int xt = stage * kTXEntries + xbase;
-            float part[4][2];
+            float part[2][4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) { part[i][0] = 0.f; part[i][1] = 0.f; }
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int s = 0; s < 4; ++s) part[i][s] = 0.f;
 #pragma unroll
             for (int k = 0; k < kTUC; ++k) {
                 const int uu = (k + xl) & (kTUC - 1);
                 const int xrow = xt + uu * a.Wa;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    if (kFullX || xbase + 64 * i < a.Wa) {
+                for (int i = 0; i < 2; ++i) {
+                    if (kFullX || xbase + 128 * i < a.Wa) {
                         // entry = (j0 + 1) << 24 | round(t * 2^23); 0 = skipped sample
-                        const uint32_t e = sx[xrow + 64 * i];
+                        const uint32_t e = sx[xrow + 128 * i];
                         const int jp1 = static_cast<int>(e >> 24);
                         const float t = __int_as_float(0x3F800000 + static_cast<int>(e & 0xFFFFFFu)) - 1.f;
                         const float w0 = 1.f - t;
                         // skipped samples (t == 0) read the two zero rows
                         const int gi = (jp1 ? gbase + (jp1 - 1) * kTRow : zero_idx) + uu;
-                        const float g0a = sg[gi];
-                        const float g1a = sg[gi + kTRow];
-                        const float g0b = sg[gi + 4 * kTUC];
-                        const float g1b = sg[gi + kTRow + 4 * kTUC];
-                        part[i][0] = fmaf(t, g1a, fmaf(w0, g0a, part[i][0]));
-                        part[i][1] = fmaf(t, g1b, fmaf(w0, g0b, part[i][1]));
+#pragma unroll
+                        for (int s = 0; s < 4; ++s) {
+                            const float g0 = sg[gi + voff[s]];
+                            const float g1 = sg[gi + voff[s] + kTRow];
+                            part[i][s] = fmaf(t, g1, fmaf(w0, g0, part[i][s]));
+                        }
                     }
                 }
             }
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                acc[i][0] += static_cast<double>(part[i][0]);
-                acc[i][1] += static_cast<double>(part[i][1]);
-            }
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int s = 0; s < 4; ++s) acc[i][s] += static_cast<double>(part[i][s]);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
             if (++stage == kTStages) { stage = 0; phase ^= 1; }
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int x = xbase + 64 * i;
+        for (int i = 0; i < 2; ++i) {
+            const int x = xbase + 128 * i;
             if (!kFullX && x >= a.Wa) continue;
             double* dst = a.T + (static_cast<int64_t>(x) * a.Ha + m) * a.Hb + v0;
-            if (mask & (1u << vq)) dst[vq] = acc[i][0];
-            if (mask & (1u << (vq + 4))) dst[vq + 4] = acc[i][1];
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                const int v = vq + 2 * ((s + hi) & 3);
+                if (mask & (1u << v)) dst[v] = acc[i][s];
+            }
         }
     }
 }
 
-// Packed x-table for the TMA stage 1 (W_a <= 256): (j0 + 1) << 24 | round(t * 2^23), 0 for a
-// skipped sample.  t in [0, 1] keeps 2^-23 resolution; t = 0 and t = 1 stay exact.
 __global__ void pack_xtable_kernel(const int32_t* __restrict__ i0, const double* __restrict__ t, int n,
                                    uint32_t* __restrict__ out) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
