@@ -367,7 +367,7 @@ def main():
     s1_ms, s1_n = kt["stage1"]
     rows_here = p_a if world == 1 else p_a // world
     span = refocus_span_bytes((Wa, Ha, Wb, Hb), alphas) * rows_here / p_a   # per step
-    s1_gbs = span / (s1_ms / (s1_n / args.planes) / 1e3) / 1e9 if s1_n else None
+    s1_gbs = span / (s1_ms / args.steps / 1e3) / 1e9 if s1_n else None
     corr_ms = (kt["expand"][0] + gemm_ms) / args.steps
     ref_ms = (kt["coords"][0] + s1_ms + kt["stage2"][0]) / args.steps
     roof_gemm = {"kernel": "gemm_i8_tc (KB2)" if args.variant == "tc" else "gemm_popc (KB3)",

@@ -5,6 +5,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -53,9 +54,11 @@ struct cpi_ctx {
     float* gamma_current = nullptr;        // Gamma buffer written for the current totals
     CUtensorMap tm_a{}, tm_b{};
     // refocus workspaces
-    cpi::AxisTables xs{}, ys{};
-    double* T = nullptr;
-    uint32_t* xpack = nullptr;             // packed x-table for the TMA stage 1
+    cpi::AxisTables xs[cpi::kRefocusMaxFuse]{}, ys[cpi::kRefocusMaxFuse]{};
+    double* T[cpi::kRefocusMaxFuse]{};
+    bool refocus_ready = false;
+    int fuse = 4;                          // planes per Gamma pass in the TMA stage 1 (CPI_REFOCUS_FUSE)
+    uint32_t* xpack = nullptr;             // packed x-tables [kRefocusMaxFuse][W_b][W_a]
     cpi::Stage1Maps s1maps{};
     bool use_s1_tma = false;
     // accounting
@@ -175,9 +178,11 @@ void free_all(cpi_ctx* c) {
     cudaFree(c->s_a);
     cudaFree(c->s_b);
     cudaFree(c->counts);
-    cudaFree(c->xs.i0); cudaFree(c->xs.t); cudaFree(c->xs.cnt); cudaFree(c->xs.lo); cudaFree(c->xs.hi);
-    cudaFree(c->ys.i0); cudaFree(c->ys.t); cudaFree(c->ys.cnt); cudaFree(c->ys.lo); cudaFree(c->ys.hi);
-    cudaFree(c->T);
+    for (int f = 0; f < cpi::kRefocusMaxFuse; ++f) {
+        cpi::AxisTables* t2[2] = {&c->xs[f], &c->ys[f]};
+        for (auto* t : t2) { cudaFree(t->i0); cudaFree(t->t); cudaFree(t->cnt); cudaFree(t->lo); cudaFree(t->hi); }
+        cudaFree(c->T[f]);
+    }
     cudaFree(c->xpack);
     for (auto& t : c->timed) { c->event_pool.push_back(t.a); c->event_pool.push_back(t.b); }
     for (auto e : c->event_pool) cudaEventDestroy(e);
@@ -491,25 +496,33 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
                     (long long)spec->row0, (long long)spec->rows);
     CK(c, cudaSetDevice(c->dev));
     auto st = static_cast<cudaStream_t>(stream);
-    if (!c->T) {
-        cpi_status s = alloc_axis(c, c->xs, Wa, Wb);
-        if (s == CPI_OK) s = alloc_axis(c, c->ys, Ha, Hb);
-        if (s != CPI_OK) return s;
-        CK(c, cudaMalloc(&c->T, sizeof(double) * size_t(Wa) * Ha * Hb));
+    if (!c->refocus_ready) {
         c->use_s1_tma = cpi::stage1_tma_supported(Wa, Wb) && getenv("CPI_STAGE1_SIMPLE") == nullptr;
+        if (const char* ev = getenv("CPI_REFOCUS_FUSE")) c->fuse = atoi(ev);
+        if (c->fuse < 1) c->fuse = 1;
+        if (c->fuse > cpi::kRefocusMaxFuse) c->fuse = cpi::kRefocusMaxFuse;
+        const int nbuf = c->use_s1_tma ? c->fuse : 1;
+        for (int f = 0; f < nbuf; ++f) {
+            cpi_status s = alloc_axis(c, c->xs[f], Wa, Wb);
+            if (s == CPI_OK) s = alloc_axis(c, c->ys[f], Ha, Hb);
+            if (s != CPI_OK) return s;
+            CK(c, cudaMalloc(&c->T[f], sizeof(double) * size_t(Wa) * Ha * Hb));
+        }
         if (c->use_s1_tma) {
-            CK(c, cudaMalloc(&c->xpack, sizeof(uint32_t) * size_t(Wa) * Wb));
+            CK(c, cudaMalloc(&c->xpack, sizeof(uint32_t) * size_t(Wa) * Wb * cpi::kRefocusMaxFuse));
+            CK(c, cudaMemset(c->xpack, 0, sizeof(uint32_t) * size_t(Wa) * Wb * cpi::kRefocusMaxFuse));
             cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
             if (!enc) return fail(c, CPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
-            const cuuint64_t dims[2] = {cuuint64_t(Wa), cuuint64_t(Wb)};
-            const cuuint64_t strides[1] = {cuuint64_t(Wa) * 4};
-            const cuuint32_t box[2] = {cuuint32_t(Wa), 8u};
-            const cuuint32_t es[2] = {1u, 1u};
-            CUresult r = enc(&c->s1maps.xtab, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, c->xpack, dims, strides, box, es,
+            const cuuint64_t dims[3] = {cuuint64_t(Wa), cuuint64_t(Wb), cuuint64_t(cpi::kRefocusMaxFuse)};
+            const cuuint64_t strides[2] = {cuuint64_t(Wa) * 4, cuuint64_t(Wa) * Wb * 4};
+            const cuuint32_t box[3] = {cuuint32_t(Wa), 8u, 1u};
+            const cuuint32_t es[3] = {1u, 1u, 1u};
+            CUresult r = enc(&c->s1maps.xtab, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, c->xpack, dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) return fail(c, CPI_ERR_CUDA, "x-table tensor map failed (%d)", int(r));
         }
+        c->refocus_ready = true;
     }
     bool tma_now = c->use_s1_tma && (reinterpret_cast<uintptr_t>(spec->gamma_dev) & 15) == 0;
     if (tma_now) {
@@ -531,36 +544,42 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
         if (r != CUDA_SUCCESS) return fail(c, CPI_ERR_CUDA, "Gamma tensor map failed (%d)", int(r));
     }
     const int m_base = static_cast<int>(spec->row0 / Wa), m_count = static_cast<int>(spec->rows / Wa);
-    for (int p = 0; p < spec->n_planes; ++p) {
-        const double alpha = spec->alphas[p];
+    const int group = tma_now ? c->fuse : 1;
+    for (int p0 = 0; p0 < spec->n_planes; p0 += group) {
+        const int nf = std::min(group, spec->n_planes - p0);
         {
             TimedScope ts(c, KC_COORDS, st);
-            cudaError_t e = cpi::launch_refocus_coords(alpha, spec->boundary, Wa, Wb, c->xs, st);
-            if (e == cudaSuccess) e = cpi::launch_refocus_coords(alpha, spec->boundary, Ha, Hb, c->ys, st);
-            c->launches += 2;
+            cudaError_t e = cudaSuccess;
+            for (int f = 0; f < nf && e == cudaSuccess; ++f) {
+                const double alpha = spec->alphas[p0 + f];
+                e = cpi::launch_refocus_coords(alpha, spec->boundary, Wa, Wb, c->xs[f], st);
+                if (e == cudaSuccess) e = cpi::launch_refocus_coords(alpha, spec->boundary, Ha, Hb, c->ys[f], st);
+                if (e == cudaSuccess && tma_now)
+                    e = cpi::launch_pack_xtable(c->xs[f], Wa, Wb, c->xpack + size_t(f) * Wa * Wb, st);
+                c->launches += tma_now ? 3 : 2;
+            }
             if (e != cudaSuccess) return cuda_fail(c, e, "refocus coords launch");
         }
         {
             TimedScope ts(c, KC_STAGE1, st);
             cudaError_t e;
-            if (tma_now) {
-                e = cpi::launch_pack_xtable(c->xs, Wa, Wb, c->xpack, st);
-                if (e == cudaSuccess)
-                    e = cpi::launch_refocus_stage1_tma(&c->s1maps, Wa, Ha, Wb, Hb, m_base, m_count, c->xs, c->ys,
-                                                       c->xpack, c->T, c->num_sms, st);
-                c->launches += 2;
-            } else {
+            if (tma_now)
+                e = cpi::launch_refocus_stage1_tma(&c->s1maps, nf, Wa, Ha, Wb, Hb, m_base, m_count, c->xs, c->ys,
+                                                   c->T, c->num_sms, st);
+            else
                 e = cpi::launch_refocus_stage1(spec->gamma_dev, c->p_b, Wa, Ha, Wb, Hb, m_base, m_count,
-                                               c->xs, c->ys, c->T, st);
-                c->launches += 1;
-            }
+                                               c->xs[0], c->ys[0], c->T[0], st);
+            c->launches += 1;
             if (e != cudaSuccess) return cuda_fail(c, e, "refocus stage-1 launch");
         }
         {
             TimedScope ts(c, KC_STAGE2, st);
-            cudaError_t e = cpi::launch_refocus_stage2(c->T, Wa, Ha, Hb, m_base, m_count, c->xs, c->ys,
-                                                       planes + int64_t(p) * Ha * Wa, st);
-            c->launches += 1;
+            cudaError_t e = cudaSuccess;
+            for (int f = 0; f < nf && e == cudaSuccess; ++f) {
+                e = cpi::launch_refocus_stage2(c->T[f], Wa, Ha, Hb, m_base, m_count, c->xs[f], c->ys[f],
+                                               planes + int64_t(p0 + f) * Ha * Wa, st);
+                c->launches += 1;
+            }
             if (e != cudaSuccess) return cuda_fail(c, e, "refocus stage-2 launch");
         }
     }

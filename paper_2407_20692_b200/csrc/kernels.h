@@ -71,17 +71,18 @@ cudaError_t launch_refocus_coords(double alpha, int boundary, int W, int Wb, Axi
 cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
                                   int m_base, int m_count, AxisTables xs, AxisTables ys,
                                   double* T, cudaStream_t st);
-// KB5 (TMA variant): warp-specialised, persistent, TMA-fed stage 1.  Needs W_a <= 256,
-// W_b % 4 == 0 and the tensor maps of Gamma (4D: u, v, j, m) and of the packed x-table
-// (2D int64: x, u) made by make_stage1_maps.
+// KB5 (TMA variant): warp-specialised, persistent, TMA-fed stage 1 over n_fuse (<= 4) planes
+// sharing one pass over Gamma.  Needs W_a <= 256, W_b % 4 == 0, W_b <= 512, the tensor maps of
+// Gamma (4D: u, v, j, m) and of the packed x-tables (3D uint32: x, u, plane slot).
+constexpr int kRefocusMaxFuse = 4;
 struct Stage1Maps {
     CUtensorMap gamma;
     CUtensorMap xtab;
 };
 bool stage1_tma_supported(int Wa, int Wb);
-cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int Wa, int Ha, int Wb, int Hb,
-                                      int m_base, int m_count, AxisTables xs, AxisTables ys,
-                                      const uint32_t* xpack, double* T, int num_sms, cudaStream_t st);
+cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa, int Ha, int Wb, int Hb,
+                                      int m_base, int m_count, const AxisTables* xs, const AxisTables* ys,
+                                      double* const* T, int num_sms, cudaStream_t st);
 // x-table packed for the TMA stage 1: uint32 (j0 + 1) << 24 | round(t * 2^23), 0 = skipped, [Wb][Wa].
 cudaError_t launch_pack_xtable(AxisTables xs, int Wa, int Wb, uint32_t* xpack, cudaStream_t st);
 // driver entry point cuTensorMapEncodeTiled (nullptr if unavailable)

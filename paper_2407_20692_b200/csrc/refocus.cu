@@ -183,71 +183,84 @@ __global__ void stage2_kernel(const double* __restrict__ T, int Wa, int Ha, int 
 }
 
 
-// ---- KB5 (TMA variant) ------------------------------------------------------------
-// Persistent, warp-specialised.  Tile = (A row m, 8 B rows v); the tile's Gamma is
-// streamed in chunks of 8 B columns u: warp 8 (one elected lane) issues, per chunk, TMA
-// boxes of 32 j-rows x 8 v x 8 u of Gamma covering only the j span the chunk's outputs
-// touch, plus the 8 x 256 packed x-table rows, into a 2-stage smem ring (mbarrier
-// full/empty).  Warps 0..7 consume: lane = (vq = lane/8, xl = lane%8), warp = x block;
-// thread owns x = 8*warp + xl + 64*i (i < 4) and v in {vq, vq+4}.  At step k a lane reads
-// column u' = (k + xl) % 8, so the 32 lanes of a warp hit 32 distinct banks for any
-// j0 (smem row of (j, v) = 8 floats; bank = 8 v + u').
-constexpr int kTVG = 8, kTUC = 8, kTJBox = 32, kTMaxJ = 256, kTStages = 3;
+// ---- KB5 (TMA variant, F fused planes) --------------------------------------------
+// Persistent, warp-specialised.  Tile = (A row m, 8 B rows v); the tile's Gamma is streamed
+// in chunks of 8 B columns u: warp 8 (one elected lane) issues, per chunk, TMA boxes of
+// 32 j-rows x 8 v x 8 u of Gamma covering only the union of the j spans the chunk's outputs
+// touch in the F planes of the group, plus the 8 x W_a packed x-table rows of each plane,
+// into a ring of mbarrier-guarded stages.  One HBM read of the span feeds F planes.
+// Warps 0..7 consume: lane = (vq = lane/16, xl = lane%16), thread owns
+// x = 16*warp + xl + 128*i (i < 2) and v = vq + 2*((s + xl/8) % 4) for slot s < 4.  At step k
+// a lane reads column u' = (k + xl) % 8, so the 32 lanes hit 32 distinct banks
+// (bank = 8 v + u') for any j0.  fp32 taps per 8-u chunk, fp64 across chunks.
+constexpr int kTVG = 8, kTUC = 8, kTJBox = 32, kTMaxJ = 256;
 constexpr int kTRow = kTVG * kTUC;                     // floats per staged j row (64)
 constexpr int kTGFloats = kTMaxJ * kTRow;              // 64 KB per stage
-constexpr int kTXEntries = kTUC * 256;                 // 8 KB per stage (uint32 entries)
+constexpr int kTXEntries = kTUC * 256;                 // 8 KB per plane per stage (uint32 entries)
 constexpr int kTMaxChunks = 64;                        // W_b <= 512
 constexpr int kTConsumers = 8;
 constexpr int kTThreads = 32 * (kTConsumers + 1);
-// smem map (bytes): [Gamma stages][x-table stages][zero rows 2 x 64 floats][span table][barriers]
-constexpr int kTOffX = kTStages * kTGFloats * 4;
-constexpr int kTOffZ = kTOffX + kTStages * kTXEntries * 4;
-constexpr int kTOffSpan = kTOffZ + 2 * kTRow * 4;
-constexpr int kTOffBar = kTOffSpan + kTMaxChunks * 8;
-constexpr int kTSmem = kTOffBar + 4 * kTStages * 8 + 64;
+
+template <int F>
+struct S1Cfg {
+    static constexpr int kStages = F == 1 ? 3 : 2;
+    // smem map (bytes): [Gamma stages][x-table stages x F][zero rows 2 x 64 floats][span table][barriers]
+    static constexpr int kOffX = kStages * kTGFloats * 4;
+    static constexpr int kOffZ = kOffX + kStages * F * kTXEntries * 4;
+    static constexpr int kOffSpan = kOffZ + 2 * kTRow * 4;
+    static constexpr int kOffBar = kOffSpan + kTMaxChunks * 8;
+    static constexpr int kSmem = kOffBar + 4 * kStages * 8 + 64;
+};
 
 struct S1Args {
     int Wa, Ha, Wb, Hb, m_base, m_count, n_vg, n_chunks;
-    const int32_t *xlo, *xhi, *ylo, *yhi;
-    double* T;
+    const int32_t* xlo[kRefocusMaxFuse];
+    const int32_t* xhi[kRefocusMaxFuse];
+    const int32_t* ylo[kRefocusMaxFuse];
+    const int32_t* yhi[kRefocusMaxFuse];
+    double* T[kRefocusMaxFuse];
 };
 
-__device__ __forceinline__ unsigned tile_mask(const S1Args& a, int m, int v0) {
+template <int F>
+__device__ __forceinline__ unsigned tile_mask(const S1Args& a, int m, int v0, int f) {
     unsigned need = 0;
     const int nv = min(kTVG, a.Hb - v0);
     for (int v = 0; v < nv; ++v) {
-        const int lo = __ldg(a.ylo + v0 + v), hi = __ldg(a.yhi + v0 + v);
+        const int lo = __ldg(a.ylo[f] + v0 + v), hi = __ldg(a.yhi[f] + v0 + v);
         if (m >= lo && m <= hi) need |= 1u << v;
     }
     return need;
 }
 
-template <bool kFullX>
+template <bool kFullX, int F>
 __global__ void __launch_bounds__(kTThreads, 1)
 stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_x, S1Args a) {
+    using C = S1Cfg<F>;
     extern __shared__ __align__(1024) uint8_t s1_smem[];
     float* sg = reinterpret_cast<float*>(s1_smem);
-    const uint32_t* sx = reinterpret_cast<const uint32_t*>(s1_smem + kTOffX);
-    int2* span = reinterpret_cast<int2*>(s1_smem + kTOffSpan);
-    uint64_t* full = reinterpret_cast<uint64_t*>(s1_smem + kTOffBar);
-    uint64_t* empty = full + kTStages;
+    const uint32_t* sx = reinterpret_cast<const uint32_t*>(s1_smem + C::kOffX);
+    int2* span = reinterpret_cast<int2*>(s1_smem + C::kOffSpan);
+    uint64_t* full = reinterpret_cast<uint64_t*>(s1_smem + C::kOffBar);
+    uint64_t* empty = full + C::kStages;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kTStages; ++s) {
+        for (int s = 0; s < C::kStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kTConsumers);
         }
         fence_mbar_init();
     }
-    if (threadIdx.x < 2 * kTRow) sg[kTOffZ / 4 + threadIdx.x] = 0.f;
-    // j span [lo, hi] of every u chunk (lo > hi: no output uses the chunk)
+    if (threadIdx.x < 2 * kTRow) sg[C::kOffZ / 4 + threadIdx.x] = 0.f;
+    // union j span [lo, hi] over the F planes of every u chunk (lo > hi: chunk unused)
     for (int c = threadIdx.x; c < a.n_chunks; c += blockDim.x) {
         int lo = INT_MAX, hi = -1;
-        for (int k = 0; k < kTUC && c * kTUC + k < a.Wb; ++k) {
-            lo = min(lo, __ldg(a.xlo + c * kTUC + k));
-            hi = max(hi, __ldg(a.xhi + c * kTUC + k));
-        }
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+            for (int k = 0; k < kTUC && c * kTUC + k < a.Wb; ++k) {
+                lo = min(lo, __ldg(a.xlo[f] + c * kTUC + k));
+                hi = max(hi, __ldg(a.xhi[f] + c * kTUC + k));
+            }
         span[c] = make_int2(lo, hi);
     }
     __syncthreads();
@@ -261,101 +274,115 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
                 const int ml = tile / a.n_vg, vg = tile - ml * a.n_vg;
-                if (!tile_mask(a, a.m_base + ml, vg * kTVG)) continue;
+                unsigned any = 0;
+#pragma unroll
+                for (int f = 0; f < F; ++f) any |= tile_mask<F>(a, a.m_base + ml, vg * kTVG, f);
+                if (!any) continue;
                 for (int c = 0; c < a.n_chunks; ++c) {
                     const int2 sp = span[c];
                     if (sp.y < sp.x) continue;
                     const int nb = (sp.y - sp.x + kTJBox) / kTJBox;
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], nb * kTJBox * kTRow * 4 + kTUC * a.Wa * 4);
+                    mbar_expect_tx(&full[stage], nb * kTJBox * kTRow * 4 + F * kTUC * a.Wa * 4);
                     float* dst = sg + stage * kTGFloats;
                     for (int b = 0; b < nb; ++b)
                         tma_load_4d(dst + b * kTJBox * kTRow, &tm_g, &full[stage], c * kTUC, vg * kTVG,
                                     sp.x + b * kTJBox, ml);
-                    tma_load_2d(s1_smem + kTOffX + stage * kTXEntries * 4, &tm_x, &full[stage], 0, c * kTUC);
-                    if (++stage == kTStages) { stage = 0; phase ^= 1; }
+#pragma unroll
+                    for (int f = 0; f < F; ++f)
+                        tma_load_3d(s1_smem + C::kOffX + (stage * F + f) * kTXEntries * 4, &tm_x, &full[stage], 0,
+                                    c * kTUC, f);
+                    if (++stage == C::kStages) { stage = 0; phase ^= 1; }
                 }
             }
         }
         return;
     }
 
-    // consumers: lane = (vq = lane / 16, xl = lane % 16); thread owns x = 16*warp + xl + 128*i
-    // (i < 2) and v = vq + 2*s (s < 4).  At step k the lane reads column u' = (k + xl) % 8 and,
-    // for accumulator slot s, B row v = vq + 2*((s + hi) % 4) with hi = xl / 8, so the 32 lanes
-    // hit 32 distinct banks (bank = 8 v + u') for any j0.
     const int vq = lane >> 4, xl = lane & 15, hi = xl >> 3;
     const int xbase = warp * 16 + xl;
     int voff[4];                                           // float offset of slot s's v row
 #pragma unroll
     for (int s = 0; s < 4; ++s) voff[s] = (vq + 2 * ((s + hi) & 3)) * kTUC;
-    const int zero_idx = kTOffZ / 4;
+    const int zero_idx = C::kOffZ / 4;
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int ml = tile / a.n_vg, vg = tile - ml * a.n_vg;
         const int m = a.m_base + ml, v0 = vg * kTVG;
-        const unsigned mask = tile_mask(a, m, v0);
-        if (!mask) continue;
-        double acc[2][4];
+        unsigned mask[F], any = 0;
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+        for (int f = 0; f < F; ++f) { mask[f] = tile_mask<F>(a, m, v0, f); any |= mask[f]; }
+        if (!any) continue;
+        double acc[F][2][4];
 #pragma unroll
-            for (int s = 0; s < 4; ++s) acc[i][s] = 0.0;
+        for (int f = 0; f < F; ++f)
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int s = 0; s < 4; ++s) acc[f][i][s] = 0.0;
         for (int c = 0; c < a.n_chunks; ++c) {
             const int2 sp = span[c];
             if (sp.y < sp.x) continue;
             mbar_wait(&full[stage], phase);
             // float index of (j = 0, v = 0, u = 0) in this stage, rebased by the chunk's j_lo
             const int gbase = stage * kTGFloats - sp.x * kTRow;
-            const int xt = stage * kTXEntries + xbase;
-            float part[2][4];
+            float part[F][2][4];
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
+            for (int f = 0; f < F; ++f)
 #pragma unroll
-                for (int s = 0; s < 4; ++s) part[i][s] = 0.f;
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int s = 0; s < 4; ++s) part[f][i][s] = 0.f;
 #pragma unroll
             for (int k = 0; k < kTUC; ++k) {
                 const int uu = (k + xl) & (kTUC - 1);
-                const int xrow = xt + uu * a.Wa;
 #pragma unroll
-                for (int i = 0; i < 2; ++i) {
-                    if (kFullX || xbase + 128 * i < a.Wa) {
-                        // entry = (j0 + 1) << 24 | round(t * 2^23); 0 = skipped sample
-                        const uint32_t e = sx[xrow + 128 * i];
-                        const int jp1 = static_cast<int>(e >> 24);
-                        const float t = __int_as_float(0x3F800000 + static_cast<int>(e & 0xFFFFFFu)) - 1.f;
-                        const float w0 = 1.f - t;
-                        // skipped samples (t == 0) read the two zero rows
-                        const int gi = (jp1 ? gbase + (jp1 - 1) * kTRow : zero_idx) + uu;
+                for (int f = 0; f < F; ++f) {
+                    const int xrow = (stage * F + f) * kTXEntries + uu * a.Wa + xbase;
 #pragma unroll
-                        for (int s = 0; s < 4; ++s) {
-                            const float g0 = sg[gi + voff[s]];
-                            const float g1 = sg[gi + voff[s] + kTRow];
-                            part[i][s] = fmaf(t, g1, fmaf(w0, g0, part[i][s]));
+                    for (int i = 0; i < 2; ++i) {
+                        if (kFullX || xbase + 128 * i < a.Wa) {
+                            // entry = (j0 + 1) << 24 | round(t * 2^23); 0 = skipped sample
+                            const uint32_t e = sx[xrow + 128 * i];
+                            const int jp1 = static_cast<int>(e >> 24);
+                            const float t = __int_as_float(0x3F800000 + static_cast<int>(e & 0xFFFFFFu)) - 1.f;
+                            const float w0 = 1.f - t;
+                            // skipped samples (t == 0) read the two zero rows
+                            const int gi = (jp1 ? gbase + (jp1 - 1) * kTRow : zero_idx) + uu;
+#pragma unroll
+                            for (int s = 0; s < 4; ++s) {
+                                const float g0 = sg[gi + voff[s]];
+                                const float g1 = sg[gi + voff[s] + kTRow];
+                                part[f][i][s] = fmaf(t, g1, fmaf(w0, g0, part[f][i][s]));
+                            }
                         }
                     }
                 }
             }
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
+            for (int f = 0; f < F; ++f)
 #pragma unroll
-                for (int s = 0; s < 4; ++s) acc[i][s] += static_cast<double>(part[i][s]);
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int s = 0; s < 4; ++s) acc[f][i][s] += static_cast<double>(part[f][i][s]);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[stage]);
-            if (++stage == kTStages) { stage = 0; phase ^= 1; }
+            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const int x = xbase + 128 * i;
-            if (!kFullX && x >= a.Wa) continue;
-            double* dst = a.T + (static_cast<int64_t>(x) * a.Ha + m) * a.Hb + v0;
+        for (int f = 0; f < F; ++f)
 #pragma unroll
-            for (int s = 0; s < 4; ++s) {
-                const int v = vq + 2 * ((s + hi) & 3);
-                if (mask & (1u << v)) dst[v] = acc[i][s];
+            for (int i = 0; i < 2; ++i) {
+                const int x = xbase + 128 * i;
+                if (!kFullX && x >= a.Wa) continue;
+                double* dst = a.T[f] + (static_cast<int64_t>(x) * a.Ha + m) * a.Hb + v0;
+#pragma unroll
+                for (int s = 0; s < 4; ++s) {
+                    const int v = vq + 2 * ((s + hi) & 3);
+                    if (mask[f] & (1u << v)) dst[v] = acc[f][i][s];
+                }
             }
-        }
     }
 }
 
@@ -404,29 +431,43 @@ cudaError_t launch_pack_xtable(AxisTables xs, int Wa, int Wb, uint32_t* xpack, c
     return cudaGetLastError();
 }
 
-cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int Wa, int Ha, int Wb, int Hb, int m_base,
-                                      int m_count, AxisTables xs, AxisTables ys, const uint32_t* /*xpack*/,
-                                      double* T, int num_sms, cudaStream_t st) {
+template <bool kFullX, int F>
+static cudaError_t launch_s1(const Stage1Maps* maps, const S1Args& a, int grid, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(stage1_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(stage1_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTSmem);
+        cudaError_t e = cudaFuncSetAttribute(stage1_tma_kernel<kFullX, F>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, S1Cfg<F>::kSmem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    S1Args a;
+    stage1_tma_kernel<kFullX, F><<<grid, kTThreads, S1Cfg<F>::kSmem, st>>>(maps->gamma, maps->xtab, a);
+    return cudaGetLastError();
+}
+
+template <bool kFullX>
+static cudaError_t launch_s1_f(int F, const Stage1Maps* maps, const S1Args& a, int grid, cudaStream_t st) {
+    switch (F) {
+        case 1: return launch_s1<kFullX, 1>(maps, a, grid, st);
+        case 2: return launch_s1<kFullX, 2>(maps, a, grid, st);
+        case 3: return launch_s1<kFullX, 3>(maps, a, grid, st);
+        default: return launch_s1<kFullX, 4>(maps, a, grid, st);
+    }
+}
+
+cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa, int Ha, int Wb, int Hb,
+                                      int m_base, int m_count, const AxisTables* xs, const AxisTables* ys,
+                                      double* const* T, int num_sms, cudaStream_t st) {
+    if (n_fuse < 1 || n_fuse > kRefocusMaxFuse) return cudaErrorInvalidValue;
+    S1Args a{};
     a.Wa = Wa; a.Ha = Ha; a.Wb = Wb; a.Hb = Hb; a.m_base = m_base; a.m_count = m_count;
     a.n_vg = (Hb + kTVG - 1) / kTVG;
     a.n_chunks = (Wb + kTUC - 1) / kTUC;
-    a.xlo = xs.lo; a.xhi = xs.hi; a.ylo = ys.lo; a.yhi = ys.hi; a.T = T;
+    for (int f = 0; f < n_fuse; ++f) {
+        a.xlo[f] = xs[f].lo; a.xhi[f] = xs[f].hi; a.ylo[f] = ys[f].lo; a.yhi[f] = ys[f].hi; a.T[f] = T[f];
+    }
     const int tiles = m_count * a.n_vg;
     const int grid = tiles < num_sms ? tiles : num_sms;
-    if (Wa == 256)
-        stage1_tma_kernel<true><<<grid, kTThreads, kTSmem, st>>>(maps->gamma, maps->xtab, a);
-    else
-        stage1_tma_kernel<false><<<grid, kTThreads, kTSmem, st>>>(maps->gamma, maps->xtab, a);
-    return cudaGetLastError();
+    return Wa == 256 ? launch_s1_f<true>(n_fuse, maps, a, grid, st) : launch_s1_f<false>(n_fuse, maps, a, grid, st);
 }
 
 cudaError_t launch_refocus_stage2(const double* T, int Wa, int Ha, int Hb, int m_base, int m_count,
