@@ -554,9 +554,11 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
                 const double alpha = spec->alphas[p0 + f];
                 e = cpi::launch_refocus_coords(alpha, spec->boundary, Wa, Wb, c->xs[f], st);
                 if (e == cudaSuccess) e = cpi::launch_refocus_coords(alpha, spec->boundary, Ha, Hb, c->ys[f], st);
-                if (e == cudaSuccess && tma_now)
-                    e = cpi::launch_pack_xtable(c->xs[f], Wa, Wb, c->xpack + size_t(f) * Wa * Wb, st);
-                c->launches += tma_now ? 3 : 2;
+                c->launches += 2;
+            }
+            if (e == cudaSuccess && tma_now) {
+                e = cpi::launch_pack_xtable_group(c->xs, nf, Wa, Wb, c->xpack, st);
+                c->launches += 1;
             }
             if (e != cudaSuccess) return cuda_fail(c, e, "refocus coords launch");
         }

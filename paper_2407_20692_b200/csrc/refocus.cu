@@ -195,7 +195,7 @@ __global__ void stage2_kernel(const double* __restrict__ T, int Wa, int Ha, int 
 // (bank = 8 v + u') for any j0.  fp32 taps per 8-u chunk, fp64 across chunks.
 constexpr int kTVG = 8, kTUC = 8, kTJBox = 32, kTMaxJ = 256;
 constexpr int kTRow = kTVG * kTUC;                     // floats per staged j row (64)
-constexpr int kTGFloats = kTMaxJ * kTRow;              // 64 KB per stage
+constexpr int kTGFloats = (kTMaxJ + 2) * kTRow;        // 64.5 KB per stage; rows 256-257 stay zero
 constexpr int kTXEntries = kTUC * 256;                 // 8 KB per plane per stage (uint32 entries)
 constexpr int kTMaxChunks = 64;                        // W_b <= 512
 constexpr int kTConsumers = 8;
@@ -204,10 +204,9 @@ constexpr int kTThreads = 32 * (kTConsumers + 1);
 template <int F>
 struct S1Cfg {
     static constexpr int kStages = F == 1 ? 3 : 2;
-    // smem map (bytes): [Gamma stages][x-table stages x F][zero rows 2 x 64 floats][span table][barriers]
+    // smem map (bytes): [Gamma stages (258 rows each)][x-table stages x F][span table][barriers]
     static constexpr int kOffX = kStages * kTGFloats * 4;
-    static constexpr int kOffZ = kOffX + kStages * F * kTXEntries * 4;
-    static constexpr int kOffSpan = kOffZ + 2 * kTRow * 4;
+    static constexpr int kOffSpan = kOffX + kStages * F * kTXEntries * 4;
     static constexpr int kOffBar = kOffSpan + kTMaxChunks * 8;
     static constexpr int kSmem = kOffBar + 4 * kStages * 8 + 64;
 };
@@ -251,7 +250,9 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
         }
         fence_mbar_init();
     }
-    if (threadIdx.x < 2 * kTRow) sg[C::kOffZ / 4 + threadIdx.x] = 0.f;
+    // zero every staged Gamma row once: rows 256-257 of each stage are the skipped-sample
+    // rows, and a zero-weight tap past a chunk's span then reads 0 or an earlier finite value
+    for (int i = threadIdx.x; i < C::kStages * kTGFloats; i += blockDim.x) sg[i] = 0.f;
     // union j span [lo, hi] over the F planes of every u chunk (lo > hi: chunk unused)
     for (int c = threadIdx.x; c < a.n_chunks; c += blockDim.x) {
         int lo = INT_MAX, hi = -1;
@@ -304,7 +305,6 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
     int voff[4];                                           // float offset of slot s's v row
 #pragma unroll
     for (int s = 0; s < 4; ++s) voff[s] = (vq + 2 * ((s + hi) & 3)) * kTUC;
-    const int zero_idx = C::kOffZ / 4;
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -325,8 +325,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
             const int2 sp = span[c];
             if (sp.y < sp.x) continue;
             mbar_wait(&full[stage], phase);
-            // float index of (j = 0, v = 0, u = 0) in this stage, rebased by the chunk's j_lo
-            const int gbase = stage * kTGFloats - sp.x * kTRow;
+            const float* G = sg + stage * kTGFloats;
             float part[F][2][4];
 #pragma unroll
             for (int f = 0; f < F; ++f)
@@ -337,23 +336,24 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
 #pragma unroll
             for (int k = 0; k < kTUC; ++k) {
                 const int uu = (k + xl) & (kTUC - 1);
+                const float* Gu = G + uu;
 #pragma unroll
                 for (int f = 0; f < F; ++f) {
                     const int xrow = (stage * F + f) * kTXEntries + uu * a.Wa + xbase;
 #pragma unroll
                     for (int i = 0; i < 2; ++i) {
                         if (kFullX || xbase + 128 * i < a.Wa) {
-                            // entry = (j0 + 1) << 24 | round(t * 2^23); 0 = skipped sample
+                            // entry = j_rel << 23 | round(t * 2^23), j_rel = smem row of j0 relative
+                            // to the chunk's staged span (256 = zero rows: skipped sample, t = 0)
                             const uint32_t e = sx[xrow + 128 * i];
-                            const int jp1 = static_cast<int>(e >> 24);
-                            const float t = __int_as_float(0x3F800000 + static_cast<int>(e & 0xFFFFFFu)) - 1.f;
-                            const float w0 = 1.f - t;
-                            // skipped samples (t == 0) read the two zero rows
-                            const int gi = (jp1 ? gbase + (jp1 - 1) * kTRow : zero_idx) + uu;
+                            const float one_t = __int_as_float((e & 0x7FFFFFu) | 0x3F800000u);   // 1 + t
+                            const float t = one_t - 1.f;
+                            const float w0 = 2.f - one_t;
+                            const float* gp = Gu + (e >> 23) * kTRow;
 #pragma unroll
                             for (int s = 0; s < 4; ++s) {
-                                const float g0 = sg[gi + voff[s]];
-                                const float g1 = sg[gi + voff[s] + kTRow];
+                                const float g0 = gp[voff[s]];
+                                const float g1 = gp[voff[s] + kTRow];
                                 part[f][i][s] = fmaf(t, g1, fmaf(w0, g0, part[f][i][s]));
                             }
                         }
@@ -386,13 +386,29 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
     }
 }
 
-__global__ void pack_xtable_kernel(const int32_t* __restrict__ i0, const double* __restrict__ t, int n,
-                                   uint32_t* __restrict__ out) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx < n) {
-        const int j = i0[idx];
-        const uint32_t tq = static_cast<uint32_t>(__double2uint_rn(t[idx] * 8388608.0));
-        out[idx] = j < 0 ? 0u : ((static_cast<uint32_t>(j + 1) << 24) | tq);
+// Packed x-tables of a fused group of F planes for the TMA stage 1 (W_a <= 256):
+//   entry(f, u, x) = j_rel << 23 | round(t * 2^23)
+// where j_rel = j0 - j_lo(chunk of u) is the smem row of the lower tap inside the chunk's
+// staged union span (the same union the producer stages), t in [0, 1) (a t that rounds to
+// 1 moves to the next row with t = 0), and skipped samples point at the zero rows
+// (j_rel = 256, t = 0).  t keeps 2^-23 resolution; t = 0 stays exact.
+__global__ void pack_xtable_group_kernel(PackGroupArgs g, int Wa, int Wb, uint32_t* __restrict__ out) {
+    const int u = blockIdx.x, f = blockIdx.y;
+    const int c0 = (u / 8) * 8;
+    int jlo = INT_MAX;
+    for (int ff = 0; ff < g.n; ++ff)
+        for (int k = c0; k < c0 + 8 && k < Wb; ++k) jlo = min(jlo, __ldg(g.lo[ff] + k));
+    for (int x = threadIdx.x; x < Wa; x += blockDim.x) {
+        const int64_t idx = static_cast<int64_t>(u) * Wa + x;
+        const int j = __ldg(g.i0[f] + idx);
+        uint32_t e = 256u << 23;
+        if (j >= 0) {
+            uint32_t tq = static_cast<uint32_t>(__double2uint_rn(__ldg(g.t[f] + idx) * 8388608.0));
+            int jr = j - jlo;
+            if (tq >= 8388608u) { tq = 0; jr += 1; }
+            e = (static_cast<uint32_t>(jr) << 23) | tq;
+        }
+        out[(static_cast<int64_t>(f) * Wb + u) * Wa + x] = e;
     }
 }
 
@@ -425,9 +441,12 @@ cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int H
 
 bool stage1_tma_supported(int Wa, int Wb) { return Wa <= 256 && Wa >= 2 && (Wb % 4) == 0 && Wb <= 8 * kTMaxChunks; }
 
-cudaError_t launch_pack_xtable(AxisTables xs, int Wa, int Wb, uint32_t* xpack, cudaStream_t st) {
-    const int n = Wa * Wb;
-    pack_xtable_kernel<<<(n + 255) / 256, 256, 0, st>>>(xs.i0, xs.t, n, xpack);
+cudaError_t launch_pack_xtable_group(const AxisTables* xs, int n_fuse, int Wa, int Wb, uint32_t* xpack,
+                                     cudaStream_t st) {
+    PackGroupArgs g{};
+    g.n = n_fuse;
+    for (int f = 0; f < n_fuse; ++f) { g.i0[f] = xs[f].i0; g.t[f] = xs[f].t; g.lo[f] = xs[f].lo; }
+    pack_xtable_group_kernel<<<dim3(Wb, n_fuse), Wa >= 256 ? 256 : ((Wa + 31) / 32) * 32, 0, st>>>(g, Wa, Wb, xpack);
     return cudaGetLastError();
 }
 
