@@ -131,30 +131,40 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ roofline helpers -------
-def refocus_span_bytes(dims, alphas, row_range=None):
-    """Algorithmic bytes of refocus stage 1 per plane: 4 B x the Gamma entries inside the
-    separable stencil span, (sum_u |J_u|) * (sum_v |M_v|), J_u = [min j0, max j0 + 1] over
-    the outputs x that use column u (and M_v likewise) — SURVEY §8(d) 'per unit of work'."""
+def _axis_tables(W, Wb_, alpha):
+    """Per-axis support of the default map, as the kernels use it: for every
+    B coordinate the used outputs, their lower taps and the span [min i0, max i0 + 1]."""
+    c, cb = (W - 1) / 2.0, (Wb_ - 1) / 2.0
+    x = np.arange(W, dtype=np.float64)[None, :]
+    u = np.arange(Wb_, dtype=np.float64)[:, None]
+    cc = (alpha * (x - c)) + ((1.0 - alpha) * (u - cb)) + c
+    ok = (cc >= 0) & (cc <= W - 1)
+    j0 = np.minimum(np.floor(cc), W - 2)
+    lo = np.where(ok, j0, np.inf).min(1)
+    hi = np.where(ok, j0 + 1, -np.inf).max(1)
+    span = np.where(hi >= lo, hi - lo + 1, 0)
+    return ok, span
+
+
+def refocus_work(dims, alphas):
+    """Per-plane algorithmic work of refocus stage 1 (SURVEY §8(d) 'per unit of work'):
+      bytes = 4 B x Gamma entries inside the separable stencil span
+            = 4 (sum_u |J_u|)(sum_v |M_v|), J_u = [min j0, max j0 + 1] over outputs using u;
+      taps  = 2 x (valid (x, u) samples) x (sum_v |M_v|)  — one fp32 tap = one 4-byte
+              shared-memory load + one FMA in the kernel.
+    Returns (bytes, taps) summed over the planes."""
     Wa, Ha, Wb, Hb = dims
-
-    def axis(W, Wb_, alpha):
-        c, cb = (W - 1) / 2.0, (Wb_ - 1) / 2.0
-        x = np.arange(W, dtype=np.float64)[None, :]
-        u = np.arange(Wb_, dtype=np.float64)[:, None]
-        cc = (alpha * (x - c)) + ((1.0 - alpha) * (u - cb)) + c
-        ok = (cc >= 0) & (cc <= W - 1)
-        j0 = np.minimum(np.floor(cc), W - 2)
-        lo = np.where(ok, j0, np.inf).min(1)
-        hi = np.where(ok, j0 + 1, -np.inf).max(1)
-        span = np.where(hi >= lo, hi - lo + 1, 0)
-        return span
-
-    total = 0.0
+    tot_b = tot_t = 0.0
     for a in alphas:
-        sx = axis(Wa, Wb, a).sum()
-        sy = axis(Ha, Hb, a)
-        total += 4.0 * sx * sy.sum()
-    return total
+        okx, sx = _axis_tables(Wa, Wb, a)
+        _, sy = _axis_tables(Ha, Hb, a)
+        tot_b += 4.0 * sx.sum() * sy.sum()
+        tot_t += 2.0 * okx.sum() * sy.sum()
+    return tot_b, tot_t
+
+
+def refocus_span_bytes(dims, alphas):
+    return refocus_work(dims, alphas)[0]
 
 
 # ------------------------------------------------------------------ CPU baseline ----------
@@ -358,30 +368,47 @@ def main():
         return
 
     peaks, peak_src = load_peaks()
-    int8_sustained = 2.0 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])   # TOPS, i8 = 2 x bf16
-    int8_burst = 2.0 * peaks["bf16_tflops"]
+    int8_burst = 2.0 * peaks["bf16_tflops"]                                  # TOPS, i8 = 2 x bf16 (4.5/2.25)
+    int8_sustained = 2.0 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     hbm = peaks["hbm_gbs"]
+    f_clk = (clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)) * 1e6
     gemm_ms, gemm_n = kt["gemm"]
     ops = 2.0 * p_a * p_b * n                         # algorithmic: one AND/MAC per pair per frame
     gemm_tops = ops / (gemm_ms / gemm_n / 1e3) / 1e12 if gemm_n else None
+    clock_peak_tops = 148 * 8192 * 2 * f_clk / 1e12  # tcgen05 kind::i8: 8192 MAC/clk/SM
     s1_ms, s1_n = kt["stage1"]
     rows_here = p_a if world == 1 else p_a // world
-    span = refocus_span_bytes((Wa, Ha, Wb, Hb), alphas) * rows_here / p_a   # per step
-    s1_gbs = span / (s1_ms / args.steps / 1e3) / 1e9 if s1_n else None
+    span, taps = refocus_work((Wa, Ha, Wb, Hb), alphas)
+    span *= rows_here / p_a
+    taps *= rows_here / p_a
+    s1_s = s1_ms / args.steps / 1e3
+    s1_gbs = span / s1_s / 1e9 if s1_n else None
+    s1_gtaps = taps / s1_s / 1e9 if s1_n else None
+    lds_peak_gtaps = 148 * 32 * f_clk / 1e9          # 32 four-byte LDS lanes per clock per SM
     corr_ms = (kt["expand"][0] + gemm_ms) / args.steps
     ref_ms = (kt["coords"][0] + s1_ms + kt["stage2"][0]) / args.steps
-    roof_gemm = {"kernel": "gemm_i8_tc (KB2)" if args.variant == "tc" else "gemm_popc (KB3)",
-                 "bound": "tensor", "achieved": gemm_tops, "peak": int8_sustained, "unit": "TOPS",
-                 "frac": gemm_tops / int8_sustained if gemm_tops else None,
-                 "frac_of_burst": gemm_tops / int8_burst if gemm_tops else None,
-                 "peak_note": f"int8 dense = 2 x {peak_src} bf16 ({peaks['bf16_tflops']} burst, "
-                              f"{peaks.get('bf16_tflops_sustained')} sustained); sustained used",
+    roof_gemm = {"kernel": "gemm_i8_tc2 (KB2, cta_group::2)" if args.variant == "tc" else "gemm_popc (KB3)",
+                 "bound": "tensor", "achieved": gemm_tops, "peak": int8_burst, "unit": "TOPS",
+                 "frac": gemm_tops / int8_burst if gemm_tops else None,
+                 "peak_note": (f"int8 dense = 2 x {peak_src} bf16 burst {peaks['bf16_tflops']} TFLOP/s "
+                               f"(guide ratio 4.5/2.25); the sustained bf16 figure ({peaks.get('bf16_tflops_sustained')}) "
+                               f"was taken at a 1327 MHz median clock, this run's median was "
+                               f"{clk.get('sm_mhz')} MHz"),
+                 "frac_of_sustained": gemm_tops / int8_sustained if gemm_tops else None,
+                 "frac_of_clock_peak": gemm_tops / clock_peak_tops if gemm_tops else None,
+                 "clock_peak_tops": clock_peak_tops,
                  "ops_per_launch": ops, "ms_per_launch": gemm_ms / gemm_n if gemm_n else None,
                  "traffic": None}
-    roof_s1 = {"kernel": "refocus_stage1 (KB5)", "bound": "hbm", "achieved": s1_gbs, "peak": hbm,
-               "unit": "GB/s", "frac": s1_gbs / hbm if s1_gbs else None,
-               "bytes_per_step": span, "ms_per_step": s1_ms / args.steps, "traffic": None,
-               "peak_note": f"{peak_src} HBM copy bandwidth"}
+    roof_s1 = {"kernel": "refocus_stage1_tma (KB5, 4 planes per pass)", "bound": "alu",
+               "achieved": s1_gtaps, "peak": lds_peak_gtaps, "unit": "Gtap/s",
+               "frac": s1_gtaps / lds_peak_gtaps if s1_gtaps else None,
+               "peak_note": ("one fp32 tap = one 4-byte shared-memory load (+1 FFMA); peak = 148 SMs x 32 "
+                             "LDS lanes/clk x median SM clock of this run (DESIGN.md §5)"),
+               "taps_per_step": taps, "ms_per_step": s1_ms / args.steps,
+               "hbm_view": {"algorithmic_bytes_per_step": span, "achieved_gbs": s1_gbs, "peak_gbs": hbm,
+                            "frac": s1_gbs / hbm if s1_gbs else None,
+                            "note": "per-plane span bytes / time; > 1 possible because 4 planes share one HBM pass"},
+               "traffic": None}
     dominant = roof_s1 if (s1_ms > gemm_ms) else roof_gemm
     cpu = None
     if world == 1 and not args.no_cpu_baseline:

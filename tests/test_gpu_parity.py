@@ -263,3 +263,18 @@ def test_end_to_end_frames_to_planes_alpha1_ghost():
     ghost = (n * (A.T @ nB) - A.sum(0) * nB.sum()) / (n * n * 320.0)
     M = oracle.refocus(np.abs(want["gamma"]), dims, [1.0])[0].reshape(-1)
     assert np.all(np.abs(R[1].reshape(-1) - ghost) <= 1e-6 * M + 1e-30)
+
+
+@pytest.mark.parametrize("fuse", [1, 2, 3, 4])
+def test_refocus_fused_plane_groups(fuse, monkeypatch):
+    """The TMA stage 1 fuses F planes per pass over Gamma (CPI_REFOCUS_FUSE); every group size,
+    including a ragged last group (7 planes), matches the oracle per plane.  The alpha set spans
+    alpha < 1 (all samples valid, narrow j spans), alpha = 1 and alpha > 1 (skipped samples,
+    warp-level x-block skipping)."""
+    monkeypatch.setenv("CPI_REFOCUS_FUSE", str(fuse))
+    dims = (64, 40, 48, 24)
+    Wa, Ha, Wb, Hb = dims
+    G = synth.random_gamma(Wa * Ha, Wb * Hb, seed=40 + fuse)
+    alphas = [0.5, 0.77, 1.0, 1.31, 1.62, 2.0, 2.9]
+    R = _refocus_gpu(G, dims, alphas)
+    _assert_planes(R, G, dims, alphas)
