@@ -590,6 +590,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
 
 int64_t cpi_launch_count(const cpi_ctx* c) { return c ? c->launches : 0; }
 
+
 cpi_status cpi_set_timing(cpi_ctx* c, int32_t enable) {
     if (!c) return CPI_ERR_INVALID_ARG;
     drain_timing(c);

@@ -253,6 +253,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
     // zero every staged Gamma row once: rows 256-257 of each stage are the skipped-sample
     // rows, and a zero-weight tap past a chunk's span then reads 0 or an earlier finite value
     for (int i = threadIdx.x; i < C::kStages * kTGFloats; i += blockDim.x) sg[i] = 0.f;
+    fence_proxy_async_smem();   // the zeros must land before the first TMA writes these rows
     // union j span [lo, hi] over the F planes of every u chunk (lo > hi: chunk unused)
     for (int c = threadIdx.x; c < a.n_chunks; c += blockDim.x) {
         int lo = INT_MAX, hi = -1;
@@ -360,14 +361,18 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                     }
                 }
             }
+            // Release the stage to the TMA producer.  The reads above are generic-proxy loads and
+            // the refill is an async-proxy write: order them with a proxy fence before the arrive
+            // (without it the refill could land while loads of this stage are still in flight).
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
 #pragma unroll
             for (int f = 0; f < F; ++f)
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
 #pragma unroll
                     for (int s = 0; s < 4; ++s) acc[f][i][s] += static_cast<double>(part[f][i][s]);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
             if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
 #pragma unroll

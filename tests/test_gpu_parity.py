@@ -278,3 +278,28 @@ def test_refocus_fused_plane_groups(fuse, monkeypatch):
     alphas = [0.5, 0.77, 1.0, 1.31, 1.62, 2.0, 2.9]
     R = _refocus_gpu(G, dims, alphas)
     _assert_planes(R, G, dims, alphas)
+
+
+def test_refocus_repeat_bit_identical():
+    """Every refocus kernel is deterministic (fixed summation order, no atomics in the value
+    path), so repeated runs must agree bit for bit.  Catches pipeline races: e.g. a stage
+    released to the TMA producer before its shared-memory loads have returned (the reads are
+    generic-proxy, the refill async-proxy).  W_a = 256 exercises the full-x kernel; alphas
+    near 2 maximise skipped samples."""
+    dims = (256, 64, 256, 64)
+    Wa, Ha, Wb, Hb = dims
+    ctx = _ctx((0, 0, Wa, Ha), (0, 0, Wb, Hb), 1)
+    g = torch.from_numpy(synth.random_gamma(Wa * Ha, Wb * Hb, seed=1)).cuda()
+    al = synth.alpha_grid(64)
+    ref = ctx.new_planes(64)
+    ctx.refocus(al, g, ref)
+    for _ in range(3):
+        p = ctx.new_planes(64)
+        ctx.refocus(al, g, p)
+        torch.cuda.synchronize()
+        assert torch.equal(p, ref)
+    same = ctx.new_planes(4)
+    ctx.refocus([1.9] * 4, g, same)
+    torch.cuda.synchronize()
+    for s in range(1, 4):
+        assert torch.equal(same[s], same[0])
