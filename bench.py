@@ -51,8 +51,8 @@ def parse():
     p.add_argument("--roi", default="full", choices=["full", "128", "tiny"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-rows", type=int, default=8, help="oracle sample: A pixels (rows of S_ab)")
-    p.add_argument("--cpu-pixels", type=int, default=8, help="oracle sample: refocused output pixels")
+    p.add_argument("--cpu-rows", type=int, default=0, help="(unused; the sample size follows the core count)")
+    p.add_argument("--cpu-pixels", type=int, default=256, help="oracle sample: refocused output pixels")
     return p.parse_args()
 
 
@@ -168,38 +168,54 @@ def refocus_span_bytes(dims, alphas):
 
 
 # ------------------------------------------------------------------ CPU baseline ----------
-def cpu_baseline(frames_np, roi_a, roi_b, alphas, n_rows, n_pix, step_planes):
-    """The oracle as it stands, on a bounded sample of the same workload (rank 0, N=1)."""
+def cpu_baseline(frames_np, roi_a, roi_b, alphas, n_rows, n_pix, step_planes, waves=(2, 4)):
+    """The oracle as it stands, timed on a bounded sample of the same workload (rank 0, N=1).
+
+    Its phases scale differently, so they are timed separately and extrapolated to the full
+    step: single-pixel sums over every pixel (timed in full); pair sums = a fixed part (frame
+    unpacking) + a per-A-pixel part, measured with 2*cores and 4*cores A pixels on all cores;
+    refocusing = per output pixel, measured on n_pix pixels of one plane."""
     import oracle
     oracle.build()
     cores = os.cpu_count() or 1
     n = frames_np.shape[0]
     p_a = roi_a[2] * roi_a[3]
-    rows = np.linspace(0, p_a - 1, n_rows).astype(np.int64)
     t0 = time.perf_counter()
     s_a = oracle.marginals(frames_np, roi_a)
     s_b = oracle.marginals(frames_np, roi_b)
-    s_ab = oracle.pair_sums(frames_np, roi_a, roi_b, rows=rows, threads=cores)
-    g = oracle.gamma(s_ab, s_a[rows], s_b, n)
-    t_corr = time.perf_counter() - t0
-    # refocus sample: n_pix output pixels of one plane, on a Gamma whose sampled rows are
-    # the oracle's own; the rest is filled with the same rows (cost is data-independent)
+    t_marg = time.perf_counter() - t0
+    r1, r2 = waves[0] * cores, waves[1] * cores
+    rows1 = np.linspace(0, p_a - 1, r1).astype(np.int64)
+    rows2 = np.linspace(0, p_a - 1, r2).astype(np.int64)
+    t0 = time.perf_counter()
+    oracle.pair_sums(frames_np, roi_a, roi_b, rows=rows1, threads=cores)
+    t1 = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    s_ab = oracle.pair_sums(frames_np, roi_a, roi_b, rows=rows2, threads=cores)
+    g = oracle.gamma(s_ab, s_a[rows2], s_b, n)
+    t2 = time.perf_counter() - t0
+    per_wave = max(t2 - t1, 1e-9) / (waves[1] - waves[0])   # one A pixel per core
+    fixed = max(t1 - waves[0] * per_wave, 0.0)
+    t_pairs_full = fixed + per_wave * p_a / cores
     Wa, Ha, Wb, Hb = roi_a[2], roi_a[3], roi_b[2], roi_b[3]
     G = np.empty((p_a, Wb * Hb), dtype=np.float32)
-    G[:] = g[np.arange(p_a) % n_rows].astype(np.float32)
+    G[:] = g[np.arange(p_a) % r2].astype(np.float32)   # refocus cost is data-independent
     rng = np.random.default_rng(0)
     pix = np.stack([rng.integers(0, Wa, n_pix), rng.integers(0, Ha, n_pix)], 1)
     alpha = float(alphas[len(alphas) // 3])
     t0 = time.perf_counter()
     oracle.refocus(G, (Wa, Ha, Wb, Hb), [alpha], pixels=pix, threads=cores)
     t_ref = time.perf_counter() - t0
-    # the marginals are O(N P) and already complete; pair sums scale with rows
-    est_step = t_corr * (p_a / n_rows) + t_ref * (Wa * Ha / n_pix) * step_planes
+    t_ref_full = t_ref * (Wa * Ha / n_pix) * step_planes
+    est_step = t_marg + t_pairs_full + t_ref_full
     return {"value": n / est_step, "unit": "frames/s", "cores": cores, "kind": "oracle",
-            "sample": (f"{n_rows} of {p_a} A pixels x all {Wb*Hb} B pixels x all {n} frames "
-                       f"({t_corr:.1f} s) + {n_pix} of {Wa*Ha} output pixels of 1 of {step_planes} "
-                       f"planes ({t_ref:.1f} s); step time extrapolated linearly by rows/pixels/planes"),
-            "extrapolated_step_s": est_step}
+            "sample": (f"single-pixel sums over all {p_a}+{Wb*Hb} pixels x {n} frames ({t_marg:.1f} s); "
+                       f"pair sums for {r1} and {r2} of {p_a} A pixels x all B pixels x all frames "
+                       f"({t1:.1f} s, {t2:.1f} s) -> fixed {fixed:.1f} s + {per_wave:.2f} s per {cores} A pixels; "
+                       f"refocus of {n_pix} of {Wa*Ha} output pixels of 1 plane ({t_ref:.1f} s); step time "
+                       f"extrapolated to all A pixels and {step_planes} planes"),
+            "extrapolated_step_s": est_step,
+            "extrapolated_parts_s": {"marginals": t_marg, "pair_sums": t_pairs_full, "refocus": t_ref_full}}
 
 
 # ------------------------------------------------------------------ reference arm ---------
@@ -213,8 +229,7 @@ def run_reference(args):
     vals = []
     last = None
     for i in range(args.warmup + args.steps):
-        r = cpu_baseline(frames, roi_a, roi_b, alphas, max(1, args.cpu_rows // 2),
-                         max(1, args.cpu_pixels // 2), args.planes)
+        r = cpu_baseline(frames, roi_a, roi_b, alphas, 0, max(1, args.cpu_pixels // 4), args.planes, waves=(1, 2))
         if i >= args.warmup:
             vals.append(r["value"])
             last = r
