@@ -1,0 +1,88 @@
+"""Frame-sharded pipeline through the CUDA backend (paper_2407_20692_b200.parallel.CudaBackend)
+with 2 ranks sharing one GPU over gloo.  No kernel waits on another rank (the collectives run on
+the host through gloo), so this is safe on one device; it exercises the product's multi-GPU
+code path end to end: per-rank int32 partial sums, all-reduce of the marginals, row
+reduce-scatter, cpi_finalize_counts of the owned rows, row-shard refocusing and the plane
+all-reduce.  Result: Gamma rows bit-identical to the single-context run, planes within fp
+rounding of it (shard planes are summed in fp32)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+ROI_A, ROI_B = (0, 0, 32, 16), (256, 0, 24, 12)
+N = 1500
+ALPHAS = [0.6, 1.0, 1.45]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    import synth
+    from paper_2407_20692_b200 import parallel
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        frames = synth.bernoulli_frames(N, 0.2, seed=77)
+        lo, hi = parallel.frame_slice(N, rank, world)
+        be = parallel.CudaBackend(ROI_A, ROI_B, hi - lo, device=0)
+
+        class GlooCuda:
+            """gloo collectives need host tensors: stage through the host (plumbing only)."""
+            device = be.device
+
+            def local_sums(self, fr):
+                return tuple(t.cpu() if hasattr(t, "cpu") else t for t in be.local_sums(fr))
+
+            def finalize_rows(self, s_ab_rows, row0, s_a, s_b, n_tot):
+                return be.finalize_rows(s_ab_rows.cuda(), row0, s_a.cuda(), s_b.cuda(), n_tot).cpu()
+
+            def refocus(self, alphas, gamma_rows, row0, rows):
+                return be.refocus(alphas, gamma_rows.cuda(), row0, rows).cpu()
+
+        res = parallel.correlate_and_refocus(GlooCuda(), np.ascontiguousarray(frames[lo:hi]), ROI_A, ROI_B, ALPHAS)
+        q.put((rank, res.n_tot, res.row0, res.rows, res.gamma_rows.numpy(), res.planes.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_on_one_gpu_match_single_context():
+    import torch.multiprocessing as mp
+    import synth
+    from paper_2407_20692_b200 import Context
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    frames = synth.bernoulli_frames(N, 0.2, seed=77)
+    c = Context(ROI_A, ROI_B, N)
+    c.load_frames(frames)
+    g = c.correlate(c.new_gamma())
+    planes = c.new_planes(len(ALPHAS))
+    c.refocus(ALPHAS, g, planes)
+    torch.cuda.synchronize()
+    G = g.cpu().numpy()
+    P = planes.cpu().numpy()
+    for rank, n_tot, row0, rows, g_rows, pl in out:
+        assert n_tot == N
+        np.testing.assert_array_equal(g_rows, G[row0:row0 + rows])
+        np.testing.assert_allclose(pl, P, rtol=1e-5, atol=1e-9)
