@@ -120,9 +120,13 @@ const char *cpi_status_string(cpi_status s);
 
 /* Load one batch of n_frames whole packed frames (frame-major, row-major, 1 bpp,
  * layout.width_px/8 bytes per row: "Input Dataset") as the input of the
- * next cpi_correlate.  where = CPI_HOST copies asynchronously on `stream`; CPI_DEVICE
- * uses the pointer in place.  Errors: INVALID_ARG, CAPACITY (n_frames > max_frames),
- * CUDA.  n_frames = 0 is allowed (the next correlate adds nothing). */
+ * next cpi_correlate.  where = CPI_HOST: asynchronous copy into one of two device staging
+ * buffers on an internal copy stream, so it overlaps the compute of the previous batch; the
+ * next cpi_correlate makes `stream` wait for it.  The host buffer must stay unchanged until
+ * the work of that cpi_correlate has completed on `stream` (pinned memory gives a truly
+ * asynchronous copy).  where = CPI_DEVICE uses the pointer in place.  Errors: INVALID_ARG,
+ * CAPACITY (n_frames > max_frames), CUDA.  n_frames = 0 is allowed (the next correlate adds
+ * nothing). */
 cpi_status cpi_load_frames(cpi_ctx *ctx, const void *packed, int64_t n_frames, int32_t where,
                            void *stream);
 

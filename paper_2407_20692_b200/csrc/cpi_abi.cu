@@ -40,7 +40,13 @@ struct cpi_ctx {
     int64_t k_cap = 0;                     // frames capacity rounded to 128
     int64_t ld_op = 0;                     // operand leading dimension (bytes or 32-bit words)
     int64_t frame_bytes = 0;
-    uint8_t* frames_dev = nullptr;         // staging for host loads
+    uint8_t* frames_dev[2] = {nullptr, nullptr};   // double-buffered staging for host loads
+    cudaStream_t copy_stream = nullptr;    // host->device copies overlap the previous batch's compute
+    cudaEvent_t ev_loaded[2] = {nullptr, nullptr};    // copy into buffer b complete
+    cudaEvent_t ev_consumed[2] = {nullptr, nullptr};  // expand of buffer b complete (buffer reusable)
+    bool consumed_valid[2] = {false, false};
+    int next_buf = 0;
+    int cur_buf = -1;                      // buffer of the loaded batch (-1: device pointer)
     const uint8_t* frames_cur = nullptr;
     int64_t n_cur = 0;
     bool loaded = false;
@@ -172,7 +178,13 @@ cpi_status make_tmap(cpi_ctx* c, CUtensorMap* m, void* base, int64_t rows, int64
 }
 
 void free_all(cpi_ctx* c) {
-    cudaFree(c->frames_dev);
+    cudaFree(c->frames_dev[0]);
+    cudaFree(c->frames_dev[1]);
+    for (int b = 0; b < 2; ++b) {
+        if (c->ev_loaded[b]) cudaEventDestroy(c->ev_loaded[b]);
+        if (c->ev_consumed[b]) cudaEventDestroy(c->ev_consumed[b]);
+    }
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     cudaFree(c->op_a);
     cudaFree(c->op_b);
     cudaFree(c->s_a);
@@ -281,7 +293,13 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
     const size_t op_elem = c->popc ? 4 : 1;
     cudaError_t e = cudaSuccess;
     auto chk = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
-    chk(cudaMalloc(&c->frames_dev, size_t(c->frame_bytes) * cfg->max_frames));
+    chk(cudaMalloc(&c->frames_dev[0], size_t(c->frame_bytes) * cfg->max_frames));
+    chk(cudaMalloc(&c->frames_dev[1], size_t(c->frame_bytes) * cfg->max_frames));
+    chk(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+        chk(cudaEventCreateWithFlags(&c->ev_loaded[b], cudaEventDisableTiming));
+        chk(cudaEventCreateWithFlags(&c->ev_consumed[b], cudaEventDisableTiming));
+    }
     chk(cudaMalloc(&c->op_a, size_t(c->rows_a) * c->ld_op * op_elem));
     chk(cudaMalloc(&c->op_b, size_t(c->rows_b) * c->ld_op * op_elem));
     chk(cudaMalloc(&c->s_a, sizeof(int32_t) * c->p_a));
@@ -333,11 +351,23 @@ cpi_status cpi_load_frames(cpi_ctx* c, const void* packed, int64_t n, int32_t wh
     CK(c, cudaSetDevice(c->dev));
     auto st = static_cast<cudaStream_t>(stream);
     if (where == CPI_HOST) {
+        // copy into the staging buffer not used by the previous batch, on the internal copy
+        // stream, once the last expand that read this buffer is done; cpi_correlate makes
+        // `stream` wait for the copy.  The copy therefore overlaps the previous batch's GEMM and
+        // refocusing instead of queueing behind them.
+        (void)st;
+        const int b = c->next_buf;
+        c->next_buf ^= 1;
+        if (c->consumed_valid[b]) CK(c, cudaStreamWaitEvent(c->copy_stream, c->ev_consumed[b], 0));
         if (n > 0)
-            CK(c, cudaMemcpyAsync(c->frames_dev, packed, size_t(n) * c->frame_bytes, cudaMemcpyHostToDevice, st));
-        c->frames_cur = c->frames_dev;
+            CK(c, cudaMemcpyAsync(c->frames_dev[b], packed, size_t(n) * c->frame_bytes, cudaMemcpyHostToDevice,
+                                  c->copy_stream));
+        CK(c, cudaEventRecord(c->ev_loaded[b], c->copy_stream));
+        c->frames_cur = c->frames_dev[b];
+        c->cur_buf = b;
     } else {
         c->frames_cur = static_cast<const uint8_t*>(packed);
+        c->cur_buf = -1;
     }
     c->n_cur = n;
     c->loaded = true;
@@ -361,6 +391,7 @@ cpi_status cpi_correlate(cpi_ctx* c, float* gamma, void* stream) {
         TimedScope ts(c, KC_EXPAND, st);
         const cpi::RoiDev ra{c->cfg.roi_a.x0, c->cfg.roi_a.y0, c->cfg.roi_a.width, c->cfg.roi_a.height};
         const cpi::RoiDev rb{c->cfg.roi_b.x0, c->cfg.roi_b.y0, c->cfg.roi_b.width, c->cfg.roi_b.height};
+        if (c->cur_buf >= 0) CK(c, cudaStreamWaitEvent(st, c->ev_loaded[c->cur_buf], 0));
         if (n > 0) {
             cpi::launch_expand(c->frames_cur, n, L.width_px / 8, L.height_px, L.bit_order, ra, c->op_a,
                                c->ld_op, k_pad, c->s_a, c->popc, st);
@@ -368,6 +399,10 @@ cpi_status cpi_correlate(cpi_ctx* c, float* gamma, void* stream) {
                                c->ld_op, k_pad, c->s_b, c->popc, st);
             c->launches += 2;
             CK(c, cudaGetLastError());
+        }
+        if (c->cur_buf >= 0) {
+            CK(c, cudaEventRecord(c->ev_consumed[c->cur_buf], st));
+            c->consumed_valid[c->cur_buf] = true;
         }
     }
     const int64_t n_tot = c->n_tot + n;
