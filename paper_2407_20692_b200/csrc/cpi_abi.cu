@@ -65,6 +65,8 @@ struct cpi_ctx {
     bool refocus_ready = false;
     int fuse = 4;                          // planes per Gamma pass in the TMA stage 1 (CPI_REFOCUS_FUSE)
     uint32_t* xpack = nullptr;             // packed x-tables [kRefocusMaxFuse][W_b][W_a]
+    uint32_t* ypack = nullptr;             // packed y-tables [kRefocusMaxFuse][H_b][H_a]
+    bool use_s2_staged = false;
     cpi::Stage1Maps s1maps{};
     bool use_s1_tma = false;
     // accounting
@@ -196,6 +198,7 @@ void free_all(cpi_ctx* c) {
         cudaFree(c->T[f]);
     }
     cudaFree(c->xpack);
+    cudaFree(c->ypack);
     for (auto& t : c->timed) { c->event_pool.push_back(t.a); c->event_pool.push_back(t.b); }
     for (auto e : c->event_pool) cudaEventDestroy(e);
 }
@@ -536,7 +539,10 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
         if (const char* ev = getenv("CPI_REFOCUS_FUSE")) c->fuse = atoi(ev);
         if (c->fuse < 1) c->fuse = 1;
         if (c->fuse > cpi::kRefocusMaxFuse) c->fuse = cpi::kRefocusMaxFuse;
+        c->use_s2_staged = cpi::stage2_staged_supported(Ha) && getenv("CPI_STAGE2_SIMPLE") == nullptr;
         const int nbuf = c->use_s1_tma ? c->fuse : 1;
+        if (c->use_s2_staged)
+            CK(c, cudaMalloc(&c->ypack, sizeof(uint32_t) * size_t(Ha) * Hb * cpi::kRefocusMaxFuse));
         for (int f = 0; f < nbuf; ++f) {
             cpi_status s = alloc_axis(c, c->xs[f], Wa, Wb);
             if (s == CPI_OK) s = alloc_axis(c, c->ys[f], Ha, Hb);
@@ -595,6 +601,10 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
                 e = cpi::launch_pack_xtable_group(c->xs, nf, Wa, Wb, c->xpack, st);
                 c->launches += 1;
             }
+            if (e == cudaSuccess && c->use_s2_staged) {
+                e = cpi::launch_pack_ytable_group(c->ys, nf, Ha, Hb, c->ypack, st);
+                c->launches += 1;
+            }
             if (e != cudaSuccess) return cuda_fail(c, e, "refocus coords launch");
         }
         {
@@ -612,10 +622,16 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
         {
             TimedScope ts(c, KC_STAGE2, st);
             cudaError_t e = cudaSuccess;
-            for (int f = 0; f < nf && e == cudaSuccess; ++f) {
-                e = cpi::launch_refocus_stage2(c->T[f], Wa, Ha, Hb, m_base, m_count, c->xs[f], c->ys[f],
-                                               planes + int64_t(p0 + f) * Ha * Wa, st);
+            if (c->use_s2_staged) {
+                e = cpi::launch_refocus_stage2_group(c->T, nf, Wa, Ha, Hb, m_base, m_base + m_count, c->xs, c->ys,
+                                                     c->ypack, planes + int64_t(p0) * Ha * Wa, st);
                 c->launches += 1;
+            } else {
+                for (int f = 0; f < nf && e == cudaSuccess; ++f) {
+                    e = cpi::launch_refocus_stage2(c->T[f], Wa, Ha, Hb, m_base, m_count, c->xs[f], c->ys[f],
+                                                   planes + int64_t(p0 + f) * Ha * Wa, st);
+                    c->launches += 1;
+                }
             }
             if (e != cudaSuccess) return cuda_fail(c, e, "refocus stage-2 launch");
         }

@@ -103,5 +103,13 @@ EncodeTiledFn encode_tiled_fn();
 cudaError_t launch_refocus_stage2(const double* T, int Wa, int Ha, int Hb, int m_base,
                                   int m_count, AxisTables xs, AxisTables ys, float* plane,
                                   cudaStream_t st);
+// staged stage 2 (KB6'): one launch for n_fuse planes written to planes[f * Ha * Wa]; rows of
+// T outside [m_lo, m_hi) count as 0.  Needs the packed y-tables [n_fuse][Hb][Ha] (H_a <= 512).
+bool stage2_staged_supported(int Ha);
+cudaError_t launch_pack_ytable_group(const AxisTables* ys, int n_fuse, int Ha, int Hb, uint32_t* ypack,
+                                     cudaStream_t st);
+cudaError_t launch_refocus_stage2_group(double* const* T, int n_fuse, int Wa, int Ha, int Hb, int m_lo, int m_hi,
+                                        const AxisTables* xs, const AxisTables* ys, const uint32_t* ypack,
+                                        float* planes, cudaStream_t st);
 
 }  // namespace cpi

@@ -417,7 +417,158 @@ __global__ void pack_xtable_group_kernel(PackGroupArgs g, int Wa, int Wb, uint32
     }
 }
 
+// ---- KB6 (staged): stage 2 for a fused group of planes -------------------------------
+// grid (ceil(W_a / 2), F); CTA = 2 output columns x of one plane, thread = output row y
+// (H_a <= 256).  The CTA walks v in chunks of 8: it stages T[x][m][v0..v0+7] for every m
+// (64-byte coalesced row segments; rows outside the used band [lo_y(v), hi_y(v)] and outside
+// the caller's row shard [m_lo, m_hi) are stored as 0) transposed to [x][v][m], plus the
+// chunk's packed y-table rows; every thread then gathers its two taps per (x, v) from shared
+// memory.  The next chunk's loads are issued into registers before the current chunk is
+// consumed, so HBM latency overlaps the gathers.  T is read from HBM once per plane.
+constexpr int kS2VC = 8, kS2XB = 2, kS2Threads = 256, kS2MI = 256 / (kS2Threads / kS2VC);
+
+struct S2Args {
+    int Wa, Ha, Hb, m_lo, m_hi;
+    const double* T[kRefocusMaxFuse];
+    const int32_t* xcnt[kRefocusMaxFuse];
+    const int32_t* ycnt[kRefocusMaxFuse];
+    const int32_t* ylo[kRefocusMaxFuse];
+    const int32_t* yhi[kRefocusMaxFuse];
+    const uint32_t* ypack;                       // [F][H_b][H_a]
+    float* plane[kRefocusMaxFuse];
+};
+
+__global__ void __launch_bounds__(kS2Threads)
+stage2_staged_kernel(S2Args a) {
+    extern __shared__ __align__(16) uint8_t s2_smem[];
+    const int f = blockIdx.y, x0 = blockIdx.x * kS2XB;
+    const int Ha = a.Ha, Hb = a.Hb, P = Ha + 2;           // staged row pitch (rows Ha, Ha+1 = 0)
+    double* ts = reinterpret_cast<double*>(s2_smem);                     // [kS2XB][kS2VC][P]
+    uint32_t* tab = reinterpret_cast<uint32_t*>(ts + kS2XB * kS2VC * P);  // [kS2VC][Ha]
+    const double* T = a.T[f];
+    const uint32_t* yp = a.ypack + static_cast<int64_t>(f) * Hb * Ha;
+    const int32_t* ylo = a.ylo[f];
+    const int32_t* yhi = a.yhi[f];
+    for (int i = threadIdx.x; i < kS2XB * kS2VC * 2; i += blockDim.x) ts[(i >> 1) * P + Ha + (i & 1)] = 0.0;
+    // loader role: thread = (vv = tid % 8, m = tid / 8 + 32 k), both x of the CTA
+    const int vl = threadIdx.x & (kS2VC - 1), ml = threadIdx.x / kS2VC;
+    double pre[kS2XB][kS2MI];
+    uint32_t ptab[kS2MI];
+    auto prefetch = [&](int v0) {
+        const int v = v0 + vl, nvalid = min(kS2VC, Hb - v0) * Ha;   // table entries of real v rows
+        int lo = 1, hi = 0;
+        if (v < Hb) { lo = max(__ldg(ylo + v), a.m_lo); hi = min(__ldg(yhi + v), a.m_hi - 1); }
+#pragma unroll
+        for (int k = 0; k < kS2MI; ++k) {
+            const int m = ml + k * (kS2Threads / kS2VC);
+            const bool ok = m >= lo && m <= hi;
+#pragma unroll
+            for (int xb = 0; xb < kS2XB; ++xb) {
+                const int x = x0 + xb;
+                pre[xb][k] = ok && x < a.Wa ? __ldg(T + (static_cast<int64_t>(x) * Ha + m) * Hb + v) : 0.0;
+            }
+            const int i = threadIdx.x + k * kS2Threads;               // table entry (vv, y)
+            ptab[k] = i < nvalid ? __ldg(yp + static_cast<int64_t>(v0) * Ha + i) : (static_cast<uint32_t>(Ha) << 23);
+        }
+    };
+    double sum[kS2XB];
+#pragma unroll
+    for (int xb = 0; xb < kS2XB; ++xb) sum[xb] = 0.0;
+    const int y = threadIdx.x;
+    prefetch(0);
+    for (int v0 = 0; v0 < Hb; v0 += kS2VC) {
+        __syncthreads();                                  // previous chunk consumed
+#pragma unroll
+        for (int k = 0; k < kS2MI; ++k) {
+            const int m = ml + k * (kS2Threads / kS2VC);
+            if (m < Ha) {
+#pragma unroll
+                for (int xb = 0; xb < kS2XB; ++xb) ts[(xb * kS2VC + vl) * P + m] = pre[xb][k];
+            }
+            const int i = threadIdx.x + k * kS2Threads;
+            if (i < kS2VC * Ha) tab[i] = ptab[k];
+        }
+        __syncthreads();
+        if (v0 + kS2VC < Hb) prefetch(v0 + kS2VC);        // in flight while this chunk is gathered
+        if (y < Ha) {
+#pragma unroll
+            for (int vv = 0; vv < kS2VC; ++vv) {
+                const uint32_t e = tab[vv * Ha + y];
+                const int m0 = static_cast<int>(e >> 23);
+                const double t = static_cast<double>(e & 0x7FFFFFu) * (1.0 / 8388608.0);
+                const double w0 = 1.0 - t;
+#pragma unroll
+                for (int xb = 0; xb < kS2XB; ++xb) {
+                    const double* row = ts + (xb * kS2VC + vv) * P + m0;
+                    sum[xb] = fma(t, row[1], fma(w0, row[0], sum[xb]));
+                }
+            }
+        }
+    }
+    if (y < Ha) {
+        const int64_t cy = __ldg(a.ycnt[f] + y);
+#pragma unroll
+        for (int xb = 0; xb < kS2XB; ++xb) {
+            const int x = x0 + xb;
+            if (x >= a.Wa) continue;
+            const int64_t c = cy * __ldg(a.xcnt[f] + x);
+            a.plane[f][static_cast<int64_t>(y) * a.Wa + x] = c ? static_cast<float>(sum[xb] / static_cast<double>(c)) : 0.f;
+        }
+    }
+}
+
+// Packed y-tables of a group: entry(f, v, y) = m0 << 23 | round(t * 2^23); skipped samples
+// point at the zero rows (m0 = H_a, t = 0); a t that rounds to 1 moves to m0 + 1 with t = 0.
+__global__ void pack_ytable_kernel(PackGroupArgs g, int Ha, int Hb, uint32_t* __restrict__ out) {
+    const int v = blockIdx.x, f = blockIdx.y;
+    for (int y = threadIdx.x; y < Ha; y += blockDim.x) {
+        const int64_t idx = static_cast<int64_t>(v) * Ha + y;
+        const int m0 = __ldg(g.i0[f] + idx);
+        uint32_t e = static_cast<uint32_t>(Ha) << 23;
+        if (m0 >= 0) {
+            uint32_t tq = static_cast<uint32_t>(__double2uint_rn(__ldg(g.t[f] + idx) * 8388608.0));
+            int mr = m0;
+            if (tq >= 8388608u) { tq = 0; mr += 1; }
+            e = (static_cast<uint32_t>(mr) << 23) | tq;
+        }
+        out[(static_cast<int64_t>(f) * Hb + v) * Ha + y] = e;
+    }
+}
+
 }  // namespace
+
+bool stage2_staged_supported(int Ha) { return Ha >= 2 && Ha <= kS2Threads; }
+
+cudaError_t launch_pack_ytable_group(const AxisTables* ys, int n_fuse, int Ha, int Hb, uint32_t* ypack,
+                                     cudaStream_t st) {
+    PackGroupArgs g{};
+    g.n = n_fuse;
+    for (int f = 0; f < n_fuse; ++f) { g.i0[f] = ys[f].i0; g.t[f] = ys[f].t; g.lo[f] = ys[f].lo; }
+    pack_ytable_kernel<<<dim3(Hb, n_fuse), Ha >= 256 ? 256 : ((Ha + 31) / 32) * 32, 0, st>>>(g, Ha, Hb, ypack);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_refocus_stage2_group(double* const* T, int n_fuse, int Wa, int Ha, int Hb, int m_lo, int m_hi,
+                                        const AxisTables* xs, const AxisTables* ys, const uint32_t* ypack,
+                                        float* planes, cudaStream_t st) {
+    if (n_fuse < 1 || n_fuse > kRefocusMaxFuse || !stage2_staged_supported(Ha)) return cudaErrorInvalidValue;
+    S2Args a{};
+    a.Wa = Wa; a.Ha = Ha; a.Hb = Hb; a.m_lo = m_lo; a.m_hi = m_hi; a.ypack = ypack;
+    for (int f = 0; f < n_fuse; ++f) {
+        a.T[f] = T[f]; a.xcnt[f] = xs[f].cnt; a.ycnt[f] = ys[f].cnt; a.ylo[f] = ys[f].lo; a.yhi[f] = ys[f].hi;
+        a.plane[f] = planes + static_cast<int64_t>(f) * Ha * Wa;
+    }
+    const size_t smem = sizeof(double) * kS2XB * kS2VC * (Ha + 2) + sizeof(uint32_t) * kS2VC * Ha;
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        cudaError_t e = cudaFuncSetAttribute(stage2_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        attr = smem;
+    }
+    stage2_staged_kernel<<<dim3((Wa + kS2XB - 1) / kS2XB, n_fuse), kS2Threads, smem, st>>>(a);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_refocus_coords(double alpha, int boundary, int W, int Wb, AxisTables tab,
                                   cudaStream_t st) {
