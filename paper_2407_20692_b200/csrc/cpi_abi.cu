@@ -65,7 +65,8 @@ struct cpi_ctx {
     bool refocus_ready = false;
     int fuse = 4;                          // planes per Gamma pass in the TMA stage 1 (CPI_REFOCUS_FUSE)
     uint32_t* xpack = nullptr;             // packed x-tables [kRefocusMaxFuse][W_b][W_a]
-    uint32_t* ypack = nullptr;             // packed y-tables [kRefocusMaxFuse][H_b][H_a]
+    uint32_t* ypack = nullptr;
+    uint32_t* xblk = nullptr;              // x-block masks [kRefocusMaxFuse][W_b / 8]             // packed y-tables [kRefocusMaxFuse][H_b][H_a]
     bool use_s2_staged = false;
     cpi::Stage1Maps s1maps{};
     bool use_s1_tma = false;
@@ -199,6 +200,7 @@ void free_all(cpi_ctx* c) {
     }
     cudaFree(c->xpack);
     cudaFree(c->ypack);
+    cudaFree(c->xblk);
     for (auto& t : c->timed) { c->event_pool.push_back(t.a); c->event_pool.push_back(t.b); }
     for (auto e : c->event_pool) cudaEventDestroy(e);
 }
@@ -552,6 +554,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
         if (c->use_s1_tma) {
             CK(c, cudaMalloc(&c->xpack, sizeof(uint32_t) * size_t(Wa) * Wb * cpi::kRefocusMaxFuse));
             CK(c, cudaMemset(c->xpack, 0, sizeof(uint32_t) * size_t(Wa) * Wb * cpi::kRefocusMaxFuse));
+            CK(c, cudaMalloc(&c->xblk, sizeof(uint32_t) * size_t((Wb + 7) / 8) * cpi::kRefocusMaxFuse));
             cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
             if (!enc) return fail(c, CPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
             const cuuint64_t dims[3] = {cuuint64_t(Wa), cuuint64_t(Wb), cuuint64_t(cpi::kRefocusMaxFuse)};
@@ -598,7 +601,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
                 c->launches += 2;
             }
             if (e == cudaSuccess && tma_now) {
-                e = cpi::launch_pack_xtable_group(c->xs, nf, Wa, Wb, c->xpack, st);
+                e = cpi::launch_pack_xtable_group(c->xs, nf, Wa, Wb, c->xpack, c->xblk, st);
                 c->launches += 1;
             }
             if (e == cudaSuccess && c->use_s2_staged) {
@@ -612,7 +615,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
             cudaError_t e;
             if (tma_now)
                 e = cpi::launch_refocus_stage1_tma(&c->s1maps, nf, Wa, Ha, Wb, Hb, m_base, m_count, c->xs, c->ys,
-                                                   c->T, c->num_sms, st);
+                                                   c->T, c->xblk, c->num_sms, st);
             else
                 e = cpi::launch_refocus_stage1(spec->gamma_dev, c->p_b, Wa, Ha, Wb, Hb, m_base, m_count,
                                                c->xs[0], c->ys[0], c->T[0], st);

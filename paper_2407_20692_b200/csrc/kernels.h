@@ -82,9 +82,10 @@ struct Stage1Maps {
 bool stage1_tma_supported(int Wa, int Wb);
 cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa, int Ha, int Wb, int Hb,
                                       int m_base, int m_count, const AxisTables* xs, const AxisTables* ys,
-                                      double* const* T, int num_sms, cudaStream_t st);
+                                      double* const* T, const uint32_t* xblk, int num_sms, cudaStream_t st);
 // x-tables of a fused group packed for the TMA stage 1: uint32 j_rel << 23 | round(t * 2^23),
-// [n_fuse][Wb][Wa] (see refocus.cu).
+// [n_fuse][Wb][Wa] (see refocus.cu), and xblk[n_fuse][ceil(Wb / 8)]: bit b set if some
+// x in [16 b, 16 b + 16) has a used sample for some u of the 8-column chunk.
 struct PackGroupArgs {
     int n;
     const int32_t* i0[kRefocusMaxFuse];
@@ -92,7 +93,7 @@ struct PackGroupArgs {
     const int32_t* lo[kRefocusMaxFuse];
 };
 cudaError_t launch_pack_xtable_group(const AxisTables* xs, int n_fuse, int Wa, int Wb, uint32_t* xpack,
-                                     cudaStream_t st);
+                                     uint32_t* xblk, cudaStream_t st);
 // driver entry point cuTensorMapEncodeTiled (nullptr if unavailable)
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,

@@ -17,6 +17,7 @@
 // stages 8-column (u) slabs of the rows j it needs into padded shared memory (odd word
 // stride -> conflict-free gathers), and each thread owns one output x.
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -201,13 +202,50 @@ constexpr int kTMaxChunks = 64;                        // W_b <= 512
 constexpr int kTConsumers = 8;
 constexpr int kTThreads = 32 * (kTConsumers + 1);
 
+// packed fp32 pairs for FFMA2 (sm_100a fma.rn.f32x2): lo = first, hi = second
+__device__ __forceinline__ uint64_t pack_f32x2(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float unpack_f32x2(uint64_t v, int hi) {
+    float lo_f, hi_f;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo_f), "=f"(hi_f) : "l"(v));
+    return hi ? hi_f : lo_f;
+}
+// d = (w, w) * g + c on both halves; w2 is the pre-packed broadcast of w
+__device__ __forceinline__ uint64_t ffma2(float, uint64_t g, uint64_t c, uint64_t w2) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(w2), "l"(g), "l"(c));
+    return d;
+}
+
+// The 8 taps of one packed x-table entry for one lane: 4 v slots x 2 corners, as FFMA2 pairs
+// (lane-wise identical to scalar fmaf in the same order).  entry = j_rel << 23 | round(t * 2^23),
+// j_rel = smem row of j0 relative to the chunk's staged span (256 = zero rows: skipped, t = 0).
+__device__ __forceinline__ void s1_taps(uint64_t (&part)[2], uint32_t e, const float* Gu, const int (&voff)[4]) {
+    const float one_t = __int_as_float((e & 0x7FFFFFu) | 0x3F800000u);   // 1 + t
+    const float t = one_t - 1.f;
+    const float w0 = 2.f - one_t;
+    const float* gp = Gu + (e >> 23) * kTRow;
+    const uint64_t t2 = pack_f32x2(t, t), w2 = pack_f32x2(w0, w0);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const uint64_t g0 = pack_f32x2(gp[voff[2 * p]], gp[voff[2 * p + 1]]);
+        const uint64_t g1 = pack_f32x2(gp[voff[2 * p] + kTRow], gp[voff[2 * p + 1] + kTRow]);
+        part[p] = ffma2(t, g1, ffma2(w0, g0, part[p], w2), t2);
+    }
+}
+
 template <int F>
 struct S1Cfg {
     static constexpr int kStages = F == 1 ? 3 : 2;
-    // smem map (bytes): [Gamma stages (258 rows each)][x-table stages x F][span table][barriers]
+    // smem map (bytes): [Gamma stages (258 rows each)][x-table stages x F][span table]
+    //                   [x-block masks][barriers]
     static constexpr int kOffX = kStages * kTGFloats * 4;
     static constexpr int kOffSpan = kOffX + kStages * F * kTXEntries * 4;
-    static constexpr int kOffBar = kOffSpan + kTMaxChunks * 8;
+    static constexpr int kOffXblk = kOffSpan + kTMaxChunks * 8;
+    static constexpr int kOffBar = kOffXblk + kTMaxChunks * 4;
     static constexpr int kSmem = kOffBar + 4 * kStages * 8 + 64;
 };
 
@@ -218,6 +256,7 @@ struct S1Args {
     const int32_t* ylo[kRefocusMaxFuse];
     const int32_t* yhi[kRefocusMaxFuse];
     double* T[kRefocusMaxFuse];
+    const uint32_t* xblk;                    // [F][n_chunks] x-block masks (OR-ed over F in smem)
 };
 
 template <int F>
@@ -231,7 +270,7 @@ __device__ __forceinline__ unsigned tile_mask(const S1Args& a, int m, int v0, in
     return need;
 }
 
-template <bool kFullX, int F>
+template <bool kFullX, int F, bool kSkip>
 __global__ void __launch_bounds__(kTThreads, 1)
 stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_x, S1Args a) {
     using C = S1Cfg<F>;
@@ -264,6 +303,13 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                 hi = max(hi, __ldg(a.xhi[f] + c * kTUC + k));
             }
         span[c] = make_int2(lo, hi);
+    }
+    uint32_t* xblk = reinterpret_cast<uint32_t*>(s1_smem + C::kOffXblk);
+    for (int c = threadIdx.x; c < a.n_chunks; c += blockDim.x) {   // OR over the group's planes
+        uint32_t b = 0;
+#pragma unroll
+        for (int f = 0; f < F; ++f) b |= __ldg(a.xblk + f * a.n_chunks + c);
+        xblk[c] = b;
     }
     __syncthreads();
     const int n_tiles = a.m_count * a.n_vg;
@@ -327,38 +373,42 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
             if (sp.y < sp.x) continue;
             mbar_wait(&full[stage], phase);
             const float* G = sg + stage * kTGFloats;
-            float part[F][2][4];
+            // fp32 partial sums of this chunk as packed pairs (slots s = 2p, 2p + 1): the taps run
+            // on FFMA2 (fma.rn.f32x2), lane-wise identical to two scalar fmaf in the same order
+            uint64_t part[F][2][2];
 #pragma unroll
             for (int f = 0; f < F; ++f)
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
 #pragma unroll
-                    for (int s = 0; s < 4; ++s) part[f][i][s] = 0.f;
+                    for (int p = 0; p < 2; ++p) part[f][i][p] = 0ull;
+            const uint32_t* sxs = sx + stage * F * kTXEntries + xbase;
+            if constexpr (kSkip) {
+                // i-outer order with a warp-uniform skip of a 16-wide x block that has no used
+                // sample in this chunk for any plane of the group
+                const uint32_t xb = xblk[c] >> warp;
 #pragma unroll
-            for (int k = 0; k < kTUC; ++k) {
-                const int uu = (k + xl) & (kTUC - 1);
-                const float* Gu = G + uu;
+                for (int i = 0; i < 2; ++i) {
+                    if (!((xb >> (8 * i)) & 1u)) continue;
+                    if (!kFullX && xbase + 128 * i >= a.Wa) continue;
 #pragma unroll
-                for (int f = 0; f < F; ++f) {
-                    const int xrow = (stage * F + f) * kTXEntries + uu * a.Wa + xbase;
+                    for (int k = 0; k < kTUC; ++k) {
+                        const int uu = (k + xl) & (kTUC - 1);
 #pragma unroll
-                    for (int i = 0; i < 2; ++i) {
-                        if (kFullX || xbase + 128 * i < a.Wa) {
-                            // entry = j_rel << 23 | round(t * 2^23), j_rel = smem row of j0 relative
-                            // to the chunk's staged span (256 = zero rows: skipped sample, t = 0)
-                            const uint32_t e = sx[xrow + 128 * i];
-                            const float one_t = __int_as_float((e & 0x7FFFFFu) | 0x3F800000u);   // 1 + t
-                            const float t = one_t - 1.f;
-                            const float w0 = 2.f - one_t;
-                            const float* gp = Gu + (e >> 23) * kTRow;
-#pragma unroll
-                            for (int s = 0; s < 4; ++s) {
-                                const float g0 = gp[voff[s]];
-                                const float g1 = gp[voff[s] + kTRow];
-                                part[f][i][s] = fmaf(t, g1, fmaf(w0, g0, part[f][i][s]));
-                            }
-                        }
+                        for (int f = 0; f < F; ++f)
+                            s1_taps(part[f][i], sxs[f * kTXEntries + uu * a.Wa + 128 * i], G + uu, voff);
                     }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < kTUC; ++k) {
+                    const int uu = (k + xl) & (kTUC - 1);
+#pragma unroll
+                    for (int f = 0; f < F; ++f)
+#pragma unroll
+                        for (int i = 0; i < 2; ++i)
+                            if (kFullX || xbase + 128 * i < a.Wa)
+                                s1_taps(part[f][i], sxs[f * kTXEntries + uu * a.Wa + 128 * i], G + uu, voff);
                 }
             }
             // Release the stage to the TMA producer.  The reads above are generic-proxy loads and
@@ -372,7 +422,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
 #pragma unroll
-                    for (int s = 0; s < 4; ++s) acc[f][i][s] += static_cast<double>(part[f][i][s]);
+                    for (int s = 0; s < 4; ++s) acc[f][i][s] += static_cast<double>(unpack_f32x2(part[f][i][s >> 1], s & 1));
             if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
 #pragma unroll
@@ -397,24 +447,34 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
 // staged union span (the same union the producer stages), t in [0, 1) (a t that rounds to
 // 1 moves to the next row with t = 0), and skipped samples point at the zero rows
 // (j_rel = 256, t = 0).  t keeps 2^-23 resolution; t = 0 stays exact.
-__global__ void pack_xtable_group_kernel(PackGroupArgs g, int Wa, int Wb, uint32_t* __restrict__ out) {
-    const int u = blockIdx.x, f = blockIdx.y;
-    const int c0 = (u / 8) * 8;
+__global__ void pack_xtable_group_kernel(PackGroupArgs g, int Wa, int Wb, uint32_t* __restrict__ out,
+                                         uint32_t* __restrict__ xblk) {
+    const int c = blockIdx.x, f = blockIdx.y, c0 = c * 8, n_chunks = gridDim.x;
+    __shared__ uint32_t sblk;
+    if (threadIdx.x == 0) sblk = 0;
     int jlo = INT_MAX;
     for (int ff = 0; ff < g.n; ++ff)
         for (int k = c0; k < c0 + 8 && k < Wb; ++k) jlo = min(jlo, __ldg(g.lo[ff] + k));
+    __syncthreads();
     for (int x = threadIdx.x; x < Wa; x += blockDim.x) {
-        const int64_t idx = static_cast<int64_t>(u) * Wa + x;
-        const int j = __ldg(g.i0[f] + idx);
-        uint32_t e = 256u << 23;
-        if (j >= 0) {
-            uint32_t tq = static_cast<uint32_t>(__double2uint_rn(__ldg(g.t[f] + idx) * 8388608.0));
-            int jr = j - jlo;
-            if (tq >= 8388608u) { tq = 0; jr += 1; }
-            e = (static_cast<uint32_t>(jr) << 23) | tq;
+        bool used = false;
+        for (int u = c0; u < c0 + 8 && u < Wb; ++u) {
+            const int64_t idx = static_cast<int64_t>(u) * Wa + x;
+            const int j = __ldg(g.i0[f] + idx);
+            uint32_t e = 256u << 23;
+            if (j >= 0) {
+                uint32_t tq = static_cast<uint32_t>(__double2uint_rn(__ldg(g.t[f] + idx) * 8388608.0));
+                int jr = j - jlo;
+                if (tq >= 8388608u) { tq = 0; jr += 1; }
+                e = (static_cast<uint32_t>(jr) << 23) | tq;
+                used = true;
+            }
+            out[(static_cast<int64_t>(f) * Wb + u) * Wa + x] = e;
         }
-        out[(static_cast<int64_t>(f) * Wb + u) * Wa + x] = e;
+        if (used) atomicOr(&sblk, 1u << (x >> 4));
     }
+    __syncthreads();
+    if (threadIdx.x == 0) xblk[f * n_chunks + c] = sblk;
 }
 
 // ---- KB6 (staged): stage 2 for a fused group of planes -------------------------------
@@ -598,51 +658,56 @@ cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int H
 bool stage1_tma_supported(int Wa, int Wb) { return Wa <= 256 && Wa >= 2 && (Wb % 4) == 0 && Wb <= 8 * kTMaxChunks; }
 
 cudaError_t launch_pack_xtable_group(const AxisTables* xs, int n_fuse, int Wa, int Wb, uint32_t* xpack,
-                                     cudaStream_t st) {
+                                     uint32_t* xblk, cudaStream_t st) {
     PackGroupArgs g{};
     g.n = n_fuse;
     for (int f = 0; f < n_fuse; ++f) { g.i0[f] = xs[f].i0; g.t[f] = xs[f].t; g.lo[f] = xs[f].lo; }
-    pack_xtable_group_kernel<<<dim3(Wb, n_fuse), Wa >= 256 ? 256 : ((Wa + 31) / 32) * 32, 0, st>>>(g, Wa, Wb, xpack);
+    pack_xtable_group_kernel<<<dim3((Wb + 7) / 8, n_fuse), Wa >= 256 ? 256 : ((Wa + 31) / 32) * 32, 0, st>>>(
+        g, Wa, Wb, xpack, xblk);
     return cudaGetLastError();
 }
 
-template <bool kFullX, int F>
+template <bool kFullX, int F, bool kSkip>
 static cudaError_t launch_s1(const Stage1Maps* maps, const S1Args& a, int grid, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(stage1_tma_kernel<kFullX, F>,
+        cudaError_t e = cudaFuncSetAttribute(stage1_tma_kernel<kFullX, F, kSkip>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, S1Cfg<F>::kSmem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    stage1_tma_kernel<kFullX, F><<<grid, kTThreads, S1Cfg<F>::kSmem, st>>>(maps->gamma, maps->xtab, a);
+    stage1_tma_kernel<kFullX, F, kSkip><<<grid, kTThreads, S1Cfg<F>::kSmem, st>>>(maps->gamma, maps->xtab, a);
     return cudaGetLastError();
 }
 
-template <bool kFullX>
+template <bool kFullX, bool kSkip>
 static cudaError_t launch_s1_f(int F, const Stage1Maps* maps, const S1Args& a, int grid, cudaStream_t st) {
     switch (F) {
-        case 1: return launch_s1<kFullX, 1>(maps, a, grid, st);
-        case 2: return launch_s1<kFullX, 2>(maps, a, grid, st);
-        case 3: return launch_s1<kFullX, 3>(maps, a, grid, st);
-        default: return launch_s1<kFullX, 4>(maps, a, grid, st);
+        case 1: return launch_s1<kFullX, 1, kSkip>(maps, a, grid, st);
+        case 2: return launch_s1<kFullX, 2, kSkip>(maps, a, grid, st);
+        case 3: return launch_s1<kFullX, 3, kSkip>(maps, a, grid, st);
+        default: return launch_s1<kFullX, 4, kSkip>(maps, a, grid, st);
     }
 }
 
 cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa, int Ha, int Wb, int Hb,
                                       int m_base, int m_count, const AxisTables* xs, const AxisTables* ys,
-                                      double* const* T, int num_sms, cudaStream_t st) {
+                                      double* const* T, const uint32_t* xblk, int num_sms, cudaStream_t st) {
     if (n_fuse < 1 || n_fuse > kRefocusMaxFuse) return cudaErrorInvalidValue;
     S1Args a{};
     a.Wa = Wa; a.Ha = Ha; a.Wb = Wb; a.Hb = Hb; a.m_base = m_base; a.m_count = m_count;
     a.n_vg = (Hb + kTVG - 1) / kTVG;
     a.n_chunks = (Wb + kTUC - 1) / kTUC;
+    a.xblk = xblk;
     for (int f = 0; f < n_fuse; ++f) {
         a.xlo[f] = xs[f].lo; a.xhi[f] = xs[f].hi; a.ylo[f] = ys[f].lo; a.yhi[f] = ys[f].hi; a.T[f] = T[f];
     }
     const int tiles = m_count * a.n_vg;
     const int grid = tiles < num_sms ? tiles : num_sms;
-    return Wa == 256 ? launch_s1_f<true>(n_fuse, maps, a, grid, st) : launch_s1_f<false>(n_fuse, maps, a, grid, st);
+    static const bool skip = getenv("CPI_S1_NOSKIP") == nullptr;   // A/B knob for the x-block skip
+    if (skip)
+        return Wa == 256 ? launch_s1_f<true, true>(n_fuse, maps, a, grid, st) : launch_s1_f<false, true>(n_fuse, maps, a, grid, st);
+    return Wa == 256 ? launch_s1_f<true, false>(n_fuse, maps, a, grid, st) : launch_s1_f<false, false>(n_fuse, maps, a, grid, st);
 }
 
 cudaError_t launch_refocus_stage2(const double* T, int Wa, int Ha, int Hb, int m_base, int m_count,
