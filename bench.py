@@ -13,8 +13,9 @@ the two kernels' roofline fractions alongside.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cb200|reference]
 Multi-GPU: launched by torch.distributed.run; frames shard across ranks (weak scaling:
-10^4 frames per rank), NCCL all-reduce + reduce-scatter of the sums, refocus of each
-rank's Gamma rows, all-reduce of the planes (paper_2407_20692_b200.parallel).
+10^4 frames per rank); the pair-sum GEMM runs in row panels whose NCCL reduce-scatter starts
+as each panel finishes (overlapping the next panels), Gamma rows are owned block-cyclically,
+each rank refocuses its rows and the planes are all-reduced (paper_2407_20692_b200.parallel).
 """
 from __future__ import annotations
 
@@ -281,41 +282,28 @@ def main():
     frames_dev = frames_host.to(dev)
     stream = torch.cuda.current_stream(dev)
 
-    keep = world > 1
-    ctx = Context(roi_a, roi_b, n, device=local, variant=args.variant, keep_counts=keep)
-    gamma = ctx.new_gamma() if world == 1 else None
-    planes = ctx.new_planes(args.planes)
-    planes_host = torch.empty(planes.shape, dtype=torch.float32).pin_memory()
-    if world > 1:
-        row0, rows = parallel.row_shard(Wa, Ha, rank, world)
-        s_ab = torch.empty((p_a, p_b), dtype=torch.int32, device=dev)
-        s_a = torch.empty(p_a, dtype=torch.int32, device=dev)
-        s_b = torch.empty(p_b, dtype=torch.int32, device=dev)
-        gamma_rows = torch.empty((rows, p_b), dtype=torch.float32, device=dev)
-        marg = torch.empty(p_a + p_b + 1, dtype=torch.int64, device=dev)
-        s_ab_rows = torch.empty((rows, p_b), dtype=torch.int32, device=dev)
+    if world == 1:
+        ctx = Context(roi_a, roi_b, n, device=local, variant=args.variant)
+        gamma = ctx.new_gamma()
+        planes = ctx.new_planes(args.planes)
+    else:
+        # frame-sharded pipeline (parallel.py): GEMM row panels reduce-scattered as they finish,
+        # block-cyclic Gamma row ownership, shard refocus, plane all-reduce
+        backend = parallel.CudaBackend(roi_a, roi_b, n, device=local, variant=args.variant)
+        ctx = backend.ctx
+    planes_host = torch.empty((args.planes, Ha, Wa), dtype=torch.float32).pin_memory()
 
     def step(src):
-        """one pass of a1..a6; src = device frames (resident) or pinned host frames (e2e)"""
+        """one pass of a1..a6; src = device frames (resident) or pinned host frames (e2e);
+        returns the plane stack"""
         if world == 1:
             ctx.reset()          # a new acquisition: zero S_a, S_b, N (memsets)
             ctx.load_frames(src)
             ctx.correlate(gamma)
             ctx.refocus(alphas, gamma, planes)
-            return
-        ctx.reset()
-        ctx.load_frames(src)
-        ctx.correlate(None)
-        ctx.get_counts(s_ab, s_a, s_b)
-        marg[:p_a].copy_(s_a)
-        marg[p_a:p_a + p_b].copy_(s_b)
-        marg[-1].fill_(n)
-        dist.all_reduce(marg)
-        dist.reduce_scatter_tensor(s_ab_rows, s_ab)
-        ctx.finalize_counts(s_ab_rows, row0, marg[:p_a].to(torch.int32), marg[p_a:p_a + p_b].to(torch.int32),
-                            n * world, gamma_rows)
-        ctx.refocus(alphas, gamma_rows, planes, row0=row0, rows=rows)
-        dist.all_reduce(planes)
+            return planes
+        res = parallel.correlate_and_refocus(backend, src, roi_a, roi_b, alphas)
+        return res.planes
 
     def barrier():
         if world > 1:
@@ -356,15 +344,13 @@ def main():
     e2e = None
     if not args.no_e2e:
         for _ in range(1):
-            step(frames_host)
-            planes_host.copy_(planes, non_blocking=True)
+            planes_host.copy_(step(frames_host), non_blocking=True)
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            step(frames_host)
-            planes_host.copy_(planes, non_blocking=True)
+            planes_host.copy_(step(frames_host), non_blocking=True)
         e1.record(stream)
         barrier()
         te = e0.elapsed_time(e1)
@@ -373,7 +359,7 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
         e2e = {"value": n * world / (te / args.steps / 1e3), "unit": "frames/s",
-               "h2d_bytes_per_step": int(frames_np.nbytes), "d2h_bytes_per_step": int(planes.numel() * 4),
+               "h2d_bytes_per_step": int(frames_np.nbytes), "d2h_bytes_per_step": int(planes_host.numel() * 4),
                "ms_per_step": te / args.steps}
 
     if rank != 0:

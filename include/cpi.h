@@ -98,6 +98,13 @@ typedef struct {
                                leading dimension P_b (e.g. cpi_correlate's output) */
     int64_t row0, rows;     /* multiples of roi_a.width; a single GPU passes 0, P_a.  A row
                                shard yields that shard's additive share of every plane. */
+    int32_t row_block;      /* A-row layout of the shard (SURVEY §8(e) load balance): the
+                               shard's local A-row l is global A-row
+                                 m(l) = row0/W_a + (l / row_block) * row_stride + l % row_block,
+                               i.e. blocks of row_block consecutive A-rows every row_stride
+                               A-rows (block-cyclic ownership).  row_block <= 0: contiguous
+                               (m(l) = row0/W_a + l).  Needs row_stride >= row_block. */
+    int32_t row_stride;
 } cpi_refocus_spec;
 
 typedef struct cpi_ctx cpi_ctx;   /* opaque, owned by the library */
@@ -142,6 +149,29 @@ cpi_status cpi_load_frames(cpi_ctx *ctx, const void *packed, int64_t n_frames, i
  * Errors: STATE (nothing loaded; second batch without KEEP_COUNTS; no output at all),
  * CUDA. */
 cpi_status cpi_correlate(cpi_ctx *ctx, float *gamma_dev, void *stream);
+
+/* Row panel of cpi_correlate, for pipelining the multi-GPU reduction with the GEMM (SURVEY
+ * §8(e): "panelise the GEMM over p_a row blocks and launch each panel's RS as soon as it is
+ * done"): the same accumulation restricted to A pixels [row0, row0 + rows):
+ *   S_ab[p][q] += sum_i A^i_p B^i_q  for row0 <= p < row0 + rows  (+ Gamma rows if gamma_dev)
+ * The first cpi_correlate_rows of a loaded batch also expands it and adds its S_a, S_b and
+ * N_TOT (so Gamma rows use the totals including this batch); later calls on the same batch
+ * only run the GEMM.  The caller must cover every row exactly once per batch; rows not
+ * covered miss that batch's pair sums.  gamma_dev, if non-NULL, is the full [P_a][P_b]
+ * buffer (only the panel's rows are written).  row0 must be a multiple of
+ * cpi_row_align(ctx); rows too unless row0 + rows == P_a.
+ * Errors: STATE (nothing loaded; batch already consumed by cpi_correlate; no output),
+ * INVALID_ARG (range / alignment), CUDA. */
+cpi_status cpi_correlate_rows(cpi_ctx *ctx, int64_t row0, int64_t rows, float *gamma_dev, void *stream);
+
+/* Row alignment (A pixels) of cpi_correlate_rows panels for this context's GEMM variant. */
+int64_t cpi_row_align(const cpi_ctx *ctx);
+
+/* Borrow the device pointers of the accumulated sums (valid until cpi_destroy; contents
+ * change with every correlate / reset): s_ab int32 [P_a][P_b] (NULL without
+ * CPI_KEEP_COUNTS), s_a int32 [P_a], s_b int32 [P_b].  Lets a caller run collectives on the
+ * library's buffers without copies.  Any out pointer may be NULL.  Errors: INVALID_ARG. */
+cpi_status cpi_counts_dev(cpi_ctx *ctx, int32_t **s_ab, int32_t **s_a, int32_t **s_b);
 
 /* Gamma of Eq. (1) from the accumulated sums:
  *   Gamma[p][q] = (N*S_ab[p][q] - S_a[p]*S_b[q]) / N^2   (= (1/N) S_ab - (S_a/N)(S_b/N))

@@ -25,7 +25,7 @@ KC_GEMM, KC_EXPAND, KC_STAGE1, KC_STAGE2, KC_FINALIZE, KC_COORDS = range(6)
 EXPORTS = ["cpi_create", "cpi_destroy", "cpi_last_error", "cpi_status_string", "cpi_load_frames",
            "cpi_correlate", "cpi_finalize", "cpi_finalize_counts", "cpi_get_counts", "cpi_reset",
            "cpi_refocus", "cpi_launch_count", "cpi_set_timing", "cpi_kernel_time_ms",
-           "cpi_abi_version"]
+           "cpi_abi_version", "cpi_correlate_rows", "cpi_row_align", "cpi_counts_dev"]
 
 
 class CpiError(RuntimeError):
@@ -53,7 +53,8 @@ class Config(ctypes.Structure):
 class RefocusSpec(ctypes.Structure):
     _fields_ = [("alphas", ctypes.POINTER(ctypes.c_double)), ("n_planes", ctypes.c_int32),
                 ("boundary", ctypes.c_int32), ("gamma_dev", ctypes.c_void_p),
-                ("row0", ctypes.c_int64), ("rows", ctypes.c_int64)]
+                ("row0", ctypes.c_int64), ("rows", ctypes.c_int64),
+                ("row_block", ctypes.c_int32), ("row_stride", ctypes.c_int32)]
 
 
 _lib = None
@@ -93,6 +94,9 @@ def load():
         "cpi_set_timing": ([P, i32], i32),
         "cpi_kernel_time_ms": ([P, i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)], i32),
         "cpi_abi_version": ([], i32),
+        "cpi_correlate_rows": ([P, i64, i64, P, P], i32),
+        "cpi_row_align": ([P], i64),
+        "cpi_counts_dev": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)

@@ -118,6 +118,39 @@ class Context:
         self._check(self._lib.cpi_correlate(self._h, self._ptr(gamma), self._stream(stream)))
         return gamma
 
+    def correlate_rows(self, row0: int, rows: int, gamma=None, stream=None):
+        """cpi_correlate_rows: the loaded batch's pair sums for A pixels [row0, row0+rows)
+        (the first call of a batch also expands it and adds S_a, S_b, N)."""
+        if gamma is not None:
+            self._check_gamma(gamma)
+        self._check(self._lib.cpi_correlate_rows(self._h, int(row0), int(rows), self._ptr(gamma),
+                                                 self._stream(stream)))
+        return gamma
+
+    def row_align(self) -> int:
+        """cpi_row_align: A-pixel alignment of correlate_rows panels."""
+        return int(self._lib.cpi_row_align(self._h))
+
+    def counts_views(self):
+        """cpi_counts_dev as torch tensors viewing the library's buffers (no copy):
+        (s_ab [P_a][P_b] or None, s_a [P_a], s_b [P_b]), int32, valid until close()."""
+        torch = _torch()
+        pab, pa, pb = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        self._check(self._lib.cpi_counts_dev(self._h, ctypes.byref(pab), ctypes.byref(pa), ctypes.byref(pb)))
+
+        def view(ptr, shape):
+            if not ptr.value:
+                return None
+            n = int(np.prod(shape))
+
+            class _Arr:   # __cuda_array_interface__ wrapper of a borrowed device pointer
+                __cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<i4", "data": (ptr.value, False),
+                                            "version": 3, "strides": None}
+            t = torch.as_tensor(_Arr(), device=f"cuda:{self.device}")
+            assert t.numel() == n and t.data_ptr() == ptr.value
+            return t
+        return view(pab, (self.p_a, self.p_b)), view(pa, (self.p_a,)), view(pb, (self.p_b,))
+
     def finalize(self, gamma=None, stream=None) -> int:
         """cpi_finalize: Gamma from the accumulated sums; returns N_TOT."""
         if gamma is not None:
@@ -145,14 +178,15 @@ class Context:
         self._check(self._lib.cpi_reset(self._h, self._stream(stream)))
 
     def refocus(self, alphas: Sequence[float], gamma, planes, row0: int = 0, rows: Optional[int] = None,
-                boundary: int = _lib.CPI_SKIP_RENORMALIZE, stream=None):
-        """cpi_refocus: planes [n_planes][H_a][W_a] fp32 from Gamma rows [row0, row0+rows)
-        (gamma points at row row0, leading dimension P_b)."""
+                boundary: int = _lib.CPI_SKIP_RENORMALIZE, row_block: int = 0, row_stride: int = 0, stream=None):
+        """cpi_refocus: planes [n_planes][H_a][W_a] fp32 from a Gamma row shard of `rows` pixel
+        rows (leading dimension P_b) starting at A row row0 / W_a; row_block > 0 makes the
+        shard block-cyclic (local A row l -> row0/W_a + (l // row_block) * row_stride + l % row_block)."""
         al = np.ascontiguousarray(alphas, dtype=np.float64).ravel()
         if rows is None:
             rows = self.p_a - row0
         spec = _lib.RefocusSpec(al.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), al.size, int(boundary),
-                                self._ptr(gamma), int(row0), int(rows))
+                                self._ptr(gamma), int(row0), int(rows), int(row_block), int(row_stride))
         self._check(self._lib.cpi_refocus(self._h, ctypes.byref(spec), self._ptr(planes), self._stream(stream)))
         return planes
 

@@ -181,6 +181,19 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* m,
         "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_addr(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_2sm_hint(void* dst, const CUtensorMap* m, uint64_t* bar,
+                                                     int32_t c0, int32_t c1, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_addr(bar)), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ void tmem_alloc_2sm(uint32_t* slot, uint32_t ncols) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
                  "r"(ncols)
@@ -276,7 +289,7 @@ __device__ __forceinline__ float gamma_entry(int32_t s, int32_t sa, int32_t sb, 
 // Epilogue of one 32-column chunk of one accumulator row (thread = row): optional int32
 // counts (with accumulation of the previous batches) and Gamma.  r[] holds the TMEM values;
 // sbs points at the chunk's 32 S_b values in shared memory.
-template <bool kSmall>
+template <bool kSmall, bool kStream = false>
 __device__ __forceinline__ void epilogue_chunk_vec(uint32_t (&r)[32], int32_t* cp, int accumulate,
                                                    float* gp, const int32_t* sbs, int32_t sa,
                                                    const GammaScale& gs) {
@@ -301,7 +314,10 @@ __device__ __forceinline__ void epilogue_chunk_vec(uint32_t (&r)[32], int32_t* c
             g.y = gamma_entry_t<kSmall>(int(r[e + 1]), sa, sb.y, gs);
             g.z = gamma_entry_t<kSmall>(int(r[e + 2]), sa, sb.z, gs);
             g.w = gamma_entry_t<kSmall>(int(r[e + 3]), sa, sb.w, gs);
-            *reinterpret_cast<float4*>(gp + e) = g;
+            if (kStream)
+                __stcs(reinterpret_cast<float4*>(gp + e), g);   // evict-first: keep L2 for operands
+            else
+                *reinterpret_cast<float4*>(gp + e) = g;
         }
     }
 }

@@ -50,6 +50,11 @@ struct cpi_ctx {
     const uint8_t* frames_cur = nullptr;
     int64_t n_cur = 0;
     bool loaded = false;
+    bool expanded = false;                 // the loaded batch is expanded (cpi_correlate_rows)
+    bool consumed = false;                 // the loaded batch went through cpi_correlate
+    int accumulate = 0;                    // the loaded batch adds to earlier batches' counts
+    int64_t gemm_batches = 0;              // batches with frames since the last reset
+    bool counts_stale = true;              // kept counts not yet written since the last reset (zero on read)
     void* op_a = nullptr;
     void* op_b = nullptr;
     int32_t* s_a = nullptr;
@@ -65,8 +70,8 @@ struct cpi_ctx {
     bool refocus_ready = false;
     int fuse = 4;                          // planes per Gamma pass in the TMA stage 1 (CPI_REFOCUS_FUSE)
     uint32_t* xpack = nullptr;             // packed x-tables [kRefocusMaxFuse][W_b][W_a]
-    uint32_t* ypack = nullptr;
-    uint32_t* xblk = nullptr;              // x-block masks [kRefocusMaxFuse][W_b / 8]             // packed y-tables [kRefocusMaxFuse][H_b][H_a]
+    uint32_t* ypack = nullptr;             // packed y-tables [kRefocusMaxFuse][H_b][H_a]
+    uint32_t* xblk = nullptr;              // x-block masks [kRefocusMaxFuse][W_b / 8]
     bool use_s2_staged = false;
     cpi::Stage1Maps s1maps{};
     bool use_s1_tma = false;
@@ -218,7 +223,7 @@ cpi_status alloc_axis(cpi_ctx* c, cpi::AxisTables& t, int W, int Wb) {
 
 extern "C" {
 
-int32_t cpi_abi_version(void) { return 100; }
+int32_t cpi_abi_version(void) { return 101; }
 
 const char* cpi_status_string(cpi_status s) {
     switch (s) {
@@ -376,12 +381,110 @@ cpi_status cpi_load_frames(cpi_ctx* c, const void* packed, int64_t n, int32_t wh
     }
     c->n_cur = n;
     c->loaded = true;
+    c->expanded = false;
+    c->consumed = false;
     return CPI_OK;
+}
+
+namespace {
+
+// KB1 for the loaded batch: expand both RoIs into the K-major operands and add the batch's
+// single-pixel sums and frame count to the totals.
+cpi_status expand_batch(cpi_ctx* c, cudaStream_t st) {
+    const int64_t n = c->n_cur;
+    const cpi_layout& L = c->cfg.layout;
+    const int64_t k_pad = round_up(n, kKAlign);
+    TimedScope ts(c, KC_EXPAND, st);
+    const cpi::RoiDev ra{c->cfg.roi_a.x0, c->cfg.roi_a.y0, c->cfg.roi_a.width, c->cfg.roi_a.height};
+    const cpi::RoiDev rb{c->cfg.roi_b.x0, c->cfg.roi_b.y0, c->cfg.roi_b.width, c->cfg.roi_b.height};
+    if (c->cur_buf >= 0) CK(c, cudaStreamWaitEvent(st, c->ev_loaded[c->cur_buf], 0));
+    if (n > 0) {
+        cpi::launch_expand(c->frames_cur, n, L.width_px / 8, L.height_px, L.bit_order, ra, c->op_a,
+                           c->ld_op, k_pad, c->s_a, c->popc, st);
+        cpi::launch_expand(c->frames_cur, n, L.width_px / 8, L.height_px, L.bit_order, rb, c->op_b,
+                           c->ld_op, k_pad, c->s_b, c->popc, st);
+        c->launches += 2;
+        CK(c, cudaGetLastError());
+    }
+    if (c->cur_buf >= 0) {
+        CK(c, cudaEventRecord(c->ev_consumed[c->cur_buf], st));
+        c->consumed_valid[c->cur_buf] = true;
+    }
+    // the first batch with frames overwrites the kept counts (no memset after cpi_reset)
+    c->accumulate = c->gemm_batches > 0 ? 1 : 0;
+    if (n > 0) { c->gemm_batches += 1; c->counts_stale = false; }
+    c->n_tot += n;
+    c->batches += 1;
+    c->expanded = true;
+    return CPI_OK;
+}
+
+// Kept counts read before any batch wrote them are zero.
+cpi_status ensure_counts(cpi_ctx* c, cudaStream_t st) {
+    if (c->keep && c->counts_stale) {
+        CK(c, cudaMemsetAsync(c->counts, 0, sizeof(int32_t) * size_t(c->p_a) * c->p_b, st));
+        c->counts_stale = false;
+    }
+    return CPI_OK;
+}
+
+// Pair-sum GEMM (+ fused Gamma) over A pixel rows [row0, row0 + rows) of the expanded batch.
+cpi_status gemm_rows(cpi_ctx* c, int64_t row0, int64_t rows, float* gamma, cudaStream_t st) {
+    const int64_t k_pad = round_up(c->n_cur, kKAlign);
+    cpi::Epilogue epi{};
+    epi.s_a = c->s_a;
+    epi.s_b = c->s_b;
+    epi.gamma = gamma;
+    epi.ldg = c->p_b;
+    epi.counts = c->keep ? c->counts : nullptr;
+    epi.ldc = c->p_b;
+    epi.accumulate = c->accumulate;
+    epi.p_a = static_cast<int>(std::min(c->p_a, row0 + rows));
+    epi.p_b = static_cast<int>(c->p_b);
+    epi.vec = (c->p_b % 4) == 0;
+    epi.n = static_cast<double>(c->n_tot > 0 ? c->n_tot : 1);
+    epi.inv_n2 = 1.0 / (epi.n * epi.n);
+    {
+        static const int cache_mode = getenv("CPI_GEMM_CACHE") ? atoi(getenv("CPI_GEMM_CACHE")) : 0;
+        epi.cache = cache_mode;   // L2 policy knob of the CTA-pair GEMM (see kernels.h Epilogue::cache)
+    }
+    TimedScope ts(c, KC_GEMM, st);
+    cudaError_t e;
+    if (c->popc) {
+        const int64_t T = cpi::gemm_popc_block();
+        epi.m_tile0 = static_cast<int>(row0 / T);
+        e = cpi::launch_gemm_popc(static_cast<const uint32_t*>(c->op_a), static_cast<const uint32_t*>(c->op_b),
+                                  c->ld_op, k_pad / 32, epi, st);
+    } else if (c->pair) {
+        const int64_t bm = cpi::gemm_tc2_block_m();
+        epi.m_tile0 = static_cast<int>(row0 / bm);
+        e = cpi::launch_gemm_tc2(&c->tm_a, &c->tm_b, static_cast<int>((rows + bm - 1) / bm),
+                                 static_cast<int>(c->rows_b / cpi::gemm_tc2_block_n()),
+                                 static_cast<int>(k_pad / kKAlign), epi, c->num_sms, st);
+    } else {
+        const int64_t bm = cpi::gemm_tc_block_m();
+        epi.m_tile0 = static_cast<int>(row0 / bm);
+        e = cpi::launch_gemm_tc(&c->tm_a, &c->tm_b, static_cast<int>((rows + bm - 1) / bm),
+                                static_cast<int>(c->rows_b / cpi::gemm_tc_block_n()),
+                                static_cast<int>(k_pad / kKAlign), epi, c->num_sms, st);
+    }
+    c->launches += 1;
+    if (e != cudaSuccess) return cuda_fail(c, e, "pair-sum GEMM launch");
+    return CPI_OK;
+}
+
+}  // namespace
+
+int64_t cpi_row_align(const cpi_ctx* c) {
+    if (!c) return 0;
+    if (c->popc) return cpi::gemm_popc_block();
+    return c->pair ? cpi::gemm_tc2_block_m() : cpi::gemm_tc_block_m();
 }
 
 cpi_status cpi_correlate(cpi_ctx* c, float* gamma, void* stream) {
     if (!c) return CPI_ERR_INVALID_ARG;
-    if (!c->loaded) return fail(c, CPI_ERR_STATE, "cpi_correlate before cpi_load_frames");
+    if (!c->loaded || c->consumed || c->expanded)
+        return fail(c, CPI_ERR_STATE, "cpi_correlate needs a freshly loaded batch (cpi_load_frames)");
     if (!c->keep && c->batches > 0)
         return fail(c, CPI_ERR_STATE, "second batch needs CPI_KEEP_COUNTS (or cpi_reset)");
     if (!c->keep && !gamma)
@@ -390,69 +493,76 @@ cpi_status cpi_correlate(cpi_ctx* c, float* gamma, void* stream) {
     if (gamma && c->n_tot + n == 0) return fail(c, CPI_ERR_ZERO_FRAMES, "Gamma needs N_TOT >= 1");
     CK(c, cudaSetDevice(c->dev));
     auto st = static_cast<cudaStream_t>(stream);
-    const cpi_layout& L = c->cfg.layout;
-    const int64_t k_pad = round_up(n, kKAlign);
-    {
-        TimedScope ts(c, KC_EXPAND, st);
-        const cpi::RoiDev ra{c->cfg.roi_a.x0, c->cfg.roi_a.y0, c->cfg.roi_a.width, c->cfg.roi_a.height};
-        const cpi::RoiDev rb{c->cfg.roi_b.x0, c->cfg.roi_b.y0, c->cfg.roi_b.width, c->cfg.roi_b.height};
-        if (c->cur_buf >= 0) CK(c, cudaStreamWaitEvent(st, c->ev_loaded[c->cur_buf], 0));
-        if (n > 0) {
-            cpi::launch_expand(c->frames_cur, n, L.width_px / 8, L.height_px, L.bit_order, ra, c->op_a,
-                               c->ld_op, k_pad, c->s_a, c->popc, st);
-            cpi::launch_expand(c->frames_cur, n, L.width_px / 8, L.height_px, L.bit_order, rb, c->op_b,
-                               c->ld_op, k_pad, c->s_b, c->popc, st);
-            c->launches += 2;
-            CK(c, cudaGetLastError());
-        }
-        if (c->cur_buf >= 0) {
-            CK(c, cudaEventRecord(c->ev_consumed[c->cur_buf], st));
-            c->consumed_valid[c->cur_buf] = true;
-        }
-    }
-    const int64_t n_tot = c->n_tot + n;
-    cpi::Epilogue epi{};
-    epi.s_a = c->s_a;
-    epi.s_b = c->s_b;
-    epi.gamma = gamma;
-    epi.ldg = c->p_b;
-    epi.counts = c->keep ? c->counts : nullptr;
-    epi.ldc = c->p_b;
-    epi.accumulate = c->batches > 0 ? 1 : 0;
-    epi.p_a = static_cast<int>(c->p_a);
-    epi.p_b = static_cast<int>(c->p_b);
-    epi.vec = (c->p_b % 4) == 0;
-    epi.n = static_cast<double>(n_tot > 0 ? n_tot : 1);
-    epi.inv_n2 = 1.0 / (epi.n * epi.n);
+    cpi_status s = expand_batch(c, st);
+    if (s != CPI_OK) return s;
     if (n > 0) {
-        TimedScope ts(c, KC_GEMM, st);
-        cudaError_t e;
-        if (c->popc)
-            e = cpi::launch_gemm_popc(static_cast<const uint32_t*>(c->op_a), static_cast<const uint32_t*>(c->op_b),
-                                      c->ld_op, k_pad / 32, epi, st);
-        else if (c->pair)
-            e = cpi::launch_gemm_tc2(&c->tm_a, &c->tm_b, static_cast<int>(c->rows_a / cpi::gemm_tc2_block_m()),
-                                     static_cast<int>(c->rows_b / cpi::gemm_tc2_block_n()),
-                                     static_cast<int>(k_pad / kKAlign), epi, c->num_sms, st);
-        else
-            e = cpi::launch_gemm_tc(&c->tm_a, &c->tm_b, static_cast<int>(c->rows_a / cpi::gemm_tc_block_m()),
-                                    static_cast<int>(c->rows_b / cpi::gemm_tc_block_n()),
-                                    static_cast<int>(k_pad / kKAlign), epi, c->num_sms, st);
-        c->launches += 1;
-        if (e != cudaSuccess) return cuda_fail(c, e, "pair-sum GEMM launch");
+        s = gemm_rows(c, 0, c->p_a, gamma, st);
+        if (s != CPI_OK) return s;
     } else if (gamma) {
         // empty batch: Gamma of the unchanged totals from the kept counts
         if (!c->keep) return fail(c, CPI_ERR_STATE, "empty batch and no kept counts");
+        s = ensure_counts(c, st);
+        if (s != CPI_OK) return s;
         TimedScope ts(c, KC_FINALIZE, st);
         cudaError_t e = cpi::launch_finalize(c->counts, c->p_b, c->p_a, c->p_b, c->s_a, c->s_b,
-                                             static_cast<double>(n_tot), gamma, c->p_b, st);
+                                             static_cast<double>(c->n_tot), gamma, c->p_b, st);
         c->launches += 1;
         if (e != cudaSuccess) return cuda_fail(c, e, "finalize launch");
     }
-    c->n_tot = n_tot;
-    c->batches += 1;
+    c->consumed = true;
     c->loaded = false;
     c->gamma_current = gamma;
+    return CPI_OK;
+}
+
+cpi_status cpi_correlate_rows(cpi_ctx* c, int64_t row0, int64_t rows, float* gamma, void* stream) {
+    if (!c) return CPI_ERR_INVALID_ARG;
+    if (!c->loaded || c->consumed)
+        return fail(c, CPI_ERR_STATE, "cpi_correlate_rows needs a loaded batch not consumed by cpi_correlate");
+    if (!c->expanded && !c->keep && c->batches > 0)
+        return fail(c, CPI_ERR_STATE, "second batch needs CPI_KEEP_COUNTS (or cpi_reset)");
+    if (!c->keep && !gamma)
+        return fail(c, CPI_ERR_STATE, "gamma_dev is NULL and CPI_KEEP_COUNTS is off: pair sums would be lost");
+    const int64_t align = cpi_row_align(c);
+    if (row0 < 0 || rows <= 0 || row0 + rows > c->p_a || row0 % align || (rows % align && row0 + rows != c->p_a))
+        return fail(c, CPI_ERR_INVALID_ARG, "rows [%lld, +%lld) must lie in [0, P_a) on multiples of %lld",
+                    (long long)row0, (long long)rows, (long long)align);
+    if (gamma && c->n_tot + (c->expanded ? 0 : c->n_cur) == 0)
+        return fail(c, CPI_ERR_ZERO_FRAMES, "Gamma needs N_TOT >= 1");
+    CK(c, cudaSetDevice(c->dev));
+    auto st = static_cast<cudaStream_t>(stream);
+    if (!c->expanded) {
+        cpi_status s = expand_batch(c, st);
+        if (s != CPI_OK) return s;
+    }
+    if (c->n_cur > 0) {
+        cpi_status s = gemm_rows(c, row0, rows, gamma, st);
+        if (s != CPI_OK) return s;
+    } else if (gamma) {
+        if (!c->keep) return fail(c, CPI_ERR_STATE, "empty batch and no kept counts");
+        cpi_status s = ensure_counts(c, st);
+        if (s != CPI_OK) return s;
+        TimedScope ts(c, KC_FINALIZE, st);
+        cudaError_t e = cpi::launch_finalize(c->counts + row0 * c->p_b, c->p_b, rows, c->p_b, c->s_a + row0, c->s_b,
+                                             static_cast<double>(c->n_tot), gamma + row0 * c->p_b, c->p_b, st);
+        c->launches += 1;
+        if (e != cudaSuccess) return cuda_fail(c, e, "finalize launch");
+    }
+    c->gamma_current = nullptr;   // only a panel of Gamma is current
+    return CPI_OK;
+}
+
+cpi_status cpi_counts_dev(cpi_ctx* c, int32_t** s_ab, int32_t** s_a, int32_t** s_b) {
+    if (!c) return CPI_ERR_INVALID_ARG;
+    if (s_ab && c->keep) {
+        CK(c, cudaSetDevice(c->dev));
+        cpi_status s = ensure_counts(c, nullptr);   // zeros visible to any later stream work
+        if (s != CPI_OK) return s;
+        CK(c, cudaDeviceSynchronize());
+    }
+    if (s_ab) *s_ab = c->keep ? c->counts : nullptr;
+    if (s_a) *s_a = c->s_a;
+    if (s_b) *s_b = c->s_b;
     return CPI_OK;
 }
 
@@ -465,6 +575,8 @@ cpi_status cpi_finalize(cpi_ctx* c, float* gamma, int64_t* n_tot, void* stream) 
     if (!c->keep) return fail(c, CPI_ERR_STATE, "Gamma from counts needs CPI_KEEP_COUNTS");
     CK(c, cudaSetDevice(c->dev));
     auto st = static_cast<cudaStream_t>(stream);
+    cpi_status s = ensure_counts(c, st);
+    if (s != CPI_OK) return s;
     TimedScope ts(c, KC_FINALIZE, st);
     cudaError_t e = cpi::launch_finalize(c->counts, c->p_b, c->p_a, c->p_b, c->s_a, c->s_b,
                                          static_cast<double>(c->n_tot), gamma, c->p_b, st);
@@ -497,6 +609,10 @@ cpi_status cpi_get_counts(cpi_ctx* c, int32_t* s_ab, int32_t* s_a, int32_t* s_b,
     if (s_ab && !c->keep) return fail(c, CPI_ERR_STATE, "S_ab requested but CPI_KEEP_COUNTS is off");
     CK(c, cudaSetDevice(c->dev));
     auto st = static_cast<cudaStream_t>(stream);
+    if (s_ab) {
+        cpi_status s = ensure_counts(c, st);
+        if (s != CPI_OK) return s;
+    }
     if (s_ab) CK(c, cudaMemcpyAsync(s_ab, c->counts, sizeof(int32_t) * size_t(c->p_a) * c->p_b, cudaMemcpyDeviceToDevice, st));
     if (s_a) CK(c, cudaMemcpyAsync(s_a, c->s_a, sizeof(int32_t) * c->p_a, cudaMemcpyDeviceToDevice, st));
     if (s_b) CK(c, cudaMemcpyAsync(s_b, c->s_b, sizeof(int32_t) * c->p_b, cudaMemcpyDeviceToDevice, st));
@@ -510,9 +626,10 @@ cpi_status cpi_reset(cpi_ctx* c, void* stream) {
     auto st = static_cast<cudaStream_t>(stream);
     CK(c, cudaMemsetAsync(c->s_a, 0, sizeof(int32_t) * c->p_a, st));
     CK(c, cudaMemsetAsync(c->s_b, 0, sizeof(int32_t) * c->p_b, st));
-    if (c->keep) CK(c, cudaMemsetAsync(c->counts, 0, sizeof(int32_t) * size_t(c->p_a) * c->p_b, st));
+    c->counts_stale = true;                  // zeroed lazily: the next batch overwrites them
     c->n_tot = 0;
     c->batches = 0;
+    c->gemm_batches = 0;
     c->gamma_current = nullptr;
     c->loaded = false;
     return CPI_OK;
@@ -588,6 +705,14 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
         if (r != CUDA_SUCCESS) return fail(c, CPI_ERR_CUDA, "Gamma tensor map failed (%d)", int(r));
     }
     const int m_base = static_cast<int>(spec->row0 / Wa), m_count = static_cast<int>(spec->rows / Wa);
+    const bool cyclic = spec->row_block > 0 && spec->row_block < m_count;
+    const int m_block = cyclic ? spec->row_block : 0, m_stride = cyclic ? spec->row_stride : 0;
+    if (cyclic) {
+        if (m_stride < m_block)
+            return fail(c, CPI_ERR_INVALID_ARG, "row_stride %d < row_block %d", m_stride, m_block);
+        const int64_t last = m_base + int64_t((m_count - 1) / m_block) * m_stride + (m_count - 1) % m_block;
+        if (last >= Ha) return fail(c, CPI_ERR_INVALID_ARG, "block-cyclic shard reaches A row %lld >= H_a", (long long)last);
+    }
     const int group = tma_now ? c->fuse : 1;
     for (int p0 = 0; p0 < spec->n_planes; p0 += group) {
         const int nf = std::min(group, spec->n_planes - p0);
@@ -614,11 +739,14 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
             TimedScope ts(c, KC_STAGE1, st);
             cudaError_t e;
             if (tma_now)
-                e = cpi::launch_refocus_stage1_tma(&c->s1maps, nf, Wa, Ha, Wb, Hb, m_base, m_count, c->xs, c->ys,
-                                                   c->T, c->xblk, c->num_sms, st);
-            else
+                e = cpi::launch_refocus_stage1_tma(&c->s1maps, nf, Wa, Ha, Wb, Hb, m_base, m_count, m_block, m_stride,
+                                                   c->xs, c->ys, c->T, c->xblk, c->num_sms, st);
+            else if (!cyclic)
                 e = cpi::launch_refocus_stage1(spec->gamma_dev, c->p_b, Wa, Ha, Wb, Hb, m_base, m_count,
                                                c->xs[0], c->ys[0], c->T[0], st);
+            else
+                return fail(c, CPI_ERR_UNSUPPORTED, "block-cyclic shards need the TMA stage 1 (W_a <= 256, W_b %% 4 == 0, "
+                                                    "16-byte aligned Gamma)");
             c->launches += 1;
             if (e != cudaSuccess) return cuda_fail(c, e, "refocus stage-1 launch");
         }
@@ -626,9 +754,11 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
             TimedScope ts(c, KC_STAGE2, st);
             cudaError_t e = cudaSuccess;
             if (c->use_s2_staged) {
-                e = cpi::launch_refocus_stage2_group(c->T, nf, Wa, Ha, Hb, m_base, m_base + m_count, c->xs, c->ys,
-                                                     c->ypack, planes + int64_t(p0) * Ha * Wa, st);
+                e = cpi::launch_refocus_stage2_group(c->T, nf, Wa, Ha, Hb, m_base, m_count, m_block, m_stride, c->xs,
+                                                     c->ys, c->ypack, planes + int64_t(p0) * Ha * Wa, st);
                 c->launches += 1;
+            } else if (cyclic) {
+                return fail(c, CPI_ERR_UNSUPPORTED, "block-cyclic shards need H_a <= 256");
             } else {
                 for (int f = 0; f < nf && e == cudaSuccess; ++f) {
                     e = cpi::launch_refocus_stage2(c->T[f], Wa, Ha, Hb, m_base, m_count, c->xs[f], c->ys[f],

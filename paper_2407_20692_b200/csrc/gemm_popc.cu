@@ -19,7 +19,7 @@ gemm_popc_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
     __shared__ uint32_t As[KW][T + 1];
     __shared__ uint32_t Bs[KW][T + 1];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    const int64_t row0 = static_cast<int64_t>(blockIdx.y) * T;
+    const int64_t row0 = static_cast<int64_t>(blockIdx.y + epi.m_tile0) * T;
     const int64_t col0 = static_cast<int64_t>(blockIdx.x) * T;
     int acc[4][4] = {};
     for (int64_t w0 = 0; w0 < kw; w0 += KW) {
@@ -86,7 +86,8 @@ int gemm_popc_block() { return T; }
 
 cudaError_t launch_gemm_popc(const uint32_t* a, const uint32_t* b, int64_t ldw, int64_t kw,
                              const Epilogue& epi, cudaStream_t st) {
-    dim3 grid(static_cast<unsigned>((epi.p_b + T - 1) / T), static_cast<unsigned>((epi.p_a + T - 1) / T));
+    dim3 grid(static_cast<unsigned>((epi.p_b + T - 1) / T),
+              static_cast<unsigned>((epi.p_a - static_cast<int64_t>(epi.m_tile0) * T + T - 1) / T));
     gemm_popc_kernel<<<grid, 256, 0, st>>>(a, b, ldw, kw, epi);
     return cudaGetLastError();
 }

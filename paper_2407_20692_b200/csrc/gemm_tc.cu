@@ -85,6 +85,7 @@ gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_consta
             for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
                 int tm, tn;
                 tile_coords(t, m_tiles, n_tiles, tm, tn);
+                tm += epi.m_tile0;
                 for (int kb = 0; kb < k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], kStageBytes);
@@ -129,6 +130,7 @@ gemm_i8_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_consta
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
             int tm, tn;
             tile_coords(t, m_tiles, n_tiles, tm, tn);
+            tm += epi.m_tile0;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             mbar_wait(&tfull[acc], acc_phase);

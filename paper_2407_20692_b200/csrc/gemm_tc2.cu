@@ -81,14 +81,21 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            const uint64_t pol = l2_policy_evict_last();
             for (int t = pair; t < num_tiles; t += num_pairs) {
                 int tm, tn;
                 tile_coords(t, m_tiles, n_tiles, tm, tn);
+                tm += epi.m_tile0;
                 for (int kb = 0; kb < k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_expect_tx(&full[stage], 2 * kStageBytes);
-                    tma_load_2d_2sm(sA + stage * kABytes, &tma_a, &full[stage], kb * BK, tm * BM + rank * HM);
-                    tma_load_2d_2sm(sB + stage * kBBytes, &tma_b, &full[stage], kb * BK, tn * BN + rank * HN);
+                    if (epi.cache & 2) {
+                        tma_load_2d_2sm_hint(sA + stage * kABytes, &tma_a, &full[stage], kb * BK, tm * BM + rank * HM, pol);
+                        tma_load_2d_2sm_hint(sB + stage * kBBytes, &tma_b, &full[stage], kb * BK, tn * BN + rank * HN, pol);
+                    } else {
+                        tma_load_2d_2sm(sA + stage * kABytes, &tma_a, &full[stage], kb * BK, tm * BM + rank * HM);
+                        tma_load_2d_2sm(sB + stage * kBBytes, &tma_b, &full[stage], kb * BK, tn * BN + rank * HN);
+                    }
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -129,6 +136,7 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
         for (int t = pair; t < num_tiles; t += num_pairs, ++local) {
             int tm, tn;
             tile_coords(t, m_tiles, n_tiles, tm, tn);
+            tm += epi.m_tile0;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             mbar_wait(&tfull[acc], acc_phase);
@@ -155,8 +163,13 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
                     float* gp = epi.gamma ? epi.gamma + static_cast<int64_t>(row) * epi.ldg + col0 : nullptr;
                     const int32_t* sbc = sbs + 32 * c;
                     if (epi.vec && col0 + 32 <= epi.p_b) {
-                        if (gs.small) epilogue_chunk_vec<true>(r, cp, epi.accumulate, gp, sbc, sa, gs);
-                        else epilogue_chunk_vec<false>(r, cp, epi.accumulate, gp, sbc, sa, gs);
+                        if (epi.cache & 1) {
+                            if (gs.small) epilogue_chunk_vec<true, true>(r, cp, epi.accumulate, gp, sbc, sa, gs);
+                            else epilogue_chunk_vec<false, true>(r, cp, epi.accumulate, gp, sbc, sa, gs);
+                        } else {
+                            if (gs.small) epilogue_chunk_vec<true>(r, cp, epi.accumulate, gp, sbc, sa, gs);
+                            else epilogue_chunk_vec<false>(r, cp, epi.accumulate, gp, sbc, sa, gs);
+                        }
                     } else {
                         epilogue_chunk_tail(r, min(32, epi.p_b - col0), cp, epi.accumulate, gp, sbc, sa, gs);
                     }

@@ -23,6 +23,8 @@ struct Epilogue {
     int vec;              // 16-byte vector stores allowed (ldg, ldc, p_b multiples of 4)
     double n;             // N_TOT (all batches)
     double inv_n2;        // 1 / N_TOT^2 (kept for reference; kernels use make_gamma_scale(n))
+    int cache;            // bit 0: Gamma stores evict-first (st.global.cs); bit 1: operand loads L2 evict_last
+    int m_tile0;          // first M tile of this launch (row panels: cpi_correlate_rows)
 };
 
 // KB1: expand one RoI of packed frames into a K-major operand (bytes 0/1, or packed
@@ -81,8 +83,9 @@ struct Stage1Maps {
 };
 bool stage1_tma_supported(int Wa, int Wb);
 cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa, int Ha, int Wb, int Hb,
-                                      int m_base, int m_count, const AxisTables* xs, const AxisTables* ys,
-                                      double* const* T, const uint32_t* xblk, int num_sms, cudaStream_t st);
+                                      int m_base, int m_count, int m_block, int m_stride, const AxisTables* xs,
+                                      const AxisTables* ys, double* const* T, const uint32_t* xblk, int num_sms,
+                                      cudaStream_t st);
 // x-tables of a fused group packed for the TMA stage 1: uint32 j_rel << 23 | round(t * 2^23),
 // [n_fuse][Wb][Wa] (see refocus.cu), and xblk[n_fuse][ceil(Wb / 8)]: bit b set if some
 // x in [16 b, 16 b + 16) has a used sample for some u of the 8-column chunk.
@@ -104,13 +107,15 @@ EncodeTiledFn encode_tiled_fn();
 cudaError_t launch_refocus_stage2(const double* T, int Wa, int Ha, int Hb, int m_base,
                                   int m_count, AxisTables xs, AxisTables ys, float* plane,
                                   cudaStream_t st);
+// Shard A rows (both stages): local A row l is global row m_base + (l / m_block) * m_stride
+// + l % m_block, l < m_count (m_block <= 0: contiguous).
 // staged stage 2 (KB6'): one launch for n_fuse planes written to planes[f * Ha * Wa]; rows of
-// T outside [m_lo, m_hi) count as 0.  Needs the packed y-tables [n_fuse][Hb][Ha] (H_a <= 512).
+// T outside the shard count as 0.  Needs the packed y-tables [n_fuse][Hb][Ha] (H_a <= 256).
 bool stage2_staged_supported(int Ha);
 cudaError_t launch_pack_ytable_group(const AxisTables* ys, int n_fuse, int Ha, int Hb, uint32_t* ypack,
                                      cudaStream_t st);
-cudaError_t launch_refocus_stage2_group(double* const* T, int n_fuse, int Wa, int Ha, int Hb, int m_lo, int m_hi,
-                                        const AxisTables* xs, const AxisTables* ys, const uint32_t* ypack,
-                                        float* planes, cudaStream_t st);
+cudaError_t launch_refocus_stage2_group(double* const* T, int n_fuse, int Wa, int Ha, int Hb, int m_base, int m_count,
+                                        int m_block, int m_stride, const AxisTables* xs, const AxisTables* ys,
+                                        const uint32_t* ypack, float* planes, cudaStream_t st);
 
 }  // namespace cpi

@@ -251,6 +251,7 @@ struct S1Cfg {
 
 struct S1Args {
     int Wa, Ha, Wb, Hb, m_base, m_count, n_vg, n_chunks;
+    int m_block, m_stride;                   // shard A-row l -> m_base + (l / m_block) * m_stride + l % m_block
     const int32_t* xlo[kRefocusMaxFuse];
     const int32_t* xhi[kRefocusMaxFuse];
     const int32_t* ylo[kRefocusMaxFuse];
@@ -258,6 +259,11 @@ struct S1Args {
     double* T[kRefocusMaxFuse];
     const uint32_t* xblk;                    // [F][n_chunks] x-block masks (OR-ed over F in smem)
 };
+
+// global A row of the shard's local A row l (block-cyclic row ownership)
+__device__ __forceinline__ int shard_row(const S1Args& a, int l) {
+    return a.m_base + (l / a.m_block) * a.m_stride + l % a.m_block;
+}
 
 template <int F>
 __device__ __forceinline__ unsigned tile_mask(const S1Args& a, int m, int v0, int f) {
@@ -324,7 +330,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                 const int ml = tile / a.n_vg, vg = tile - ml * a.n_vg;
                 unsigned any = 0;
 #pragma unroll
-                for (int f = 0; f < F; ++f) any |= tile_mask<F>(a, a.m_base + ml, vg * kTVG, f);
+                for (int f = 0; f < F; ++f) any |= tile_mask<F>(a, shard_row(a, ml), vg * kTVG, f);
                 if (!any) continue;
                 for (int c = 0; c < a.n_chunks; ++c) {
                     const int2 sp = span[c];
@@ -356,7 +362,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
     uint32_t phase = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int ml = tile / a.n_vg, vg = tile - ml * a.n_vg;
-        const int m = a.m_base + ml, v0 = vg * kTVG;
+        const int m = shard_row(a, ml), v0 = vg * kTVG;
         unsigned mask[F], any = 0;
 #pragma unroll
         for (int f = 0; f < F; ++f) { mask[f] = tile_mask<F>(a, m, v0, f); any |= mask[f]; }
@@ -488,7 +494,8 @@ __global__ void pack_xtable_group_kernel(PackGroupArgs g, int Wa, int Wb, uint32
 constexpr int kS2VC = 8, kS2XB = 2, kS2Threads = 256, kS2MI = 256 / (kS2Threads / kS2VC);
 
 struct S2Args {
-    int Wa, Ha, Hb, m_lo, m_hi;
+    int Wa, Ha, Hb;
+    int m_base, m_count, m_block, m_stride;      // rows of T present: the shard's A rows (see S1Args)
     const double* T[kRefocusMaxFuse];
     const int32_t* xcnt[kRefocusMaxFuse];
     const int32_t* ycnt[kRefocusMaxFuse];
@@ -498,7 +505,7 @@ struct S2Args {
     float* plane[kRefocusMaxFuse];
 };
 
-__global__ void __launch_bounds__(kS2Threads)
+__global__ void __launch_bounds__(kS2Threads, 3)
 stage2_staged_kernel(S2Args a) {
     extern __shared__ __align__(16) uint8_t s2_smem[];
     const int f = blockIdx.y, x0 = blockIdx.x * kS2XB;
@@ -514,14 +521,23 @@ stage2_staged_kernel(S2Args a) {
     const int vl = threadIdx.x & (kS2VC - 1), ml = threadIdx.x / kS2VC;
     double pre[kS2XB][kS2MI];
     uint32_t ptab[kS2MI];
+    uint32_t present = 0;                          // bit k: this thread's row m = ml + 32 k is in the shard
+#pragma unroll
+    for (int k = 0; k < kS2MI; ++k) {
+        const int rel = ml + k * (kS2Threads / kS2VC) - a.m_base;
+        if (rel >= 0) {
+            const int blk = rel / a.m_stride, off = rel - blk * a.m_stride;
+            if (off < a.m_block && blk * a.m_block + off < a.m_count) present |= 1u << k;
+        }
+    }
     auto prefetch = [&](int v0) {
         const int v = v0 + vl, nvalid = min(kS2VC, Hb - v0) * Ha;   // table entries of real v rows
         int lo = 1, hi = 0;
-        if (v < Hb) { lo = max(__ldg(ylo + v), a.m_lo); hi = min(__ldg(yhi + v), a.m_hi - 1); }
+        if (v < Hb) { lo = __ldg(ylo + v); hi = __ldg(yhi + v); }
 #pragma unroll
         for (int k = 0; k < kS2MI; ++k) {
             const int m = ml + k * (kS2Threads / kS2VC);
-            const bool ok = m >= lo && m <= hi;
+            const bool ok = m >= lo && m <= hi && ((present >> k) & 1u);
 #pragma unroll
             for (int xb = 0; xb < kS2XB; ++xb) {
                 const int x = x0 + xb;
@@ -608,12 +624,15 @@ cudaError_t launch_pack_ytable_group(const AxisTables* ys, int n_fuse, int Ha, i
     return cudaGetLastError();
 }
 
-cudaError_t launch_refocus_stage2_group(double* const* T, int n_fuse, int Wa, int Ha, int Hb, int m_lo, int m_hi,
-                                        const AxisTables* xs, const AxisTables* ys, const uint32_t* ypack,
-                                        float* planes, cudaStream_t st) {
+cudaError_t launch_refocus_stage2_group(double* const* T, int n_fuse, int Wa, int Ha, int Hb, int m_base, int m_count,
+                                        int m_block, int m_stride, const AxisTables* xs, const AxisTables* ys,
+                                        const uint32_t* ypack, float* planes, cudaStream_t st) {
     if (n_fuse < 1 || n_fuse > kRefocusMaxFuse || !stage2_staged_supported(Ha)) return cudaErrorInvalidValue;
     S2Args a{};
-    a.Wa = Wa; a.Ha = Ha; a.Hb = Hb; a.m_lo = m_lo; a.m_hi = m_hi; a.ypack = ypack;
+    a.Wa = Wa; a.Ha = Ha; a.Hb = Hb; a.ypack = ypack;
+    a.m_base = m_base; a.m_count = m_count;
+    a.m_block = m_block > 0 ? m_block : (m_count > 0 ? m_count : 1);
+    a.m_stride = m_block > 0 ? m_stride : a.m_block;
     for (int f = 0; f < n_fuse; ++f) {
         a.T[f] = T[f]; a.xcnt[f] = xs[f].cnt; a.ycnt[f] = ys[f].cnt; a.ylo[f] = ys[f].lo; a.yhi[f] = ys[f].hi;
         a.plane[f] = planes + static_cast<int64_t>(f) * Ha * Wa;
@@ -691,11 +710,14 @@ static cudaError_t launch_s1_f(int F, const Stage1Maps* maps, const S1Args& a, i
 }
 
 cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa, int Ha, int Wb, int Hb,
-                                      int m_base, int m_count, const AxisTables* xs, const AxisTables* ys,
-                                      double* const* T, const uint32_t* xblk, int num_sms, cudaStream_t st) {
+                                      int m_base, int m_count, int m_block, int m_stride, const AxisTables* xs,
+                                      const AxisTables* ys, double* const* T, const uint32_t* xblk, int num_sms,
+                                      cudaStream_t st) {
     if (n_fuse < 1 || n_fuse > kRefocusMaxFuse) return cudaErrorInvalidValue;
     S1Args a{};
     a.Wa = Wa; a.Ha = Ha; a.Wb = Wb; a.Hb = Hb; a.m_base = m_base; a.m_count = m_count;
+    a.m_block = m_block > 0 ? m_block : (m_count > 0 ? m_count : 1);
+    a.m_stride = m_block > 0 ? m_stride : a.m_block;
     a.n_vg = (Hb + kTVG - 1) / kTVG;
     a.n_chunks = (Wb + kTUC - 1) / kTUC;
     a.xblk = xblk;

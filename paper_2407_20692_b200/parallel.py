@@ -3,14 +3,15 @@
 SURVEY §8(e) / BASELINE north_star: frames shard naturally.  Rank g of G takes a
 contiguous frame slice, accumulates int32 partial S_ab, S_a, S_b, N over it (Eq. (1)'s
 sums are exactly additive), then
-  1. all-reduce(sum) of [S_a | S_b | N]                    (tiny),
-  2. reduce-scatter(sum) of S_ab by A-row blocks            (the one real exchange),
-  3. finalise its own Gamma row shard (cpi_finalize_counts),
-  4. refocus its own rows into partial planes (refocusing is linear in Gamma and the
+  1. runs the pair-sum GEMM in row panels and reduce-scatters(sum) each panel as soon as it
+     is done (the one real exchange, overlapped with the next panels' GEMM),
+  2. all-reduce(sum) of [S_a | S_b | N]                    (tiny),
+  3. finalises its own Gamma rows (cpi_finalize_counts),
+  4. refocuses its own rows into partial planes (refocusing is linear in Gamma and the
      normalisation is geometry-only, so shard planes add up),
   5. all-reduce(sum) of the planes.
-Shards are whole A rows (multiples of W_a) so each rank's refocus stage 1 sees complete
-(m, v) blocks.
+Ownership is block-cyclic over whole A rows (``ShardPlan``): every rank holds rows spread
+over the whole RoI, which balances the refocusing work for alpha < 1.
 
 The compute steps are supplied by a backend object so the same orchestration runs with
 the CUDA library (``CudaBackend``) or, in CPU tests, with any other implementation of
@@ -34,86 +35,169 @@ def frame_slice(n_frames: int, rank: int, world: int) -> tuple[int, int]:
 
 
 def row_shard(width_a: int, height_a: int, rank: int, world: int) -> tuple[int, int]:
-    """A-row block [row0, row0 + rows) of Gamma owned by a rank (whole A rows, equal
-    blocks: reduce-scatter needs equal chunks, so H_a must be divisible by world)."""
+    """Contiguous A-row block [row0, row0 + rows) of a rank (whole A rows, equal blocks).
+    Kept for callers that want contiguous ownership; the pipeline uses ``shard_plan``."""
     if height_a % world:
         raise ValueError(f"H_a = {height_a} must be divisible by the world size {world}")
     m_per = height_a // world
     return rank * m_per * width_a, m_per * width_a
 
 
+@dataclass(frozen=True)
+class ShardPlan:
+    """Block-cyclic ownership of Gamma's A rows (SURVEY §8(e) load balance + panelised RS).
+    The GEMM runs in ``panels`` row panels of ``world * block`` A rows; in every panel rank g
+    owns the g-th block of ``block`` consecutive A rows, so its shard is the A rows
+        m(l) = m_base + (l // block) * stride + l % block,   l < m_count,
+    with m_base = g * block, stride = world * block.  Every panel's reduce-scatter can start
+    as soon as that panel's GEMM is done, and every rank owns rows spread over the whole
+    A RoI (refocusing work per rank balanced for every alpha)."""
+    width_a: int
+    height_a: int
+    world: int
+    rank: int
+    block: int
+    panels: int
+
+    @property
+    def m_base(self) -> int:
+        return self.rank * self.block
+
+    @property
+    def stride(self) -> int:
+        return self.world * self.block
+
+    @property
+    def m_count(self) -> int:
+        return self.block * self.panels
+
+    @property
+    def panel_rows(self) -> int:          # A pixels per panel
+        return self.world * self.block * self.width_a
+
+    def a_rows(self):
+        """Global A-row index of each local A row of the shard."""
+        l = torch.arange(self.m_count)
+        return self.m_base + (l // self.block) * self.stride + l % self.block
+
+    def pixel_rows(self):
+        """Global Gamma row (A pixel) of each local row of the shard."""
+        m = self.a_rows()
+        return (m[:, None] * self.width_a + torch.arange(self.width_a)[None, :]).reshape(-1)
+
+
+def shard_plan(width_a: int, height_a: int, rank: int, world: int, row_align: int = 1,
+               min_panel_rows: int = 8192) -> ShardPlan:
+    """Smallest block (A rows per rank per panel) whose panel is a multiple of the GEMM's row
+    alignment and holds at least ``min_panel_rows`` A pixels (launch / collective overhead vs
+    pipelining); one panel of contiguous blocks if none qualifies (always valid)."""
+    if height_a % world:
+        raise ValueError(f"H_a = {height_a} must be divisible by the world size {world}")
+    m_per = height_a // world
+    if world > 1:
+        for block in range(1, m_per + 1):
+            rows = world * block * width_a
+            if m_per % block == 0 and rows % row_align == 0 and rows >= min(min_panel_rows, width_a * height_a):
+                return ShardPlan(width_a, height_a, world, rank, block, m_per // block)
+    return ShardPlan(width_a, height_a, world, rank, m_per, 1)
+
+
 @dataclass
 class ShardResult:
     n_tot: int
-    row0: int
-    rows: int
-    gamma_rows: torch.Tensor          # [rows][P_b] fp32
+    plan: ShardPlan
+    gamma_rows: torch.Tensor          # [m_count * W_a][P_b] fp32, rows plan.pixel_rows()
     planes: Optional[torch.Tensor]    # [P][H_a][W_a] fp32 (summed over ranks) or None
 
 
-def _reduce_scatter_rows(full: torch.Tensor, rows: int, group) -> torch.Tensor:
-    out = torch.empty((rows, full.shape[1]), dtype=full.dtype, device=full.device)
+def _reduce_scatter_async(out: torch.Tensor, full: torch.Tensor, group):
+    """Sum `full` over ranks and keep this rank's equal chunk in `out` (async on NCCL)."""
     if dist.get_backend(group) == "nccl":
-        dist.reduce_scatter_tensor(out, full, op=dist.ReduceOp.SUM, group=group)
-    else:   # gloo has no reduce_scatter_tensor: all-reduce then keep the own block
-        dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group)
-        r = dist.get_rank(group)
-        out.copy_(full[r * rows:(r + 1) * rows])
-    return out
+        return dist.reduce_scatter_tensor(out, full, op=dist.ReduceOp.SUM, group=group, async_op=True)
+    # gloo has no reduce_scatter_tensor: all-reduce a copy, keep the own chunk
+    tmp = full.clone()
+    dist.all_reduce(tmp, op=dist.ReduceOp.SUM, group=group)
+    r, rows = dist.get_rank(group), out.shape[0]
+    out.copy_(tmp[r * rows:(r + 1) * rows])
+    return None
 
 
-def correlate_and_refocus(backend, frames_local, roi_a, roi_b, alphas=None, group=None) -> ShardResult:
-    """Run the frame-sharded pipeline on this rank.  ``backend`` provides:
-         local_sums(frames) -> (s_ab [P_a][P_b] int32, s_a [P_a] int32, s_b [P_b] int32, n)
-         finalize_rows(s_ab_rows, row0, s_a, s_b, n_tot) -> gamma rows fp32
-         refocus(alphas, gamma_rows, row0, rows) -> planes [P][H_a][W_a] fp32
-    all tensors on ``backend.device``."""
+def correlate_and_refocus(backend, frames_local, roi_a, roi_b, alphas=None, group=None,
+                          min_panel_rows: int = 8192) -> ShardResult:
+    """Run the frame-sharded pipeline on this rank.  ``backend`` provides
+         row_align                          GEMM row-panel alignment (A pixels)
+         begin(frames)                      load this rank's frames
+         panel_counts(row0, rows)           int32 [rows][P_b] pair sums of A pixels [row0, +rows)
+                                            over this rank's frames (launched on the current stream)
+         marginals() -> (s_a, s_b, n)       this rank's S_a, S_b (int32), frame count
+         finalize_rows(s_ab_rows, s_a_rows, s_b, n_tot) -> Gamma rows fp32
+         refocus(alphas, gamma_rows, row0, rows, row_block, row_stride) -> planes fp32
+    with all tensors on ``backend.device``."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    s_ab, s_a, s_b, n = backend.local_sums(frames_local)
-    p_a, p_b = s_a.numel(), s_b.numel()
+    Wa, Ha = roi_a[2], roi_a[3]
+    p_a, p_b = Wa * Ha, roi_b[2] * roi_b[3]
+    plan = shard_plan(Wa, Ha, rank, world, backend.row_align, min_panel_rows)
+    dev = backend.device
+    backend.begin(frames_local)
+    chunk = plan.block * Wa
+    shard = torch.empty((plan.panels, chunk, p_b), dtype=torch.int32, device=dev)
+    works = []
+    for k in range(plan.panels):
+        panel = backend.panel_counts(k * plan.panel_rows, plan.panel_rows)
+        works.append(_reduce_scatter_async(shard[k], panel, group))
+    s_a, s_b, n = backend.marginals()
     marg = torch.cat([s_a.to(torch.int64), s_b.to(torch.int64),
                       torch.tensor([n], dtype=torch.int64, device=s_a.device)])
     dist.all_reduce(marg, op=dist.ReduceOp.SUM, group=group)
+    for w in works:
+        if w is not None:
+            w.wait()
     s_a_tot = marg[:p_a].to(torch.int32)
     s_b_tot = marg[p_a:p_a + p_b].to(torch.int32)
     n_tot = int(marg[-1].item())
-    row0, rows = row_shard(roi_a[2], roi_a[3], rank, world)
-    s_ab_rows = _reduce_scatter_rows(s_ab, rows, group)
-    gamma_rows = backend.finalize_rows(s_ab_rows, row0, s_a_tot, s_b_tot, n_tot)
+    s_a_rows = s_a_tot[plan.pixel_rows().to(s_a_tot.device)].contiguous()
+    gamma_rows = backend.finalize_rows(shard.view(-1, p_b), s_a_rows, s_b_tot, n_tot)
     planes = None
     if alphas is not None and len(alphas):
-        planes = backend.refocus(alphas, gamma_rows, row0, rows)
+        planes = backend.refocus(alphas, gamma_rows, plan.m_base * Wa, plan.m_count * Wa, plan.block, plan.stride)
         dist.all_reduce(planes, op=dist.ReduceOp.SUM, group=group)
-    return ShardResult(n_tot, row0, rows, gamma_rows, planes)
+    return ShardResult(n_tot, plan, gamma_rows, planes)
 
 
 class CudaBackend:
-    """The five pipeline steps on one B200 through the C ABI (libcpi.so)."""
+    """The pipeline steps on one B200 through the C ABI (libcpi.so): the GEMM runs in row
+    panels (cpi_correlate_rows) whose pair sums are handed to the collectives in place
+    (cpi_counts_dev views, no copies)."""
 
     def __init__(self, roi_a, roi_b, max_frames: int, device: int = 0, variant: str = "tc"):
         from .cpi import Context
         self.ctx = Context(roi_a, roi_b, max_frames, device=device, variant=variant, keep_counts=True)
         self.device = torch.device(f"cuda:{device}")
         self.roi_a = roi_a
+        self.row_align = self.ctx.row_align()
+        self._s_ab, self._s_a, self._s_b = self.ctx.counts_views()
+        self._n = 0
 
-    def local_sums(self, frames):
+    def begin(self, frames):
         c = self.ctx
         c.reset()
-        c.load_frames(frames)
-        c.correlate(None)
-        s_ab = torch.empty((c.p_a, c.p_b), dtype=torch.int32, device=self.device)
-        s_a = torch.empty(c.p_a, dtype=torch.int32, device=self.device)
-        s_b = torch.empty(c.p_b, dtype=torch.int32, device=self.device)
-        n = c.get_counts(s_ab, s_a, s_b)
-        return s_ab, s_a, s_b, n
+        self._n = c.load_frames(frames)
 
-    def finalize_rows(self, s_ab_rows, row0, s_a, s_b, n_tot):
+    def panel_counts(self, row0, rows):
+        self.ctx.correlate_rows(row0, rows)
+        return self._s_ab[row0:row0 + rows]
+
+    def marginals(self):
+        return self._s_a, self._s_b, self._n
+
+    def finalize_rows(self, s_ab_rows, s_a_rows, s_b, n_tot):
         g = torch.empty(s_ab_rows.shape, dtype=torch.float32, device=self.device)
-        self.ctx.finalize_counts(s_ab_rows.contiguous(), row0, s_a.contiguous(), s_b.contiguous(), n_tot, g)
+        self.ctx.finalize_counts(s_ab_rows.contiguous(), 0, s_a_rows.contiguous(), s_b.contiguous(), n_tot, g)
         return g
 
-    def refocus(self, alphas, gamma_rows, row0, rows):
+    def refocus(self, alphas, gamma_rows, row0, rows, row_block=0, row_stride=0):
         planes = self.ctx.new_planes(len(alphas))
-        self.ctx.refocus(alphas, gamma_rows, planes, row0=row0, rows=rows)
+        self.ctx.refocus(alphas, gamma_rows, planes, row0=row0, rows=rows, row_block=row_block,
+                         row_stride=row_stride)
         return planes

@@ -23,23 +23,31 @@ ALPHAS = [0.6, 1.0, 1.7]
 
 
 class OracleBackend:
-    """The five pipeline steps computed by the CPU oracle (test stand-in for CudaBackend)."""
+    """The pipeline steps computed by the CPU oracle (test stand-in for CudaBackend)."""
     device = torch.device("cpu")
+    row_align = 1
 
-    def local_sums(self, frames):
-        r = oracle.correlate(frames, ROI_A, ROI_B)
-        return (torch.from_numpy(r["s_ab"].astype(np.int32)), torch.from_numpy(r["s_a"].astype(np.int32)),
-                torch.from_numpy(r["s_b"].astype(np.int32)), int(r["n"]))
+    def begin(self, frames):
+        self.r = oracle.correlate(frames, ROI_A, ROI_B)
 
-    def finalize_rows(self, s_ab_rows, row0, s_a, s_b, n_tot):
-        rows = s_ab_rows.shape[0]
-        g = oracle.gamma(s_ab_rows.numpy(), s_a.numpy()[row0:row0 + rows], s_b.numpy(), n_tot)
+    def panel_counts(self, row0, rows):
+        return torch.from_numpy(self.r["s_ab"][row0:row0 + rows].astype(np.int32))
+
+    def marginals(self):
+        return (torch.from_numpy(self.r["s_a"].astype(np.int32)), torch.from_numpy(self.r["s_b"].astype(np.int32)),
+                int(self.r["n"]))
+
+    def finalize_rows(self, s_ab_rows, s_a_rows, s_b, n_tot):
+        g = oracle.gamma(s_ab_rows.numpy(), s_a_rows.numpy(), s_b.numpy(), n_tot)
         return torch.from_numpy(g.astype(np.float32))
 
-    def refocus(self, alphas, gamma_rows, row0, rows):
+    def refocus(self, alphas, gamma_rows, row0, rows, row_block, row_stride):
         Wa, Ha, Wb, Hb = DIMS
         G = np.zeros((Wa * Ha, Wb * Hb), dtype=np.float32)
-        G[row0:row0 + rows] = gamma_rows.numpy()
+        l = np.arange(rows // Wa)                     # include/cpi.h cpi_refocus_spec row map
+        m = row0 // Wa + (l // row_block) * row_stride + l % row_block
+        pix = (m[:, None] * Wa + np.arange(Wa)[None, :]).reshape(-1)
+        G[pix] = gamma_rows.numpy()
         return torch.from_numpy(oracle.refocus(G, DIMS, alphas).astype(np.float32))
 
 
@@ -51,25 +59,28 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, min_panel_rows):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         frames = synth.bernoulli_frames(N, 0.3, seed=31)
         lo, hi = parallel.frame_slice(N, rank, world)
-        res = parallel.correlate_and_refocus(OracleBackend(), frames[lo:hi], ROI_A, ROI_B, ALPHAS)
-        q.put((rank, res.n_tot, res.row0, res.rows, res.gamma_rows.numpy(), res.planes.numpy()))
+        res = parallel.correlate_and_refocus(OracleBackend(), frames[lo:hi], ROI_A, ROI_B, ALPHAS,
+                                             min_panel_rows=min_panel_rows)
+        q.put((rank, res.n_tot, res.plan, res.gamma_rows.numpy(), res.planes.numpy()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_frame_sharded_pipeline_matches_single_process(world):
+@pytest.mark.parametrize("world,min_panel_rows", [(2, 8192), (4, 8192), (2, 1), (4, 1)])
+def test_frame_sharded_pipeline_matches_single_process(world, min_panel_rows):
+    """min_panel_rows = 1: one A row per rank per panel (cyclic ownership, several panels);
+    8192: one panel of contiguous blocks at this small RoI."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, min_panel_rows)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=300) for _ in range(world)]
@@ -81,11 +92,14 @@ def test_frame_sharded_pipeline_matches_single_process(world):
     G = full["gamma"].astype(np.float32)
     want_planes = oracle.refocus(G, DIMS, ALPHAS)
     covered = np.zeros(G.shape[0], dtype=int)
-    for rank, n_tot, row0, rows, g_rows, planes in out:
-        assert n_tot == N
-        assert row0 == rank * rows and rows == G.shape[0] // world
-        np.testing.assert_array_equal(g_rows, G[row0:row0 + rows])
-        covered[row0:row0 + rows] += 1
+    for rank, n_tot, plan, g_rows, planes in out:
+        assert n_tot == N and plan.rank == rank and plan.world == world
+        if min_panel_rows == 1:
+            assert plan.block == 1 and plan.panels == DIMS[1] // world      # cyclic A rows
+        rows = plan.pixel_rows().numpy()
+        assert g_rows.shape[0] == rows.size == G.shape[0] // world
+        np.testing.assert_array_equal(g_rows, G[rows])
+        covered[rows] += 1
         np.testing.assert_allclose(planes, want_planes, rtol=1e-5, atol=1e-7)
     assert np.all(covered == 1)
 
@@ -100,3 +114,16 @@ def test_slicing_helpers():
     assert parallel.row_shard(256, 256, 3, 8) == (3 * 32 * 256, 32 * 256)
     with pytest.raises(ValueError):
         parallel.row_shard(256, 250, 0, 8)
+    # block-cyclic plans: every A row owned exactly once, panels aligned to the GEMM tile
+    for (W, H, world, align) in [(256, 256, 8, 256), (256, 256, 2, 256), (128, 128, 4, 256), (12, 8, 4, 256),
+                                 (12, 8, 2, 1), (32, 16, 2, 128)]:
+        owned = np.zeros(H, dtype=int)
+        for r in range(world):
+            p = parallel.shard_plan(W, H, r, world, align)
+            assert p.panel_rows % align == 0 or p.panels == 1
+            assert p.m_count * world == H
+            owned[p.a_rows().numpy()] += 1
+        assert np.all(owned == 1)
+    p = parallel.shard_plan(256, 256, 3, 8, 256)
+    assert (p.block, p.panels, p.stride, p.m_base) == (4, 8, 32, 12)
+    assert p.a_rows()[:6].tolist() == [12, 13, 14, 15, 44, 45]

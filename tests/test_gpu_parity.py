@@ -303,3 +303,67 @@ def test_refocus_repeat_bit_identical():
     torch.cuda.synchronize()
     for s in range(1, 4):
         assert torch.equal(same[s], same[0])
+
+
+@pytest.mark.parametrize("variant", ["tc", "popc"])
+def test_correlate_rows_panels_match_full(variant):
+    """cpi_correlate_rows (SURVEY §8(e) panelised GEMM): covering A pixels with aligned row
+    panels, over two accumulated batches with different panel splits, gives counts and
+    Gamma bit-identical to cpi_correlate, and the borrowed count views alias the library's."""
+    roi_a, roi_b = (3, 5, 64, 20), (260, 7, 24, 10)          # P_a = 1280 (5 x 256 rows), P_b = 240
+    fr = synth.bernoulli_frames(700, 0.2, seed=44)
+    full = _gpu_sums(fr, roi_a, roi_b, variant=variant, batches=[300, 400])
+    ctx = _ctx(roi_a, roi_b, 400, variant=variant, keep_counts=True)
+    al = ctx.row_align()
+    assert al > 0 and ctx.p_a % al == 0
+    g = ctx.new_gamma()
+    splits = [[(0, al), (al, 3 * al), (3 * al, ctx.p_a - 3 * al)], [(0, ctx.p_a)]]
+    for (lo, hi), panels in zip([(0, 300), (300, 700)], splits):
+        ctx.load_frames(np.ascontiguousarray(fr[lo:hi]))
+        for r0, rows in panels[::-1]:                         # any order
+            ctx.correlate_rows(r0, rows, g)
+    s_ab, s_a, s_b = ctx.counts_views()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(s_ab.cpu().numpy(), full["s_ab"])
+    np.testing.assert_array_equal(s_a.cpu().numpy(), full["s_a"])
+    np.testing.assert_array_equal(s_b.cpu().numpy(), full["s_b"])
+    np.testing.assert_array_equal(g.cpu().numpy(), full["gamma"])
+    # errors: misaligned panel, whole-batch correlate after a panel of the same batch
+    from paper_2407_20692_b200 import CpiError
+    ctx.load_frames(np.ascontiguousarray(fr[:10]))
+    with pytest.raises(CpiError, match="INVALID_ARG"):
+        ctx.correlate_rows(1, al)
+    ctx.correlate_rows(0, al)
+    with pytest.raises(CpiError, match="STATE"):
+        ctx.correlate(g)
+
+
+@pytest.mark.parametrize("block", [1, 2])
+def test_refocus_block_cyclic_shards(block):
+    """Block-cyclic A-row shards (cpi_refocus_spec row_block / row_stride, the multi-GPU
+    ownership of parallel.ShardPlan): each shard's planes equal the oracle's planes of Gamma
+    restricted to the shard's rows, and the shards of all ranks add up to the whole plane."""
+    dims = (20, 16, 12, 12)
+    Wa, Ha, Wb, Hb = dims
+    G = synth.random_gamma(Wa * Ha, Wb * Hb, seed=9)
+    al = [0.6, 1.0, 1.7]
+    world = 4
+    whole = _refocus_gpu(G, dims, al)
+    total = np.zeros_like(whole)
+    ctx = _ctx((0, 0, Wa, Ha), (0, 0, Wb, Hb), 1)
+    for rank in range(world):
+        stride = world * block
+        m = np.array([rank * block + (l // block) * stride + l % block for l in range(Ha // world)])
+        pix = (m[:, None] * Wa + np.arange(Wa)[None, :]).reshape(-1)
+        rows_g = torch.from_numpy(np.ascontiguousarray(G[pix], dtype=np.float32)).cuda()
+        planes = ctx.new_planes(len(al))
+        ctx.refocus(al, rows_g, planes, row0=rank * block * Wa, rows=pix.size, row_block=block, row_stride=stride)
+        torch.cuda.synchronize()
+        R = planes.cpu().numpy().astype(np.float64)
+        Gs = np.zeros_like(G)
+        Gs[pix] = G[pix]
+        Ro = oracle.refocus(Gs, dims, al)
+        M = oracle.refocus(np.abs(Gs.astype(np.float64)), dims, al)
+        assert np.all(np.abs(R - Ro) <= 1e-6 * M + 1e-30)
+        total += R
+    np.testing.assert_allclose(total, whole, rtol=1e-5, atol=1e-7)

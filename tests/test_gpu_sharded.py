@@ -2,8 +2,8 @@
 with 2 ranks sharing one GPU over gloo.  No kernel waits on another rank (the collectives run on
 the host through gloo), so this is safe on one device; it exercises the product's multi-GPU
 code path end to end: per-rank int32 partial sums, all-reduce of the marginals, row
-reduce-scatter, cpi_finalize_counts of the owned rows, row-shard refocusing and the plane
-all-reduce.  Result: Gamma rows bit-identical to the single-context run, planes within fp
+reduce-scatter of GEMM row panels (cpi_correlate_rows), cpi_finalize_counts of the owned
+block-cyclic rows, block-cyclic refocusing and the plane all-reduce.  Result: Gamma rows bit-identical to the single-context run, planes within fp
 rounding of it (shard planes are summed in fp32)."""
 import os
 import socket
@@ -14,7 +14,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
-ROI_A, ROI_B = (0, 0, 32, 16), (256, 0, 24, 12)
+ROI_A, ROI_B = (0, 0, 32, 32), (256, 0, 24, 12)      # P_a = 1024: four 256-row panels at world 2
 N = 1500
 ALPHAS = [0.6, 1.0, 1.45]
 
@@ -41,19 +41,29 @@ def _worker(rank, world, port, q):
 
         class GlooCuda:
             """gloo collectives need host tensors: stage through the host (plumbing only)."""
-            device = be.device
+            device = torch.device("cpu")
+            row_align = be.row_align
 
-            def local_sums(self, fr):
-                return tuple(t.cpu() if hasattr(t, "cpu") else t for t in be.local_sums(fr))
+            def begin(self, fr):
+                be.begin(fr)
 
-            def finalize_rows(self, s_ab_rows, row0, s_a, s_b, n_tot):
-                return be.finalize_rows(s_ab_rows.cuda(), row0, s_a.cuda(), s_b.cuda(), n_tot).cpu()
+            def panel_counts(self, row0, rows):
+                return be.panel_counts(row0, rows).cpu()
 
-            def refocus(self, alphas, gamma_rows, row0, rows):
-                return be.refocus(alphas, gamma_rows.cuda(), row0, rows).cpu()
+            def marginals(self):
+                s_a, s_b, n = be.marginals()
+                return s_a.cpu(), s_b.cpu(), n
 
-        res = parallel.correlate_and_refocus(GlooCuda(), np.ascontiguousarray(frames[lo:hi]), ROI_A, ROI_B, ALPHAS)
-        q.put((rank, res.n_tot, res.row0, res.rows, res.gamma_rows.numpy(), res.planes.numpy()))
+            def finalize_rows(self, s_ab_rows, s_a_rows, s_b, n_tot):
+                return be.finalize_rows(s_ab_rows.cuda(), s_a_rows.cuda(), s_b.cuda(), n_tot).cpu()
+
+            def refocus(self, alphas, gamma_rows, row0, rows, row_block, row_stride):
+                return be.refocus(alphas, gamma_rows.cuda(), row0, rows, row_block, row_stride).cpu()
+
+        res = parallel.correlate_and_refocus(GlooCuda(), np.ascontiguousarray(frames[lo:hi]), ROI_A, ROI_B, ALPHAS,
+                                             min_panel_rows=1)
+        q.put((rank, res.n_tot, res.plan.pixel_rows().numpy(), res.plan.panels, res.gamma_rows.numpy(),
+               res.planes.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -82,7 +92,7 @@ def test_two_ranks_on_one_gpu_match_single_context():
     torch.cuda.synchronize()
     G = g.cpu().numpy()
     P = planes.cpu().numpy()
-    for rank, n_tot, row0, rows, g_rows, pl in out:
-        assert n_tot == N
-        np.testing.assert_array_equal(g_rows, G[row0:row0 + rows])
+    for rank, n_tot, rows, panels, g_rows, pl in out:
+        assert n_tot == N and panels > 1           # several row panels, block-cyclic ownership
+        np.testing.assert_array_equal(g_rows, G[rows])
         np.testing.assert_allclose(pl, P, rtol=1e-5, atol=1e-9)
