@@ -48,7 +48,7 @@ def parse():
     p.add_argument("--frames", type=int, default=10_000, help="frames per step per rank")
     p.add_argument("--planes", type=int, default=64, help="refocus planes per step")
     p.add_argument("--occupancy", type=float, default=0.05, help="Bernoulli f of the synthetic bits")
-    p.add_argument("--variant", default="tc", choices=["tc", "popc"])
+    p.add_argument("--variant", default="tc", choices=["tc", "popc", "fp4"])
     p.add_argument("--roi", default="full", choices=["full", "128", "tiny"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -369,8 +369,6 @@ def main():
         return
 
     peaks, peak_src = load_peaks()
-    int8_burst = 2.0 * peaks["bf16_tflops"]                                  # TOPS, i8 = 2 x bf16 (4.5/2.25)
-    int8_sustained = 2.0 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     hbm = peaks["hbm_gbs"]
     f_clk = (clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)) * 1e6
     gemm_ms, gemm_n = kt["gemm"]
@@ -388,14 +386,20 @@ def main():
     lds_peak_gtaps = 148 * 32 * f_clk / 1e9          # 32 four-byte LDS lanes per clock per SM
     corr_ms = (kt["expand"][0] + gemm_ms) / args.steps
     ref_ms = (kt["coords"][0] + s1_ms + kt["stage2"][0]) / args.steps
-    roof_gemm = {"kernel": "gemm_i8_tc2 (KB2, cta_group::2)" if args.variant == "tc" else "gemm_popc (KB3)",
-                 "bound": "tensor", "achieved": gemm_tops, "peak": int8_burst, "unit": "TOPS",
-                 "frac": gemm_tops / int8_burst if gemm_tops else None,
-                 "peak_note": (f"int8 dense = 2 x {peak_src} bf16 burst {peaks['bf16_tflops']} TFLOP/s "
-                               f"(guide ratio 4.5/2.25); the sustained bf16 figure ({peaks.get('bf16_tflops_sustained')}) "
-                               f"was taken at a 1327 MHz median clock, this run's median was "
-                               f"{clk.get('sm_mhz')} MHz"),
-                 "frac_of_sustained": gemm_tops / int8_sustained if gemm_tops else None,
+    # the FP4 variant runs kind::mxf4: its own peak is 4 x bf16 (nominal 9 / 2.25 PFLOP/s)
+    ratio, dname = (4.0, "fp4 (e2m1, kind::mxf4)") if args.variant == "fp4" else (2.0, "int8")
+    tc_burst, tc_sustained = ratio * peaks["bf16_tflops"], ratio * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    if args.variant == "fp4":
+        clock_peak_tops *= 2.0                        # 16384 e2m1 MAC/clk/SM
+    roof_gemm = {"kernel": {"tc": "gemm_i8_tc2 (KB2, cta_group::2, kind::i8)", "popc": "gemm_popc (KB3)",
+                            "fp4": "gemm_i8_tc2<fp4> (KB2, cta_group::2, kind::mxf4)"}[args.variant],
+                 "bound": "tensor", "achieved": gemm_tops, "peak": tc_burst, "unit": "TOPS",
+                 "frac": gemm_tops / tc_burst if gemm_tops else None,
+                 "peak_note": (f"{dname} dense = {ratio:g} x {peak_src} bf16 burst {peaks['bf16_tflops']} TFLOP/s "
+                               f"(guide ratio {ratio * 2.25:g}/2.25); the sustained bf16 figure "
+                               f"({peaks.get('bf16_tflops_sustained')}) was taken at a 1327 MHz median clock, this "
+                               f"run's median was {clk.get('sm_mhz')} MHz"),
+                 "frac_of_sustained": gemm_tops / tc_sustained if gemm_tops else None,
                  "frac_of_clock_peak": gemm_tops / clock_peak_tops if gemm_tops else None,
                  "clock_peak_tops": clock_peak_tops,
                  "ops_per_launch": ops, "ms_per_launch": gemm_ms / gemm_n if gemm_n else None,

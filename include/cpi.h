@@ -68,6 +68,11 @@ typedef int32_t cpi_status;
 #define CPI_KEEP_COUNTS   2u  /* keep int32 S_ab [P_a][P_b] in a library workspace: needed for
                                  multi-batch accumulation, cpi_get_counts of S_ab,
                                  and cpi_finalize from counts.  Costs 4*P_a*P_b bytes. */
+#define CPI_VARIANT_FP4   4u  /* S_ab on tcgen05 kind::mxf4 (block-scaled FP4) tensor cores: bits
+                                 expanded to E2M1 0.0 / 1.0 (2 frames per byte), all block scales
+                                 2^0, fp32 accumulation -- every partial sum is an integer
+                                 < 2^24, so S_ab is exact for batches of < 2^24 frames; twice the
+                                 int8 MMA rate.  Exclusive with CPI_VARIANT_POPC. */
 
 /* Boundary policy of refocusing. */
 #define CPI_SKIP_RENORMALIZE 0  /* sample counts only if 0 <= c_A <= W-1 on both axes; mean */
@@ -141,7 +146,8 @@ cpi_status cpi_load_frames(cpi_ctx *ctx, const void *packed, int64_t n_frames, i
  *   S_a[p] += sum_i A^i_p,  S_b[q] += sum_i B^i_q,  N_TOT += n_frames,
  *   S_ab[p][q] += sum_i A^i_p B^i_q   (int32, exact; N_TOT < 2^31)
  * on the device: bits are expanded to K-major uint8 operands ("bit-unpacking") and
- * S_ab runs on tcgen05 kind::i8 (CPI_VARIANT_TC) or popcount(AND) (CPI_VARIANT_POPC).
+ * S_ab runs on tcgen05 kind::i8 (CPI_VARIANT_TC), kind::mxf4 (CPI_VARIANT_FP4) or popcount(AND)
+ * (CPI_VARIANT_POPC).
  * If gamma_dev != NULL the GEMM epilogue also writes Gamma for the accumulated totals
  * (fused normalisation, see cpi_finalize for the formula) into gamma_dev [P_a][P_b].
  * Without CPI_KEEP_COUNTS only one correlate per cpi_reset is allowed (nothing to

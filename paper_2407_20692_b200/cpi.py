@@ -30,9 +30,9 @@ class Context:
                  bit_order: int = _lib.CPI_LSB_FIRST, device: int = 0, variant: str = "tc",
                  keep_counts: bool = False):
         self._lib = _lib.load()
-        flags = (_lib.CPI_VARIANT_POPC if variant == "popc" else _lib.CPI_VARIANT_TC)
-        if variant not in ("tc", "popc"):
-            raise ValueError("variant must be 'tc' or 'popc'")
+        if variant not in ("tc", "popc", "fp4"):
+            raise ValueError("variant must be 'tc', 'popc' or 'fp4'")
+        flags = {"tc": _lib.CPI_VARIANT_TC, "popc": _lib.CPI_VARIANT_POPC, "fp4": _lib.CPI_VARIANT_FP4}[variant]
         if keep_counts:
             flags |= _lib.CPI_KEEP_COUNTS
         cfg = _lib.Config(_lib.Layout(width, height, bit_order), _lib.Roi(*roi_a), _lib.Roi(*roi_b),

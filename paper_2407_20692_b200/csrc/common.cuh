@@ -213,6 +213,25 @@ __device__ __forceinline__ void mma_i8_2sm(uint32_t d_tmem, uint64_t adesc, uint
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// D[tmem] (+)= A * B^T, kind::mxf4 block-scaled (E2M1 x E2M1 -> F32, K = 64 per MMA, one
+// UE8M0 scale per 32 K elements read from TMEM at sfa / sfb), CTA pair.
+__device__ __forceinline__ void mma_mxf4_2sm(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t sfa_tmem, uint32_t sfb_tmem, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(sfa_tmem), "r"(sfb_tmem), "r"(accumulate)
+        : "memory");
+}
+// Fill 16 TMEM columns of this warp's 32-lane quadrant with one 32-bit value.
+__device__ __forceinline__ void tmem_fill_x16(uint32_t taddr, uint32_t v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1};"
+        ::"r"(taddr), "r"(v)
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 // Leader only: arrive once on the barrier at this offset in both CTAs of the pair when the
 // previously issued MMAs complete.
 __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
@@ -243,6 +262,15 @@ __host__ __device__ constexpr uint32_t idesc_u8_s32(int M, int N) {
            | (0u << 7) | (0u << 10)                    // a/b format = UINT8
            | (0u << 15) | (0u << 16)                   // K-major A and B
            | (static_cast<uint32_t>(N >> 3) << 17)     // N / 8
+           | (static_cast<uint32_t>(M >> 4) << 24);    // M / 16
+}
+
+// Instruction descriptor, kind::mxf4 block-scaled: A = B = E2M1 (1), both K-major, scale
+// factors UE8M0 (bit 23), scale-factor ids 0, dense K = 64.
+__host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
+    return (1u << 7) | (1u << 10)                      // a/b format = E2M1
+           | (static_cast<uint32_t>(N >> 3) << 17)     // N / 8
+           | (1u << 23)                                // scale format UE8M0
            | (static_cast<uint32_t>(M >> 4) << 24);    // M / 16
 }
 

@@ -35,6 +35,8 @@ struct cpi_ctx {
     int dev = 0;
     int num_sms = 148;
     bool popc = false, keep = false, pair = true;   // pair: cta_group::2 GEMM
+    bool fp4 = false;                      // kind::mxf4 GEMM on E2M1 operands (2 frames per byte)
+    int64_t k_align = 128;                 // frames per GEMM K block
     int64_t p_a = 0, p_b = 0;
     int64_t rows_a = 0, rows_b = 0;        // padded operand rows
     int64_t k_cap = 0;                     // frames capacity rounded to 128
@@ -264,8 +266,12 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
     if (cfg->max_frames < 1) return fail(nullptr, CPI_ERR_INVALID_ARG, "max_frames must be >= 1");
     if (cfg->max_frames >= (int64_t(1) << 31) - kKAlign)
         return fail(nullptr, CPI_ERR_INVALID_ARG, "max_frames must be < 2^31 (int32 sums)");
-    if (cfg->flags & ~(CPI_VARIANT_POPC | CPI_KEEP_COUNTS))
+    if (cfg->flags & ~(CPI_VARIANT_POPC | CPI_KEEP_COUNTS | CPI_VARIANT_FP4))
         return fail(nullptr, CPI_ERR_INVALID_ARG, "unknown flags 0x%x", cfg->flags);
+    if ((cfg->flags & CPI_VARIANT_POPC) && (cfg->flags & CPI_VARIANT_FP4))
+        return fail(nullptr, CPI_ERR_INVALID_ARG, "CPI_VARIANT_POPC and CPI_VARIANT_FP4 are exclusive");
+    if ((cfg->flags & CPI_VARIANT_FP4) && cfg->max_frames >= (int64_t(1) << 24))
+        return fail(nullptr, CPI_ERR_INVALID_ARG, "CPI_VARIANT_FP4 needs max_frames < 2^24 (exact fp32 sums)");
 
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -285,15 +291,22 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
     c->dev = cfg->device;
     c->num_sms = prop.multiProcessorCount;
     c->popc = (cfg->flags & CPI_VARIANT_POPC) != 0;
+    c->fp4 = (cfg->flags & CPI_VARIANT_FP4) != 0;
     c->keep = (cfg->flags & CPI_KEEP_COUNTS) != 0;
     c->p_a = int64_t(cfg->roi_a.width) * cfg->roi_a.height;
     c->p_b = int64_t(cfg->roi_b.width) * cfg->roi_b.height;
-    c->k_cap = round_up(cfg->max_frames, kKAlign);
+    c->k_align = c->fp4 ? 2 * kKAlign : kKAlign;
+    c->k_cap = round_up(cfg->max_frames, c->k_align);
     c->frame_bytes = int64_t(L.width_px / 8) * L.height_px;
     if (c->popc) {
         c->rows_a = round_up(c->p_a, cpi::gemm_popc_block());
         c->rows_b = round_up(c->p_b, cpi::gemm_popc_block());
         c->ld_op = c->k_cap / 32;   // 32-bit words
+    } else if (c->fp4) {
+        c->pair = true;
+        c->rows_a = round_up(c->p_a, cpi::gemm_tc2_block_m());
+        c->rows_b = round_up(c->p_b, cpi::gemm_f4_block_n());
+        c->ld_op = c->k_cap / 2;    // bytes (2 frames per byte)
     } else {
         c->pair = getenv("CPI_GEMM_1CTA") == nullptr;
         c->rows_a = round_up(c->p_a, c->pair ? cpi::gemm_tc2_block_m() : cpi::gemm_tc_block_m());
@@ -329,7 +342,8 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
     }
     if (!c->popc) {
         const uint32_t box_a = c->pair ? cpi::gemm_tc2_box_rows() : cpi::gemm_tc_block_m();
-        const uint32_t box_b = c->pair ? cpi::gemm_tc2_box_rows() : cpi::gemm_tc_block_n();
+        const uint32_t box_b = c->fp4 ? cpi::gemm_f4_box_rows_b() : c->pair ? cpi::gemm_tc2_box_rows()
+                                                                            : cpi::gemm_tc_block_n();
         cpi_status s = make_tmap(c, &c->tm_a, c->op_a, c->rows_a, c->ld_op, box_a);
         if (s == CPI_OK) s = make_tmap(c, &c->tm_b, c->op_b, c->rows_b, c->ld_op, box_b);
         if (s != CPI_OK) {
@@ -393,16 +407,17 @@ namespace {
 cpi_status expand_batch(cpi_ctx* c, cudaStream_t st) {
     const int64_t n = c->n_cur;
     const cpi_layout& L = c->cfg.layout;
-    const int64_t k_pad = round_up(n, kKAlign);
+    const int64_t k_pad = round_up(n, c->k_align);
+    const int mode = c->popc ? cpi::kExpandBits : c->fp4 ? cpi::kExpandE2M1 : cpi::kExpandU8;
     TimedScope ts(c, KC_EXPAND, st);
     const cpi::RoiDev ra{c->cfg.roi_a.x0, c->cfg.roi_a.y0, c->cfg.roi_a.width, c->cfg.roi_a.height};
     const cpi::RoiDev rb{c->cfg.roi_b.x0, c->cfg.roi_b.y0, c->cfg.roi_b.width, c->cfg.roi_b.height};
     if (c->cur_buf >= 0) CK(c, cudaStreamWaitEvent(st, c->ev_loaded[c->cur_buf], 0));
     if (n > 0) {
         cpi::launch_expand(c->frames_cur, n, L.width_px / 8, L.height_px, L.bit_order, ra, c->op_a,
-                           c->ld_op, k_pad, c->s_a, c->popc, st);
+                           c->ld_op, k_pad, c->s_a, mode, st);
         cpi::launch_expand(c->frames_cur, n, L.width_px / 8, L.height_px, L.bit_order, rb, c->op_b,
-                           c->ld_op, k_pad, c->s_b, c->popc, st);
+                           c->ld_op, k_pad, c->s_b, mode, st);
         c->launches += 2;
         CK(c, cudaGetLastError());
     }
@@ -430,7 +445,7 @@ cpi_status ensure_counts(cpi_ctx* c, cudaStream_t st) {
 
 // Pair-sum GEMM (+ fused Gamma) over A pixel rows [row0, row0 + rows) of the expanded batch.
 cpi_status gemm_rows(cpi_ctx* c, int64_t row0, int64_t rows, float* gamma, cudaStream_t st) {
-    const int64_t k_pad = round_up(c->n_cur, kKAlign);
+    const int64_t k_pad = round_up(c->n_cur, c->k_align);
     cpi::Epilogue epi{};
     epi.s_a = c->s_a;
     epi.s_b = c->s_b;
@@ -455,6 +470,12 @@ cpi_status gemm_rows(cpi_ctx* c, int64_t row0, int64_t rows, float* gamma, cudaS
         epi.m_tile0 = static_cast<int>(row0 / T);
         e = cpi::launch_gemm_popc(static_cast<const uint32_t*>(c->op_a), static_cast<const uint32_t*>(c->op_b),
                                   c->ld_op, k_pad / 32, epi, st);
+    } else if (c->fp4) {
+        const int64_t bm = cpi::gemm_tc2_block_m();
+        epi.m_tile0 = static_cast<int>(row0 / bm);
+        e = cpi::launch_gemm_f4(&c->tm_a, &c->tm_b, static_cast<int>((rows + bm - 1) / bm),
+                                static_cast<int>(c->rows_b / cpi::gemm_f4_block_n()),
+                                static_cast<int>(k_pad / c->k_align), epi, c->num_sms, st);
     } else if (c->pair) {
         const int64_t bm = cpi::gemm_tc2_block_m();
         epi.m_tile0 = static_cast<int>(row0 / bm);

@@ -10,7 +10,8 @@
 // lane produces 4 consecutive frames of it, so a warp stores 128 contiguous bytes of the
 // pixel's K-major operand row (fully coalesced).  Frames in [n, k_pad) are written as
 // zeros, so the GEMM's K tail is inert.  The bit-stream variant (KB3 operand) ballots the
-// same bits into pixel-major 32-bit words (bit f%32 of word f/32 = frame f).
+// same bits into pixel-major 32-bit words (bit f%32 of word f/32 = frame f); the E2M1
+// variant (FP4 GEMM operand) writes 4 frames as 4 nibbles (0x2 = 1.0), 64 B per warp.
 #include "kernels.h"
 
 namespace cpi {
@@ -22,7 +23,7 @@ constexpr int kFramesCta = 512; // frames per CTA
 constexpr int kRowStride = 65;  // bytes per staged frame row: odd word stride -> no bank conflicts
 constexpr int kMaxWidth = 512;
 
-template <bool kBits>
+template <int kMode>
 __global__ void __launch_bounds__(kThreads)
 expand_kernel(const uint8_t* __restrict__ frames, int64_t n, int row_bytes, int frame_h, int msb,
               RoiDev roi, void* __restrict__ op, int64_t ld, int64_t k_pad, int32_t* __restrict__ s) {
@@ -52,7 +53,18 @@ expand_kernel(const uint8_t* __restrict__ frames, int64_t n, int row_bytes, int 
             const int sh = msb ? 7 - (col & 7) : (col & 7);
             const int64_t prow = static_cast<int64_t>(m) * roi.w + j;
             int c;
-            if constexpr (!kBits) {
+            if constexpr (kMode == kExpandE2M1) {
+                // 4 frames -> 4 nibbles (E2M1 1.0 = 0x2), frame f in nibble f % 2 of byte f / 2
+                uint32_t word = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    word |= static_cast<uint32_t>((sbits[(4 * lane + k) * kRowStride + b] >> sh) & 1) << (4 * k + 1);
+                *reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(op) + prow * ld + ((f0 + 4 * lane) >> 1)) =
+                    static_cast<uint16_t>(word);
+                c = __popc(word);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            } else if constexpr (kMode == kExpandU8) {
                 uint32_t word = 0;
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
@@ -86,16 +98,19 @@ expand_kernel(const uint8_t* __restrict__ frames, int64_t n, int row_bytes, int 
 }  // namespace
 
 void launch_expand(const uint8_t* frames, int64_t n, int row_bytes, int frame_h, int msb,
-                   RoiDev roi, void* op, int64_t ld, int64_t k_pad, int32_t* s, bool bitstreams,
+                   RoiDev roi, void* op, int64_t ld, int64_t k_pad, int32_t* s, int mode,
                    cudaStream_t st) {
     if (k_pad <= 0) return;
     dim3 grid(static_cast<unsigned>((k_pad + kFramesCta - 1) / kFramesCta), roi.h);
-    if (bitstreams)
-        expand_kernel<true><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
-                                                       ld, k_pad, s);
+    if (mode == kExpandBits)
+        expand_kernel<kExpandBits><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
+                                                              ld, k_pad, s);
+    else if (mode == kExpandE2M1)
+        expand_kernel<kExpandE2M1><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
+                                                              ld, k_pad, s);
     else
-        expand_kernel<false><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
-                                                        ld, k_pad, s);
+        expand_kernel<kExpandU8><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
+                                                            ld, k_pad, s);
 }
 
 }  // namespace cpi

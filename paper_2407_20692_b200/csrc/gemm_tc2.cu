@@ -18,16 +18,28 @@
 namespace cpi {
 namespace {
 
-constexpr int BM = 256, BN = 256, BK = 128;       // pair tile; BK in bytes
-constexpr int HM = BM / 2, HN = BN / 2;           // per-CTA halves
-constexpr int kStages = 6;
-constexpr int kABytes = HM * BK;                  // 16 KB
-constexpr int kBBytes = HN * BK;                  // 16 KB
-constexpr int kStageBytes = kABytes + kBBytes;    // per CTA
+// kF4 = false: kind::i8, u8 operands (1 frame per byte), BN = 256, accumulators in TMEM
+//              columns [0, 512).
+// kF4 = true:  kind::mxf4 block-scaled, E2M1 operands (2 frames per byte), BN = 224 so that
+//              the two accumulators (448 columns) leave room for the scale factors (all
+//              2^0 = UE8M0 127) in columns [448, 480); fp32 accumulators hold exact integers.
+// BK = 128 bytes of K per stage in both (128 frames i8, 256 frames fp4); each MMA consumes
+// 32 bytes of K (K = 32 u8 or K = 64 e2m1).
+template <bool kF4>
+struct Tc2 {
+    static constexpr int BM = 256, BN = kF4 ? 224 : 256, BK = 128;
+    static constexpr int HM = BM / 2, HN = BN / 2;          // per-CTA halves
+    static constexpr int kStages = 6;
+    static constexpr int kABytes = HM * BK;                 // 16 KB
+    static constexpr int kBBytes = HN * BK;                 // 16 / 14 KB
+    static constexpr int kStageBytes = kABytes + kBBytes;   // per CTA
+    static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + 2 * BN * 4;
+    static constexpr uint32_t kSfCol = 448;                 // fp4: SFA at 448, SFB at 464
+};
+constexpr int BM = 256, BK = 128;
 constexpr int kThreads = 192;
-constexpr int kTmemCols = 512;                    // 2 accumulators x 256 columns
+constexpr int kTmemCols = 512;
 constexpr int kGroupM = 8;                        // pair-tile rows per raster group
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + 2 * BN * 4;
 
 __device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int& tm, int& tn) {
     const int group = kGroupM * n_tiles;
@@ -39,9 +51,13 @@ __device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int
     tn = r / gm;
 }
 
+template <bool kF4>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                    int m_tiles, int n_tiles, int k_blocks, Epilogue epi) {
+    using P = Tc2<kF4>;
+    constexpr int BN = P::BN, HM = P::HM, HN = P::HN, kStages = P::kStages;
+    constexpr int kABytes = P::kABytes, kBBytes = P::kBBytes, kStageBytes = P::kStageBytes;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sA = smem;
     uint8_t* sB = smem + kStages * kABytes;
@@ -74,6 +90,17 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if constexpr (kF4) {
+        // block scale factors 2^0 (UE8M0 127) in every lane of the SF columns of both CTAs
+        if (warp < 4) {
+            const uint32_t lane_base = tmem_base + (static_cast<uint32_t>(32 * warp) << 16) + P::kSfCol;
+            tmem_fill_x16(lane_base, 0x7F7F7F7Fu);
+            tmem_fill_x16(lane_base + 16, 0x7F7F7F7Fu);
+        }
+        tc_fence_before();
+        cluster_sync();
+        tc_fence_after();
+    }
     const int num_tiles = m_tiles * n_tiles;
     const int pair = blockIdx.x >> 1, num_pairs = gridDim.x >> 1;
 
@@ -102,7 +129,8 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
         }
     } else if (warp == kMmaWarp) {
         if (leader && lane == 0) {
-            constexpr uint32_t idesc = idesc_u8_s32(BM, BN);
+            constexpr uint32_t idesc = kF4 ? idesc_mxf4(BM, BN) : idesc_u8_s32(BM, BN);
+            const uint32_t sfa = tmem_base + P::kSfCol, sfb = tmem_base + P::kSfCol + 16;
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
@@ -118,9 +146,14 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
                     const uint32_t a0 = smem_u32(sA + stage * kABytes);
                     const uint32_t b0 = smem_u32(sB + stage * kBBytes);
 #pragma unroll
-                    for (int k = 0; k < BK / 32; ++k)
-                        mma_i8_2sm(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), idesc,
-                                   (kb | k) != 0);
+                    for (int k = 0; k < BK / 32; ++k) {
+                        if constexpr (kF4)
+                            mma_mxf4_2sm(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), idesc, sfa, sfb,
+                                         (kb | k) != 0);
+                        else
+                            mma_i8_2sm(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), idesc,
+                                       (kb | k) != 0);
+                    }
                     mma_commit_2sm(&empty[stage]);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
@@ -157,6 +190,10 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(taddr + 32 * c, r);
                 tmem_wait_ld();
+                if constexpr (kF4) {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) r[e] = static_cast<uint32_t>(__float2int_rn(__uint_as_float(r[e])));
+                }
                 const int col0 = tn * BN + 32 * c;
                 if (row_ok && col0 < epi.p_b) {
                     int32_t* cp = epi.counts ? epi.counts + static_cast<int64_t>(row) * epi.ldc + col0 : nullptr;
@@ -193,25 +230,39 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
 }  // namespace
 
 int gemm_tc2_block_m() { return BM; }
-int gemm_tc2_block_n() { return BN; }
-int gemm_tc2_box_rows() { return HM; }
+int gemm_tc2_block_n() { return Tc2<false>::BN; }
+int gemm_tc2_box_rows() { return Tc2<false>::HM; }
+int gemm_f4_block_n() { return Tc2<true>::BN; }
+int gemm_f4_box_rows_b() { return Tc2<true>::HN; }
 
-cudaError_t launch_gemm_tc2(const CUtensorMap* tma_a, const CUtensorMap* tma_b, int m_tiles,
-                            int n_tiles, int k_blocks, const Epilogue& epi, int num_sms,
-                            cudaStream_t st) {
+template <bool kF4>
+static cudaError_t launch_tc2(const CUtensorMap* tma_a, const CUtensorMap* tma_b, int m_tiles, int n_tiles,
+                              int k_blocks, const Epilogue& epi, int num_sms, cudaStream_t st) {
     static bool attr_done = false;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_i8_tc2_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaError_t e = cudaFuncSetAttribute(gemm_i8_tc2_kernel<kF4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Tc2<kF4>::kSmemBytes);
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
     const int tiles = m_tiles * n_tiles;
     int pairs = num_sms / 2;
     if (tiles < pairs) pairs = tiles;
-    gemm_i8_tc2_kernel<<<2 * pairs, kThreads, kSmemBytes, st>>>(*tma_a, *tma_b, m_tiles, n_tiles,
-                                                                 k_blocks, epi);
+    gemm_i8_tc2_kernel<kF4><<<2 * pairs, kThreads, Tc2<kF4>::kSmemBytes, st>>>(*tma_a, *tma_b, m_tiles, n_tiles,
+                                                                             k_blocks, epi);
     return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_tc2(const CUtensorMap* tma_a, const CUtensorMap* tma_b, int m_tiles,
+                            int n_tiles, int k_blocks, const Epilogue& epi, int num_sms,
+                            cudaStream_t st) {
+    return launch_tc2<false>(tma_a, tma_b, m_tiles, n_tiles, k_blocks, epi, num_sms, st);
+}
+
+cudaError_t launch_gemm_f4(const CUtensorMap* tma_a, const CUtensorMap* tma_b, int m_tiles,
+                           int n_tiles, int k_blocks, const Epilogue& epi, int num_sms,
+                           cudaStream_t st) {
+    return launch_tc2<true>(tma_a, tma_b, m_tiles, n_tiles, k_blocks, epi, num_sms, st);
 }
 
 }  // namespace cpi

@@ -27,11 +27,13 @@ struct Epilogue {
     int m_tile0;          // first M tile of this launch (row panels: cpi_correlate_rows)
 };
 
-// KB1: expand one RoI of packed frames into a K-major operand (bytes 0/1, or packed
-// pixel-major 32-bit bit streams when `bitstreams`), zero-filling frames [n, k_pad),
-// and accumulate the single-pixel sums into s[P].
+// KB1: expand one RoI of packed frames into a K-major operand, zero-filling frames [n, k_pad),
+// and accumulate the single-pixel sums into s[P].  mode: kExpandU8 bytes 0/1 (kind::i8),
+// kExpandBits pixel-major 32-bit bit streams (popcount), kExpandE2M1 nibbles 0x0 / 0x2
+// (E2M1 0.0 / 1.0, frame 2i in the low nibble of byte i; kind::mxf4).
+enum { kExpandU8 = 0, kExpandBits = 1, kExpandE2M1 = 2 };
 void launch_expand(const uint8_t* frames, int64_t n, int row_bytes, int frame_h, int msb,
-                   RoiDev roi, void* op, int64_t ld, int64_t k_pad, int32_t* s, bool bitstreams,
+                   RoiDev roi, void* op, int64_t ld, int64_t k_pad, int32_t* s, int mode,
                    cudaStream_t st);
 
 // KB2: persistent tcgen05 kind::i8 GEMM  S = A^T B  (A: [M_pad][K] u8, B: [N_pad][K] u8,
@@ -49,6 +51,13 @@ cudaError_t launch_gemm_tc2(const CUtensorMap* tma_a, const CUtensorMap* tma_b, 
 int gemm_tc2_block_m();
 int gemm_tc2_block_n();
 int gemm_tc2_box_rows();
+// KB2 FP4 variant (tcgen05 kind::mxf4, all block scales 2^0): E2M1 operands with 2 frames
+// per byte, K-major, 128-B swizzle; M = 256, N = 224 per pair; k_blocks of 256 frames.
+cudaError_t launch_gemm_f4(const CUtensorMap* tma_a, const CUtensorMap* tma_b, int m_tiles,
+                           int n_tiles, int k_blocks, const Epilogue& epi, int num_sms,
+                           cudaStream_t st);
+int gemm_f4_block_n();
+int gemm_f4_box_rows_b();
 
 // KB3: popcount(AND) GEMM on CUDA cores over 32-bit bit streams [rows][ldw].
 cudaError_t launch_gemm_popc(const uint32_t* a, const uint32_t* b, int64_t ldw, int64_t kw,

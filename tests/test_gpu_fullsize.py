@@ -66,9 +66,12 @@ def test_fullsize_gamma_bench_configuration(frames, oracle_rows):
     assert np.all(np.abs(got_p - R) <= 1e-6 * M + 1e-30), np.max(np.abs(got_p - R) / np.maximum(M, 1e-300))
 
 
-def test_fullsize_counts_exact(frames, oracle_rows):
+@pytest.mark.parametrize("variant", ["tc", "fp4"])
+def test_fullsize_counts_exact(frames, oracle_rows, variant):
+    """configs[1] kept counts (tcgen05 kind::i8, and the kind::mxf4 FP4 variant): sampled rows
+    bit-exact, marginals exact, whole-matrix row/column/total sums equal the closed forms."""
     from paper_2407_20692_b200 import Context
-    ctx = Context(synth.ROI_FULL_A, synth.ROI_FULL_B, 10_000, keep_counts=True)
+    ctx = Context(synth.ROI_FULL_A, synth.ROI_FULL_B, 10_000, keep_counts=True, variant=variant)
     ctx.load_frames(frames)
     ctx.correlate(None)
     s_ab = torch.empty((65536, 65536), dtype=torch.int32, device="cuda")

@@ -68,7 +68,7 @@ def _check_sums(got, want):
     assert got["n"] == want["n"]
 
 
-@pytest.mark.parametrize("variant", ["tc", "popc"])
+@pytest.mark.parametrize("variant", ["tc", "popc", "fp4"])
 def test_tiny_config_bit_exact(variant):
     """BASELINE configs[0]: 8x8 rho_a x 4x4 rho_b (non byte-aligned), 1000 frames."""
     fr = synth.bernoulli_frames(1000, 0.05, seed=synth.SEED_ARMS)
@@ -78,8 +78,8 @@ def test_tiny_config_bit_exact(variant):
     _assert_gamma(got["gamma"], want["gamma"])
 
 
-@pytest.mark.parametrize("variant", ["tc", "popc"])
-@pytest.mark.parametrize("n", [1, 31, 127, 129, 1000, 2600])
+@pytest.mark.parametrize("variant", ["tc", "popc", "fp4"])
+@pytest.mark.parametrize("n", [1, 31, 127, 129, 255, 257, 1000, 2600])
 def test_ragged_tiles_and_k_tails(variant, n):
     """Several M/N tiles with ragged edges (P_a = 1500, P_b = 380) and K tails (N not a
     multiple of 128): zero padding must be inert."""
@@ -91,13 +91,14 @@ def test_ragged_tiles_and_k_tails(variant, n):
     _assert_gamma(got["gamma"], want["gamma"])
 
 
-def test_chaotic_light_dense_and_identities():
+@pytest.mark.parametrize("variant", ["tc", "fp4"])
+def test_chaotic_light_dense_and_identities(variant):
     """Correlated (speckle) data with exact identities: same RoI on both arms -> S_ab
     symmetric; Gamma diagonal = f(1-f) (exact rational), checked through the GPU path."""
     roi = (10, 20, 40, 24)
     fr = synth.speckle_frames(3000, roi, (300, 20, 40, 24), f=0.3, grain=3, shift_b=(0, 0))
     want = oracle.correlate(fr, roi, roi)
-    got = _gpu_sums(fr, roi, roi, "tc")
+    got = _gpu_sums(fr, roi, roi, variant)
     _check_sums(got, want)
     np.testing.assert_array_equal(got["s_ab"], got["s_ab"].T)
     _assert_gamma(got["gamma"], want["gamma"])
@@ -111,6 +112,9 @@ def test_multi_batch_accumulation_and_virtual_ranks():
     fr = synth.bernoulli_frames(3000, 0.1, seed=5)
     one = _gpu_sums(fr, roi_a, roi_b, "tc")
     three = _gpu_sums(fr, roi_a, roi_b, "tc", batches=[1000, 1, 1999])
+    three_f4 = _gpu_sums(fr, roi_a, roi_b, "fp4", batches=[1000, 1, 1999])
+    _check_sums(three_f4, one)
+    np.testing.assert_array_equal(three_f4["gamma"], one["gamma"])
     _check_sums(three, one)
     np.testing.assert_array_equal(three["gamma"], one["gamma"])
     parts = [_gpu_sums(fr[a:b], roi_a, roi_b, "tc", gamma=False) for a, b in [(0, 700), (700, 2048), (2048, 3000)]]
@@ -305,7 +309,7 @@ def test_refocus_repeat_bit_identical():
         assert torch.equal(same[s], same[0])
 
 
-@pytest.mark.parametrize("variant", ["tc", "popc"])
+@pytest.mark.parametrize("variant", ["tc", "popc", "fp4"])
 def test_correlate_rows_panels_match_full(variant):
     """cpi_correlate_rows (SURVEY §8(e) panelised GEMM): covering A pixels with aligned row
     panels, over two accumulated batches with different panel splits, gives counts and
