@@ -2,9 +2,9 @@
 """bench.py — CPI hot path on B200: frames -> Gamma (Eq. 1) -> refocused plane stack.
 
 One *step* = one pass of the whole hot path over one batch:
-  N frames resident in HBM -> expand + marginals (KB1) -> S_ab on tcgen05 kind::i8 with
-  the fused exact normalisation (KB2) -> fp32 Gamma -> refocus into a P-plane stack
-  (KB5a/KB5/KB6).
+  N frames resident in HBM -> expand + marginals (KB1) -> S_ab on tcgen05 tensor cores
+  (default kind::mxf4 on E2M1 0/1 operands, exact; --variant tc = kind::i8) with the fused
+  exact normalisation (KB2) -> fp32 Gamma -> refocus into a P-plane stack (KB5a/KB5/KB6).
 Workload at N=1 (BASELINE.json configs[1] + configs[3]): SwissSPAD2 256x512 frames,
 rho_a = left 256x256 half, rho_b = right 256x256 half, 10^4
 Bernoulli(0.05) frames per step, 64 refocus planes alpha = linspace(0.5, 2, 64).
@@ -48,7 +48,9 @@ def parse():
     p.add_argument("--frames", type=int, default=10_000, help="frames per step per rank")
     p.add_argument("--planes", type=int, default=64, help="refocus planes per step")
     p.add_argument("--occupancy", type=float, default=0.05, help="Bernoulli f of the synthetic bits")
-    p.add_argument("--variant", default="tc", choices=["tc", "popc", "fp4"])
+    p.add_argument("--variant", default="fp4", choices=["tc", "popc", "fp4"],
+                   help="pair-sum GEMM: fp4 = tcgen05 kind::mxf4 on E2M1 0/1 (default, exact), "
+                        "tc = kind::i8, popc = popcount(AND)")
     p.add_argument("--roi", default="full", choices=["full", "128", "tiny"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -421,7 +423,10 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8 x u8 -> s32 (S_ab), f64 -> f32 (Gamma), f32/f64 (refocus)",
+        "vs_baseline": None,
+        "dtype": {"tc": "u8 x u8 -> s32 (S_ab)", "popc": "u32 popc(and) -> s32 (S_ab)",
+                  "fp4": "e2m1 {0,1} x e2m1 -> f32 exact integers -> s32 (S_ab)"}[args.variant]
+                 + ", f64 -> f32 (Gamma), f32/f64 (refocus)",
         "data": "synthetic",
         "config": {"workload": (f"configs[1] (+configs[3] stack): SwissSPAD2 256x512 frames, rho_a {roi_a}, "
                                 f"rho_b {roi_b}, {n} Bernoulli({args.occupancy}) frames per rank per step "
