@@ -52,6 +52,8 @@ def parse():
                    help="pair-sum GEMM: fp4 = tcgen05 kind::mxf4 on E2M1 0/1 (default, exact), "
                         "tc = kind::i8, popc = popcount(AND)")
     p.add_argument("--roi", default="full", choices=["full", "128", "tiny"])
+    p.add_argument("--gamma-order", default="ublocked", choices=["ublocked", "rowmajor"],
+                   help="column order of the step's Gamma (include/cpi.h CPI_GAMMA_UBLOCKED)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-rows", type=int, default=0, help="(unused; the sample size follows the core count)")
@@ -285,13 +287,15 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     if world == 1:
-        ctx = Context(roi_a, roi_b, n, device=local, variant=args.variant)
+        ctx = Context(roi_a, roi_b, n, device=local, variant=args.variant,
+                      gamma_blocked=args.gamma_order == "ublocked")
         gamma = ctx.new_gamma()
         planes = ctx.new_planes(args.planes)
     else:
         # frame-sharded pipeline (parallel.py): GEMM row panels reduce-scattered as they finish,
         # block-cyclic Gamma row ownership, shard refocus, plane all-reduce
-        backend = parallel.CudaBackend(roi_a, roi_b, n, device=local, variant=args.variant)
+        backend = parallel.CudaBackend(roi_a, roi_b, n, device=local, variant=args.variant,
+                                       gamma_blocked=args.gamma_order == "ublocked")
         ctx = backend.ctx
     planes_host = torch.empty((args.planes, Ha, Wa), dtype=torch.float32).pin_memory()
 
@@ -432,7 +436,7 @@ def main():
                                 f"rho_b {roi_b}, {n} Bernoulli({args.occupancy}) frames per rank per step "
                                 f"-> Gamma {p_a}x{p_b} -> {args.planes}-plane refocus stack"),
                    "frames_per_step_per_rank": n, "planes_per_step": args.planes,
-                   "alphas": "linspace(0.5, 2.0, P)", "variant": args.variant,
+                   "alphas": "linspace(0.5, 2.0, P)", "variant": args.variant, "gamma_order": args.gamma_order,
                    "parallelism": f"frame-sharded x{world}" if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (Gamma 17 GB, operands 1.3 GB) - no flush needed"},
         "gpu_launches": launches,

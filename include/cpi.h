@@ -73,6 +73,13 @@ typedef int32_t cpi_status;
                                  2^0, fp32 accumulation -- every partial sum is an integer
                                  < 2^24, so S_ab is exact for batches of < 2^24 frames; twice the
                                  int8 MMA rate.  Exclusive with CPI_VARIANT_POPC. */
+#define CPI_GAMMA_UBLOCKED 8u /* B pixels are ordered u-blocked everywhere in this context: B pixel
+                                 q = v*W_b + u has index (u/8)*(8*H_b) + 8*v + u%8 in S_b, in the
+                                 columns of S_ab and of every Gamma it writes or cpi_refocus reads
+                                 (A pixels and rows unchanged).  The GEMM then produces, and
+                                 refocusing stages, each 8 u x 8 v block as one contiguous 256-B
+                                 segment (faster refocus, same arithmetic).  Needs
+                                 roi_b.width % 8 == 0. */
 
 /* Boundary policy of refocusing. */
 #define CPI_SKIP_RENORMALIZE 0  /* sample counts only if 0 <= c_A <= W-1 on both axes; mean */

@@ -28,13 +28,15 @@ class Context:
 
     def __init__(self, roi_a, roi_b, max_frames: int, *, width: int = FRAME_W, height: int = FRAME_H,
                  bit_order: int = _lib.CPI_LSB_FIRST, device: int = 0, variant: str = "tc",
-                 keep_counts: bool = False):
+                 keep_counts: bool = False, gamma_blocked: bool = False):
         self._lib = _lib.load()
         if variant not in ("tc", "popc", "fp4"):
             raise ValueError("variant must be 'tc', 'popc' or 'fp4'")
         flags = {"tc": _lib.CPI_VARIANT_TC, "popc": _lib.CPI_VARIANT_POPC, "fp4": _lib.CPI_VARIANT_FP4}[variant]
         if keep_counts:
             flags |= _lib.CPI_KEEP_COUNTS
+        if gamma_blocked:     # u-blocked Gamma column order (include/cpi.h CPI_GAMMA_UBLOCKED)
+            flags |= _lib.CPI_GAMMA_UBLOCKED
         cfg = _lib.Config(_lib.Layout(width, height, bit_order), _lib.Roi(*roi_a), _lib.Roi(*roi_b),
                           int(max_frames), int(device), flags)
         h = ctypes.c_void_p()
@@ -51,6 +53,7 @@ class Context:
         self.max_frames = int(max_frames)
         self.variant = variant
         self.keep_counts = keep_counts
+        self.gamma_blocked = gamma_blocked
         self._keep = []   # host buffers that must outlive an async copy
 
     # -- helpers ----------------------------------------------------------------------
@@ -207,6 +210,16 @@ class Context:
         torch = _torch()
         if not (g.is_cuda and g.dtype == torch.float32 and g.is_contiguous() and g.numel() >= self.p_a * self.p_b):
             raise ValueError("gamma must be a contiguous CUDA float32 tensor with P_a*P_b elements")
+
+    def b_index(self):
+        """Index of every B pixel q = v * W_b + u in S_b and in the columns of S_ab / Gamma
+        (identity unless gamma_blocked, include/cpi.h CPI_GAMMA_UBLOCKED)."""
+        Wb, Hb = self.roi_b[2], self.roi_b[3]
+        q = np.arange(Wb * Hb)
+        if not self.gamma_blocked:
+            return q
+        v, u = q // Wb, q % Wb
+        return (u // 8) * (8 * Hb) + 8 * v + (u % 8)
 
     def new_gamma(self):
         torch = _torch()

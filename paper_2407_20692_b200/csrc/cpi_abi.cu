@@ -36,6 +36,7 @@ struct cpi_ctx {
     int num_sms = 148;
     bool popc = false, keep = false, pair = true;   // pair: cta_group::2 GEMM
     bool fp4 = false;                      // kind::mxf4 GEMM on E2M1 operands (2 frames per byte)
+    bool ublocked = false;                 // B pixels in u-blocked order (CPI_GAMMA_UBLOCKED)
     int64_t k_align = 128;                 // frames per GEMM K block
     int64_t p_a = 0, p_b = 0;
     int64_t rows_a = 0, rows_b = 0;        // padded operand rows
@@ -266,7 +267,9 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
     if (cfg->max_frames < 1) return fail(nullptr, CPI_ERR_INVALID_ARG, "max_frames must be >= 1");
     if (cfg->max_frames >= (int64_t(1) << 31) - kKAlign)
         return fail(nullptr, CPI_ERR_INVALID_ARG, "max_frames must be < 2^31 (int32 sums)");
-    if (cfg->flags & ~(CPI_VARIANT_POPC | CPI_KEEP_COUNTS | CPI_VARIANT_FP4))
+    if ((cfg->flags & CPI_GAMMA_UBLOCKED) && cfg->roi_b.width % 8)
+        return fail(nullptr, CPI_ERR_UNSUPPORTED, "CPI_GAMMA_UBLOCKED needs roi_b.width %% 8 == 0");
+    if (cfg->flags & ~(CPI_VARIANT_POPC | CPI_KEEP_COUNTS | CPI_VARIANT_FP4 | CPI_GAMMA_UBLOCKED))
         return fail(nullptr, CPI_ERR_INVALID_ARG, "unknown flags 0x%x", cfg->flags);
     if ((cfg->flags & CPI_VARIANT_POPC) && (cfg->flags & CPI_VARIANT_FP4))
         return fail(nullptr, CPI_ERR_INVALID_ARG, "CPI_VARIANT_POPC and CPI_VARIANT_FP4 are exclusive");
@@ -296,6 +299,7 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
     c->p_a = int64_t(cfg->roi_a.width) * cfg->roi_a.height;
     c->p_b = int64_t(cfg->roi_b.width) * cfg->roi_b.height;
     c->k_align = c->fp4 ? 2 * kKAlign : kKAlign;
+    c->ublocked = (cfg->flags & CPI_GAMMA_UBLOCKED) != 0;
     c->k_cap = round_up(cfg->max_frames, c->k_align);
     c->frame_bytes = int64_t(L.width_px / 8) * L.height_px;
     if (c->popc) {
@@ -415,9 +419,9 @@ cpi_status expand_batch(cpi_ctx* c, cudaStream_t st) {
     if (c->cur_buf >= 0) CK(c, cudaStreamWaitEvent(st, c->ev_loaded[c->cur_buf], 0));
     if (n > 0) {
         cpi::launch_expand(c->frames_cur, n, L.width_px / 8, L.height_px, L.bit_order, ra, c->op_a,
-                           c->ld_op, k_pad, c->s_a, mode, st);
+                           c->ld_op, k_pad, c->s_a, mode, false, st);
         cpi::launch_expand(c->frames_cur, n, L.width_px / 8, L.height_px, L.bit_order, rb, c->op_b,
-                           c->ld_op, k_pad, c->s_b, mode, st);
+                           c->ld_op, k_pad, c->s_b, mode, c->ublocked, st);
         c->launches += 2;
         CK(c, cudaGetLastError());
     }
@@ -707,7 +711,23 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
         c->refocus_ready = true;
     }
     bool tma_now = c->use_s1_tma && (reinterpret_cast<uintptr_t>(spec->gamma_dev) & 15) == 0;
-    if (tma_now) {
+    if (c->ublocked && !tma_now)
+        return fail(c, CPI_ERR_UNSUPPORTED, "u-blocked Gamma needs the TMA stage 1 (W_a <= 256, W_b %% 4 == 0, "
+                                            "16-byte aligned Gamma)");
+    if (tma_now && c->ublocked) {
+        cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
+        // (u % 8, v, u / 8, j, m): box 8 x 8 x 1 x 32 x 1 lands as [j][v][u] like the 4D map
+        const cuuint64_t dims[5] = {8u, cuuint64_t(Hb), cuuint64_t(Wb / 8), cuuint64_t(Wa), cuuint64_t(spec->rows / Wa)};
+        const cuuint64_t strides[4] = {32u, cuuint64_t(Hb) * 32, cuuint64_t(c->p_b) * 4, cuuint64_t(Wa) * c->p_b * 4};
+        const cuuint32_t box[5] = {8u, 8u, 1u, 32u, 1u};
+        const cuuint32_t es[5] = {1u, 1u, 1u, 1u, 1u};
+        CUresult r = enc(&c->s1maps.gamma, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(spec->gamma_dev),
+                         dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(c, CPI_ERR_CUDA, "u-blocked Gamma tensor map failed (%d)", int(r));
+        c->s1maps.gamma_5d = 1;
+    } else if (tma_now) {
+        c->s1maps.gamma_5d = 0;
         cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
         const cuuint64_t dims[4] = {cuuint64_t(Wb), cuuint64_t(Hb), cuuint64_t(Wa), cuuint64_t(spec->rows / Wa)};
         const cuuint64_t strides[3] = {cuuint64_t(Wb) * 4, cuuint64_t(c->p_b) * 4, cuuint64_t(Wa) * c->p_b * 4};

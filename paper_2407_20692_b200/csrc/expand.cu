@@ -26,7 +26,8 @@ constexpr int kMaxWidth = 512;
 template <int kMode>
 __global__ void __launch_bounds__(kThreads)
 expand_kernel(const uint8_t* __restrict__ frames, int64_t n, int row_bytes, int frame_h, int msb,
-              RoiDev roi, void* __restrict__ op, int64_t ld, int64_t k_pad, int32_t* __restrict__ s) {
+              RoiDev roi, void* __restrict__ op, int64_t ld, int64_t k_pad, int32_t* __restrict__ s,
+              int ublocked) {
     __shared__ uint8_t sbits[kSub * kRowStride];
     __shared__ int cnt[kMaxWidth];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -51,7 +52,8 @@ expand_kernel(const uint8_t* __restrict__ frames, int64_t n, int row_bytes, int 
             const int col = roi.x0 + j;
             const int b = (col >> 3) - b0;
             const int sh = msb ? 7 - (col & 7) : (col & 7);
-            const int64_t prow = static_cast<int64_t>(m) * roi.w + j;
+            const int64_t prow = ublocked ? static_cast<int64_t>(j >> 3) * (8 * roi.h) + 8 * m + (j & 7)
+                                          : static_cast<int64_t>(m) * roi.w + j;
             int c;
             if constexpr (kMode == kExpandE2M1) {
                 // 4 frames -> 4 nibbles (E2M1 1.0 = 0x2), frame f in nibble f % 2 of byte f / 2
@@ -92,25 +94,27 @@ expand_kernel(const uint8_t* __restrict__ frames, int64_t n, int row_bytes, int 
     }
     __syncthreads();
     for (int j = tid; j < roi.w; j += kThreads)
-        if (cnt[j]) atomicAdd(s + static_cast<int64_t>(m) * roi.w + j, cnt[j]);
+        if (cnt[j])
+            atomicAdd(s + (ublocked ? static_cast<int64_t>(j >> 3) * (8 * roi.h) + 8 * m + (j & 7)
+                                    : static_cast<int64_t>(m) * roi.w + j), cnt[j]);
 }
 
 }  // namespace
 
 void launch_expand(const uint8_t* frames, int64_t n, int row_bytes, int frame_h, int msb,
                    RoiDev roi, void* op, int64_t ld, int64_t k_pad, int32_t* s, int mode,
-                   cudaStream_t st) {
+                   bool ublocked, cudaStream_t st) {
     if (k_pad <= 0) return;
     dim3 grid(static_cast<unsigned>((k_pad + kFramesCta - 1) / kFramesCta), roi.h);
     if (mode == kExpandBits)
         expand_kernel<kExpandBits><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
-                                                              ld, k_pad, s);
+                                                              ld, k_pad, s, ublocked ? 1 : 0);
     else if (mode == kExpandE2M1)
         expand_kernel<kExpandE2M1><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
-                                                              ld, k_pad, s);
+                                                              ld, k_pad, s, ublocked ? 1 : 0);
     else
         expand_kernel<kExpandU8><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
-                                                            ld, k_pad, s);
+                                                            ld, k_pad, s, ublocked ? 1 : 0);
 }
 
 }  // namespace cpi

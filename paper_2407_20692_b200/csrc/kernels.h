@@ -32,9 +32,11 @@ struct Epilogue {
 // kExpandBits pixel-major 32-bit bit streams (popcount), kExpandE2M1 nibbles 0x0 / 0x2
 // (E2M1 0.0 / 1.0, frame 2i in the low nibble of byte i; kind::mxf4).
 enum { kExpandU8 = 0, kExpandBits = 1, kExpandE2M1 = 2 };
+// ublocked: pixel (m, j) of the RoI is written to operand row / sum slot
+// (j / 8) * (8 * roi.h) + 8 * m + j % 8 instead of m * roi.w + j (CPI_GAMMA_UBLOCKED, B arm).
 void launch_expand(const uint8_t* frames, int64_t n, int row_bytes, int frame_h, int msb,
                    RoiDev roi, void* op, int64_t ld, int64_t k_pad, int32_t* s, int mode,
-                   cudaStream_t st);
+                   bool ublocked, cudaStream_t st);
 
 // KB2: persistent tcgen05 kind::i8 GEMM  S = A^T B  (A: [M_pad][K] u8, B: [N_pad][K] u8,
 // both K-major) with the fused epilogue.  k_blocks = K / 128.
@@ -87,8 +89,9 @@ cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int H
 // Gamma (4D: u, v, j, m) and of the packed x-tables (3D uint32: x, u, plane slot).
 constexpr int kRefocusMaxFuse = 4;
 struct Stage1Maps {
-    CUtensorMap gamma;
+    CUtensorMap gamma;       // 4D (u, v, j, m) row-major Gamma, or 5D (u%8, v, u/8, j, m) u-blocked
     CUtensorMap xtab;
+    int gamma_5d = 0;
 };
 bool stage1_tma_supported(int Wa, int Wb);
 cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa, int Ha, int Wb, int Hb,

@@ -258,6 +258,7 @@ struct S1Args {
     const int32_t* yhi[kRefocusMaxFuse];
     double* T[kRefocusMaxFuse];
     const uint32_t* xblk;                    // [F][n_chunks] x-block masks (OR-ed over F in smem)
+    int gamma_5d;                            // Gamma map is 5D u-blocked (u%8, v, u/8, j, m)
 };
 
 // global A row of the shard's local A row l (block-cyclic row ownership)
@@ -339,9 +340,14 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], nb * kTJBox * kTRow * 4 + F * kTUC * a.Wa * 4);
                     float* dst = sg + stage * kTGFloats;
-                    for (int b = 0; b < nb; ++b)
-                        tma_load_4d(dst + b * kTJBox * kTRow, &tm_g, &full[stage], c * kTUC, vg * kTVG,
-                                    sp.x + b * kTJBox, ml);
+                    for (int b = 0; b < nb; ++b) {
+                        if (a.gamma_5d)   // u-blocked Gamma: one 256-B segment per (j, chunk)
+                            tma_load_5d(dst + b * kTJBox * kTRow, &tm_g, &full[stage], 0, vg * kTVG, c,
+                                        sp.x + b * kTJBox, ml);
+                        else
+                            tma_load_4d(dst + b * kTJBox * kTRow, &tm_g, &full[stage], c * kTUC, vg * kTVG,
+                                        sp.x + b * kTJBox, ml);
+                    }
 #pragma unroll
                     for (int f = 0; f < F; ++f)
                         tma_load_3d(s1_smem + C::kOffX + (stage * F + f) * kTXEntries * 4, &tm_x, &full[stage], 0,
@@ -721,6 +727,7 @@ cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa
     a.n_vg = (Hb + kTVG - 1) / kTVG;
     a.n_chunks = (Wb + kTUC - 1) / kTUC;
     a.xblk = xblk;
+    a.gamma_5d = maps->gamma_5d;
     for (int f = 0; f < n_fuse; ++f) {
         a.xlo[f] = xs[f].lo; a.xhi[f] = xs[f].hi; a.ylo[f] = ys[f].lo; a.yhi[f] = ys[f].hi; a.T[f] = T[f];
     }

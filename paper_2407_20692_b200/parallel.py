@@ -170,9 +170,13 @@ class CudaBackend:
     panels (cpi_correlate_rows) whose pair sums are handed to the collectives in place
     (cpi_counts_dev views, no copies)."""
 
-    def __init__(self, roi_a, roi_b, max_frames: int, device: int = 0, variant: str = "tc"):
+    def __init__(self, roi_a, roi_b, max_frames: int, device: int = 0, variant: str = "tc",
+                 gamma_blocked: bool = False):
+        """gamma_blocked: B pixels in the u-blocked order (faster refocusing); S_b and the
+        columns of ShardResult.gamma_rows then follow ctx.b_index()."""
         from .cpi import Context
-        self.ctx = Context(roi_a, roi_b, max_frames, device=device, variant=variant, keep_counts=True)
+        self.ctx = Context(roi_a, roi_b, max_frames, device=device, variant=variant, keep_counts=True,
+                           gamma_blocked=gamma_blocked)
         self.device = torch.device(f"cuda:{device}")
         self.roi_a = roi_a
         self.row_align = self.ctx.row_align()

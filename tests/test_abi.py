@@ -67,6 +67,7 @@ def _cfg(lib_mod, roi_a=(0, 0, 256, 256), roi_b=(256, 0, 256, 256), w=512, h=256
     (dict(flags=0x80), -1),
     (dict(flags=0x1 | 0x4), -1),                    # POPC and FP4 are exclusive
     (dict(flags=0x4, max_frames=1 << 24), -1),      # FP4: exact fp32 sums need N < 2^24
+    (dict(flags=0x8, roi_b=(256, 0, 12, 8)), -12),  # u-blocked Gamma needs W_b % 8 == 0
     (dict(order=5), -1),
 ])
 def test_create_rejects_bad_config(lib, kw, status):

@@ -371,3 +371,46 @@ def test_refocus_block_cyclic_shards(block):
         assert np.all(np.abs(R - Ro) <= 1e-6 * M + 1e-30)
         total += R
     np.testing.assert_allclose(total, whole, rtol=1e-5, atol=1e-7)
+
+
+@pytest.mark.parametrize("variant,roi_b", [("tc", (256, 0, 16, 12)), ("fp4", (256, 0, 24, 10)),
+                                            ("popc", (260, 3, 40, 6))])
+def test_gamma_ublocked_layout(variant, roi_b):
+    """CPI_GAMMA_UBLOCKED: B pixels in u-blocked order everywhere (S_b, S_ab and Gamma columns,
+    fused epilogue, panels, cpi_finalize, cpi_finalize_counts) hold exactly the row-major
+    values at the permuted indices, and refocusing gives planes bit-identical to the
+    row-major path."""
+    roi_a = (0, 0, 24, 16)
+    fr = synth.bernoulli_frames(900, 0.2, seed=61)
+    ref = _ctx(roi_a, roi_b, 900, variant=variant, keep_counts=True)
+    blk = _ctx(roi_a, roi_b, 900, variant=variant, keep_counts=True, gamma_blocked=True)
+    g_ref, g_blk = ref.new_gamma(), blk.new_gamma()
+    for c, g in ((ref, g_ref), (blk, g_blk)):
+        c.load_frames(fr)
+        c.correlate(g)
+    idx = blk.b_index()
+    assert sorted(idx.tolist()) == list(range(roi_b[2] * roi_b[3]))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(g_blk.cpu().numpy()[:, idx], g_ref.cpu().numpy())
+    sr, sb = ref.counts_views(), blk.counts_views()
+    np.testing.assert_array_equal(sb[0].cpu().numpy()[:, idx], sr[0].cpu().numpy())
+    np.testing.assert_array_equal(sb[1].cpu().numpy(), sr[1].cpu().numpy())
+    np.testing.assert_array_equal(sb[2].cpu().numpy()[idx], sr[2].cpu().numpy())
+    al = [0.6, 1.0, 1.7]
+    p_ref, p_blk = ref.new_planes(3), blk.new_planes(3)
+    ref.refocus(al, g_ref, p_ref)
+    blk.refocus(al, g_blk, p_blk)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(p_blk.cpu().numpy(), p_ref.cpu().numpy())
+    # cpi_finalize and cpi_finalize_counts on the blocked sums
+    for c in (ref, blk):
+        c.load_frames(fr[:10])
+        c.correlate(None)
+    g2, g2r, g3 = blk.new_gamma(), ref.new_gamma(), blk.new_gamma()
+    blk.finalize(g2)
+    ref.finalize(g2r)
+    s_ab, s_a, s_b = blk.counts_views()
+    blk.finalize_counts(s_ab, 0, s_a, s_b, 910, g3)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(g2.cpu().numpy()[:, idx], g2r.cpu().numpy())
+    np.testing.assert_array_equal(g3.cpu().numpy(), g2.cpu().numpy())
