@@ -72,8 +72,9 @@ def _load():
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double]
             lib.oracle_interp4.restype = ctypes.c_double
             lib.oracle_refocus.argtypes = [P, i32, i32, i32, i32, i32, P, i32, i32, P, i64, P, P, i32]
+            lib.oracle_refocus_affine.argtypes = [P, i32, i32, i32, i32, i32, P, i32, i32, P, i64, P, P, i32]
             for f in ("oracle_unpack", "oracle_marginals", "oracle_pair_sums", "oracle_gamma",
-                      "oracle_gamma_spec", "oracle_refocus"):
+                      "oracle_gamma_spec", "oracle_refocus", "oracle_refocus_affine"):
                 getattr(lib, f).restype = ctypes.c_int
             _lib = lib
     return _lib
@@ -224,4 +225,44 @@ def refocus(g: np.ndarray, dims, alphas, boundary: int = BOUNDARY_SKIP, pixels=N
     if pixels is None:
         out = out.reshape(al.size, Ha, Wa)
         cnt = cnt.reshape(al.size, Ha, Wa)
+    return (out, cnt) if return_counts else out
+
+
+def default_map(alpha: float):
+    """The SPEC default map as a general affine map row (refocus_affine layout)."""
+    a = float(alpha)
+    b = 1.0 - a
+    return [a, b, 0.0, 0.0, 1.0, 0.0, a, b, 0.0, 0.0, 1.0, 0.0]
+
+
+def refocus_affine(g: np.ndarray, dims, maps, boundary: int = BOUNDARY_SKIP, pixels=None,
+                   threads: int = 0, return_counts: bool = False):
+    """Refocused planes under general affine maps (S:273 RefocusMap):
+    maps = [P][12] rows {ax, bx, cx, dx, ex, fx, ay, by, cy, dy, ey, fy} (see
+    cpi_oracle.c refocus_pixel_affine).  Output as refocus()."""
+    g = np.ascontiguousarray(g)
+    f32 = g.dtype == np.float32
+    if not f32:
+        g = np.ascontiguousarray(g, dtype=np.float64)
+    Wa, Ha, Wb, Hb = dims
+    if g.shape != (Wa * Ha, Wb * Hb):
+        raise ValueError("gamma must be [Wa*Ha][Wb*Hb]")
+    mp = np.ascontiguousarray(maps, dtype=np.float64).reshape(-1, 12)
+    if pixels is None:
+        pix = None
+        npix = Wa * Ha
+    else:
+        pix = np.ascontiguousarray(pixels, dtype=np.int32).reshape(-1, 2)
+        npix = pix.shape[0]
+    out = np.empty((mp.shape[0], npix), dtype=np.float64)
+    cnt = np.empty((mp.shape[0], npix), dtype=np.int64)
+    rc = _load().oracle_refocus_affine(_ptr(g), int(f32), Wa, Ha, Wb, Hb, _ptr(mp), mp.shape[0],
+                                       int(boundary), None if pix is None else _ptr(pix), npix,
+                                       _ptr(out), _ptr(cnt), int(threads))
+    if rc == -2:
+        raise ValueError("map coefficients must be finite")
+    _check(rc, "refocus_affine")
+    if pixels is None:
+        out = out.reshape(mp.shape[0], Ha, Wa)
+        cnt = cnt.reshape(mp.shape[0], Ha, Wa)
     return (out, cnt) if return_counts else out

@@ -12,7 +12,9 @@
  *   - refocusing: for every output pixel the mean over the angular (B) lattice of the
  *     4D multilinear interpolation of Gamma at plane-dependent coordinates
  *     ("Refocusing", "4D multilinear interpolation", S:274 default map,
- *     S:290-302 interp4/refocus_plane, SURVEY §8(c) Q10-Q14 readings).
+ *     S:290-302 interp4/refocus_plane, SURVEY §8(c) Q10-Q14 readings), for the default map
+ *     and for a general per-plane affine map of all four coordinates (S:273 RefocusMap,
+ *     SURVEY NEXT f3(ii)).
  *
  * Floating point: fp64 throughout; compile with -ffp-contract=off so every
  * a*b+c below is two rounded operations, exactly as written.
@@ -279,4 +281,77 @@ int oracle_refocus(const void *g, int g_f32, int Wa, int Ha, int Wb, int Hb,
     return 0;
 }
 
-int oracle_version(void) { return 1; }
+/* General RefocusMap: four affine coordinate functions per plane, each of the form
+ * a*x + b*u + c on the x axis (a*y + b*v + c on the y axis), with coordinates relative to the
+ * arm centres ("coordinates relative to centers"):
+ *   c_Ax = ((ax*(x - c_ax)) + (bx*(u - c_bx))) + cx  + c_ax
+ *   c_Bx = ((dx*(x - c_ax)) + (ex*(u - c_bx))) + fx  + c_bx
+ *   c_Ay = ((ay*(y - c_ay)) + (by*(v - c_by))) + cy  + c_ay
+ *   c_By = ((dy*(y - c_ay)) + (ey*(v - c_by))) + fy  + c_by
+ * map[12] = {ax, bx, cx, dx, ex, fx, ay, by, cy, dy, ey, fy}.  The default map is
+ * {a, 1 - a, 0, 0, 1, 0} on both axes (same values as refocus_pixel: adding +0.0 and
+ * c_B = u exactly).  boundary 0: a sample counts only if all four coordinates lie in their
+ * closed lattice intervals; boundary 1: each coordinate is clamped.  The sample value is
+ * interp4 (16 corners); output = sum / count (0 if no sample). */
+static double refocus_pixel_affine(const void *g, int g_f32, int Wa, int Ha, int Wb, int Hb,
+                                   const double *mp, int boundary, int x, int y, int64_t *count_out) {
+    const double cax = (Wa - 1) / 2.0, cay = (Ha - 1) / 2.0;
+    const double cbx = (Wb - 1) / 2.0, cby = (Hb - 1) / 2.0;
+    const double xr = (double)x - cax, yr = (double)y - cay;
+    double sum = 0.0;
+    int64_t cnt = 0;
+    for (int v = 0; v < Hb; v++) {
+        const double vr = (double)v - cby;
+        double cAy = (((mp[6] * yr) + (mp[7] * vr)) + mp[8]) + cay;
+        double cBy = (((mp[9] * yr) + (mp[10] * vr)) + mp[11]) + cby;
+        for (int u = 0; u < Wb; u++) {
+            const double ur = (double)u - cbx;
+            double cAx = (((mp[0] * xr) + (mp[1] * ur)) + mp[2]) + cax;
+            double cBx = (((mp[3] * xr) + (mp[4] * ur)) + mp[5]) + cbx;
+            double ay = cAy, by = cBy;
+            if (boundary == 0) {
+                if (!(cAx >= 0.0 && cAx <= (double)(Wa - 1))) continue;
+                if (!(cBx >= 0.0 && cBx <= (double)(Wb - 1))) continue;
+                if (!(ay >= 0.0 && ay <= (double)(Ha - 1))) continue;
+                if (!(by >= 0.0 && by <= (double)(Hb - 1))) continue;
+            } else {
+                cAx = fmin(fmax(cAx, 0.0), (double)(Wa - 1));
+                cBx = fmin(fmax(cBx, 0.0), (double)(Wb - 1));
+                ay = fmin(fmax(ay, 0.0), (double)(Ha - 1));
+                by = fmin(fmax(by, 0.0), (double)(Hb - 1));
+            }
+            sum = sum + oracle_interp4(g, g_f32, Wa, Ha, Wb, Hb, cAx, cBx, ay, by);
+            cnt++;
+        }
+    }
+    if (count_out) *count_out = cnt;
+    return cnt ? sum / (double)cnt : 0.0;
+}
+
+/* Refocus a stack under general maps: maps[12 * p .. 12 * p + 11] for plane p (layout of
+ * refocus_pixel_affine); other arguments as oracle_refocus.  Non-finite coefficient -> -2. */
+int oracle_refocus_affine(const void *g, int g_f32, int Wa, int Ha, int Wb, int Hb,
+                          const double *maps, int n_planes, int boundary, const int32_t *pix,
+                          int64_t npix, double *out, int64_t *counts, int nthreads) {
+    if (Wa < 1 || Ha < 1 || Wb < 1 || Hb < 1 || n_planes < 0) return -1;
+    for (int i = 0; i < 12 * n_planes; i++)
+        if (!isfinite(maps[i])) return -2;
+    if (pix == NULL) npix = (int64_t)Wa * Ha;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for collapse(2) schedule(dynamic, 16)
+#endif
+    for (int p = 0; p < n_planes; p++)
+        for (int64_t k = 0; k < npix; k++) {
+            const int x = pix ? pix[2 * k] : (int)(k % Wa);
+            const int y = pix ? pix[2 * k + 1] : (int)(k / Wa);
+            int64_t c = 0;
+            out[(int64_t)p * npix + k] =
+                refocus_pixel_affine(g, g_f32, Wa, Ha, Wb, Hb, maps + 12 * p, boundary, x, y, &c);
+            if (counts) counts[(int64_t)p * npix + k] = c;
+        }
+    (void)nthreads;
+    return 0;
+}
+
+int oracle_version(void) { return 2; }

@@ -235,3 +235,125 @@ def test_degenerate_alpha_rejected():
     for bad in (0.0, float("nan"), float("inf")):
         with pytest.raises(ValueError):
             oracle.refocus(G, (2, 2, 2, 2), [bad])
+
+
+# ---- general affine maps (S:273 RefocusMap) ---------------------------
+
+def _coords_np(mp, dims):
+    """Coordinate arrays of a general map (inputs of the check: the map's definition)."""
+    Wa, Ha, Wb, Hb = dims
+    cax, cay, cbx, cby = (Wa - 1) / 2, (Ha - 1) / 2, (Wb - 1) / 2, (Hb - 1) / 2
+    xr = np.arange(Wa, dtype=np.float64)[:, None] - cax
+    ur = np.arange(Wb, dtype=np.float64)[None, :] - cbx
+    yr = np.arange(Ha, dtype=np.float64)[:, None] - cay
+    vr = np.arange(Hb, dtype=np.float64)[None, :] - cby
+    CAX = mp[0] * xr + mp[1] * ur + mp[2] + cax        # [x][u]
+    CBX = mp[3] * xr + mp[4] * ur + mp[5] + cbx
+    CAY = mp[6] * yr + mp[7] * vr + mp[8] + cay        # [y][v]
+    CBY = mp[9] * yr + mp[10] * vr + mp[11] + cby
+    VX = (CAX >= 0) & (CAX <= Wa - 1) & (CBX >= 0) & (CBX <= Wb - 1)
+    VY = (CAY >= 0) & (CAY <= Ha - 1) & (CBY >= 0) & (CBY <= Hb - 1)
+    return CAX, CBX, CAY, CBY, VX, VY
+
+
+def _dense_affine_np(G, dims, mp):
+    """Independent dense evaluation for a general map: materialised coordinates, the 16-corner
+    multilinear weights as separate per-axis 1D linear weights (numpy), skip_and_renormalize."""
+    Wa, Ha, Wb, Hb = dims
+    G4 = np.asarray(G, dtype=np.float64).reshape(Ha, Wa, Hb, Wb)     # [m][j][n][k]
+    CAX, CBX, CAY, CBY, VX, VY = _coords_np(mp, dims)
+
+    def lin(c, W):   # lower corner and weights of 1D linear interpolation on [0, W-1]
+        i0 = np.clip(np.minimum(np.floor(c), W - 2), 0, None).astype(int)
+        return i0, c - i0
+    J0, TJ = lin(CAX, Wa)
+    K0, TK = lin(CBX, Wb)
+    M0, TM = lin(CAY, Ha)
+    N0, TN = lin(CBY, Hb)
+    out = np.zeros((Ha, Wa))
+    cnt = np.zeros((Ha, Wa), dtype=np.int64)
+    for y in range(Ha):
+        for v in range(Hb):
+            if not VY[y, v]:
+                continue
+            for x in range(Wa):
+                for u in range(Wb):
+                    if not VX[x, u]:
+                        continue
+                    acc = 0.0
+                    for dm, wm in ((0, 1 - TM[y, v]), (1, TM[y, v])):
+                        for dn, wn in ((0, 1 - TN[y, v]), (1, TN[y, v])):
+                            for dj, wj in ((0, 1 - TJ[x, u]), (1, TJ[x, u])):
+                                for dk, wk in ((0, 1 - TK[x, u]), (1, TK[x, u])):
+                                    acc += wm * wn * wj * wk * G4[M0[y, v] + dm, J0[x, u] + dj,
+                                                                   N0[y, v] + dn, K0[x, u] + dk]
+                    out[y, x] += acc
+                    cnt[y, x] += 1
+    return np.where(cnt > 0, out / np.maximum(cnt, 1), 0.0), cnt
+
+
+@pytest.mark.parametrize("boundary", [0, 1])
+def test_affine_default_map_is_bit_identical(boundary):
+    """The default map written as a general map gives the default refocus bit for bit."""
+    dims = (9, 7, 8, 5)
+    G = synth.random_gamma(63, 40, seed=21)
+    al = [0.5, 0.8, 1.0, 1.37, 2.0]
+    for g in (G, G.astype(np.float64)):
+        R = oracle.refocus(g, dims, al, boundary=boundary)
+        Ra = oracle.refocus_affine(g, dims, [oracle.default_map(a) for a in al], boundary=boundary)
+        np.testing.assert_array_equal(Ra, R)
+
+
+MAPS = [
+    [0.7, 0.3, 0.25, 0.0, 0.5, -0.3, 1.3, -0.3, -0.4, 0.1, 0.8, 0.2],     # fractional B coordinates
+    [1.0, 0.0, 0.0, 0.25, 0.75, 0.1, 0.9, 0.1, 0.0, -0.2, 1.1, 0.0],
+    [2.0, -1.0, 0.5, 0.0, 1.0, 0.0, 0.5, 0.5, 0.0, 0.0, 1.0, 0.0],        # integral B (GPU fast path)
+]
+
+
+@pytest.mark.parametrize("mp", MAPS)
+def test_affine_dense_materialised(mp):
+    """General maps vs the dense numpy evaluation (values and counts)."""
+    dims = (6, 5, 7, 4)
+    G = synth.random_gamma(30, 28, seed=8)
+    R, C = oracle.refocus_affine(G, dims, [mp], return_counts=True)
+    Rd, Cd = _dense_affine_np(G, dims, np.array(mp))
+    np.testing.assert_array_equal(C[0], Cd)
+    np.testing.assert_allclose(R[0], Rd, rtol=1e-12, atol=1e-15)
+
+
+@pytest.mark.parametrize("mp", MAPS)
+def test_affine_exact_on_affine_gamma(mp):
+    """Multilinear interpolation reproduces affine data exactly: for
+    Gamma(j,k,m,n) = c0 + c1 j + c2 k + c3 m + c4 n the refocused pixel is the mean over valid
+    samples of c0 + c1 c_Ax + c2 c_Bx + c3 c_Ay + c4 c_By (closed form, no interpolation)."""
+    dims = (8, 6, 7, 5)
+    Wa, Ha, Wb, Hb = dims
+    c0, c1, c2, c3, c4 = 0.3, 0.25, -0.5, 0.125, 1.0
+    m, j, n, k = np.meshgrid(np.arange(Ha), np.arange(Wa), np.arange(Hb), np.arange(Wb), indexing="ij")
+    G = (c0 + c1 * j + c2 * k + c3 * m + c4 * n).reshape(Wa * Ha, Wb * Hb)
+    R = oracle.refocus_affine(G, dims, [mp])[0]
+    CAX, CBX, CAY, CBY, VX, VY = _coords_np(np.array(mp), dims)
+    for y in range(Ha):
+        for x in range(Wa):
+            vals = [c0 + c1 * CAX[x, u] + c2 * CBX[x, u] + c3 * CAY[y, v] + c4 * CBY[y, v]
+                    for v in range(Hb) for u in range(Wb) if VX[x, u] and VY[y, v]]
+            want = np.mean(vals) if vals else 0.0
+            assert abs(R[y, x] - want) <= 1e-12 * (1 + abs(want))
+
+
+def test_affine_identity_map_is_angular_mean():
+    """a = 1, b = 0 on the A axes and the identity on the B axes: R(x,y) = mean over (u,v) of
+    Gamma[(y, x)][(v, u)] (plain angular marginal)."""
+    dims = (5, 4, 6, 3)
+    Wa, Ha, Wb, Hb = dims
+    G = synth.random_gamma(20, 18, seed=3)
+    ident = [1.0, 0.0, 0.0, 0.0, 1.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0, 0.0]
+    R = oracle.refocus_affine(G, dims, [ident])[0]
+    want = np.asarray(G, dtype=np.float64).reshape(Ha, Wa, Hb * Wb).mean(axis=2)
+    np.testing.assert_allclose(R, want, rtol=1e-13)
+
+
+def test_affine_nonfinite_rejected():
+    with pytest.raises(ValueError):
+        oracle.refocus_affine(np.zeros((4, 4), np.float32), (2, 2, 2, 2), [[np.nan] + [0.0] * 11])
