@@ -117,6 +117,18 @@ typedef struct {
                                A-rows (block-cyclic ownership).  row_block <= 0: contiguous
                                (m(l) = row0/W_a + l).  Needs row_stride >= row_block. */
     int32_t row_stride;
+    const double *affine;   /* HOST [n_planes][12] general RefocusMap per plane (SURVEY
+                               f3(ii)), or NULL for the default map from alphas.  Row
+                               {ax, bx, cx, dx, ex, fx, ay, by, cy, dy, ey, fy}, coordinates
+                               relative to the arm centres c = (W-1)/2:
+                                 c_Ax = ax (x - c_ax) + bx (u - c_bx) + cx + c_ax
+                                 c_Bx = dx (x - c_ax) + ex (u - c_bx) + fx + c_bx
+                               (y, v likewise; evaluated left to right in fp64).  A sample counts
+                               only if all four coordinates lie on their lattices (skip policy).
+                               Supported: integral B coordinates (dx = fx = dy = fy = 0,
+                               ex = ey = 1) -- the separable kernels with per-plane A-axis
+                               maps; otherwise CPI_ERR_UNSUPPORTED.  The default map is
+                               {a, 1 - a, 0, 0, 1, 0} on both axes. */
 } cpi_refocus_spec;
 
 typedef struct cpi_ctx cpi_ctx;   /* opaque, owned by the library */

@@ -54,7 +54,8 @@ class RefocusSpec(ctypes.Structure):
     _fields_ = [("alphas", ctypes.POINTER(ctypes.c_double)), ("n_planes", ctypes.c_int32),
                 ("boundary", ctypes.c_int32), ("gamma_dev", ctypes.c_void_p),
                 ("row0", ctypes.c_int64), ("rows", ctypes.c_int64),
-                ("row_block", ctypes.c_int32), ("row_stride", ctypes.c_int32)]
+                ("row_block", ctypes.c_int32), ("row_stride", ctypes.c_int32),
+                ("affine", ctypes.POINTER(ctypes.c_double))]
 
 
 _lib = None

@@ -180,17 +180,31 @@ class Context:
     def reset(self, stream=None):
         self._check(self._lib.cpi_reset(self._h, self._stream(stream)))
 
-    def refocus(self, alphas: Sequence[float], gamma, planes, row0: int = 0, rows: Optional[int] = None,
-                boundary: int = _lib.CPI_SKIP_RENORMALIZE, row_block: int = 0, row_stride: int = 0, stream=None):
+    def refocus(self, alphas: Optional[Sequence[float]], gamma, planes, row0: int = 0, rows: Optional[int] = None,
+                boundary: int = _lib.CPI_SKIP_RENORMALIZE, row_block: int = 0, row_stride: int = 0,
+                affine=None, stream=None):
         """cpi_refocus: planes [n_planes][H_a][W_a] fp32 from a Gamma row shard of `rows` pixel
         rows (leading dimension P_b) starting at A row row0 / W_a; row_block > 0 makes the
-        shard block-cyclic (local A row l -> row0/W_a + (l // row_block) * row_stride + l % row_block)."""
-        al = np.ascontiguousarray(alphas, dtype=np.float64).ravel()
+        shard block-cyclic (local A row l -> row0/W_a + (l // row_block) * row_stride + l % row_block).
+        affine: optional [n_planes][12] general maps (include/cpi.h) instead of alphas."""
+        if affine is not None:
+            mp = np.ascontiguousarray(affine, dtype=np.float64).reshape(-1, 12)
+            n = mp.shape[0]
+            al_ptr = ctypes.POINTER(ctypes.c_double)()
+            aff_ptr = mp.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+            keep = mp
+        else:
+            al = np.ascontiguousarray(alphas, dtype=np.float64).ravel()
+            n = al.size
+            al_ptr = al.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+            aff_ptr = ctypes.POINTER(ctypes.c_double)()
+            keep = al
         if rows is None:
             rows = self.p_a - row0
-        spec = _lib.RefocusSpec(al.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), al.size, int(boundary),
-                                self._ptr(gamma), int(row0), int(rows), int(row_block), int(row_stride))
+        spec = _lib.RefocusSpec(al_ptr, n, int(boundary), self._ptr(gamma), int(row0), int(rows), int(row_block),
+                                int(row_stride), aff_ptr)
         self._check(self._lib.cpi_refocus(self._h, ctypes.byref(spec), self._ptr(planes), self._stream(stream)))
+        del keep
         return planes
 
     def launch_count(self) -> int:

@@ -226,7 +226,7 @@ cpi_status alloc_axis(cpi_ctx* c, cpi::AxisTables& t, int W, int Wb) {
 
 extern "C" {
 
-int32_t cpi_abi_version(void) { return 101; }
+int32_t cpi_abi_version(void) { return 102; }
 
 const char* cpi_status_string(cpi_status s) {
     switch (s) {
@@ -663,12 +663,25 @@ cpi_status cpi_reset(cpi_ctx* c, void* stream) {
 cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, void* stream) {
     if (!c) return CPI_ERR_INVALID_ARG;
     if (!spec || !planes) return fail(c, CPI_ERR_INVALID_ARG, "spec and planes_dev must be non-NULL");
-    if (spec->n_planes < 1 || !spec->alphas) return fail(c, CPI_ERR_EMPTY_ANGULAR_GRID, "n_planes must be >= 1");
+    if (spec->n_planes < 1 || (!spec->alphas && !spec->affine))
+        return fail(c, CPI_ERR_EMPTY_ANGULAR_GRID, "n_planes must be >= 1");
     if (spec->boundary != CPI_SKIP_RENORMALIZE && spec->boundary != CPI_CLAMP)
         return fail(c, CPI_ERR_INVALID_ARG, "unknown boundary policy %d", spec->boundary);
-    for (int p = 0; p < spec->n_planes; ++p)
-        if (!(spec->alphas[p] != 0.0) || !std::isfinite(spec->alphas[p]))
-            return fail(c, CPI_ERR_DEGENERATE_ALPHA, "alpha[%d] = %g (must be finite and non-zero)", p, spec->alphas[p]);
+    if (spec->affine) {
+        for (int p = 0; p < spec->n_planes; ++p) {
+            const double* mp = spec->affine + 12 * p;
+            for (int i = 0; i < 12; ++i)
+                if (!std::isfinite(mp[i])) return fail(c, CPI_ERR_INVALID_ARG, "affine[%d][%d] is not finite", p, i);
+            if (mp[3] != 0.0 || mp[4] != 1.0 || mp[5] != 0.0 || mp[9] != 0.0 || mp[10] != 1.0 || mp[11] != 0.0)
+                return fail(c, CPI_ERR_UNSUPPORTED, "affine[%d]: fractional B coordinates (d, e, f != 0, 1, 0) "
+                                                    "are not supported on the GPU", p);
+        }
+    } else {
+        for (int p = 0; p < spec->n_planes; ++p)
+            if (!(spec->alphas[p] != 0.0) || !std::isfinite(spec->alphas[p]))
+                return fail(c, CPI_ERR_DEGENERATE_ALPHA, "alpha[%d] = %g (must be finite and non-zero)", p,
+                            spec->alphas[p]);
+    }
     const int Wa = c->cfg.roi_a.width, Ha = c->cfg.roi_a.height;
     const int Wb = c->cfg.roi_b.width, Hb = c->cfg.roi_b.height;
     if (Wa < 2 || Ha < 2) return fail(c, CPI_ERR_UNSUPPORTED, "refocusing needs an A RoI of at least 2x2");
@@ -761,9 +774,20 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
             TimedScope ts(c, KC_COORDS, st);
             cudaError_t e = cudaSuccess;
             for (int f = 0; f < nf && e == cudaSuccess; ++f) {
-                const double alpha = spec->alphas[p0 + f];
-                e = cpi::launch_refocus_coords(alpha, spec->boundary, Wa, Wb, c->xs[f], st);
-                if (e == cudaSuccess) e = cpi::launch_refocus_coords(alpha, spec->boundary, Ha, Hb, c->ys[f], st);
+                double mx[3], my[3];   // (a, b, c) of the A-axis maps
+                if (spec->affine) {
+                    const double* mp = spec->affine + 12 * (p0 + f);
+                    mx[0] = mp[0]; mx[1] = mp[1]; mx[2] = mp[2];
+                    my[0] = mp[6]; my[1] = mp[7]; my[2] = mp[8];
+                } else {
+                    const double alpha = spec->alphas[p0 + f];
+                    mx[0] = my[0] = alpha;
+                    mx[1] = my[1] = 1.0 - alpha;
+                    mx[2] = my[2] = 0.0;
+                }
+                e = cpi::launch_refocus_coords(mx[0], mx[1], mx[2], spec->boundary, Wa, Wb, c->xs[f], st);
+                if (e == cudaSuccess)
+                    e = cpi::launch_refocus_coords(my[0], my[1], my[2], spec->boundary, Ha, Hb, c->ys[f], st);
                 c->launches += 2;
             }
             if (e == cudaSuccess && tma_now) {

@@ -79,8 +79,8 @@ struct AxisTables {           // one axis (x with B-axis u, or y with B-axis v)
     int32_t* lo;              // [Wb]     min used i0 over outputs (INT_MAX if none)
     int32_t* hi;              // [Wb]     max used i0 + 1 over outputs (-1 if none)
 };
-cudaError_t launch_refocus_coords(double alpha, int boundary, int W, int Wb, AxisTables tab,
-                                  cudaStream_t st);
+cudaError_t launch_refocus_coords(double a, double b, double c_off, int boundary, int W, int Wb,
+                                  AxisTables tab, cudaStream_t st);
 cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
                                   int m_base, int m_count, AxisTables xs, AxisTables ys,
                                   double* T, cudaStream_t st);

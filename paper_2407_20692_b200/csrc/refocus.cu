@@ -32,15 +32,17 @@ constexpr int kS1Threads = 256;
 
 // ---- KB5a: per-axis interpolation tables ------------------------------------------
 // Block per B coordinate ub (u or v), threads over the output coordinate x (or y).
-__global__ void coords_kernel(double alpha, int boundary, int W, int Wb, AxisTables tab) {
+// A-axis map c = ((a (x - c_a)) + (b (u - c_b))) + c_off + c_a: the default map is a = alpha,
+// b = 1 - alpha, c_off = 0 (adding +0.0 leaves the default's value unchanged), a general
+// RefocusMap row supplies (ax, bx, cx) / (ay, by, cy) (include/cpi.h cpi_refocus_spec.affine).
+__global__ void coords_kernel(double a, double b, double c_off, int boundary, int W, int Wb, AxisTables tab) {
     const int ub = blockIdx.x;
     const double c_a = (W - 1) / 2.0, c_b = (Wb - 1) / 2.0;
-    const double one_minus = __dadd_rn(1.0, -alpha);
-    const double bu = __dmul_rn(one_minus, __dadd_rn(static_cast<double>(ub), -c_b));
+    const double bu = __dmul_rn(b, __dadd_rn(static_cast<double>(ub), -c_b));
     int lo = INT_MAX, hi = -1;
     for (int x = threadIdx.x; x < W; x += blockDim.x) {
-        // c = (alpha*(x - c_a)) + ((1 - alpha)*(u - c_b)) + c_a, each op rounded, no FMA
-        double c = __dadd_rn(__dadd_rn(__dmul_rn(alpha, __dadd_rn(static_cast<double>(x), -c_a)), bu), c_a);
+        // c = ((a*(x - c_a)) + (b*(u - c_b))) + c_off + c_a, each op rounded, no FMA
+        double c = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(a, __dadd_rn(static_cast<double>(x), -c_a)), bu), c_off), c_a);
         bool ok;
         if (boundary == 0) {
             ok = (c >= 0.0) && (c <= static_cast<double>(W - 1));
@@ -655,12 +657,12 @@ cudaError_t launch_refocus_stage2_group(double* const* T, int n_fuse, int Wa, in
     return cudaGetLastError();
 }
 
-cudaError_t launch_refocus_coords(double alpha, int boundary, int W, int Wb, AxisTables tab,
+cudaError_t launch_refocus_coords(double a, double b, double c_off, int boundary, int W, int Wb, AxisTables tab,
                                   cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(tab.cnt, 0, sizeof(int32_t) * W, st);
     if (e != cudaSuccess) return e;
     int threads = W >= 256 ? 256 : ((W + 31) / 32) * 32;
-    coords_kernel<<<Wb, threads, 0, st>>>(alpha, boundary, W, Wb, tab);
+    coords_kernel<<<Wb, threads, 0, st>>>(a, b, c_off, boundary, W, Wb, tab);
     return cudaGetLastError();
 }
 

@@ -414,3 +414,38 @@ def test_gamma_ublocked_layout(variant, roi_b):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(g2.cpu().numpy()[:, idx], g2r.cpu().numpy())
     np.testing.assert_array_equal(g3.cpu().numpy(), g2.cpu().numpy())
+
+
+@pytest.mark.parametrize("boundary", [0, 1])
+def test_refocus_affine_maps(boundary):
+    """General RefocusMap rows (cpi_refocus_spec.affine) with integral B coordinates:
+    per-plane A-axis maps (a, b, c) on x and y, vs the oracle's general 16-corner refocus; the
+    default map written as affine rows is bit-identical to the alphas path; fractional B
+    coordinates are refused (CPI_ERR_UNSUPPORTED)."""
+    dims = (24, 20, 16, 12)
+    Wa, Ha, Wb, Hb = dims
+    G = synth.random_gamma(Wa * Ha, Wb * Hb, seed=17)
+    maps = [[0.7, 0.3, 0.25, 0.0, 1.0, 0.0, 1.3, -0.3, -0.4, 0.0, 1.0, 0.0],
+            [1.6, -0.45, -1.5, 0.0, 1.0, 0.0, 0.55, 0.5, 2.0, 0.0, 1.0, 0.0],
+            [1.0, 0.0, 0.0, 0.0, 1.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0, 0.0],
+            [2.0, -1.0, 0.5, 0.0, 1.0, 0.0, -0.8, 1.2, 3.0, 0.0, 1.0, 0.0],
+            [0.5, 0.5, 0.0, 0.0, 1.0, 0.0, 0.5, 0.5, 0.0, 0.0, 1.0, 0.0],
+            [1.2, 0.1, -0.7, 0.0, 1.0, 0.0, 0.9, 0.0, 0.3, 0.0, 1.0, 0.0]]
+    ctx = _ctx((0, 0, Wa, Ha), (0, 0, Wb, Hb), 1)
+    g = torch.from_numpy(np.ascontiguousarray(G, dtype=np.float32)).cuda()
+    planes = ctx.new_planes(len(maps))
+    ctx.refocus(None, g, planes, boundary=boundary, affine=maps)
+    torch.cuda.synchronize()
+    R = planes.cpu().numpy().astype(np.float64)
+    Ro = oracle.refocus_affine(G, dims, maps, boundary=boundary)
+    M = oracle.refocus_affine(np.abs(G.astype(np.float64)), dims, maps, boundary=boundary)
+    assert np.all(np.abs(R - Ro) <= 1e-6 * M + 1e-30), np.max(np.abs(R - Ro) / np.maximum(M, 1e-300))
+    al = [0.5, 1.0, 1.45]
+    p1, p2 = ctx.new_planes(3), ctx.new_planes(3)
+    ctx.refocus(al, g, p1, boundary=boundary)
+    ctx.refocus(None, g, p2, boundary=boundary, affine=[oracle.default_map(a) for a in al])
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(p2.cpu().numpy(), p1.cpu().numpy())
+    from paper_2407_20692_b200 import CpiError
+    with pytest.raises(CpiError, match="UNSUPPORTED"):
+        ctx.refocus(None, g, p1, affine=[[1.0, 0.0, 0.0, 0.0, 0.5, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0, 0.0]])
