@@ -773,23 +773,24 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
         {
             TimedScope ts(c, KC_COORDS, st);
             cudaError_t e = cudaSuccess;
-            for (int f = 0; f < nf && e == cudaSuccess; ++f) {
-                double mx[3], my[3];   // (a, b, c) of the A-axis maps
+            cpi::CoordsGroupArgs cg{};
+            cg.Wa = Wa; cg.Ha = Ha; cg.Wb = Wb; cg.Hb = Hb; cg.boundary = spec->boundary;
+            for (int f = 0; f < nf; ++f) {   // (a, b, c) of the A-axis maps of plane p0 + f
                 if (spec->affine) {
                     const double* mp = spec->affine + 12 * (p0 + f);
-                    mx[0] = mp[0]; mx[1] = mp[1]; mx[2] = mp[2];
-                    my[0] = mp[6]; my[1] = mp[7]; my[2] = mp[8];
+                    const double m6[6] = {mp[0], mp[1], mp[2], mp[6], mp[7], mp[8]};
+                    for (int i = 0; i < 6; ++i) cg.map[f][i] = m6[i];
                 } else {
                     const double alpha = spec->alphas[p0 + f];
-                    mx[0] = my[0] = alpha;
-                    mx[1] = my[1] = 1.0 - alpha;
-                    mx[2] = my[2] = 0.0;
+                    cg.map[f][0] = cg.map[f][3] = alpha;
+                    cg.map[f][1] = cg.map[f][4] = 1.0 - alpha;
+                    cg.map[f][2] = cg.map[f][5] = 0.0;
                 }
-                e = cpi::launch_refocus_coords(mx[0], mx[1], mx[2], spec->boundary, Wa, Wb, c->xs[f], st);
-                if (e == cudaSuccess)
-                    e = cpi::launch_refocus_coords(my[0], my[1], my[2], spec->boundary, Ha, Hb, c->ys[f], st);
-                c->launches += 2;
+                cg.xs[f] = c->xs[f];
+                cg.ys[f] = c->ys[f];
             }
+            e = cpi::launch_refocus_coords_group(cg, nf, st);
+            c->launches += 2;
             if (e == cudaSuccess && tma_now) {
                 e = cpi::launch_pack_xtable_group(c->xs, nf, Wa, Wb, c->xpack, c->xblk, st);
                 c->launches += 1;

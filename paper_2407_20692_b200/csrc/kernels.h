@@ -81,6 +81,14 @@ struct AxisTables {           // one axis (x with B-axis u, or y with B-axis v)
 };
 cudaError_t launch_refocus_coords(double a, double b, double c_off, int boundary, int W, int Wb,
                                   AxisTables tab, cudaStream_t st);
+// All coordinate tables of a fused plane group in two launches (tables + counts);
+// map[f] = {ax, bx, cx, ay, by, cy} of plane f's A-axis maps.
+struct CoordsGroupArgs {
+    int Wa, Ha, Wb, Hb, boundary;
+    double map[4][6];
+    AxisTables xs[4], ys[4];
+};
+cudaError_t launch_refocus_coords_group(const CoordsGroupArgs& g, int n_fuse, cudaStream_t st);
 cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
                                   int m_base, int m_count, AxisTables xs, AxisTables ys,
                                   double* T, cudaStream_t st);

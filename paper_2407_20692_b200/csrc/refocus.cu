@@ -35,8 +35,34 @@ constexpr int kS1Threads = 256;
 // A-axis map c = ((a (x - c_a)) + (b (u - c_b))) + c_off + c_a: the default map is a = alpha,
 // b = 1 - alpha, c_off = 0 (adding +0.0 leaves the default's value unchanged), a general
 // RefocusMap row supplies (ax, bx, cx) / (ay, by, cy) (include/cpi.h cpi_refocus_spec.affine).
+__device__ __forceinline__ void coords_block(double a, double b, double c_off, int boundary, int W, int Wb,
+                                             AxisTables tab, int ub, bool count);
 __global__ void coords_kernel(double a, double b, double c_off, int boundary, int W, int Wb, AxisTables tab) {
-    const int ub = blockIdx.x;
+    coords_block(a, b, c_off, boundary, W, Wb, tab, blockIdx.x, true);
+}
+// One launch for a fused group: blockIdx = (B coordinate, plane, axis 0 = x / 1 = y); the
+// per-output counts are left to count_kernel (no atomics, no memsets).
+__global__ void coords_group_kernel(CoordsGroupArgs g) {
+    const int ax = blockIdx.z, f = blockIdx.y, ub = blockIdx.x;
+    const int W = ax ? g.Ha : g.Wa, Wb = ax ? g.Hb : g.Wb;
+    if (ub >= Wb) return;
+    coords_block(g.map[f][3 * ax], g.map[f][3 * ax + 1], g.map[f][3 * ax + 2], g.boundary, W, Wb,
+                 ax ? g.ys[f] : g.xs[f], ub, false);
+}
+// cnt[x] = number of B coordinates with a used sample at output coordinate x.
+__global__ void count_kernel(CoordsGroupArgs g) {
+    const int ax = blockIdx.z, f = blockIdx.y;
+    const int W = ax ? g.Ha : g.Wa, Wb = ax ? g.Hb : g.Wb;
+    const AxisTables& t = ax ? g.ys[f] : g.xs[f];
+    for (int x = threadIdx.x; x < W; x += blockDim.x) {
+        int c = 0;
+#pragma unroll 8
+        for (int ub = 0; ub < Wb; ++ub) c += __ldg(t.i0 + static_cast<int64_t>(ub) * W + x) >= 0;
+        t.cnt[x] = c;
+    }
+}
+__device__ __forceinline__ void coords_block(double a, double b, double c_off, int boundary, int W, int Wb,
+                                             AxisTables tab, int ub, bool count) {
     const double c_a = (W - 1) / 2.0, c_b = (Wb - 1) / 2.0;
     const double bu = __dmul_rn(b, __dadd_rn(static_cast<double>(ub), -c_b));
     int lo = INT_MAX, hi = -1;
@@ -59,7 +85,7 @@ __global__ void coords_kernel(double a, double b, double c_off, int boundary, in
             t = __dadd_rn(c, -f);
             lo = min(lo, i0);
             hi = max(hi, i0 + 1);
-            atomicAdd(tab.cnt + x, 1);
+            if (count) atomicAdd(tab.cnt + x, 1);
         }
         tab.i0[static_cast<int64_t>(ub) * W + x] = ok ? i0 : -1;
         tab.t[static_cast<int64_t>(ub) * W + x] = t;
@@ -654,6 +680,17 @@ cudaError_t launch_refocus_stage2_group(double* const* T, int n_fuse, int Wa, in
         attr = smem;
     }
     stage2_staged_kernel<<<dim3((Wa + kS2XB - 1) / kS2XB, n_fuse), kS2Threads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_refocus_coords_group(const CoordsGroupArgs& g, int n_fuse, cudaStream_t st) {
+    const int nub = g.Wb > g.Hb ? g.Wb : g.Hb;
+    const int wmax = g.Wa > g.Ha ? g.Wa : g.Ha;
+    const int threads = wmax >= 256 ? 256 : ((wmax + 31) / 32) * 32;
+    coords_group_kernel<<<dim3(nub, n_fuse, 2), threads, 0, st>>>(g);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    count_kernel<<<dim3(1, n_fuse, 2), threads, 0, st>>>(g);
     return cudaGetLastError();
 }
 
