@@ -79,7 +79,7 @@ def test_tiny_config_bit_exact(variant):
 
 
 @pytest.mark.parametrize("variant", ["tc", "popc", "fp4"])
-@pytest.mark.parametrize("n", [1, 31, 127, 129, 255, 257, 1000, 2600])
+@pytest.mark.parametrize("n", [1, 31, 127, 129, 255, 257, 1000, 2600, 12500])
 def test_ragged_tiles_and_k_tails(variant, n):
     """Several M/N tiles with ragged edges (P_a = 1500, P_b = 380) and K tails (N not a
     multiple of 128): zero padding must be inert."""

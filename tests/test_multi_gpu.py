@@ -1,0 +1,44 @@
+"""SURVEY §4 tier T3: the frame-sharded pipeline on 2-8 real GPUs (one rank per GPU, NCCL,
+launched with torch.distributed.run).  Gamma gathered from the ranks' block-cyclic shards is
+bit-identical to one GPU's Gamma (integer sums), and the all-reduced planes equal the
+single-GPU planes to fp32 summation order.  Skipped when fewer than 2 GPUs are visible (the
+gloo tests cover the orchestration on CPU; test_gpu_sharded.py covers it on one GPU)."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs (one rank per GPU)")
+@pytest.mark.parametrize("variant", ["fp4", "tc"])
+def test_frame_sharded_nccl_matches_single_gpu(tmp_path, variant):
+    sys.path.insert(0, HERE)
+    import _mgpu_worker as w
+    import synth
+    from paper_2407_20692_b200 import Context
+    world = min(torch.cuda.device_count(), 8)
+    out = tmp_path / "mgpu.npz"
+    env = dict(os.environ, CPI_MGPU_VARIANT=variant)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + os.getpid() % 1000),
+           os.path.join(HERE, "_mgpu_worker.py"), str(out)]
+    subprocess.run(cmd, check=True, env=env, timeout=900)
+    got = np.load(out)
+    frames = synth.bernoulli_frames(w.N, 0.1, seed=99)
+    ctx = Context(w.ROI_A, w.ROI_B, w.N, variant=variant, gamma_blocked=True)
+    ctx.load_frames(frames)
+    g = ctx.correlate(ctx.new_gamma())
+    planes = ctx.new_planes(len(w.ALPHAS))
+    ctx.refocus(w.ALPHAS, g, planes)
+    torch.cuda.synchronize()
+    assert int(got["n_tot"]) == w.N and int(got["panels"]) >= 1
+    np.testing.assert_array_equal(got["gamma"], g.cpu().numpy())
+    np.testing.assert_allclose(got["planes"], planes.cpu().numpy(), rtol=1e-5, atol=1e-9)
