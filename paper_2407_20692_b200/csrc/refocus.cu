@@ -772,7 +772,7 @@ cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa
     }
     const int tiles = m_count * a.n_vg;
     const int grid = tiles < num_sms ? tiles : num_sms;
-    static const bool skip = getenv("CPI_S1_NOSKIP") == nullptr;   // A/B knob for the x-block skip
+    const bool skip = getenv("CPI_S1_NOSKIP") == nullptr;   // A/B knob for the x-block skip (read per launch)
     if (skip)
         return Wa == 256 ? launch_s1_f<true, true>(n_fuse, maps, a, grid, st) : launch_s1_f<false, true>(n_fuse, maps, a, grid, st);
     return Wa == 256 ? launch_s1_f<true, false>(n_fuse, maps, a, grid, st) : launch_s1_f<false, false>(n_fuse, maps, a, grid, st);

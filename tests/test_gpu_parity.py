@@ -284,6 +284,22 @@ def test_refocus_fused_plane_groups(fuse, monkeypatch):
     _assert_planes(R, G, dims, alphas)
 
 
+@pytest.mark.parametrize("knobs", [{"CPI_STAGE1_SIMPLE": "1"}, {"CPI_STAGE2_SIMPLE": "1"},
+                                   {"CPI_STAGE1_SIMPLE": "1", "CPI_STAGE2_SIMPLE": "1"}, {"CPI_S1_NOSKIP": "1"}])
+@pytest.mark.parametrize("boundary", [0, 1])
+def test_refocus_fallback_kernels(knobs, boundary, monkeypatch):
+    """The fallback kernels (plain stage 1 for W_a > 256, W_b % 4 != 0 or unaligned Gamma;
+    warp-per-pixel stage 2 for H_a > 256) and the no-skip stage 1 agree with the oracle."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    dims = (40, 33, 36, 10)
+    Wa, Ha, Wb, Hb = dims
+    G = synth.random_gamma(Wa * Ha, Wb * Hb, seed=5)
+    alphas = [0.5, 1.0, 1.3, 2.0]
+    R = _refocus_gpu(G, dims, alphas, boundary=boundary)
+    _assert_planes(R, G, dims, alphas, boundary=boundary)
+
+
 def test_refocus_repeat_bit_identical():
     """Every refocus kernel is deterministic (fixed summation order, no atomics in the value
     path), so repeated runs must agree bit for bit.  Catches pipeline races: e.g. a stage
