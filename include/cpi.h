@@ -125,10 +125,13 @@ typedef struct {
                                  c_Bx = dx (x - c_ax) + ex (u - c_bx) + fx + c_bx
                                (y, v likewise; evaluated left to right in fp64).  A sample counts
                                only if all four coordinates lie on their lattices (skip policy).
-                               Supported: integral B coordinates (dx = fx = dy = fy = 0,
-                               ex = ey = 1) -- the separable kernels with per-plane A-axis
-                               maps; otherwise CPI_ERR_UNSUPPORTED.  The default map is
-                               {a, 1 - a, 0, 0, 1, 0} on both axes. */
+                               GPU support: B coordinates independent of the output pixel
+                               (dx = dy = 0).  Integral B (ex = ey = 1, fx = fy = 0) runs the
+                               fast separable kernels; fractional B (any ex, fx, ey, fy) runs
+                               the general-B kernels (2 x 2 corners per stage, row-major B
+                               order, contiguous row shards); dx or dy != 0 ->
+                               CPI_ERR_UNSUPPORTED.  The default map is {a, 1 - a, 0, 0, 1, 0}
+                               on both axes. */
 } cpi_refocus_spec;
 
 typedef struct cpi_ctx cpi_ctx;   /* opaque, owned by the library */

@@ -69,6 +69,7 @@ struct cpi_ctx {
     CUtensorMap tm_a{}, tm_b{};
     // refocus workspaces
     cpi::AxisTables xs[cpi::kRefocusMaxFuse]{}, ys[cpi::kRefocusMaxFuse]{};
+    cpi::AxisTables bxs{}, bys{};          // fractional-B path: B supports per u / v
     double* T[cpi::kRefocusMaxFuse]{};
     bool refocus_ready = false;
     int fuse = 4;                          // planes per Gamma pass in the TMA stage 1 (CPI_REFOCUS_FUSE)
@@ -204,6 +205,8 @@ void free_all(cpi_ctx* c) {
     for (int f = 0; f < cpi::kRefocusMaxFuse; ++f) {
         cpi::AxisTables* t2[2] = {&c->xs[f], &c->ys[f]};
         for (auto* t : t2) { cudaFree(t->i0); cudaFree(t->t); cudaFree(t->cnt); cudaFree(t->lo); cudaFree(t->hi); }
+        if (f == 0)
+            for (auto* t : {&c->bxs, &c->bys}) { cudaFree(t->i0); cudaFree(t->t); cudaFree(t->cnt); cudaFree(t->lo); cudaFree(t->hi); }
         cudaFree(c->T[f]);
     }
     cudaFree(c->xpack);
@@ -667,14 +670,16 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
         return fail(c, CPI_ERR_EMPTY_ANGULAR_GRID, "n_planes must be >= 1");
     if (spec->boundary != CPI_SKIP_RENORMALIZE && spec->boundary != CPI_CLAMP)
         return fail(c, CPI_ERR_INVALID_ARG, "unknown boundary policy %d", spec->boundary);
+    bool genb = false;   // some plane has fractional B coordinates -> general-B kernels
     if (spec->affine) {
         for (int p = 0; p < spec->n_planes; ++p) {
             const double* mp = spec->affine + 12 * p;
             for (int i = 0; i < 12; ++i)
                 if (!std::isfinite(mp[i])) return fail(c, CPI_ERR_INVALID_ARG, "affine[%d][%d] is not finite", p, i);
-            if (mp[3] != 0.0 || mp[4] != 1.0 || mp[5] != 0.0 || mp[9] != 0.0 || mp[10] != 1.0 || mp[11] != 0.0)
-                return fail(c, CPI_ERR_UNSUPPORTED, "affine[%d]: fractional B coordinates (d, e, f != 0, 1, 0) "
+            if (mp[3] != 0.0 || mp[9] != 0.0)
+                return fail(c, CPI_ERR_UNSUPPORTED, "affine[%d]: B coordinates depending on x / y (dx, dy != 0) "
                                                     "are not supported on the GPU", p);
+            if (mp[4] != 1.0 || mp[5] != 0.0 || mp[10] != 1.0 || mp[11] != 0.0) genb = true;
         }
     } else {
         for (int p = 0; p < spec->n_planes; ++p)
@@ -723,7 +728,16 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
         }
         c->refocus_ready = true;
     }
-    bool tma_now = c->use_s1_tma && (reinterpret_cast<uintptr_t>(spec->gamma_dev) & 15) == 0;
+    if (genb) {
+        if (c->ublocked) return fail(c, CPI_ERR_UNSUPPORTED, "fractional B coordinates need the row-major B order");
+        if (Wb < 2 || Hb < 2) return fail(c, CPI_ERR_UNSUPPORTED, "fractional B coordinates need a B RoI of 2x2 or more");
+        if (!c->bxs.i0) {
+            cpi_status s = alloc_axis(c, c->bxs, 1, Wb);
+            if (s == CPI_OK) s = alloc_axis(c, c->bys, 1, Hb);
+            if (s != CPI_OK) return s;
+        }
+    }
+    bool tma_now = !genb && c->use_s1_tma && (reinterpret_cast<uintptr_t>(spec->gamma_dev) & 15) == 0;
     if (c->ublocked && !tma_now)
         return fail(c, CPI_ERR_UNSUPPORTED, "u-blocked Gamma needs the TMA stage 1 (W_a <= 256, W_b %% 4 == 0, "
                                             "16-byte aligned Gamma)");
@@ -766,6 +780,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
             return fail(c, CPI_ERR_INVALID_ARG, "row_stride %d < row_block %d", m_stride, m_block);
         const int64_t last = m_base + int64_t((m_count - 1) / m_block) * m_stride + (m_count - 1) % m_block;
         if (last >= Ha) return fail(c, CPI_ERR_INVALID_ARG, "block-cyclic shard reaches A row %lld >= H_a", (long long)last);
+        if (genb) return fail(c, CPI_ERR_UNSUPPORTED, "fractional B coordinates need contiguous row shards");
     }
     const int group = tma_now ? c->fuse : 1;
     for (int p0 = 0; p0 < spec->n_planes; p0 += group) {
@@ -788,7 +803,15 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
                 }
                 cg.xs[f] = c->xs[f];
                 cg.ys[f] = c->ys[f];
+                const double* mp = spec->affine ? spec->affine + 12 * (p0 + f) : nullptr;
+                cg.bmap[f][0] = mp ? mp[4] : 1.0;
+                cg.bmap[f][1] = mp ? mp[5] : 0.0;
+                cg.bmap[f][2] = mp ? mp[10] : 1.0;
+                cg.bmap[f][3] = mp ? mp[11] : 0.0;
+                cg.bx[f] = c->bxs;
+                cg.by[f] = c->bys;
             }
+            cg.genb = genb ? 1 : 0;
             e = cpi::launch_refocus_coords_group(cg, nf, st);
             c->launches += 2;
             if (e == cudaSuccess && tma_now) {
@@ -804,7 +827,10 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
         {
             TimedScope ts(c, KC_STAGE1, st);
             cudaError_t e;
-            if (tma_now)
+            if (genb)
+                e = cpi::launch_refocus_stage1_genb(spec->gamma_dev, c->p_b, Wa, Ha, Wb, Hb, m_base, m_count, c->xs[0],
+                                                    c->bxs, c->T[0], st);
+            else if (tma_now)
                 e = cpi::launch_refocus_stage1_tma(&c->s1maps, nf, Wa, Ha, Wb, Hb, m_base, m_count, m_block, m_stride,
                                                    c->xs, c->ys, c->T, c->xblk, c->num_sms, st);
             else if (!cyclic)
@@ -819,7 +845,11 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, 
         {
             TimedScope ts(c, KC_STAGE2, st);
             cudaError_t e = cudaSuccess;
-            if (c->use_s2_staged) {
+            if (genb) {
+                e = cpi::launch_refocus_stage2_genb(c->T[0], Wa, Ha, Hb, m_base, m_count, c->xs[0], c->ys[0], c->bys,
+                                                    planes + int64_t(p0) * Ha * Wa, st);
+                c->launches += 1;
+            } else if (c->use_s2_staged) {
                 e = cpi::launch_refocus_stage2_group(c->T, nf, Wa, Ha, Hb, m_base, m_count, m_block, m_stride, c->xs,
                                                      c->ys, c->ypack, planes + int64_t(p0) * Ha * Wa, st);
                 c->launches += 1;

@@ -87,8 +87,21 @@ struct CoordsGroupArgs {
     int Wa, Ha, Wb, Hb, boundary;
     double map[4][6];
     AxisTables xs[4], ys[4];
+    double bmap[4][4];          // B-axis maps (ex, fx, ey, fy): c_B = ((e (u - c_b)) + f) + c_b;
+                                // (1, 0, 1, 0) = integral B lattice (default).  A sample whose B
+                                // coordinate leaves [0, W_b - 1] is skipped (skip policy).
+    AxisTables bx[4], by[4];    // fractional-B path only: B support per u / v (i0 [W_b], t [W_b])
+    int genb;                   // fill bx / by
 };
 cudaError_t launch_refocus_coords_group(const CoordsGroupArgs& g, int n_fuse, cudaStream_t st);
+// General-B refocus (maps with fractional B coordinates that depend on u / v only): plain
+// staged stage 1 with 2 x 2 corners per sample into T[x][m][n] for every (m, n), and a
+// warp-per-pixel stage 2 with 2 x 2 corners.  Row-major Gamma, contiguous row shards.
+cudaError_t launch_refocus_stage1_genb(const float* gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
+                                       int m_base, int m_count, AxisTables xs, AxisTables bx, double* T,
+                                       cudaStream_t st);
+cudaError_t launch_refocus_stage2_genb(const double* T, int Wa, int Ha, int Hb, int m_base, int m_count,
+                                       AxisTables xs, AxisTables ys, AxisTables by, float* plane, cudaStream_t st);
 cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
                                   int m_base, int m_count, AxisTables xs, AxisTables ys,
                                   double* T, cudaStream_t st);

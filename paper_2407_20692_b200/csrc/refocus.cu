@@ -36,9 +36,15 @@ constexpr int kS1Threads = 256;
 // b = 1 - alpha, c_off = 0 (adding +0.0 leaves the default's value unchanged), a general
 // RefocusMap row supplies (ax, bx, cx) / (ay, by, cy) (include/cpi.h cpi_refocus_spec.affine).
 __device__ __forceinline__ void coords_block(double a, double b, double c_off, int boundary, int W, int Wb,
-                                             AxisTables tab, int ub, bool count);
+                                             AxisTables tab, int ub, bool count, bool b_ok = true);
 __global__ void coords_kernel(double a, double b, double c_off, int boundary, int W, int Wb, AxisTables tab) {
     coords_block(a, b, c_off, boundary, W, Wb, tab, blockIdx.x, true);
+}
+// B coordinate of lattice index ub: c_B = ((e (ub - c_b)) + f) + c_b (fp64, oracle order); the
+// integral map (1, 0) gives ub exactly.
+__device__ __forceinline__ double b_coord(double e, double f, int Wb, int ub) {
+    const double c_b = (Wb - 1) / 2.0;
+    return __dadd_rn(__dadd_rn(__dmul_rn(e, __dadd_rn(static_cast<double>(ub), -c_b)), f), c_b);
 }
 // One launch for a fused group: blockIdx = (B coordinate, plane, axis 0 = x / 1 = y); the
 // per-output counts are left to count_kernel (no atomics, no memsets).
@@ -46,8 +52,20 @@ __global__ void coords_group_kernel(CoordsGroupArgs g) {
     const int ax = blockIdx.z, f = blockIdx.y, ub = blockIdx.x;
     const int W = ax ? g.Ha : g.Wa, Wb = ax ? g.Hb : g.Wb;
     if (ub >= Wb) return;
+    // the sample needs its B coordinate on the lattice too (skip policy)
+    const double e = g.bmap[f][2 * ax], fo = g.bmap[f][2 * ax + 1];
+    const double cb = b_coord(e, fo, Wb, ub);
+    const bool b_ok = g.boundary != 0 || (cb >= 0.0 && cb <= static_cast<double>(Wb - 1));
     coords_block(g.map[f][3 * ax], g.map[f][3 * ax + 1], g.map[f][3 * ax + 2], g.boundary, W, Wb,
-                 ax ? g.ys[f] : g.xs[f], ub, false);
+                 ax ? g.ys[f] : g.xs[f], ub, false, b_ok);
+    if (g.genb && threadIdx.x == 0) {   // B support of this lattice index (clamped under CPI_CLAMP)
+        const double c = fmin(fmax(cb, 0.0), static_cast<double>(Wb - 1));
+        double fl = floor(c);
+        if (fl > static_cast<double>(Wb - 2)) fl = static_cast<double>(Wb - 2);
+        const AxisTables& bt = ax ? g.by[f] : g.bx[f];
+        bt.i0[ub] = static_cast<int>(fl);
+        bt.t[ub] = __dadd_rn(c, -fl);
+    }
 }
 // cnt[x] = number of B coordinates with a used sample at output coordinate x.
 __global__ void count_kernel(CoordsGroupArgs g) {
@@ -62,7 +80,7 @@ __global__ void count_kernel(CoordsGroupArgs g) {
     }
 }
 __device__ __forceinline__ void coords_block(double a, double b, double c_off, int boundary, int W, int Wb,
-                                             AxisTables tab, int ub, bool count) {
+                                             AxisTables tab, int ub, bool count, bool b_ok) {
     const double c_a = (W - 1) / 2.0, c_b = (Wb - 1) / 2.0;
     const double bu = __dmul_rn(b, __dadd_rn(static_cast<double>(ub), -c_b));
     int lo = INT_MAX, hi = -1;
@@ -71,7 +89,7 @@ __device__ __forceinline__ void coords_block(double a, double b, double c_off, i
         double c = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(a, __dadd_rn(static_cast<double>(x), -c_a)), bu), c_off), c_a);
         bool ok;
         if (boundary == 0) {
-            ok = (c >= 0.0) && (c <= static_cast<double>(W - 1));
+            ok = b_ok && (c >= 0.0) && (c <= static_cast<double>(W - 1));
         } else {
             c = fmin(fmax(c, 0.0), static_cast<double>(W - 1));
             ok = true;
@@ -645,6 +663,116 @@ __global__ void pack_ytable_kernel(PackGroupArgs g, int Ha, int Hb, uint32_t* __
     }
 }
 
+// ---- general-B refocus (fractional B coordinates depending on u / v only) ----------------
+// Stage 1: CTA = (8 B rows n, A row m, 256 x); u is walked in chunks whose B supports span at
+// most kGbCols columns; the chunk's Gamma rows (n, j in span) x those columns are staged in
+// padded smem and each thread (x) takes 2 x 2 corners per (u, n).
+constexpr int kGbCols = 10, kGbPad = 11, kGbMaxU = 8;
+
+__global__ void __launch_bounds__(kS1Threads)
+stage1_genb_kernel(const float* __restrict__ gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb, int m_base,
+                   AxisTables xs, AxisTables bx, double* __restrict__ T) {
+    extern __shared__ float sgb[];   // [kVG][nj][kGbPad]
+    const int n0 = blockIdx.x * kVG;
+    const int m = m_base + blockIdx.y;
+    const int x = blockIdx.z * kS1Threads + threadIdx.x;
+    const int nv = min(kVG, Hb - n0);
+    double acc[kVG];
+#pragma unroll
+    for (int v = 0; v < kVG; ++v) acc[v] = 0.0;
+    const float* g_m = gamma + static_cast<int64_t>(m - m_base) * Wa * ldg;
+    int u0 = 0;
+    while (u0 < Wb) {
+        // grow the chunk while its B supports fit kGbCols columns (block-uniform)
+        int klo = INT_MAX, khi = -1, jlo = INT_MAX, jhi = -1, nu = 0;
+        while (u0 + nu < Wb && nu < kGbMaxU) {
+            const int k = __ldg(bx.i0 + u0 + nu);
+            const int l = min(klo, k), h = max(khi, k + 1);
+            if (h - l + 1 > kGbCols) break;
+            klo = l; khi = h;
+            jlo = min(jlo, __ldg(xs.lo + u0 + nu));
+            jhi = max(jhi, __ldg(xs.hi + u0 + nu));
+            ++nu;
+        }
+        const int nk = khi - klo + 1;
+        if (jhi >= jlo) {
+            const int nj = jhi - jlo + 1;
+            __syncthreads();
+            for (int rr = threadIdx.x; rr < nv * nj * nk; rr += kS1Threads) {
+                const int v = rr / (nj * nk), rem = rr - v * nj * nk, jj = rem / nk, kk = rem - jj * nk;
+                sgb[(v * nj + jj) * kGbPad + kk] =
+                    __ldg(g_m + static_cast<int64_t>(jlo + jj) * ldg + static_cast<int64_t>(n0 + v) * Wb + klo + kk);
+            }
+            __syncthreads();
+            if (x < Wa) {
+                float part[kVG];
+#pragma unroll
+                for (int v = 0; v < kVG; ++v) part[v] = 0.f;
+                for (int q = 0; q < nu; ++q) {
+                    const int u = u0 + q;
+                    const int64_t ti = static_cast<int64_t>(u) * Wa + x;
+                    const int j0 = __ldg(xs.i0 + ti);
+                    if (j0 < 0) continue;
+                    const float t = static_cast<float>(__ldg(xs.t + ti)), w0 = 1.f - t;
+                    const float tk = static_cast<float>(__ldg(bx.t + u)), wk0 = 1.f - tk;
+                    const int kk = __ldg(bx.i0 + u) - klo;
+                    const float* s0 = sgb + (j0 - jlo) * kGbPad + kk;
+#pragma unroll
+                    for (int v = 0; v < kVG; ++v) {
+                        if (v < nv) {
+                            const float* r = s0 + v * nj * kGbPad;
+                            const float lo = fmaf(tk, r[1], wk0 * r[0]);
+                            const float hi = fmaf(tk, r[kGbPad + 1], wk0 * r[kGbPad]);
+                            part[v] = fmaf(t, hi, fmaf(w0, lo, part[v]));
+                        }
+                    }
+                }
+#pragma unroll
+                for (int v = 0; v < kVG; ++v) acc[v] += static_cast<double>(part[v]);
+            }
+        }
+        u0 += nu;
+    }
+    if (x < Wa) {
+        double* dst = T + (static_cast<int64_t>(x) * Ha + m) * Hb + n0;
+        for (int v = 0; v < nv; ++v) dst[v] = acc[v];
+    }
+}
+
+// Stage 2: one warp per output pixel (x, y); lanes over v; 2 x 2 corners (m, n) of T.
+__global__ void stage2_genb_kernel(const double* __restrict__ T, int Wa, int Ha, int Hb, int m_lo, int m_hi,
+                                   AxisTables xs, AxisTables ys, AxisTables by, float* __restrict__ plane) {
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= static_cast<int64_t>(Wa) * Ha) return;
+    const int x = static_cast<int>(gw % Wa), y = static_cast<int>(gw / Wa);
+    const double* Tx = T + static_cast<int64_t>(x) * Ha * Hb;
+    double sum = 0.0;
+    for (int v = lane; v < Hb; v += 32) {
+        const int64_t ti = static_cast<int64_t>(v) * Ha + y;
+        const int m0 = __ldg(ys.i0 + ti);
+        if (m0 < 0) continue;
+        const double t = __ldg(ys.t + ti);
+        const int n = __ldg(by.i0 + v);
+        const double tn = __ldg(by.t + v);
+        double c[2];
+        for (int dm = 0; dm < 2; ++dm) {
+            const int mm = m0 + dm;
+            const bool in = mm >= m_lo && mm < m_hi;
+            const double a0 = in ? Tx[static_cast<int64_t>(mm) * Hb + n] : 0.0;
+            const double a1 = in ? Tx[static_cast<int64_t>(mm) * Hb + n + 1] : 0.0;
+            c[dm] = __dadd_rn(1.0, -tn) * a0 + tn * a1;
+        }
+        sum += __dadd_rn(1.0, -t) * c[0] + t * c[1];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) {
+        const int64_t cnt = static_cast<int64_t>(__ldg(xs.cnt + x)) * __ldg(ys.cnt + y);
+        plane[static_cast<int64_t>(y) * Wa + x] = cnt ? static_cast<float>(sum / static_cast<double>(cnt)) : 0.f;
+    }
+}
+
 }  // namespace
 
 bool stage2_staged_supported(int Ha) { return Ha >= 2 && Ha <= kS2Threads; }
@@ -784,6 +912,31 @@ cudaError_t launch_refocus_stage2(const double* T, int Wa, int Ha, int Hb, int m
     const int64_t blocks = (warps * 32 + 255) / 256;
     stage2_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(T, Wa, Ha, Hb, m_base, m_base + m_count,
                                                                  xs, ys, plane);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_refocus_stage1_genb(const float* gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
+                                       int m_base, int m_count, AxisTables xs, AxisTables bx, double* T,
+                                       cudaStream_t st) {
+    const size_t smem = static_cast<size_t>(kVG) * Wa * kGbPad * sizeof(float);
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        cudaError_t e = cudaFuncSetAttribute(stage1_genb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        attr = smem;
+    }
+    dim3 grid((Hb + kVG - 1) / kVG, m_count, (Wa + kS1Threads - 1) / kS1Threads);
+    stage1_genb_kernel<<<grid, kS1Threads, smem, st>>>(gamma, ldg, Wa, Ha, Wb, Hb, m_base, xs, bx, T);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_refocus_stage2_genb(const double* T, int Wa, int Ha, int Hb, int m_base, int m_count,
+                                       AxisTables xs, AxisTables ys, AxisTables by, float* plane, cudaStream_t st) {
+    const int64_t warps = static_cast<int64_t>(Wa) * Ha;
+    const int64_t blocks = (warps * 32 + 255) / 256;
+    stage2_genb_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(T, Wa, Ha, Hb, m_base, m_base + m_count, xs,
+                                                                      ys, by, plane);
     return cudaGetLastError();
 }
 

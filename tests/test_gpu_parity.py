@@ -463,5 +463,28 @@ def test_refocus_affine_maps(boundary):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(p2.cpu().numpy(), p1.cpu().numpy())
     from paper_2407_20692_b200 import CpiError
-    with pytest.raises(CpiError, match="UNSUPPORTED"):
-        ctx.refocus(None, g, p1, affine=[[1.0, 0.0, 0.0, 0.0, 0.5, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0, 0.0]])
+    with pytest.raises(CpiError, match="UNSUPPORTED"):      # B coordinate depending on x
+        ctx.refocus(None, g, p1, affine=[[1.0, 0.0, 0.0, 0.1, 1.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0, 0.0]])
+
+
+@pytest.mark.parametrize("boundary", [0, 1])
+def test_refocus_affine_fractional_b(boundary):
+    """General maps with fractional B coordinates (ex, fx, ey, fy arbitrary; dx = dy = 0): the
+    general-B kernels (2 x 2 corners per stage) vs the oracle's 16-corner refocus, 1e-6 M."""
+    dims = (24, 20, 16, 12)
+    Wa, Ha, Wb, Hb = dims
+    G = synth.random_gamma(Wa * Ha, Wb * Hb, seed=23)
+    maps = [[0.7, 0.3, 0.25, 0.0, 0.5, -0.3, 1.3, -0.3, -0.4, 0.0, 0.8, 0.2],
+            [1.0, 0.0, 0.0, 0.0, 0.75, 0.1, 0.9, 0.1, 0.0, 0.0, 1.1, 0.0],
+            [1.6, -0.45, -1.5, 0.0, 1.25, 0.5, 0.55, 0.5, 2.0, 0.0, 0.6, -1.0],
+            [2.0, -1.0, 0.5, 0.0, -0.9, 0.0, 0.5, 0.5, 0.0, 0.0, 1.9, 0.3],
+            [0.8, 0.2, 0.0, 0.0, 1.0, 0.0, 1.2, -0.2, 0.0, 0.0, 1.0, 0.0]]   # last: integral B in a mixed call
+    ctx = _ctx((0, 0, Wa, Ha), (0, 0, Wb, Hb), 1)
+    g = torch.from_numpy(np.ascontiguousarray(G, dtype=np.float32)).cuda()
+    planes = ctx.new_planes(len(maps))
+    ctx.refocus(None, g, planes, boundary=boundary, affine=maps)
+    torch.cuda.synchronize()
+    R = planes.cpu().numpy().astype(np.float64)
+    Ro = oracle.refocus_affine(G, dims, maps, boundary=boundary)
+    M = oracle.refocus_affine(np.abs(G.astype(np.float64)), dims, maps, boundary=boundary)
+    assert np.all(np.abs(R - Ro) <= 1e-6 * M + 1e-30), np.max(np.abs(R - Ro) / np.maximum(M, 1e-300))
