@@ -107,7 +107,12 @@ typedef struct {
     int32_t n_planes;       /* >= 1 */
     int32_t boundary;       /* CPI_SKIP_RENORMALIZE | CPI_CLAMP */
     const float *gamma_dev; /* DEVICE Gamma rows [row0, row0 + rows) of [P_a][P_b], row-major,
-                               leading dimension P_b (e.g. cpi_correlate's output) */
+                               leading dimension P_b (e.g. cpi_correlate's output), or NULL:
+                               refocus this context's current totals (SURVEY §8(b)
+                               CPI_FROM_COUNTS) -- the Gamma the last cpi_correlate /
+                               cpi_finalize wrote, else Gamma finalised from the kept counts
+                               into a library workspace (CPI_KEEP_COUNTS, 4 P_a P_b bytes);
+                               then row0 = 0, rows = P_a. */
     int64_t row0, rows;     /* multiples of roi_a.width; a single GPU passes 0, P_a.  A row
                                shard yields that shard's additive share of every plane. */
     int32_t row_block;      /* A-row layout of the shard (SURVEY §8(e) load balance): the

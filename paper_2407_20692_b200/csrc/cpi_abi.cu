@@ -66,6 +66,7 @@ struct cpi_ctx {
     int64_t n_tot = 0;
     int64_t batches = 0;
     float* gamma_current = nullptr;        // Gamma buffer written for the current totals
+    float* gamma_ws = nullptr;             // library Gamma for cpi_refocus from counts (lazy)
     CUtensorMap tm_a{}, tm_b{};
     // refocus workspaces
     cpi::AxisTables xs[cpi::kRefocusMaxFuse]{}, ys[cpi::kRefocusMaxFuse]{};
@@ -212,6 +213,7 @@ void free_all(cpi_ctx* c) {
     cudaFree(c->xpack);
     cudaFree(c->ypack);
     cudaFree(c->xblk);
+    cudaFree(c->gamma_ws);
     for (auto& t : c->timed) { c->event_pool.push_back(t.a); c->event_pool.push_back(t.b); }
     for (auto e : c->event_pool) cudaEventDestroy(e);
 }
@@ -663,9 +665,26 @@ cpi_status cpi_reset(cpi_ctx* c, void* stream) {
     return CPI_OK;
 }
 
-cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, void* stream) {
+cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* planes, void* stream) {
     if (!c) return CPI_ERR_INVALID_ARG;
-    if (!spec || !planes) return fail(c, CPI_ERR_INVALID_ARG, "spec and planes_dev must be non-NULL");
+    if (!spec_in || !planes) return fail(c, CPI_ERR_INVALID_ARG, "spec and planes_dev must be non-NULL");
+    cpi_refocus_spec spec_local = *spec_in;
+    const cpi_refocus_spec* spec = &spec_local;
+    if (!spec_local.gamma_dev) {
+        // the context's current totals (SURVEY §8(b) CPI_FROM_COUNTS): the fused / finalised
+        // Gamma of the last call, else Gamma finalised from the kept counts
+        if (c->n_tot == 0) return fail(c, CPI_ERR_ZERO_FRAMES, "refocus from counts needs N_TOT >= 1");
+        if (!c->gamma_current) {
+            if (!c->keep) return fail(c, CPI_ERR_STATE, "gamma_dev is NULL: no current Gamma and no kept counts");
+            if (!c->gamma_ws) CK(c, cudaMalloc(&c->gamma_ws, sizeof(float) * size_t(c->p_a) * c->p_b));
+            cpi_status s = cpi_finalize(c, c->gamma_ws, nullptr, stream);
+            if (s != CPI_OK) return s;
+        }
+        spec_local.gamma_dev = c->gamma_current;
+        spec_local.row0 = 0;
+        spec_local.rows = c->p_a;
+        spec_local.row_block = 0;
+    }
     if (spec->n_planes < 1 || (!spec->alphas && !spec->affine))
         return fail(c, CPI_ERR_EMPTY_ANGULAR_GRID, "n_planes must be >= 1");
     if (spec->boundary != CPI_SKIP_RENORMALIZE && spec->boundary != CPI_CLAMP)

@@ -488,3 +488,36 @@ def test_refocus_affine_fractional_b(boundary):
     Ro = oracle.refocus_affine(G, dims, maps, boundary=boundary)
     M = oracle.refocus_affine(np.abs(G.astype(np.float64)), dims, maps, boundary=boundary)
     assert np.all(np.abs(R - Ro) <= 1e-6 * M + 1e-30), np.max(np.abs(R - Ro) / np.maximum(M, 1e-300))
+
+
+def test_refocus_from_current_totals():
+    """cpi_refocus with gamma_dev = NULL (SURVEY §8(b) CPI_FROM_COUNTS) refocuses the context's
+    current totals: the fused Gamma of the last correlate, or Gamma finalised from the kept
+    counts after further batches -- bit-identical to passing that Gamma explicitly."""
+    from paper_2407_20692_b200 import CpiError
+    roi_a, roi_b = (0, 0, 32, 24), (256, 0, 20, 16)
+    fr = synth.bernoulli_frames(1500, 0.1, seed=71)
+    al = [0.6, 1.0, 1.4]
+    ctx = _ctx(roi_a, roi_b, 1000, keep_counts=True)
+    g = ctx.new_gamma()
+    ctx.load_frames(fr[:1000])
+    ctx.correlate(g)
+    p_none, p_expl = ctx.new_planes(3), ctx.new_planes(3)
+    ctx.refocus(al, None, p_none)
+    ctx.refocus(al, g, p_expl)
+    ctx.load_frames(fr[1000:])
+    ctx.correlate(None)                       # totals move on; Gamma now only in the counts
+    p2_none = ctx.new_planes(3)
+    ctx.refocus(al, None, p2_none)
+    g2 = ctx.new_gamma()
+    ctx.finalize(g2)
+    p2_expl = ctx.new_planes(3)
+    ctx.refocus(al, g2, p2_expl)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(p_none.cpu().numpy(), p_expl.cpu().numpy())
+    np.testing.assert_array_equal(p2_none.cpu().numpy(), p2_expl.cpu().numpy())
+    want = oracle.correlate(fr, roi_a, roi_b)
+    _assert_planes(p2_none.cpu().numpy().astype(np.float64), want["gamma"], (32, 24, 20, 16), al)
+    bare = _ctx(roi_a, roi_b, 100)
+    with pytest.raises(CpiError, match="ZERO_FRAMES|STATE"):
+        bare.refocus(al, None, bare.new_planes(3))
