@@ -716,7 +716,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
     CK(c, cudaSetDevice(c->dev));
     auto st = static_cast<cudaStream_t>(stream);
     if (!c->refocus_ready) {
-        c->use_s1_tma = cpi::stage1_tma_supported(Wa, Wb) && getenv("CPI_STAGE1_SIMPLE") == nullptr;
+        c->use_s1_tma = cpi::stage1_tma_supported(Wa, Wb, Hb) && getenv("CPI_STAGE1_SIMPLE") == nullptr;
         if (const char* ev = getenv("CPI_REFOCUS_FUSE")) c->fuse = atoi(ev);
         if (c->fuse < 1) c->fuse = 1;
         if (c->fuse > cpi::kRefocusMaxFuse) c->fuse = cpi::kRefocusMaxFuse;

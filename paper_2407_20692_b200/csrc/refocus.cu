@@ -291,7 +291,8 @@ struct S1Cfg {
     static constexpr int kOffX = kStages * kTGFloats * 4;
     static constexpr int kOffSpan = kOffX + kStages * F * kTXEntries * 4;
     static constexpr int kOffXblk = kOffSpan + kTMaxChunks * 8;
-    static constexpr int kOffBar = kOffXblk + kTMaxChunks * 4;
+    static constexpr int kOffYb = kOffXblk + kTMaxChunks * 4;   // int2 [F][H_b <= 256] y bands
+    static constexpr int kOffBar = kOffYb + F * 256 * 8;
     static constexpr int kSmem = kOffBar + 4 * kStages * 8 + 64;
 };
 
@@ -312,13 +313,14 @@ __device__ __forceinline__ int shard_row(const S1Args& a, int l) {
     return a.m_base + (l / a.m_block) * a.m_stride + l % a.m_block;
 }
 
-template <int F>
-__device__ __forceinline__ unsigned tile_mask(const S1Args& a, int m, int v0, int f) {
+// v rows of the tile (m, v0..v0+7) that plane f needs: m inside the used band [lo_y(v), hi_y(v)]
+// of stage 2 (bands staged in smem once per CTA)
+__device__ __forceinline__ unsigned tile_mask(const int2* yband, int Hb, int m, int v0, int f) {
     unsigned need = 0;
-    const int nv = min(kTVG, a.Hb - v0);
+    const int nv = min(kTVG, Hb - v0);
     for (int v = 0; v < nv; ++v) {
-        const int lo = __ldg(a.ylo[f] + v0 + v), hi = __ldg(a.yhi[f] + v0 + v);
-        if (m >= lo && m <= hi) need |= 1u << v;
+        const int2 b = yband[f * 256 + v0 + v];
+        if (m >= b.x && m <= b.y) need |= 1u << v;
     }
     return need;
 }
@@ -357,6 +359,11 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
             }
         span[c] = make_int2(lo, hi);
     }
+    int2* yband = reinterpret_cast<int2*>(s1_smem + C::kOffYb);
+    for (int i = threadIdx.x; i < F * a.Hb; i += blockDim.x) {
+        const int f = i / a.Hb, v = i - f * a.Hb;
+        yband[f * 256 + v] = make_int2(__ldg(a.ylo[f] + v), __ldg(a.yhi[f] + v));
+    }
     uint32_t* xblk = reinterpret_cast<uint32_t*>(s1_smem + C::kOffXblk);
     for (int c = threadIdx.x; c < a.n_chunks; c += blockDim.x) {   // OR over the group's planes
         uint32_t b = 0;
@@ -377,7 +384,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                 const int ml = tile / a.n_vg, vg = tile - ml * a.n_vg;
                 unsigned any = 0;
 #pragma unroll
-                for (int f = 0; f < F; ++f) any |= tile_mask<F>(a, shard_row(a, ml), vg * kTVG, f);
+                for (int f = 0; f < F; ++f) any |= tile_mask(yband, a.Hb, shard_row(a, ml), vg * kTVG, f);
                 if (!any) continue;
                 for (int c = 0; c < a.n_chunks; ++c) {
                     const int2 sp = span[c];
@@ -417,7 +424,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
         const int m = shard_row(a, ml), v0 = vg * kTVG;
         unsigned mask[F], any = 0;
 #pragma unroll
-        for (int f = 0; f < F; ++f) { mask[f] = tile_mask<F>(a, m, v0, f); any |= mask[f]; }
+        for (int f = 0; f < F; ++f) { mask[f] = tile_mask(yband, a.Hb, m, v0, f); any |= mask[f]; }
         if (!any) continue;
         double acc[F][2][4];
 #pragma unroll
@@ -847,7 +854,9 @@ cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int H
     return cudaGetLastError();
 }
 
-bool stage1_tma_supported(int Wa, int Wb) { return Wa <= 256 && Wa >= 2 && (Wb % 4) == 0 && Wb <= 8 * kTMaxChunks; }
+bool stage1_tma_supported(int Wa, int Wb, int Hb) {
+    return Wa <= 256 && Wa >= 2 && (Wb % 4) == 0 && Wb <= 8 * kTMaxChunks && Hb <= 256;
+}
 
 cudaError_t launch_pack_xtable_group(const AxisTables* xs, int n_fuse, int Wa, int Wb, uint32_t* xpack,
                                      uint32_t* xblk, cudaStream_t st) {
