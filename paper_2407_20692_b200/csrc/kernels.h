@@ -106,7 +106,7 @@ cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int H
                                   int m_base, int m_count, AxisTables xs, AxisTables ys,
                                   double* T, cudaStream_t st);
 // KB5 (TMA variant): warp-specialised, persistent, TMA-fed stage 1 over n_fuse (<= 4) planes
-// sharing one pass over Gamma.  Needs W_a <= 256, W_b % 4 == 0, W_b <= 512, the tensor maps of
+// sharing one pass over Gamma.  Needs W_a <= 256 with W_a % 4 == 0, W_b % 4 == 0, W_b <= 512, H_b <= 256, the tensor maps of
 // Gamma (4D: u, v, j, m) and of the packed x-tables (3D uint32: x, u, plane slot).
 constexpr int kRefocusMaxFuse = 4;
 struct Stage1Maps {

@@ -855,7 +855,8 @@ cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int H
 }
 
 bool stage1_tma_supported(int Wa, int Wb, int Hb) {
-    return Wa <= 256 && Wa >= 2 && (Wb % 4) == 0 && Wb <= 8 * kTMaxChunks && Hb <= 256;
+    // 16-byte TMA strides: W_a (x-table rows) and W_b (Gamma rows) multiples of 4 floats
+    return Wa <= 256 && Wa >= 4 && (Wa % 4) == 0 && (Wb % 4) == 0 && Wb <= 8 * kTMaxChunks && Hb <= 256;
 }
 
 cudaError_t launch_pack_xtable_group(const AxisTables* xs, int n_fuse, int Wa, int Wb, uint32_t* xpack,
