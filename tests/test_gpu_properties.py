@@ -56,3 +56,59 @@ def test_random_refocus(wa, ha, wb, hb, alphas, boundary, seed):
     Ro = oracle.refocus(G, dims, alphas, boundary=boundary)
     M = oracle.refocus(np.abs(G.astype(np.float64)), dims, alphas, boundary=boundary)
     assert np.all(np.abs(R - Ro) <= 1e-6 * M + 1e-30)
+
+
+coef = st.floats(-1.5, 1.5)
+
+
+@settings(max_examples=20, deadline=None, suppress_health_check=list(HealthCheck))
+@given(wa=st.integers(2, 24), ha=st.integers(2, 20), wb=st.integers(2, 16), hb=st.integers(2, 10),
+       n_planes=st.integers(1, 3), boundary=st.sampled_from([0, 1]), integral_b=st.booleans(),
+       seed=st.integers(0, 2**31 - 1), data=st.data())
+def test_random_affine_maps(wa, ha, wb, hb, n_planes, boundary, integral_b, seed, data):
+    """Random general RefocusMap rows (dx = dy = 0), integral or fractional B, vs the oracle."""
+    from paper_2407_20692_b200 import Context
+    maps = []
+    for _ in range(n_planes):
+        ax, bx, cx, ay, by, cy = (data.draw(coef) for _ in range(6))
+        if integral_b:
+            ex, fx, ey, fy = 1.0, 0.0, 1.0, 0.0
+        else:
+            ex, fx, ey, fy = (data.draw(st.floats(0.3, 1.8)), data.draw(coef), data.draw(st.floats(0.3, 1.8)),
+                              data.draw(coef))
+        maps.append([ax, bx, cx, 0.0, ex, fx, ay, by, cy, 0.0, ey, fy])
+    dims = (wa, ha, wb, hb)
+    G = synth.random_gamma(wa * ha, wb * hb, seed=seed)
+    ctx = Context((0, 0, wa, ha), (0, 0, wb, hb), 1)
+    g = torch.from_numpy(np.ascontiguousarray(G, dtype=np.float32)).cuda()
+    planes = ctx.new_planes(n_planes)
+    ctx.refocus(None, g, planes, boundary=boundary, affine=maps)
+    torch.cuda.synchronize()
+    R = planes.cpu().numpy().astype(np.float64)
+    Ro = oracle.refocus_affine(G, dims, maps, boundary=boundary)
+    M = oracle.refocus_affine(np.abs(G.astype(np.float64)), dims, maps, boundary=boundary)
+    assert np.all(np.abs(R - Ro) <= 1e-6 * M + 1e-30)
+
+
+@settings(max_examples=15, deadline=None, suppress_health_check=list(HealthCheck))
+@given(h=st.integers(1, 40), w=st.integers(8, 40), n=st.integers(1, 600), variant=st.sampled_from(["tc", "fp4", "popc"]),
+       cuts=st.lists(st.integers(1, 8), min_size=0, max_size=4), seed=st.integers(0, 2**31 - 1))
+def test_random_row_panels(h, w, n, variant, cuts, seed):
+    """cpi_correlate_rows over random aligned panel splits equals cpi_correlate bit for bit."""
+    from paper_2407_20692_b200 import Context
+    roi_a, roi_b = (0, 0, w, h), (300, 10, 12, 9)
+    fr = synth.bernoulli_frames(n, 0.3, seed=seed)
+    full = Context(roi_a, roi_b, n, variant=variant, keep_counts=True)
+    full.load_frames(fr)
+    gf = full.correlate(full.new_gamma())
+    part = Context(roi_a, roi_b, n, variant=variant, keep_counts=True)
+    al, pa = part.row_align(), part.p_a
+    bounds = sorted({min(pa, c * al) for c in cuts} | {0, pa})
+    gp = part.new_gamma()
+    part.load_frames(fr)
+    for r0, r1 in zip(bounds[:-1], bounds[1:]):
+        if r1 > r0:
+            part.correlate_rows(r0, r1 - r0, gp)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(part.counts_views()[0].cpu().numpy(), full.counts_views()[0].cpu().numpy())
+    np.testing.assert_array_equal(gp.cpu().numpy(), gf.cpu().numpy())
