@@ -245,6 +245,8 @@ constexpr int kTRow = kTVG * kTUC;                     // floats per staged j ro
 constexpr int kTGFloats = (kTMaxJ + 2) * kTRow;        // 64.5 KB per stage; rows 256-257 stay zero
 constexpr int kTXEntries = kTUC * 256;                 // 8 KB per plane per stage (uint32 entries)
 constexpr int kTMaxChunks = 64;                        // W_b <= 512
+// staged j rows of the TMA stage 1 for an A RoI of width W_a (the zero rows follow them)
+__host__ __device__ constexpr int stage1_rows(int Wa) { return Wa <= 128 ? 128 : kTMaxJ; }
 constexpr int kTConsumers = 8;
 constexpr int kTThreads = 32 * (kTConsumers + 1);
 
@@ -283,13 +285,17 @@ __device__ __forceinline__ void s1_taps(uint64_t (&part)[2], uint32_t e, const f
     }
 }
 
-template <int F>
+// kJ = staged j rows (W_a <= kJ): 256, or 128 for A RoIs up to 128 wide, whose smaller stages
+// give a 4-deep ring; rows kJ, kJ + 1 of every stage stay zero (skipped samples).
+template <int F, int kJ = kTMaxJ>
 struct S1Cfg {
-    static constexpr int kStages = F == 1 ? 3 : 2;
+    static constexpr int kGFloats = (kJ + 2) * kTRow;
+    static constexpr int kStages = kJ <= 128 ? 4 : (F == 1 ? 3 : 2);
     // smem map (bytes): [Gamma stages (258 rows each)][x-table stages x F][span table]
     //                   [x-block masks][barriers]
-    static constexpr int kOffX = kStages * kTGFloats * 4;
-    static constexpr int kOffSpan = kOffX + kStages * F * kTXEntries * 4;
+    static constexpr int kOffX = kStages * kGFloats * 4;
+    static constexpr int kXEntries = kTUC * kJ;             // x-table entries per (stage, plane) slot
+    static constexpr int kOffSpan = kOffX + kStages * F * kXEntries * 4;
     static constexpr int kOffXblk = kOffSpan + kTMaxChunks * 8;
     static constexpr int kOffYb = kOffXblk + kTMaxChunks * 4;   // int2 [F][H_b <= 256] y bands
     static constexpr int kOffBar = kOffYb + F * 256 * 8;
@@ -325,10 +331,10 @@ __device__ __forceinline__ unsigned tile_mask(const int2* yband, int Hb, int m, 
     return need;
 }
 
-template <bool kFullX, int F, bool kSkip>
+template <bool kFullX, int F, bool kSkip, int kJ>
 __global__ void __launch_bounds__(kTThreads, 1)
 stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_x, S1Args a) {
-    using C = S1Cfg<F>;
+    using C = S1Cfg<F, kJ>;
     extern __shared__ __align__(1024) uint8_t s1_smem[];
     float* sg = reinterpret_cast<float*>(s1_smem);
     const uint32_t* sx = reinterpret_cast<const uint32_t*>(s1_smem + C::kOffX);
@@ -346,7 +352,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
     }
     // zero every staged Gamma row once: rows 256-257 of each stage are the skipped-sample
     // rows, and a zero-weight tap past a chunk's span then reads 0 or an earlier finite value
-    for (int i = threadIdx.x; i < C::kStages * kTGFloats; i += blockDim.x) sg[i] = 0.f;
+    for (int i = threadIdx.x; i < C::kStages * C::kGFloats; i += blockDim.x) sg[i] = 0.f;
     fence_proxy_async_smem();   // the zeros must land before the first TMA writes these rows
     // union j span [lo, hi] over the F planes of every u chunk (lo > hi: chunk unused)
     for (int c = threadIdx.x; c < a.n_chunks; c += blockDim.x) {
@@ -392,7 +398,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                     const int nb = (sp.y - sp.x + kTJBox) / kTJBox;
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], nb * kTJBox * kTRow * 4 + F * kTUC * a.Wa * 4);
-                    float* dst = sg + stage * kTGFloats;
+                    float* dst = sg + stage * C::kGFloats;
                     for (int b = 0; b < nb; ++b) {
                         if (a.gamma_5d)   // u-blocked Gamma: one 256-B segment per (j, chunk)
                             tma_load_5d(dst + b * kTJBox * kTRow, &tm_g, &full[stage], 0, vg * kTVG, c,
@@ -403,7 +409,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                     }
 #pragma unroll
                     for (int f = 0; f < F; ++f)
-                        tma_load_3d(s1_smem + C::kOffX + (stage * F + f) * kTXEntries * 4, &tm_x, &full[stage], 0,
+                        tma_load_3d(s1_smem + C::kOffX + (stage * F + f) * C::kXEntries * 4, &tm_x, &full[stage], 0,
                                     c * kTUC, f);
                     if (++stage == C::kStages) { stage = 0; phase ^= 1; }
                 }
@@ -437,7 +443,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
             const int2 sp = span[c];
             if (sp.y < sp.x) continue;
             mbar_wait(&full[stage], phase);
-            const float* G = sg + stage * kTGFloats;
+            const float* G = sg + stage * C::kGFloats;
             // fp32 partial sums of this chunk as packed pairs (slots s = 2p, 2p + 1): the taps run
             // on FFMA2 (fma.rn.f32x2), lane-wise identical to two scalar fmaf in the same order
             uint64_t part[F][2][2];
@@ -447,7 +453,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                 for (int i = 0; i < 2; ++i)
 #pragma unroll
                     for (int p = 0; p < 2; ++p) part[f][i][p] = 0ull;
-            const uint32_t* sxs = sx + stage * F * kTXEntries + xbase;
+            const uint32_t* sxs = sx + stage * F * C::kXEntries + xbase;
             if constexpr (kSkip) {
                 // i-outer order with a warp-uniform skip of a 16-wide x block that has no used
                 // sample in this chunk for any plane of the group
@@ -461,7 +467,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                         const int uu = (k + xl) & (kTUC - 1);
 #pragma unroll
                         for (int f = 0; f < F; ++f)
-                            s1_taps(part[f][i], sxs[f * kTXEntries + uu * a.Wa + 128 * i], G + uu, voff);
+                            s1_taps(part[f][i], sxs[f * C::kXEntries + uu * a.Wa + 128 * i], G + uu, voff);
                     }
                 }
             } else {
@@ -473,7 +479,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
 #pragma unroll
                         for (int i = 0; i < 2; ++i)
                             if (kFullX || xbase + 128 * i < a.Wa)
-                                s1_taps(part[f][i], sxs[f * kTXEntries + uu * a.Wa + 128 * i], G + uu, voff);
+                                s1_taps(part[f][i], sxs[f * C::kXEntries + uu * a.Wa + 128 * i], G + uu, voff);
                 }
             }
             // Release the stage to the TMA producer.  The reads above are generic-proxy loads and
@@ -511,8 +517,8 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
 // where j_rel = j0 - j_lo(chunk of u) is the smem row of the lower tap inside the chunk's
 // staged union span (the same union the producer stages), t in [0, 1) (a t that rounds to
 // 1 moves to the next row with t = 0), and skipped samples point at the zero rows
-// (j_rel = 256, t = 0).  t keeps 2^-23 resolution; t = 0 stays exact.
-__global__ void pack_xtable_group_kernel(PackGroupArgs g, int Wa, int Wb, uint32_t* __restrict__ out,
+// (j_rel = zrow = the stage's row capacity, t = 0).  t keeps 2^-23 resolution; t = 0 stays exact.
+__global__ void pack_xtable_group_kernel(PackGroupArgs g, int Wa, int Wb, uint32_t zrow, uint32_t* __restrict__ out,
                                          uint32_t* __restrict__ xblk) {
     const int c = blockIdx.x, f = blockIdx.y, c0 = c * 8, n_chunks = gridDim.x;
     __shared__ uint32_t sblk;
@@ -526,7 +532,7 @@ __global__ void pack_xtable_group_kernel(PackGroupArgs g, int Wa, int Wb, uint32
         for (int u = c0; u < c0 + 8 && u < Wb; ++u) {
             const int64_t idx = static_cast<int64_t>(u) * Wa + x;
             const int j = __ldg(g.i0[f] + idx);
-            uint32_t e = 256u << 23;
+            uint32_t e = zrow << 23;
             if (j >= 0) {
                 uint32_t tq = static_cast<uint32_t>(__double2uint_rn(__ldg(g.t[f] + idx) * 8388608.0));
                 int jr = j - jlo;
@@ -865,30 +871,30 @@ cudaError_t launch_pack_xtable_group(const AxisTables* xs, int n_fuse, int Wa, i
     g.n = n_fuse;
     for (int f = 0; f < n_fuse; ++f) { g.i0[f] = xs[f].i0; g.t[f] = xs[f].t; g.lo[f] = xs[f].lo; }
     pack_xtable_group_kernel<<<dim3((Wb + 7) / 8, n_fuse), Wa >= 256 ? 256 : ((Wa + 31) / 32) * 32, 0, st>>>(
-        g, Wa, Wb, xpack, xblk);
+        g, Wa, Wb, static_cast<uint32_t>(stage1_rows(Wa)), xpack, xblk);
     return cudaGetLastError();
 }
 
-template <bool kFullX, int F, bool kSkip>
+template <bool kFullX, int F, bool kSkip, int kJ>
 static cudaError_t launch_s1(const Stage1Maps* maps, const S1Args& a, int grid, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(stage1_tma_kernel<kFullX, F, kSkip>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, S1Cfg<F>::kSmem);
+        cudaError_t e = cudaFuncSetAttribute(stage1_tma_kernel<kFullX, F, kSkip, kJ>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, S1Cfg<F, kJ>::kSmem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    stage1_tma_kernel<kFullX, F, kSkip><<<grid, kTThreads, S1Cfg<F>::kSmem, st>>>(maps->gamma, maps->xtab, a);
+    stage1_tma_kernel<kFullX, F, kSkip, kJ><<<grid, kTThreads, S1Cfg<F, kJ>::kSmem, st>>>(maps->gamma, maps->xtab, a);
     return cudaGetLastError();
 }
 
-template <bool kFullX, bool kSkip>
+template <bool kFullX, bool kSkip, int kJ>
 static cudaError_t launch_s1_f(int F, const Stage1Maps* maps, const S1Args& a, int grid, cudaStream_t st) {
     switch (F) {
-        case 1: return launch_s1<kFullX, 1, kSkip>(maps, a, grid, st);
-        case 2: return launch_s1<kFullX, 2, kSkip>(maps, a, grid, st);
-        case 3: return launch_s1<kFullX, 3, kSkip>(maps, a, grid, st);
-        default: return launch_s1<kFullX, 4, kSkip>(maps, a, grid, st);
+        case 1: return launch_s1<kFullX, 1, kSkip, kJ>(maps, a, grid, st);
+        case 2: return launch_s1<kFullX, 2, kSkip, kJ>(maps, a, grid, st);
+        case 3: return launch_s1<kFullX, 3, kSkip, kJ>(maps, a, grid, st);
+        default: return launch_s1<kFullX, 4, kSkip, kJ>(maps, a, grid, st);
     }
 }
 
@@ -911,9 +917,14 @@ cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa
     const int tiles = m_count * a.n_vg;
     const int grid = tiles < num_sms ? tiles : num_sms;
     const bool skip = getenv("CPI_S1_NOSKIP") == nullptr;   // A/B knob for the x-block skip (read per launch)
+    if (stage1_rows(Wa) == 128)
+        return skip ? launch_s1_f<false, true, 128>(n_fuse, maps, a, grid, st)
+                    : launch_s1_f<false, false, 128>(n_fuse, maps, a, grid, st);
     if (skip)
-        return Wa == 256 ? launch_s1_f<true, true>(n_fuse, maps, a, grid, st) : launch_s1_f<false, true>(n_fuse, maps, a, grid, st);
-    return Wa == 256 ? launch_s1_f<true, false>(n_fuse, maps, a, grid, st) : launch_s1_f<false, false>(n_fuse, maps, a, grid, st);
+        return Wa == 256 ? launch_s1_f<true, true, 256>(n_fuse, maps, a, grid, st)
+                         : launch_s1_f<false, true, 256>(n_fuse, maps, a, grid, st);
+    return Wa == 256 ? launch_s1_f<true, false, 256>(n_fuse, maps, a, grid, st)
+                     : launch_s1_f<false, false, 256>(n_fuse, maps, a, grid, st);
 }
 
 cudaError_t launch_refocus_stage2(const double* T, int Wa, int Ha, int Hb, int m_base, int m_count,
