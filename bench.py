@@ -69,6 +69,14 @@ def rois(name):
     return synth.ROI_TINY_A, synth.ROI_TINY_B
 
 
+def load_traffic():
+    """ncu DRAM bytes per launch of the dominant kernels (profiles/r01_traffic.json)."""
+    try:
+        return json.loads((ROOT / "profiles" / "r01_traffic.json").read_text())
+    except Exception:
+        return {}
+
+
 def load_peaks():
     try:
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
@@ -375,6 +383,7 @@ def main():
         return
 
     peaks, peak_src = load_peaks()
+    traffic = load_traffic()
     hbm = peaks["hbm_gbs"]
     f_clk = (clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)) * 1e6
     gemm_ms, gemm_n = kt["gemm"]
@@ -409,7 +418,10 @@ def main():
                  "frac_of_clock_peak": gemm_tops / clock_peak_tops if gemm_tops else None,
                  "clock_peak_tops": clock_peak_tops,
                  "ops_per_launch": ops, "ms_per_launch": gemm_ms / gemm_n if gemm_n else None,
-                 "traffic": None}
+                 "traffic": traffic.get("gemm_i8_tc2_kernel<fp4>" if args.variant == "fp4" else
+                                        "gemm_i8_tc2_kernel<i8>", {}).get("bytes_per_launch")
+                 if args.variant != "popc" else None,
+                 "traffic_note": "ncu dram read + write bytes per launch (profiles/r01_traffic.json)"}
     roof_s1 = {"kernel": "refocus_stage1_tma (KB5, 4 planes per pass)", "bound": "alu",
                "achieved": s1_gtaps, "peak": lds_peak_gtaps, "unit": "Gtap/s",
                "frac": s1_gtaps / lds_peak_gtaps if s1_gtaps else None,
@@ -419,7 +431,9 @@ def main():
                "hbm_view": {"algorithmic_bytes_per_step": span, "achieved_gbs": s1_gbs, "peak_gbs": hbm,
                             "frac": s1_gbs / hbm if s1_gbs else None,
                             "note": "per-plane span bytes / time; > 1 possible because 4 planes share one HBM pass"},
-               "traffic": None}
+               "traffic": traffic.get("stage1_tma_kernel<1,4,1>", {}).get("bytes_per_launch"),
+               "traffic_note": ("ncu dram read + write bytes of one 4-plane launch (profiles/r01_traffic.json); "
+                                "achieved is per step (16 launches)")}
     dominant = roof_s1 if (s1_ms > gemm_ms) else roof_gemm
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
