@@ -765,7 +765,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
         // (u % 8, v, u / 8, j, m): box 8 x 8 x 1 x 32 x 1 lands as [j][v][u] like the 4D map
         const cuuint64_t dims[5] = {8u, cuuint64_t(Hb), cuuint64_t(Wb / 8), cuuint64_t(Wa), cuuint64_t(spec->rows / Wa)};
         const cuuint64_t strides[4] = {32u, cuuint64_t(Hb) * 32, cuuint64_t(c->p_b) * 4, cuuint64_t(Wa) * c->p_b * 4};
-        const cuuint32_t box[5] = {8u, 8u, 1u, 32u, 1u};
+        const cuuint32_t box[5] = {8u, cuuint32_t(cpi::stage1_vgroup(Wa)), 1u, 32u, 1u};
         const cuuint32_t es[5] = {1u, 1u, 1u, 1u, 1u};
         CUresult r = enc(&c->s1maps.gamma, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(spec->gamma_dev),
                          dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -777,7 +777,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
         cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
         const cuuint64_t dims[4] = {cuuint64_t(Wb), cuuint64_t(Hb), cuuint64_t(Wa), cuuint64_t(spec->rows / Wa)};
         const cuuint64_t strides[3] = {cuuint64_t(Wb) * 4, cuuint64_t(c->p_b) * 4, cuuint64_t(Wa) * c->p_b * 4};
-        const cuuint32_t box[4] = {8u, 8u, 32u, 1u};
+        const cuuint32_t box[4] = {8u, cuuint32_t(cpi::stage1_vgroup(Wa)), 32u, 1u};
         const cuuint32_t es[4] = {1u, 1u, 1u, 1u};
         // L2 sector promotion of the Gamma stream (tuning knob CPI_S1_L2PROMO = 0/64/128/256)
         CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;

@@ -115,6 +115,7 @@ struct Stage1Maps {
     int gamma_5d = 0;
 };
 bool stage1_tma_supported(int Wa, int Wb, int Hb);
+int stage1_vgroup(int Wa);   // B rows v per stage-1 tile (Gamma tensor-map box height)
 cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa, int Ha, int Wb, int Hb,
                                       int m_base, int m_count, int m_block, int m_stride, const AxisTables* xs,
                                       const AxisTables* ys, double* const* T, const uint32_t* xblk, int num_sms,

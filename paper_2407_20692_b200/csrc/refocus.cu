@@ -247,6 +247,8 @@ constexpr int kTXEntries = kTUC * 256;                 // 8 KB per plane per sta
 constexpr int kTMaxChunks = 64;                        // W_b <= 512
 // staged j rows of the TMA stage 1 for an A RoI of width W_a (the zero rows follow them)
 __host__ __device__ constexpr int stage1_rows(int Wa) { return Wa <= 128 ? 128 : kTMaxJ; }
+// B rows v per stage-1 tile: 16 for A RoIs up to 128 wide (their 130-row stages leave room), else 8
+__host__ __device__ constexpr int stage1_vg(int kJ) { return kJ <= 128 ? 16 : kTVG; }
 constexpr int kTConsumers = 8;
 constexpr int kTThreads = 32 * (kTConsumers + 1);
 
@@ -271,16 +273,17 @@ __device__ __forceinline__ uint64_t ffma2(float, uint64_t g, uint64_t c, uint64_
 // The 8 taps of one packed x-table entry for one lane: 4 v slots x 2 corners, as FFMA2 pairs
 // (lane-wise identical to scalar fmaf in the same order).  entry = j_rel << 23 | round(t * 2^23),
 // j_rel = smem row of j0 relative to the chunk's staged span (256 = zero rows: skipped, t = 0).
-__device__ __forceinline__ void s1_taps(uint64_t (&part)[2], uint32_t e, const float* Gu, const int (&voff)[4]) {
+template <int NS, int kRow>
+__device__ __forceinline__ void s1_taps(uint64_t (&part)[NS / 2], uint32_t e, const float* Gu, const int (&voff)[NS]) {
     const float one_t = __int_as_float((e & 0x7FFFFFu) | 0x3F800000u);   // 1 + t
     const float t = one_t - 1.f;
     const float w0 = 2.f - one_t;
-    const float* gp = Gu + (e >> 23) * kTRow;
+    const float* gp = Gu + (e >> 23) * kRow;
     const uint64_t t2 = pack_f32x2(t, t), w2 = pack_f32x2(w0, w0);
 #pragma unroll
-    for (int p = 0; p < 2; ++p) {
+    for (int p = 0; p < NS / 2; ++p) {
         const uint64_t g0 = pack_f32x2(gp[voff[2 * p]], gp[voff[2 * p + 1]]);
-        const uint64_t g1 = pack_f32x2(gp[voff[2 * p] + kTRow], gp[voff[2 * p + 1] + kTRow]);
+        const uint64_t g1 = pack_f32x2(gp[voff[2 * p] + kRow], gp[voff[2 * p + 1] + kRow]);
         part[p] = ffma2(t, g1, ffma2(w0, g0, part[p], w2), t2);
     }
 }
@@ -289,8 +292,9 @@ __device__ __forceinline__ void s1_taps(uint64_t (&part)[2], uint32_t e, const f
 // give a 4-deep ring; rows kJ, kJ + 1 of every stage stay zero (skipped samples).
 template <int F, int kJ = kTMaxJ>
 struct S1Cfg {
-    static constexpr int kGFloats = (kJ + 2) * kTRow;
-    static constexpr int kStages = kJ <= 128 ? 4 : (F == 1 ? 3 : 2);
+    static constexpr int kVG = stage1_vg(kJ), kRow = kVG * kTUC;   // staged j row: kVG v x 8 u
+    static constexpr int kGFloats = (kJ + 2) * kRow;
+    static constexpr int kStages = F == 1 ? 3 : 2;   // both row capacities: ~66 KB Gamma stages
     // smem map (bytes): [Gamma stages (258 rows each)][x-table stages x F][span table]
     //                   [x-block masks][barriers]
     static constexpr int kOffX = kStages * kGFloats * 4;
@@ -321,9 +325,9 @@ __device__ __forceinline__ int shard_row(const S1Args& a, int l) {
 
 // v rows of the tile (m, v0..v0+7) that plane f needs: m inside the used band [lo_y(v), hi_y(v)]
 // of stage 2 (bands staged in smem once per CTA)
-__device__ __forceinline__ unsigned tile_mask(const int2* yband, int Hb, int m, int v0, int f) {
+__device__ __forceinline__ unsigned tile_mask(const int2* yband, int Hb, int m, int v0, int f, int vgs) {
     unsigned need = 0;
-    const int nv = min(kTVG, Hb - v0);
+    const int nv = min(vgs, Hb - v0);
     for (int v = 0; v < nv; ++v) {
         const int2 b = yband[f * 256 + v0 + v];
         if (m >= b.x && m <= b.y) need |= 1u << v;
@@ -390,21 +394,21 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                 const int ml = tile / a.n_vg, vg = tile - ml * a.n_vg;
                 unsigned any = 0;
 #pragma unroll
-                for (int f = 0; f < F; ++f) any |= tile_mask(yband, a.Hb, shard_row(a, ml), vg * kTVG, f);
+                for (int f = 0; f < F; ++f) any |= tile_mask(yband, a.Hb, shard_row(a, ml), vg * C::kVG, f, C::kVG);
                 if (!any) continue;
                 for (int c = 0; c < a.n_chunks; ++c) {
                     const int2 sp = span[c];
                     if (sp.y < sp.x) continue;
                     const int nb = (sp.y - sp.x + kTJBox) / kTJBox;
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], nb * kTJBox * kTRow * 4 + F * kTUC * a.Wa * 4);
+                    mbar_expect_tx(&full[stage], nb * kTJBox * C::kRow * 4 + F * kTUC * a.Wa * 4);
                     float* dst = sg + stage * C::kGFloats;
                     for (int b = 0; b < nb; ++b) {
                         if (a.gamma_5d)   // u-blocked Gamma: one 256-B segment per (j, chunk)
-                            tma_load_5d(dst + b * kTJBox * kTRow, &tm_g, &full[stage], 0, vg * kTVG, c,
+                            tma_load_5d(dst + b * kTJBox * C::kRow, &tm_g, &full[stage], 0, vg * C::kVG, c,
                                         sp.x + b * kTJBox, ml);
                         else
-                            tma_load_4d(dst + b * kTJBox * kTRow, &tm_g, &full[stage], c * kTUC, vg * kTVG,
+                            tma_load_4d(dst + b * kTJBox * C::kRow, &tm_g, &full[stage], c * kTUC, vg * C::kVG,
                                         sp.x + b * kTJBox, ml);
                     }
 #pragma unroll
@@ -420,25 +424,26 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
 
     const int vq = lane >> 4, xl = lane & 15, hi = xl >> 3;
     const int xbase = warp * 16 + xl;
-    int voff[4];                                           // float offset of slot s's v row
+    constexpr int NS = C::kVG / 2, NI = kJ <= 128 ? 1 : 2;   // v slots per lane, x blocks per lane
+    int voff[NS];                                          // float offset of slot s's v row
 #pragma unroll
-    for (int s = 0; s < 4; ++s) voff[s] = (vq + 2 * ((s + hi) & 3)) * kTUC;
+    for (int s = 0; s < NS; ++s) voff[s] = (vq + 2 * ((s + hi) & (NS - 1))) * kTUC;
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int ml = tile / a.n_vg, vg = tile - ml * a.n_vg;
-        const int m = shard_row(a, ml), v0 = vg * kTVG;
+        const int m = shard_row(a, ml), v0 = vg * C::kVG;
         unsigned mask[F], any = 0;
 #pragma unroll
-        for (int f = 0; f < F; ++f) { mask[f] = tile_mask(yband, a.Hb, m, v0, f); any |= mask[f]; }
+        for (int f = 0; f < F; ++f) { mask[f] = tile_mask(yband, a.Hb, m, v0, f, C::kVG); any |= mask[f]; }
         if (!any) continue;
-        double acc[F][2][4];
+        double acc[F][NI][NS];
 #pragma unroll
         for (int f = 0; f < F; ++f)
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
+            for (int i = 0; i < NI; ++i)
 #pragma unroll
-                for (int s = 0; s < 4; ++s) acc[f][i][s] = 0.0;
+                for (int s = 0; s < NS; ++s) acc[f][i][s] = 0.0;
         for (int c = 0; c < a.n_chunks; ++c) {
             const int2 sp = span[c];
             if (sp.y < sp.x) continue;
@@ -446,20 +451,20 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
             const float* G = sg + stage * C::kGFloats;
             // fp32 partial sums of this chunk as packed pairs (slots s = 2p, 2p + 1): the taps run
             // on FFMA2 (fma.rn.f32x2), lane-wise identical to two scalar fmaf in the same order
-            uint64_t part[F][2][2];
+            uint64_t part[F][NI][NS / 2];
 #pragma unroll
             for (int f = 0; f < F; ++f)
 #pragma unroll
-                for (int i = 0; i < 2; ++i)
+                for (int i = 0; i < NI; ++i)
 #pragma unroll
-                    for (int p = 0; p < 2; ++p) part[f][i][p] = 0ull;
+                    for (int p = 0; p < NS / 2; ++p) part[f][i][p] = 0ull;
             const uint32_t* sxs = sx + stage * F * C::kXEntries + xbase;
             if constexpr (kSkip) {
                 // i-outer order with a warp-uniform skip of a 16-wide x block that has no used
                 // sample in this chunk for any plane of the group
                 const uint32_t xb = xblk[c] >> warp;
 #pragma unroll
-                for (int i = 0; i < 2; ++i) {
+                for (int i = 0; i < NI; ++i) {
                     if (!((xb >> (8 * i)) & 1u)) continue;
                     if (!kFullX && xbase + 128 * i >= a.Wa) continue;
 #pragma unroll
@@ -467,7 +472,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                         const int uu = (k + xl) & (kTUC - 1);
 #pragma unroll
                         for (int f = 0; f < F; ++f)
-                            s1_taps(part[f][i], sxs[f * C::kXEntries + uu * a.Wa + 128 * i], G + uu, voff);
+                            s1_taps<NS, C::kRow>(part[f][i], sxs[f * C::kXEntries + uu * a.Wa + 128 * i], G + uu, voff);
                     }
                 }
             } else {
@@ -477,9 +482,10 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
 #pragma unroll
                     for (int f = 0; f < F; ++f)
 #pragma unroll
-                        for (int i = 0; i < 2; ++i)
+                        for (int i = 0; i < NI; ++i)
                             if (kFullX || xbase + 128 * i < a.Wa)
-                                s1_taps(part[f][i], sxs[f * C::kXEntries + uu * a.Wa + 128 * i], G + uu, voff);
+                                s1_taps<NS, C::kRow>(part[f][i], sxs[f * C::kXEntries + uu * a.Wa + 128 * i], G + uu,
+                                                     voff);
                 }
             }
             // Release the stage to the TMA producer.  The reads above are generic-proxy loads and
@@ -491,21 +497,21 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
 #pragma unroll
             for (int f = 0; f < F; ++f)
 #pragma unroll
-                for (int i = 0; i < 2; ++i)
+                for (int i = 0; i < NI; ++i)
 #pragma unroll
-                    for (int s = 0; s < 4; ++s) acc[f][i][s] += static_cast<double>(unpack_f32x2(part[f][i][s >> 1], s & 1));
+                    for (int s = 0; s < NS; ++s) acc[f][i][s] += static_cast<double>(unpack_f32x2(part[f][i][s >> 1], s & 1));
             if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
 #pragma unroll
         for (int f = 0; f < F; ++f)
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
+            for (int i = 0; i < NI; ++i) {
                 const int x = xbase + 128 * i;
                 if (!kFullX && x >= a.Wa) continue;
                 double* dst = a.T[f] + (static_cast<int64_t>(x) * a.Ha + m) * a.Hb + v0;
 #pragma unroll
-                for (int s = 0; s < 4; ++s) {
-                    const int v = vq + 2 * ((s + hi) & 3);
+                for (int s = 0; s < NS; ++s) {
+                    const int v = vq + 2 * ((s + hi) & (NS - 1));
                     if (mask[f] & (1u << v)) dst[v] = acc[f][i][s];
                 }
             }
@@ -860,6 +866,8 @@ cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int H
     return cudaGetLastError();
 }
 
+int stage1_vgroup(int Wa) { return stage1_vg(stage1_rows(Wa)); }
+
 bool stage1_tma_supported(int Wa, int Wb, int Hb) {
     // 16-byte TMA strides: W_a (x-table rows) and W_b (Gamma rows) multiples of 4 floats
     return Wa <= 256 && Wa >= 4 && (Wa % 4) == 0 && (Wb % 4) == 0 && Wb <= 8 * kTMaxChunks && Hb <= 256;
@@ -907,7 +915,7 @@ cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa
     a.Wa = Wa; a.Ha = Ha; a.Wb = Wb; a.Hb = Hb; a.m_base = m_base; a.m_count = m_count;
     a.m_block = m_block > 0 ? m_block : (m_count > 0 ? m_count : 1);
     a.m_stride = m_block > 0 ? m_stride : a.m_block;
-    a.n_vg = (Hb + kTVG - 1) / kTVG;
+    a.n_vg = (Hb + stage1_vg(stage1_rows(Wa)) - 1) / stage1_vg(stage1_rows(Wa));
     a.n_chunks = (Wb + kTUC - 1) / kTUC;
     a.xblk = xblk;
     a.gamma_5d = maps->gamma_5d;
