@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--roi", default="full", choices=["full", "128", "tiny"])
     p.add_argument("--gamma-order", default="ublocked", choices=["ublocked", "rowmajor"],
                    help="column order of the step's Gamma (include/cpi.h CPI_GAMMA_UBLOCKED)")
+    p.add_argument("--sharded", action="store_true",
+                   help="run the frame-sharded multi-GPU pipeline (NCCL) even at one rank (tests its code path)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-rows", type=int, default=0, help="(unused; the sample size follows the core count)")
@@ -276,7 +278,14 @@ def main():
             raise SystemExit("--gpus N > 1 must be launched with torch.distributed.run (one rank per GPU)")
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
-    if world > 1:
+    use_dist = world > 1 or args.sharded
+    if use_dist:
+        os.environ.setdefault("NCCL_DEBUG", "WARN")   # keep stdout to the one JSON line
+        if world == 1:   # one-rank NCCL group (no launcher): rendezvous on localhost
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29400 + os.getpid() % 500))
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
 
     from paper_2407_20692_b200 import Context
@@ -294,7 +303,7 @@ def main():
     frames_dev = frames_host.to(dev)
     stream = torch.cuda.current_stream(dev)
 
-    if world == 1:
+    if not use_dist:
         ctx = Context(roi_a, roi_b, n, device=local, variant=args.variant,
                       gamma_blocked=args.gamma_order == "ublocked")
         gamma = ctx.new_gamma()
@@ -310,7 +319,7 @@ def main():
     def step(src):
         """one pass of a1..a6; src = device frames (resident) or pinned host frames (e2e);
         returns the plane stack"""
-        if world == 1:
+        if not use_dist:
             ctx.reset()          # a new acquisition: zero S_a, S_b, N (memsets)
             ctx.load_frames(src)
             ctx.correlate(gamma)
@@ -320,7 +329,7 @@ def main():
         return res.planes
 
     def barrier():
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
@@ -347,7 +356,7 @@ def main():
                                                  ("stage2", KC_STAGE2), ("coords", KC_COORDS),
                                                  ("finalize", KC_FINALIZE))}
     ctx.set_timing(False)
-    if world > 1:
+    if use_dist:
         tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
@@ -368,7 +377,7 @@ def main():
         e1.record(stream)
         barrier()
         te = e0.elapsed_time(e1)
-        if world > 1:
+        if use_dist:
             tt = torch.tensor([te], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
@@ -377,7 +386,7 @@ def main():
                "ms_per_step": te / args.steps}
 
     if rank != 0:
-        if world > 1:
+        if use_dist:
             dist.barrier()
             dist.destroy_process_group()
         return
@@ -451,7 +460,7 @@ def main():
                                 f"-> Gamma {p_a}x{p_b} -> {args.planes}-plane refocus stack"),
                    "frames_per_step_per_rank": n, "planes_per_step": args.planes,
                    "alphas": "linspace(0.5, 2.0, P)", "variant": args.variant, "gamma_order": args.gamma_order,
-                   "parallelism": f"frame-sharded x{world}" if world > 1 else "single GPU",
+                   "parallelism": f"frame-sharded x{world}" if use_dist else "single GPU",
                    "l2": "inputs larger than L2 (Gamma 17 GB, operands 1.3 GB) - no flush needed"},
         "gpu_launches": launches,
         "roofline": dominant,
@@ -469,7 +478,7 @@ def main():
                          "i7-9700K (PAPER.md:38, 52, 279-292); no absolute timings in the text",
     }
     print(json.dumps(out))
-    if world > 1:
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
 
