@@ -234,7 +234,7 @@ def cpu_baseline(frames_np, roi_a, roi_b, alphas, n_rows, n_pix, step_planes, wa
 
 
 # ------------------------------------------------------------------ reference arm ---------
-def run_reference(args):
+def run_reference(args, json_out=None):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -258,14 +258,24 @@ def run_reference(args):
                       "planes_per_step": args.planes},
            "cpu_baseline": last,
            "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out))
+    print(json.dumps(out), file=json_out or sys.stdout, flush=True)
 
 
 # ------------------------------------------------------------------ main arm --------------
+def _claim_stdout():
+    """Route fd 1 to stderr for the rest of the run (NCCL, CUDA and library messages) and return
+    a stream on the original stdout for the one JSON line of the contract."""
+    out = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
+    return out
+
+
 def main():
     args = parse()
+    json_out = _claim_stdout()
     if args.impl == "reference":
-        run_reference(args)
+        run_reference(args, json_out)
         return
     import torch
     import torch.distributed as dist
@@ -477,7 +487,7 @@ def main():
         "paper_context": "paper: 20x (correlation) / 500x (refocus) OpenCL-GPU vs CPU on RTX 2080 Ti vs "
                          "i7-9700K (PAPER.md:38, 52, 279-292); no absolute timings in the text",
     }
-    print(json.dumps(out))
+    print(json.dumps(out), file=json_out, flush=True)
     if use_dist:
         dist.barrier()
         dist.destroy_process_group()

@@ -16,15 +16,11 @@ torch = pytest.importorskip("torch")
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
-                    reason="needs >= 2 GPUs (one rank per GPU)")
-@pytest.mark.parametrize("variant", ["fp4", "tc"])
-def test_frame_sharded_nccl_matches_single_gpu(tmp_path, variant):
+def _run(tmp_path, variant, world):
     sys.path.insert(0, HERE)
     import _mgpu_worker as w
     import synth
     from paper_2407_20692_b200 import Context
-    world = min(torch.cuda.device_count(), 8)
     out = tmp_path / "mgpu.npz"
     env = dict(os.environ, CPI_MGPU_VARIANT=variant)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
@@ -42,3 +38,17 @@ def test_frame_sharded_nccl_matches_single_gpu(tmp_path, variant):
     assert int(got["n_tot"]) == w.N and int(got["panels"]) >= 1
     np.testing.assert_array_equal(got["gamma"], g.cpu().numpy())
     np.testing.assert_allclose(got["planes"], planes.cpu().numpy(), rtol=1e-5, atol=1e-9)
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs (one rank per GPU)")
+@pytest.mark.parametrize("variant", ["fp4", "tc"])
+def test_frame_sharded_nccl_matches_single_gpu(tmp_path, variant):
+    _run(tmp_path, variant, min(torch.cuda.device_count(), 8))
+
+
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a GPU")
+def test_nccl_single_rank_pipeline(tmp_path):
+    """The NCCL code path of the pipeline (async reduce-scatter on the library's count views,
+    all-reduces) as a one-rank group under torch.distributed.run: runs on one GPU."""
+    _run(tmp_path, "fp4", 1)
