@@ -454,6 +454,26 @@ def main():
                "traffic_note": ("ncu dram read + write bytes of one 4-plane launch (profiles/r01_traffic.json); "
                                 "achieved is per step (16 launches)")}
     dominant = roof_s1 if (s1_ms > gemm_ms) else roof_gemm
+    # north_star's correlation metric is the kind::i8 kernel's fraction of the int8 peak: when
+    # the step runs the FP4 GEMM, time the kind::i8 GEMM on the same frames too (after the timed
+    # region, not part of value)
+    int8_side = None
+    if args.variant == "fp4" and not use_dist:
+        c8 = Context(roi_a, roi_b, n, device=local, variant="tc", gamma_blocked=args.gamma_order == "ublocked")
+        for it in range(5):
+            if it == 2:
+                c8.set_timing(True)
+            c8.reset()
+            c8.load_frames(frames_dev)
+            c8.correlate(gamma)
+        g8_ms, g8_n = c8.kernel_time_ms(KC_GEMM)
+        c8.close()
+        i8_tops = ops / (g8_ms / g8_n / 1e3) / 1e12
+        i8_peak = 2.0 * peaks["bf16_tflops"]
+        int8_side = {"kernel": "gemm_i8_tc2 (KB2, cta_group::2, kind::i8, int32 accumulation)",
+                     "ms_per_launch": g8_ms / g8_n, "achieved": i8_tops, "peak": i8_peak, "unit": "TOPS",
+                     "frac": i8_tops / i8_peak, "frac_of_clock_peak": i8_tops / (148 * 8192 * 2 * f_clk / 1e12),
+                     "note": "same frames, epilogue and Gamma, timed after the step loop; not part of value"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(frames_np, roi_a, roi_b, alphas, args.cpu_rows, args.cpu_pixels, args.planes)
@@ -475,6 +495,7 @@ def main():
         "gpu_launches": launches,
         "roofline": dominant,
         "rooflines": [roof_gemm, roof_s1],
+        "int8_gemm": int8_side,
         "stages_ms_per_step": {"expand": kt["expand"][0] / args.steps, "gemm": gemm_ms / args.steps,
                                "refocus_coords": kt["coords"][0] / args.steps,
                                "refocus_stage1": s1_ms / args.steps, "refocus_stage2": kt["stage2"][0] / args.steps,
