@@ -86,3 +86,12 @@ def test_null_handles(lib):
     assert lib.cpi_launch_count(None) == 0
     assert lib.cpi_load_frames(None, None, 0, 0, None) == -1
     assert lib.cpi_correlate(None, None, None) == -1
+    assert lib.cpi_correlate_rows(None, 0, 256, None, None) == -1
+    assert lib.cpi_row_align(None) == 0
+    assert lib.cpi_counts_dev(None, None, None, None) == -1
+    assert lib.cpi_finalize(None, None, None, None) == -1
+    assert lib.cpi_finalize_counts(None, None, 0, 0, None, None, 1, None, None) == -1
+    assert lib.cpi_get_counts(None, None, None, None, None, None) == -1
+    assert lib.cpi_reset(None, None) == -1
+    assert lib.cpi_refocus(None, None, None, None) == -1
+    assert lib.cpi_set_timing(None, 1) == -1
