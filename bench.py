@@ -508,6 +508,14 @@ def main():
         "paper_context": "paper: 20x (correlation) / 500x (refocus) OpenCL-GPU vs CPU on RTX 2080 Ti vs "
                          "i7-9700K (PAPER.md:38, 52, 279-292); no absolute timings in the text",
     }
+    if cpu and corr_ms and ref_ms:
+        parts = cpu["extrapolated_parts_s"]
+        out["speedup_vs_oracle"] = {
+            "correlation": (parts["marginals"] + parts["pair_sums"]) / (corr_ms / 1e3),
+            "refocus": parts["refocus"] / (ref_ms / 1e3),
+            "note": (f"oracle stage times on {cpu['cores']} host cores (extrapolated, see cpu_baseline) / GPU "
+                     "stage times of this run; the paper's 20x / 500x compare OpenCL on an RTX 2080 Ti with "
+                     "its own CPU code on an i7-9700K")}
     print(json.dumps(out), file=json_out, flush=True)
     if use_dist:
         dist.barrier()
