@@ -99,6 +99,83 @@ expand_kernel(const uint8_t* __restrict__ frames, int64_t n, int row_bytes, int 
                                     : static_cast<int64_t>(m) * roi.w + j), cnt[j]);
 }
 
+// u8 / E2M1 operands, byte-column parallel: the sub-block's bytes are staged transposed,
+// [byte column][frame], so one 32-bit shared load gives a lane 4 consecutive frames of 8 pixels.
+// For bit s of the byte, x = (word >> s) & 0x01010101 holds the 4 frames' bits at byte positions
+// 0, 8, 16, 24: that is the u8 operand word as is; for E2M1 the bits are folded onto nibbles
+// 0..3 (frames 0, 2, 1, 3 of the group -- A and B use the same order, so the K sum is
+// unchanged) and shifted to 0x2 = 1.0.  Pixel counts: popc + one warp REDUX per pixel.
+constexpr int kTStride = kSub + 4;    // bytes per staged byte column (keeps 32-bit alignment)
+
+template <int kMode>
+__global__ void __launch_bounds__(kThreads)
+expand_cols_kernel(const uint8_t* __restrict__ frames, int64_t n, int row_bytes, int frame_h, int msb,
+                   RoiDev roi, void* __restrict__ op, int64_t ld, int64_t k_pad, int32_t* __restrict__ s,
+                   int ublocked, int words) {
+    __shared__ __align__(16) uint8_t sbt[(kMaxWidth / 8 + 1) * kTStride];
+    __shared__ int cnt[kMaxWidth];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int m = blockIdx.y;
+    const int b0 = roi.x0 >> 3;
+    const int nb = ((roi.x0 + roi.w - 1) >> 3) - b0 + 1;
+    for (int j = tid; j < roi.w; j += kThreads) cnt[j] = 0;
+    const int64_t f_begin = static_cast<int64_t>(blockIdx.x) * kFramesCta;
+    const int64_t row_off = static_cast<int64_t>(roi.y0 + m) * row_bytes + b0;
+    for (int sub = 0; sub < kFramesCta / kSub; ++sub) {
+        const int64_t f0 = f_begin + sub * kSub;
+        if (f0 >= k_pad) break;
+        __syncthreads();
+        if (words) {   // 4-byte loads of the word range covering the RoI's bytes
+            const int wb0 = b0 & ~3, nw = (b0 + nb - wb0 + 3) >> 2;
+            const int64_t row_w = static_cast<int64_t>(roi.y0 + m) * row_bytes + wb0;
+            for (int idx = tid; idx < kSub * nw; idx += kThreads) {
+                const int fl = idx / nw, w = idx - fl * nw;
+                const int64_t f = f0 + fl;
+                const uint32_t v = (f < n) ? __ldg(reinterpret_cast<const uint32_t*>(frames + f * frame_h * row_bytes + row_w) + w)
+                                           : 0u;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int b = 4 * w + k - (b0 - wb0);
+                    if (b >= 0 && b < nb) sbt[b * kTStride + fl] = static_cast<uint8_t>(v >> (8 * k));
+                }
+            }
+        } else {
+            for (int idx = tid; idx < kSub * nb; idx += kThreads) {
+                const int fl = idx / nb, b = idx - fl * nb;
+                const int64_t f = f0 + fl;
+                sbt[b * kTStride + fl] = (f < n) ? __ldg(frames + f * frame_h * row_bytes + row_off + b) : uint8_t(0);
+            }
+        }
+        __syncthreads();
+        for (int b = warp; b < nb; b += kThreads / 32) {
+            const uint32_t w4 = *reinterpret_cast<const uint32_t*>(sbt + b * kTStride + 4 * lane);   // frames 4 lane + 0..3
+#pragma unroll
+            for (int bit = 0; bit < 8; ++bit) {
+                const int col = (b0 + b) * 8 + (msb ? 7 - bit : bit);
+                const int j = col - roi.x0;
+                if (j < 0 || j >= roi.w) continue;          // warp-uniform
+                const uint32_t x = (w4 >> bit) & 0x01010101u;
+                const int64_t prow = ublocked ? static_cast<int64_t>(j >> 3) * (8 * roi.h) + 8 * m + (j & 7)
+                                              : static_cast<int64_t>(m) * roi.w + j;
+                if constexpr (kMode == kExpandE2M1) {
+                    const uint32_t nib = ((x | (x >> 12)) & 0x1111u) << 1;   // 4 nibbles, 0x2 = 1.0
+                    *reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(op) + prow * ld + ((f0 + 4 * lane) >> 1)) =
+                        static_cast<uint16_t>(nib);
+                } else {
+                    *reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(op) + prow * ld + f0 + 4 * lane) = x;
+                }
+                const int c = __reduce_add_sync(0xffffffffu, __popc(x));
+                if (lane == 0) cnt[j] += c;                 // pixel j belongs to this warp only
+            }
+        }
+    }
+    __syncthreads();
+    for (int j = tid; j < roi.w; j += kThreads)
+        if (cnt[j])
+            atomicAdd(s + (ublocked ? static_cast<int64_t>(j >> 3) * (8 * roi.h) + 8 * m + (j & 7)
+                                    : static_cast<int64_t>(m) * roi.w + j), cnt[j]);
+}
+
 }  // namespace
 
 void launch_expand(const uint8_t* frames, int64_t n, int row_bytes, int frame_h, int msb,
@@ -109,12 +186,16 @@ void launch_expand(const uint8_t* frames, int64_t n, int row_bytes, int frame_h,
     if (mode == kExpandBits)
         expand_kernel<kExpandBits><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
                                                               ld, k_pad, s, ublocked ? 1 : 0);
-    else if (mode == kExpandE2M1)
-        expand_kernel<kExpandE2M1><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
-                                                              ld, k_pad, s, ublocked ? 1 : 0);
-    else
-        expand_kernel<kExpandU8><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
-                                                            ld, k_pad, s, ublocked ? 1 : 0);
+    else {
+        // word loads need 4-byte aligned frame rows
+        const int words = (row_bytes % 4 == 0 && (reinterpret_cast<uintptr_t>(frames) & 3) == 0) ? 1 : 0;
+        if (mode == kExpandE2M1)
+            expand_cols_kernel<kExpandE2M1><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
+                                                                       ld, k_pad, s, ublocked ? 1 : 0, words);
+        else
+            expand_cols_kernel<kExpandU8><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
+                                                                     ld, k_pad, s, ublocked ? 1 : 0, words);
+    }
 }
 
 }  // namespace cpi
