@@ -54,6 +54,9 @@ def parse():
     p.add_argument("--roi", default="full", choices=["full", "128", "tiny"])
     p.add_argument("--gamma-order", default="ublocked", choices=["ublocked", "rowmajor"],
                    help="column order of the step's Gamma (include/cpi.h CPI_GAMMA_UBLOCKED)")
+    p.add_argument("--parallel-mode", default="rows", choices=["rows", "tiles"],
+                   help="multi-GPU: rows = frame sharding + panelised reduce-scatter (north_star); tiles = "
+                        "all-gather of frames + each rank's own Gamma rows (SURVEY §8(e) control)")
     p.add_argument("--sharded", action="store_true",
                    help="run the frame-sharded multi-GPU pipeline (NCCL) even at one rank (tests its code path)")
     p.add_argument("--no-e2e", action="store_true")
@@ -321,8 +324,9 @@ def main():
     else:
         # frame-sharded pipeline (parallel.py): GEMM row panels reduce-scattered as they finish,
         # block-cyclic Gamma row ownership, shard refocus, plane all-reduce
-        backend = parallel.CudaBackend(roi_a, roi_b, n, device=local, variant=args.variant,
-                                       gamma_blocked=args.gamma_order == "ublocked")
+        tiles = args.parallel_mode == "tiles"
+        backend = parallel.CudaBackend(roi_a, roi_b, n * world if tiles else n, device=local, variant=args.variant,
+                                       gamma_blocked=args.gamma_order == "ublocked", keep_counts=not tiles)
         ctx = backend.ctx
     planes_host = torch.empty((args.planes, Ha, Wa), dtype=torch.float32).pin_memory()
 
@@ -335,7 +339,8 @@ def main():
             ctx.correlate(gamma)
             ctx.refocus(alphas, gamma, planes)
             return planes
-        res = parallel.correlate_and_refocus(backend, src, roi_a, roi_b, alphas)
+        run = parallel.correlate_and_refocus_tiles if tiles else parallel.correlate_and_refocus
+        res = run(backend, src, roi_a, roi_b, alphas)
         return res.planes
 
     def barrier():
@@ -490,7 +495,9 @@ def main():
                                 f"-> Gamma {p_a}x{p_b} -> {args.planes}-plane refocus stack"),
                    "frames_per_step_per_rank": n, "planes_per_step": args.planes,
                    "alphas": "linspace(0.5, 2.0, P)", "variant": args.variant, "gamma_order": args.gamma_order,
-                   "parallelism": f"frame-sharded x{world}" if use_dist else "single GPU",
+                   "parallelism": (f"frame-sharded x{world}" + (" (output-tile sharding)" if args.parallel_mode == "tiles"
+                                                                else " (panelised reduce-scatter)"))
+                   if use_dist else "single GPU",
                    "l2": "inputs larger than L2 (Gamma 17 GB, operands 1.3 GB) - no flush needed"},
         "gpu_launches": launches,
         "roofline": dominant,

@@ -197,6 +197,12 @@ cpi_status cpi_correlate(cpi_ctx *ctx, float *gamma_dev, void *stream);
  * INVALID_ARG (range / alignment), CUDA. */
 cpi_status cpi_correlate_rows(cpi_ctx *ctx, int64_t row0, int64_t rows, float *gamma_dev, void *stream);
 
+/* cpi_correlate_rows writing the panel's Gamma rows compactly: gamma_rows_dev (non-NULL) is
+ * fp32 [rows][P_b] holding A pixels row0 .. row0 + rows - 1 (output-tile sharding: a rank
+ * computes only the Gamma rows it owns, over all frames, without a full-size buffer).
+ * Errors as cpi_correlate_rows. */
+cpi_status cpi_correlate_rows_to(cpi_ctx *ctx, int64_t row0, int64_t rows, float *gamma_rows_dev, void *stream);
+
 /* Row alignment (A pixels) of cpi_correlate_rows panels for this context's GEMM variant. */
 int64_t cpi_row_align(const cpi_ctx *ctx);
 

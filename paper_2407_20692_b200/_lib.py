@@ -25,7 +25,7 @@ KC_GEMM, KC_EXPAND, KC_STAGE1, KC_STAGE2, KC_FINALIZE, KC_COORDS = range(6)
 EXPORTS = ["cpi_create", "cpi_destroy", "cpi_last_error", "cpi_status_string", "cpi_load_frames",
            "cpi_correlate", "cpi_finalize", "cpi_finalize_counts", "cpi_get_counts", "cpi_reset",
            "cpi_refocus", "cpi_launch_count", "cpi_set_timing", "cpi_kernel_time_ms",
-           "cpi_abi_version", "cpi_correlate_rows", "cpi_row_align", "cpi_counts_dev"]
+           "cpi_abi_version", "cpi_correlate_rows", "cpi_row_align", "cpi_counts_dev", "cpi_correlate_rows_to"]
 
 
 class CpiError(RuntimeError):
@@ -96,6 +96,7 @@ def load():
         "cpi_kernel_time_ms": ([P, i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)], i32),
         "cpi_abi_version": ([], i32),
         "cpi_correlate_rows": ([P, i64, i64, P, P], i32),
+        "cpi_correlate_rows_to": ([P, i64, i64, P, P], i32),
         "cpi_row_align": ([P], i64),
         "cpi_counts_dev": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)], i32),
     }

@@ -130,6 +130,17 @@ class Context:
                                                  self._stream(stream)))
         return gamma
 
+    def correlate_rows_to(self, row0: int, rows: int, gamma_rows, stream=None):
+        """cpi_correlate_rows_to: as correlate_rows, Gamma rows written compactly to
+        gamma_rows (CUDA float32 [rows][P_b])."""
+        torch = _torch()
+        if not (gamma_rows.is_cuda and gamma_rows.dtype == torch.float32 and gamma_rows.is_contiguous()
+                and gamma_rows.numel() >= rows * self.p_b):
+            raise ValueError("gamma_rows must be a contiguous CUDA float32 tensor with rows * P_b elements")
+        self._check(self._lib.cpi_correlate_rows_to(self._h, int(row0), int(rows), self._ptr(gamma_rows),
+                                                    self._stream(stream)))
+        return gamma_rows
+
     def row_align(self) -> int:
         """cpi_row_align: A-pixel alignment of correlate_rows panels."""
         return int(self._lib.cpi_row_align(self._h))

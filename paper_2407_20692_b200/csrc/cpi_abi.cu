@@ -545,6 +545,17 @@ cpi_status cpi_correlate(cpi_ctx* c, float* gamma, void* stream) {
     return CPI_OK;
 }
 
+cpi_status cpi_correlate_rows(cpi_ctx* c, int64_t row0, int64_t rows, float* gamma, void* stream);
+
+cpi_status cpi_correlate_rows_to(cpi_ctx* c, int64_t row0, int64_t rows, float* gamma_rows, void* stream) {
+    if (!c) return CPI_ERR_INVALID_ARG;
+    if (!gamma_rows) return fail(c, CPI_ERR_INVALID_ARG, "gamma_rows_dev is NULL");
+    // the kernels address Gamma as base + row * P_b: shift the base so row0 lands on gamma_rows
+    float* base = reinterpret_cast<float*>(reinterpret_cast<uintptr_t>(gamma_rows) -
+                                           static_cast<uintptr_t>(row0) * static_cast<uintptr_t>(c->p_b) * sizeof(float));
+    return cpi_correlate_rows(c, row0, rows, base, stream);
+}
+
 cpi_status cpi_correlate_rows(cpi_ctx* c, int64_t row0, int64_t rows, float* gamma, void* stream) {
     if (!c) return CPI_ERR_INVALID_ARG;
     if (!c->loaded || c->consumed)

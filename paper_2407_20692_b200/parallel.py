@@ -87,18 +87,24 @@ class ShardPlan:
 
 
 def shard_plan(width_a: int, height_a: int, rank: int, world: int, row_align: int = 1,
-               min_panel_rows: int = 8192) -> ShardPlan:
+               min_panel_rows: int = 8192, block_aligned: bool = False) -> ShardPlan:
     """Smallest block (A rows per rank per panel) whose panel is a multiple of the GEMM's row
     alignment and holds at least ``min_panel_rows`` A pixels (launch / collective overhead vs
-    pipelining); one panel of contiguous blocks if none qualifies (always valid)."""
+    pipelining); one panel of contiguous blocks if none qualifies (always valid).
+    block_aligned: each rank's block itself must be row-aligned (output-tile sharding runs
+    the GEMM on the rank's own blocks)."""
     if height_a % world:
         raise ValueError(f"H_a = {height_a} must be divisible by the world size {world}")
     m_per = height_a // world
     if world > 1:
         for block in range(1, m_per + 1):
             rows = world * block * width_a
-            if m_per % block == 0 and rows % row_align == 0 and rows >= min(min_panel_rows, width_a * height_a):
+            unit = block * width_a if block_aligned else rows
+            if m_per % block == 0 and unit % row_align == 0 and rows >= min(min_panel_rows, width_a * height_a):
                 return ShardPlan(width_a, height_a, world, rank, block, m_per // block)
+        if block_aligned and (m_per * width_a) % row_align and rank < world - 1:
+            raise ValueError(f"no row-aligned block-cyclic plan for W_a = {width_a}, H_a = {height_a}, "
+                             f"world {world}, alignment {row_align}")
     return ShardPlan(width_a, height_a, world, rank, m_per, 1)
 
 
@@ -165,22 +171,70 @@ def correlate_and_refocus(backend, frames_local, roi_a, roi_b, alphas=None, grou
     return ShardResult(n_tot, plan, gamma_rows, planes)
 
 
+def _gather_frames(frames_local, group, device) -> torch.Tensor:
+    """All ranks' frame slices concatenated in rank order (= the global frame order)."""
+    world = dist.get_world_size(group)
+    t = torch.as_tensor(frames_local).to(device)
+    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=device)
+    ns = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(ns, n, group=group)
+    ns = [int(x.item()) for x in ns]
+    n_max = max(ns)
+    padded = torch.zeros((n_max,) + tuple(t.shape[1:]), dtype=t.dtype, device=device)
+    padded[:t.shape[0]] = t
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((world * n_max,) + tuple(t.shape[1:]), dtype=t.dtype, device=device)
+        dist.all_gather_into_tensor(out, padded, group=group)
+        parts = [out[r * n_max:r * n_max + ns[r]] for r in range(world)]
+    else:
+        lst = [torch.empty_like(padded) for _ in range(world)]
+        dist.all_gather(lst, padded, group=group)
+        parts = [lst[r][:ns[r]] for r in range(world)]
+    return torch.cat(parts).contiguous()
+
+
+def correlate_and_refocus_tiles(backend, frames_local, roi_a, roi_b, alphas=None, group=None,
+                                min_panel_rows: int = 8192) -> ShardResult:
+    """Output-tile sharding (SURVEY §8(e) control measurement): the packed frames are
+    all-gathered (each rank's slice is 16 KB per frame, ~1.3 GB per rank at 10^5 frames), then
+    every rank runs the GEMM with the fused exact normalisation on its own block-cyclic Gamma
+    rows over all frames (``backend.rows_to``), refocuses them and the planes are all-reduced.
+    No reduce-scatter of the 4 P_a P_b-byte partial sums.  ``backend`` as for
+    correlate_and_refocus plus rows_to(row0, rows, out) -> Gamma rows [row0, +rows) into out."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    Wa, Ha = roi_a[2], roi_a[3]
+    p_b = roi_b[2] * roi_b[3]
+    plan = shard_plan(Wa, Ha, rank, world, backend.row_align, min_panel_rows, block_aligned=True)
+    frames_all = _gather_frames(frames_local, group, backend.device)
+    backend.begin(frames_all)
+    chunk = plan.block * Wa
+    gamma_rows = torch.empty((plan.panels * chunk, p_b), dtype=torch.float32, device=backend.device)
+    for k in range(plan.panels):
+        backend.rows_to(k * plan.panel_rows + rank * chunk, chunk, gamma_rows[k * chunk:(k + 1) * chunk])
+    planes = None
+    if alphas is not None and len(alphas):
+        planes = backend.refocus(alphas, gamma_rows, plan.m_base * Wa, plan.m_count * Wa, plan.block, plan.stride)
+        dist.all_reduce(planes, op=dist.ReduceOp.SUM, group=group)
+    return ShardResult(int(frames_all.shape[0]), plan, gamma_rows, planes)
+
+
 class CudaBackend:
     """The pipeline steps on one B200 through the C ABI (libcpi.so): the GEMM runs in row
     panels (cpi_correlate_rows) whose pair sums are handed to the collectives in place
     (cpi_counts_dev views, no copies)."""
 
     def __init__(self, roi_a, roi_b, max_frames: int, device: int = 0, variant: str = "tc",
-                 gamma_blocked: bool = False):
+                 gamma_blocked: bool = False, keep_counts: bool = True):
         """gamma_blocked: B pixels in the u-blocked order (faster refocusing); S_b and the
         columns of ShardResult.gamma_rows then follow ctx.b_index()."""
         from .cpi import Context
-        self.ctx = Context(roi_a, roi_b, max_frames, device=device, variant=variant, keep_counts=True,
+        self.ctx = Context(roi_a, roi_b, max_frames, device=device, variant=variant, keep_counts=keep_counts,
                            gamma_blocked=gamma_blocked)
         self.device = torch.device(f"cuda:{device}")
         self.roi_a = roi_a
         self.row_align = self.ctx.row_align()
-        self._s_ab, self._s_a, self._s_b = self.ctx.counts_views()
+        self._s_ab, self._s_a, self._s_b = self.ctx.counts_views()   # s_ab None without kept counts
         self._n = 0
 
     def begin(self, frames):
@@ -194,6 +248,10 @@ class CudaBackend:
 
     def marginals(self):
         return self._s_a, self._s_b, self._n
+
+    def rows_to(self, row0, rows, out):
+        self.ctx.correlate_rows_to(row0, rows, out)
+        return out
 
     def finalize_rows(self, s_ab_rows, s_a_rows, s_b, n_tot):
         g = torch.empty(s_ab_rows.shape, dtype=torch.float32, device=self.device)

@@ -25,10 +25,12 @@ def main(out_path: str) -> None:
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     frames = synth.bernoulli_frames(N, 0.1, seed=99)
     lo, hi = parallel.frame_slice(N, rank, world)
-    be = parallel.CudaBackend(ROI_A, ROI_B, hi - lo, device=local, variant=os.environ.get("CPI_MGPU_VARIANT", "fp4"),
-                              gamma_blocked=True)
-    res = parallel.correlate_and_refocus(be, np.ascontiguousarray(frames[lo:hi]), ROI_A, ROI_B, ALPHAS,
-                                         min_panel_rows=256)
+    tiles = os.environ.get("CPI_MGPU_MODE", "rows") == "tiles"
+    be = parallel.CudaBackend(ROI_A, ROI_B, N if tiles else hi - lo, device=local,
+                              variant=os.environ.get("CPI_MGPU_VARIANT", "fp4"), gamma_blocked=True,
+                              keep_counts=not tiles)
+    run = parallel.correlate_and_refocus_tiles if tiles else parallel.correlate_and_refocus
+    res = run(be, np.ascontiguousarray(frames[lo:hi]), ROI_A, ROI_B, ALPHAS, min_panel_rows=256)
     rows = res.plan.pixel_rows().to(res.gamma_rows.device)
     gathered_g = [torch.empty_like(res.gamma_rows) for _ in range(world)]
     gathered_r = [torch.empty_like(rows) for _ in range(world)]

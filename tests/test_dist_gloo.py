@@ -37,6 +37,10 @@ class OracleBackend:
         return (torch.from_numpy(self.r["s_a"].astype(np.int32)), torch.from_numpy(self.r["s_b"].astype(np.int32)),
                 int(self.r["n"]))
 
+    def rows_to(self, row0, rows, out):
+        out.copy_(torch.from_numpy(self.r["gamma"][row0:row0 + rows].astype(np.float32)))
+        return out
+
     def finalize_rows(self, s_ab_rows, s_a_rows, s_b, n_tot):
         g = oracle.gamma(s_ab_rows.numpy(), s_a_rows.numpy(), s_b.numpy(), n_tot)
         return torch.from_numpy(g.astype(np.float32))
@@ -127,3 +131,46 @@ def test_slicing_helpers():
     p = parallel.shard_plan(256, 256, 3, 8, 256)
     assert (p.block, p.panels, p.stride, p.m_base) == (4, 8, 32, 12)
     assert p.a_rows()[:6].tolist() == [12, 13, 14, 15, 44, 45]
+
+
+def _worker_tiles(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        frames = synth.bernoulli_frames(N, 0.3, seed=31)
+        lo, hi = parallel.frame_slice(N, rank, world)
+        res = parallel.correlate_and_refocus_tiles(OracleBackend(), frames[lo:hi], ROI_A, ROI_B, ALPHAS,
+                                                   min_panel_rows=1)
+        q.put((rank, res.n_tot, res.plan, res.gamma_rows.numpy(), res.planes.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_output_tile_sharding_matches_single_process(world):
+    """Output-tile sharding (SURVEY §8(e) control): frames all-gathered, each rank computes its
+    own block-cyclic Gamma rows over all frames; rows equal the single-process oracle, planes
+    merge by all-reduce."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_tiles, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    frames = synth.bernoulli_frames(N, 0.3, seed=31)
+    full = oracle.correlate(frames, ROI_A, ROI_B)
+    G = full["gamma"].astype(np.float32)
+    want_planes = oracle.refocus(G, DIMS, ALPHAS)
+    covered = np.zeros(G.shape[0], dtype=int)
+    for rank, n_tot, plan, g_rows, planes in out:
+        assert n_tot == N
+        rows = plan.pixel_rows().numpy()
+        np.testing.assert_array_equal(g_rows, G[rows])
+        covered[rows] += 1
+        np.testing.assert_allclose(planes, want_planes, rtol=1e-5, atol=1e-7)
+    assert np.all(covered == 1)

@@ -27,7 +27,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, mode="rows"):
     import torch.distributed as dist
     import synth
     from paper_2407_20692_b200 import parallel
@@ -37,7 +37,8 @@ def _worker(rank, world, port, q):
     try:
         frames = synth.bernoulli_frames(N, 0.2, seed=77)
         lo, hi = parallel.frame_slice(N, rank, world)
-        be = parallel.CudaBackend(ROI_A, ROI_B, hi - lo, device=0)
+        be = parallel.CudaBackend(ROI_A, ROI_B, N if mode == "tiles" else hi - lo, device=0,
+                                  keep_counts=mode != "tiles")
 
         class GlooCuda:
             """gloo collectives need host tensors: stage through the host (plumbing only)."""
@@ -54,21 +55,27 @@ def _worker(rank, world, port, q):
                 s_a, s_b, n = be.marginals()
                 return s_a.cpu(), s_b.cpu(), n
 
+            def rows_to(self, row0, rows, out):
+                tmp = torch.empty(tuple(out.shape), dtype=torch.float32, device="cuda")
+                out.copy_(be.rows_to(row0, rows, tmp).cpu())
+                return out
+
             def finalize_rows(self, s_ab_rows, s_a_rows, s_b, n_tot):
                 return be.finalize_rows(s_ab_rows.cuda(), s_a_rows.cuda(), s_b.cuda(), n_tot).cpu()
 
             def refocus(self, alphas, gamma_rows, row0, rows, row_block, row_stride):
                 return be.refocus(alphas, gamma_rows.cuda(), row0, rows, row_block, row_stride).cpu()
 
-        res = parallel.correlate_and_refocus(GlooCuda(), np.ascontiguousarray(frames[lo:hi]), ROI_A, ROI_B, ALPHAS,
-                                             min_panel_rows=1)
+        run = parallel.correlate_and_refocus_tiles if mode == "tiles" else parallel.correlate_and_refocus
+        res = run(GlooCuda(), np.ascontiguousarray(frames[lo:hi]), ROI_A, ROI_B, ALPHAS, min_panel_rows=1)
         q.put((rank, res.n_tot, res.plan.pixel_rows().numpy(), res.plan.panels, res.gamma_rows.numpy(),
                res.planes.numpy()))
     finally:
         dist.destroy_process_group()
 
 
-def test_two_ranks_on_one_gpu_match_single_context():
+@pytest.mark.parametrize("mode", ["rows", "tiles"])
+def test_two_ranks_on_one_gpu_match_single_context(mode):
     import torch.multiprocessing as mp
     import synth
     from paper_2407_20692_b200 import Context
@@ -76,7 +83,7 @@ def test_two_ranks_on_one_gpu_match_single_context():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, mode)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=600) for _ in range(world)]

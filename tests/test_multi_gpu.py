@@ -16,13 +16,13 @@ torch = pytest.importorskip("torch")
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def _run(tmp_path, variant, world):
+def _run(tmp_path, variant, world, mode="rows"):
     sys.path.insert(0, HERE)
     import _mgpu_worker as w
     import synth
     from paper_2407_20692_b200 import Context
     out = tmp_path / "mgpu.npz"
-    env = dict(os.environ, CPI_MGPU_VARIANT=variant)
+    env = dict(os.environ, CPI_MGPU_VARIANT=variant, CPI_MGPU_MODE=mode)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + os.getpid() % 1000),
            os.path.join(HERE, "_mgpu_worker.py"), str(out)]
@@ -42,13 +42,14 @@ def _run(tmp_path, variant, world):
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs >= 2 GPUs (one rank per GPU)")
-@pytest.mark.parametrize("variant", ["fp4", "tc"])
-def test_frame_sharded_nccl_matches_single_gpu(tmp_path, variant):
-    _run(tmp_path, variant, min(torch.cuda.device_count(), 8))
+@pytest.mark.parametrize("variant,mode", [("fp4", "rows"), ("tc", "rows"), ("fp4", "tiles")])
+def test_frame_sharded_nccl_matches_single_gpu(tmp_path, variant, mode):
+    _run(tmp_path, variant, min(torch.cuda.device_count(), 8), mode)
 
 
 @pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a GPU")
-def test_nccl_single_rank_pipeline(tmp_path):
-    """The NCCL code path of the pipeline (async reduce-scatter on the library's count views,
-    all-reduces) as a one-rank group under torch.distributed.run: runs on one GPU."""
-    _run(tmp_path, "fp4", 1)
+@pytest.mark.parametrize("mode", ["rows", "tiles"])
+def test_nccl_single_rank_pipeline(tmp_path, mode):
+    """The NCCL code path of both pipelines (async reduce-scatter on the library's count views /
+    all-gather of frames, all-reduces) as a one-rank group under torch.distributed.run."""
+    _run(tmp_path, "fp4", 1, mode)
