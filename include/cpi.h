@@ -132,9 +132,13 @@ typedef struct {
                                only if all four coordinates lie on their lattices (skip policy).
                                GPU support: B coordinates independent of the output pixel
                                (dx = dy = 0).  Integral B (ex = ey = 1, fx = fy = 0) runs the
-                               fast separable kernels; fractional B (any ex, fx, ey, fy) runs
-                               the general-B kernels (2 x 2 corners per stage, row-major B
-                               order, contiguous row shards); dx or dy != 0 ->
+                               fast separable kernels directly.  Any other (ex, fx, ey, fy):
+                               the library resamples Gamma onto the B lattice once per distinct
+                               B map (a rows x P_b fp32 workspace, allocated on first use and
+                               kept) and runs the same fast kernels, consecutive planes with
+                               one B map fused; if that workspace cannot be allocated it falls
+                               back to general-B kernels (2 x 2 corners per stage, row-major B
+                               order, contiguous row shards only).  dx or dy != 0 ->
                                CPI_ERR_UNSUPPORTED.  The default map is {a, 1 - a, 0, 0, 1, 0}
                                on both axes. */
 } cpi_refocus_spec;
@@ -261,7 +265,8 @@ int64_t cpi_launch_count(const cpi_ctx *ctx);
 /* Per-kernel timing: when enabled, the library records CUDA events around its main
  * kernels on the launching stream; cpi_kernel_time_ms returns the accumulated device time
  * of one kernel class since the last reset (0 = GEMM, 1 = expand, 2 = refocus stage 1,
- * 3 = refocus stage 2, 4 = finalize, 5 = refocus coords) and its launch count.
+ * 3 = refocus stage 2, 4 = finalize, 5 = refocus coords, 6 = fractional-B resample) and its
+ * launch count.
  * Enabling timing synchronises each timed launch's end event lazily (at query time). */
 cpi_status cpi_set_timing(cpi_ctx *ctx, int32_t enable);
 cpi_status cpi_kernel_time_ms(cpi_ctx *ctx, int32_t kernel_class, double *ms, int64_t *launches);

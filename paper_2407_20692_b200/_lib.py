@@ -19,7 +19,7 @@ CPI_LSB_FIRST, CPI_MSB_FIRST = 0, 1
 CPI_HOST, CPI_DEVICE = 0, 1
 CPI_VARIANT_TC, CPI_VARIANT_POPC, CPI_KEEP_COUNTS, CPI_VARIANT_FP4, CPI_GAMMA_UBLOCKED = 0, 1, 2, 4, 8
 CPI_SKIP_RENORMALIZE, CPI_CLAMP = 0, 1
-KC_GEMM, KC_EXPAND, KC_STAGE1, KC_STAGE2, KC_FINALIZE, KC_COORDS = range(6)
+KC_GEMM, KC_EXPAND, KC_STAGE1, KC_STAGE2, KC_FINALIZE, KC_COORDS, KC_RESAMPLE = range(7)
 
 # every symbol include/cpi.h declares
 EXPORTS = ["cpi_create", "cpi_destroy", "cpi_last_error", "cpi_status_string", "cpi_load_frames",

@@ -22,7 +22,7 @@ namespace {
 constexpr int64_t kKAlign = 128;   // frames per GEMM K block (bytes of one swizzle row)
 
 enum KernelClass { KC_GEMM = 0, KC_EXPAND = 1, KC_STAGE1 = 2, KC_STAGE2 = 3, KC_FINALIZE = 4,
-                   KC_COORDS = 5, KC_COUNT = 6 };
+                   KC_COORDS = 5, KC_RESAMPLE = 6, KC_COUNT = 7 };
 
 thread_local std::string g_create_error;
 
@@ -71,6 +71,8 @@ struct cpi_ctx {
     // refocus workspaces
     cpi::AxisTables xs[cpi::kRefocusMaxFuse]{}, ys[cpi::kRefocusMaxFuse]{};
     cpi::AxisTables bxs{}, bys{};          // fractional-B path: B supports per u / v
+    float* bws = nullptr;                  // fractional-B path: Gamma resampled onto the B lattice (lazy)
+    size_t bws_bytes = 0;
     double* T[cpi::kRefocusMaxFuse]{};
     bool refocus_ready = false;
     int fuse = 4;                          // planes per Gamma pass in the TMA stage 1 (CPI_REFOCUS_FUSE)
@@ -214,6 +216,7 @@ void free_all(cpi_ctx* c) {
     cudaFree(c->ypack);
     cudaFree(c->xblk);
     cudaFree(c->gamma_ws);
+    cudaFree(c->bws);
     for (auto& t : c->timed) { c->event_pool.push_back(t.a); c->event_pool.push_back(t.b); }
     for (auto e : c->event_pool) cudaEventDestroy(e);
 }
@@ -231,7 +234,7 @@ cpi_status alloc_axis(cpi_ctx* c, cpi::AxisTables& t, int W, int Wb) {
 
 extern "C" {
 
-int32_t cpi_abi_version(void) { return 102; }
+int32_t cpi_abi_version(void) { return 103; }
 
 const char* cpi_status_string(cpi_status s) {
     switch (s) {
@@ -758,50 +761,90 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
         }
         c->refocus_ready = true;
     }
+    // B map of plane p: (ex, fx, ey, fy); identity = integral B lattice
+    auto bkey = [&](int p, double* k) {
+        const double* mp = spec->affine ? spec->affine + 12 * p : nullptr;
+        k[0] = mp ? mp[4] : 1.0; k[1] = mp ? mp[5] : 0.0; k[2] = mp ? mp[10] : 1.0; k[3] = mp ? mp[11] : 0.0;
+    };
+    auto frac_b = [&](int p) {
+        double k[4];
+        bkey(p, k);
+        return k[0] != 1.0 || k[1] != 0.0 || k[2] != 1.0 || k[3] != 0.0;
+    };
+    auto same_b = [&](int p, int q) {
+        double k[4], l[4];
+        bkey(p, k);
+        bkey(q, l);
+        return k[0] == l[0] && k[1] == l[1] && k[2] == l[2] && k[3] == l[3];
+    };
+    // Fractional B: resample Gamma onto the B lattice once per distinct B map and run the fast
+    // separable path (launch_resample_b); the direct general-B kernels remain for when the
+    // workspace (rows x P_b fp32) cannot be allocated, or under CPI_GENB_DIRECT (A/B knob).
+    bool resample = false;
     if (genb) {
-        if (c->ublocked) return fail(c, CPI_ERR_UNSUPPORTED, "fractional B coordinates need the row-major B order");
         if (Wb < 2 || Hb < 2) return fail(c, CPI_ERR_UNSUPPORTED, "fractional B coordinates need a B RoI of 2x2 or more");
         if (!c->bxs.i0) {
             cpi_status s = alloc_axis(c, c->bxs, 1, Wb);
             if (s == CPI_OK) s = alloc_axis(c, c->bys, 1, Hb);
             if (s != CPI_OK) return s;
         }
+        resample = getenv("CPI_GENB_DIRECT") == nullptr;
+        const size_t need = sizeof(float) * size_t(spec->rows) * size_t(c->p_b);
+        if (resample && c->bws_bytes < need) {
+            cudaFree(c->bws);
+            c->bws = nullptr;
+            c->bws_bytes = 0;
+            if (cudaMalloc(&c->bws, need) == cudaSuccess) {
+                c->bws_bytes = need;
+            } else {
+                (void)cudaGetLastError();
+                resample = false;
+            }
+        }
     }
-    bool tma_now = !genb && c->use_s1_tma && (reinterpret_cast<uintptr_t>(spec->gamma_dev) & 15) == 0;
+    const bool direct = genb && !resample;
+    if (direct && c->ublocked)
+        return fail(c, CPI_ERR_UNSUPPORTED, "fractional B coordinates without the resample workspace need the "
+                                            "row-major B order");
+    bool tma_now = !direct && c->use_s1_tma && (reinterpret_cast<uintptr_t>(spec->gamma_dev) & 15) == 0;
     if (c->ublocked && !tma_now)
         return fail(c, CPI_ERR_UNSUPPORTED, "u-blocked Gamma needs the TMA stage 1 (W_a <= 256, W_b %% 4 == 0, "
                                             "16-byte aligned Gamma)");
-    if (tma_now && c->ublocked) {
+    const float* encoded = nullptr;   // Gamma base the stage-1 tensor map currently describes
+    auto encode_gamma = [&](const float* g) -> cpi_status {
+        if (g == encoded) return CPI_OK;
         cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
-        // (u % 8, v, u / 8, j, m): box 8 x 8 x 1 x 32 x 1 lands as [j][v][u] like the 4D map
-        const cuuint64_t dims[5] = {8u, cuuint64_t(Hb), cuuint64_t(Wb / 8), cuuint64_t(Wa), cuuint64_t(spec->rows / Wa)};
-        const cuuint64_t strides[4] = {32u, cuuint64_t(Hb) * 32, cuuint64_t(c->p_b) * 4, cuuint64_t(Wa) * c->p_b * 4};
-        const cuuint32_t box[5] = {8u, cuuint32_t(cpi::stage1_vgroup(Wa)), 1u, 32u, 1u};
-        const cuuint32_t es[5] = {1u, 1u, 1u, 1u, 1u};
-        CUresult r = enc(&c->s1maps.gamma, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(spec->gamma_dev),
-                         dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(c, CPI_ERR_CUDA, "u-blocked Gamma tensor map failed (%d)", int(r));
-        c->s1maps.gamma_5d = 1;
-    } else if (tma_now) {
-        c->s1maps.gamma_5d = 0;
-        cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
-        const cuuint64_t dims[4] = {cuuint64_t(Wb), cuuint64_t(Hb), cuuint64_t(Wa), cuuint64_t(spec->rows / Wa)};
-        const cuuint64_t strides[3] = {cuuint64_t(Wb) * 4, cuuint64_t(c->p_b) * 4, cuuint64_t(Wa) * c->p_b * 4};
-        const cuuint32_t box[4] = {8u, cuuint32_t(cpi::stage1_vgroup(Wa)), 32u, 1u};
-        const cuuint32_t es[4] = {1u, 1u, 1u, 1u};
-        // L2 sector promotion of the Gamma stream (tuning knob CPI_S1_L2PROMO = 0/64/128/256)
-        CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-        if (const char* ev = getenv("CPI_S1_L2PROMO")) {
-            const int v = atoi(ev);
-            promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                  : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+        CUresult r;
+        if (c->ublocked) {
+            // (u % 8, v, u / 8, j, m): box 8 x 8 x 1 x 32 x 1 lands as [j][v][u] like the 4D map
+            const cuuint64_t dims[5] = {8u, cuuint64_t(Hb), cuuint64_t(Wb / 8), cuuint64_t(Wa), cuuint64_t(spec->rows / Wa)};
+            const cuuint64_t strides[4] = {32u, cuuint64_t(Hb) * 32, cuuint64_t(c->p_b) * 4, cuuint64_t(Wa) * c->p_b * 4};
+            const cuuint32_t box[5] = {8u, cuuint32_t(cpi::stage1_vgroup(Wa)), 1u, 32u, 1u};
+            const cuuint32_t es[5] = {1u, 1u, 1u, 1u, 1u};
+            r = enc(&c->s1maps.gamma, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(g), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            c->s1maps.gamma_5d = 1;
+        } else {
+            const cuuint64_t dims[4] = {cuuint64_t(Wb), cuuint64_t(Hb), cuuint64_t(Wa), cuuint64_t(spec->rows / Wa)};
+            const cuuint64_t strides[3] = {cuuint64_t(Wb) * 4, cuuint64_t(c->p_b) * 4, cuuint64_t(Wa) * c->p_b * 4};
+            const cuuint32_t box[4] = {8u, cuuint32_t(cpi::stage1_vgroup(Wa)), 32u, 1u};
+            const cuuint32_t es[4] = {1u, 1u, 1u, 1u};
+            // L2 sector promotion of the Gamma stream (tuning knob CPI_S1_L2PROMO = 0/64/128/256)
+            CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+            if (const char* ev = getenv("CPI_S1_L2PROMO")) {
+                const int v = atoi(ev);
+                promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                      : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+            }
+            r = enc(&c->s1maps.gamma, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(g), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            c->s1maps.gamma_5d = 0;
         }
-        CUresult r = enc(&c->s1maps.gamma, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(spec->gamma_dev),
-                         dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(c, CPI_ERR_CUDA, "Gamma tensor map failed (%d)", int(r));
-    }
+        encoded = g;
+        return CPI_OK;
+    };
     const int m_base = static_cast<int>(spec->row0 / Wa), m_count = static_cast<int>(spec->rows / Wa);
     const bool cyclic = spec->row_block > 0 && spec->row_block < m_count;
     const int m_block = cyclic ? spec->row_block : 0, m_stride = cyclic ? spec->row_stride : 0;
@@ -810,11 +853,17 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
             return fail(c, CPI_ERR_INVALID_ARG, "row_stride %d < row_block %d", m_stride, m_block);
         const int64_t last = m_base + int64_t((m_count - 1) / m_block) * m_stride + (m_count - 1) % m_block;
         if (last >= Ha) return fail(c, CPI_ERR_INVALID_ARG, "block-cyclic shard reaches A row %lld >= H_a", (long long)last);
-        if (genb) return fail(c, CPI_ERR_UNSUPPORTED, "fractional B coordinates need contiguous row shards");
+        if (direct) return fail(c, CPI_ERR_UNSUPPORTED, "fractional B coordinates without the resample workspace "
+                                                        "need contiguous row shards");
     }
     const int group = tma_now ? c->fuse : 1;
-    for (int p0 = 0; p0 < spec->n_planes; p0 += group) {
-        const int nf = std::min(group, spec->n_planes - p0);
+    int resampled = -1;   // plane whose B map the workspace currently holds
+    for (int p0 = 0; p0 < spec->n_planes;) {
+        // a fused group: consecutive planes sharing one Gamma source (one B map when resampling)
+        int nf = 1;
+        while (nf < group && p0 + nf < spec->n_planes && (!resample || same_b(p0, p0 + nf))) ++nf;
+        const bool from_ws = resample && frac_b(p0);
+        const float* gsrc = from_ws ? c->bws : spec->gamma_dev;
         {
             TimedScope ts(c, KC_COORDS, st);
             cudaError_t e = cudaSuccess;
@@ -833,15 +882,11 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
                 }
                 cg.xs[f] = c->xs[f];
                 cg.ys[f] = c->ys[f];
-                const double* mp = spec->affine ? spec->affine + 12 * (p0 + f) : nullptr;
-                cg.bmap[f][0] = mp ? mp[4] : 1.0;
-                cg.bmap[f][1] = mp ? mp[5] : 0.0;
-                cg.bmap[f][2] = mp ? mp[10] : 1.0;
-                cg.bmap[f][3] = mp ? mp[11] : 0.0;
-                cg.bx[f] = c->bxs;
+                bkey(p0 + f, cg.bmap[f]);
+                cg.bx[f] = c->bxs;   // one B map per group: every f writes the same supports
                 cg.by[f] = c->bys;
             }
-            cg.genb = genb ? 1 : 0;
+            cg.genb = direct || from_ws ? 1 : 0;   // B supports for the direct kernels / the resample
             e = cpi::launch_refocus_coords_group(cg, nf, st);
             c->launches += 2;
             if (e == cudaSuccess && tma_now) {
@@ -854,17 +899,29 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
             }
             if (e != cudaSuccess) return cuda_fail(c, e, "refocus coords launch");
         }
+        if (from_ws && (resampled < 0 || !same_b(p0, resampled))) {
+            TimedScope ts(c, KC_RESAMPLE, st);
+            cudaError_t e = cpi::launch_resample_b(spec->gamma_dev, c->bws, spec->rows, Wb, Hb, c->ublocked ? 1 : 0,
+                                                   spec->affine[12 * p0 + 10], c->bxs, c->bys, st);
+            c->launches += 1;
+            if (e != cudaSuccess) return cuda_fail(c, e, "B resample launch");
+            resampled = p0;
+        }
+        if (tma_now) {
+            cpi_status s = encode_gamma(gsrc);
+            if (s != CPI_OK) return s;
+        }
         {
             TimedScope ts(c, KC_STAGE1, st);
             cudaError_t e;
-            if (genb)
+            if (direct)
                 e = cpi::launch_refocus_stage1_genb(spec->gamma_dev, c->p_b, Wa, Ha, Wb, Hb, m_base, m_count, c->xs[0],
                                                     c->bxs, c->T[0], st);
             else if (tma_now)
                 e = cpi::launch_refocus_stage1_tma(&c->s1maps, nf, Wa, Ha, Wb, Hb, m_base, m_count, m_block, m_stride,
                                                    c->xs, c->ys, c->T, c->xblk, c->num_sms, st);
             else if (!cyclic)
-                e = cpi::launch_refocus_stage1(spec->gamma_dev, c->p_b, Wa, Ha, Wb, Hb, m_base, m_count,
+                e = cpi::launch_refocus_stage1(gsrc, c->p_b, Wa, Ha, Wb, Hb, m_base, m_count,
                                                c->xs[0], c->ys[0], c->T[0], st);
             else
                 return fail(c, CPI_ERR_UNSUPPORTED, "block-cyclic shards need the TMA stage 1 (W_a <= 256, W_b %% 4 == 0, "
@@ -875,7 +932,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
         {
             TimedScope ts(c, KC_STAGE2, st);
             cudaError_t e = cudaSuccess;
-            if (genb) {
+            if (direct) {
                 e = cpi::launch_refocus_stage2_genb(c->T[0], Wa, Ha, Hb, m_base, m_count, c->xs[0], c->ys[0], c->bys,
                                                     planes + int64_t(p0) * Ha * Wa, st);
                 c->launches += 1;
@@ -894,6 +951,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
             }
             if (e != cudaSuccess) return cuda_fail(c, e, "refocus stage-2 launch");
         }
+        p0 += nf;
     }
     return CPI_OK;
 }

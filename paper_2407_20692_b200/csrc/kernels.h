@@ -102,6 +102,12 @@ cudaError_t launch_refocus_stage1_genb(const float* gamma, int64_t ldg, int Wa, 
                                        cudaStream_t st);
 cudaError_t launch_refocus_stage2_genb(const double* T, int Wa, int Ha, int Hb, int m_base, int m_count,
                                        AxisTables xs, AxisTables ys, AxisTables by, float* plane, cudaStream_t st);
+// General-B pre-pass (default route for fractional B): Gamma'(p; v, u) = bilinear of Gamma(p; ., .)
+// at the B support (by[v], bx[u]) for rows A pixels of P_b slots each (B order row-major or
+// u-blocked), so that the separable fast path runs Gamma' with the identity B map.  ey = the
+// map's B-row scale (bounds the B support rows of a band: banded shared-memory form if small).
+cudaError_t launch_resample_b(const float* src, float* dst, int64_t rows, int Wb, int Hb, int ublocked, double ey,
+                              AxisTables bx, AxisTables by, cudaStream_t st);
 cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
                                   int m_base, int m_count, AxisTables xs, AxisTables ys,
                                   double* T, cudaStream_t st);

@@ -17,6 +17,7 @@
 // stages 8-column (u) slabs of the rows j it needs into padded shared memory (odd word
 // stride -> conflict-free gathers), and each thread owns one output x.
 #include <climits>
+#include <cmath>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -792,7 +793,179 @@ __global__ void stage2_genb_kernel(const double* __restrict__ T, int Wa, int Ha,
     }
 }
 
+// ---- general-B pre-pass: resample Gamma onto the B lattice -------------------------------
+// With B coordinates that depend on u / v only (dx = dy = 0), the 16-corner multilinear weight
+// of a sample factorises into (A corners) x (B corners), so
+//   sum_A w_A sum_B w_B Gamma(A corner; B corner) = sum_A w_A Gamma'(A corner; v, u),
+//   Gamma'(p; v, u) = (1 - t_v) [(1 - t_u) G(n, k) + t_u G(n, k + 1)] + t_v [(1 - t_u) G(n + 1, k) + t_u G(n + 1, k + 1)]
+// with (k, t_u) = bx[u], (n, t_v) = by[v] the B support of the map (skipped samples are
+// removed by the A tables, which carry the B lattice test).  Gamma' then runs through the
+// separable fast path with the identity B map.  grid (rows, ceil(P_b / (kV * 256))); thread =
+// kV consecutive B slots of one A pixel (same v, consecutive u in both B orders).
+template <int kV>
+__global__ void __launch_bounds__(256)
+resample_b_kernel(const float* __restrict__ src, float* __restrict__ dst, int Wb, int Hb, int ub,
+                  const int32_t* __restrict__ bxi, const double* __restrict__ bxt, const int32_t* __restrict__ byi,
+                  const double* __restrict__ byt) {
+    const int64_t pb = static_cast<int64_t>(Wb) * Hb;
+    const int q = (blockIdx.y * 256 + threadIdx.x) * kV;
+    if (q >= pb) return;
+    const int64_t p = blockIdx.x;
+    int v, u0;
+    if (ub) {
+        const int u8 = q / (8 * Hb), r = q - u8 * 8 * Hb;
+        v = r >> 3;
+        u0 = u8 * 8 + (r & 7);
+    } else {
+        v = q / Wb;
+        u0 = q - v * Wb;
+    }
+    const float* s = src + p * pb;
+    const int n = __ldg(byi + v);
+    const double tv = __ldg(byt + v), wv = __dadd_rn(1.0, -tv);
+    float out[kV];
+#pragma unroll
+    for (int i = 0; i < kV; ++i) {
+        const int u = u0 + i;
+        const int k = __ldg(bxi + u);
+        const double tu = __ldg(bxt + u), wu = __dadd_rn(1.0, -tu);
+        int64_t i00, i01, i10, i11;
+        if (ub) {
+            const int64_t c0 = static_cast<int64_t>(k >> 3) * 8 * Hb + (k & 7);
+            const int64_t c1 = static_cast<int64_t>((k + 1) >> 3) * 8 * Hb + ((k + 1) & 7);
+            i00 = c0 + 8 * n; i01 = c1 + 8 * n; i10 = c0 + 8 * (n + 1); i11 = c1 + 8 * (n + 1);
+        } else {
+            i00 = static_cast<int64_t>(n) * Wb + k; i01 = i00 + 1; i10 = i00 + Wb; i11 = i10 + 1;
+        }
+        const double lo = wu * static_cast<double>(__ldg(s + i00)) + tu * static_cast<double>(__ldg(s + i01));
+        const double hi = wu * static_cast<double>(__ldg(s + i10)) + tu * static_cast<double>(__ldg(s + i11));
+        out[i] = static_cast<float>(wv * lo + tv * hi);
+    }
+    float* d = dst + p * pb + q;
+    if constexpr (kV == 4) {
+        __stcs(reinterpret_cast<float4*>(d), make_float4(out[0], out[1], out[2], out[3]));
+    } else {
+        d[0] = out[0];
+    }
+}
+
+// Banded form (the default): CTA = (A pixel p, band of kRsV B rows v).  The band's B support
+// rows n in [lo, hi + 1] (n(v) is monotone in v, so the band ends bound it) are staged in
+// shared memory with coalesced 16-byte loads, de-blocked to row-major [n][k] with a padded row
+// stride; each thread then owns B columns u (weights loaded once) and walks the band's rows v,
+// four shared-memory taps and three FMAs per output, stores coalesced across the warp.  The
+// host sizes the stage to the map's bound on the support rows (cap = ceil(|ey| (kRsV - 1)) + 4,
+// 20 rows for |ey| <= 1, so several CTAs per SM keep loads in flight) and launches this form
+// only when cap <= kRsCap, else the gather form above.
+constexpr int kRsV = 16, kRsCap = 40;
+__host__ __device__ constexpr int rs_pitch(int Wb) { return Wb + 8; }
+template <bool kUB>
+__global__ void __launch_bounds__(256)
+resample_b_band_kernel(const float* __restrict__ src, float* __restrict__ dst, int Wb, int Hb, int cap,
+                       const int32_t* __restrict__ bxi, const double* __restrict__ bxt,
+                       const int32_t* __restrict__ byi, const double* __restrict__ byt) {
+    extern __shared__ float4 rs_sm4[];
+    float* s_g = reinterpret_cast<float*>(rs_sm4);   // [kRsCap][pitch]
+    __shared__ int s_vr[kRsV];                       // support row of v0 + i, relative to lo
+    __shared__ float s_vt[kRsV];
+    const int pitch = rs_pitch(Wb);
+    const int64_t pb = static_cast<int64_t>(Wb) * Hb;
+    const int64_t p = blockIdx.x;
+    const int v0 = blockIdx.y * kRsV, nv = min(kRsV, Hb - v0);
+    const int na = __ldg(byi + v0), nz = __ldg(byi + v0 + nv - 1);
+    const int lo = min(na, nz), rows = max(na, nz) + 2 - lo;   // support rows [lo, lo + rows)
+    if (threadIdx.x < nv) {
+        s_vr[threadIdx.x] = (__ldg(byi + v0 + threadIdx.x) - lo) * pitch;
+        s_vt[threadIdx.x] = static_cast<float>(__ldg(byt + v0 + threadIdx.x));
+    }
+    const float* s = src + p * pb;
+    if (rows > cap) {   // cannot happen for the host's cap; kept as a safe global-memory path
+        for (int w = threadIdx.x; w < nv * Wb; w += 256) {
+            const int v = v0 + w / Wb, u = w % Wb;
+            const int n = __ldg(byi + v), k = __ldg(bxi + u);
+            const float tu = static_cast<float>(__ldg(bxt + u)), tv = static_cast<float>(__ldg(byt + v));
+            auto at = [&](int nn, int kk) {
+                return __ldg(s + (kUB ? static_cast<int64_t>(kk >> 3) * 8 * Hb + 8 * nn + (kk & 7)
+                                      : static_cast<int64_t>(nn) * Wb + kk));
+            };
+            const float a = fmaf(tu, at(n, k + 1), (1.f - tu) * at(n, k));
+            const float b = fmaf(tu, at(n + 1, k + 1), (1.f - tu) * at(n + 1, k));
+            dst[p * pb + (kUB ? static_cast<int64_t>(u >> 3) * 8 * Hb + 8 * v + (u & 7) : static_cast<int64_t>(v) * Wb + u)] =
+                fmaf(tv, b - a, a);
+        }
+        return;
+    }
+    if constexpr (kUB) {
+        // (k / 8, n, k % 8): per 8-column block the support rows are one run of 8 rows floats
+        const int per = 2 * rows;   // float4 per 8-column block
+        for (int i = threadIdx.x; i < (Wb / 8) * per; i += 256) {
+            const int kb = i / per, r4 = i - kb * per;
+            const float4 x = __ldg(reinterpret_cast<const float4*>(s + static_cast<int64_t>(kb) * 8 * Hb + 8 * lo) + r4);
+            *reinterpret_cast<float4*>(s_g + (r4 >> 1) * pitch + kb * 8 + (r4 & 1) * 4) = x;
+        }
+    } else {
+        const int q4 = Wb / 4;
+        const float4* g4 = reinterpret_cast<const float4*>(s + static_cast<int64_t>(lo) * Wb);
+        for (int i = threadIdx.x; i < rows * q4; i += 256) {
+            const int r = i / q4, c4 = i - r * q4;
+            *reinterpret_cast<float4*>(s_g + r * pitch + 4 * c4) = __ldg(g4 + i);
+        }
+    }
+    __syncthreads();
+    float* d = dst + p * pb;
+    for (int u = threadIdx.x; u < Wb; u += 256) {
+        const int k = __ldg(bxi + u);
+        const float tu = static_cast<float>(__ldg(bxt + u)), wu = 1.f - tu;
+        const float* col = s_g + k;
+        float* o = d + (kUB ? static_cast<int64_t>(u >> 3) * 8 * Hb + 8 * v0 + (u & 7) : static_cast<int64_t>(v0) * Wb + u);
+        const int ostep = kUB ? 8 : Wb;
+#pragma unroll 4
+        for (int i = 0; i < nv; ++i) {
+            const float* r0 = col + s_vr[i];
+            const float tv = s_vt[i];
+            const float a = fmaf(tu, r0[1], wu * r0[0]);
+            const float b = fmaf(tu, r0[pitch + 1], wu * r0[pitch]);
+            __stcs(o + i * ostep, fmaf(tv, b - a, a));
+        }
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_resample_b(const float* src, float* dst, int64_t rows, int Wb, int Hb, int ublocked, double ey,
+                              AxisTables bx, AxisTables by, cudaStream_t st) {
+    if (rows <= 0) return cudaSuccess;
+    if (rows > 0x7fffffffLL || Wb < 2 || Hb < 2) return cudaErrorInvalidValue;
+    const int64_t pb = static_cast<int64_t>(Wb) * Hb;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+    // support rows of a band: |n(v0 + kRsV - 1) - n(v0)| + 2 <= ceil(|ey| (kRsV - 1)) + 3 (+1 margin)
+    const double span = std::ceil(std::fabs(ey) * (kRsV - 1)) + 4;
+    const bool band = aligned && Wb % 4 == 0 && (!ublocked || Wb % 8 == 0) && span <= kRsCap &&
+                      getenv("CPI_RESAMPLE_GATHER") == nullptr;
+    if (band) {
+        const int cap = static_cast<int>(span);
+        const size_t smem = size_t(cap) * rs_pitch(Wb) * 4;
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(ublocked ? resample_b_band_kernel<true> : resample_b_band_kernel<false>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+        }
+        const dim3 grid(static_cast<unsigned>(rows), static_cast<unsigned>((Hb + kRsV - 1) / kRsV));
+        if (ublocked)
+            resample_b_band_kernel<true><<<grid, 256, smem, st>>>(src, dst, Wb, Hb, cap, bx.i0, bx.t, by.i0, by.t);
+        else
+            resample_b_band_kernel<false><<<grid, 256, smem, st>>>(src, dst, Wb, Hb, cap, bx.i0, bx.t, by.i0, by.t);
+        return cudaGetLastError();
+    }
+    const bool vec = Wb % 4 == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+    const int per = vec ? 4 * 256 : 256;
+    const dim3 grid(static_cast<unsigned>(rows), static_cast<unsigned>((pb + per - 1) / per));
+    if (vec)
+        resample_b_kernel<4><<<grid, 256, 0, st>>>(src, dst, Wb, Hb, ublocked, bx.i0, bx.t, by.i0, by.t);
+    else
+        resample_b_kernel<1><<<grid, 256, 0, st>>>(src, dst, Wb, Hb, ublocked, bx.i0, bx.t, by.i0, by.t);
+    return cudaGetLastError();
+}
 
 bool stage2_staged_supported(int Ha) { return Ha >= 2 && Ha <= kS2Threads; }
 

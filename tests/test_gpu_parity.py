@@ -468,17 +468,31 @@ def test_refocus_affine_maps(boundary):
 
 
 @pytest.mark.parametrize("boundary", [0, 1])
-def test_refocus_affine_fractional_b(boundary):
-    """General maps with fractional B coordinates (ex, fx, ey, fy arbitrary; dx = dy = 0): the
-    general-B kernels (2 x 2 corners per stage) vs the oracle's 16-corner refocus, 1e-6 M."""
+@pytest.mark.parametrize("route", ["band", "gather", "direct"])
+def test_refocus_affine_fractional_b(boundary, route, monkeypatch):
+    """General maps with fractional B coordinates (ex, fx, ey, fy arbitrary; dx = dy = 0) vs the
+    oracle's 16-corner refocus, 1e-6 M.  Default route: Gamma resampled onto the B lattice once
+    per distinct B map (planes 0-2 share one and run as one fused group, plane 7 repeats it after
+    other maps), then the separable fast path; the resample runs banded in shared memory, or as
+    a gather (CPI_RESAMPLE_GATHER, and always for |ey| > 2.4 such as plane 9's); direct = the
+    general-B kernels (CPI_GENB_DIRECT)."""
+    if route == "direct":
+        monkeypatch.setenv("CPI_GENB_DIRECT", "1")
+    elif route == "gather":
+        monkeypatch.setenv("CPI_RESAMPLE_GATHER", "1")
     dims = (24, 20, 16, 12)
     Wa, Ha, Wb, Hb = dims
     G = synth.random_gamma(Wa * Ha, Wb * Hb, seed=23)
     maps = [[0.7, 0.3, 0.25, 0.0, 0.5, -0.3, 1.3, -0.3, -0.4, 0.0, 0.8, 0.2],
+            [1.1, -0.1, 0.0, 0.0, 0.5, -0.3, 0.9, 0.1, 0.3, 0.0, 0.8, 0.2],
+            [0.6, 0.4, -0.2, 0.0, 0.5, -0.3, 1.0, 0.0, 0.0, 0.0, 0.8, 0.2],
             [1.0, 0.0, 0.0, 0.0, 0.75, 0.1, 0.9, 0.1, 0.0, 0.0, 1.1, 0.0],
             [1.6, -0.45, -1.5, 0.0, 1.25, 0.5, 0.55, 0.5, 2.0, 0.0, 0.6, -1.0],
             [2.0, -1.0, 0.5, 0.0, -0.9, 0.0, 0.5, 0.5, 0.0, 0.0, 1.9, 0.3],
-            [0.8, 0.2, 0.0, 0.0, 1.0, 0.0, 1.2, -0.2, 0.0, 0.0, 1.0, 0.0]]   # last: integral B in a mixed call
+            [0.8, 0.2, 0.0, 0.0, 1.0, 0.0, 1.2, -0.2, 0.0, 0.0, 1.0, 0.0],   # integral B in a mixed call
+            [0.9, 0.1, 0.1, 0.0, 0.5, -0.3, 0.7, 0.3, 0.0, 0.0, 0.8, 0.2],
+            [1.0, 0.0, 0.0, 0.0, 1.0, 2.0, 1.0, 0.0, 0.0, 0.0, 1.0, -1.0],   # integer B shift
+            [0.9, 0.1, 0.0, 0.0, -0.6, 0.2, 1.1, -0.1, 0.0, 0.0, -3.0, 0.4]]   # |ey| > 2.4: gather form
     ctx = _ctx((0, 0, Wa, Ha), (0, 0, Wb, Hb), 1)
     g = torch.from_numpy(np.ascontiguousarray(G, dtype=np.float32)).cuda()
     planes = ctx.new_planes(len(maps))
@@ -488,6 +502,46 @@ def test_refocus_affine_fractional_b(boundary):
     Ro = oracle.refocus_affine(G, dims, maps, boundary=boundary)
     M = oracle.refocus_affine(np.abs(G.astype(np.float64)), dims, maps, boundary=boundary)
     assert np.all(np.abs(R - Ro) <= 1e-6 * M + 1e-30), np.max(np.abs(R - Ro) / np.maximum(M, 1e-300))
+
+
+@pytest.mark.parametrize("boundary", [0, 1])
+def test_refocus_fractional_b_ublocked_block_cyclic(boundary):
+    """Fractional B through the resample route on u-blocked Gamma columns and block-cyclic
+    A-row shards (the multi-GPU layout): each shard matches the oracle on Gamma restricted to
+    its rows, and the shards add up to the unsharded row-major result."""
+    dims = (24, 16, 16, 12)
+    Wa, Ha, Wb, Hb = dims
+    G = synth.random_gamma(Wa * Ha, Wb * Hb, seed=29)
+    maps = [[0.7, 0.3, 0.25, 0.0, 0.5, -0.3, 1.3, -0.3, -0.4, 0.0, 0.8, 0.2],
+            [1.2, -0.2, 0.0, 0.0, 0.5, -0.3, 0.8, 0.2, 0.0, 0.0, 0.8, 0.2],
+            [1.6, -0.45, -1.5, 0.0, 1.25, 0.5, 0.55, 0.5, 2.0, 0.0, 0.6, -1.0]]
+    row = _ctx((0, 0, Wa, Ha), (0, 0, Wb, Hb), 1)
+    whole = row.new_planes(len(maps))
+    row.refocus(None, torch.from_numpy(np.ascontiguousarray(G, dtype=np.float32)).cuda(), whole,
+                boundary=boundary, affine=maps)
+    blk = _ctx((0, 0, Wa, Ha), (0, 0, Wb, Hb), 1, gamma_blocked=True)
+    idx = blk.b_index()
+    world, block = 4, 2
+    total = np.zeros((len(maps), Ha, Wa))
+    for rank in range(world):
+        stride = world * block
+        m = np.array([rank * block + (l // block) * stride + l % block for l in range(Ha // world)])
+        pix = (m[:, None] * Wa + np.arange(Wa)[None, :]).reshape(-1)
+        Gb = np.empty((pix.size, Wb * Hb), dtype=np.float32)
+        Gb[:, idx] = G[pix]
+        planes = blk.new_planes(len(maps))
+        blk.refocus(None, torch.from_numpy(Gb).cuda(), planes, boundary=boundary, affine=maps,
+                    row0=rank * block * Wa, rows=pix.size, row_block=block, row_stride=stride)
+        torch.cuda.synchronize()
+        R = planes.cpu().numpy().astype(np.float64)
+        Gs = np.zeros_like(G)
+        Gs[pix] = G[pix]
+        Ro = oracle.refocus_affine(Gs, dims, maps, boundary=boundary)
+        M = oracle.refocus_affine(np.abs(Gs.astype(np.float64)), dims, maps, boundary=boundary)
+        assert np.all(np.abs(R - Ro) <= 1e-6 * M + 1e-30), np.max(np.abs(R - Ro) / np.maximum(M, 1e-300))
+        total += R
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(total, whole.cpu().numpy(), rtol=1e-5, atol=1e-7)
 
 
 def test_refocus_from_current_totals():
