@@ -129,7 +129,7 @@ def _reduce_scatter_async(out: torch.Tensor, full: torch.Tensor, group):
 
 
 def correlate_and_refocus(backend, frames_local, roi_a, roi_b, alphas=None, group=None,
-                          min_panel_rows: int = 8192) -> ShardResult:
+                          min_panel_rows: int = 8192, affine=None) -> ShardResult:
     """Run the frame-sharded pipeline on this rank.  ``backend`` provides
          row_align                          GEMM row-panel alignment (A pixels)
          begin(frames)                      load this rank's frames
@@ -137,8 +137,9 @@ def correlate_and_refocus(backend, frames_local, roi_a, roi_b, alphas=None, grou
                                             over this rank's frames (launched on the current stream)
          marginals() -> (s_a, s_b, n)       this rank's S_a, S_b (int32), frame count
          finalize_rows(s_ab_rows, s_a_rows, s_b, n_tot) -> Gamma rows fp32
-         refocus(alphas, gamma_rows, row0, rows, row_block, row_stride) -> planes fp32
-    with all tensors on ``backend.device``."""
+         refocus(alphas, gamma_rows, row0, rows, row_block, row_stride, affine) -> planes fp32
+    with all tensors on ``backend.device``.  affine: optional [planes][12] general RefocusMap
+    rows (include/cpi.h) used instead of alphas."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     Wa, Ha = roi_a[2], roi_a[3]
@@ -164,11 +165,19 @@ def correlate_and_refocus(backend, frames_local, roi_a, roi_b, alphas=None, grou
     n_tot = int(marg[-1].item())
     s_a_rows = s_a_tot[plan.pixel_rows().to(s_a_tot.device)].contiguous()
     gamma_rows = backend.finalize_rows(shard.view(-1, p_b), s_a_rows, s_b_tot, n_tot)
-    planes = None
-    if alphas is not None and len(alphas):
-        planes = backend.refocus(alphas, gamma_rows, plan.m_base * Wa, plan.m_count * Wa, plan.block, plan.stride)
-        dist.all_reduce(planes, op=dist.ReduceOp.SUM, group=group)
+    planes = _refocus_shard(backend, plan, Wa, gamma_rows, alphas, affine, group)
     return ShardResult(n_tot, plan, gamma_rows, planes)
+
+
+def _refocus_shard(backend, plan, Wa, gamma_rows, alphas, affine, group):
+    """Refocus this rank's block-cyclic Gamma rows and sum the partial planes over ranks
+    (refocusing is linear in Gamma).  affine rows replace alphas when given."""
+    if affine is None and (alphas is None or not len(alphas)):
+        return None
+    args = (gamma_rows, plan.m_base * Wa, plan.m_count * Wa, plan.block, plan.stride)
+    planes = backend.refocus(alphas, *args) if affine is None else backend.refocus(None, *args, affine=affine)
+    dist.all_reduce(planes, op=dist.ReduceOp.SUM, group=group)
+    return planes
 
 
 def _gather_frames(frames_local, group, device) -> torch.Tensor:
@@ -194,7 +203,7 @@ def _gather_frames(frames_local, group, device) -> torch.Tensor:
 
 
 def correlate_and_refocus_tiles(backend, frames_local, roi_a, roi_b, alphas=None, group=None,
-                                min_panel_rows: int = 8192) -> ShardResult:
+                                min_panel_rows: int = 8192, affine=None) -> ShardResult:
     """Output-tile sharding (SURVEY §8(e) control measurement): the packed frames are
     all-gathered (each rank's slice is 16 KB per frame, ~1.3 GB per rank at 10^5 frames), then
     every rank runs the GEMM with the fused exact normalisation on its own block-cyclic Gamma
@@ -212,10 +221,7 @@ def correlate_and_refocus_tiles(backend, frames_local, roi_a, roi_b, alphas=None
     gamma_rows = torch.empty((plan.panels * chunk, p_b), dtype=torch.float32, device=backend.device)
     for k in range(plan.panels):
         backend.rows_to(k * plan.panel_rows + rank * chunk, chunk, gamma_rows[k * chunk:(k + 1) * chunk])
-    planes = None
-    if alphas is not None and len(alphas):
-        planes = backend.refocus(alphas, gamma_rows, plan.m_base * Wa, plan.m_count * Wa, plan.block, plan.stride)
-        dist.all_reduce(planes, op=dist.ReduceOp.SUM, group=group)
+    planes = _refocus_shard(backend, plan, Wa, gamma_rows, alphas, affine, group)
     return ShardResult(int(frames_all.shape[0]), plan, gamma_rows, planes)
 
 
@@ -258,8 +264,8 @@ class CudaBackend:
         self.ctx.finalize_counts(s_ab_rows.contiguous(), 0, s_a_rows.contiguous(), s_b.contiguous(), n_tot, g)
         return g
 
-    def refocus(self, alphas, gamma_rows, row0, rows, row_block=0, row_stride=0):
-        planes = self.ctx.new_planes(len(alphas))
+    def refocus(self, alphas, gamma_rows, row0, rows, row_block=0, row_stride=0, affine=None):
+        planes = self.ctx.new_planes(len(affine) if affine is not None else len(alphas))
         self.ctx.refocus(alphas, gamma_rows, planes, row0=row0, rows=rows, row_block=row_block,
-                         row_stride=row_stride)
+                         row_stride=row_stride, affine=affine)
         return planes

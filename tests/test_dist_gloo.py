@@ -20,6 +20,9 @@ ROI_A, ROI_B = (0, 0, 12, 8), (256, 0, 10, 6)
 DIMS = (12, 8, 10, 6)
 N = 900
 ALPHAS = [0.6, 1.0, 1.7]
+# general RefocusMap rows (include/cpi.h), fractional B coordinates on both axes
+MAPS = [[0.7, 0.3, 0.25, 0.0, 0.5, -0.3, 1.3, -0.3, -0.4, 0.0, 0.8, 0.2],
+        [1.6, -0.45, -1.5, 0.0, 1.25, 0.5, 0.55, 0.5, 2.0, 0.0, 0.6, -1.0]]
 
 
 class OracleBackend:
@@ -45,13 +48,15 @@ class OracleBackend:
         g = oracle.gamma(s_ab_rows.numpy(), s_a_rows.numpy(), s_b.numpy(), n_tot)
         return torch.from_numpy(g.astype(np.float32))
 
-    def refocus(self, alphas, gamma_rows, row0, rows, row_block, row_stride):
+    def refocus(self, alphas, gamma_rows, row0, rows, row_block, row_stride, affine=None):
         Wa, Ha, Wb, Hb = DIMS
         G = np.zeros((Wa * Ha, Wb * Hb), dtype=np.float32)
         l = np.arange(rows // Wa)                     # include/cpi.h cpi_refocus_spec row map
         m = row0 // Wa + (l // row_block) * row_stride + l % row_block
         pix = (m[:, None] * Wa + np.arange(Wa)[None, :]).reshape(-1)
         G[pix] = gamma_rows.numpy()
+        if affine is not None:
+            return torch.from_numpy(oracle.refocus_affine(G, DIMS, affine).astype(np.float32))
         return torch.from_numpy(oracle.refocus(G, DIMS, alphas).astype(np.float32))
 
 
@@ -63,7 +68,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, min_panel_rows):
+def _worker(rank, world, port, q, min_panel_rows, affine=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -71,20 +76,22 @@ def _worker(rank, world, port, q, min_panel_rows):
         frames = synth.bernoulli_frames(N, 0.3, seed=31)
         lo, hi = parallel.frame_slice(N, rank, world)
         res = parallel.correlate_and_refocus(OracleBackend(), frames[lo:hi], ROI_A, ROI_B, ALPHAS,
-                                             min_panel_rows=min_panel_rows)
+                                             min_panel_rows=min_panel_rows, affine=MAPS if affine else None)
         q.put((rank, res.n_tot, res.plan, res.gamma_rows.numpy(), res.planes.numpy()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,min_panel_rows", [(2, 8192), (4, 8192), (2, 1), (4, 1)])
-def test_frame_sharded_pipeline_matches_single_process(world, min_panel_rows):
+@pytest.mark.parametrize("world,min_panel_rows,affine", [(2, 8192, False), (4, 8192, False), (2, 1, False),
+                                                         (4, 1, False), (2, 1, True)])
+def test_frame_sharded_pipeline_matches_single_process(world, min_panel_rows, affine):
     """min_panel_rows = 1: one A row per rank per panel (cyclic ownership, several panels);
-    8192: one panel of contiguous blocks at this small RoI."""
+    8192: one panel of contiguous blocks at this small RoI; affine: general maps (fractional
+    B) instead of alphas."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, min_panel_rows)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, min_panel_rows, affine)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=300) for _ in range(world)]
@@ -94,7 +101,7 @@ def test_frame_sharded_pipeline_matches_single_process(world, min_panel_rows):
     frames = synth.bernoulli_frames(N, 0.3, seed=31)
     full = oracle.correlate(frames, ROI_A, ROI_B)
     G = full["gamma"].astype(np.float32)
-    want_planes = oracle.refocus(G, DIMS, ALPHAS)
+    want_planes = oracle.refocus_affine(G, DIMS, MAPS) if affine else oracle.refocus(G, DIMS, ALPHAS)
     covered = np.zeros(G.shape[0], dtype=int)
     for rank, n_tot, plan, g_rows, planes in out:
         assert n_tot == N and plan.rank == rank and plan.world == world

@@ -17,6 +17,8 @@ torch = pytest.importorskip("torch")
 ROI_A, ROI_B = (0, 0, 32, 32), (256, 0, 24, 12)      # P_a = 1024: four 256-row panels at world 2
 N = 1500
 ALPHAS = [0.6, 1.0, 1.45]
+MAPS = [[0.7, 0.3, 0.25, 0.0, 0.5, -0.3, 1.3, -0.3, -0.4, 0.0, 0.8, 0.2],      # fractional B
+        [1.2, -0.2, 0.0, 0.0, 0.5, -0.3, 0.8, 0.2, 0.0, 0.0, 0.8, 0.2]]
 
 
 def _free_port():
@@ -27,7 +29,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, mode="rows"):
+def _worker(rank, world, port, q, mode="rows", affine=False):
     import torch.distributed as dist
     import synth
     from paper_2407_20692_b200 import parallel
@@ -63,19 +65,20 @@ def _worker(rank, world, port, q, mode="rows"):
             def finalize_rows(self, s_ab_rows, s_a_rows, s_b, n_tot):
                 return be.finalize_rows(s_ab_rows.cuda(), s_a_rows.cuda(), s_b.cuda(), n_tot).cpu()
 
-            def refocus(self, alphas, gamma_rows, row0, rows, row_block, row_stride):
-                return be.refocus(alphas, gamma_rows.cuda(), row0, rows, row_block, row_stride).cpu()
+            def refocus(self, alphas, gamma_rows, row0, rows, row_block, row_stride, affine=None):
+                return be.refocus(alphas, gamma_rows.cuda(), row0, rows, row_block, row_stride, affine=affine).cpu()
 
         run = parallel.correlate_and_refocus_tiles if mode == "tiles" else parallel.correlate_and_refocus
-        res = run(GlooCuda(), np.ascontiguousarray(frames[lo:hi]), ROI_A, ROI_B, ALPHAS, min_panel_rows=1)
+        res = run(GlooCuda(), np.ascontiguousarray(frames[lo:hi]), ROI_A, ROI_B, ALPHAS, min_panel_rows=1,
+                  affine=MAPS if affine else None)
         q.put((rank, res.n_tot, res.plan.pixel_rows().numpy(), res.plan.panels, res.gamma_rows.numpy(),
                res.planes.numpy()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["rows", "tiles"])
-def test_two_ranks_on_one_gpu_match_single_context(mode):
+@pytest.mark.parametrize("mode,affine", [("rows", False), ("tiles", False), ("rows", True)])
+def test_two_ranks_on_one_gpu_match_single_context(mode, affine):
     import torch.multiprocessing as mp
     import synth
     from paper_2407_20692_b200 import Context
@@ -83,7 +86,7 @@ def test_two_ranks_on_one_gpu_match_single_context(mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, mode)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, mode, affine)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=600) for _ in range(world)]
@@ -94,8 +97,11 @@ def test_two_ranks_on_one_gpu_match_single_context(mode):
     c = Context(ROI_A, ROI_B, N)
     c.load_frames(frames)
     g = c.correlate(c.new_gamma())
-    planes = c.new_planes(len(ALPHAS))
-    c.refocus(ALPHAS, g, planes)
+    planes = c.new_planes(len(MAPS) if affine else len(ALPHAS))
+    if affine:
+        c.refocus(None, g, planes, affine=MAPS)
+    else:
+        c.refocus(ALPHAS, g, planes)
     torch.cuda.synchronize()
     G = g.cpu().numpy()
     P = planes.cpu().numpy()
