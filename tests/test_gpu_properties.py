@@ -61,12 +61,15 @@ def test_random_refocus(wa, ha, wb, hb, alphas, boundary, seed):
 coef = st.floats(-1.5, 1.5)
 
 
-@settings(max_examples=20, deadline=None, suppress_health_check=list(HealthCheck))
+@settings(max_examples=40, deadline=None, suppress_health_check=list(HealthCheck))
 @given(wa=st.integers(2, 24), ha=st.integers(2, 20), wb=st.integers(2, 16), hb=st.integers(2, 10),
        n_planes=st.integers(1, 3), boundary=st.sampled_from([0, 1]), integral_b=st.booleans(),
+       route=st.sampled_from(["", "CPI_RESAMPLE_GATHER", "CPI_GENB_DIRECT"]),
        seed=st.integers(0, 2**31 - 1), data=st.data())
-def test_random_affine_maps(wa, ha, wb, hb, n_planes, boundary, integral_b, seed, data):
-    """Random general RefocusMap rows (dx = dy = 0), integral or fractional B, vs the oracle."""
+def test_random_affine_maps(wa, ha, wb, hb, n_planes, boundary, integral_b, route, seed, data):
+    """Random general RefocusMap rows (dx = dy = 0), integral or fractional B, vs the oracle;
+    fractional B through the banded or gather B resample, or the direct general-B kernels."""
+    import os
     from paper_2407_20692_b200 import Context
     maps = []
     for _ in range(n_planes):
@@ -82,8 +85,13 @@ def test_random_affine_maps(wa, ha, wb, hb, n_planes, boundary, integral_b, seed
     ctx = Context((0, 0, wa, ha), (0, 0, wb, hb), 1)
     g = torch.from_numpy(np.ascontiguousarray(G, dtype=np.float32)).cuda()
     planes = ctx.new_planes(n_planes)
-    ctx.refocus(None, g, planes, boundary=boundary, affine=maps)
-    torch.cuda.synchronize()
+    if route:
+        os.environ[route] = "1"
+    try:
+        ctx.refocus(None, g, planes, boundary=boundary, affine=maps)
+        torch.cuda.synchronize()
+    finally:
+        os.environ.pop(route, None)
     R = planes.cpu().numpy().astype(np.float64)
     Ro = oracle.refocus_affine(G, dims, maps, boundary=boundary)
     M = oracle.refocus_affine(np.abs(G.astype(np.float64)), dims, maps, boundary=boundary)

@@ -357,3 +357,38 @@ def test_affine_identity_map_is_angular_mean():
 def test_affine_nonfinite_rejected():
     with pytest.raises(ValueError):
         oracle.refocus_affine(np.zeros((4, 4), np.float32), (2, 2, 2, 2), [[np.nan] + [0.0] * 11])
+
+
+def _resample_b_np(G, dims, ex, fx, ey, fy):
+    """Gamma resampled onto the B lattice (DESIGN R15): G'[(m, j)][(v, u)] = bilinear of
+    G[(m, j)][(., .)] at (c_By(v), c_Bx(u)), coordinates clamped to the lattice.  numpy."""
+    Wa, Ha, Wb, Hb = dims
+    G4 = np.asarray(G, dtype=np.float64).reshape(Ha * Wa, Hb, Wb)
+    cbx, cby = (Wb - 1) / 2, (Hb - 1) / 2
+    cu = np.clip(ex * (np.arange(Wb) - cbx) + fx + cbx, 0, Wb - 1)
+    cv = np.clip(ey * (np.arange(Hb) - cby) + fy + cby, 0, Hb - 1)
+    k0 = np.minimum(np.floor(cu), Wb - 2).astype(int)
+    n0 = np.minimum(np.floor(cv), Hb - 2).astype(int)
+    tu, tv = cu - k0, cv - n0
+    rows = (1 - tv)[None, :, None] * G4[:, n0, :] + tv[None, :, None] * G4[:, n0 + 1, :]     # [p][v][k]
+    out = (1 - tu)[None, None, :] * rows[:, :, k0] + tu[None, None, :] * rows[:, :, k0 + 1]  # [p][v][u]
+    return out.reshape(Wa * Ha, Hb * Wb)
+
+
+@pytest.mark.parametrize("boundary,bmap", [(0, (0.8, 0.3, 0.6, -0.5)), (1, (0.8, 0.3, 0.6, -0.5)),
+                                           (1, (1.3, -0.7, 1.6, 0.9))])
+def test_fractional_b_factorises_through_b_resample(boundary, bmap):
+    """R15: with B coordinates depending on u, v only, the 16-corner weight factorises into
+    A corners x B corners, so refocusing Gamma with the fractional-B map equals refocusing the
+    B-resampled Gamma' with the identity B map (the GPU's default route).  Skip policy: B maps
+    that stay on the lattice (so no sample is dropped for its B coordinate); clamp: any map."""
+    dims = (7, 6, 7, 5)
+    Wa, Ha, Wb, Hb = dims
+    G = synth.random_gamma(Wa * Ha, Wb * Hb, seed=41)
+    ex, fx, ey, fy = bmap
+    amaps = [(0.7, 0.3, 0.25, 1.3, -0.3, -0.4), (1.6, -0.45, -1.5, 0.55, 0.5, 2.0), (1.0, 0.0, 0.0, 1.0, 0.0, 0.0)]
+    frac = [[a[0], a[1], a[2], 0.0, ex, fx, a[3], a[4], a[5], 0.0, ey, fy] for a in amaps]
+    ident = [[a[0], a[1], a[2], 0.0, 1.0, 0.0, a[3], a[4], a[5], 0.0, 1.0, 0.0] for a in amaps]
+    R = oracle.refocus_affine(G, dims, frac, boundary=boundary)
+    Rr = oracle.refocus_affine(_resample_b_np(G, dims, ex, fx, ey, fy), dims, ident, boundary=boundary)
+    np.testing.assert_allclose(Rr, R, rtol=1e-11, atol=1e-15)
