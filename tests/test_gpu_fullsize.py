@@ -8,6 +8,7 @@ The oracle cannot compute 2^32 x 10^4 pair-frames, so:
     matrix: row sums = A^T n_B, column sums = B^T n_A, total = n_A . n_B;
   * S_a, S_b: bit-exact in full;
   * planes: 3 planes x 24 sampled output pixels vs the oracle on the GPU's own fp32 Gamma
+    (plus 4 general maps with fractional B coordinates)
     (stage-isolated), tolerance 1e-6 M per output.
 """
 import numpy as np
@@ -52,6 +53,12 @@ def test_fullsize_gamma_bench_configuration(frames, oracle_rows):
     alphas = synth.alpha_grid(64)
     planes = ctx.new_planes(64)
     ctx.refocus(alphas, g, planes)
+    # general maps with fractional B at full size (the B-resample route): three planes share a
+    # B map (one resample, one fused group), one has its own
+    maps = [[a, 1 - a, 0.25, 0.0, 0.9, 0.3, a, 1 - a, -0.25, 0.0, 0.8, -0.2] for a in (0.6, 1.0, 1.7)]
+    maps.append([1.3, -0.3, 0.5, 0.0, 1.1, -0.6, 0.8, 0.2, 0.0, 0.0, 0.95, 0.4])
+    aplanes = ctx.new_planes(len(maps))
+    ctx.refocus(None, g, aplanes, affine=maps)
     torch.cuda.synchronize()
     sel = [0, 21, 63]                     # alpha = 0.5, 1.0, 2.0
     rng = np.random.default_rng(3)
@@ -64,6 +71,11 @@ def test_fullsize_gamma_bench_configuration(frames, oracle_rows):
     P = planes.cpu().numpy().astype(np.float64)
     got_p = np.stack([P[s][pix[:, 1], pix[:, 0]] for s in sel])
     assert np.all(np.abs(got_p - R) <= 1e-6 * M + 1e-30), np.max(np.abs(got_p - R) / np.maximum(M, 1e-300))
+    Ra = oracle.refocus_affine(G, (256, 256, 256, 256), maps, pixels=pix)
+    Ma = oracle.refocus_affine(np.abs(G), (256, 256, 256, 256), maps, pixels=pix)
+    PA = aplanes.cpu().numpy().astype(np.float64)
+    got_a = np.stack([PA[s][pix[:, 1], pix[:, 0]] for s in range(len(maps))])
+    assert np.all(np.abs(got_a - Ra) <= 1e-6 * Ma + 1e-30), np.max(np.abs(got_a - Ra) / np.maximum(Ma, 1e-300))
 
 
 @pytest.mark.parametrize("variant", ["tc", "fp4"])
