@@ -79,8 +79,6 @@ struct AxisTables {           // one axis (x with B-axis u, or y with B-axis v)
     int32_t* lo;              // [Wb]     min used i0 over outputs (INT_MAX if none)
     int32_t* hi;              // [Wb]     max used i0 + 1 over outputs (-1 if none)
 };
-cudaError_t launch_refocus_coords(double a, double b, double c_off, int boundary, int W, int Wb,
-                                  AxisTables tab, cudaStream_t st);
 // All coordinate tables of a fused plane group in two launches (tables + counts);
 // map[f] = {ax, bx, cx, ay, by, cy} of plane f's A-axis maps.
 struct CoordsGroupArgs {

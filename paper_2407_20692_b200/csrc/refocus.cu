@@ -37,10 +37,7 @@ constexpr int kS1Threads = 256;
 // b = 1 - alpha, c_off = 0 (adding +0.0 leaves the default's value unchanged), a general
 // RefocusMap row supplies (ax, bx, cx) / (ay, by, cy) (include/cpi.h cpi_refocus_spec.affine).
 __device__ __forceinline__ void coords_block(double a, double b, double c_off, int boundary, int W, int Wb,
-                                             AxisTables tab, int ub, bool count, bool b_ok = true);
-__global__ void coords_kernel(double a, double b, double c_off, int boundary, int W, int Wb, AxisTables tab) {
-    coords_block(a, b, c_off, boundary, W, Wb, tab, blockIdx.x, true);
-}
+                                             AxisTables tab, int ub, bool b_ok);
 // B coordinate of lattice index ub: c_B = ((e (ub - c_b)) + f) + c_b (fp64, oracle order); the
 // integral map (1, 0) gives ub exactly.
 __device__ __forceinline__ double b_coord(double e, double f, int Wb, int ub) {
@@ -58,7 +55,7 @@ __global__ void coords_group_kernel(CoordsGroupArgs g) {
     const double cb = b_coord(e, fo, Wb, ub);
     const bool b_ok = g.boundary != 0 || (cb >= 0.0 && cb <= static_cast<double>(Wb - 1));
     coords_block(g.map[f][3 * ax], g.map[f][3 * ax + 1], g.map[f][3 * ax + 2], g.boundary, W, Wb,
-                 ax ? g.ys[f] : g.xs[f], ub, false, b_ok);
+                 ax ? g.ys[f] : g.xs[f], ub, b_ok);
     if (g.genb && threadIdx.x == 0) {   // B support of this lattice index (clamped under CPI_CLAMP)
         const double c = fmin(fmax(cb, 0.0), static_cast<double>(Wb - 1));
         double fl = floor(c);
@@ -81,7 +78,7 @@ __global__ void count_kernel(CoordsGroupArgs g) {
     }
 }
 __device__ __forceinline__ void coords_block(double a, double b, double c_off, int boundary, int W, int Wb,
-                                             AxisTables tab, int ub, bool count, bool b_ok) {
+                                             AxisTables tab, int ub, bool b_ok) {
     const double c_a = (W - 1) / 2.0, c_b = (Wb - 1) / 2.0;
     const double bu = __dmul_rn(b, __dadd_rn(static_cast<double>(ub), -c_b));
     int lo = INT_MAX, hi = -1;
@@ -104,7 +101,6 @@ __device__ __forceinline__ void coords_block(double a, double b, double c_off, i
             t = __dadd_rn(c, -f);
             lo = min(lo, i0);
             hi = max(hi, i0 + 1);
-            if (count) atomicAdd(tab.cnt + x, 1);
         }
         tab.i0[static_cast<int64_t>(ub) * W + x] = ok ? i0 : -1;
         tab.t[static_cast<int64_t>(ub) * W + x] = t;
@@ -1011,15 +1007,6 @@ cudaError_t launch_refocus_coords_group(const CoordsGroupArgs& g, int n_fuse, cu
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     count_kernel<<<dim3(1, n_fuse, 2), threads, 0, st>>>(g);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_refocus_coords(double a, double b, double c_off, int boundary, int W, int Wb, AxisTables tab,
-                                  cudaStream_t st) {
-    cudaError_t e = cudaMemsetAsync(tab.cnt, 0, sizeof(int32_t) * W, st);
-    if (e != cudaSuccess) return e;
-    int threads = W >= 256 ? 256 : ((W + 31) / 32) * 32;
-    coords_kernel<<<Wb, threads, 0, st>>>(a, b, c_off, boundary, W, Wb, tab);
     return cudaGetLastError();
 }
 
