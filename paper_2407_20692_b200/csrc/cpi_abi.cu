@@ -73,7 +73,7 @@ struct cpi_ctx {
     cpi::AxisTables bxs{}, bys{};          // fractional-B path: B supports per u / v
     float* bws = nullptr;                  // fractional-B path: Gamma resampled onto the B lattice (lazy)
     size_t bws_bytes = 0;
-    double* T[cpi::kRefocusMaxFuse]{};
+    cpi::TElem* T[cpi::kRefocusMaxFuse]{};
     bool refocus_ready = false;
     int fuse = 4;                          // planes per Gamma pass in the TMA stage 1 (CPI_REFOCUS_FUSE)
     uint32_t* xpack = nullptr;             // packed x-tables [kRefocusMaxFuse][W_b][W_a]
@@ -742,7 +742,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
             cpi_status s = alloc_axis(c, c->xs[f], Wa, Wb);
             if (s == CPI_OK) s = alloc_axis(c, c->ys[f], Ha, Hb);
             if (s != CPI_OK) return s;
-            CK(c, cudaMalloc(&c->T[f], sizeof(double) * size_t(Wa) * Ha * Hb));
+            CK(c, cudaMalloc(&c->T[f], sizeof(cpi::TElem) * size_t(Wa) * Ha * Hb));
         }
         if (c->use_s1_tma) {
             CK(c, cudaMalloc(&c->xpack, sizeof(uint32_t) * size_t(Wa) * Wb * cpi::kRefocusMaxFuse));

@@ -71,7 +71,11 @@ cudaError_t launch_finalize(const int32_t* counts, int64_t ldc, int64_t rows, in
                             const int32_t* s_a_rows, const int32_t* s_b, double n, float* gamma,
                             int64_t ldg, cudaStream_t st);
 
-// KB5/KB6 refocusing.
+// KB5/KB6 refocusing.  T (the stage-1 output, [W_a][H_a][H_b] per plane) is stored in fp32:
+// the taps accumulate in fp32 per chunk and fp64 across chunks, and one rounding of the
+// finished sum adds <= 2^-24 of T(|Gamma|) <= 2^-24 M to a plane; it halves
+// the T traffic of both stages.
+using TElem = float;
 struct AxisTables {           // one axis (x with B-axis u, or y with B-axis v)
     int32_t* i0;              // [Wb][W]  lower interpolation index, -1 = sample skipped
     double* t;                // [Wb][W]  interpolation fraction
@@ -96,9 +100,9 @@ cudaError_t launch_refocus_coords_group(const CoordsGroupArgs& g, int n_fuse, cu
 // staged stage 1 with 2 x 2 corners per sample into T[x][m][n] for every (m, n), and a
 // warp-per-pixel stage 2 with 2 x 2 corners.  Row-major Gamma, contiguous row shards.
 cudaError_t launch_refocus_stage1_genb(const float* gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
-                                       int m_base, int m_count, AxisTables xs, AxisTables bx, double* T,
+                                       int m_base, int m_count, AxisTables xs, AxisTables bx, TElem* T,
                                        cudaStream_t st);
-cudaError_t launch_refocus_stage2_genb(const double* T, int Wa, int Ha, int Hb, int m_base, int m_count,
+cudaError_t launch_refocus_stage2_genb(const TElem* T, int Wa, int Ha, int Hb, int m_base, int m_count,
                                        AxisTables xs, AxisTables ys, AxisTables by, float* plane, cudaStream_t st);
 // General-B pre-pass (default route for fractional B): Gamma'(p; v, u) = bilinear of Gamma(p; ., .)
 // at the B support (by[v], bx[u]) for rows A pixels of P_b slots each (B order row-major or
@@ -108,7 +112,7 @@ cudaError_t launch_resample_b(const float* src, float* dst, int64_t rows, int Wb
                               AxisTables bx, AxisTables by, cudaStream_t st);
 cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
                                   int m_base, int m_count, AxisTables xs, AxisTables ys,
-                                  double* T, cudaStream_t st);
+                                  TElem* T, cudaStream_t st);
 // KB5 (TMA variant): warp-specialised, persistent, TMA-fed stage 1 over n_fuse (<= 4) planes
 // sharing one pass over Gamma.  Needs W_a <= 256 with W_a % 4 == 0, W_b % 4 == 0, W_b <= 512, H_b <= 256, the tensor maps of
 // Gamma (4D: u, v, j, m) and of the packed x-tables (3D uint32: x, u, plane slot).
@@ -122,7 +126,7 @@ bool stage1_tma_supported(int Wa, int Wb, int Hb);
 int stage1_vgroup(int Wa);   // B rows v per stage-1 tile (Gamma tensor-map box height)
 cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa, int Ha, int Wb, int Hb,
                                       int m_base, int m_count, int m_block, int m_stride, const AxisTables* xs,
-                                      const AxisTables* ys, double* const* T, const uint32_t* xblk, int num_sms,
+                                      const AxisTables* ys, TElem* const* T, const uint32_t* xblk, int num_sms,
                                       cudaStream_t st);
 // x-tables of a fused group packed for the TMA stage 1: uint32 j_rel << 23 | round(t * 2^23),
 // [n_fuse][Wb][Wa] (see refocus.cu), and xblk[n_fuse][ceil(Wb / 8)]: bit b set if some
@@ -142,7 +146,7 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 EncodeTiledFn encode_tiled_fn();
 
-cudaError_t launch_refocus_stage2(const double* T, int Wa, int Ha, int Hb, int m_base,
+cudaError_t launch_refocus_stage2(const TElem* T, int Wa, int Ha, int Hb, int m_base,
                                   int m_count, AxisTables xs, AxisTables ys, float* plane,
                                   cudaStream_t st);
 // Shard A rows (both stages): local A row l is global row m_base + (l / m_block) * m_stride
@@ -152,7 +156,7 @@ cudaError_t launch_refocus_stage2(const double* T, int Wa, int Ha, int Hb, int m
 bool stage2_staged_supported(int Ha);
 cudaError_t launch_pack_ytable_group(const AxisTables* ys, int n_fuse, int Ha, int Hb, uint32_t* ypack,
                                      cudaStream_t st);
-cudaError_t launch_refocus_stage2_group(double* const* T, int n_fuse, int Wa, int Ha, int Hb, int m_base, int m_count,
+cudaError_t launch_refocus_stage2_group(TElem* const* T, int n_fuse, int Wa, int Ha, int Hb, int m_base, int m_count,
                                         int m_block, int m_stride, const AxisTables* xs, const AxisTables* ys,
                                         const uint32_t* ypack, float* planes, cudaStream_t st);
 

@@ -126,7 +126,7 @@ __device__ __forceinline__ void coords_block(double a, double b, double c_off, i
 // grid (ceil(Hb / kVG), m_count, ceil(Wa / 256)); thread = output x.
 __global__ void __launch_bounds__(kS1Threads)
 stage1_kernel(const float* __restrict__ gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
-              int m_base, AxisTables xs, AxisTables ys, double* __restrict__ T) {
+              int m_base, AxisTables xs, AxisTables ys, TElem* __restrict__ T) {
     extern __shared__ float sm[];   // [kVG][nj][kPad]
     const int v0 = blockIdx.x * kVG;
     const int m = m_base + blockIdx.y;
@@ -193,7 +193,7 @@ stage1_kernel(const float* __restrict__ gamma, int64_t ldg, int Wa, int Ha, int 
         }
     }
     if (x < Wa) {
-        double* dst = T + (static_cast<int64_t>(x) * Ha + m) * Hb + v0;
+        TElem* dst = T + (static_cast<int64_t>(x) * Ha + m) * Hb + v0;
         for (int v = 0; v < nv; ++v)
             if (need & (1u << v)) dst[v] = acc[v];
     }
@@ -201,13 +201,13 @@ stage1_kernel(const float* __restrict__ gamma, int64_t ldg, int Wa, int Ha, int 
 
 // ---- KB6: stage 2 -----------------------------------------------------------------
 // One warp per output pixel (x, y); lanes stride over v; warp-shuffle fp64 reduction.
-__global__ void stage2_kernel(const double* __restrict__ T, int Wa, int Ha, int Hb, int m_lo,
+__global__ void stage2_kernel(const TElem* __restrict__ T, int Wa, int Ha, int Hb, int m_lo,
                               int m_hi, AxisTables xs, AxisTables ys, float* __restrict__ plane) {
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (gw >= static_cast<int64_t>(Wa) * Ha) return;
     const int x = static_cast<int>(gw % Wa), y = static_cast<int>(gw / Wa);
-    const double* Tx = T + static_cast<int64_t>(x) * Ha * Hb;
+    const TElem* Tx = T + static_cast<int64_t>(x) * Ha * Hb;
     double sum = 0.0;
     for (int v = lane; v < Hb; v += 32) {
         const int64_t ti = static_cast<int64_t>(v) * Ha + y;
@@ -310,7 +310,7 @@ struct S1Args {
     const int32_t* xhi[kRefocusMaxFuse];
     const int32_t* ylo[kRefocusMaxFuse];
     const int32_t* yhi[kRefocusMaxFuse];
-    double* T[kRefocusMaxFuse];
+    TElem* T[kRefocusMaxFuse];
     const uint32_t* xblk;                    // [F][n_chunks] x-block masks (OR-ed over F in smem)
     int gamma_5d;                            // Gamma map is 5D u-blocked (u%8, v, u/8, j, m)
 };
@@ -505,7 +505,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
             for (int i = 0; i < NI; ++i) {
                 const int x = xbase + 128 * i;
                 if (!kFullX && x >= a.Wa) continue;
-                double* dst = a.T[f] + (static_cast<int64_t>(x) * a.Ha + m) * a.Hb + v0;
+                TElem* dst = a.T[f] + (static_cast<int64_t>(x) * a.Ha + m) * a.Hb + v0;
 #pragma unroll
                 for (int s = 0; s < NS; ++s) {
                     const int v = vq + 2 * ((s + hi) & (NS - 1));
@@ -553,18 +553,19 @@ __global__ void pack_xtable_group_kernel(PackGroupArgs g, int Wa, int Wb, uint32
 
 // ---- KB6 (staged): stage 2 for a fused group of planes -------------------------------
 // grid (ceil(W_a / 2), F); CTA = 2 output columns x of one plane, thread = output row y
-// (H_a <= 256).  The CTA walks v in chunks of 8: it stages T[x][m][v0..v0+7] for every m
-// (64-byte coalesced row segments; rows outside the used band [lo_y(v), hi_y(v)] and outside
+// (H_a <= 256).  The CTA walks v in chunks of 16: it stages T[x][m][v0..v0+15] for every m
+// (64-byte coalesced fp32 row segments; rows outside the used band [lo_y(v), hi_y(v)] and outside
 // the caller's row shard [m_lo, m_hi) are stored as 0) transposed to [x][v][m], plus the
 // chunk's packed y-table rows; every thread then gathers its two taps per (x, v) from shared
-// memory.  The next chunk's loads are issued into registers before the current chunk is
-// consumed, so HBM latency overlaps the gathers.  T is read from HBM once per plane.
-constexpr int kS2VC = 8, kS2XB = 2, kS2Threads = 256, kS2MI = 256 / (kS2Threads / kS2VC);
+// memory (the pair interpolated in fp32, accumulated over v in fp64).  The next chunk's loads
+// are issued into registers before the current chunk is consumed, so HBM latency overlaps
+// the gathers.  T is read from HBM once per plane.
+constexpr int kS2VC = 16, kS2XB = 2, kS2Threads = 256, kS2MI = 256 / (kS2Threads / kS2VC);
 
 struct S2Args {
     int Wa, Ha, Hb;
     int m_base, m_count, m_block, m_stride;      // rows of T present: the shard's A rows (see S1Args)
-    const double* T[kRefocusMaxFuse];
+    const TElem* T[kRefocusMaxFuse];
     const int32_t* xcnt[kRefocusMaxFuse];
     const int32_t* ycnt[kRefocusMaxFuse];
     const int32_t* ylo[kRefocusMaxFuse];
@@ -578,16 +579,16 @@ stage2_staged_kernel(S2Args a) {
     extern __shared__ __align__(16) uint8_t s2_smem[];
     const int f = blockIdx.y, x0 = blockIdx.x * kS2XB;
     const int Ha = a.Ha, Hb = a.Hb, P = Ha + 2;           // staged row pitch (rows Ha, Ha+1 = 0)
-    double* ts = reinterpret_cast<double*>(s2_smem);                     // [kS2XB][kS2VC][P]
+    TElem* ts = reinterpret_cast<TElem*>(s2_smem);                       // [kS2XB][kS2VC][P]
     uint32_t* tab = reinterpret_cast<uint32_t*>(ts + kS2XB * kS2VC * P);  // [kS2VC][Ha]
-    const double* T = a.T[f];
+    const TElem* T = a.T[f];
     const uint32_t* yp = a.ypack + static_cast<int64_t>(f) * Hb * Ha;
     const int32_t* ylo = a.ylo[f];
     const int32_t* yhi = a.yhi[f];
-    for (int i = threadIdx.x; i < kS2XB * kS2VC * 2; i += blockDim.x) ts[(i >> 1) * P + Ha + (i & 1)] = 0.0;
+    for (int i = threadIdx.x; i < kS2XB * kS2VC * 2; i += blockDim.x) ts[(i >> 1) * P + Ha + (i & 1)] = 0.f;
     // loader role: thread = (vv = tid % 8, m = tid / 8 + 32 k), both x of the CTA
     const int vl = threadIdx.x & (kS2VC - 1), ml = threadIdx.x / kS2VC;
-    double pre[kS2XB][kS2MI];
+    TElem pre[kS2XB][kS2MI];
     uint32_t ptab[kS2MI];
     uint32_t present = 0;                          // bit k: this thread's row m = ml + 32 k is in the shard
 #pragma unroll
@@ -609,7 +610,7 @@ stage2_staged_kernel(S2Args a) {
 #pragma unroll
             for (int xb = 0; xb < kS2XB; ++xb) {
                 const int x = x0 + xb;
-                pre[xb][k] = ok && x < a.Wa ? __ldg(T + (static_cast<int64_t>(x) * Ha + m) * Hb + v) : 0.0;
+                pre[xb][k] = ok && x < a.Wa ? __ldg(T + (static_cast<int64_t>(x) * Ha + m) * Hb + v) : 0.f;
             }
             const int i = threadIdx.x + k * kS2Threads;               // table entry (vv, y)
             ptab[k] = i < nvalid ? __ldg(yp + static_cast<int64_t>(v0) * Ha + i) : (static_cast<uint32_t>(Ha) << 23);
@@ -639,12 +640,11 @@ stage2_staged_kernel(S2Args a) {
             for (int vv = 0; vv < kS2VC; ++vv) {
                 const uint32_t e = tab[vv * Ha + y];
                 const int m0 = static_cast<int>(e >> 23);
-                const double t = static_cast<double>(e & 0x7FFFFFu) * (1.0 / 8388608.0);
-                const double w0 = 1.0 - t;
+                const float t = static_cast<float>(e & 0x7FFFFFu) * (1.f / 8388608.f);   // exact
 #pragma unroll
                 for (int xb = 0; xb < kS2XB; ++xb) {
-                    const double* row = ts + (xb * kS2VC + vv) * P + m0;
-                    sum[xb] = fma(t, row[1], fma(w0, row[0], sum[xb]));
+                    const TElem* row = ts + (xb * kS2VC + vv) * P + m0;
+                    sum[xb] += static_cast<double>(fmaf(t, row[1] - row[0], row[0]));
                 }
             }
         }
@@ -687,7 +687,7 @@ constexpr int kGbCols = 10, kGbPad = 11, kGbMaxU = 8;
 
 __global__ void __launch_bounds__(kS1Threads)
 stage1_genb_kernel(const float* __restrict__ gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb, int m_base,
-                   AxisTables xs, AxisTables bx, double* __restrict__ T) {
+                   AxisTables xs, AxisTables bx, TElem* __restrict__ T) {
     extern __shared__ float sgb[];   // [kVG][nj][kGbPad]
     const int n0 = blockIdx.x * kVG;
     const int m = m_base + blockIdx.y;
@@ -750,19 +750,19 @@ stage1_genb_kernel(const float* __restrict__ gamma, int64_t ldg, int Wa, int Ha,
         u0 += nu;
     }
     if (x < Wa) {
-        double* dst = T + (static_cast<int64_t>(x) * Ha + m) * Hb + n0;
+        TElem* dst = T + (static_cast<int64_t>(x) * Ha + m) * Hb + n0;
         for (int v = 0; v < nv; ++v) dst[v] = acc[v];
     }
 }
 
 // Stage 2: one warp per output pixel (x, y); lanes over v; 2 x 2 corners (m, n) of T.
-__global__ void stage2_genb_kernel(const double* __restrict__ T, int Wa, int Ha, int Hb, int m_lo, int m_hi,
+__global__ void stage2_genb_kernel(const TElem* __restrict__ T, int Wa, int Ha, int Hb, int m_lo, int m_hi,
                                    AxisTables xs, AxisTables ys, AxisTables by, float* __restrict__ plane) {
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (gw >= static_cast<int64_t>(Wa) * Ha) return;
     const int x = static_cast<int>(gw % Wa), y = static_cast<int>(gw / Wa);
-    const double* Tx = T + static_cast<int64_t>(x) * Ha * Hb;
+    const TElem* Tx = T + static_cast<int64_t>(x) * Ha * Hb;
     double sum = 0.0;
     for (int v = lane; v < Hb; v += 32) {
         const int64_t ti = static_cast<int64_t>(v) * Ha + y;
@@ -974,7 +974,7 @@ cudaError_t launch_pack_ytable_group(const AxisTables* ys, int n_fuse, int Ha, i
     return cudaGetLastError();
 }
 
-cudaError_t launch_refocus_stage2_group(double* const* T, int n_fuse, int Wa, int Ha, int Hb, int m_base, int m_count,
+cudaError_t launch_refocus_stage2_group(TElem* const* T, int n_fuse, int Wa, int Ha, int Hb, int m_base, int m_count,
                                         int m_block, int m_stride, const AxisTables* xs, const AxisTables* ys,
                                         const uint32_t* ypack, float* planes, cudaStream_t st) {
     if (n_fuse < 1 || n_fuse > kRefocusMaxFuse || !stage2_staged_supported(Ha)) return cudaErrorInvalidValue;
@@ -987,7 +987,7 @@ cudaError_t launch_refocus_stage2_group(double* const* T, int n_fuse, int Wa, in
         a.T[f] = T[f]; a.xcnt[f] = xs[f].cnt; a.ycnt[f] = ys[f].cnt; a.ylo[f] = ys[f].lo; a.yhi[f] = ys[f].hi;
         a.plane[f] = planes + static_cast<int64_t>(f) * Ha * Wa;
     }
-    const size_t smem = sizeof(double) * kS2XB * kS2VC * (Ha + 2) + sizeof(uint32_t) * kS2VC * Ha;
+    const size_t smem = sizeof(TElem) * kS2XB * kS2VC * (Ha + 2) + sizeof(uint32_t) * kS2VC * Ha;
     static size_t attr = 0;
     if (smem > 48 * 1024 && smem > attr) {
         cudaError_t e = cudaFuncSetAttribute(stage2_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1011,7 +1011,7 @@ cudaError_t launch_refocus_coords_group(const CoordsGroupArgs& g, int n_fuse, cu
 }
 
 cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
-                                  int m_base, int m_count, AxisTables xs, AxisTables ys, double* T,
+                                  int m_base, int m_count, AxisTables xs, AxisTables ys, TElem* T,
                                   cudaStream_t st) {
     const size_t smem = static_cast<size_t>(kVG) * Wa * kPad * sizeof(float);
     static size_t attr = 0;
@@ -1068,7 +1068,7 @@ static cudaError_t launch_s1_f(int F, const Stage1Maps* maps, const S1Args& a, i
 
 cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa, int Ha, int Wb, int Hb,
                                       int m_base, int m_count, int m_block, int m_stride, const AxisTables* xs,
-                                      const AxisTables* ys, double* const* T, const uint32_t* xblk, int num_sms,
+                                      const AxisTables* ys, TElem* const* T, const uint32_t* xblk, int num_sms,
                                       cudaStream_t st) {
     if (n_fuse < 1 || n_fuse > kRefocusMaxFuse) return cudaErrorInvalidValue;
     S1Args a{};
@@ -1095,7 +1095,7 @@ cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa
                      : launch_s1_f<false, false, 256>(n_fuse, maps, a, grid, st);
 }
 
-cudaError_t launch_refocus_stage2(const double* T, int Wa, int Ha, int Hb, int m_base, int m_count,
+cudaError_t launch_refocus_stage2(const TElem* T, int Wa, int Ha, int Hb, int m_base, int m_count,
                                   AxisTables xs, AxisTables ys, float* plane, cudaStream_t st) {
     const int64_t warps = static_cast<int64_t>(Wa) * Ha;
     const int64_t blocks = (warps * 32 + 255) / 256;
@@ -1105,7 +1105,7 @@ cudaError_t launch_refocus_stage2(const double* T, int Wa, int Ha, int Hb, int m
 }
 
 cudaError_t launch_refocus_stage1_genb(const float* gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
-                                       int m_base, int m_count, AxisTables xs, AxisTables bx, double* T,
+                                       int m_base, int m_count, AxisTables xs, AxisTables bx, TElem* T,
                                        cudaStream_t st) {
     const size_t smem = static_cast<size_t>(kVG) * Wa * kGbPad * sizeof(float);
     static size_t attr = 0;
@@ -1120,7 +1120,7 @@ cudaError_t launch_refocus_stage1_genb(const float* gamma, int64_t ldg, int Wa, 
     return cudaGetLastError();
 }
 
-cudaError_t launch_refocus_stage2_genb(const double* T, int Wa, int Ha, int Hb, int m_base, int m_count,
+cudaError_t launch_refocus_stage2_genb(const TElem* T, int Wa, int Ha, int Hb, int m_base, int m_count,
                                        AxisTables xs, AxisTables ys, AxisTables by, float* plane, cudaStream_t st) {
     const int64_t warps = static_cast<int64_t>(Wa) * Ha;
     const int64_t blocks = (warps * 32 + 255) / 256;
