@@ -455,7 +455,7 @@ def main():
                "hbm_view": {"algorithmic_bytes_per_step": span, "achieved_gbs": s1_gbs, "peak_gbs": hbm,
                             "frac": s1_gbs / hbm if s1_gbs else None,
                             "note": "per-plane span bytes / time; > 1 possible because 4 planes share one HBM pass"},
-               "traffic": traffic.get("stage1_tma_kernel<1,4,1>", {}).get("bytes_per_launch"),
+               "traffic": traffic.get("stage1_tma_kernel<1,4,1,256>", {}).get("bytes_per_launch"),
                "traffic_note": ("ncu dram read + write bytes of one 4-plane launch (profiles/r01_traffic.json); "
                                 "achieved is per step (16 launches)")}
     dominant = roof_s1 if (s1_ms > gemm_ms) else roof_gemm
