@@ -65,16 +65,23 @@ __global__ void coords_group_kernel(CoordsGroupArgs g) {
         bt.t[ub] = __dadd_rn(c, -fl);
     }
 }
-// cnt[x] = number of B coordinates with a used sample at output coordinate x.
+// cnt[x] = number of B coordinates with a used sample at output coordinate x.  CTA = (32
+// outputs x, plane, axis); its 8 warps split the B coordinates and reduce in smem.
 __global__ void count_kernel(CoordsGroupArgs g) {
     const int ax = blockIdx.z, f = blockIdx.y;
     const int W = ax ? g.Ha : g.Wa, Wb = ax ? g.Hb : g.Wb;
     const AxisTables& t = ax ? g.ys[f] : g.xs[f];
-    for (int x = threadIdx.x; x < W; x += blockDim.x) {
-        int c = 0;
-#pragma unroll 8
-        for (int ub = 0; ub < Wb; ++ub) c += __ldg(t.i0 + static_cast<int64_t>(ub) * W + x) >= 0;
-        t.cnt[x] = c;
+    const int x = blockIdx.x * 32 + (threadIdx.x & 31), part = threadIdx.x >> 5, parts = blockDim.x >> 5;
+    __shared__ int sc[32][33];
+    int c = 0;
+    if (x < W)
+        for (int ub = part; ub < Wb; ub += parts) c += __ldg(t.i0 + static_cast<int64_t>(ub) * W + x) >= 0;
+    sc[threadIdx.x & 31][part] = c;
+    __syncthreads();
+    if (part == 0 && x < W) {
+        int s = 0;
+        for (int p = 0; p < parts; ++p) s += sc[threadIdx.x][p];
+        t.cnt[x] = s;
     }
 }
 __device__ __forceinline__ void coords_block(double a, double b, double c_off, int boundary, int W, int Wb,
@@ -1006,7 +1013,7 @@ cudaError_t launch_refocus_coords_group(const CoordsGroupArgs& g, int n_fuse, cu
     coords_group_kernel<<<dim3(nub, n_fuse, 2), threads, 0, st>>>(g);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    count_kernel<<<dim3(1, n_fuse, 2), threads, 0, st>>>(g);
+    count_kernel<<<dim3((wmax + 31) / 32, n_fuse, 2), 256, 0, st>>>(g);
     return cudaGetLastError();
 }
 
