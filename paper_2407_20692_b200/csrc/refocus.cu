@@ -471,12 +471,18 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                 for (int i = 0; i < NI; ++i) {
                     if (!((xb >> (8 * i)) & 1u)) continue;
                     if (!kFullX && xbase + 128 * i >= a.Wa) continue;
+                    // all x-table entries of this x block first, so entry decode overlaps taps
+                    uint32_t ent[kTUC][F];
+#pragma unroll
+                    for (int k = 0; k < kTUC; ++k)
+#pragma unroll
+                        for (int f = 0; f < F; ++f)
+                            ent[k][f] = sxs[f * C::kXEntries + ((k + xl) & (kTUC - 1)) * a.Wa + 128 * i];
 #pragma unroll
                     for (int k = 0; k < kTUC; ++k) {
                         const int uu = (k + xl) & (kTUC - 1);
 #pragma unroll
-                        for (int f = 0; f < F; ++f)
-                            s1_taps<NS, C::kRow>(part[f][i], sxs[f * C::kXEntries + uu * a.Wa + 128 * i], G + uu, voff);
+                        for (int f = 0; f < F; ++f) s1_taps<NS, C::kRow>(part[f][i], ent[k][f], G + uu, voff);
                     }
                 }
             } else {
