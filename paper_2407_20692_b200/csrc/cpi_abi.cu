@@ -472,8 +472,8 @@ cpi_status gemm_rows(cpi_ctx* c, int64_t row0, int64_t rows, float* gamma, cudaS
     epi.n = static_cast<double>(c->n_tot > 0 ? c->n_tot : 1);
     epi.inv_n2 = 1.0 / (epi.n * epi.n);
     {
-        static const int cache_mode = getenv("CPI_GEMM_CACHE") ? atoi(getenv("CPI_GEMM_CACHE")) : 0;
-        epi.cache = cache_mode;   // L2 policy knob of the CTA-pair GEMM (see kernels.h Epilogue::cache)
+        const char* cache_env = getenv("CPI_GEMM_CACHE");   // read per launch (A/B knob)
+        epi.cache = cache_env ? atoi(cache_env) : 0;   // L2 policy knob of the CTA-pair GEMM (see kernels.h Epilogue::cache)
     }
     TimedScope ts(c, KC_GEMM, st);
     cudaError_t e;

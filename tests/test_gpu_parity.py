@@ -91,6 +91,22 @@ def test_ragged_tiles_and_k_tails(variant, n):
     _assert_gamma(got["gamma"], want["gamma"])
 
 
+@pytest.mark.parametrize("knobs", [{"CPI_GEMM_1CTA": "1"}, {"CPI_GEMM_CACHE": "3"},
+                                   {"CPI_GEMM_CACHE": "1", "CPI_GEMM_1CTA": "1"}])
+@pytest.mark.parametrize("variant", ["tc", "fp4"])
+def test_gemm_knobs(knobs, variant, monkeypatch):
+    """GEMM implementation knobs: the 1-CTA int8 kernel (ignored by FP4, which
+    always runs CTA pairs) and the L2 cache-policy bits give the same exact sums."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    roi_a, roi_b = (3, 7, 50, 30), (261, 2, 20, 19)
+    fr = synth.bernoulli_frames(1300, 0.3, seed=77)
+    want = oracle.correlate(fr, roi_a, roi_b)
+    got = _gpu_sums(fr, roi_a, roi_b, variant)
+    _check_sums(got, want)
+    _assert_gamma(got["gamma"], want["gamma"])
+
+
 @pytest.mark.parametrize("variant", ["tc", "fp4"])
 def test_chaotic_light_dense_and_identities(variant):
     """Correlated (speckle) data with exact identities: same RoI on both arms -> S_ab
@@ -285,7 +301,8 @@ def test_refocus_fused_plane_groups(fuse, monkeypatch):
 
 
 @pytest.mark.parametrize("knobs", [{"CPI_STAGE1_SIMPLE": "1"}, {"CPI_STAGE2_SIMPLE": "1"},
-                                   {"CPI_STAGE1_SIMPLE": "1", "CPI_STAGE2_SIMPLE": "1"}, {"CPI_S1_NOSKIP": "1"}])
+                                   {"CPI_STAGE1_SIMPLE": "1", "CPI_STAGE2_SIMPLE": "1"}, {"CPI_S1_NOSKIP": "1"},
+                                   {"CPI_S1_L2PROMO": "0"}, {"CPI_S1_L2PROMO": "128"}, {"CPI_REFOCUS_FUSE": "3"}])
 @pytest.mark.parametrize("boundary", [0, 1])
 def test_refocus_fallback_kernels(knobs, boundary, monkeypatch):
     """The fallback kernels (plain stage 1 for W_a > 256, W_b % 4 != 0 or unaligned Gamma;
