@@ -140,7 +140,7 @@ def test_slicing_helpers():
     assert p.a_rows()[:6].tolist() == [12, 13, 14, 15, 44, 45]
 
 
-def _worker_tiles(rank, world, port, q):
+def _worker_tiles(rank, world, port, q, affine=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -148,21 +148,21 @@ def _worker_tiles(rank, world, port, q):
         frames = synth.bernoulli_frames(N, 0.3, seed=31)
         lo, hi = parallel.frame_slice(N, rank, world)
         res = parallel.correlate_and_refocus_tiles(OracleBackend(), frames[lo:hi], ROI_A, ROI_B, ALPHAS,
-                                                   min_panel_rows=1)
+                                                   min_panel_rows=1, affine=MAPS if affine else None)
         q.put((rank, res.n_tot, res.plan, res.gamma_rows.numpy(), res.planes.numpy()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_output_tile_sharding_matches_single_process(world):
+@pytest.mark.parametrize("world,affine", [(2, False), (4, False), (2, True)])
+def test_output_tile_sharding_matches_single_process(world, affine):
     """Output-tile sharding (SURVEY §8(e) control): frames all-gathered, each rank computes its
     own block-cyclic Gamma rows over all frames; rows equal the single-process oracle, planes
     merge by all-reduce."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker_tiles, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker_tiles, args=(r, world, port, q, affine)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=300) for _ in range(world)]
@@ -172,7 +172,7 @@ def test_output_tile_sharding_matches_single_process(world):
     frames = synth.bernoulli_frames(N, 0.3, seed=31)
     full = oracle.correlate(frames, ROI_A, ROI_B)
     G = full["gamma"].astype(np.float32)
-    want_planes = oracle.refocus(G, DIMS, ALPHAS)
+    want_planes = oracle.refocus_affine(G, DIMS, MAPS) if affine else oracle.refocus(G, DIMS, ALPHAS)
     covered = np.zeros(G.shape[0], dtype=int)
     for rank, n_tot, plan, g_rows, planes in out:
         assert n_tot == N
