@@ -294,16 +294,18 @@ __device__ __forceinline__ void s1_taps(uint64_t (&part)[NS / 2], uint32_t e, co
 
 // kJ = staged j rows (W_a <= kJ): 256, or 128 for A RoIs up to 128 wide, whose smaller stages
 // give a 4-deep ring; rows kJ, kJ + 1 of every stage stay zero (skipped samples).
-template <int F, int kJ = kTMaxJ>
+template <int F, int kJ = kTMaxJ, bool kGX = false>
 struct S1Cfg {
     static constexpr int kVG = stage1_vg(kJ), kRow = kVG * kTUC;   // staged j row: kVG v x 8 u
     static constexpr int kGFloats = (kJ + 2) * kRow;
-    static constexpr int kStages = F == 1 ? 3 : 2;   // both row capacities: ~66 KB Gamma stages
+    // both row capacities: ~66 KB Gamma stages; with the x-tables out of the ring (kGX) three
+    // Gamma stages fit for every F
+    static constexpr int kStages = (F == 1 || kGX) ? 3 : 2;
     // smem map (bytes): [Gamma stages (258 rows each)][x-table stages x F][span table]
     //                   [x-block masks][barriers]
     static constexpr int kOffX = kStages * kGFloats * 4;
     static constexpr int kXEntries = kTUC * kJ;             // x-table entries per (stage, plane) slot
-    static constexpr int kOffSpan = kOffX + kStages * F * kXEntries * 4;
+    static constexpr int kOffSpan = kOffX + (kGX ? 0 : kStages * F * kXEntries * 4);
     static constexpr int kOffXblk = kOffSpan + kTMaxChunks * 8;
     static constexpr int kOffYb = kOffXblk + kTMaxChunks * 4;   // int2 [F][H_b <= 256] y bands
     static constexpr int kOffBar = kOffYb + F * 256 * 8;
@@ -319,6 +321,7 @@ struct S1Args {
     const int32_t* yhi[kRefocusMaxFuse];
     TElem* T[kRefocusMaxFuse];
     const uint32_t* xblk;                    // [F][n_chunks] x-block masks (OR-ed over F in smem)
+    const uint32_t* xrot;                    // rotated global x-tables (kGX), see Stage1Maps
     int gamma_5d;                            // Gamma map is 5D u-blocked (u%8, v, u/8, j, m)
 };
 
@@ -339,10 +342,11 @@ __device__ __forceinline__ unsigned tile_mask(const int2* yband, int Hb, int m, 
     return need;
 }
 
-template <bool kFullX, int F, bool kSkip, int kJ>
+template <bool kFullX, int F, bool kSkip, int kJ, bool kGX>
 __global__ void __launch_bounds__(kTThreads, 1)
 stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_x, S1Args a) {
-    using C = S1Cfg<F, kJ>;
+    static_assert(!kGX || kSkip, "global x-tables only on the skip path");
+    using C = S1Cfg<F, kJ, kGX>;
     extern __shared__ __align__(1024) uint8_t s1_smem[];
     float* sg = reinterpret_cast<float*>(s1_smem);
     const uint32_t* sx = reinterpret_cast<const uint32_t*>(s1_smem + C::kOffX);
@@ -391,7 +395,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
     if (warp == kTConsumers) {
         if (lane == 0) {
             tma_prefetch_desc(&tm_g);
-            tma_prefetch_desc(&tm_x);
+            if constexpr (!kGX) tma_prefetch_desc(&tm_x);
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -405,7 +409,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                     if (sp.y < sp.x) continue;
                     const int nb = (sp.y - sp.x + kTJBox) / kTJBox;
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], nb * kTJBox * C::kRow * 4 + F * kTUC * a.Wa * 4);
+                    mbar_expect_tx(&full[stage], nb * kTJBox * C::kRow * 4 + (kGX ? 0 : F * kTUC * a.Wa * 4));
                     float* dst = sg + stage * C::kGFloats;
                     for (int b = 0; b < nb; ++b) {
                         if (a.gamma_5d)   // u-blocked Gamma: one 256-B segment per (j, chunk)
@@ -415,10 +419,11 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                             tma_load_4d(dst + b * kTJBox * C::kRow, &tm_g, &full[stage], c * kTUC, vg * C::kVG,
                                         sp.x + b * kTJBox, ml);
                     }
+                    if constexpr (!kGX)
 #pragma unroll
-                    for (int f = 0; f < F; ++f)
-                        tma_load_3d(s1_smem + C::kOffX + (stage * F + f) * C::kXEntries * 4, &tm_x, &full[stage], 0,
-                                    c * kTUC, f);
+                        for (int f = 0; f < F; ++f)
+                            tma_load_3d(s1_smem + C::kOffX + (stage * F + f) * C::kXEntries * 4, &tm_x, &full[stage], 0,
+                                        c * kTUC, f);
                     if (++stage == C::kStages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -434,6 +439,22 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
     for (int s = 0; s < NS; ++s) voff[s] = (vq + 2 * ((s + hi) & (NS - 1))) * kTUC;
     int stage = 0;
     uint32_t phase = 0;
+    // kGX: half h (slots 4h..4h+3) of the 8 x F entries of (chunk c, x block i) from the
+    // rotated global x-tables, one 16-byte load per plane; slot k is the entry of tap step k
+    const uint4* xr = reinterpret_cast<const uint4*>(a.xrot);
+    auto ld_half = [&](uint32_t (&e)[kTUC][F], int c, int i, int h) {
+        const int x = xbase + 128 * i;
+        if (c >= a.n_chunks || (!kFullX && x >= a.Wa)) return;
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+            const uint4 q = __ldg(xr + ((static_cast<int64_t>(f) * a.n_chunks + c) * a.Wa + x) * 2 + h);
+            e[4 * h][f] = q.x; e[4 * h + 1][f] = q.y; e[4 * h + 2][f] = q.z; e[4 * h + 3][f] = q.w;
+        }
+    };
+    auto next_chunk = [&](int c) {   // first chunk >= c with a non-empty span (n_chunks: none)
+        while (c < a.n_chunks && span[c].y < span[c].x) ++c;
+        return c;
+    };
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int ml = tile / a.n_vg, vg = tile - ml * a.n_vg;
         const int m = shard_row(a, ml), v0 = vg * C::kVG;
@@ -448,6 +469,15 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
             for (int i = 0; i < NI; ++i)
 #pragma unroll
                 for (int s = 0; s < NS; ++s) acc[f][i][s] = 0.0;
+        // kGX: each half of the next (chunk, x block) pair's entries is loaded as soon as the
+        // current pair's taps have consumed that half, so its L2 latency hides behind the
+        // other half's taps (no extra registers for a second entry set)
+        uint32_t ent[kTUC][F];
+        if constexpr (kGX) {
+            const int c0 = next_chunk(0);
+            ld_half(ent, c0, 0, 0);
+            ld_half(ent, c0, 0, 1);
+        }
         for (int c = 0; c < a.n_chunks; ++c) {
             const int2 sp = span[c];
             if (sp.y < sp.x) continue;
@@ -463,7 +493,26 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
 #pragma unroll
                     for (int p = 0; p < NS / 2; ++p) part[f][i][p] = 0ull;
             const uint32_t* sxs = sx + stage * F * C::kXEntries + xbase;
-            if constexpr (kSkip) {
+            if constexpr (kGX) {
+                const uint32_t xb = xblk[c] >> warp;
+                const int cn = next_chunk(c + 1);
+#pragma unroll
+                for (int i = 0; i < NI; ++i) {
+                    const bool act = ((xb >> (8 * i)) & 1u) && (kFullX || xbase + 128 * i < a.Wa);
+                    const int nc = i + 1 < NI ? c : cn, ni = i + 1 < NI ? i + 1 : 0;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (act)
+#pragma unroll
+                            for (int k = 4 * h; k < 4 * h + 4; ++k) {
+                                const int uu = (k + xl) & (kTUC - 1);
+#pragma unroll
+                                for (int f = 0; f < F; ++f) s1_taps<NS, C::kRow>(part[f][i], ent[k][f], G + uu, voff);
+                            }
+                        ld_half(ent, nc, ni, h);
+                    }
+                }
+            } else if constexpr (kSkip) {
                 // i-outer order with a warp-uniform skip of a 16-wide x block that has no used
                 // sample in this chunk for any plane of the group
                 const uint32_t xb = xblk[c] >> warp;
@@ -535,7 +584,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
 // 1 moves to the next row with t = 0), and skipped samples point at the zero rows
 // (j_rel = zrow = the stage's row capacity, t = 0).  t keeps 2^-23 resolution; t = 0 stays exact.
 __global__ void pack_xtable_group_kernel(PackGroupArgs g, int Wa, int Wb, uint32_t zrow, uint32_t* __restrict__ out,
-                                         uint32_t* __restrict__ xblk) {
+                                         uint32_t* __restrict__ xblk, uint32_t* __restrict__ xrot) {
     const int c = blockIdx.x, f = blockIdx.y, c0 = c * 8, n_chunks = gridDim.x;
     __shared__ uint32_t sblk;
     if (threadIdx.x == 0) sblk = 0;
@@ -545,6 +594,11 @@ __global__ void pack_xtable_group_kernel(PackGroupArgs g, int Wa, int Wb, uint32
     __syncthreads();
     for (int x = threadIdx.x; x < Wa; x += blockDim.x) {
         bool used = false;
+        // rotated copy for the global-x-table stage 1: slot k of (chunk, x) holds u = c0 + (k + x) % 8;
+        // columns past W_b point at the zero rows
+        uint32_t* rot = xrot ? xrot + ((static_cast<int64_t>(f) * n_chunks + c) * Wa + x) * 8 : nullptr;
+        if (rot)
+            for (int u = Wb; u < c0 + 8; ++u) rot[(u - c0 - x) & 7] = zrow << 23;
         for (int u = c0; u < c0 + 8 && u < Wb; ++u) {
             const int64_t idx = static_cast<int64_t>(u) * Wa + x;
             const int j = __ldg(g.i0[f] + idx);
@@ -557,6 +611,7 @@ __global__ void pack_xtable_group_kernel(PackGroupArgs g, int Wa, int Wb, uint32
                 used = true;
             }
             out[(static_cast<int64_t>(f) * Wb + u) * Wa + x] = e;
+            if (rot) rot[(u - c0 - x) & 7] = e;
         }
         if (used) atomicOr(&sblk, 1u << (x >> 4));
     }
@@ -1047,26 +1102,34 @@ bool stage1_tma_supported(int Wa, int Wb, int Hb) {
 }
 
 cudaError_t launch_pack_xtable_group(const AxisTables* xs, int n_fuse, int Wa, int Wb, uint32_t* xpack,
-                                     uint32_t* xblk, cudaStream_t st) {
+                                     uint32_t* xblk, uint32_t* xrot, cudaStream_t st) {
     PackGroupArgs g{};
     g.n = n_fuse;
     for (int f = 0; f < n_fuse; ++f) { g.i0[f] = xs[f].i0; g.t[f] = xs[f].t; g.lo[f] = xs[f].lo; }
     pack_xtable_group_kernel<<<dim3((Wb + 7) / 8, n_fuse), Wa >= 256 ? 256 : ((Wa + 31) / 32) * 32, 0, st>>>(
-        g, Wa, Wb, static_cast<uint32_t>(stage1_rows(Wa)), xpack, xblk);
+        g, Wa, Wb, static_cast<uint32_t>(stage1_rows(Wa)), xpack, xblk, xrot);
+    return cudaGetLastError();
+}
+
+template <bool kFullX, int F, bool kSkip, int kJ, bool kGX>
+static cudaError_t launch_s1_g(const Stage1Maps* maps, const S1Args& a, int grid, cudaStream_t st) {
+    using C = S1Cfg<F, kJ, kGX>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(stage1_tma_kernel<kFullX, F, kSkip, kJ, kGX>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    stage1_tma_kernel<kFullX, F, kSkip, kJ, kGX><<<grid, kTThreads, C::kSmem, st>>>(maps->gamma, maps->xtab, a);
     return cudaGetLastError();
 }
 
 template <bool kFullX, int F, bool kSkip, int kJ>
 static cudaError_t launch_s1(const Stage1Maps* maps, const S1Args& a, int grid, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(stage1_tma_kernel<kFullX, F, kSkip, kJ>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, S1Cfg<F, kJ>::kSmem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    stage1_tma_kernel<kFullX, F, kSkip, kJ><<<grid, kTThreads, S1Cfg<F, kJ>::kSmem, st>>>(maps->gamma, maps->xtab, a);
-    return cudaGetLastError();
+    if constexpr (kSkip)
+        if (a.xrot) return launch_s1_g<kFullX, F, true, kJ, true>(maps, a, grid, st);
+    return launch_s1_g<kFullX, F, kSkip, kJ, false>(maps, a, grid, st);
 }
 
 template <bool kFullX, bool kSkip, int kJ>
@@ -1091,6 +1154,7 @@ cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa
     a.n_vg = (Hb + stage1_vg(stage1_rows(Wa)) - 1) / stage1_vg(stage1_rows(Wa));
     a.n_chunks = (Wb + kTUC - 1) / kTUC;
     a.xblk = xblk;
+    a.xrot = maps->xrot;
     a.gamma_5d = maps->gamma_5d;
     for (int f = 0; f < n_fuse; ++f) {
         a.xlo[f] = xs[f].lo; a.xhi[f] = xs[f].hi; a.ylo[f] = ys[f].lo; a.yhi[f] = ys[f].hi; a.T[f] = T[f];
