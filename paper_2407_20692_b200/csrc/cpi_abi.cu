@@ -757,6 +757,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
                 CK(c, cudaMemset(c->xrot, 0, sizeof(uint32_t) * n));
             }
             c->s1maps.xrot = c->xrot;
+            if (const char* ev = getenv("CPI_S1_MC")) c->s1maps.x_multicast = atoi(ev) != 0;
             cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
             if (!enc) return fail(c, CPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
             const cuuint64_t dims[3] = {cuuint64_t(Wa), cuuint64_t(Wb), cuuint64_t(cpi::kRefocusMaxFuse)};

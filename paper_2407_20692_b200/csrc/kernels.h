@@ -125,6 +125,8 @@ struct Stage1Maps {
     // being staged in the TMA ring: [n_fuse][ceil(Wb / 8)][Wa][8] with the 8 u entries of a
     // (chunk, x) rotated so slot k holds u = (k + x) % 8; nullptr = staged x-tables
     const uint32_t* xrot = nullptr;
+    // CTA pairs share each chunk's x-tables by TMA multicast (knob CPI_S1_MC)
+    int x_multicast = 0;
 };
 bool stage1_tma_supported(int Wa, int Wb, int Hb);
 int stage1_vgroup(int Wa);   // B rows v per stage-1 tile (Gamma tensor-map box height)

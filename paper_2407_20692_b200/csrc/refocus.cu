@@ -16,6 +16,7 @@
 // Stage 1 streams Gamma from HBM once per plane: a CTA owns one A row m and 8 B rows v,
 // stages 8-column (u) slabs of the rows j it needs into padded shared memory (odd word
 // stride -> conflict-free gathers), and each thread owns one output x.
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstdlib>
@@ -342,11 +343,17 @@ __device__ __forceinline__ unsigned tile_mask(const int2* yband, int Hb, int m, 
     return need;
 }
 
-template <bool kFullX, int F, bool kSkip, int kJ, bool kGX>
+// kXM: x-table mode. 0 = staged by this CTA's TMA; 1 = read from global memory (kGX);
+// 2 = CTA pairs (cluster of 2) on two tiles in lockstep, each CTA's producer multicasting
+// half of the group's planes' tables into both CTAs' stages (kMC: half the L2 -> SM table
+// bytes per CTA; a stage is refilled once both CTAs' consumers have released it).
+template <bool kFullX, int F, bool kSkip, int kJ, int kXM>
 __global__ void __launch_bounds__(kTThreads, 1)
 stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_x, S1Args a) {
-    static_assert(!kGX || kSkip, "global x-tables only on the skip path");
+    constexpr bool kGX = kXM == 1, kMC = kXM == 2;
+    static_assert(kXM == 0 || kSkip, "global / multicast x-tables only on the skip path");
     using C = S1Cfg<F, kJ, kGX>;
+    const uint32_t rank = kMC ? cluster_ctarank() : 0;
     extern __shared__ __align__(1024) uint8_t s1_smem[];
     float* sg = reinterpret_cast<float*>(s1_smem);
     const uint32_t* sx = reinterpret_cast<const uint32_t*>(s1_smem + C::kOffX);
@@ -358,7 +365,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::kStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kTConsumers);
+            mbar_init(&empty[s], kMC ? 2 * kTConsumers : kTConsumers);
         }
         fence_mbar_init();
     }
@@ -390,7 +397,13 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
         xblk[c] = b;
     }
     __syncthreads();
+    if constexpr (kMC) cluster_sync();   // both CTAs' barriers initialised before any remote use
     const int n_tiles = a.m_count * a.n_vg;
+    // tile loop: one tile per CTA; kMC: tile pair p = (2p, 2p + 1) per cluster, the CTA of rank
+    // r on 2p + r (a missing last tile runs with an empty mask, keeping the pair in lockstep)
+    const int t_first = kMC ? 2 * static_cast<int>(blockIdx.x >> 1) + static_cast<int>(rank) : blockIdx.x;
+    const int t_step = gridDim.x;
+    const int t_end = kMC ? ((n_tiles + 1) & ~1) : n_tiles;
 
     if (warp == kTConsumers) {
         if (lane == 0) {
@@ -398,20 +411,24 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
             if constexpr (!kGX) tma_prefetch_desc(&tm_x);
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-                const int ml = tile / a.n_vg, vg = tile - ml * a.n_vg;
+            for (int tile = t_first; tile < t_end; tile += t_step) {
+                const int tl = min(tile, n_tiles - 1);
+                const int ml = tl / a.n_vg, vg = tl - ml * a.n_vg;
                 unsigned any = 0;
 #pragma unroll
                 for (int f = 0; f < F; ++f) any |= tile_mask(yband, a.Hb, shard_row(a, ml), vg * C::kVG, f, C::kVG);
-                if (!any) continue;
+                if (tile >= n_tiles) any = 0;
+                if (!kMC && !any) continue;
                 for (int c = 0; c < a.n_chunks; ++c) {
                     const int2 sp = span[c];
                     if (sp.y < sp.x) continue;
                     const int nb = (sp.y - sp.x + kTJBox) / kTJBox;
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], nb * kTJBox * C::kRow * 4 + (kGX ? 0 : F * kTUC * a.Wa * 4));
+                    if constexpr (kMC) mbar_wait_cluster(&empty[stage], phase ^ 1);
+                    else mbar_wait(&empty[stage], phase ^ 1);
+                    const int nbl = kMC && !any ? 0 : nb;   // kMC: an idle tile still takes the tables
+                    mbar_expect_tx(&full[stage], nbl * kTJBox * C::kRow * 4 + (kGX ? 0 : F * kTUC * a.Wa * 4));
                     float* dst = sg + stage * C::kGFloats;
-                    for (int b = 0; b < nb; ++b) {
+                    for (int b = 0; b < nbl; ++b) {
                         if (a.gamma_5d)   // u-blocked Gamma: one 256-B segment per (j, chunk)
                             tma_load_5d(dst + b * kTJBox * C::kRow, &tm_g, &full[stage], 0, vg * C::kVG, c,
                                         sp.x + b * kTJBox, ml);
@@ -419,7 +436,13 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                             tma_load_4d(dst + b * kTJBox * C::kRow, &tm_g, &full[stage], c * kTUC, vg * C::kVG,
                                         sp.x + b * kTJBox, ml);
                     }
-                    if constexpr (!kGX)
+                    if constexpr (kMC) {
+#pragma unroll
+                        for (int f = 0; f < F; ++f)
+                            if ((f & 1) == static_cast<int>(rank))
+                                tma_load_3d_mc(s1_smem + C::kOffX + (stage * F + f) * C::kXEntries * 4, &tm_x,
+                                               &full[stage], 0, c * kTUC, f, 3);
+                    } else if constexpr (!kGX)
 #pragma unroll
                         for (int f = 0; f < F; ++f)
                             tma_load_3d(s1_smem + C::kOffX + (stage * F + f) * C::kXEntries * 4, &tm_x, &full[stage], 0,
@@ -427,6 +450,10 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                     if (++stage == C::kStages) { stage = 0; phase ^= 1; }
                 }
             }
+        }
+        if constexpr (kMC) {
+            __syncwarp();
+            cluster_sync();   // no CTA exits while its peer may still multicast or arrive into it
         }
         return;
     }
@@ -455,13 +482,18 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
         while (c < a.n_chunks && span[c].y < span[c].x) ++c;
         return c;
     };
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int ml = tile / a.n_vg, vg = tile - ml * a.n_vg;
+    const uint32_t peer_empty0 = kMC ? mapa_rank(&empty[0], rank ^ 1u) : 0u;
+    for (int tile = t_first; tile < t_end; tile += t_step) {
+        const int tl = min(tile, n_tiles - 1);
+        const int ml = tl / a.n_vg, vg = tl - ml * a.n_vg;
         const int m = shard_row(a, ml), v0 = vg * C::kVG;
         unsigned mask[F], any = 0;
 #pragma unroll
-        for (int f = 0; f < F; ++f) { mask[f] = tile_mask(yband, a.Hb, m, v0, f, C::kVG); any |= mask[f]; }
-        if (!any) continue;
+        for (int f = 0; f < F; ++f) {
+            mask[f] = tile < n_tiles ? tile_mask(yband, a.Hb, m, v0, f, C::kVG) : 0u;
+            any |= mask[f];
+        }
+        if (!kMC && !any) continue;
         double acc[F][NI][NS];
 #pragma unroll
         for (int f = 0; f < F; ++f)
@@ -482,6 +514,15 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
             const int2 sp = span[c];
             if (sp.y < sp.x) continue;
             mbar_wait(&full[stage], phase);
+            if (kMC && !any) {   // idle tile of a pair: only release the stage (both CTAs)
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&empty[stage]);
+                    mbar_arrive_cluster(peer_empty0 + stage * 8);
+                }
+                if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+                continue;
+            }
             const float* G = sg + stage * C::kGFloats;
             // fp32 partial sums of this chunk as packed pairs (slots s = 2p, 2p + 1): the taps run
             // on FFMA2 (fma.rn.f32x2), lane-wise identical to two scalar fmaf in the same order
@@ -552,7 +593,10 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
             // (without it the refill could land while loads of this stage are still in flight).
             fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (lane == 0) {
+                mbar_arrive(&empty[stage]);
+                if constexpr (kMC) mbar_arrive_cluster(peer_empty0 + stage * 8);
+            }
 #pragma unroll
             for (int f = 0; f < F; ++f)
 #pragma unroll
@@ -575,6 +619,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                 }
             }
     }
+    if constexpr (kMC) cluster_sync();
 }
 
 // Packed x-tables of a fused group of F planes for the TMA stage 1 (W_a <= 256):
@@ -1111,25 +1156,49 @@ cudaError_t launch_pack_xtable_group(const AxisTables* xs, int n_fuse, int Wa, i
     return cudaGetLastError();
 }
 
-template <bool kFullX, int F, bool kSkip, int kJ, bool kGX>
+template <bool kFullX, int F, bool kSkip, int kJ, int kXM>
 static cudaError_t launch_s1_g(const Stage1Maps* maps, const S1Args& a, int grid, cudaStream_t st) {
-    using C = S1Cfg<F, kJ, kGX>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(stage1_tma_kernel<kFullX, F, kSkip, kJ, kGX>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    using C = S1Cfg<F, kJ, kXM == 1>;
+    auto kern = stage1_tma_kernel<kFullX, F, kSkip, kJ, kXM>;
+    static int max_clusters = -1;
+    if (max_clusters < 0) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        max_clusters = 0;
+        if (kXM == 2) {   // CTA pairs that fit at once (a GPC with an odd free SM count loses one)
+            cudaLaunchConfig_t q{};
+            cudaLaunchAttribute qa{};
+            qa.id = cudaLaunchAttributeClusterDimension;
+            qa.val.clusterDim.x = 2; qa.val.clusterDim.y = 1; qa.val.clusterDim.z = 1;
+            q.gridDim = dim3(2 * 148); q.blockDim = dim3(kTThreads); q.dynamicSmemBytes = C::kSmem;
+            q.attrs = &qa; q.numAttrs = 1;
+            e = cudaOccupancyMaxActiveClusters(&max_clusters, kern, &q);
+            if (e != cudaSuccess || max_clusters < 1) return e != cudaSuccess ? e : cudaErrorInvalidConfiguration;
+        }
     }
-    stage1_tma_kernel<kFullX, F, kSkip, kJ, kGX><<<grid, kTThreads, C::kSmem, st>>>(maps->gamma, maps->xtab, a);
-    return cudaGetLastError();
+    if constexpr (kXM == 2) {
+        const int pairs = (a.m_count * a.n_vg + 1) / 2;
+        const int clusters = std::min(std::min(max_clusters, (grid + 1) / 2), pairs);
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute at{};
+        at.id = cudaLaunchAttributeClusterDimension;
+        at.val.clusterDim.x = 2; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
+        cfg.gridDim = dim3(2 * clusters); cfg.blockDim = dim3(kTThreads); cfg.dynamicSmemBytes = C::kSmem;
+        cfg.stream = st; cfg.attrs = &at; cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, maps->gamma, maps->xtab, a);
+    } else {
+        kern<<<grid, kTThreads, C::kSmem, st>>>(maps->gamma, maps->xtab, a);
+        return cudaGetLastError();
+    }
 }
 
 template <bool kFullX, int F, bool kSkip, int kJ>
 static cudaError_t launch_s1(const Stage1Maps* maps, const S1Args& a, int grid, cudaStream_t st) {
-    if constexpr (kSkip)
-        if (a.xrot) return launch_s1_g<kFullX, F, true, kJ, true>(maps, a, grid, st);
-    return launch_s1_g<kFullX, F, kSkip, kJ, false>(maps, a, grid, st);
+    if constexpr (kSkip) {
+        if (a.xrot) return launch_s1_g<kFullX, F, true, kJ, 1>(maps, a, grid, st);
+        if (maps->x_multicast) return launch_s1_g<kFullX, F, true, kJ, 2>(maps, a, grid, st);
+    }
+    return launch_s1_g<kFullX, F, kSkip, kJ, 0>(maps, a, grid, st);
 }
 
 template <bool kFullX, bool kSkip, int kJ>
