@@ -504,11 +504,11 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
         // kGX: each half of the next (chunk, x block) pair's entries is loaded as soon as the
         // current pair's taps have consumed that half, so its L2 latency hides behind the
         // other half's taps (no extra registers for a second entry set)
-        uint32_t ent[kTUC][F];
+        uint32_t xent[kTUC][F];
         if constexpr (kGX) {
             const int c0 = next_chunk(0);
-            ld_half(ent, c0, 0, 0);
-            ld_half(ent, c0, 0, 1);
+            ld_half(xent, c0, 0, 0);
+            ld_half(xent, c0, 0, 1);
         }
         for (int c = 0; c < a.n_chunks; ++c) {
             const int2 sp = span[c];
@@ -548,9 +548,9 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                             for (int k = 4 * h; k < 4 * h + 4; ++k) {
                                 const int uu = (k + xl) & (kTUC - 1);
 #pragma unroll
-                                for (int f = 0; f < F; ++f) s1_taps<NS, C::kRow>(part[f][i], ent[k][f], G + uu, voff);
+                                for (int f = 0; f < F; ++f) s1_taps<NS, C::kRow>(part[f][i], xent[k][f], G + uu, voff);
                             }
-                        ld_half(ent, nc, ni, h);
+                        ld_half(xent, nc, ni, h);
                     }
                 }
             } else if constexpr (kSkip) {
