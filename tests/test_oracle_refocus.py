@@ -22,11 +22,13 @@ from tests._util import pack, unpack_np
 GOLDEN = Path(__file__).parent / "golden"
 
 
-def _dense_refocus_np(G, dims, alpha):
+def _dense_refocus_np(G, dims, alpha, clamp=False):
     """Independent dense evaluation (SPEC.md:307 'precompute all coordinates, interpolate
     from materialised arrays'): coordinate arrays for every (x,u) and (y,v), the
     bilinear interpolation on the A axes (B coordinates are integers under the default
-    map), skip_and_renormalize.  numpy, vectorised, no shared code with the C oracle."""
+    map), skip_and_renormalize, or (clamp=True, S:279 / SURVEY §8(c) c2 "CPI_CLAMP") each A
+    coordinate clamped into [0, W-1] with every sample counted.  numpy, vectorised, no shared
+    code with the C oracle."""
     Wa, Ha, Wb, Hb = dims
     G4 = np.asarray(G, dtype=np.float64).reshape(Ha, Wa, Hb, Wb)   # [m][j][v][u]
     cax, cay, cbx, cby = (Wa - 1) / 2, (Ha - 1) / 2, (Wb - 1) / 2, (Hb - 1) / 2
@@ -38,6 +40,9 @@ def _dense_refocus_np(G, dims, alpha):
     CY = (alpha * (y - cay)) + ((1 - alpha) * (v - cby)) + cay          # [y][v]
     VX = (CX >= 0) & (CX <= Wa - 1)
     VY = (CY >= 0) & (CY <= Ha - 1)
+    if clamp:
+        CX, CY = np.clip(CX, 0, Wa - 1), np.clip(CY, 0, Ha - 1)
+        VX, VY = np.ones_like(VX), np.ones_like(VY)
     J0 = np.clip(np.minimum(np.floor(CX), Wa - 2), 0, None).astype(int)
     M0 = np.clip(np.minimum(np.floor(CY), Ha - 2), 0, None).astype(int)
     TX, TY = CX - J0, CY - M0
@@ -190,6 +195,43 @@ def test_dense_materialised_oracle(alpha):
         np.testing.assert_allclose(R[0], D, rtol=0, atol=1e-12)
 
 
+@pytest.mark.parametrize("alpha", [0.6, 1.3, 2.0, -0.8])
+def test_dense_materialised_oracle_clamp(alpha):
+    """CPI_CLAMP branch on RANDOM Gamma vs the dense numpy evaluation
+    with its own clamp: counts are P_b everywhere and values agree within 1e-12.  Random data
+    detects a wrong clamp bound (e.g. W instead of W - 1), which constant data cannot."""
+    dims = (7, 6, 5, 4)
+    Wa, Ha, Wb, Hb = dims
+    G = np.random.default_rng(15).random((Wa * Ha, Wb * Hb)) - 0.5
+    R, cnt = oracle.refocus(G, dims, [alpha], boundary=oracle.BOUNDARY_CLAMP, return_counts=True)
+    D, dcnt = _dense_refocus_np(G, dims, alpha, clamp=True)
+    assert np.all(cnt[0] == Wb * Hb) and np.all(dcnt == Wb * Hb)
+    np.testing.assert_allclose(R[0], D, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("alpha", [0.6, 1.3, 2.0])
+def test_clamp_ramp_closed_form(alpha):
+    """Closed form of the clamp branch: on affine Gamma = a + b j' + c m' (primes: centred),
+    interpolation is exact and every sample counts, so
+        R(x, y) = a + b mean_u(clip(c_x(x,u), 0, W_a-1) - c_ax) + c mean_v(clip(c_y(y,v), 0, H_a-1) - c_ay)
+    with c_x, c_y the default map.  Linear extrapolation is exact on affine data too, so
+    a clamp to the wrong bound changes the coordinate means and fails here."""
+    Wa, Ha, Wb, Hb = 11, 9, 7, 6
+    a, b, c = 0.01, -0.003, 0.002
+    cax, cay, cbx, cby = (Wa - 1) / 2, (Ha - 1) / 2, (Wb - 1) / 2, (Hb - 1) / 2
+    j = np.arange(Wa) - cax
+    m = np.arange(Ha) - cay
+    G4 = (a + b * j[None, :, None, None] + c * m[:, None, None, None]) * np.ones((1, 1, Hb, Wb))
+    G = G4.reshape(Ha * Wa, Hb * Wb)
+    R = oracle.refocus(G, (Wa, Ha, Wb, Hb), [alpha], boundary=oracle.BOUNDARY_CLAMP)[0]
+    x, u = np.arange(Wa)[:, None], np.arange(Wb)[None, :]
+    y, v = np.arange(Ha)[:, None], np.arange(Hb)[None, :]
+    mx = np.clip(alpha * (x - cax) + (1 - alpha) * (u - cbx) + cax, 0, Wa - 1).mean(1) - cax
+    my = np.clip(alpha * (y - cay) + (1 - alpha) * (v - cby) + cay, 0, Ha - 1).mean(1) - cay
+    expect = a + b * mx[None, :] + c * my[:, None]
+    np.testing.assert_allclose(R, expect, rtol=0, atol=1e-15)
+
+
 def test_counts_are_separable():
     """The skip rule is per axis, so count(x,y) = cnt_x(x) * cnt_y(y) with
     cnt_x(x) = #{u : 0 <= alpha(x - c_a) + (1-alpha)(u - c_b) + c_a <= W_a - 1} (brute force)."""
@@ -256,12 +298,17 @@ def _coords_np(mp, dims):
     return CAX, CBX, CAY, CBY, VX, VY
 
 
-def _dense_affine_np(G, dims, mp):
+def _dense_affine_np(G, dims, mp, clamp=False):
     """Independent dense evaluation for a general map: materialised coordinates, the 16-corner
-    multilinear weights as separate per-axis 1D linear weights (numpy), skip_and_renormalize."""
+    multilinear weights as separate per-axis 1D linear weights (numpy), skip_and_renormalize
+    (or clamp=True: every coordinate clamped onto its lattice interval, every sample counted)."""
     Wa, Ha, Wb, Hb = dims
     G4 = np.asarray(G, dtype=np.float64).reshape(Ha, Wa, Hb, Wb)     # [m][j][n][k]
     CAX, CBX, CAY, CBY, VX, VY = _coords_np(mp, dims)
+    if clamp:
+        CAX, CBX = np.clip(CAX, 0, Wa - 1), np.clip(CBX, 0, Wb - 1)
+        CAY, CBY = np.clip(CAY, 0, Ha - 1), np.clip(CBY, 0, Hb - 1)
+        VX, VY = np.ones_like(VX), np.ones_like(VY)
 
     def lin(c, W):   # lower corner and weights of 1D linear interpolation on [0, W-1]
         i0 = np.clip(np.minimum(np.floor(c), W - 2), 0, None).astype(int)
@@ -340,6 +387,18 @@ def test_affine_exact_on_affine_gamma(mp):
                     for v in range(Hb) for u in range(Wb) if VX[x, u] and VY[y, v]]
             want = np.mean(vals) if vals else 0.0
             assert abs(R[y, x] - want) <= 1e-12 * (1 + abs(want))
+
+
+@pytest.mark.parametrize("mp", [MAPS[0], MAPS[2]])
+def test_affine_dense_materialised_clamp(mp):
+    """General maps under CPI_CLAMP vs the dense numpy evaluation with its own clamp (every
+    sample counts)."""
+    dims = (6, 5, 7, 4)
+    G = synth.random_gamma(30, 28, seed=9)
+    R, C = oracle.refocus_affine(G, dims, [mp], boundary=oracle.BOUNDARY_CLAMP, return_counts=True)
+    Rd, Cd = _dense_affine_np(G, dims, np.array(mp), clamp=True)
+    assert np.all(C[0] == 28) and np.all(Cd == 28)
+    np.testing.assert_allclose(R[0], Rd, rtol=1e-12, atol=1e-15)
 
 
 def test_affine_identity_map_is_angular_mean():
