@@ -37,6 +37,9 @@ sys.path.insert(0, str(ROOT))
 import synth  # noqa: E402
 
 METRIC = "frames/s into Gamma (and % int8 TC peak); refocused planes/s (% HBM BW)"
+# the step's default configuration (tests/test_gpu_fullsize.py runs exactly this against the oracle)
+STEP_VARIANT = "fp4"
+STEP_GAMMA_ORDER = "ublocked"
 
 
 def parse():
@@ -48,11 +51,11 @@ def parse():
     p.add_argument("--frames", type=int, default=10_000, help="frames per step per rank")
     p.add_argument("--planes", type=int, default=64, help="refocus planes per step")
     p.add_argument("--occupancy", type=float, default=0.05, help="Bernoulli f of the synthetic bits")
-    p.add_argument("--variant", default="fp4", choices=["tc", "popc", "fp4"],
+    p.add_argument("--variant", default=STEP_VARIANT, choices=["tc", "popc", "fp4"],
                    help="pair-sum GEMM: fp4 = tcgen05 kind::mxf4 on E2M1 0/1 (default, exact), "
                         "tc = kind::i8, popc = popcount(AND)")
     p.add_argument("--roi", default="full", choices=["full", "128", "tiny"])
-    p.add_argument("--gamma-order", default="ublocked", choices=["ublocked", "rowmajor"],
+    p.add_argument("--gamma-order", default=STEP_GAMMA_ORDER, choices=["ublocked", "rowmajor"],
                    help="column order of the step's Gamma (include/cpi.h CPI_GAMMA_UBLOCKED)")
     p.add_argument("--parallel-mode", default="rows", choices=["rows", "tiles"],
                    help="multi-GPU: rows = frame sharding + panelised reduce-scatter (north_star); tiles = "
@@ -61,7 +64,6 @@ def parse():
                    help="run the frame-sharded multi-GPU pipeline (NCCL) even at one rank (tests its code path)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-rows", type=int, default=0, help="(unused; the sample size follows the core count)")
     p.add_argument("--cpu-pixels", type=int, default=256, help="oracle sample: refocused output pixels")
     return p.parse_args()
 
@@ -318,7 +320,7 @@ def main():
 
     if not use_dist:
         ctx = Context(roi_a, roi_b, n, device=local, variant=args.variant,
-                      gamma_blocked=args.gamma_order == "ublocked")
+                      gamma_order=args.gamma_order)
         gamma = ctx.new_gamma()
         planes = ctx.new_planes(args.planes)
     else:
@@ -326,7 +328,7 @@ def main():
         # block-cyclic Gamma row ownership, shard refocus, plane all-reduce
         tiles = args.parallel_mode == "tiles"
         backend = parallel.CudaBackend(roi_a, roi_b, n * world if tiles else n, device=local, variant=args.variant,
-                                       gamma_blocked=args.gamma_order == "ublocked", keep_counts=not tiles)
+                                       gamma_order=args.gamma_order, keep_counts=not tiles)
         ctx = backend.ctx
     planes_host = torch.empty((args.planes, Ha, Wa), dtype=torch.float32).pin_memory()
 
@@ -464,7 +466,7 @@ def main():
     # region, not part of value)
     int8_side = None
     if args.variant == "fp4" and not use_dist:
-        c8 = Context(roi_a, roi_b, n, device=local, variant="tc", gamma_blocked=args.gamma_order == "ublocked")
+        c8 = Context(roi_a, roi_b, n, device=local, variant="tc", gamma_order=args.gamma_order)
         for it in range(5):
             if it == 2:
                 c8.set_timing(True)
@@ -481,7 +483,7 @@ def main():
                      "note": "same frames, epilogue and Gamma, timed after the step loop; not part of value"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(frames_np, roi_a, roi_b, alphas, args.cpu_rows, args.cpu_pixels, args.planes)
+        cpu = cpu_baseline(frames_np, roi_a, roi_b, alphas, 0, args.cpu_pixels, args.planes)
     out = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",

@@ -16,6 +16,8 @@ from . import _lib
 from ._lib import CpiError
 
 FRAME_W, FRAME_H = 512, 256   # SwissSPAD2 frame
+# B pixel (Gamma column) orders, include/cpi.h: row-major q = v W_b + u, or u-blocked
+GAMMA_ORDERS = {"rowmajor": 0, "ublocked": _lib.CPI_GAMMA_UBLOCKED}
 
 
 def _torch():
@@ -28,15 +30,18 @@ class Context:
 
     def __init__(self, roi_a, roi_b, max_frames: int, *, width: int = FRAME_W, height: int = FRAME_H,
                  bit_order: int = _lib.CPI_LSB_FIRST, device: int = 0, variant: str = "tc",
-                 keep_counts: bool = False, gamma_blocked: bool = False):
+                 keep_counts: bool = False, gamma_blocked: bool = False, gamma_order: Optional[str] = None):
         self._lib = _lib.load()
         if variant not in ("tc", "popc", "fp4"):
             raise ValueError("variant must be 'tc', 'popc' or 'fp4'")
         flags = {"tc": _lib.CPI_VARIANT_TC, "popc": _lib.CPI_VARIANT_POPC, "fp4": _lib.CPI_VARIANT_FP4}[variant]
         if keep_counts:
             flags |= _lib.CPI_KEEP_COUNTS
-        if gamma_blocked:     # u-blocked Gamma column order (include/cpi.h CPI_GAMMA_UBLOCKED)
-            flags |= _lib.CPI_GAMMA_UBLOCKED
+        if gamma_order is None:
+            gamma_order = "ublocked" if gamma_blocked else "rowmajor"
+        if gamma_order not in GAMMA_ORDERS:
+            raise ValueError(f"gamma_order must be one of {sorted(GAMMA_ORDERS)}")
+        flags |= GAMMA_ORDERS[gamma_order]   # B pixel (Gamma column) order, include/cpi.h
         cfg = _lib.Config(_lib.Layout(width, height, bit_order), _lib.Roi(*roi_a), _lib.Roi(*roi_b),
                           int(max_frames), int(device), flags)
         h = ctypes.c_void_p()
@@ -53,7 +58,8 @@ class Context:
         self.max_frames = int(max_frames)
         self.variant = variant
         self.keep_counts = keep_counts
-        self.gamma_blocked = gamma_blocked
+        self.gamma_order = gamma_order
+        self.gamma_blocked = gamma_order == "ublocked"
         self._keep = []   # host buffers that must outlive an async copy
 
     # -- helpers ----------------------------------------------------------------------
@@ -238,10 +244,10 @@ class Context:
 
     def b_index(self):
         """Index of every B pixel q = v * W_b + u in S_b and in the columns of S_ab / Gamma
-        (identity unless gamma_blocked, include/cpi.h CPI_GAMMA_UBLOCKED)."""
+        (identity for the row-major order, include/cpi.h CPI_GAMMA_UBLOCKED)."""
         Wb, Hb = self.roi_b[2], self.roi_b[3]
         q = np.arange(Wb * Hb)
-        if not self.gamma_blocked:
+        if self.gamma_order == "rowmajor":
             return q
         v, u = q // Wb, q % Wb
         return (u // 8) * (8 * Hb) + 8 * v + (u % 8)

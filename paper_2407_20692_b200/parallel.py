@@ -231,12 +231,12 @@ class CudaBackend:
     (cpi_counts_dev views, no copies)."""
 
     def __init__(self, roi_a, roi_b, max_frames: int, device: int = 0, variant: str = "tc",
-                 gamma_blocked: bool = False, keep_counts: bool = True):
-        """gamma_blocked: B pixels in the u-blocked order (faster refocusing); S_b and the
-        columns of ShardResult.gamma_rows then follow ctx.b_index()."""
+                 gamma_blocked: bool = False, keep_counts: bool = True, gamma_order=None):
+        """gamma_order (or gamma_blocked = "ublocked"): the B pixel order (faster refocusing);
+        S_b and the columns of ShardResult.gamma_rows then follow ctx.b_index()."""
         from .cpi import Context
         self.ctx = Context(roi_a, roi_b, max_frames, device=device, variant=variant, keep_counts=keep_counts,
-                           gamma_blocked=gamma_blocked)
+                           gamma_blocked=gamma_blocked, gamma_order=gamma_order)
         self.device = torch.device(f"cuda:{device}")
         self.roi_a = roi_a
         self.row_align = self.ctx.row_align()

@@ -38,12 +38,26 @@ def _popc_halves(frames):
     return popc[frames[:, :, 0:32]].sum(axis=(1, 2)), popc[frames[:, :, 32:64]].sum(axis=(1, 2))
 
 
-def test_fullsize_gamma_bench_configuration(frames, oracle_rows):
+def _bench_step_config():
+    """The GEMM variant and Gamma column order bench.py's step runs by default."""
+    import bench
+    return bench.STEP_VARIANT, bench.STEP_GAMMA_ORDER
+
+
+@pytest.mark.parametrize("cfg", ["bench", "tc-rowmajor"])
+def test_fullsize_gamma_bench_configuration(frames, oracle_rows, cfg):
+    """cfg = "bench": the exact configuration bench.py times (its default GEMM variant and Gamma
+    column order, fused Gamma epilogue, no kept counts, the 64-plane stack through the fused
+    stage-1 groups); "tc-rowmajor": kind::i8 with row-major Gamma.  Gamma columns are mapped
+    back to q = v * W_b + u with ctx.b_index() before comparing with the oracle."""
     from paper_2407_20692_b200 import Context
-    ctx = Context(synth.ROI_FULL_A, synth.ROI_FULL_B, 10_000)       # bench: no kept counts
+    variant, order = _bench_step_config() if cfg == "bench" else ("tc", "rowmajor")
+    ctx = Context(synth.ROI_FULL_A, synth.ROI_FULL_B, 10_000, variant=variant,
+                  gamma_order=order)                                   # bench: no kept counts
     ctx.load_frames(torch.from_numpy(frames).cuda())
     g = ctx.correlate(ctx.new_gamma())
-    got = g[torch.from_numpy(ROWS).cuda()].cpu().numpy().astype(np.float64)
+    bidx = torch.from_numpy(ctx.b_index()).cuda()
+    got = g[torch.from_numpy(ROWS).cuda()][:, bidx].cpu().numpy().astype(np.float64)
     want = oracle_rows["gamma"]
     zero = want == 0
     assert np.all(got[zero] == 0)
@@ -64,7 +78,7 @@ def test_fullsize_gamma_bench_configuration(frames, oracle_rows):
     rng = np.random.default_rng(3)
     pix = np.stack([rng.integers(0, 256, 24), rng.integers(0, 256, 24)], 1)
     pix[:4] = [[0, 0], [255, 255], [0, 255], [128, 127]]
-    G = g.cpu().numpy()
+    G = g[:, bidx].cpu().numpy()        # row-major B order for the oracle
     del g
     R = oracle.refocus(G, (256, 256, 256, 256), alphas[sel], pixels=pix)
     M = oracle.refocus(np.abs(G), (256, 256, 256, 256), alphas[sel], pixels=pix)
