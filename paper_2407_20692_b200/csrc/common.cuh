@@ -303,12 +303,14 @@ __host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
 // exact integer; it is formed
 //   * in int32 when N <= 46340 (|N*s - sa*sb| <= N^2 < 2^31), converted once to fp32 and
 //     multiplied by fp32(1/N^2): three roundings, <= 1.8e-7 relative;
-//   * otherwise from exact fp64 products (all terms < 2^53), one fp64 multiply by 1/N^2 and
-//     one rounding to fp32: <= 6e-8 relative.
+//   * otherwise in int64 (|N*s - sa*sb| <= N^2 < 2^62 for N < 2^31), converted once to fp64
+//     (exact below 2^53, else one rounding), one fp64 multiply by 1/N^2 and one rounding to
+//     fp32: <= 6e-8 relative.
 // An exact zero numerator gives +0 on both paths.
 struct GammaScale {
     int small;          // N <= 46340: int32 path
     int32_t n_i;        // N
+    int64_t n_l;        // N
     float inv_n2_f;     // fp32(1 / N^2)
     double n_d;         // N
     double inv_n2_d;    // fp64(1 / N^2)
@@ -319,6 +321,7 @@ __host__ __device__ inline GammaScale make_gamma_scale(double n) {
     GammaScale g;
     g.small = n <= kGammaInt32MaxN ? 1 : 0;
     g.n_i = g.small ? static_cast<int32_t>(n) : 0;
+    g.n_l = static_cast<int64_t>(n);
     g.n_d = n;
     g.inv_n2_d = 1.0 / (n * n);
     g.inv_n2_f = static_cast<float>(g.inv_n2_d);
@@ -330,9 +333,8 @@ __device__ __forceinline__ float gamma_entry_t(int32_t s, int32_t sa, int32_t sb
         const int32_t num = g.n_i * s - sa * sb;
         return __fmul_rn(__int2float_rn(num), g.inv_n2_f);
     } else {
-        const double num = __fma_rn(static_cast<double>(s), g.n_d,
-                                    -__dmul_rn(static_cast<double>(sa), static_cast<double>(sb)));
-        return __double2float_rn(__dmul_rn(num, g.inv_n2_d));
+        const long long num = static_cast<long long>(g.n_l) * s - static_cast<long long>(sa) * sb;
+        return __double2float_rn(__dmul_rn(__ll2double_rn(num), g.inv_n2_d));
     }
 }
 __device__ __forceinline__ float gamma_entry(int32_t s, int32_t sa, int32_t sb, const GammaScale& g) {

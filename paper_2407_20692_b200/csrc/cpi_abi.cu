@@ -77,7 +77,6 @@ struct cpi_ctx {
     bool refocus_ready = false;
     int fuse = 4;                          // planes per Gamma pass in the TMA stage 1 (CPI_REFOCUS_FUSE)
     uint32_t* xpack = nullptr;             // packed x-tables [kRefocusMaxFuse][W_b][W_a]
-    uint32_t* xrot = nullptr;              // rotated global x-tables (Stage1Maps::xrot), or nullptr
     uint32_t* ypack = nullptr;             // packed y-tables [kRefocusMaxFuse][H_b][H_a]
     uint32_t* xblk = nullptr;              // x-block masks [kRefocusMaxFuse][W_b / 8]
     bool use_s2_staged = false;
@@ -214,7 +213,6 @@ void free_all(cpi_ctx* c) {
         cudaFree(c->T[f]);
     }
     cudaFree(c->xpack);
-    cudaFree(c->xrot);
     cudaFree(c->ypack);
     cudaFree(c->xblk);
     cudaFree(c->gamma_ws);
@@ -420,6 +418,8 @@ namespace {
 // single-pixel sums and frame count to the totals.
 cpi_status expand_batch(cpi_ctx* c, cudaStream_t st) {
     const int64_t n = c->n_cur;
+    if (c->n_tot + n >= (int64_t(1) << 31))   // int32 S_a, S_b, S_ab and counts (include/cpi.h)
+        return fail(c, CPI_ERR_CAPACITY, "N_TOT would reach %lld >= 2^31 (int32 sums)", (long long)(c->n_tot + n));
     const cpi_layout& L = c->cfg.layout;
     const int64_t k_pad = round_up(n, c->k_align);
     const int mode = c->popc ? cpi::kExpandBits : c->fp4 ? cpi::kExpandE2M1 : cpi::kExpandU8;
@@ -750,14 +750,6 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
             CK(c, cudaMalloc(&c->xpack, sizeof(uint32_t) * size_t(Wa) * Wb * cpi::kRefocusMaxFuse));
             CK(c, cudaMemset(c->xpack, 0, sizeof(uint32_t) * size_t(Wa) * Wb * cpi::kRefocusMaxFuse));
             CK(c, cudaMalloc(&c->xblk, sizeof(uint32_t) * size_t((Wb + 7) / 8) * cpi::kRefocusMaxFuse));
-            // stage-1 x-tables read from global memory instead of the TMA ring (knob CPI_S1_GX)
-            if (const char* ev = getenv("CPI_S1_GX"); ev && atoi(ev) != 0) {
-                const size_t n = size_t((Wb + 7) / 8) * Wa * 8 * cpi::kRefocusMaxFuse;
-                CK(c, cudaMalloc(&c->xrot, sizeof(uint32_t) * n));
-                CK(c, cudaMemset(c->xrot, 0, sizeof(uint32_t) * n));
-            }
-            c->s1maps.xrot = c->xrot;
-            if (const char* ev = getenv("CPI_S1_MC")) c->s1maps.x_multicast = atoi(ev) != 0;
             cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
             if (!enc) return fail(c, CPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
             const cuuint64_t dims[3] = {cuuint64_t(Wa), cuuint64_t(Wb), cuuint64_t(cpi::kRefocusMaxFuse)};
@@ -900,7 +892,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
             e = cpi::launch_refocus_coords_group(cg, nf, st);
             c->launches += 2;
             if (e == cudaSuccess && tma_now) {
-                e = cpi::launch_pack_xtable_group(c->xs, nf, Wa, Wb, c->xpack, c->xblk, c->xrot, st);
+                e = cpi::launch_pack_xtable_group(c->xs, nf, Wa, Wb, c->xpack, c->xblk, st);
                 c->launches += 1;
             }
             if (e == cudaSuccess && c->use_s2_staged) {

@@ -186,13 +186,9 @@ int gemm_tc_block_n() { return BN; }
 cudaError_t launch_gemm_tc(const CUtensorMap* tma_a, const CUtensorMap* tma_b, int m_tiles,
                            int n_tiles, int k_blocks, const Epilogue& epi, int num_sms,
                            cudaStream_t st) {
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_i8_tc_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-        if (e != cudaSuccess) return e;
-        attr_done = true;
-    }
+    // the attribute is per device: set it before every launch (a host-side call, negligible)
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e != cudaSuccess) return e;
     const int tiles = m_tiles * n_tiles;
     const int grid = tiles < num_sms ? tiles : num_sms;
     gemm_i8_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(*tma_a, *tma_b, m_tiles, n_tiles,

@@ -238,13 +238,10 @@ int gemm_f4_box_rows_b() { return Tc2<true>::HN; }
 template <bool kF4>
 static cudaError_t launch_tc2(const CUtensorMap* tma_a, const CUtensorMap* tma_b, int m_tiles, int n_tiles,
                               int k_blocks, const Epilogue& epi, int num_sms, cudaStream_t st) {
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_i8_tc2_kernel<kF4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             Tc2<kF4>::kSmemBytes);
-        if (e != cudaSuccess) return e;
-        attr_done = true;
-    }
+    // the attribute is per device: set it before every launch (a host-side call, negligible)
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_tc2_kernel<kF4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Tc2<kF4>::kSmemBytes);
+    if (e != cudaSuccess) return e;
     const int tiles = m_tiles * n_tiles;
     int pairs = num_sms / 2;
     if (tiles < pairs) pairs = tiles;

@@ -121,12 +121,6 @@ struct Stage1Maps {
     CUtensorMap gamma;       // 4D (u, v, j, m) row-major Gamma, or 5D (u%8, v, u/8, j, m) u-blocked
     CUtensorMap xtab;
     int gamma_5d = 0;
-    // x-tables read by the consumers straight from global memory (L2-resident) instead of
-    // being staged in the TMA ring: [n_fuse][ceil(Wb / 8)][Wa][8] with the 8 u entries of a
-    // (chunk, x) rotated so slot k holds u = (k + x) % 8; nullptr = staged x-tables
-    const uint32_t* xrot = nullptr;
-    // CTA pairs share each chunk's x-tables by TMA multicast (knob CPI_S1_MC)
-    int x_multicast = 0;
 };
 bool stage1_tma_supported(int Wa, int Wb, int Hb);
 int stage1_vgroup(int Wa);   // B rows v per stage-1 tile (Gamma tensor-map box height)
@@ -144,7 +138,7 @@ struct PackGroupArgs {
     const int32_t* lo[kRefocusMaxFuse];
 };
 cudaError_t launch_pack_xtable_group(const AxisTables* xs, int n_fuse, int Wa, int Wb, uint32_t* xpack,
-                                     uint32_t* xblk, uint32_t* xrot, cudaStream_t st);
+                                     uint32_t* xblk, cudaStream_t st);
 // driver entry point cuTensorMapEncodeTiled (nullptr if unavailable)
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,

@@ -295,18 +295,18 @@ __device__ __forceinline__ void s1_taps(uint64_t (&part)[NS / 2], uint32_t e, co
 
 // kJ = staged j rows (W_a <= kJ): 256, or 128 for A RoIs up to 128 wide, whose smaller stages
 // give a 4-deep ring; rows kJ, kJ + 1 of every stage stay zero (skipped samples).
-template <int F, int kJ = kTMaxJ, bool kGX = false>
+template <int F, int kJ = kTMaxJ>
 struct S1Cfg {
     static constexpr int kVG = stage1_vg(kJ), kRow = kVG * kTUC;   // staged j row: kVG v x 8 u
     static constexpr int kGFloats = (kJ + 2) * kRow;
-    // both row capacities: ~66 KB Gamma stages; with the x-tables out of the ring (kGX) three
-    // Gamma stages fit for every F
-    static constexpr int kStages = (F == 1 || kGX) ? 3 : 2;
+    // both row capacities: ~66 KB Gamma stages (three fit next to one plane's x-tables, two next
+    // to 2-4 planes' tables)
+    static constexpr int kStages = F == 1 ? 3 : 2;
     // smem map (bytes): [Gamma stages (258 rows each)][x-table stages x F][span table]
     //                   [x-block masks][barriers]
     static constexpr int kOffX = kStages * kGFloats * 4;
     static constexpr int kXEntries = kTUC * kJ;             // x-table entries per (stage, plane) slot
-    static constexpr int kOffSpan = kOffX + (kGX ? 0 : kStages * F * kXEntries * 4);
+    static constexpr int kOffSpan = kOffX + kStages * F * kXEntries * 4;
     static constexpr int kOffXblk = kOffSpan + kTMaxChunks * 8;
     static constexpr int kOffYb = kOffXblk + kTMaxChunks * 4;   // int2 [F][H_b <= 256] y bands
     static constexpr int kOffBar = kOffYb + F * 256 * 8;
@@ -322,7 +322,6 @@ struct S1Args {
     const int32_t* yhi[kRefocusMaxFuse];
     TElem* T[kRefocusMaxFuse];
     const uint32_t* xblk;                    // [F][n_chunks] x-block masks (OR-ed over F in smem)
-    const uint32_t* xrot;                    // rotated global x-tables (kGX), see Stage1Maps
     int gamma_5d;                            // Gamma map is 5D u-blocked (u%8, v, u/8, j, m)
 };
 
@@ -343,17 +342,10 @@ __device__ __forceinline__ unsigned tile_mask(const int2* yband, int Hb, int m, 
     return need;
 }
 
-// kXM: x-table mode. 0 = staged by this CTA's TMA; 1 = read from global memory (kGX);
-// 2 = CTA pairs (cluster of 2) on two tiles in lockstep, each CTA's producer multicasting
-// half of the group's planes' tables into both CTAs' stages (kMC: half the L2 -> SM table
-// bytes per CTA; a stage is refilled once both CTAs' consumers have released it).
-template <bool kFullX, int F, bool kSkip, int kJ, int kXM>
+template <bool kFullX, int F, bool kSkip, int kJ>
 __global__ void __launch_bounds__(kTThreads, 1)
 stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_x, S1Args a) {
-    constexpr bool kGX = kXM == 1, kMC = kXM == 2;
-    static_assert(kXM == 0 || kSkip, "global / multicast x-tables only on the skip path");
-    using C = S1Cfg<F, kJ, kGX>;
-    const uint32_t rank = kMC ? cluster_ctarank() : 0;
+    using C = S1Cfg<F, kJ>;
     extern __shared__ __align__(1024) uint8_t s1_smem[];
     float* sg = reinterpret_cast<float*>(s1_smem);
     const uint32_t* sx = reinterpret_cast<const uint32_t*>(s1_smem + C::kOffX);
@@ -365,7 +357,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::kStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kMC ? 2 * kTConsumers : kTConsumers);
+            mbar_init(&empty[s], kTConsumers);
         }
         fence_mbar_init();
     }
@@ -397,38 +389,29 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
         xblk[c] = b;
     }
     __syncthreads();
-    if constexpr (kMC) cluster_sync();   // both CTAs' barriers initialised before any remote use
     const int n_tiles = a.m_count * a.n_vg;
-    // tile loop: one tile per CTA; kMC: tile pair p = (2p, 2p + 1) per cluster, the CTA of rank
-    // r on 2p + r (a missing last tile runs with an empty mask, keeping the pair in lockstep)
-    const int t_first = kMC ? 2 * static_cast<int>(blockIdx.x >> 1) + static_cast<int>(rank) : blockIdx.x;
-    const int t_step = gridDim.x;
-    const int t_end = kMC ? ((n_tiles + 1) & ~1) : n_tiles;
+    const int t_first = blockIdx.x, t_step = gridDim.x, t_end = n_tiles;   // persistent tile loop
 
     if (warp == kTConsumers) {
         if (lane == 0) {
             tma_prefetch_desc(&tm_g);
-            if constexpr (!kGX) tma_prefetch_desc(&tm_x);
+            tma_prefetch_desc(&tm_x);
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = t_first; tile < t_end; tile += t_step) {
-                const int tl = min(tile, n_tiles - 1);
-                const int ml = tl / a.n_vg, vg = tl - ml * a.n_vg;
+                const int ml = tile / a.n_vg, vg = tile - ml * a.n_vg;
                 unsigned any = 0;
 #pragma unroll
                 for (int f = 0; f < F; ++f) any |= tile_mask(yband, a.Hb, shard_row(a, ml), vg * C::kVG, f, C::kVG);
-                if (tile >= n_tiles) any = 0;
-                if (!kMC && !any) continue;
+                if (!any) continue;
                 for (int c = 0; c < a.n_chunks; ++c) {
                     const int2 sp = span[c];
                     if (sp.y < sp.x) continue;
                     const int nb = (sp.y - sp.x + kTJBox) / kTJBox;
-                    if constexpr (kMC) mbar_wait_cluster(&empty[stage], phase ^ 1);
-                    else mbar_wait(&empty[stage], phase ^ 1);
-                    const int nbl = kMC && !any ? 0 : nb;   // kMC: an idle tile still takes the tables
-                    mbar_expect_tx(&full[stage], nbl * kTJBox * C::kRow * 4 + (kGX ? 0 : F * kTUC * a.Wa * 4));
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], nb * kTJBox * C::kRow * 4 + F * kTUC * a.Wa * 4);
                     float* dst = sg + stage * C::kGFloats;
-                    for (int b = 0; b < nbl; ++b) {
+                    for (int b = 0; b < nb; ++b) {
                         if (a.gamma_5d)   // u-blocked Gamma: one 256-B segment per (j, chunk)
                             tma_load_5d(dst + b * kTJBox * C::kRow, &tm_g, &full[stage], 0, vg * C::kVG, c,
                                         sp.x + b * kTJBox, ml);
@@ -436,24 +419,13 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                             tma_load_4d(dst + b * kTJBox * C::kRow, &tm_g, &full[stage], c * kTUC, vg * C::kVG,
                                         sp.x + b * kTJBox, ml);
                     }
-                    if constexpr (kMC) {
 #pragma unroll
-                        for (int f = 0; f < F; ++f)
-                            if ((f & 1) == static_cast<int>(rank))
-                                tma_load_3d_mc(s1_smem + C::kOffX + (stage * F + f) * C::kXEntries * 4, &tm_x,
-                                               &full[stage], 0, c * kTUC, f, 3);
-                    } else if constexpr (!kGX)
-#pragma unroll
-                        for (int f = 0; f < F; ++f)
+                    for (int f = 0; f < F; ++f)
                             tma_load_3d(s1_smem + C::kOffX + (stage * F + f) * C::kXEntries * 4, &tm_x, &full[stage], 0,
                                         c * kTUC, f);
                     if (++stage == C::kStages) { stage = 0; phase ^= 1; }
                 }
             }
-        }
-        if constexpr (kMC) {
-            __syncwarp();
-            cluster_sync();   // no CTA exits while its peer may still multicast or arrive into it
         }
         return;
     }
@@ -466,34 +438,16 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
     for (int s = 0; s < NS; ++s) voff[s] = (vq + 2 * ((s + hi) & (NS - 1))) * kTUC;
     int stage = 0;
     uint32_t phase = 0;
-    // kGX: half h (slots 4h..4h+3) of the 8 x F entries of (chunk c, x block i) from the
-    // rotated global x-tables, one 16-byte load per plane; slot k is the entry of tap step k
-    const uint4* xr = reinterpret_cast<const uint4*>(a.xrot);
-    auto ld_half = [&](uint32_t (&e)[kTUC][F], int c, int i, int h) {
-        const int x = xbase + 128 * i;
-        if (c >= a.n_chunks || (!kFullX && x >= a.Wa)) return;
-#pragma unroll
-        for (int f = 0; f < F; ++f) {
-            const uint4 q = __ldg(xr + ((static_cast<int64_t>(f) * a.n_chunks + c) * a.Wa + x) * 2 + h);
-            e[4 * h][f] = q.x; e[4 * h + 1][f] = q.y; e[4 * h + 2][f] = q.z; e[4 * h + 3][f] = q.w;
-        }
-    };
-    auto next_chunk = [&](int c) {   // first chunk >= c with a non-empty span (n_chunks: none)
-        while (c < a.n_chunks && span[c].y < span[c].x) ++c;
-        return c;
-    };
-    const uint32_t peer_empty0 = kMC ? mapa_rank(&empty[0], rank ^ 1u) : 0u;
     for (int tile = t_first; tile < t_end; tile += t_step) {
-        const int tl = min(tile, n_tiles - 1);
-        const int ml = tl / a.n_vg, vg = tl - ml * a.n_vg;
+        const int ml = tile / a.n_vg, vg = tile - ml * a.n_vg;
         const int m = shard_row(a, ml), v0 = vg * C::kVG;
         unsigned mask[F], any = 0;
 #pragma unroll
         for (int f = 0; f < F; ++f) {
-            mask[f] = tile < n_tiles ? tile_mask(yband, a.Hb, m, v0, f, C::kVG) : 0u;
+            mask[f] = tile_mask(yband, a.Hb, m, v0, f, C::kVG);
             any |= mask[f];
         }
-        if (!kMC && !any) continue;
+        if (!any) continue;
         double acc[F][NI][NS];
 #pragma unroll
         for (int f = 0; f < F; ++f)
@@ -501,28 +455,10 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
             for (int i = 0; i < NI; ++i)
 #pragma unroll
                 for (int s = 0; s < NS; ++s) acc[f][i][s] = 0.0;
-        // kGX: each half of the next (chunk, x block) pair's entries is loaded as soon as the
-        // current pair's taps have consumed that half, so its L2 latency hides behind the
-        // other half's taps (no extra registers for a second entry set)
-        uint32_t xent[kTUC][F];
-        if constexpr (kGX) {
-            const int c0 = next_chunk(0);
-            ld_half(xent, c0, 0, 0);
-            ld_half(xent, c0, 0, 1);
-        }
         for (int c = 0; c < a.n_chunks; ++c) {
             const int2 sp = span[c];
             if (sp.y < sp.x) continue;
             mbar_wait(&full[stage], phase);
-            if (kMC && !any) {   // idle tile of a pair: only release the stage (both CTAs)
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&empty[stage]);
-                    mbar_arrive_cluster(peer_empty0 + stage * 8);
-                }
-                if (++stage == C::kStages) { stage = 0; phase ^= 1; }
-                continue;
-            }
             const float* G = sg + stage * C::kGFloats;
             // fp32 partial sums of this chunk as packed pairs (slots s = 2p, 2p + 1): the taps run
             // on FFMA2 (fma.rn.f32x2), lane-wise identical to two scalar fmaf in the same order
@@ -534,26 +470,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
 #pragma unroll
                     for (int p = 0; p < NS / 2; ++p) part[f][i][p] = 0ull;
             const uint32_t* sxs = sx + stage * F * C::kXEntries + xbase;
-            if constexpr (kGX) {
-                const uint32_t xb = xblk[c] >> warp;
-                const int cn = next_chunk(c + 1);
-#pragma unroll
-                for (int i = 0; i < NI; ++i) {
-                    const bool act = ((xb >> (8 * i)) & 1u) && (kFullX || xbase + 128 * i < a.Wa);
-                    const int nc = i + 1 < NI ? c : cn, ni = i + 1 < NI ? i + 1 : 0;
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        if (act)
-#pragma unroll
-                            for (int k = 4 * h; k < 4 * h + 4; ++k) {
-                                const int uu = (k + xl) & (kTUC - 1);
-#pragma unroll
-                                for (int f = 0; f < F; ++f) s1_taps<NS, C::kRow>(part[f][i], xent[k][f], G + uu, voff);
-                            }
-                        ld_half(xent, nc, ni, h);
-                    }
-                }
-            } else if constexpr (kSkip) {
+            if constexpr (kSkip) {
                 // i-outer order with a warp-uniform skip of a 16-wide x block that has no used
                 // sample in this chunk for any plane of the group
                 const uint32_t xb = xblk[c] >> warp;
@@ -593,10 +510,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
             // (without it the refill could land while loads of this stage are still in flight).
             fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&empty[stage]);
-                if constexpr (kMC) mbar_arrive_cluster(peer_empty0 + stage * 8);
-            }
+            if (lane == 0) mbar_arrive(&empty[stage]);
 #pragma unroll
             for (int f = 0; f < F; ++f)
 #pragma unroll
@@ -619,7 +533,6 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                 }
             }
     }
-    if constexpr (kMC) cluster_sync();
 }
 
 // Packed x-tables of a fused group of F planes for the TMA stage 1 (W_a <= 256):
@@ -629,7 +542,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
 // 1 moves to the next row with t = 0), and skipped samples point at the zero rows
 // (j_rel = zrow = the stage's row capacity, t = 0).  t keeps 2^-23 resolution; t = 0 stays exact.
 __global__ void pack_xtable_group_kernel(PackGroupArgs g, int Wa, int Wb, uint32_t zrow, uint32_t* __restrict__ out,
-                                         uint32_t* __restrict__ xblk, uint32_t* __restrict__ xrot) {
+                                         uint32_t* __restrict__ xblk) {
     const int c = blockIdx.x, f = blockIdx.y, c0 = c * 8, n_chunks = gridDim.x;
     __shared__ uint32_t sblk;
     if (threadIdx.x == 0) sblk = 0;
@@ -639,11 +552,6 @@ __global__ void pack_xtable_group_kernel(PackGroupArgs g, int Wa, int Wb, uint32
     __syncthreads();
     for (int x = threadIdx.x; x < Wa; x += blockDim.x) {
         bool used = false;
-        // rotated copy for the global-x-table stage 1: slot k of (chunk, x) holds u = c0 + (k + x) % 8;
-        // columns past W_b point at the zero rows
-        uint32_t* rot = xrot ? xrot + ((static_cast<int64_t>(f) * n_chunks + c) * Wa + x) * 8 : nullptr;
-        if (rot)
-            for (int u = Wb; u < c0 + 8; ++u) rot[(u - c0 - x) & 7] = zrow << 23;
         for (int u = c0; u < c0 + 8 && u < Wb; ++u) {
             const int64_t idx = static_cast<int64_t>(u) * Wa + x;
             const int j = __ldg(g.i0[f] + idx);
@@ -656,7 +564,6 @@ __global__ void pack_xtable_group_kernel(PackGroupArgs g, int Wa, int Wb, uint32
                 used = true;
             }
             out[(static_cast<int64_t>(f) * Wb + u) * Wa + x] = e;
-            if (rot) rot[(u - c0 - x) & 7] = e;
         }
         if (used) atomicOr(&sblk, 1u << (x >> 4));
     }
@@ -1101,12 +1008,10 @@ cudaError_t launch_refocus_stage2_group(TElem* const* T, int n_fuse, int Wa, int
         a.plane[f] = planes + static_cast<int64_t>(f) * Ha * Wa;
     }
     const size_t smem = sizeof(TElem) * kS2XB * kS2VC * (Ha + 2) + sizeof(uint32_t) * kS2VC * Ha;
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
+    if (smem > 48 * 1024) {   // per-device attribute: set before every launch
         cudaError_t e = cudaFuncSetAttribute(stage2_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
-        attr = smem;
     }
     stage2_staged_kernel<<<dim3((Wa + kS2XB - 1) / kS2XB, n_fuse), kS2Threads, smem, st>>>(a);
     return cudaGetLastError();
@@ -1127,12 +1032,10 @@ cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int H
                                   int m_base, int m_count, AxisTables xs, AxisTables ys, TElem* T,
                                   cudaStream_t st) {
     const size_t smem = static_cast<size_t>(kVG) * Wa * kPad * sizeof(float);
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
+    if (smem > 48 * 1024) {   // per-device attribute: set before every launch
         cudaError_t e = cudaFuncSetAttribute(stage1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
-        attr = smem;
     }
     dim3 grid((Hb + kVG - 1) / kVG, m_count, (Wa + kS1Threads - 1) / kS1Threads);
     stage1_kernel<<<grid, kS1Threads, smem, st>>>(gamma, ldg, Wa, Ha, Wb, Hb, m_base, xs, ys, T);
@@ -1147,58 +1050,24 @@ bool stage1_tma_supported(int Wa, int Wb, int Hb) {
 }
 
 cudaError_t launch_pack_xtable_group(const AxisTables* xs, int n_fuse, int Wa, int Wb, uint32_t* xpack,
-                                     uint32_t* xblk, uint32_t* xrot, cudaStream_t st) {
+                                     uint32_t* xblk, cudaStream_t st) {
     PackGroupArgs g{};
     g.n = n_fuse;
     for (int f = 0; f < n_fuse; ++f) { g.i0[f] = xs[f].i0; g.t[f] = xs[f].t; g.lo[f] = xs[f].lo; }
     pack_xtable_group_kernel<<<dim3((Wb + 7) / 8, n_fuse), Wa >= 256 ? 256 : ((Wa + 31) / 32) * 32, 0, st>>>(
-        g, Wa, Wb, static_cast<uint32_t>(stage1_rows(Wa)), xpack, xblk, xrot);
+        g, Wa, Wb, static_cast<uint32_t>(stage1_rows(Wa)), xpack, xblk);
     return cudaGetLastError();
-}
-
-template <bool kFullX, int F, bool kSkip, int kJ, int kXM>
-static cudaError_t launch_s1_g(const Stage1Maps* maps, const S1Args& a, int grid, cudaStream_t st) {
-    using C = S1Cfg<F, kJ, kXM == 1>;
-    auto kern = stage1_tma_kernel<kFullX, F, kSkip, kJ, kXM>;
-    static int max_clusters = -1;
-    if (max_clusters < 0) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-        if (e != cudaSuccess) return e;
-        max_clusters = 0;
-        if (kXM == 2) {   // CTA pairs that fit at once (a GPC with an odd free SM count loses one)
-            cudaLaunchConfig_t q{};
-            cudaLaunchAttribute qa{};
-            qa.id = cudaLaunchAttributeClusterDimension;
-            qa.val.clusterDim.x = 2; qa.val.clusterDim.y = 1; qa.val.clusterDim.z = 1;
-            q.gridDim = dim3(2 * 148); q.blockDim = dim3(kTThreads); q.dynamicSmemBytes = C::kSmem;
-            q.attrs = &qa; q.numAttrs = 1;
-            e = cudaOccupancyMaxActiveClusters(&max_clusters, kern, &q);
-            if (e != cudaSuccess || max_clusters < 1) return e != cudaSuccess ? e : cudaErrorInvalidConfiguration;
-        }
-    }
-    if constexpr (kXM == 2) {
-        const int pairs = (a.m_count * a.n_vg + 1) / 2;
-        const int clusters = std::min(std::min(max_clusters, (grid + 1) / 2), pairs);
-        cudaLaunchConfig_t cfg{};
-        cudaLaunchAttribute at{};
-        at.id = cudaLaunchAttributeClusterDimension;
-        at.val.clusterDim.x = 2; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
-        cfg.gridDim = dim3(2 * clusters); cfg.blockDim = dim3(kTThreads); cfg.dynamicSmemBytes = C::kSmem;
-        cfg.stream = st; cfg.attrs = &at; cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, kern, maps->gamma, maps->xtab, a);
-    } else {
-        kern<<<grid, kTThreads, C::kSmem, st>>>(maps->gamma, maps->xtab, a);
-        return cudaGetLastError();
-    }
 }
 
 template <bool kFullX, int F, bool kSkip, int kJ>
 static cudaError_t launch_s1(const Stage1Maps* maps, const S1Args& a, int grid, cudaStream_t st) {
-    if constexpr (kSkip) {
-        if (a.xrot) return launch_s1_g<kFullX, F, true, kJ, 1>(maps, a, grid, st);
-        if (maps->x_multicast) return launch_s1_g<kFullX, F, true, kJ, 2>(maps, a, grid, st);
-    }
-    return launch_s1_g<kFullX, F, kSkip, kJ, 0>(maps, a, grid, st);
+    using C = S1Cfg<F, kJ>;
+    auto kern = stage1_tma_kernel<kFullX, F, kSkip, kJ>;
+    // the attribute is per device: set it before every launch (a host-side call, negligible)
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, kTThreads, C::kSmem, st>>>(maps->gamma, maps->xtab, a);
+    return cudaGetLastError();
 }
 
 template <bool kFullX, bool kSkip, int kJ>
@@ -1223,7 +1092,6 @@ cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa
     a.n_vg = (Hb + stage1_vg(stage1_rows(Wa)) - 1) / stage1_vg(stage1_rows(Wa));
     a.n_chunks = (Wb + kTUC - 1) / kTUC;
     a.xblk = xblk;
-    a.xrot = maps->xrot;
     a.gamma_5d = maps->gamma_5d;
     for (int f = 0; f < n_fuse; ++f) {
         a.xlo[f] = xs[f].lo; a.xhi[f] = xs[f].hi; a.ylo[f] = ys[f].lo; a.yhi[f] = ys[f].hi; a.T[f] = T[f];
@@ -1254,12 +1122,10 @@ cudaError_t launch_refocus_stage1_genb(const float* gamma, int64_t ldg, int Wa, 
                                        int m_base, int m_count, AxisTables xs, AxisTables bx, TElem* T,
                                        cudaStream_t st) {
     const size_t smem = static_cast<size_t>(kVG) * Wa * kGbPad * sizeof(float);
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
+    if (smem > 48 * 1024) {   // per-device attribute: set before every launch
         cudaError_t e = cudaFuncSetAttribute(stage1_genb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
-        attr = smem;
     }
     dim3 grid((Hb + kVG - 1) / kVG, m_count, (Wa + kS1Threads - 1) / kS1Threads);
     stage1_genb_kernel<<<grid, kS1Threads, smem, st>>>(gamma, ldg, Wa, Ha, Wb, Hb, m_base, xs, bx, T);

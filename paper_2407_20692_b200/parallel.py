@@ -102,7 +102,8 @@ def shard_plan(width_a: int, height_a: int, rank: int, world: int, row_align: in
             unit = block * width_a if block_aligned else rows
             if m_per % block == 0 and unit % row_align == 0 and rows >= min(min_panel_rows, width_a * height_a):
                 return ShardPlan(width_a, height_a, world, rank, block, m_per // block)
-        if block_aligned and (m_per * width_a) % row_align and rank < world - 1:
+        # every rank raises (none may enter a collective the others never reach)
+        if block_aligned and (m_per * width_a) % row_align:
             raise ValueError(f"no row-aligned block-cyclic plan for W_a = {width_a}, H_a = {height_a}, "
                              f"world {world}, alignment {row_align}")
     return ShardPlan(width_a, height_a, world, rank, m_per, 1)

@@ -14,10 +14,15 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running (minutes)")
 
 
-def pytest_collection_modifyitems(config, items):
-    """GPU tests fail loudly (not skip) when selected with -m gpu on a box without CUDA,
-    so a silent CPU run can never masquerade as GPU parity."""
-    pass
+def pytest_runtest_setup(item):
+    """GPU tests fail loudly (never skip) when they run on a box without a CUDA device, so a
+    CPU-only run can never masquerade as GPU parity.  The CPU tier deselects them with
+    -m "not gpu"."""
+    if item.get_closest_marker("gpu") is not None:
+        import torch
+        if not torch.cuda.is_available():
+            pytest.fail("GPU test selected but no CUDA device is visible (run the CPU tier with -m 'not gpu')",
+                        pytrace=False)
 
 
 @pytest.fixture(scope="session")

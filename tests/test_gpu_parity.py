@@ -317,30 +317,6 @@ def test_refocus_fallback_kernels(knobs, boundary, monkeypatch):
     _assert_planes(R, G, dims, alphas, boundary=boundary)
 
 
-@pytest.mark.parametrize("dims", [(256, 24, 256, 20), (128, 16, 100, 20), (200, 12, 260, 9), (64, 40, 48, 24),
-                                  (96, 15, 40, 8)])
-@pytest.mark.parametrize("fuse", [1, 3, 4])
-@pytest.mark.parametrize("knob", ["CPI_S1_GX", "CPI_S1_MC"])
-def test_refocus_xtable_modes(dims, fuse, knob, monkeypatch):
-    """Stage 1 with the x-tables read from global memory (CPI_S1_GX=1: three Gamma stages in
-    the ring, entries prefetched half an x block ahead) or shared by CTA pairs through TMA
-    multicast (CPI_S1_MC=1: clusters of 2 on two tiles in lockstep, each producer loading half
-    of the planes' tables into both CTAs) runs the same fp32 taps in the same order as the
-    staged-table kernel, so the planes are bit-identical to it, and within the plane
-    tolerance of the oracle.  Shapes: full-x W_a = 256, the 128-row stage, ragged W_a with a
-    4-column last u chunk (W_b = 260), a small RoI, and an odd tile count (15 tiles: the
-    last pair has an idle CTA)."""
-    Wa, Ha, Wb, Hb = dims
-    monkeypatch.setenv("CPI_REFOCUS_FUSE", str(fuse))
-    G = synth.random_gamma(Wa * Ha, Wb * Hb, seed=Wa + Wb + fuse)
-    alphas = [0.5, 0.77, 1.0, 1.31, 1.62, 2.0, 2.9]
-    ref = _refocus_gpu(G, dims, alphas)
-    monkeypatch.setenv(knob, "1")
-    R = _refocus_gpu(G, dims, alphas)
-    assert np.array_equal(R, ref)
-    _assert_planes(R, G, dims, alphas)
-
-
 def test_refocus_repeat_bit_identical():
     """Every refocus kernel is deterministic (fixed summation order, no atomics in the value
     path), so repeated runs must agree bit for bit.  Catches pipeline races: e.g. a stage
