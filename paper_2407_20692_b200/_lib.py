@@ -18,6 +18,7 @@ STATUS = {
 CPI_LSB_FIRST, CPI_MSB_FIRST = 0, 1
 CPI_HOST, CPI_DEVICE = 0, 1
 CPI_VARIANT_TC, CPI_VARIANT_POPC, CPI_KEEP_COUNTS, CPI_VARIANT_FP4, CPI_GAMMA_UBLOCKED = 0, 1, 2, 4, 8
+CPI_GAMMA_VMAJOR = 16
 CPI_SKIP_RENORMALIZE, CPI_CLAMP = 0, 1
 KC_GEMM, KC_EXPAND, KC_STAGE1, KC_STAGE2, KC_FINALIZE, KC_COORDS, KC_RESAMPLE = range(7)
 

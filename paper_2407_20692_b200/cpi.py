@@ -16,8 +16,8 @@ from . import _lib
 from ._lib import CpiError
 
 FRAME_W, FRAME_H = 512, 256   # SwissSPAD2 frame
-# B pixel (Gamma column) orders, include/cpi.h: row-major q = v W_b + u, or u-blocked
-GAMMA_ORDERS = {"rowmajor": 0, "ublocked": _lib.CPI_GAMMA_UBLOCKED}
+# B pixel (Gamma column) orders, include/cpi.h: row-major q = v W_b + u, u-blocked, v-major u H_b + v
+GAMMA_ORDERS = {"rowmajor": 0, "ublocked": _lib.CPI_GAMMA_UBLOCKED, "vmajor": _lib.CPI_GAMMA_VMAJOR}
 
 
 def _torch():
@@ -244,12 +244,14 @@ class Context:
 
     def b_index(self):
         """Index of every B pixel q = v * W_b + u in S_b and in the columns of S_ab / Gamma
-        (identity for the row-major order, include/cpi.h CPI_GAMMA_UBLOCKED)."""
+        (identity for the row-major order; include/cpi.h CPI_GAMMA_UBLOCKED, CPI_GAMMA_VMAJOR)."""
         Wb, Hb = self.roi_b[2], self.roi_b[3]
         q = np.arange(Wb * Hb)
         if self.gamma_order == "rowmajor":
             return q
         v, u = q // Wb, q % Wb
+        if self.gamma_order == "vmajor":
+            return u * Hb + v
         return (u // 8) * (8 * Hb) + 8 * v + (u % 8)
 
     def new_gamma(self):

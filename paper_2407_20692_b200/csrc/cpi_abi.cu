@@ -37,6 +37,7 @@ struct cpi_ctx {
     bool popc = false, keep = false, pair = true;   // pair: cta_group::2 GEMM
     bool fp4 = false;                      // kind::mxf4 GEMM on E2M1 operands (2 frames per byte)
     bool ublocked = false;                 // B pixels in u-blocked order (CPI_GAMMA_UBLOCKED)
+    int order = cpi::kOrderRowMajor;       // B pixel order (row-major / u-blocked / v-major)
     int64_t k_align = 128;                 // frames per GEMM K block
     int64_t p_a = 0, p_b = 0;
     int64_t rows_a = 0, rows_b = 0;        // padded operand rows
@@ -82,6 +83,21 @@ struct cpi_ctx {
     bool use_s2_staged = false;
     cpi::Stage1Maps s1maps{};
     bool use_s1_tma = false;
+    // v-major refocus (KB5w, refocus_w.cu): per-plane tables of a batch of up to kWBatch planes
+    static constexpr int kWBatch = 64;
+    bool w_ready = false;
+    int w_batch = 0;                       // planes per batch (allocated)
+    cpi::AxisTables wxs[kWBatch]{}, wys[kWBatch]{};
+    const int32_t** w_i0s = nullptr;       // device arrays of the tables' pointers (pack_w inputs)
+    const double** w_ts = nullptr;
+    const int32_t** w_ylo = nullptr;
+    const int32_t** w_yhi = nullptr;
+    uint32_t* w_ent = nullptr;             // [batch][W_b][x_pad] (j0 | t)
+    uint2* w_steps = nullptr;              // [batch][W_b][x_pad] step entries
+    int2* w_span = nullptr;                // [groups][x tiles][W_b]
+    int2* w_mband = nullptr;               // [groups][v blocks]
+    uint32_t* w_ypack = nullptr;           // [batch][H_b][H_a]
+    cpi::TElem* w_T = nullptr;             // [batch][W_a][H_a][H_b]
     // accounting
     int64_t launches = 0;
     bool timing = false;
@@ -217,6 +233,11 @@ void free_all(cpi_ctx* c) {
     cudaFree(c->xblk);
     cudaFree(c->gamma_ws);
     cudaFree(c->bws);
+    for (int f = 0; f < cpi_ctx::kWBatch; ++f)
+        for (auto* t : {&c->wxs[f], &c->wys[f]}) { cudaFree(t->i0); cudaFree(t->t); cudaFree(t->cnt); cudaFree(t->lo); cudaFree(t->hi); }
+    cudaFree(c->w_i0s); cudaFree(c->w_ts); cudaFree(c->w_ylo); cudaFree(c->w_yhi);
+    cudaFree(c->w_ent); cudaFree(c->w_steps); cudaFree(c->w_span); cudaFree(c->w_mband);
+    cudaFree(c->w_ypack); cudaFree(c->w_T);
     for (auto& t : c->timed) { c->event_pool.push_back(t.a); c->event_pool.push_back(t.b); }
     for (auto e : c->event_pool) cudaEventDestroy(e);
 }
@@ -230,11 +251,229 @@ cpi_status alloc_axis(cpi_ctx* c, cpi::AxisTables& t, int W, int Wb) {
     return CPI_OK;
 }
 
+// Largest union j span (rows, incl. the t -> 1 rounding row) of any (plane group, x tile, u) of
+// planes [p0, p0 + n): the A-axis map c(x, u) = ((a (x - c_a)) + (b (u - c_b))) + cc + c_a is affine
+// in x, so the union over a tile's outputs and the group's planes is spanned by the endpoint
+// values; used samples lie in [0, W_a - 1] (skip) or are clamped into it.
+int w_max_span(const double (*maps)[6], int n, int Wa, int Wb) {
+    const int xt = cpi::stage1_w_xtile(), gf = cpi::stage1_w_group();
+    const double ca = (Wa - 1) / 2.0, cb = (Wb - 1) / 2.0;
+    int worst = 0;
+    for (int g = 0; g < n; g += gf)
+        for (int x0 = 0; x0 < Wa; x0 += xt) {
+            const int x1 = std::min(Wa, x0 + xt) - 1;
+            for (int u = 0; u < Wb; ++u) {
+                double lo = 1e300, hi = -1e300;
+                for (int f = g; f < std::min(n, g + gf); ++f)
+                    for (int x : {x0, x1}) {
+                        const double cc = ((maps[f][0] * (x - ca)) + (maps[f][1] * (u - cb))) + maps[f][2] + ca;
+                        lo = std::min(lo, cc);
+                        hi = std::max(hi, cc);
+                    }
+                lo = std::max(lo, 0.0);
+                hi = std::min(hi, double(Wa - 1));
+                if (hi < lo) continue;
+                worst = std::max(worst, int(std::floor(hi) - std::floor(lo)) + 3);
+            }
+        }
+    return worst;
+}
+
+// Refocusing for the v-major B order (CPI_GAMMA_VMAJOR): batches of up to kWBatch planes; per
+// batch the coordinate tables of every plane, one pack_w, one launch of the window stage 1 (KB5w)
+// and the staged stage 2 per group of 4.  Planes of one batch share one Gamma source (the
+// caller's Gamma, or one B-resampled Gamma for a fractional B map).
+cpi_status refocus_vmajor(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, cudaStream_t st, bool resample) {
+    const int Wa = c->cfg.roi_a.width, Ha = c->cfg.roi_a.height;
+    const int Wb = c->cfg.roi_b.width, Hb = c->cfg.roi_b.height;
+    const int m_base = static_cast<int>(spec->row0 / Wa), m_count = static_cast<int>(spec->rows / Wa);
+    const bool cyclic = spec->row_block > 0 && spec->row_block < m_count;
+    const int m_block = cyclic ? spec->row_block : 0, m_stride = cyclic ? spec->row_stride : 0;
+    const bool w_ok = cpi::stage1_w_supported(Wa, Hb) && cpi::stage2_staged_supported(Ha) &&
+                      (reinterpret_cast<uintptr_t>(spec->gamma_dev) & 15) == 0 && getenv("CPI_STAGE1_SIMPLE") == nullptr;
+    if (!w_ok && cyclic)
+        return fail(c, CPI_ERR_UNSUPPORTED, "block-cyclic shards in the v-major order need the window stage 1 "
+                                            "(W_a <= 256, H_a <= 256, 16-byte aligned Gamma)");
+    if (!c->w_ready) {
+        const int nb = cpi_ctx::kWBatch;
+        for (int f = 0; f < nb; ++f) {
+            cpi_status s = alloc_axis(c, c->wxs[f], Wa, Wb);
+            if (s == CPI_OK) s = alloc_axis(c, c->wys[f], Ha, Hb);
+            if (s != CPI_OK) return s;
+        }
+        const int64_t xpad = (Wa + cpi::stage1_w_xtile() - 1) / cpi::stage1_w_xtile() * cpi::stage1_w_xtile();
+        const int64_t n_xt = xpad / cpi::stage1_w_xtile(), n_vb = (Hb + cpi::stage1_w_vblock() - 1) / cpi::stage1_w_vblock();
+        const int64_t n_g = (nb + cpi::stage1_w_group() - 1) / cpi::stage1_w_group();
+        CK(c, cudaMalloc(&c->w_i0s, sizeof(void*) * nb));
+        CK(c, cudaMalloc(&c->w_ts, sizeof(void*) * nb));
+        CK(c, cudaMalloc(&c->w_ylo, sizeof(void*) * nb));
+        CK(c, cudaMalloc(&c->w_yhi, sizeof(void*) * nb));
+        std::vector<const void*> h(4 * nb);
+        for (int f = 0; f < nb; ++f) {
+            h[f] = c->wxs[f].i0; h[nb + f] = c->wxs[f].t; h[2 * nb + f] = c->wys[f].lo; h[3 * nb + f] = c->wys[f].hi;
+        }
+        CK(c, cudaMemcpy(c->w_i0s, h.data(), sizeof(void*) * nb, cudaMemcpyHostToDevice));
+        CK(c, cudaMemcpy(c->w_ts, h.data() + nb, sizeof(void*) * nb, cudaMemcpyHostToDevice));
+        CK(c, cudaMemcpy(c->w_ylo, h.data() + 2 * nb, sizeof(void*) * nb, cudaMemcpyHostToDevice));
+        CK(c, cudaMemcpy(c->w_yhi, h.data() + 3 * nb, sizeof(void*) * nb, cudaMemcpyHostToDevice));
+        CK(c, cudaMalloc(&c->w_ent, sizeof(uint32_t) * nb * Wb * xpad));
+        CK(c, cudaMalloc(&c->w_steps, sizeof(uint2) * nb * Wb * xpad));
+        CK(c, cudaMalloc(&c->w_span, sizeof(int2) * n_g * n_xt * Wb));
+        CK(c, cudaMalloc(&c->w_mband, sizeof(int2) * n_g * n_vb));
+        CK(c, cudaMalloc(&c->w_ypack, sizeof(uint32_t) * size_t(nb) * Hb * Ha));
+        CK(c, cudaMalloc(&c->w_T, sizeof(cpi::TElem) * size_t(nb) * Wa * Ha * Hb));
+        c->w_batch = nb;
+        c->w_ready = true;
+    }
+    auto bkey = [&](int p, double* k) {
+        const double* mp = spec->affine ? spec->affine + 12 * p : nullptr;
+        k[0] = mp ? mp[4] : 1.0; k[1] = mp ? mp[5] : 0.0; k[2] = mp ? mp[10] : 1.0; k[3] = mp ? mp[11] : 0.0;
+    };
+    auto frac_b = [&](int p) {
+        double k[4];
+        bkey(p, k);
+        return k[0] != 1.0 || k[1] != 0.0 || k[2] != 1.0 || k[3] != 0.0;
+    };
+    auto same_b = [&](int p, int q) {
+        double k[4], l[4];
+        bkey(p, k);
+        bkey(q, l);
+        return k[0] == l[0] && k[1] == l[1] && k[2] == l[2] && k[3] == l[3];
+    };
+    const int64_t t_plane = int64_t(Wa) * Ha * Hb;
+    const int gf = cpi::stage1_w_group();
+    int resampled = -1;
+    for (int p0 = 0; p0 < spec->n_planes;) {
+        int nb = 1;   // planes of this batch: one Gamma source
+        while (nb < c->w_batch && p0 + nb < spec->n_planes && (!resample || same_b(p0, p0 + nb))) ++nb;
+        const bool from_ws = resample && frac_b(p0);
+        const float* gsrc = from_ws ? c->bws : spec->gamma_dev;
+        double maps[cpi_ctx::kWBatch][6];
+        for (int f = 0; f < nb; ++f) {
+            if (spec->affine) {
+                const double* mp = spec->affine + 12 * (p0 + f);
+                const double m6[6] = {mp[0], mp[1], mp[2], mp[6], mp[7], mp[8]};
+                for (int i = 0; i < 6; ++i) maps[f][i] = m6[i];
+            } else {
+                const double alpha = spec->alphas[p0 + f];
+                maps[f][0] = maps[f][3] = alpha;
+                maps[f][1] = maps[f][4] = 1.0 - alpha;
+                maps[f][2] = maps[f][5] = 0.0;
+            }
+        }
+        const bool w_now = w_ok && w_max_span(maps, nb, Wa, Wb) <= cpi::stage1_w_max_span();
+        if (!w_now && cyclic)
+            return fail(c, CPI_ERR_UNSUPPORTED, "block-cyclic shards in the v-major order need the window stage 1; "
+                                                "a plane's span exceeds its stage (A-axis slope above ~2.2)");
+        {
+            TimedScope ts(c, KC_COORDS, st);
+            cudaError_t e = cudaSuccess;
+            for (int g0 = 0; g0 < nb && e == cudaSuccess; g0 += gf) {
+                const int nf = std::min(gf, nb - g0);
+                cpi::CoordsGroupArgs cg{};
+                cg.Wa = Wa; cg.Ha = Ha; cg.Wb = Wb; cg.Hb = Hb; cg.boundary = spec->boundary;
+                for (int f = 0; f < nf; ++f) {
+                    for (int i = 0; i < 6; ++i) cg.map[f][i] = maps[g0 + f][i];
+                    cg.xs[f] = c->wxs[g0 + f];
+                    cg.ys[f] = c->wys[g0 + f];
+                    bkey(p0 + g0 + f, cg.bmap[f]);
+                    cg.bx[f] = c->bxs;
+                    cg.by[f] = c->bys;
+                }
+                cg.genb = from_ws ? 1 : 0;
+                e = cpi::launch_refocus_coords_group(cg, nf, st);
+                c->launches += 2;
+                if (e == cudaSuccess) {
+                    e = cpi::launch_pack_ytable_group(c->wys + g0, nf, Ha, Hb, c->w_ypack + int64_t(g0) * Hb * Ha, st);
+                    c->launches += 1;
+                }
+            }
+            if (e == cudaSuccess && w_now) {
+                e = cpi::launch_pack_w(c->w_i0s, c->w_ts, c->w_ylo, c->w_yhi, nb, Wa, Wb, Hb, c->w_ent, c->w_steps,
+                                       c->w_span, c->w_mband, st);
+                c->launches += 4;
+            }
+            if (e != cudaSuccess) return cuda_fail(c, e, "refocus coords launch");
+        }
+        if (from_ws && (resampled < 0 || !same_b(p0, resampled))) {
+            TimedScope ts(c, KC_RESAMPLE, st);
+            cudaError_t e = cpi::launch_resample_b(spec->gamma_dev, c->bws, spec->rows, Wb, Hb, c->order,
+                                                   spec->affine[12 * p0 + 10], c->bxs, c->bys, st);
+            c->launches += 1;
+            if (e != cudaSuccess) return cuda_fail(c, e, "B resample launch");
+            resampled = p0;
+        }
+        {
+            TimedScope ts(c, KC_STAGE1, st);
+            cudaError_t e = cudaSuccess;
+            if (w_now) {
+                cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
+                if (!enc) return fail(c, CPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+                CUtensorMap tg, te;
+                const cuuint64_t gd[4] = {cuuint64_t(Hb), cuuint64_t(Wb), cuuint64_t(Wa), cuuint64_t(m_count)};
+                const cuuint64_t gs[3] = {cuuint64_t(Hb) * 4, cuuint64_t(c->p_b) * 4, cuuint64_t(Wa) * c->p_b * 4};
+                const cuuint32_t gb[4] = {cuuint32_t(cpi::stage1_w_vblock()), 1u, cuuint32_t(cpi::stage1_w_jbox()), 1u};
+                const cuuint32_t es4[4] = {1u, 1u, 1u, 1u};
+                CUresult r = enc(&tg, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(gsrc), gd, gs, gb, es4,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                if (r != CUDA_SUCCESS) return fail(c, CPI_ERR_CUDA, "Gamma tensor map (v-major) failed (%d)", int(r));
+                const int64_t xpad = (Wa + cpi::stage1_w_xtile() - 1) / cpi::stage1_w_xtile() * cpi::stage1_w_xtile();
+                const cuuint64_t ed[3] = {cuuint64_t(2 * xpad), cuuint64_t(Wb), cuuint64_t(nb)};
+                const cuuint64_t est[2] = {cuuint64_t(2 * xpad) * 4, cuuint64_t(2 * xpad) * Wb * 4};
+                const cuuint32_t eb[3] = {cuuint32_t(2 * cpi::stage1_w_xtile()), 1u, cuuint32_t(cpi::stage1_w_group())};
+                const cuuint32_t es3[3] = {1u, 1u, 1u};
+                r = enc(&te, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, c->w_steps, ed, est, eb, es3, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                if (r != CUDA_SUCCESS) return fail(c, CPI_ERR_CUDA, "step-entry tensor map failed (%d)", int(r));
+                cpi::S1WArgs a{};
+                a.Wa = Wa; a.Ha = Ha; a.Wb = Wb; a.Hb = Hb;
+                a.m_base = m_base; a.m_count = m_count; a.m_block = m_block; a.m_stride = m_stride;
+                a.n_planes = nb; a.span = c->w_span; a.mband = c->w_mband; a.T = c->w_T; a.t_plane = t_plane;
+                e = cpi::launch_refocus_stage1_w(&tg, &te, a, c->num_sms, st);
+                c->launches += 1;
+            } else {
+                for (int f = 0; f < nb && e == cudaSuccess; ++f) {
+                    e = cpi::launch_refocus_stage1(gsrc, c->p_b, Wa, Ha, Wb, Hb, m_base, m_count, c->wxs[f], c->wys[f],
+                                                   c->w_T + f * t_plane, st, 1);
+                    c->launches += 1;
+                }
+            }
+            if (e != cudaSuccess) return cuda_fail(c, e, "refocus stage-1 launch");
+        }
+        {
+            TimedScope ts(c, KC_STAGE2, st);
+            cudaError_t e = cudaSuccess;
+            for (int g0 = 0; g0 < nb && e == cudaSuccess; g0 += gf) {
+                const int nf = std::min(gf, nb - g0);
+                if (cpi::stage2_staged_supported(Ha)) {
+                    cpi::TElem* Tp[cpi::kRefocusMaxFuse];
+                    for (int f = 0; f < nf; ++f) Tp[f] = c->w_T + (g0 + f) * t_plane;
+                    e = cpi::launch_refocus_stage2_group(Tp, nf, Wa, Ha, Hb, m_base, m_count, m_block, m_stride,
+                                                         c->wxs + g0, c->wys + g0, c->w_ypack + int64_t(g0) * Hb * Ha,
+                                                         planes + int64_t(p0 + g0) * Ha * Wa, st);
+                    c->launches += 1;
+                } else {
+                    for (int f = 0; f < nf && e == cudaSuccess; ++f) {
+                        e = cpi::launch_refocus_stage2(c->w_T + (g0 + f) * t_plane, Wa, Ha, Hb, m_base, m_count,
+                                                       c->wxs[g0 + f], c->wys[g0 + f],
+                                                       planes + int64_t(p0 + g0 + f) * Ha * Wa, st);
+                        c->launches += 1;
+                    }
+                }
+            }
+            if (e != cudaSuccess) return cuda_fail(c, e, "refocus stage-2 launch");
+        }
+        p0 += nb;
+    }
+    return CPI_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
-int32_t cpi_abi_version(void) { return 103; }
+int32_t cpi_abi_version(void) { return 104; }
 
 const char* cpi_status_string(cpi_status s) {
     switch (s) {
@@ -277,7 +516,11 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
         return fail(nullptr, CPI_ERR_INVALID_ARG, "max_frames must be < 2^31 (int32 sums)");
     if ((cfg->flags & CPI_GAMMA_UBLOCKED) && cfg->roi_b.width % 8)
         return fail(nullptr, CPI_ERR_UNSUPPORTED, "CPI_GAMMA_UBLOCKED needs roi_b.width %% 8 == 0");
-    if (cfg->flags & ~(CPI_VARIANT_POPC | CPI_KEEP_COUNTS | CPI_VARIANT_FP4 | CPI_GAMMA_UBLOCKED))
+    if ((cfg->flags & CPI_GAMMA_VMAJOR) && (cfg->flags & CPI_GAMMA_UBLOCKED))
+        return fail(nullptr, CPI_ERR_INVALID_ARG, "CPI_GAMMA_VMAJOR and CPI_GAMMA_UBLOCKED are exclusive");
+    if ((cfg->flags & CPI_GAMMA_VMAJOR) && cfg->roi_b.height % 4)
+        return fail(nullptr, CPI_ERR_UNSUPPORTED, "CPI_GAMMA_VMAJOR needs roi_b.height %% 4 == 0");
+    if (cfg->flags & ~(CPI_VARIANT_POPC | CPI_KEEP_COUNTS | CPI_VARIANT_FP4 | CPI_GAMMA_UBLOCKED | CPI_GAMMA_VMAJOR))
         return fail(nullptr, CPI_ERR_INVALID_ARG, "unknown flags 0x%x", cfg->flags);
     if ((cfg->flags & CPI_VARIANT_POPC) && (cfg->flags & CPI_VARIANT_FP4))
         return fail(nullptr, CPI_ERR_INVALID_ARG, "CPI_VARIANT_POPC and CPI_VARIANT_FP4 are exclusive");
@@ -308,6 +551,8 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
     c->p_b = int64_t(cfg->roi_b.width) * cfg->roi_b.height;
     c->k_align = c->fp4 ? 2 * kKAlign : kKAlign;
     c->ublocked = (cfg->flags & CPI_GAMMA_UBLOCKED) != 0;
+    c->order = c->ublocked ? cpi::kOrderUBlocked
+                           : (cfg->flags & CPI_GAMMA_VMAJOR) ? cpi::kOrderVMajor : cpi::kOrderRowMajor;
     c->k_cap = round_up(cfg->max_frames, c->k_align);
     c->frame_bytes = int64_t(L.width_px / 8) * L.height_px;
     if (c->popc) {
@@ -429,9 +674,9 @@ cpi_status expand_batch(cpi_ctx* c, cudaStream_t st) {
     if (c->cur_buf >= 0) CK(c, cudaStreamWaitEvent(st, c->ev_loaded[c->cur_buf], 0));
     if (n > 0) {
         cpi::launch_expand(c->frames_cur, n, L.width_px / 8, L.height_px, L.bit_order, ra, c->op_a,
-                           c->ld_op, k_pad, c->s_a, mode, false, st);
+                           c->ld_op, k_pad, c->s_a, mode, cpi::kOrderRowMajor, st);
         cpi::launch_expand(c->frames_cur, n, L.width_px / 8, L.height_px, L.bit_order, rb, c->op_b,
-                           c->ld_op, k_pad, c->s_b, mode, c->ublocked, st);
+                           c->ld_op, k_pad, c->s_b, mode, c->order, st);
         c->launches += 2;
         CK(c, cudaGetLastError());
     }
@@ -731,7 +976,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
                     (long long)spec->row0, (long long)spec->rows);
     CK(c, cudaSetDevice(c->dev));
     auto st = static_cast<cudaStream_t>(stream);
-    if (!c->refocus_ready) {
+    if (!c->refocus_ready && c->order != cpi::kOrderVMajor) {
         c->use_s1_tma = cpi::stage1_tma_supported(Wa, Wb, Hb) && getenv("CPI_STAGE1_SIMPLE") == nullptr;
         if (const char* ev = getenv("CPI_REFOCUS_FUSE")) c->fuse = atoi(ev);
         if (c->fuse < 1) c->fuse = 1;
@@ -805,6 +1050,19 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
         }
     }
     const bool direct = genb && !resample;
+    if (c->order == cpi::kOrderVMajor) {
+        if (direct)
+            return fail(c, CPI_ERR_UNSUPPORTED, "fractional B coordinates without the resample workspace need the "
+                                                "row-major B order");
+        if (spec->row_block > 0 && spec->row_block < spec->rows / Wa && spec->row_stride < spec->row_block)
+            return fail(c, CPI_ERR_INVALID_ARG, "row_stride %d < row_block %d", spec->row_stride, spec->row_block);
+        if (spec->row_block > 0 && spec->row_block < spec->rows / Wa) {
+            const int mb = static_cast<int>(spec->row0 / Wa), mc = static_cast<int>(spec->rows / Wa);
+            const int64_t last = mb + int64_t((mc - 1) / spec->row_block) * spec->row_stride + (mc - 1) % spec->row_block;
+            if (last >= Ha) return fail(c, CPI_ERR_INVALID_ARG, "block-cyclic shard reaches A row %lld >= H_a", (long long)last);
+        }
+        return refocus_vmajor(c, spec, planes, st, resample);
+    }
     if (direct && c->ublocked)
         return fail(c, CPI_ERR_UNSUPPORTED, "fractional B coordinates without the resample workspace need the "
                                             "row-major B order");
@@ -903,7 +1161,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
         }
         if (from_ws && (resampled < 0 || !same_b(p0, resampled))) {
             TimedScope ts(c, KC_RESAMPLE, st);
-            cudaError_t e = cpi::launch_resample_b(spec->gamma_dev, c->bws, spec->rows, Wb, Hb, c->ublocked ? 1 : 0,
+            cudaError_t e = cpi::launch_resample_b(spec->gamma_dev, c->bws, spec->rows, Wb, Hb, c->order,
                                                    spec->affine[12 * p0 + 10], c->bxs, c->bys, st);
             c->launches += 1;
             if (e != cudaSuccess) return cuda_fail(c, e, "B resample launch");

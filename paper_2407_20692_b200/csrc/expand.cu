@@ -18,6 +18,14 @@ namespace cpi {
 namespace {
 
 constexpr int kThreads = 256;
+
+// operand row / sum slot of RoI pixel (m, j) (include/cpi.h B pixel orders): row-major m * w + j,
+// u-blocked (j / 8) * (8 h) + 8 m + j % 8 (CPI_GAMMA_UBLOCKED), v-major j * h + m (CPI_GAMMA_VMAJOR)
+__device__ __forceinline__ int64_t pixel_slot(int order, int m, int j, const RoiDev& roi) {
+    if (order == kOrderUBlocked) return static_cast<int64_t>(j >> 3) * (8 * roi.h) + 8 * m + (j & 7);
+    if (order == kOrderVMajor) return static_cast<int64_t>(j) * roi.h + m;
+    return static_cast<int64_t>(m) * roi.w + j;
+}
 constexpr int kSub = 128;       // frames per staged sub-block
 constexpr int kFramesCta = 512; // frames per CTA
 constexpr int kRowStride = 65;  // bytes per staged frame row: odd word stride -> no bank conflicts
@@ -27,7 +35,7 @@ template <int kMode>
 __global__ void __launch_bounds__(kThreads)
 expand_kernel(const uint8_t* __restrict__ frames, int64_t n, int row_bytes, int frame_h, int msb,
               RoiDev roi, void* __restrict__ op, int64_t ld, int64_t k_pad, int32_t* __restrict__ s,
-              int ublocked) {
+              int order) {
     __shared__ uint8_t sbits[kSub * kRowStride];
     __shared__ int cnt[kMaxWidth];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -52,8 +60,7 @@ expand_kernel(const uint8_t* __restrict__ frames, int64_t n, int row_bytes, int 
             const int col = roi.x0 + j;
             const int b = (col >> 3) - b0;
             const int sh = msb ? 7 - (col & 7) : (col & 7);
-            const int64_t prow = ublocked ? static_cast<int64_t>(j >> 3) * (8 * roi.h) + 8 * m + (j & 7)
-                                          : static_cast<int64_t>(m) * roi.w + j;
+            const int64_t prow = pixel_slot(order, m, j, roi);
             int c;
             if constexpr (kMode == kExpandE2M1) {
                 // 4 frames -> 4 nibbles (E2M1 1.0 = 0x2), frame f in nibble f % 2 of byte f / 2
@@ -95,8 +102,7 @@ expand_kernel(const uint8_t* __restrict__ frames, int64_t n, int row_bytes, int 
     __syncthreads();
     for (int j = tid; j < roi.w; j += kThreads)
         if (cnt[j])
-            atomicAdd(s + (ublocked ? static_cast<int64_t>(j >> 3) * (8 * roi.h) + 8 * m + (j & 7)
-                                    : static_cast<int64_t>(m) * roi.w + j), cnt[j]);
+            atomicAdd(s + pixel_slot(order, m, j, roi), cnt[j]);
 }
 
 // u8 / E2M1 operands, byte-column parallel: the sub-block's bytes are staged transposed,
@@ -111,7 +117,7 @@ template <int kMode>
 __global__ void __launch_bounds__(kThreads)
 expand_cols_kernel(const uint8_t* __restrict__ frames, int64_t n, int row_bytes, int frame_h, int msb,
                    RoiDev roi, void* __restrict__ op, int64_t ld, int64_t k_pad, int32_t* __restrict__ s,
-                   int ublocked, int words) {
+                   int order, int words) {
     __shared__ __align__(16) uint8_t sbt[(kMaxWidth / 8 + 1) * kTStride];
     __shared__ int cnt[kMaxWidth];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -155,8 +161,7 @@ expand_cols_kernel(const uint8_t* __restrict__ frames, int64_t n, int row_bytes,
                 const int j = col - roi.x0;
                 if (j < 0 || j >= roi.w) continue;          // warp-uniform
                 const uint32_t x = (w4 >> bit) & 0x01010101u;
-                const int64_t prow = ublocked ? static_cast<int64_t>(j >> 3) * (8 * roi.h) + 8 * m + (j & 7)
-                                              : static_cast<int64_t>(m) * roi.w + j;
+                const int64_t prow = pixel_slot(order, m, j, roi);
                 if constexpr (kMode == kExpandE2M1) {
                     const uint32_t nib = ((x | (x >> 12)) & 0x1111u) << 1;   // 4 nibbles, 0x2 = 1.0
                     *reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(op) + prow * ld + ((f0 + 4 * lane) >> 1)) =
@@ -172,29 +177,28 @@ expand_cols_kernel(const uint8_t* __restrict__ frames, int64_t n, int row_bytes,
     __syncthreads();
     for (int j = tid; j < roi.w; j += kThreads)
         if (cnt[j])
-            atomicAdd(s + (ublocked ? static_cast<int64_t>(j >> 3) * (8 * roi.h) + 8 * m + (j & 7)
-                                    : static_cast<int64_t>(m) * roi.w + j), cnt[j]);
+            atomicAdd(s + pixel_slot(order, m, j, roi), cnt[j]);
 }
 
 }  // namespace
 
 void launch_expand(const uint8_t* frames, int64_t n, int row_bytes, int frame_h, int msb,
                    RoiDev roi, void* op, int64_t ld, int64_t k_pad, int32_t* s, int mode,
-                   bool ublocked, cudaStream_t st) {
+                   int order, cudaStream_t st) {
     if (k_pad <= 0) return;
     dim3 grid(static_cast<unsigned>((k_pad + kFramesCta - 1) / kFramesCta), roi.h);
     if (mode == kExpandBits)
         expand_kernel<kExpandBits><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
-                                                              ld, k_pad, s, ublocked ? 1 : 0);
+                                                              ld, k_pad, s, order);
     else {
         // word loads need 4-byte aligned frame rows
         const int words = (row_bytes % 4 == 0 && (reinterpret_cast<uintptr_t>(frames) & 3) == 0) ? 1 : 0;
         if (mode == kExpandE2M1)
             expand_cols_kernel<kExpandE2M1><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
-                                                                       ld, k_pad, s, ublocked ? 1 : 0, words);
+                                                                       ld, k_pad, s, order, words);
         else
             expand_cols_kernel<kExpandU8><<<grid, kThreads, 0, st>>>(frames, n, row_bytes, frame_h, msb, roi, op,
-                                                                     ld, k_pad, s, ublocked ? 1 : 0, words);
+                                                                     ld, k_pad, s, order, words);
     }
 }
 

@@ -32,11 +32,13 @@ struct Epilogue {
 // kExpandBits pixel-major 32-bit bit streams (popcount), kExpandE2M1 nibbles 0x0 / 0x2
 // (E2M1 0.0 / 1.0, frame 2i in the low nibble of byte i; kind::mxf4).
 enum { kExpandU8 = 0, kExpandBits = 1, kExpandE2M1 = 2 };
-// ublocked: pixel (m, j) of the RoI is written to operand row / sum slot
-// (j / 8) * (8 * roi.h) + 8 * m + j % 8 instead of m * roi.w + j (CPI_GAMMA_UBLOCKED, B arm).
+// order: operand row / sum slot of RoI pixel (m, j): kOrderRowMajor m * roi.w + j, kOrderUBlocked
+// (j / 8) * (8 * roi.h) + 8 * m + j % 8 (CPI_GAMMA_UBLOCKED), kOrderVMajor j * roi.h + m
+// (CPI_GAMMA_VMAJOR); the B arm follows the context's order, the A arm is always row-major.
+enum { kOrderRowMajor = 0, kOrderUBlocked = 1, kOrderVMajor = 2 };
 void launch_expand(const uint8_t* frames, int64_t n, int row_bytes, int frame_h, int msb,
                    RoiDev roi, void* op, int64_t ld, int64_t k_pad, int32_t* s, int mode,
-                   bool ublocked, cudaStream_t st);
+                   int order, cudaStream_t st);
 
 // KB2: persistent tcgen05 kind::i8 GEMM  S = A^T B  (A: [M_pad][K] u8, B: [N_pad][K] u8,
 // both K-major) with the fused epilogue.  k_blocks = K / 128.
@@ -108,11 +110,12 @@ cudaError_t launch_refocus_stage2_genb(const TElem* T, int Wa, int Ha, int Hb, i
 // at the B support (by[v], bx[u]) for rows A pixels of P_b slots each (B order row-major or
 // u-blocked), so that the separable fast path runs Gamma' with the identity B map.  ey = the
 // map's B-row scale (bounds the B support rows of a band: banded shared-memory form if small).
-cudaError_t launch_resample_b(const float* src, float* dst, int64_t rows, int Wb, int Hb, int ublocked, double ey,
+cudaError_t launch_resample_b(const float* src, float* dst, int64_t rows, int Wb, int Hb, int order, double ey,
                               AxisTables bx, AxisTables by, cudaStream_t st);
+// plain staged stage 1 (fallback): row-major B order, or v-major with vmajor = 1
 cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
                                   int m_base, int m_count, AxisTables xs, AxisTables ys,
-                                  TElem* T, cudaStream_t st);
+                                  TElem* T, cudaStream_t st, int vmajor = 0);
 // KB5 (TMA variant): warp-specialised, persistent, TMA-fed stage 1 over n_fuse (<= 4) planes
 // sharing one pass over Gamma.  Needs W_a <= 256 with W_a % 4 == 0, W_b % 4 == 0, W_b <= 512, H_b <= 256, the tensor maps of
 // Gamma (4D: u, v, j, m) and of the packed x-tables (3D uint32: x, u, plane slot).
@@ -139,6 +142,33 @@ struct PackGroupArgs {
 };
 cudaError_t launch_pack_xtable_group(const AxisTables* xs, int n_fuse, int Wa, int Wb, uint32_t* xpack,
                                      uint32_t* xblk, cudaStream_t st);
+// KB5w (refocus_w.cu): stage 1 with window reuse along x, for Gamma in the v-major B order
+// (CPI_GAMMA_VMAJOR).  One launch refocuses a batch of n_planes planes (groups of 4 share each
+// staged slab); fp64 accumulators in TMEM.  Tensor maps: Gamma 4D (v, u, j, local m) with box
+// (64, 1, 16, 1); step entries 3D uint32 (2 words per x, x padded to 128, u, plane) with box
+// (256, 1, 4).  launch_pack_w fills ent (32-bit j0 | t table [plane][u][x_pad]), the spans, the
+// m bands and the 64-bit step entries [plane][u][x_pad] from the coordinate tables.
+struct S1WArgs {
+    int Wa, Ha, Wb, Hb;
+    int m_base, m_count, m_block, m_stride;   // shard rows (see S1Args)
+    int n_planes;
+    int n_groups, n_xt, n_vb;                 // filled by the launcher
+    const int2* span;                         // [n_groups][n_xt][W_b] union j span per (group, x tile, u)
+    const int2* mband;                        // [n_groups][n_vb] union A-row band read by stage 2
+    float* T;                                 // plane p at T + p * t_plane: [W_a][H_a][H_b]
+    int64_t t_plane;
+};
+bool stage1_w_supported(int Wa, int Hb);
+int stage1_w_xtile();      // outputs x per tile (entry table x padding)
+int stage1_w_vblock();     // B rows v per tile (Gamma box width)
+int stage1_w_group();      // planes per group (entry box depth)
+int stage1_w_jbox();       // j rows per Gamma box
+int stage1_w_max_span();   // staged j rows per stage (plane groups with a longer span use refocus.cu)
+cudaError_t launch_pack_w(const int32_t* const* i0s_dev, const double* const* ts_dev, const int32_t* const* ylo_dev,
+                          const int32_t* const* yhi_dev, int n_planes, int Wa, int Wb, int Hb, uint32_t* ent,
+                          uint2* steps, int2* span, int2* mband, cudaStream_t st);
+cudaError_t launch_refocus_stage1_w(const CUtensorMap* tm_gamma, const CUtensorMap* tm_ent, const S1WArgs& a,
+                                    int num_sms, cudaStream_t st);
 // driver entry point cuTensorMapEncodeTiled (nullptr if unavailable)
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,

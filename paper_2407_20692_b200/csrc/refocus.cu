@@ -134,7 +134,7 @@ __device__ __forceinline__ void coords_block(double a, double b, double c_off, i
 // grid (ceil(Hb / kVG), m_count, ceil(Wa / 256)); thread = output x.
 __global__ void __launch_bounds__(kS1Threads)
 stage1_kernel(const float* __restrict__ gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
-              int m_base, AxisTables xs, AxisTables ys, TElem* __restrict__ T) {
+              int m_base, AxisTables xs, AxisTables ys, TElem* __restrict__ T, int vmajor) {
     extern __shared__ float sm[];   // [kVG][nj][kPad]
     const int v0 = blockIdx.x * kVG;
     const int m = m_base + blockIdx.y;
@@ -164,8 +164,13 @@ stage1_kernel(const float* __restrict__ gamma, int64_t ldg, int Wa, int Ha, int 
         // stage rows (v, j), columns [u0, u0+nu): Gamma[(m, j)][(v0+v, u)]
         for (int rr = threadIdx.x; rr < nv * nj; rr += kS1Threads) {
             const int v = rr / nj, jj = rr - v * nj;
-            const float* src = g_m + static_cast<int64_t>(jlo + jj) * ldg + static_cast<int64_t>(v0 + v) * Wb + u0;
             float* dst = sm + (v * nj + jj) * kPad;
+            if (vmajor) {   // B pixel (u, v) at column u * H_b + v (CPI_GAMMA_VMAJOR)
+                const float* col = g_m + static_cast<int64_t>(jlo + jj) * ldg + static_cast<int64_t>(u0) * Hb + v0 + v;
+                for (int k = 0; k < nu; ++k) dst[k] = __ldg(col + static_cast<int64_t>(k) * Hb);
+                continue;
+            }
+            const float* src = g_m + static_cast<int64_t>(jlo + jj) * ldg + static_cast<int64_t>(v0 + v) * Wb + u0;
             if (nu == kUC && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
                 const float4 p0 = __ldg(reinterpret_cast<const float4*>(src));
                 const float4 p1 = __ldg(reinterpret_cast<const float4*>(src) + 1);
@@ -865,6 +870,28 @@ resample_b_kernel(const float* __restrict__ src, float* __restrict__ dst, int Wb
     }
 }
 
+// v-major B order (CPI_GAMMA_VMAJOR, slot q = u * H_b + v): thread = one slot; consecutive threads
+// take consecutive v of one u, so the corner reads (n(v), n(v) + 1 of columns k(u), k(u) + 1) and
+// the stores are coalesced.
+__global__ void __launch_bounds__(256)
+resample_b_vmajor_kernel(const float* __restrict__ src, float* __restrict__ dst, int Wb, int Hb,
+                         const int32_t* __restrict__ bxi, const double* __restrict__ bxt,
+                         const int32_t* __restrict__ byi, const double* __restrict__ byt) {
+    const int64_t pb = static_cast<int64_t>(Wb) * Hb;
+    const int64_t q = static_cast<int64_t>(blockIdx.y) * 256 + threadIdx.x;
+    if (q >= pb) return;
+    const int64_t p = blockIdx.x;
+    const int u = static_cast<int>(q / Hb), v = static_cast<int>(q - static_cast<int64_t>(u) * Hb);
+    const float* s = src + p * pb;
+    const int n = __ldg(byi + v), k = __ldg(bxi + u);
+    const double tv = __ldg(byt + v), wv = __dadd_rn(1.0, -tv);
+    const double tu = __ldg(bxt + u), wu = __dadd_rn(1.0, -tu);
+    const int64_t c0 = static_cast<int64_t>(k) * Hb, c1 = c0 + Hb;
+    const double lo = wu * static_cast<double>(__ldg(s + c0 + n)) + tu * static_cast<double>(__ldg(s + c1 + n));
+    const double hi = wu * static_cast<double>(__ldg(s + c0 + n + 1)) + tu * static_cast<double>(__ldg(s + c1 + n + 1));
+    __stcs(dst + p * pb + q, static_cast<float>(wv * lo + tv * hi));
+}
+
 // Banded form (the default): CTA = (A pixel p, band of kRsV B rows v).  The band's B support
 // rows n in [lo, hi + 1] (n(v) is monotone in v, so the band ends bound it) are staged in
 // shared memory with coalesced 16-byte loads, de-blocked to row-major [n][k] with a padded row
@@ -948,11 +975,17 @@ resample_b_band_kernel(const float* __restrict__ src, float* __restrict__ dst, i
 
 }  // namespace
 
-cudaError_t launch_resample_b(const float* src, float* dst, int64_t rows, int Wb, int Hb, int ublocked, double ey,
+cudaError_t launch_resample_b(const float* src, float* dst, int64_t rows, int Wb, int Hb, int order, double ey,
                               AxisTables bx, AxisTables by, cudaStream_t st) {
     if (rows <= 0) return cudaSuccess;
     if (rows > 0x7fffffffLL || Wb < 2 || Hb < 2) return cudaErrorInvalidValue;
     const int64_t pb = static_cast<int64_t>(Wb) * Hb;
+    if (order == kOrderVMajor) {
+        const dim3 grid(static_cast<unsigned>(rows), static_cast<unsigned>((pb + 255) / 256));
+        resample_b_vmajor_kernel<<<grid, 256, 0, st>>>(src, dst, Wb, Hb, bx.i0, bx.t, by.i0, by.t);
+        return cudaGetLastError();
+    }
+    const int ublocked = order == kOrderUBlocked ? 1 : 0;
     const bool aligned = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
     // support rows of a band: |n(v0 + kRsV - 1) - n(v0)| + 2 <= ceil(|ey| (kRsV - 1)) + 3 (+1 margin)
     const double span = std::ceil(std::fabs(ey) * (kRsV - 1)) + 4;
@@ -1030,7 +1063,7 @@ cudaError_t launch_refocus_coords_group(const CoordsGroupArgs& g, int n_fuse, cu
 
 cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int Ha, int Wb, int Hb,
                                   int m_base, int m_count, AxisTables xs, AxisTables ys, TElem* T,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, int vmajor) {
     const size_t smem = static_cast<size_t>(kVG) * Wa * kPad * sizeof(float);
     if (smem > 48 * 1024) {   // per-device attribute: set before every launch
         cudaError_t e = cudaFuncSetAttribute(stage1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1038,7 +1071,7 @@ cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int H
         if (e != cudaSuccess) return e;
     }
     dim3 grid((Hb + kVG - 1) / kVG, m_count, (Wa + kS1Threads - 1) / kS1Threads);
-    stage1_kernel<<<grid, kS1Threads, smem, st>>>(gamma, ldg, Wa, Ha, Wb, Hb, m_base, xs, ys, T);
+    stage1_kernel<<<grid, kS1Threads, smem, st>>>(gamma, ldg, Wa, Ha, Wb, Hb, m_base, xs, ys, T, vmajor);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,488 @@
+// refocus_w.cu — KB5w: refocus stage 1 with window reuse along x (
+// SPEC.md:274 default map).
+//
+//   T_p[x][m][v] = sum_u [(1 - t(x,u)) Gamma(m, j0(x,u); v, u) + t(x,u) Gamma(m, j0(x,u) + 1; v, u)]
+//
+// The TMA stage 1 of refocus.cu gives every lane its own (x, v) samples, so every tap costs one
+// 4-byte shared-memory load and the shared-memory pipe bounds it.  Here all 32 lanes
+// of a warp work on the SAME (plane, x, u) sample and on 128 different B rows v (four per lane),
+// so the support (j0, t) is warp-uniform, and a warp walks 8 consecutive outputs x for one u: the
+// lower tap row of output x + 1 is j0(x) + d with d = 0 or 1 for alpha <= 1 (1 or 2 for
+// 1 < alpha <= 2), so the two rows (j0, j0 + 1) of consecutive outputs overlap and stay in
+// registers.  A warp-step is 128 v x 2 corners = 256 taps for d loads of 512 B (16 B per lane,
+// conflict-free), i.e. alpha / 2 shared-memory bytes per tap instead of 4 on average.  Skipped
+// samples and outputs outside the RoI add exact zeros without loads.
+//
+// The per-step logic is precomputed (pack_w_steps_kernel): a 64-bit step entry per (plane, u, x)
+// holds t, the byte offset of row j0 in the stage and the load action in the warp's walk order.
+//
+// Layout: Gamma with the B pixels in v-major order (include/cpi.h CPI_GAMMA_VMAJOR): column
+// q = u * H_b + v, so for one (A pixel (m, j), u) the v are contiguous.  A tile = (A row m, 128 B
+// rows v, 64 outputs x, group of 4 planes); warps 0-7 take planes 0-1 of the group and warps 8-15
+// planes 2-3, 8 outputs x each.  Per u, lane 0 of warp 0 TMA-loads the group's union j span of
+// Gamma[(m, j)][(u, v0 .. v0 + 127)] (<= 144 rows of 512 B) and the step entries of the tile into a
+// 3-deep ring.  fp32 partials stay in registers for 8 u and are then added into fp64 accumulators
+// that live in TMEM (64 per lane, 512 columns per CTA).  Tiles are ordered (m, v-block) outer and
+// (plane group, x tile) inner, so the Gamma slab of the tiles in flight (32 MB per (m, v-block)) is
+// reused from L2 by every plane group: Gamma crosses HBM about once per launch for the whole stack.
+#include <climits>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cpi {
+namespace {
+
+constexpr int kWX = 64;                            // outputs x per tile
+constexpr int kWV = 128;                           // B rows v per tile (4 per lane)
+constexpr int kWWarps = 16;
+constexpr int kWXW = 8;                            // outputs x per warp
+constexpr int kWF = 4;                             // planes per group
+constexpr int kWFW = 2;                            // planes per warp
+constexpr int kWBox = 16;                          // j rows per Gamma TMA box
+constexpr int kWRows = 144;                        // staged j rows (9 boxes); larger spans -> refocus.cu
+constexpr int kWStages = 3;
+constexpr int kWFlush = 8;                         // u per fp32 partial before the fp64 flush
+// no separate producer warp: a 17th warp would put 5 warps on one SM sub-partition and cap the
+// registers at 96 (the 64 fp32 partials per lane would spill); lane 0 of warp 0 issues the loads
+constexpr int kWThreads = 32 * kWWarps;
+constexpr int kWRowBytes = kWV * 4;                // 512 B per staged row
+constexpr int kWGBytes = kWRows * kWRowBytes;      // 72 KB of Gamma per stage
+constexpr int kWEBytes = kWF * kWX * 8;            // 2 KB of step entries per stage
+constexpr int kWStageBytes = kWGBytes + kWEBytes;
+constexpr int kWOffBar = kWStages * kWStageBytes;
+constexpr int kWSmem = kWOffBar + 2 * kWStages * 8 + 16 + 32;   // barriers, TMEM slot, producer cursor
+constexpr uint32_t kWInvalid = 0xFFFFFFFFu;        // 32-bit (j0 | t) table: skipped sample / padding x
+// 64-bit step entry of (plane, u, x) for a warp walking its 8 outputs x in order.  The warp keeps
+// two row registers, slot A for the even and slot B for the odd stage row of the pair (j0, j0 + 1):
+//   lo = weight of the even row (1 - t if j0 - span_lo is even, else t; fp32, exact), 0 for a
+//        skipped sample;
+//   hi = even row (bits 0-7) | odd row (bits 8-15) | load slot A (bit 16) | load slot B (bit 17) |
+//        the bits of 1.0f (0x3F800000, bits 23-29) for a used sample, so the odd row's weight is
+//        float(hi & 0x3F800000) - lo, exactly (and 0 - 0 = 0 for a skipped sample: its taps add
+//        exact zeros).  A row already in its slot is not reloaded.
+constexpr uint32_t kWOne = 0x3F800000u;
+constexpr uint32_t kWTmemCols = 512;
+
+static_assert(kWSmem <= 232448, "stage-1 window kernel exceeds the 227 KB shared-memory limit");
+static_assert(kWWarps * kWXW == kWX * (kWF / kWFW), "warps x outputs x planes must cover the tile");
+
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float2 upk2(uint64_t v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+// d = w * g + c on both fp32 halves (sm_100a fma.rn.f32x2), w = (w, w) pre-packed
+__device__ __forceinline__ uint64_t fma2(uint64_t w, uint64_t g, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(w), "l"(g), "l"(c));
+    return d;
+}
+
+// g = 16 bytes of shared memory at addr if flag != 0 (a warp-uniform predicate: no wavefront
+// when off), else unchanged
+__device__ __forceinline__ void w_lds_if(uint4& g, uint32_t addr, uint32_t flag) {
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %4, 0;\n\t"
+        "@p ld.shared.v4.u32 {%0, %1, %2, %3}, [%5];\n\t}"
+        : "+r"(g.x), "+r"(g.y), "+r"(g.z), "+r"(g.w)
+        : "r"(flag), "r"(addr)
+        : "memory");
+}
+
+__device__ __forceinline__ int w_shard_row(const S1WArgs& a, int l) {
+    return a.m_base + (l / a.m_block) * a.m_stride + l % a.m_block;
+}
+
+// tile t -> (local A row, v block) outer, (plane group, x tile) inner
+struct WTile { int ml, vb, g, xt; };
+__device__ __forceinline__ WTile w_tile(const S1WArgs& a, int t) {
+    const int inner = a.n_groups * a.n_xt;
+    const int o = t / inner, i = t - o * inner;
+    WTile w;
+    w.ml = o / a.n_vb;
+    w.vb = o - w.ml * a.n_vb;
+    w.g = i / a.n_xt;
+    w.xt = i - w.g * a.n_xt;
+    return w;
+}
+__device__ __forceinline__ bool w_needed(const S1WArgs& a, const WTile& w, int m) {
+    const int2 b = __ldg(a.mband + w.g * a.n_vb + w.vb);
+    return m >= b.x && m <= b.y;
+}
+
+// Producer cursor: the next (tile, u) stage to load, in the consumers' order.
+struct WProducer {
+    int t, u, stage;
+    uint32_t phase;
+    bool tile_ok;   // tile t checked and needed
+};
+// Issue the next stage (if any) into the ring; waits until its slot is free.
+__device__ __forceinline__ void w_produce(WProducer& p, const S1WArgs& a, int n_tiles, const CUtensorMap* tm_g,
+                                          const CUtensorMap* tm_e, uint8_t* smem, uint64_t* full, uint64_t* empty) {
+    while (p.t < n_tiles) {
+        const WTile w = w_tile(a, p.t);
+        if (!p.tile_ok) {
+            if (!w_needed(a, w, w_shard_row(a, w.ml))) { p.t += gridDim.x; continue; }
+            p.tile_ok = true;
+            p.u = 0;
+        }
+        const int2* sp_row = a.span + static_cast<int64_t>(w.g * a.n_xt + w.xt) * a.Wb;
+        while (p.u < a.Wb) {
+            const int2 sp = __ldg(sp_row + p.u);
+            if (sp.y >= sp.x) {
+                const int nb = (sp.y - sp.x + kWBox) / kWBox;
+                mbar_wait(&empty[p.stage], p.phase ^ 1);
+                mbar_expect_tx(&full[p.stage], nb * kWBox * kWRowBytes + kWEBytes);
+                uint8_t* dst = smem + p.stage * kWStageBytes;
+                for (int b = 0; b < nb; ++b)
+                    tma_load_4d(dst + b * kWBox * kWRowBytes, tm_g, &full[p.stage], w.vb * kWV, p.u,
+                                sp.x + b * kWBox, w.ml);
+                tma_load_3d(dst + kWGBytes, tm_e, &full[p.stage], 2 * w.xt * kWX, p.u, w.g * kWF);
+                if (++p.stage == kWStages) { p.stage = 0; p.phase ^= 1; }
+                ++p.u;
+                return;
+            }
+            ++p.u;
+        }
+        p.tile_ok = false;
+        p.t += gridDim.x;
+    }
+}
+
+// fp64 accumulators of a warp in TMEM: plane pl (of the warp's 2), output i, v slot k (of the
+// lane's 4) at columns 64 pl + 8 i + 2 k (+1: high word).  r holds columns [32 half, +32) of one
+// plane (outputs 4 half .. 4 half + 3); adds the fp32 partials (r ignored when first).
+__device__ __forceinline__ void w_combine(const uint64_t (&pp)[kWXW][2], uint32_t (&r)[32], int half, bool first) {
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii) {
+        const int i = 4 * half + ii;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const float2 p = upk2(pp[i][q]);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int c = 8 * ii + 4 * q + 2 * h;
+                double d = static_cast<double>(h ? p.y : p.x);
+                if (!first) d += __hiloint2double(static_cast<int>(r[c + 1]), static_cast<int>(r[c]));
+                r[c] = static_cast<uint32_t>(__double2loint(d));
+                r[c + 1] = static_cast<uint32_t>(__double2hiint(d));
+            }
+        }
+    }
+}
+// Add the fp32 partials into the fp64 accumulators in TMEM and zero them.
+__device__ __forceinline__ void w_flush(uint64_t (&part)[kWFW][kWXW][2], uint32_t tbase, bool first) {
+#pragma unroll
+    for (int pl = 0; pl < kWFW; ++pl)
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            uint32_t r[32];
+            const uint32_t col = tbase + 64 * pl + 32 * half;
+            if (!first) {
+                tmem_ld_32x32b_x32(col, r);
+                tmem_wait_ld();
+            }
+            w_combine(part[pl], r, half, first);
+            tmem_st_32x32b_x32(col, r);
+        }
+    tmem_wait_st();
+#pragma unroll
+    for (int pl = 0; pl < kWFW; ++pl)
+#pragma unroll
+        for (int i = 0; i < kWXW; ++i) part[pl][i][0] = part[pl][i][1] = 0ull;
+}
+
+__global__ void __launch_bounds__(kWThreads, 1)
+stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_e, S1WArgs a) {
+    extern __shared__ __align__(1024) uint8_t w_smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(w_smem + kWOffBar);
+    uint64_t* empty = full + kWStages;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(empty + kWStages);
+    // the producer's cursor lives in shared memory: only lane 0 of warp 0 touches it, and keeping
+    // it out of the register file leaves the registers to the fp32 partials
+    WProducer* prod = reinterpret_cast<WProducer*>(w_smem + kWOffBar + 2 * kWStages * 8 + 16);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kWStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kWWarps);
+        }
+        fence_mbar_init();
+        *prod = WProducer{static_cast<int>(blockIdx.x), 0, 0, 0u, false};
+    }
+    if (warp == 0) tmem_alloc(tslot, kWTmemCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const int n_tiles = a.m_count * a.n_vb * a.n_groups * a.n_xt;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tm_g);
+        tma_prefetch_desc(&tm_e);
+        WProducer p = *prod;
+        for (int k = 0; k < kWStages; ++k) w_produce(p, a, n_tiles, &tm_g, &tm_e, w_smem, full, empty);
+        *prod = p;
+    }
+
+    // warp: planes 2 (warp / 8) + {0, 1} of the group, outputs x = x tile + 8 (warp % 8) + i;
+    // lane: B rows v = v block + 4 lane + {0..3}
+    const int wp = warp >> 3, wx = warp & 7;
+    const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + static_cast<uint32_t>(warp >> 2) * 128u;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const WTile w = w_tile(a, t);
+        const int m = w_shard_row(a, w.ml);
+        if (!w_needed(a, w, m)) continue;
+        const int nfw = min(kWFW, a.n_planes - w.g * kWF - kWFW * wp);   // this warp's planes (may be <= 0)
+        const int2* sp_row = a.span + static_cast<int64_t>(w.g * a.n_xt + w.xt) * a.Wb;
+        uint64_t part[kWFW][kWXW][2];
+#pragma unroll
+        for (int pl = 0; pl < kWFW; ++pl)
+#pragma unroll
+            for (int i = 0; i < kWXW; ++i) part[pl][i][0] = part[pl][i][1] = 0ull;
+        bool first = true;   // no fp64 partial in TMEM yet for this tile
+        int nst = 0;
+        for (int u = 0; u < a.Wb; ++u) {
+            const int2 sp = __ldg(sp_row + u);
+            if (sp.y < sp.x) continue;
+            mbar_wait(&full[stage], phase);
+            const uint8_t* sbase = w_smem + stage * kWStageBytes;
+            const uint4* E = reinterpret_cast<const uint4*>(sbase + kWGBytes);
+            const uint32_t gaddr = smem_u32(sbase) + 16u * lane;   // this lane's 16 bytes (4 v) of row 0
+#pragma unroll
+            for (int pl = 0; pl < kWFW; ++pl) {
+                if (pl < nfw) {
+                    const uint4* Ep = E + ((kWFW * wp + pl) * kWX + wx * kWXW) / 2;
+                    uint4 ga = make_uint4(0u, 0u, 0u, 0u), gb = ga;   // even / odd row of the window
+#pragma unroll
+                    for (int i = 0; i < kWXW; i += 2) {
+                        const uint4 e2 = Ep[i / 2];   // entries of outputs i, i + 1 (broadcast)
+#pragma unroll
+                        for (int k = 0; k < 2; ++k) {
+                            const uint32_t lo = k ? e2.z : e2.x, hi = k ? e2.w : e2.y;
+                            w_lds_if(ga, gaddr + ((hi & 0xFFu) << 9), hi & 0x10000u);
+                            w_lds_if(gb, gaddr + ((hi >> 8 & 0xFFu) << 9), hi & 0x20000u);
+                            const float wa = __uint_as_float(lo);
+                            const float wb = __uint_as_float(hi & kWOne) - wa;
+                            const uint64_t wa2 = pk2(wa, wa), wb2 = pk2(wb, wb);
+                            uint64_t* pp = part[pl][i + k];
+                            pp[0] = fma2(wb2, pk2(__uint_as_float(gb.x), __uint_as_float(gb.y)),
+                                         fma2(wa2, pk2(__uint_as_float(ga.x), __uint_as_float(ga.y)), pp[0]));
+                            pp[1] = fma2(wb2, pk2(__uint_as_float(gb.z), __uint_as_float(gb.w)),
+                                         fma2(wa2, pk2(__uint_as_float(ga.z), __uint_as_float(ga.w)), pp[1]));
+                        }
+                    }
+                }
+            }
+            // release the stage (generic-proxy reads before the async-proxy refill)
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (warp == 0 && lane == 0) {   // refill this slot once every warp released it
+                WProducer p = *prod;
+                w_produce(p, a, n_tiles, &tm_g, &tm_e, w_smem, full, empty);
+                *prod = p;
+            }
+            __syncwarp();
+            if (++stage == kWStages) { stage = 0; phase ^= 1; }
+            if (++nst == kWFlush) {
+                w_flush(part, tbase, first);
+                first = false;
+                nst = 0;
+            }
+        }
+        // tile end: fp64 sum (TMEM + partial) rounded once to fp32 T, for v < H_b, x < W_a
+        const int v = w.vb * kWV + 4 * lane;
+        const int x0 = w.xt * kWX + wx * kWXW;
+#pragma unroll
+        for (int pl = 0; pl < kWFW; ++pl) {
+            if (pl < nfw) {
+                float* Tf = a.T + static_cast<int64_t>(w.g * kWF + kWFW * wp + pl) * a.t_plane;
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    uint32_t r[32];
+                    if (!first) {
+                        tmem_ld_32x32b_x32(tbase + 64 * pl + 32 * half, r);
+                        tmem_wait_ld();
+                    }
+                    w_combine(part[pl], r, half, first);
+#pragma unroll
+                    for (int ii = 0; ii < 4; ++ii) {
+                        const int x = x0 + 4 * half + ii;
+                        float o[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            o[k] = static_cast<float>(__hiloint2double(static_cast<int>(r[8 * ii + 2 * k + 1]),
+                                                                       static_cast<int>(r[8 * ii + 2 * k])));
+                        if (x < a.Wa && v < a.Hb)
+                            *reinterpret_cast<float4*>(Tf + (static_cast<int64_t>(x) * a.Ha + m) * a.Hb + v) =
+                                make_float4(o[0], o[1], o[2], o[3]);
+                    }
+                }
+            }
+        }
+    }
+    // all warps done with TMEM before warp 0 frees it
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem, kWTmemCols);
+    }
+}
+
+// ---- pack: per-plane entries, per-(group, x tile, u) spans, step entries, m bands ----------
+// entry(f, u, x) = j0 << 23 | round(t * 2^23) (a t that rounds to 1 moves to j0 + 1 with t = 0),
+// kWInvalid for skipped samples and for the padding columns x >= W_a.
+__global__ void pack_w_entries_kernel(const int32_t* const* i0s, const double* const* ts, int Wa, int Wb, int xpad,
+                                      uint32_t* __restrict__ ent) {
+    const int u = blockIdx.x, f = blockIdx.y;
+    const int32_t* i0 = i0s[f];
+    const double* tt = ts[f];
+    for (int x = threadIdx.x; x < xpad; x += blockDim.x) {
+        uint32_t e = kWInvalid;
+        if (x < Wa) {
+            const int64_t idx = static_cast<int64_t>(u) * Wa + x;
+            const int j = __ldg(i0 + idx);
+            if (j >= 0) {
+                uint32_t tq = static_cast<uint32_t>(__double2uint_rn(__ldg(tt + idx) * 8388608.0));
+                int jj = j;
+                if (tq >= 8388608u) { tq = 0; jj += 1; }
+                e = (static_cast<uint32_t>(jj) << 23) | tq;
+            }
+        }
+        ent[(static_cast<int64_t>(f) * Wb + u) * xpad + x] = e;
+    }
+}
+// span(g, xt, u) = [min j0, max j0 + 1] over the group's planes and the tile's outputs (lo > hi: none)
+__global__ void pack_w_span_kernel(const uint32_t* __restrict__ ent, int n_planes, int Wb, int xpad, int n_xt,
+                                   int2* __restrict__ span) {
+    const int u = blockIdx.x, g = blockIdx.y, xt = blockIdx.z;
+    int lo = INT_MAX, hi = -1;
+    for (int f = g * kWF; f < min(n_planes, g * kWF + kWF); ++f) {
+        const uint32_t e = __ldg(ent + (static_cast<int64_t>(f) * Wb + u) * xpad + xt * kWX + threadIdx.x);
+        if (e != kWInvalid) {
+            const int j = static_cast<int>(e >> 23);
+            lo = min(lo, j);
+            hi = max(hi, j + 1);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    __shared__ int slo[kWX / 32], shi[kWX / 32];
+    if ((threadIdx.x & 31) == 0) { slo[threadIdx.x >> 5] = lo; shi[threadIdx.x >> 5] = hi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < kWX / 32; ++k) { lo = min(lo, slo[k]); hi = max(hi, shi[k]); }
+        span[(static_cast<int64_t>(g) * n_xt + xt) * Wb + u] = hi >= lo ? make_int2(lo, hi) : make_int2(1, 0);
+    }
+}
+// step entries (see kWOne): one thread per (plane, u, warp block of 8 outputs x) scans the block
+// in the warp's walk order, tracking which stage row each slot holds; rows are relative to the
+// span of (group, x tile, u).
+__global__ void pack_w_steps_kernel(const uint32_t* __restrict__ ent, const int2* __restrict__ span, int Wb, int xpad,
+                                    int n_xt, uint2* __restrict__ steps) {
+    const int u = blockIdx.x, f = blockIdx.y, blk = threadIdx.x;
+    if (blk >= xpad / kWXW) return;
+    const int x0 = blk * kWXW, xt = x0 / kWX, g = f / kWF;
+    const int2 sp = __ldg(span + (static_cast<int64_t>(g) * n_xt + xt) * Wb + u);
+    const int64_t base = (static_cast<int64_t>(f) * Wb + u) * xpad + x0;
+    int ra = -1, rb = -1;   // stage rows in slots A (even) and B (odd)
+    for (int i = 0; i < kWXW; ++i) {
+        const uint32_t e = __ldg(ent + base + i);
+        uint2 s2 = make_uint2(0u, 0u);
+        if (e != kWInvalid) {
+            const int r0 = static_cast<int>(e >> 23) - sp.x;               // stage row of j0 (< kWRows - 1)
+            const float t = static_cast<float>(e & 0x7FFFFFu) * (1.f / 8388608.f);   // exact
+            const bool ev = (r0 & 1) == 0;
+            const int re = ev ? r0 : r0 + 1, ro = ev ? r0 + 1 : r0;
+            const uint32_t la = ra != re, lb = rb != ro;
+            ra = re;
+            rb = ro;
+            s2.x = __float_as_uint(ev ? 1.f - t : t);                     // exact
+            s2.y = static_cast<uint32_t>(re) | (static_cast<uint32_t>(ro) << 8) | (la << 16) | (lb << 17) | kWOne;
+        }
+        steps[base + i] = s2;
+    }
+}
+// mband(g, vb) = union over the group's planes and the block's B rows v of the A rows stage 2
+// reads, [lo_y(v), hi_y(v)] (tiles outside it are not computed)
+__global__ void pack_w_mband_kernel(const int32_t* const* ylo, const int32_t* const* yhi, int n_planes, int Hb, int n_vb,
+                                    int2* __restrict__ mband) {
+    const int vb = blockIdx.x, g = blockIdx.y;
+    int lo = INT_MAX, hi = -1;
+    const int v = vb * kWV + threadIdx.x;
+    if (v < Hb)
+        for (int f = g * kWF; f < min(n_planes, g * kWF + kWF); ++f) {
+            const int l = __ldg(ylo[f] + v), h = __ldg(yhi[f] + v);
+            if (h >= l) { lo = min(lo, l); hi = max(hi, h); }
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    __shared__ int slo[kWV / 32], shi[kWV / 32];
+    if ((threadIdx.x & 31) == 0) { slo[threadIdx.x >> 5] = lo; shi[threadIdx.x >> 5] = hi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < kWV / 32; ++k) { lo = min(lo, slo[k]); hi = max(hi, shi[k]); }
+        mband[g * n_vb + vb] = hi >= lo ? make_int2(lo, hi) : make_int2(1, 0);
+    }
+}
+
+}  // namespace
+
+int stage1_w_xtile() { return kWX; }
+int stage1_w_vblock() { return kWV; }
+int stage1_w_group() { return kWF; }
+int stage1_w_jbox() { return kWBox; }
+int stage1_w_max_span() { return kWRows; }
+bool stage1_w_supported(int Wa, int Hb) { return Wa >= 2 && Wa <= 256 && Hb >= 4 && Hb % 4 == 0; }
+
+cudaError_t launch_pack_w(const int32_t* const* i0s_dev, const double* const* ts_dev, const int32_t* const* ylo_dev,
+                          const int32_t* const* yhi_dev, int n_planes, int Wa, int Wb, int Hb, uint32_t* ent,
+                          uint2* steps, int2* span, int2* mband, cudaStream_t st) {
+    const int xpad = ((Wa + kWX - 1) / kWX) * kWX, n_xt = xpad / kWX;
+    const int n_groups = (n_planes + kWF - 1) / kWF, n_vb = (Hb + kWV - 1) / kWV;
+    pack_w_entries_kernel<<<dim3(Wb, n_planes), 128, 0, st>>>(i0s_dev, ts_dev, Wa, Wb, xpad, ent);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    pack_w_span_kernel<<<dim3(Wb, n_groups, n_xt), kWX, 0, st>>>(ent, n_planes, Wb, xpad, n_xt, span);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    pack_w_steps_kernel<<<dim3(Wb, n_planes), ((xpad / kWXW + 31) / 32) * 32, 0, st>>>(ent, span, Wb, xpad, n_xt, steps);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    pack_w_mband_kernel<<<dim3(n_vb, n_groups), kWV, 0, st>>>(ylo_dev, yhi_dev, n_planes, Hb, n_vb, mband);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_refocus_stage1_w(const CUtensorMap* tm_gamma, const CUtensorMap* tm_ent, const S1WArgs& a_in,
+                                    int num_sms, cudaStream_t st) {
+    S1WArgs a = a_in;
+    a.n_xt = (a.Wa + kWX - 1) / kWX;
+    a.n_vb = (a.Hb + kWV - 1) / kWV;
+    a.n_groups = (a.n_planes + kWF - 1) / kWF;
+    if (a.m_block <= 0) { a.m_block = a.m_count > 0 ? a.m_count : 1; a.m_stride = a.m_block; }
+    const int64_t tiles = static_cast<int64_t>(a.m_count) * a.n_vb * a.n_groups * a.n_xt;
+    if (tiles <= 0) return cudaSuccess;
+    if (tiles > 0x7fffffffLL) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(stage1_w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmem);
+    if (e != cudaSuccess) return e;
+    const int grid = static_cast<int>(tiles < num_sms ? tiles : num_sms);
+    stage1_w_kernel<<<grid, kWThreads, kWSmem, st>>>(*tm_gamma, *tm_ent, a);
+    return cudaGetLastError();
+}
+
+}  // namespace cpi
