@@ -55,7 +55,7 @@ def parse():
                    help="pair-sum GEMM: fp4 = tcgen05 kind::mxf4 on E2M1 0/1 (default, exact), "
                         "tc = kind::i8, popc = popcount(AND)")
     p.add_argument("--roi", default="full", choices=["full", "128", "tiny"])
-    p.add_argument("--gamma-order", default=STEP_GAMMA_ORDER, choices=["ublocked", "rowmajor"],
+    p.add_argument("--gamma-order", default=STEP_GAMMA_ORDER, choices=["ublocked", "rowmajor", "vmajor"],
                    help="column order of the step's Gamma (include/cpi.h CPI_GAMMA_UBLOCKED)")
     p.add_argument("--parallel-mode", default="rows", choices=["rows", "tiles"],
                    help="multi-GPU: rows = frame sharding + panelised reduce-scatter (north_star); tiles = "

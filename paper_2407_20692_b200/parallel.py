@@ -172,13 +172,17 @@ def correlate_and_refocus(backend, frames_local, roi_a, roi_b, alphas=None, grou
 
 def _refocus_shard(backend, plan, Wa, gamma_rows, alphas, affine, group):
     """Refocus this rank's block-cyclic Gamma rows and sum the partial planes over ranks
-    (refocusing is linear in Gamma).  affine rows replace alphas when given."""
+    (refocusing is linear in Gamma).  affine rows replace alphas when given.
+    The partial planes are summed in fp64 and rounded once to fp32: each
+    rank's fp32 plane is within 2^-24 of its fp64 value relative to that rank's M, M is additive
+    over row shards, so the sum stays within ~2^-23 M of the single-GPU plane."""
     if affine is None and (alphas is None or not len(alphas)):
         return None
     args = (gamma_rows, plan.m_base * Wa, plan.m_count * Wa, plan.block, plan.stride)
     planes = backend.refocus(alphas, *args) if affine is None else backend.refocus(None, *args, affine=affine)
-    dist.all_reduce(planes, op=dist.ReduceOp.SUM, group=group)
-    return planes
+    p64 = planes.to(torch.float64)
+    dist.all_reduce(p64, op=dist.ReduceOp.SUM, group=group)
+    return p64.to(torch.float32)
 
 
 def _gather_frames(frames_local, group, device) -> torch.Tensor:

@@ -129,7 +129,7 @@ def test_vmajor_cyclic_shards_sum_to_whole():
         Gs[pix] = G[pix]
         _assert_planes(R, Gs, dims, al)
         total += R
-    np.testing.assert_allclose(total, whole, rtol=1e-5, atol=1e-7)
+    _assert_planes(total, G, dims, al)       # the shards' sum meets the whole-plane bar
 
 
 @pytest.mark.parametrize("variant", ["tc", "fp4"])
