@@ -64,7 +64,7 @@ def parse():
                    help="run the frame-sharded multi-GPU pipeline (NCCL) even at one rank (tests its code path)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-pixels", type=int, default=256, help="oracle sample: refocused output pixels")
+    p.add_argument("--cpu-pixels", type=int, default=48, help="oracle sample: refocused output pixels per alpha")
     return p.parse_args()
 
 
@@ -188,54 +188,84 @@ def refocus_span_bytes(dims, alphas):
 
 
 # ------------------------------------------------------------------ CPU baseline ----------
-def cpu_baseline(frames_np, roi_a, roi_b, alphas, n_rows, n_pix, step_planes, waves=(2, 4)):
-    """The oracle as it stands, timed on a bounded sample of the same workload (rank 0, N=1).
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    Its phases scale differently, so they are timed separately and extrapolated to the full
-    step: single-pixel sums over every pixel (timed in full); pair sums = a fixed part (frame
-    unpacking) + a per-A-pixel part, measured with 2*cores and 4*cores A pixels on all cores;
-    refocusing = per output pixel, measured on n_pix pixels of one plane."""
+
+def _oracle_step_estimate(oracle, frames_np, roi_a, roi_b, alphas, step_planes, threads, n_s, rows_pair, n_pix, G):
+    """One timed pass of the oracle over a bounded sample of the step, extrapolated to the step.
+    Every phase is linear in what is sampled: single-pixel sums and pair sums in the frame count
+    (first n_s frames), pair sums also in the A pixels (rows_pair and 2 rows_pair rows, all B
+    pixels: fixed unpacking + per-row part), refocusing in output pixels and planes (n_pix pixels
+    at each of 8 alphas spread over the stack's grid)."""
+    n = frames_np.shape[0]
+    fs = frames_np[:n_s]
+    p_a = roi_a[2] * roi_a[3]
+    t0 = time.perf_counter()
+    s_a = oracle.marginals(fs, roi_a)
+    s_b = oracle.marginals(fs, roi_b)
+    t_marg = (time.perf_counter() - t0) * n / n_s
+    r1 = np.linspace(0, p_a - 1, rows_pair).astype(np.int64)
+    r2 = np.linspace(0, p_a - 1, 2 * rows_pair).astype(np.int64)
+    t0 = time.perf_counter()
+    oracle.pair_sums(fs, roi_a, roi_b, rows=r1, threads=threads)
+    t1 = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    s_ab = oracle.pair_sums(fs, roi_a, roi_b, rows=r2, threads=threads)
+    g = oracle.gamma(s_ab, s_a[r2], s_b, n_s)                      # Eq. (1) on the sampled rows
+    t2 = time.perf_counter() - t0
+    per_row = max(t2 - t1, 1e-9) / rows_pair
+    fixed = max(t1 - rows_pair * per_row, 0.0)
+    t_pairs = (fixed + per_row * p_a) * n / n_s
+    Wa, Ha, Wb, Hb = roi_a[2], roi_a[3], roi_b[2], roi_b[3]
+    if G[0, 0] != G[0, 0]:                                            # first pass: fill the refocus input
+        G[:] = g[np.arange(p_a) % g.shape[0]].astype(np.float32)      # (refocus cost is data-independent)
+    sel = np.unique(np.linspace(0, len(alphas) - 1, 8).astype(int))
+    rng = np.random.default_rng(0)
+    pix = np.stack([rng.integers(0, Wa, n_pix), rng.integers(0, Ha, n_pix)], 1)
+    t0 = time.perf_counter()
+    oracle.refocus(G, (Wa, Ha, Wb, Hb), np.asarray(alphas)[sel], pixels=pix, threads=threads)
+    t_ref = (time.perf_counter() - t0) / (len(sel) * n_pix) * (Wa * Ha) * step_planes
+    return {"marginals": t_marg, "pair_sums": t_pairs, "refocus": t_ref}
+
+
+def cpu_baseline(frames_np, roi_a, roi_b, alphas, n_pix, step_planes, reps=3, one_core=True):
+    """The oracle as it stands, timed on the box's host cores on a bounded sample of the same
+    workload (rank 0, N = 1; SURVEY §8(d) "oracle timed beside it"): >= 3 repetitions on all
+    cores (median), plus one repetition on 1 core; CPU model and core count reported."""
     import oracle
     oracle.build()
     cores = os.cpu_count() or 1
     n = frames_np.shape[0]
-    p_a = roi_a[2] * roi_a[3]
-    t0 = time.perf_counter()
-    s_a = oracle.marginals(frames_np, roi_a)
-    s_b = oracle.marginals(frames_np, roi_b)
-    t_marg = time.perf_counter() - t0
-    r1, r2 = waves[0] * cores, waves[1] * cores
-    rows1 = np.linspace(0, p_a - 1, r1).astype(np.int64)
-    rows2 = np.linspace(0, p_a - 1, r2).astype(np.int64)
-    t0 = time.perf_counter()
-    oracle.pair_sums(frames_np, roi_a, roi_b, rows=rows1, threads=cores)
-    t1 = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    s_ab = oracle.pair_sums(frames_np, roi_a, roi_b, rows=rows2, threads=cores)
-    g = oracle.gamma(s_ab, s_a[rows2], s_b, n)
-    t2 = time.perf_counter() - t0
-    per_wave = max(t2 - t1, 1e-9) / (waves[1] - waves[0])   # one A pixel per core
-    fixed = max(t1 - waves[0] * per_wave, 0.0)
-    t_pairs_full = fixed + per_wave * p_a / cores
-    Wa, Ha, Wb, Hb = roi_a[2], roi_a[3], roi_b[2], roi_b[3]
-    G = np.empty((p_a, Wb * Hb), dtype=np.float32)
-    G[:] = g[np.arange(p_a) % r2].astype(np.float32)   # refocus cost is data-independent
-    rng = np.random.default_rng(0)
-    pix = np.stack([rng.integers(0, Wa, n_pix), rng.integers(0, Ha, n_pix)], 1)
-    alpha = float(alphas[len(alphas) // 3])
-    t0 = time.perf_counter()
-    oracle.refocus(G, (Wa, Ha, Wb, Hb), [alpha], pixels=pix, threads=cores)
-    t_ref = time.perf_counter() - t0
-    t_ref_full = t_ref * (Wa * Ha / n_pix) * step_planes
-    est_step = t_marg + t_pairs_full + t_ref_full
-    return {"value": n / est_step, "unit": "frames/s", "cores": cores, "kind": "oracle",
-            "sample": (f"single-pixel sums over all {p_a}+{Wb*Hb} pixels x {n} frames ({t_marg:.1f} s); "
-                       f"pair sums for {r1} and {r2} of {p_a} A pixels x all B pixels x all frames "
-                       f"({t1:.1f} s, {t2:.1f} s) -> fixed {fixed:.1f} s + {per_wave:.2f} s per {cores} A pixels; "
-                       f"refocus of {n_pix} of {Wa*Ha} output pixels of 1 plane ({t_ref:.1f} s); step time "
-                       f"extrapolated to all A pixels and {step_planes} planes"),
-            "extrapolated_step_s": est_step,
-            "extrapolated_parts_s": {"marginals": t_marg, "pair_sums": t_pairs_full, "refocus": t_ref_full}}
+    n_s = min(n, 512)
+    G = np.empty((roi_a[2] * roi_a[3], roi_b[2] * roi_b[3]), dtype=np.float32)   # one refocus input for all passes
+    G[0, 0] = np.nan
+    runs = [_oracle_step_estimate(oracle, frames_np, roi_a, roi_b, alphas, step_planes, cores, n_s, cores, n_pix, G)
+            for _ in range(reps)]
+    tot = [sum(r.values()) for r in runs]
+    med = runs[int(np.argsort(tot)[len(tot) // 2])]
+    est = sum(med.values())
+    out = {"value": n / est, "unit": "frames/s", "cores": cores, "kind": "oracle", "cpu_model": _cpu_model(),
+           "reps": reps, "rep_step_s": tot,
+           "sample": (f"first {n_s} of {n} frames; single-pixel sums over all {roi_a[2] * roi_a[3]}+"
+                      f"{roi_b[2] * roi_b[3]} pixels; pair sums for {cores} and {2 * cores} A pixels x all B "
+                      f"pixels; refocus of {n_pix} output pixels at 8 alphas spread over the {len(alphas)}-plane "
+                      f"grid; each phase extrapolated linearly (frames, A pixels, output pixels x planes) to the "
+                      f"step; median of {reps} repetitions on {cores} threads"),
+           "extrapolated_step_s": est, "extrapolated_parts_s": med}
+    if one_core:
+        r1 = _oracle_step_estimate(oracle, frames_np, roi_a, roi_b, alphas, step_planes, 1, min(n_s, 256), 1,
+                                   max(4, n_pix // 8), G)
+        out["one_core"] = {"value": n / sum(r1.values()), "unit": "frames/s", "extrapolated_parts_s": r1,
+                           "sample": "first 256 frames, pair sums for 1 and 2 A pixels, refocus of "
+                                     f"{max(4, n_pix // 8)} pixels at 8 alphas, 1 repetition on 1 thread"}
+    return out
 
 
 # ------------------------------------------------------------------ reference arm ---------
@@ -249,7 +279,8 @@ def run_reference(args, json_out=None):
     vals = []
     last = None
     for i in range(args.warmup + args.steps):
-        r = cpu_baseline(frames, roi_a, roi_b, alphas, 0, max(1, args.cpu_pixels // 4), args.planes, waves=(1, 2))
+        r = cpu_baseline(frames, roi_a, roi_b, alphas, max(8, args.cpu_pixels // 4), args.planes, reps=1,
+                         one_core=False)
         if i >= args.warmup:
             vals.append(r["value"])
             last = r
@@ -483,7 +514,7 @@ def main():
                      "note": "same frames, epilogue and Gamma, timed after the step loop; not part of value"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(frames_np, roi_a, roi_b, alphas, 0, args.cpu_pixels, args.planes)
+        cpu = cpu_baseline(frames_np, roi_a, roi_b, alphas, args.cpu_pixels, args.planes)
     out = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",

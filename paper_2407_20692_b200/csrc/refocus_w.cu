@@ -21,7 +21,7 @@
 // rows v, 64 outputs x, group of 4 planes); warps 0-7 take planes 0-1 of the group and warps 8-15
 // planes 2-3, 8 outputs x each.  Per u, lane 0 of warp 0 TMA-loads the group's union j span of
 // Gamma[(m, j)][(u, v0 .. v0 + 127)] (<= 144 rows of 512 B) and the step entries of the tile into a
-// 3-deep ring.  fp32 partials stay in registers for 8 u and are then added into fp64 accumulators
+// 3-deep ring (the last warp to release a slot refills it).  fp32 partials stay in registers for 8 u and are then added into fp64 accumulators
 // that live in TMEM (64 per lane, 512 columns per CTA).  Tiles are ordered (m, v-block) outer and
 // (plane group, x tile) inner, so the Gamma slab of the tiles in flight (32 MB per (m, v-block)) is
 // reused from L2 by every plane group: Gamma crosses HBM about once per launch for the whole stack.
@@ -44,14 +44,19 @@ constexpr int kWRows = 144;                        // staged j rows (9 boxes); l
 constexpr int kWStages = 3;
 constexpr int kWFlush = 8;                         // u per fp32 partial before the fp64 flush
 // no separate producer warp: a 17th warp would put 5 warps on one SM sub-partition and cap the
-// registers at 96 (the 64 fp32 partials per lane would spill); lane 0 of warp 0 issues the loads
+// registers at 96 (the 64 fp32 partials per lane would spill); the last warp to release a ring
+// slot issues its refill
 constexpr int kWThreads = 32 * kWWarps;
 constexpr int kWRowBytes = kWV * 4;                // 512 B per staged row
 constexpr int kWGBytes = kWRows * kWRowBytes;      // 72 KB of Gamma per stage
 constexpr int kWEBytes = kWF * kWX * 8;            // 2 KB of step entries per stage
 constexpr int kWStageBytes = kWGBytes + kWEBytes;
-constexpr int kWOffBar = kWStages * kWStageBytes;
-constexpr int kWSmem = kWOffBar + 2 * kWStages * 8 + 16 + 32;   // barriers, TMEM slot, producer cursor
+constexpr int kWOffBar = kWStages * kWStageBytes;              // full barriers
+constexpr int kWOffHdr = kWOffBar + kWStages * 8;               // stage headers (16 B each)
+constexpr int kWOffCur = kWOffHdr + kWStages * 16;              // issue cursor (16 B)
+constexpr int kWOffRel = kWOffCur + 16;                         // release counters
+constexpr int kWOffTmem = kWOffRel + kWStages * 4;              // TMEM base slot
+constexpr int kWSmem = kWOffTmem + 16;
 constexpr uint32_t kWInvalid = 0xFFFFFFFFu;        // 32-bit (j0 | t) table: skipped sample / padding x
 // 64-bit step entry of (plane, u, x) for a warp walking its 8 outputs x in order.  The warp keeps
 // two row registers, slot A for the even and slot B for the odd stage row of the pair (j0, j0 + 1):
@@ -115,43 +120,82 @@ __device__ __forceinline__ bool w_needed(const S1WArgs& a, const WTile& w, int m
     return m >= b.x && m <= b.y;
 }
 
-// Producer cursor: the next (tile, u) stage to load, in the consumers' order.
-struct WProducer {
-    int t, u, stage;
-    uint32_t phase;
-    bool tile_ok;   // tile t checked and needed
+// Stage ring protocol.  There is no producer warp (a 17th warp would cap the registers at 96):
+// the warp that releases a slot LAST (a shared-memory counter per slot) issues its refill, so no
+// warp ever waits for an empty slot.  Refills happen in stage order: the last releaser of stage k
+// releases after every warp released k - 1, and every warp's release of k - 1 happens after
+// that warp's own refill issue of stage k - 1 + kWStages.  The refill writes a header into the
+// slot -- which tile the stage belongs to and whether it is the tile's first / last stage -- so
+// the consumers only follow headers (no tile or span logic of their own); tile = -1 ends the CTA.
+struct WCursor {   // the next (tile, u) stage to load (shared memory, touched by one issuer at a time)
+    int t, u;
+    int tile_started;   // the current tile has issued a stage
+    int pad;
 };
-// Issue the next stage (if any) into the ring; waits until its slot is free.
-__device__ __forceinline__ void w_produce(WProducer& p, const S1WArgs& a, int n_tiles, const CUtensorMap* tm_g,
-                                          const CUtensorMap* tm_e, uint8_t* smem, uint64_t* full, uint64_t* empty) {
-    while (p.t < n_tiles) {
-        const WTile w = w_tile(a, p.t);
-        if (!p.tile_ok) {
-            if (!w_needed(a, w, w_shard_row(a, w.ml))) { p.t += gridDim.x; continue; }
-            p.tile_ok = true;
-            p.u = 0;
-        }
+struct WHeader {
+    int tile;    // -1: no more stages
+    int flags;   // bit 0: first stage of the tile, bit 1: last stage of the tile
+    int pad[2];
+};
+
+// Next non-empty (tile, u) stage of this CTA after the cursor; returns false at the end.
+__device__ __forceinline__ bool w_next(WCursor& c, const S1WArgs& a, int n_tiles, int2& sp, bool& first) {
+    while (c.t < n_tiles) {
+        const WTile w = w_tile(a, c.t);
+        if (c.u == 0 && !c.tile_started && !w_needed(a, w, w_shard_row(a, w.ml))) { c.t += gridDim.x; continue; }
         const int2* sp_row = a.span + static_cast<int64_t>(w.g * a.n_xt + w.xt) * a.Wb;
-        while (p.u < a.Wb) {
-            const int2 sp = __ldg(sp_row + p.u);
+        while (c.u < a.Wb) {
+            sp = __ldg(sp_row + c.u);
             if (sp.y >= sp.x) {
-                const int nb = (sp.y - sp.x + kWBox) / kWBox;
-                mbar_wait(&empty[p.stage], p.phase ^ 1);
-                mbar_expect_tx(&full[p.stage], nb * kWBox * kWRowBytes + kWEBytes);
-                uint8_t* dst = smem + p.stage * kWStageBytes;
-                for (int b = 0; b < nb; ++b)
-                    tma_load_4d(dst + b * kWBox * kWRowBytes, tm_g, &full[p.stage], w.vb * kWV, p.u,
-                                sp.x + b * kWBox, w.ml);
-                tma_load_3d(dst + kWGBytes, tm_e, &full[p.stage], 2 * w.xt * kWX, p.u, w.g * kWF);
-                if (++p.stage == kWStages) { p.stage = 0; p.phase ^= 1; }
-                ++p.u;
-                return;
+                first = !c.tile_started;
+                c.tile_started = 1;
+                return true;
             }
-            ++p.u;
+            ++c.u;
         }
-        p.tile_ok = false;
-        p.t += gridDim.x;
+        c.t += gridDim.x;
+        c.u = 0;
+        c.tile_started = 0;
     }
+    return false;
+}
+// Has the tile of the cursor another non-empty stage after u? (the last-stage flag)
+__device__ __forceinline__ bool w_more_in_tile(const S1WArgs& a, int t, int u) {
+    const WTile w = w_tile(a, t);
+    const int2* sp_row = a.span + static_cast<int64_t>(w.g * a.n_xt + w.xt) * a.Wb;
+    for (int uu = u + 1; uu < a.Wb; ++uu) {
+        const int2 sp = __ldg(sp_row + uu);
+        if (sp.y >= sp.x) return true;
+    }
+    return false;
+}
+// Issue the next stage into ring slot s (single thread).
+__device__ __forceinline__ void w_issue(WCursor* cur, WHeader* hdr, int s, const S1WArgs& a, int n_tiles,
+                                        const CUtensorMap* tm_g, const CUtensorMap* tm_e, uint8_t* smem,
+                                        uint64_t* full) {
+    WCursor c = *cur;
+    int2 sp;
+    bool first;
+    if (!w_next(c, a, n_tiles, sp, first)) {
+        hdr[s].tile = -1;
+        hdr[s].flags = 0;
+        *cur = c;
+        mbar_arrive(&full[s]);   // release: consumers see the end marker
+        return;
+    }
+    const WTile w = w_tile(a, c.t);
+    const bool last = !w_more_in_tile(a, c.t, c.u);
+    hdr[s].tile = c.t;
+    hdr[s].flags = (first ? 1 : 0) | (last ? 2 : 0);
+    const int nb = (sp.y - sp.x + kWBox) / kWBox;
+    mbar_expect_tx(&full[s], nb * kWBox * kWRowBytes + kWEBytes);
+    uint8_t* dst = smem + s * kWStageBytes;
+    for (int b = 0; b < nb; ++b)
+        tma_load_4d(dst + b * kWBox * kWRowBytes, tm_g, &full[s], w.vb * kWV, c.u, sp.x + b * kWBox, w.ml);
+    tma_load_3d(dst + kWGBytes, tm_e, &full[s], 2 * w.xt * kWX, c.u, w.g * kWF);
+    ++c.u;
+    if (last) { c.t += gridDim.x; c.u = 0; c.tile_started = 0; }
+    *cur = c;
 }
 
 // fp64 accumulators of a warp in TMEM: plane pl (of the warp's 2), output i, v slot k (of the
@@ -201,132 +245,133 @@ __global__ void __launch_bounds__(kWThreads, 1)
 stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_e, S1WArgs a) {
     extern __shared__ __align__(1024) uint8_t w_smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(w_smem + kWOffBar);
-    uint64_t* empty = full + kWStages;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(empty + kWStages);
-    // the producer's cursor lives in shared memory: only lane 0 of warp 0 touches it, and keeping
-    // it out of the register file leaves the registers to the fp32 partials
-    WProducer* prod = reinterpret_cast<WProducer*>(w_smem + kWOffBar + 2 * kWStages * 8 + 16);
+    WHeader* hdr = reinterpret_cast<WHeader*>(w_smem + kWOffHdr);
+    WCursor* cur = reinterpret_cast<WCursor*>(w_smem + kWOffCur);
+    int* rel = reinterpret_cast<int*>(w_smem + kWOffRel);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(w_smem + kWOffTmem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_tiles = a.m_count * a.n_vb * a.n_groups * a.n_xt;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kWStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kWWarps);
+            rel[s] = 0;
         }
         fence_mbar_init();
-        *prod = WProducer{static_cast<int>(blockIdx.x), 0, 0, 0u, false};
+        *cur = WCursor{static_cast<int>(blockIdx.x), 0, 0, 0};
+        tma_prefetch_desc(&tm_g);
+        tma_prefetch_desc(&tm_e);
+        for (int s = 0; s < kWStages; ++s) w_issue(cur, hdr, s, a, n_tiles, &tm_g, &tm_e, w_smem, full);
     }
     if (warp == 0) tmem_alloc(tslot, kWTmemCols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tslot;
-    const int n_tiles = a.m_count * a.n_vb * a.n_groups * a.n_xt;
-
-    if (warp == 0 && lane == 0) {
-        tma_prefetch_desc(&tm_g);
-        tma_prefetch_desc(&tm_e);
-        WProducer p = *prod;
-        for (int k = 0; k < kWStages; ++k) w_produce(p, a, n_tiles, &tm_g, &tm_e, w_smem, full, empty);
-        *prod = p;
-    }
 
     // warp: planes 2 (warp / 8) + {0, 1} of the group, outputs x = x tile + 8 (warp % 8) + i;
     // lane: B rows v = v block + 4 lane + {0..3}
     const int wp = warp >> 3, wx = warp & 7;
     const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + static_cast<uint32_t>(warp >> 2) * 128u;
+    const uint32_t lane16 = 16u * lane;
+    uint64_t part[kWFW][kWXW][2];
+    bool first = true;   // no fp64 partial in TMEM yet for this tile
+    int nst = 0, nfw = 0;
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const WTile w = w_tile(a, t);
-        const int m = w_shard_row(a, w.ml);
-        if (!w_needed(a, w, m)) continue;
-        const int nfw = min(kWFW, a.n_planes - w.g * kWF - kWFW * wp);   // this warp's planes (may be <= 0)
-        const int2* sp_row = a.span + static_cast<int64_t>(w.g * a.n_xt + w.xt) * a.Wb;
-        uint64_t part[kWFW][kWXW][2];
+    for (;;) {
+        mbar_wait(&full[stage], phase);
+        const WHeader h = hdr[stage];
+        if (h.tile < 0) break;
+        if (h.flags & 1) {   // first stage of a tile
+            const WTile w = w_tile(a, h.tile);
+            nfw = min(kWFW, a.n_planes - w.g * kWF - kWFW * wp);   // this warp's planes (may be <= 0)
 #pragma unroll
-        for (int pl = 0; pl < kWFW; ++pl)
+            for (int pl = 0; pl < kWFW; ++pl)
 #pragma unroll
-            for (int i = 0; i < kWXW; ++i) part[pl][i][0] = part[pl][i][1] = 0ull;
-        bool first = true;   // no fp64 partial in TMEM yet for this tile
-        int nst = 0;
-        for (int u = 0; u < a.Wb; ++u) {
-            const int2 sp = __ldg(sp_row + u);
-            if (sp.y < sp.x) continue;
-            mbar_wait(&full[stage], phase);
-            const uint8_t* sbase = w_smem + stage * kWStageBytes;
-            const uint4* E = reinterpret_cast<const uint4*>(sbase + kWGBytes);
-            const uint32_t gaddr = smem_u32(sbase) + 16u * lane;   // this lane's 16 bytes (4 v) of row 0
+                for (int i = 0; i < kWXW; ++i) part[pl][i][0] = part[pl][i][1] = 0ull;
+            first = true;
+            nst = 0;
+        }
+        const uint8_t* sbase = w_smem + stage * kWStageBytes;
+        const uint4* E = reinterpret_cast<const uint4*>(sbase + kWGBytes);
+        const uint32_t gaddr = smem_u32(sbase) + lane16;   // this lane's 16 bytes (4 v) of row 0
+#pragma unroll
+        for (int pl = 0; pl < kWFW; ++pl) {
+            if (pl < nfw) {
+                const uint4* Ep = E + ((kWFW * wp + pl) * kWX + wx * kWXW) / 2;
+                uint4 ga = make_uint4(0u, 0u, 0u, 0u), gb = ga;   // even / odd row of the window
+#pragma unroll
+                for (int i = 0; i < kWXW; i += 2) {
+                    const uint4 e2 = Ep[i / 2];   // entries of outputs i, i + 1 (broadcast)
+#pragma unroll
+                    for (int k = 0; k < 2; ++k) {
+                        const uint32_t lo = k ? e2.z : e2.x, hi = k ? e2.w : e2.y;
+                        w_lds_if(ga, gaddr + ((hi & 0xFFu) << 9), hi & 0x10000u);
+                        w_lds_if(gb, gaddr + ((hi >> 8 & 0xFFu) << 9), hi & 0x20000u);
+                        const float wa = __uint_as_float(lo);
+                        const float wb = __uint_as_float(hi & kWOne) - wa;
+                        const uint64_t wa2 = pk2(wa, wa), wb2 = pk2(wb, wb);
+                        uint64_t* pp = part[pl][i + k];
+                        pp[0] = fma2(wb2, pk2(__uint_as_float(gb.x), __uint_as_float(gb.y)),
+                                     fma2(wa2, pk2(__uint_as_float(ga.x), __uint_as_float(ga.y)), pp[0]));
+                        pp[1] = fma2(wb2, pk2(__uint_as_float(gb.z), __uint_as_float(gb.w)),
+                                     fma2(wa2, pk2(__uint_as_float(ga.z), __uint_as_float(ga.w)), pp[1]));
+                    }
+                }
+            }
+        }
+        // release the slot (generic-proxy reads before the async-proxy refill); the
+        // last warp to release it issues the refill
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();
+            if (atomicAdd(&rel[stage], 1) == kWWarps - 1) {
+                rel[stage] = 0;
+                __threadfence_block();
+                w_issue(cur, hdr, stage, a, n_tiles, &tm_g, &tm_e, w_smem, full);
+            }
+        }
+        __syncwarp();
+        const int this_stage = stage;
+        if (++stage == kWStages) { stage = 0; phase ^= 1; }
+        (void)this_stage;
+        if (h.flags & 2) {   // last stage of the tile: fp64 sum (TMEM + partial) -> fp32 T
+            const WTile w = w_tile(a, h.tile);
+            const int m = w_shard_row(a, w.ml);
+            const int v = w.vb * kWV + 4 * lane;
+            const int x0 = w.xt * kWX + wx * kWXW;
 #pragma unroll
             for (int pl = 0; pl < kWFW; ++pl) {
                 if (pl < nfw) {
-                    const uint4* Ep = E + ((kWFW * wp + pl) * kWX + wx * kWXW) / 2;
-                    uint4 ga = make_uint4(0u, 0u, 0u, 0u), gb = ga;   // even / odd row of the window
+                    float* Tf = a.T + static_cast<int64_t>(w.g * kWF + kWFW * wp + pl) * a.t_plane;
 #pragma unroll
-                    for (int i = 0; i < kWXW; i += 2) {
-                        const uint4 e2 = Ep[i / 2];   // entries of outputs i, i + 1 (broadcast)
+                    for (int half = 0; half < 2; ++half) {
+                        uint32_t r[32];
+                        if (!first) {
+                            tmem_ld_32x32b_x32(tbase + 64 * pl + 32 * half, r);
+                            tmem_wait_ld();
+                        }
+                        w_combine(part[pl], r, half, first);
 #pragma unroll
-                        for (int k = 0; k < 2; ++k) {
-                            const uint32_t lo = k ? e2.z : e2.x, hi = k ? e2.w : e2.y;
-                            w_lds_if(ga, gaddr + ((hi & 0xFFu) << 9), hi & 0x10000u);
-                            w_lds_if(gb, gaddr + ((hi >> 8 & 0xFFu) << 9), hi & 0x20000u);
-                            const float wa = __uint_as_float(lo);
-                            const float wb = __uint_as_float(hi & kWOne) - wa;
-                            const uint64_t wa2 = pk2(wa, wa), wb2 = pk2(wb, wb);
-                            uint64_t* pp = part[pl][i + k];
-                            pp[0] = fma2(wb2, pk2(__uint_as_float(gb.x), __uint_as_float(gb.y)),
-                                         fma2(wa2, pk2(__uint_as_float(ga.x), __uint_as_float(ga.y)), pp[0]));
-                            pp[1] = fma2(wb2, pk2(__uint_as_float(gb.z), __uint_as_float(gb.w)),
-                                         fma2(wa2, pk2(__uint_as_float(ga.z), __uint_as_float(ga.w)), pp[1]));
+                        for (int ii = 0; ii < 4; ++ii) {
+                            const int x = x0 + 4 * half + ii;
+                            float o[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                o[k] = static_cast<float>(__hiloint2double(static_cast<int>(r[8 * ii + 2 * k + 1]),
+                                                                           static_cast<int>(r[8 * ii + 2 * k])));
+                            if (x < a.Wa && v < a.Hb)
+                                *reinterpret_cast<float4*>(Tf + (static_cast<int64_t>(x) * a.Ha + m) * a.Hb + v) =
+                                    make_float4(o[0], o[1], o[2], o[3]);
                         }
                     }
                 }
             }
-            // release the stage (generic-proxy reads before the async-proxy refill)
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
-            if (warp == 0 && lane == 0) {   // refill this slot once every warp released it
-                WProducer p = *prod;
-                w_produce(p, a, n_tiles, &tm_g, &tm_e, w_smem, full, empty);
-                *prod = p;
-            }
-            __syncwarp();
-            if (++stage == kWStages) { stage = 0; phase ^= 1; }
-            if (++nst == kWFlush) {
-                w_flush(part, tbase, first);
-                first = false;
-                nst = 0;
-            }
-        }
-        // tile end: fp64 sum (TMEM + partial) rounded once to fp32 T, for v < H_b, x < W_a
-        const int v = w.vb * kWV + 4 * lane;
-        const int x0 = w.xt * kWX + wx * kWXW;
-#pragma unroll
-        for (int pl = 0; pl < kWFW; ++pl) {
-            if (pl < nfw) {
-                float* Tf = a.T + static_cast<int64_t>(w.g * kWF + kWFW * wp + pl) * a.t_plane;
-#pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    uint32_t r[32];
-                    if (!first) {
-                        tmem_ld_32x32b_x32(tbase + 64 * pl + 32 * half, r);
-                        tmem_wait_ld();
-                    }
-                    w_combine(part[pl], r, half, first);
-#pragma unroll
-                    for (int ii = 0; ii < 4; ++ii) {
-                        const int x = x0 + 4 * half + ii;
-                        float o[4];
-#pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            o[k] = static_cast<float>(__hiloint2double(static_cast<int>(r[8 * ii + 2 * k + 1]),
-                                                                       static_cast<int>(r[8 * ii + 2 * k])));
-                        if (x < a.Wa && v < a.Hb)
-                            *reinterpret_cast<float4*>(Tf + (static_cast<int64_t>(x) * a.Ha + m) * a.Hb + v) =
-                                make_float4(o[0], o[1], o[2], o[3]);
-                    }
-                }
-            }
+        } else if (++nst == kWFlush) {
+            w_flush(part, tbase, first);
+            first = false;
+            nst = 0;
         }
     }
     // all warps done with TMEM before warp 0 frees it
