@@ -51,6 +51,7 @@ typedef int32_t cpi_status;
 #define CPI_ERR_CUDA               (-10) /* CUDA runtime/driver failure or no sm_100 device */
 #define CPI_ERR_OOM                (-11) /* device allocation failure */
 #define CPI_ERR_UNSUPPORTED        (-12) /* feature not available for this configuration */
+#define CPI_ERR_NCCL               (-13) /* NCCL unavailable (libnccl.so.2 not loadable) or an NCCL call failed */
 
 /* Frame layout.  bit_order: column c of a row is bit (c % 8) of
  * byte c/8 (CPI_LSB_FIRST, declared convention S:110) or bit 7 - c % 8 (CPI_MSB_FIRST). */
@@ -109,8 +110,22 @@ typedef struct {
                                P:68-69: A = left half, B = right half for the paper's data */
     int64_t max_frames;     /* capacity of one cpi_load_frames batch (>= 1) */
     int32_t device;         /* CUDA device ordinal; must be compute capability 10.0 */
-    uint32_t flags;         /* CPI_VARIANT_* | CPI_KEEP_COUNTS */
+    uint32_t flags;         /* CPI_VARIANT_* | CPI_KEEP_COUNTS | CPI_GAMMA_* */
+    /* Frame-sharded multi-GPU mode (north_star; one context per GPU, one process per
+     * GPU): world >= 2 makes this context rank `rank` of `world`.  cpi_create then joins a library-
+     * owned NCCL communicator (collective: every rank must call cpi_create) identified by nccl_id
+     * (CPI_NCCL_ID_BYTES bytes from cpi_nccl_unique_id on one rank, shared out of band), and needs
+     * CPI_KEEP_COUNTS and H_a % world == 0.  Each rank loads and correlates its own contiguous
+     * slice of the frame sequence (Eq. (1)'s sums are additive); cpi_finalize reduces
+     * across ranks and finalises the rank's own Gamma rows; cpi_refocus from the current totals
+     * (gamma_dev NULL) refocuses them and all-reduces the planes.  world == 1 with a non-NULL
+     * nccl_id runs the same multi-GPU code path as a one-rank group.  Otherwise (world <= 1, no id):
+     * single GPU (a zero-initialised config is a single-GPU config). */
+    int32_t rank, world;
+    const uint8_t *nccl_id;
 } cpi_config;
+
+#define CPI_NCCL_ID_BYTES 128
 
 typedef struct {
     const double *alphas;   /* HOST array of n_planes refocusing parameters alpha (finite, != 0) */
@@ -228,11 +243,33 @@ cpi_status cpi_counts_dev(cpi_ctx *ctx, int32_t **s_ab, int32_t **s_a, int32_t *
 
 /* Gamma of Eq. (1) from the accumulated sums:
  *   Gamma[p][q] = (N*S_ab[p][q] - S_a[p]*S_b[q]) / N^2   (= (1/N) S_ab - (S_a/N)(S_b/N))
- * with the numerator formed exactly (fp64 FMA of exact integers) and one rounding to fp32.
- * If the last cpi_correlate already wrote Gamma for the current totals and gamma_dev is
- * NULL or that same buffer, nothing is launched.  Otherwise needs CPI_KEEP_COUNTS.
- * *n_tot (optional) receives N_TOT.  Errors: ZERO_FRAMES, STATE, INVALID_ARG, CUDA. */
-cpi_status cpi_finalize(cpi_ctx *ctx, float *gamma_dev, int64_t *n_tot, void *stream);
+ * with the numerator formed exactly (integer) and one rounding to fp32.
+ * Single GPU: if the last cpi_correlate already wrote Gamma for the current totals and gamma_dev
+ * is NULL or that same buffer, nothing is launched.  Otherwise needs CPI_KEEP_COUNTS; gamma_dev is
+ * [P_a][P_b].  *row0 = 0, *rows = P_a.
+ * Multi-GPU (cfg.world >= 2, or a one-rank group): the cross-rank reduction runs here, stream-ordered on
+ * `stream` over the library's NCCL communicator: C2 all-reduce of [S_a | S_b | N] (int32) and C1
+ * reduce-scatter of the int32 partial S_ab in row panels, so that this rank receives the exact
+ * totals of its own A rows, which it finalises into gamma_dev (compact [rows][P_b], may be NULL:
+ * a library workspace, then refocus with gamma_dev = NULL).  The owned rows are block-cyclic (load
+ * balance of refocusing for alpha < 1): local Gamma row r is A pixel
+ *   p(r) = (row0 / W_a + (r / W_a / row_block) * row_stride + (r / W_a) % row_block) * W_a + r % W_a
+ * with row_block, row_stride from cpi_shard_layout; *row0 = first owned A pixel, *rows = owned
+ * A pixels.  Integer sums: Gamma is bit-identical for any world size.
+ * Outputs n_tot (global N_TOT), row0, rows are optional.  Errors: ZERO_FRAMES, STATE, INVALID_ARG,
+ * CUDA, NCCL. */
+cpi_status cpi_finalize(cpi_ctx *ctx, float *gamma_dev, int64_t *n_tot, int64_t *row0, int64_t *rows,
+                        void *stream);
+
+/* Block-cyclic ownership of this rank's Gamma rows (see cpi_finalize): blocks of row_block A rows
+ * every row_stride A rows, starting at A row row0 / W_a.  Single GPU: row_block = row_stride = H_a.
+ * Either pointer may be NULL.  Errors: INVALID_ARG. */
+cpi_status cpi_shard_layout(const cpi_ctx *ctx, int32_t *row_block, int32_t *row_stride);
+
+/* A new NCCL unique id (CPI_NCCL_ID_BYTES bytes into id) for the cpi_config.nccl_id of a
+ * multi-GPU group: call on one rank, share the bytes with the others (any out-of-band channel).
+ * Errors: INVALID_ARG, NCCL (libnccl.so.2 unavailable). */
+cpi_status cpi_nccl_unique_id(uint8_t *id);
 
 /* Stateless finalisation of an externally reduced row shard (frame-sharded multi-GPU:
  * SURVEY §8(e), after an all-reduce of S_a/S_b/N and a reduce-scatter of S_ab rows):
@@ -252,8 +289,13 @@ cpi_status cpi_get_counts(cpi_ctx *ctx, int32_t *s_ab_dev, int32_t *s_a_dev, int
 /* Zero the accumulated sums (start a new acquisition). */
 cpi_status cpi_reset(cpi_ctx *ctx, void *stream);
 
-/* Refocus Gamma into a stack of planes ("Refocusing"):
- * for plane alpha and output pixel (x, y) of the A lattice,
+/* Refocus Gamma into a stack of planes ("Refocusing").
+ * Multi-GPU contexts with spec->gamma_dev = NULL refocus this rank's own Gamma rows (those the
+ * last cpi_finalize produced) and all-reduce the planes in fp64, so every rank
+ * returns the whole stack (each rank's fp32 share is within 2^-24 of its own M, M is additive over
+ * row shards, so the sum meets the single-GPU 1e-6 M bar).  With an explicit gamma_dev a
+ * multi-GPU context refocuses that shard only (no reduction), as a single-GPU context does.
+ * For plane alpha and output pixel (x, y) of the A lattice,
  *   R(x,y) = (1/count) * sum over B lattice (u, v) of the multilinear interpolation of
  *            Gamma at A coordinates
  *              c_x = alpha*(x - c_ax) + (1 - alpha)*(u - c_bx) + c_ax

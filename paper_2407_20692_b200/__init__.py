@@ -7,6 +7,6 @@ The compute lives in libcpi.so (C ABI: include/cpi.h); this package is its thin 
 (`cpi`) plus the frame-sharded multi-GPU orchestration over torch.distributed (`parallel`).
 """
 from ._lib import CpiError, CPI_CLAMP, CPI_SKIP_RENORMALIZE  # noqa: F401
-from .cpi import Context, abi_version  # noqa: F401
+from .cpi import Context, abi_version, nccl_unique_id  # noqa: F401
 
-__all__ = ["Context", "CpiError", "abi_version", "CPI_CLAMP", "CPI_SKIP_RENORMALIZE"]
+__all__ = ["Context", "CpiError", "abi_version", "nccl_unique_id", "CPI_CLAMP", "CPI_SKIP_RENORMALIZE"]

@@ -13,8 +13,9 @@ STATUS = {
     0: "CPI_OK", -1: "CPI_ERR_INVALID_ARG", -2: "CPI_ERR_LAYOUT", -3: "CPI_ERR_ROI_OUT_OF_BOUNDS",
     -4: "CPI_ERR_SIZE_MISMATCH", -5: "CPI_ERR_CAPACITY", -6: "CPI_ERR_ZERO_FRAMES",
     -7: "CPI_ERR_DEGENERATE_ALPHA", -8: "CPI_ERR_EMPTY_ANGULAR_GRID", -9: "CPI_ERR_STATE",
-    -10: "CPI_ERR_CUDA", -11: "CPI_ERR_OOM", -12: "CPI_ERR_UNSUPPORTED",
+    -10: "CPI_ERR_CUDA", -11: "CPI_ERR_OOM", -12: "CPI_ERR_UNSUPPORTED", -13: "CPI_ERR_NCCL",
 }
+CPI_NCCL_ID_BYTES = 128
 CPI_LSB_FIRST, CPI_MSB_FIRST = 0, 1
 CPI_HOST, CPI_DEVICE = 0, 1
 CPI_VARIANT_TC, CPI_VARIANT_POPC, CPI_KEEP_COUNTS, CPI_VARIANT_FP4, CPI_GAMMA_UBLOCKED = 0, 1, 2, 4, 8
@@ -26,7 +27,8 @@ KC_GEMM, KC_EXPAND, KC_STAGE1, KC_STAGE2, KC_FINALIZE, KC_COORDS, KC_RESAMPLE = 
 EXPORTS = ["cpi_create", "cpi_destroy", "cpi_last_error", "cpi_status_string", "cpi_load_frames",
            "cpi_correlate", "cpi_finalize", "cpi_finalize_counts", "cpi_get_counts", "cpi_reset",
            "cpi_refocus", "cpi_launch_count", "cpi_set_timing", "cpi_kernel_time_ms",
-           "cpi_abi_version", "cpi_correlate_rows", "cpi_row_align", "cpi_counts_dev", "cpi_correlate_rows_to"]
+           "cpi_abi_version", "cpi_correlate_rows", "cpi_row_align", "cpi_counts_dev", "cpi_correlate_rows_to",
+           "cpi_shard_layout", "cpi_nccl_unique_id"]
 
 
 class CpiError(RuntimeError):
@@ -48,7 +50,8 @@ class Layout(ctypes.Structure):
 
 class Config(ctypes.Structure):
     _fields_ = [("layout", Layout), ("roi_a", Roi), ("roi_b", Roi), ("max_frames", ctypes.c_int64),
-                ("device", ctypes.c_int32), ("flags", ctypes.c_uint32)]
+                ("device", ctypes.c_int32), ("flags", ctypes.c_uint32), ("rank", ctypes.c_int32),
+                ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p)]
 
 
 class RefocusSpec(ctypes.Structure):
@@ -87,7 +90,9 @@ def load():
         "cpi_status_string": ([i32], ctypes.c_char_p),
         "cpi_load_frames": ([P, P, i64, i32, P], i32),
         "cpi_correlate": ([P, P, P], i32),
-        "cpi_finalize": ([P, P, ctypes.POINTER(i64), P], i32),
+        "cpi_finalize": ([P, P, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64), P], i32),
+        "cpi_shard_layout": ([P, ctypes.POINTER(i32), ctypes.POINTER(i32)], i32),
+        "cpi_nccl_unique_id": ([P], i32),
         "cpi_finalize_counts": ([P, P, i64, i64, P, P, i64, P, P], i32),
         "cpi_get_counts": ([P, P, P, P, ctypes.POINTER(i64), P], i32),
         "cpi_reset": ([P, P], i32),

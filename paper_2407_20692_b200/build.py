@@ -13,7 +13,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libcpi.so"
-SOURCES = ["cpi_abi.cu", "expand.cu", "gemm_tc.cu", "gemm_tc2.cu", "gemm_popc.cu", "refocus.cu", "refocus_w.cu"]
+SOURCES = ["cpi_abi.cu", "expand.cu", "gemm_tc.cu", "gemm_tc2.cu", "gemm_popc.cu", "refocus.cu", "refocus_w.cu", "comm.cu"]
 HEADERS = ["common.cuh", "kernels.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     with ThreadPoolExecutor(max(1, min(len(SOURCES), os.cpu_count() or 1))) as ex:
         objs = list(ex.map(compile_one, SOURCES))
     tmp = str(LIB) + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]   # NCCL: dlopen
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

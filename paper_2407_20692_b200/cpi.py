@@ -30,7 +30,11 @@ class Context:
 
     def __init__(self, roi_a, roi_b, max_frames: int, *, width: int = FRAME_W, height: int = FRAME_H,
                  bit_order: int = _lib.CPI_LSB_FIRST, device: int = 0, variant: str = "tc",
-                 keep_counts: bool = False, gamma_blocked: bool = False, gamma_order: Optional[str] = None):
+                 keep_counts: bool = False, gamma_blocked: bool = False, gamma_order: Optional[str] = None,
+                 rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None):
+        """rank / world / nccl_id: frame-sharded multi-GPU mode (include/cpi.h cpi_config; world >= 2
+        needs keep_counts and the same nccl_unique_id() bytes on every rank; cpi_create is
+        collective)."""
         self._lib = _lib.load()
         if variant not in ("tc", "popc", "fp4"):
             raise ValueError("variant must be 'tc', 'popc' or 'fp4'")
@@ -42,8 +46,14 @@ class Context:
         if gamma_order not in GAMMA_ORDERS:
             raise ValueError(f"gamma_order must be one of {sorted(GAMMA_ORDERS)}")
         flags |= GAMMA_ORDERS[gamma_order]   # B pixel (Gamma column) order, include/cpi.h
+        self._id_buf = None
+        if world > 1 or nccl_id is not None:
+            if nccl_id is None or len(nccl_id) != _lib.CPI_NCCL_ID_BYTES:
+                raise ValueError(f"world > 1 needs nccl_id of {_lib.CPI_NCCL_ID_BYTES} bytes (nccl_unique_id())")
+            self._id_buf = ctypes.create_string_buffer(bytes(nccl_id), _lib.CPI_NCCL_ID_BYTES)
         cfg = _lib.Config(_lib.Layout(width, height, bit_order), _lib.Roi(*roi_a), _lib.Roi(*roi_b),
-                          int(max_frames), int(device), flags)
+                          int(max_frames), int(device), flags, int(rank), int(world),
+                          ctypes.cast(self._id_buf, ctypes.c_void_p) if self._id_buf is not None else None)
         h = ctypes.c_void_p()
         st = self._lib.cpi_create(ctypes.byref(cfg), ctypes.byref(h))
         if st != 0:
@@ -58,6 +68,9 @@ class Context:
         self.max_frames = int(max_frames)
         self.variant = variant
         self.keep_counts = keep_counts
+        self.rank, self.world = (int(rank), int(world)) if world > 1 else (0, 1)
+        self.sharded = self._id_buf is not None
+        self.shard_rows = (0, self.p_a)    # owned Gamma rows (A pixels) of the last finalize
         self.gamma_order = gamma_order
         self.gamma_blocked = gamma_order == "ublocked"
         self._keep = []   # host buffers that must outlive an async copy
@@ -172,12 +185,31 @@ class Context:
         return view(pab, (self.p_a, self.p_b)), view(pa, (self.p_a,)), view(pb, (self.p_b,))
 
     def finalize(self, gamma=None, stream=None) -> int:
-        """cpi_finalize: Gamma from the accumulated sums; returns N_TOT."""
-        if gamma is not None:
+        """cpi_finalize: Gamma from the accumulated sums; returns N_TOT.  Multi-GPU: the cross-rank
+        reduction runs here and gamma (optional) receives this rank's rows [rows][P_b]
+        (self.shard_rows = (row0, rows), layout from shard_layout())."""
+        if gamma is not None and not self.sharded:
             self._check_gamma(gamma)
-        n = ctypes.c_int64(0)
-        self._check(self._lib.cpi_finalize(self._h, self._ptr(gamma), ctypes.byref(n), self._stream(stream)))
+        n, r0, rows = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
+        self._check(self._lib.cpi_finalize(self._h, self._ptr(gamma), ctypes.byref(n), ctypes.byref(r0),
+                                           ctypes.byref(rows), self._stream(stream)))
+        self.shard_rows = (r0.value, rows.value)
         return n.value
+
+    def shard_layout(self):
+        """cpi_shard_layout: (row_block, row_stride) of this rank's block-cyclic A rows."""
+        b, st = ctypes.c_int32(0), ctypes.c_int32(0)
+        self._check(self._lib.cpi_shard_layout(self._h, ctypes.byref(b), ctypes.byref(st)))
+        return b.value, st.value
+
+    def shard_pixel_rows(self):
+        """Global A pixel of each local Gamma row owned by this rank (include/cpi.h cpi_finalize)."""
+        row0, rows = self.shard_rows
+        block, stride = self.shard_layout()
+        Wa = self.roi_a[2]
+        lr = np.arange(rows // Wa)
+        m = row0 // Wa + (lr // block) * stride + lr % block
+        return (m[:, None] * Wa + np.arange(Wa)[None, :]).reshape(-1)
 
     def finalize_counts(self, s_ab_rows, row0: int, s_a, s_b, n_tot: int, gamma_rows, stream=None):
         """cpi_finalize_counts: stateless Gamma of an externally reduced row shard."""
@@ -266,3 +298,12 @@ class Context:
 
 def abi_version() -> int:
     return int(_lib.load().cpi_abi_version())
+
+
+def nccl_unique_id() -> bytes:
+    """cpi_nccl_unique_id: a new NCCL unique id for a multi-GPU group (share it with every rank)."""
+    buf = ctypes.create_string_buffer(_lib.CPI_NCCL_ID_BYTES)
+    st = _lib.load().cpi_nccl_unique_id(buf)
+    if st != 0:
+        raise CpiError(st, "cpi_nccl_unique_id failed (libnccl.so.2 unavailable?)")
+    return buf.raw

@@ -98,6 +98,17 @@ struct cpi_ctx {
     int2* w_mband = nullptr;               // [groups][v blocks]
     uint32_t* w_ypack = nullptr;           // [batch][H_b][H_a]
     cpi::TElem* w_T = nullptr;             // [batch][W_a][H_a][H_b]
+    // frame-sharded multi-GPU mode (cfg.world >= 2): library-owned NCCL communicator and shard plan
+    int world = 1, rank = 0;
+    ncclComm_t comm = nullptr;
+    int sh_block = 0, sh_panels = 1, sh_m_base = 0, sh_m_count = 0, sh_stride = 0;   // A rows
+    int32_t* sh_counts = nullptr;          // [m_count * W_a][P_b] reduced pair sums of the owned rows
+    int32_t* sh_marg = nullptr;            // [P_a + P_b + 1] all-reduced S_a | S_b | N
+    float* sh_gamma_ws = nullptr;          // owned Gamma rows (library workspace)
+    float* sh_gamma_cur = nullptr;         // owned Gamma rows written by the last cpi_finalize
+    int32_t n_local_i32 = 0;
+    double* planes64 = nullptr;            // fp64 plane all-reduce buffer
+    size_t planes64_n = 0;
     // accounting
     int64_t launches = 0;
     bool timing = false;
@@ -238,6 +249,11 @@ void free_all(cpi_ctx* c) {
     cudaFree(c->w_i0s); cudaFree(c->w_ts); cudaFree(c->w_ylo); cudaFree(c->w_yhi);
     cudaFree(c->w_ent); cudaFree(c->w_steps); cudaFree(c->w_span); cudaFree(c->w_mband);
     cudaFree(c->w_ypack); cudaFree(c->w_T);
+    cudaFree(c->sh_counts); cudaFree(c->sh_marg); cudaFree(c->sh_gamma_ws); cudaFree(c->planes64);
+    if (c->comm) {
+        if (const cpi::NcclApi* api = cpi::nccl_api()) api->comm_destroy(c->comm);
+        c->comm = nullptr;
+    }
     for (auto& t : c->timed) { c->event_pool.push_back(t.a); c->event_pool.push_back(t.b); }
     for (auto e : c->event_pool) cudaEventDestroy(e);
 }
@@ -473,7 +489,7 @@ cpi_status refocus_vmajor(cpi_ctx* c, const cpi_refocus_spec* spec, float* plane
 
 extern "C" {
 
-int32_t cpi_abi_version(void) { return 104; }
+int32_t cpi_abi_version(void) { return 200; }
 
 const char* cpi_status_string(cpi_status s) {
     switch (s) {
@@ -490,6 +506,7 @@ const char* cpi_status_string(cpi_status s) {
         case CPI_ERR_CUDA: return "CPI_ERR_CUDA";
         case CPI_ERR_OOM: return "CPI_ERR_OOM";
         case CPI_ERR_UNSUPPORTED: return "CPI_ERR_UNSUPPORTED";
+        case CPI_ERR_NCCL: return "CPI_ERR_NCCL";
         default: return "CPI_ERR_UNKNOWN";
     }
 }
@@ -527,6 +544,20 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
     if ((cfg->flags & CPI_VARIANT_FP4) && cfg->max_frames >= (int64_t(1) << 24))
         return fail(nullptr, CPI_ERR_INVALID_ARG, "CPI_VARIANT_FP4 needs max_frames < 2^24 (exact fp32 sums)");
 
+    // multi-GPU mode: world >= 2, or world == 1 with an nccl_id (the same code path as a one-rank group)
+    const int world = cfg->world > 1 ? cfg->world : 1;
+    const bool sharded = cfg->world > 1 || (cfg->world == 1 && cfg->nccl_id);
+    if (sharded) {
+        if (cfg->rank < 0 || cfg->rank >= world)
+            return fail(nullptr, CPI_ERR_INVALID_ARG, "rank %d outside [0, world = %d)", cfg->rank, world);
+        if (!cfg->nccl_id) return fail(nullptr, CPI_ERR_INVALID_ARG, "multi-GPU config needs nccl_id");
+        if (!(cfg->flags & CPI_KEEP_COUNTS))
+            return fail(nullptr, CPI_ERR_INVALID_ARG, "multi-GPU config needs CPI_KEEP_COUNTS (partial pair sums)");
+        if (cfg->roi_a.height % world)
+            return fail(nullptr, CPI_ERR_INVALID_ARG, "H_a = %d must be divisible by world = %d", cfg->roi_a.height,
+                        world);
+        if (!cpi::nccl_api()) return fail(nullptr, CPI_ERR_NCCL, "libnccl.so.2 could not be loaded");
+    }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         return fail(nullptr, CPI_ERR_CUDA, "no CUDA device visible");
@@ -597,6 +628,41 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
         delete c;
         return s;
     }
+    if (sharded) {
+        // shard plan: block-cyclic A rows, the smallest block whose panel (world
+        // blocks) holds >= 8192 A pixels, so each reduce-scatter call moves >= 32 KB per B pixel row
+        c->world = world;
+        c->rank = cfg->rank;
+        const int Wa = cfg->roi_a.width, m_per = cfg->roi_a.height / world;
+        int block = m_per;
+        for (int b = 1; b <= m_per; ++b)
+            if (m_per % b == 0 && int64_t(world) * b * Wa >= std::min<int64_t>(8192, c->p_a)) { block = b; break; }
+        c->sh_block = block;
+        c->sh_panels = m_per / block;
+        c->sh_m_base = c->rank * block;
+        c->sh_m_count = m_per;
+        c->sh_stride = world * block;
+        cudaError_t ea = cudaMalloc(&c->sh_counts, sizeof(int32_t) * size_t(m_per) * Wa * c->p_b);
+        if (ea == cudaSuccess) ea = cudaMalloc(&c->sh_marg, sizeof(int32_t) * size_t(c->p_a + c->p_b + 1));
+        if (ea != cudaSuccess) {
+            cpi_status s = cuda_fail(nullptr, ea, "cpi_create shard workspaces");
+            free_all(c);
+            delete c;
+            return s;
+        }
+        ncclUniqueId id;
+        static_assert(sizeof(id) == CPI_NCCL_ID_BYTES, "NCCL unique id size");
+        std::memcpy(&id, cfg->nccl_id, sizeof(id));
+        const ncclResult_t r = cpi::nccl_api()->comm_init_rank(&c->comm, world, id, c->rank);
+        if (r != ncclSuccess) {
+            c->comm = nullptr;
+            const cpi_status s = fail(nullptr, CPI_ERR_NCCL, "ncclCommInitRank: %s", cpi::nccl_api()->error_string(r));
+            free_all(c);
+            delete c;
+            return s;
+        }
+    }
+    c->cfg.nccl_id = nullptr;   // the caller's buffer is not kept
     if (!c->popc) {
         const uint32_t box_a = c->pair ? cpi::gemm_tc2_box_rows() : cpi::gemm_tc_block_m();
         const uint32_t box_b = c->fp4 ? cpi::gemm_f4_box_rows_b() : c->pair ? cpi::gemm_tc2_box_rows()
@@ -769,6 +835,8 @@ cpi_status cpi_correlate(cpi_ctx* c, float* gamma, void* stream) {
         return fail(c, CPI_ERR_STATE, "second batch needs CPI_KEEP_COUNTS (or cpi_reset)");
     if (!c->keep && !gamma)
         return fail(c, CPI_ERR_STATE, "gamma_dev is NULL and CPI_KEEP_COUNTS is off: pair sums would be lost");
+    if (c->comm && gamma)
+        return fail(c, CPI_ERR_STATE, "multi-GPU context: the pair sums are partial; Gamma comes from cpi_finalize");
     const int64_t n = c->n_cur;
     if (gamma && c->n_tot + n == 0) return fail(c, CPI_ERR_ZERO_FRAMES, "Gamma needs N_TOT >= 1");
     CK(c, cudaSetDevice(c->dev));
@@ -857,15 +925,76 @@ cpi_status cpi_counts_dev(cpi_ctx* c, int32_t** s_ab, int32_t** s_a, int32_t** s
     return CPI_OK;
 }
 
-cpi_status cpi_finalize(cpi_ctx* c, float* gamma, int64_t* n_tot, void* stream) {
+namespace {
+cpi_status nccl_fail(cpi_ctx* c, ncclResult_t r, const char* where) {
+    return fail(c, CPI_ERR_NCCL, "%s: %s", where, cpi::nccl_api()->error_string(r));
+}
+#define NK(c, call)                                                     \
+    do {                                                                \
+        ncclResult_t r_ = (call);                                       \
+        if (r_ != ncclSuccess) return nccl_fail((c), r_, #call);        \
+    } while (0)
+
+// Multi-GPU finalize: C2 all-reduce of [S_a | S_b | N], C1 panelised reduce-scatter
+// of the int32 partial pair sums (rank r receives block r of every panel), then the owned rows'
+// Gamma.  All stream-ordered on st; one host sync to read the global N (the normalisation scale).
+cpi_status finalize_sharded(cpi_ctx* c, float* gamma, int64_t* n_tot, cudaStream_t st) {
+    const cpi::NcclApi* api = cpi::nccl_api();
+    const int Wa = c->cfg.roi_a.width;
+    cpi_status s = ensure_counts(c, st);
+    if (s != CPI_OK) return s;
+    c->n_local_i32 = static_cast<int32_t>(c->n_tot);
+    CK(c, cudaMemcpyAsync(c->sh_marg, c->s_a, sizeof(int32_t) * c->p_a, cudaMemcpyDeviceToDevice, st));
+    CK(c, cudaMemcpyAsync(c->sh_marg + c->p_a, c->s_b, sizeof(int32_t) * c->p_b, cudaMemcpyDeviceToDevice, st));
+    CK(c, cudaMemcpyAsync(c->sh_marg + c->p_a + c->p_b, &c->n_local_i32, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    const int64_t chunk = int64_t(c->sh_block) * Wa, panel = chunk * c->world;
+    NK(c, api->group_start());
+    NK(c, api->all_reduce(c->sh_marg, c->sh_marg, size_t(c->p_a + c->p_b + 1), ncclInt32, ncclSum, c->comm, st));
+    for (int k = 0; k < c->sh_panels; ++k)
+        NK(c, api->reduce_scatter(c->counts + k * panel * c->p_b, c->sh_counts + k * chunk * c->p_b,
+                                  size_t(chunk * c->p_b), ncclInt32, ncclSum, c->comm, st));
+    NK(c, api->group_end());
+    int32_t n_glob = 0;
+    CK(c, cudaMemcpyAsync(&n_glob, c->sh_marg + c->p_a + c->p_b, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(c, cudaStreamSynchronize(st));
+    if (n_glob <= 0) return fail(c, CPI_ERR_ZERO_FRAMES, "global N_TOT = 0");
+    float* out = gamma;
+    if (!out) {
+        if (!c->sh_gamma_ws) CK(c, cudaMalloc(&c->sh_gamma_ws, sizeof(float) * size_t(c->sh_m_count) * Wa * c->p_b));
+        out = c->sh_gamma_ws;
+    }
+    TimedScope ts(c, KC_FINALIZE, st);
+    for (int k = 0; k < c->sh_panels; ++k) {
+        cudaError_t e = cpi::launch_finalize(c->sh_counts + k * chunk * c->p_b, c->p_b, chunk, c->p_b,
+                                             c->sh_marg + k * panel + c->rank * chunk, c->sh_marg + c->p_a,
+                                             static_cast<double>(n_glob), out + k * chunk * c->p_b, c->p_b, st);
+        c->launches += 1;
+        if (e != cudaSuccess) return cuda_fail(c, e, "finalize launch");
+    }
+    c->sh_gamma_cur = out;
+    if (n_tot) *n_tot = n_glob;
+    return CPI_OK;
+}
+}  // namespace
+
+cpi_status cpi_finalize(cpi_ctx* c, float* gamma, int64_t* n_tot, int64_t* row0, int64_t* rows, void* stream) {
     if (!c) return CPI_ERR_INVALID_ARG;
+    CK(c, cudaSetDevice(c->dev));
+    auto st = static_cast<cudaStream_t>(stream);
+    if (c->comm) {
+        cpi_status s = finalize_sharded(c, gamma, n_tot, st);
+        if (s != CPI_OK) return s;
+        if (row0) *row0 = int64_t(c->sh_m_base) * c->cfg.roi_a.width;
+        if (rows) *rows = int64_t(c->sh_m_count) * c->cfg.roi_a.width;
+        return CPI_OK;
+    }
     if (c->n_tot == 0) return fail(c, CPI_ERR_ZERO_FRAMES, "N_TOT = 0");
     if (n_tot) *n_tot = c->n_tot;
+    if (row0) *row0 = 0;
+    if (rows) *rows = c->p_a;
     if (c->gamma_current && (!gamma || gamma == c->gamma_current)) return CPI_OK;
     if (!gamma) return fail(c, CPI_ERR_INVALID_ARG, "gamma_dev is NULL and no fused Gamma exists");
     if (!c->keep) return fail(c, CPI_ERR_STATE, "Gamma from counts needs CPI_KEEP_COUNTS");
-    CK(c, cudaSetDevice(c->dev));
-    auto st = static_cast<cudaStream_t>(stream);
     cpi_status s = ensure_counts(c, st);
     if (s != CPI_OK) return s;
     TimedScope ts(c, KC_FINALIZE, st);
@@ -874,6 +1003,24 @@ cpi_status cpi_finalize(cpi_ctx* c, float* gamma, int64_t* n_tot, void* stream) 
     c->launches += 1;
     if (e != cudaSuccess) return cuda_fail(c, e, "finalize launch");
     c->gamma_current = gamma;
+    return CPI_OK;
+}
+
+cpi_status cpi_shard_layout(const cpi_ctx* c, int32_t* row_block, int32_t* row_stride) {
+    if (!c) return CPI_ERR_INVALID_ARG;
+    const int ha = c->cfg.roi_a.height;
+    if (row_block) *row_block = c->comm ? c->sh_block : ha;
+    if (row_stride) *row_stride = c->comm ? c->sh_stride : ha;
+    return CPI_OK;
+}
+
+cpi_status cpi_nccl_unique_id(uint8_t* id) {
+    if (!id) return CPI_ERR_INVALID_ARG;
+    const cpi::NcclApi* api = cpi::nccl_api();
+    if (!api) return CPI_ERR_NCCL;
+    ncclUniqueId u;
+    if (api->get_unique_id(&u) != ncclSuccess) return CPI_ERR_NCCL;
+    std::memcpy(id, &u, sizeof(u));
     return CPI_OK;
 }
 
@@ -931,6 +1078,32 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
     if (!spec_in || !planes) return fail(c, CPI_ERR_INVALID_ARG, "spec and planes_dev must be non-NULL");
     cpi_refocus_spec spec_local = *spec_in;
     const cpi_refocus_spec* spec = &spec_local;
+    if (!spec_local.gamma_dev && c->comm) {
+        // this rank's Gamma rows of the last cpi_finalize, then the fp64 plane all-reduce (C3)
+        if (!c->sh_gamma_cur) return fail(c, CPI_ERR_STATE, "multi-GPU refocus from the totals needs cpi_finalize first");
+        const int Wa = c->cfg.roi_a.width, Ha = c->cfg.roi_a.height;
+        spec_local.gamma_dev = c->sh_gamma_cur;
+        spec_local.row0 = int64_t(c->sh_m_base) * Wa;
+        spec_local.rows = int64_t(c->sh_m_count) * Wa;
+        spec_local.row_block = c->sh_block;
+        spec_local.row_stride = c->sh_stride;
+        cpi_status s = cpi_refocus(c, &spec_local, planes, stream);
+        if (s != CPI_OK) return s;
+        auto st = static_cast<cudaStream_t>(stream);
+        const size_t n = size_t(spec->n_planes) * Ha * Wa;
+        if (c->planes64_n < n) {
+            cudaFree(c->planes64);
+            c->planes64 = nullptr;
+            c->planes64_n = 0;
+            CK(c, cudaMalloc(&c->planes64, sizeof(double) * n));
+            c->planes64_n = n;
+        }
+        CK(c, cpi::launch_f32_to_f64(planes, c->planes64, int64_t(n), st));
+        NK(c, cpi::nccl_api()->all_reduce(c->planes64, c->planes64, n, ncclFloat64, ncclSum, c->comm, st));
+        CK(c, cpi::launch_f64_to_f32(c->planes64, planes, int64_t(n), st));
+        c->launches += 2;
+        return CPI_OK;
+    }
     if (!spec_local.gamma_dev) {
         // the context's current totals (SURVEY §8(b) CPI_FROM_COUNTS): the fused / finalised
         // Gamma of the last call, else Gamma finalised from the kept counts
@@ -938,7 +1111,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
         if (!c->gamma_current) {
             if (!c->keep) return fail(c, CPI_ERR_STATE, "gamma_dev is NULL: no current Gamma and no kept counts");
             if (!c->gamma_ws) CK(c, cudaMalloc(&c->gamma_ws, sizeof(float) * size_t(c->p_a) * c->p_b));
-            cpi_status s = cpi_finalize(c, c->gamma_ws, nullptr, stream);
+            cpi_status s = cpi_finalize(c, c->gamma_ws, nullptr, nullptr, nullptr, stream);
             if (s != CPI_OK) return s;
         }
         spec_local.gamma_dev = c->gamma_current;

@@ -3,6 +3,7 @@
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nccl.h>   // types of the run-time loaded NCCL (comm.cu); libcpi does not link it
 
 namespace cpi {
 
@@ -189,5 +190,20 @@ cudaError_t launch_pack_ytable_group(const AxisTables* ys, int n_fuse, int Ha, i
 cudaError_t launch_refocus_stage2_group(TElem* const* T, int n_fuse, int Wa, int Ha, int Hb, int m_base, int m_count,
                                         int m_block, int m_stride, const AxisTables* xs, const AxisTables* ys,
                                         const uint32_t* ypack, float* planes, cudaStream_t st);
+
+// NCCL entry points, resolved from libnccl.so.2 at run time (comm.cu); nullptr if unavailable.
+struct NcclApi {
+    ncclResult_t (*get_unique_id)(ncclUniqueId*);
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int);
+    ncclResult_t (*comm_destroy)(ncclComm_t);
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*reduce_scatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*group_start)();
+    ncclResult_t (*group_end)();
+    const char* (*error_string)(ncclResult_t);
+};
+const NcclApi* nccl_api();
+cudaError_t launch_f32_to_f64(const float* a, double* b, int64_t n, cudaStream_t st);
+cudaError_t launch_f64_to_f32(const double* a, float* b, int64_t n, cudaStream_t st);
 
 }  // namespace cpi

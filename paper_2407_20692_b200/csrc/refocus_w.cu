@@ -18,10 +18,11 @@
 //
 // Layout: Gamma with the B pixels in v-major order (include/cpi.h CPI_GAMMA_VMAJOR): column
 // q = u * H_b + v, so for one (A pixel (m, j), u) the v are contiguous.  A tile = (A row m, 128 B
-// rows v, 64 outputs x, group of 4 planes); warps 0-7 take planes 0-1 of the group and warps 8-15
-// planes 2-3, 8 outputs x each.  Per u, lane 0 of warp 0 TMA-loads the group's union j span of
-// Gamma[(m, j)][(u, v0 .. v0 + 127)] (<= 144 rows of 512 B) and the step entries of the tile into a
-// 3-deep ring (the last warp to release a slot refills it).  fp32 partials stay in registers for 8 u and are then added into fp64 accumulators
+// rows v, 32 outputs x, group of 8 planes); warp w takes planes 2 (w / 4) + {0, 1} of the group and
+// outputs 8 (w % 4) + {0..7}.  Per u the group's union j span of Gamma[(m, j)][(u, v0 .. v0 + 127)]
+// (<= 96 rows of 512 B: 80 for the 64-plane grid) and the step entries of the tile are TMA-loaded
+// into a 4-deep ring (the last warp to release a slot refills it).  8 planes share each staged
+// slab, so Gamma crosses HBM ~0.62x as often as with 4-plane groups over 64 outputs.  fp32 partials stay in registers for 8 u and are then added into fp64 accumulators
 // that live in TMEM (64 per lane, 512 columns per CTA).  Tiles are ordered (m, v-block) outer and
 // (plane group, x tile) inner, so the Gamma slab of the tiles in flight (32 MB per (m, v-block)) is
 // reused from L2 by every plane group: Gamma crosses HBM about once per launch for the whole stack.
@@ -33,16 +34,17 @@
 namespace cpi {
 namespace {
 
-constexpr int kWX = 64;                            // outputs x per tile
+constexpr int kWX = 32;                            // outputs x per tile
 constexpr int kWV = 128;                           // B rows v per tile (4 per lane)
 constexpr int kWWarps = 16;
 constexpr int kWXW = 8;                            // outputs x per warp
-constexpr int kWF = 4;                             // planes per group
+constexpr int kWF = 8;                             // planes per group
 constexpr int kWFW = 2;                            // planes per warp
 constexpr int kWBox = 16;                          // j rows per Gamma TMA box
-constexpr int kWRows = 144;                        // staged j rows (9 boxes); larger spans -> refocus.cu
-constexpr int kWStages = 3;
+constexpr int kWRows = 96;                         // staged j rows (6 boxes); larger spans -> plain stage 1
+constexpr int kWStages = 4;
 constexpr int kWFlush = 8;                         // u per fp32 partial before the fp64 flush
+constexpr int kWPrefetch = 0;                      // stages L2-prefetched ahead of the ring (0: off; measured slower)
 // no separate producer warp: a 17th warp would put 5 warps on one SM sub-partition and cap the
 // registers at 96 (the 64 fp32 partials per lane would spill); the last warp to release a ring
 // slot issues its refill
@@ -54,7 +56,8 @@ constexpr int kWStageBytes = kWGBytes + kWEBytes;
 constexpr int kWOffBar = kWStages * kWStageBytes;              // full barriers
 constexpr int kWOffHdr = kWOffBar + kWStages * 8;               // stage headers (16 B each)
 constexpr int kWOffCur = kWOffHdr + kWStages * 16;              // issue cursor (16 B)
-constexpr int kWOffRel = kWOffCur + 16;                         // release counters
+constexpr int kWOffPre = kWOffCur + 16;                         // L2-prefetch cursor (16 B)
+constexpr int kWOffRel = kWOffPre + 16;                         // release counters
 constexpr int kWOffTmem = kWOffRel + kWStages * 4;              // TMEM base slot
 constexpr int kWSmem = kWOffTmem + 16;
 constexpr uint32_t kWInvalid = 0xFFFFFFFFu;        // 32-bit (j0 | t) table: skipped sample / padding x
@@ -71,6 +74,7 @@ constexpr uint32_t kWTmemCols = 512;
 
 static_assert(kWSmem <= 232448, "stage-1 window kernel exceeds the 227 KB shared-memory limit");
 static_assert(kWWarps * kWXW == kWX * (kWF / kWFW), "warps x outputs x planes must cover the tile");
+static_assert(kWWarps * kWFW * kWXW * 4 * 2 <= 4 * 128 * 32 * 4, "fp64 accumulators exceed TMEM");
 
 __device__ __forceinline__ uint64_t pk2(float lo, float hi) {
     uint64_t r;
@@ -169,6 +173,23 @@ __device__ __forceinline__ bool w_more_in_tile(const S1WArgs& a, int t, int u) {
     }
     return false;
 }
+// L2-prefetch the Gamma boxes of the next stage of the prefetch cursor (which runs kWPrefetch stages
+// ahead of the load cursor), so that the ring's TMA loads find them in L2.
+__device__ __forceinline__ void w_prefetch_next(WCursor* pc, const S1WArgs& a, int n_tiles, const CUtensorMap* tm_g) {
+    WCursor c = *pc;
+    int2 sp;
+    bool first;
+    if (!w_next(c, a, n_tiles, sp, first)) {
+        *pc = c;
+        return;
+    }
+    const WTile w = w_tile(a, c.t);
+    const int nb = (sp.y - sp.x + kWBox) / kWBox;
+    for (int b = 0; b < nb; ++b) tma_prefetch_4d(tm_g, w.vb * kWV, c.u, sp.x + b * kWBox, w.ml);
+    ++c.u;   // (w_next moves on to the next tile when u runs past the last column)
+    *pc = c;
+}
+
 // Issue the next stage into ring slot s (single thread).
 __device__ __forceinline__ void w_issue(WCursor* cur, WHeader* hdr, int s, const S1WArgs& a, int n_tiles,
                                         const CUtensorMap* tm_g, const CUtensorMap* tm_e, uint8_t* smem,
@@ -247,6 +268,7 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
     uint64_t* full = reinterpret_cast<uint64_t*>(w_smem + kWOffBar);
     WHeader* hdr = reinterpret_cast<WHeader*>(w_smem + kWOffHdr);
     WCursor* cur = reinterpret_cast<WCursor*>(w_smem + kWOffCur);
+    WCursor* pcur = reinterpret_cast<WCursor*>(w_smem + kWOffPre);
     int* rel = reinterpret_cast<int*>(w_smem + kWOffRel);
     uint32_t* tslot = reinterpret_cast<uint32_t*>(w_smem + kWOffTmem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -258,9 +280,12 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
         }
         fence_mbar_init();
         *cur = WCursor{static_cast<int>(blockIdx.x), 0, 0, 0};
+        *pcur = WCursor{static_cast<int>(blockIdx.x), 0, 0, 0};
         tma_prefetch_desc(&tm_g);
         tma_prefetch_desc(&tm_e);
         for (int s = 0; s < kWStages; ++s) w_issue(cur, hdr, s, a, n_tiles, &tm_g, &tm_e, w_smem, full);
+        if (kWPrefetch > 0)
+            for (int s = 0; s < kWStages + kWPrefetch; ++s) w_prefetch_next(pcur, a, n_tiles, &tm_g);
     }
     if (warp == 0) tmem_alloc(tslot, kWTmemCols);
     tc_fence_before();
@@ -268,9 +293,9 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
     tc_fence_after();
     const uint32_t tmem = *tslot;
 
-    // warp: planes 2 (warp / 8) + {0, 1} of the group, outputs x = x tile + 8 (warp % 8) + i;
+    // warp: planes 2 (warp / 4) + {0, 1} of the group, outputs x = x tile + 8 (warp % 4) + i;
     // lane: B rows v = v block + 4 lane + {0..3}
-    const int wp = warp >> 3, wx = warp & 7;
+    const int wp = warp >> 2, wx = warp & 3;
     const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + static_cast<uint32_t>(warp >> 2) * 128u;
     const uint32_t lane16 = 16u * lane;
     uint64_t part[kWFW][kWXW][2];
@@ -330,6 +355,7 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
                 rel[stage] = 0;
                 __threadfence_block();
                 w_issue(cur, hdr, stage, a, n_tiles, &tm_g, &tm_e, w_smem, full);
+                if (kWPrefetch > 0) w_prefetch_next(pcur, a, n_tiles, &tm_g);
             }
         }
         __syncwarp();

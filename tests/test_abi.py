@@ -33,7 +33,7 @@ def test_header_symbols_exported(lib):
 
 
 def test_abi_version_and_status_names(lib):
-    assert lib.cpi_abi_version() == 104
+    assert lib.cpi_abi_version() == 200
     assert lib.cpi_status_string(0) == b"CPI_OK"
     assert lib.cpi_status_string(-7) == b"CPI_ERR_DEGENERATE_ALPHA"
     assert lib.cpi_status_string(-12) == b"CPI_ERR_UNSUPPORTED"
@@ -89,7 +89,9 @@ def test_null_handles(lib):
     assert lib.cpi_correlate_rows(None, 0, 256, None, None) == -1
     assert lib.cpi_row_align(None) == 0
     assert lib.cpi_counts_dev(None, None, None, None) == -1
-    assert lib.cpi_finalize(None, None, None, None) == -1
+    assert lib.cpi_finalize(None, None, None, None, None, None) == -1
+    assert lib.cpi_shard_layout(None, None, None) == -1
+    assert lib.cpi_nccl_unique_id(None) == -1
     assert lib.cpi_finalize_counts(None, None, 0, 0, None, None, 1, None, None) == -1
     assert lib.cpi_get_counts(None, None, None, None, None, None) == -1
     assert lib.cpi_reset(None, None) == -1
