@@ -48,7 +48,8 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="cb200", choices=["cb200", "reference"])
-    p.add_argument("--frames", type=int, default=10_000, help="frames per step per rank")
+    p.add_argument("--frames", type=int, default=10_000,
+                   help="frames per step, split across the ranks (strong scaling of the configs[1] step)")
     p.add_argument("--planes", type=int, default=64, help="refocus planes per step")
     p.add_argument("--occupancy", type=float, default=0.05, help="Bernoulli f of the synthetic bits")
     p.add_argument("--variant", default=STEP_VARIANT, choices=["tc", "popc", "fp4"],
@@ -57,8 +58,11 @@ def parse():
     p.add_argument("--roi", default="full", choices=["full", "128", "tiny"])
     p.add_argument("--gamma-order", default=STEP_GAMMA_ORDER, choices=["ublocked", "rowmajor", "vmajor"],
                    help="column order of the step's Gamma (include/cpi.h CPI_GAMMA_UBLOCKED)")
-    p.add_argument("--parallel-mode", default="rows", choices=["rows", "tiles"],
-                   help="multi-GPU: rows = frame sharding + panelised reduce-scatter (north_star); tiles = "
+    p.add_argument("--parallel-mode", default="auto", choices=["auto", "lib", "rows", "tiles"],
+                   help="multi-GPU: lib = frame sharding with the library's own NCCL reduce-scatter / all-reduces "
+                        "(cpi_config rank/world, north_star); rows = the same over torch.distributed "
+                        "(parallel.py); auto = tiles when all-gathering the packed frames moves fewer bytes than "
+                        "reduce-scattering the int32 partial S_ab (N * 16 KB < 4 P_a P_b), else lib; tiles = "
                         "all-gather of frames + each rank's own Gamma rows (SURVEY §8(e) control)")
     p.add_argument("--sharded", action="store_true",
                    help="run the frame-sharded multi-GPU pipeline (NCCL) even at one rank (tests its code path)")
@@ -66,6 +70,10 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-pixels", type=int, default=48, help="oracle sample: refocused output pixels per alpha")
     return p.parse_args()
+
+
+def frame_bytes_of(args):
+    return synth.frame_bytes()
 
 
 def rois(name):
@@ -342,25 +350,43 @@ def main():
     p_a, p_b = roi_a[2] * roi_a[3], roi_b[2] * roi_b[3]
     Wa, Ha, Wb, Hb = roi_a[2], roi_a[3], roi_b[2], roi_b[3]
     alphas = synth.alpha_grid(args.planes)
-    n = args.frames
-    # this rank's slice of the global frame sequence (weak scaling: n frames per rank)
-    frames_np = synth.bernoulli_frames(n, args.occupancy, seed=synth.SEED_ARMS, frame0=rank * n)
+    n_total = args.frames
+    # this rank's contiguous slice of the step's frames (strong scaling: the same configs[1] step at
+    # every N; Eq. (1)'s sums are additive over slices)
+    f_lo, f_hi = parallel.frame_slice(n_total, rank, world)
+    n = f_hi - f_lo
+    frames_np = synth.bernoulli_frames(n, args.occupancy, seed=synth.SEED_ARMS, frame0=f_lo)
     frames_host = torch.from_numpy(frames_np).pin_memory()
     frames_dev = frames_host.to(dev)
     stream = torch.cuda.current_stream(dev)
 
+    mode, tiles = "single", False
     if not use_dist:
         ctx = Context(roi_a, roi_b, n, device=local, variant=args.variant,
                       gamma_order=args.gamma_order)
         gamma = ctx.new_gamma()
         planes = ctx.new_planes(args.planes)
     else:
-        # frame-sharded pipeline (parallel.py): GEMM row panels reduce-scattered as they finish,
-        # block-cyclic Gamma row ownership, shard refocus, plane all-reduce
-        tiles = args.parallel_mode == "tiles"
-        backend = parallel.CudaBackend(roi_a, roi_b, n * world if tiles else n, device=local, variant=args.variant,
-                                       gamma_order=args.gamma_order, keep_counts=not tiles)
-        ctx = backend.ctx
+        mode = args.parallel_mode
+        if mode == "auto":   # DESIGN §9 cost model: bytes each rank sends per step
+            mode = "tiles" if n_total * frame_bytes_of(args) < 4 * p_a * p_b else "lib"
+        tiles = mode == "tiles"
+        if mode == "lib":
+            # the library's own multi-GPU contract (include/cpi.h cpi_config rank / world / nccl_id):
+            # cpi_finalize reduce-scatters the partial S_ab and all-reduces [S_a|S_b|N] over its NCCL
+            # communicator, cpi_refocus from the totals refocuses the owned rows and all-reduces planes
+            from paper_2407_20692_b200 import nccl_unique_id
+            box = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(box, src=0)
+            ctx = Context(roi_a, roi_b, n, device=local, variant=args.variant, gamma_order=args.gamma_order,
+                          keep_counts=True, rank=rank, world=world, nccl_id=box[0])
+            planes = ctx.new_planes(args.planes)
+        else:
+            # torch.distributed orchestration (parallel.py): rows = GEMM row panels reduce-scattered as
+            # they finish; tiles = all-gather of the packed frames, each rank its own Gamma rows
+            backend = parallel.CudaBackend(roi_a, roi_b, n_total if tiles else n, device=local, variant=args.variant,
+                                           gamma_order=args.gamma_order, keep_counts=not tiles)
+            ctx = backend.ctx
     planes_host = torch.empty((args.planes, Ha, Wa), dtype=torch.float32).pin_memory()
 
     def step(src):
@@ -371,6 +397,13 @@ def main():
             ctx.load_frames(src)
             ctx.correlate(gamma)
             ctx.refocus(alphas, gamma, planes)
+            return planes
+        if mode == "lib":
+            ctx.reset()
+            ctx.load_frames(src)
+            ctx.correlate(None)
+            ctx.finalize(None)
+            ctx.refocus(alphas, None, planes)
             return planes
         run = parallel.correlate_and_refocus_tiles if tiles else parallel.correlate_and_refocus
         res = run(backend, src, roi_a, roi_b, alphas)
@@ -409,7 +442,7 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_ms = float(tt.item())
     ms_step = t_ms / args.steps
-    value = n * world / (ms_step / 1e3)
+    value = n_total / (ms_step / 1e3)
 
     # ---- end to end through the public API with host buffers --------------------------
     e2e = None
@@ -429,7 +462,7 @@ def main():
             tt = torch.tensor([te], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
-        e2e = {"value": n * world / (te / args.steps / 1e3), "unit": "frames/s",
+        e2e = {"value": n_total / (te / args.steps / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": int(frames_np.nbytes), "d2h_bytes_per_step": int(planes_host.numel() * 4),
                "ms_per_step": te / args.steps}
 
@@ -444,7 +477,8 @@ def main():
     hbm = peaks["hbm_gbs"]
     f_clk = (clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)) * 1e6
     gemm_ms, gemm_n = kt["gemm"]
-    ops = 2.0 * p_a * p_b * n                         # algorithmic: one AND/MAC per pair per frame
+    # algorithmic ops of this rank's GEMM: one AND/MAC per pair per frame (tiles: own rows, all frames)
+    ops = 2.0 * p_a * p_b * n if not (use_dist and tiles) else 2.0 * (p_a // world) * p_b * n_total
     gemm_tops = ops / (gemm_ms / gemm_n / 1e3) / 1e12 if gemm_n else None
     clock_peak_tops = 148 * 8192 * 2 * f_clk / 1e12  # tcgen05 kind::i8: 8192 MAC/clk/SM
     s1_ms, s1_n = kt["stage1"]
@@ -517,19 +551,21 @@ def main():
         cpu = cpu_baseline(frames_np, roi_a, roi_b, alphas, args.cpu_pixels, args.planes)
     out = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None,
         "dtype": {"tc": "u8 x u8 -> s32 (S_ab)", "popc": "u32 popc(and) -> s32 (S_ab)",
                   "fp4": "e2m1 {0,1} x e2m1 -> f32 exact integers -> s32 (S_ab)"}[args.variant]
                  + ", f64 -> f32 (Gamma), f32/f64 (refocus)",
         "data": "synthetic",
         "config": {"workload": (f"configs[1] (+configs[3] stack): SwissSPAD2 256x512 frames, rho_a {roi_a}, "
-                                f"rho_b {roi_b}, {n} Bernoulli({args.occupancy}) frames per rank per step "
-                                f"-> Gamma {p_a}x{p_b} -> {args.planes}-plane refocus stack"),
-                   "frames_per_step_per_rank": n, "planes_per_step": args.planes,
+                                f"rho_b {roi_b}, {n_total} Bernoulli({args.occupancy}) frames per step "
+                                f"(split across {world} rank(s)) -> Gamma {p_a}x{p_b} -> {args.planes}-plane "
+                                f"refocus stack"),
+                   "frames_per_step": n_total, "frames_per_step_per_rank": n, "planes_per_step": args.planes,
                    "alphas": "linspace(0.5, 2.0, P)", "variant": args.variant, "gamma_order": args.gamma_order,
-                   "parallelism": (f"frame-sharded x{world}" + (" (output-tile sharding)" if args.parallel_mode == "tiles"
-                                                                else " (panelised reduce-scatter)"))
+                   "parallelism": (f"frame-sharded x{world} (" + {"lib": "library NCCL reduce-scatter",
+                                                                   "rows": "torch.distributed panelised reduce-scatter",
+                                                                   "tiles": "output-tile sharding"}[mode] + ")")
                    if use_dist else "single GPU",
                    "l2": "inputs larger than L2 (Gamma 17 GB, operands 1.3 GB) - no flush needed"},
         "gpu_launches": launches,
@@ -540,7 +576,7 @@ def main():
                                "refocus_coords": kt["coords"][0] / args.steps,
                                "refocus_stage1": s1_ms / args.steps, "refocus_stage2": kt["stage2"][0] / args.steps,
                                "finalize": kt["finalize"][0] / args.steps},
-        "correlation_frames_per_s": n * world / (corr_ms / 1e3) if corr_ms else None,
+        "correlation_frames_per_s": n_total / (corr_ms / 1e3) if corr_ms else None,
         "planes_per_s": args.planes / (ref_ms / 1e3) if ref_ms else None,
         "clocks": clk,
         "e2e": e2e,

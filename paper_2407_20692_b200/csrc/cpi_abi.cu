@@ -357,7 +357,7 @@ cpi_status refocus_vmajor(cpi_ctx* c, const cpi_refocus_spec* spec, float* plane
         return k[0] == l[0] && k[1] == l[1] && k[2] == l[2] && k[3] == l[3];
     };
     const int64_t t_plane = int64_t(Wa) * Ha * Hb;
-    const int gf = cpi::stage1_w_group();
+    const int gf = cpi::kRefocusMaxFuse;   // planes per coordinate / stage-2 launch (their argument arrays)
     int resampled = -1;
     for (int p0 = 0; p0 < spec->n_planes;) {
         int nb = 1;   // planes of this batch: one Gamma source

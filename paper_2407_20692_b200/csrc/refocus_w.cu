@@ -44,7 +44,6 @@ constexpr int kWBox = 16;                          // j rows per Gamma TMA box
 constexpr int kWRows = 96;                         // staged j rows (6 boxes); larger spans -> plain stage 1
 constexpr int kWStages = 4;
 constexpr int kWFlush = 8;                         // u per fp32 partial before the fp64 flush
-constexpr int kWPrefetch = 0;                      // stages L2-prefetched ahead of the ring (0: off; measured slower)
 // no separate producer warp: a 17th warp would put 5 warps on one SM sub-partition and cap the
 // registers at 96 (the 64 fp32 partials per lane would spill); the last warp to release a ring
 // slot issues its refill
@@ -56,10 +55,11 @@ constexpr int kWStageBytes = kWGBytes + kWEBytes;
 constexpr int kWOffBar = kWStages * kWStageBytes;              // full barriers
 constexpr int kWOffHdr = kWOffBar + kWStages * 8;               // stage headers (16 B each)
 constexpr int kWOffCur = kWOffHdr + kWStages * 16;              // issue cursor (16 B)
-constexpr int kWOffPre = kWOffCur + 16;                         // L2-prefetch cursor (16 B)
-constexpr int kWOffRel = kWOffPre + 16;                         // release counters
+constexpr int kWOffRel = kWOffCur + 16;                         // release counters
 constexpr int kWOffTmem = kWOffRel + kWStages * 4;              // TMEM base slot
-constexpr int kWSmem = kWOffTmem + 16;
+constexpr int kWMaxWb = 512;                                    // B columns (tile span row copy)
+constexpr int kWOffSpan = (kWOffTmem + 16 + 15) / 16 * 16;      // the issuing cursor's tile span row
+constexpr int kWSmem = kWOffSpan + kWMaxWb * 8;
 constexpr uint32_t kWInvalid = 0xFFFFFFFFu;        // 32-bit (j0 | t) table: skipped sample / padding x
 // 64-bit step entry of (plane, u, x) for a warp walking its 8 outputs x in order.  The warp keeps
 // two row registers, slot A for the even and slot B for the odd stage row of the pair (j0, j0 + 1):
@@ -131,10 +131,10 @@ __device__ __forceinline__ bool w_needed(const S1WArgs& a, const WTile& w, int m
 // that warp's own refill issue of stage k - 1 + kWStages.  The refill writes a header into the
 // slot -- which tile the stage belongs to and whether it is the tile's first / last stage -- so
 // the consumers only follow headers (no tile or span logic of their own); tile = -1 ends the CTA.
-struct WCursor {   // the next (tile, u) stage to load (shared memory, touched by one issuer at a time)
+struct WCursor {   // the next (tile, u) stage to load (shared memory, touched by one issuing warp at a time)
     int t, u;
-    int tile_started;   // the current tile has issued a stage
-    int pad;
+    int started;   // the current tile has issued a stage
+    int loaded;    // the current tile's span row is in the shared-memory copy
 };
 struct WHeader {
     int tile;    // -1: no more stages
@@ -142,81 +142,72 @@ struct WHeader {
     int pad[2];
 };
 
-// Next non-empty (tile, u) stage of this CTA after the cursor; returns false at the end.
-__device__ __forceinline__ bool w_next(WCursor& c, const S1WArgs& a, int n_tiles, int2& sp, bool& first) {
-    while (c.t < n_tiles) {
-        const WTile w = w_tile(a, c.t);
-        if (c.u == 0 && !c.tile_started && !w_needed(a, w, w_shard_row(a, w.ml))) { c.t += gridDim.x; continue; }
-        const int2* sp_row = a.span + static_cast<int64_t>(w.g * a.n_xt + w.xt) * a.Wb;
-        while (c.u < a.Wb) {
-            sp = __ldg(sp_row + c.u);
-            if (sp.y >= sp.x) {
-                first = !c.tile_started;
-                c.tile_started = 1;
-                return true;
-            }
-            ++c.u;
+// First u >= u0 of the cursor tile with a non-empty span (-1: none); warp-collective (ballots
+// over 32 columns of the shared-memory span row).
+__device__ __forceinline__ int w_next_u(const int2* tspan, int Wb, int u0, int lane) {
+    for (int base = u0; base < Wb; base += 32) {
+        const int u = base + lane;
+        bool ne = false;
+        if (u < Wb) {
+            const int2 sp = tspan[u];
+            ne = sp.y >= sp.x;
         }
-        c.t += gridDim.x;
-        c.u = 0;
-        c.tile_started = 0;
+        const unsigned m = __ballot_sync(0xffffffffu, ne);
+        if (m) return base + __ffs(m) - 1;
     }
-    return false;
-}
-// Has the tile of the cursor another non-empty stage after u? (the last-stage flag)
-__device__ __forceinline__ bool w_more_in_tile(const S1WArgs& a, int t, int u) {
-    const WTile w = w_tile(a, t);
-    const int2* sp_row = a.span + static_cast<int64_t>(w.g * a.n_xt + w.xt) * a.Wb;
-    for (int uu = u + 1; uu < a.Wb; ++uu) {
-        const int2 sp = __ldg(sp_row + uu);
-        if (sp.y >= sp.x) return true;
-    }
-    return false;
-}
-// L2-prefetch the Gamma boxes of the next stage of the prefetch cursor (which runs kWPrefetch stages
-// ahead of the load cursor), so that the ring's TMA loads find them in L2.
-__device__ __forceinline__ void w_prefetch_next(WCursor* pc, const S1WArgs& a, int n_tiles, const CUtensorMap* tm_g) {
-    WCursor c = *pc;
-    int2 sp;
-    bool first;
-    if (!w_next(c, a, n_tiles, sp, first)) {
-        *pc = c;
-        return;
-    }
-    const WTile w = w_tile(a, c.t);
-    const int nb = (sp.y - sp.x + kWBox) / kWBox;
-    for (int b = 0; b < nb; ++b) tma_prefetch_4d(tm_g, w.vb * kWV, c.u, sp.x + b * kWBox, w.ml);
-    ++c.u;   // (w_next moves on to the next tile when u runs past the last column)
-    *pc = c;
+    return -1;
 }
 
-// Issue the next stage into ring slot s (single thread).
-__device__ __forceinline__ void w_issue(WCursor* cur, WHeader* hdr, int s, const S1WArgs& a, int n_tiles,
-                                        const CUtensorMap* tm_g, const CUtensorMap* tm_e, uint8_t* smem,
-                                        uint64_t* full) {
+// Issue the next stage into ring slot s; warp-collective (the warp that released the slot last).
+// When the cursor moves to a new tile the warp copies that tile's span row into shared memory
+// (one coalesced pass), so an issue costs shared-memory scans and lane 0's TMA instructions.
+__device__ __forceinline__ void w_issue(WCursor* cur, int2* tspan, WHeader* hdr, int s, const S1WArgs& a,
+                                        int n_tiles, const CUtensorMap* tm_g, const CUtensorMap* tm_e,
+                                        uint8_t* smem, uint64_t* full, int lane) {
     WCursor c = *cur;
-    int2 sp;
-    bool first;
-    if (!w_next(c, a, n_tiles, sp, first)) {
-        hdr[s].tile = -1;
-        hdr[s].flags = 0;
-        *cur = c;
-        mbar_arrive(&full[s]);   // release: consumers see the end marker
+    for (;;) {
+        if (c.t >= n_tiles) {
+            if (lane == 0) {
+                hdr[s].tile = -1;
+                hdr[s].flags = 0;
+                *cur = c;
+                mbar_arrive(&full[s]);   // release: consumers see the end marker
+            }
+            __syncwarp();
+            return;
+        }
+        const WTile w = w_tile(a, c.t);
+        if (!c.loaded) {
+            if (!w_needed(a, w, w_shard_row(a, w.ml))) { c.t += gridDim.x; continue; }
+            const int2* sp_row = a.span + static_cast<int64_t>(w.g * a.n_xt + w.xt) * a.Wb;
+            __syncwarp();
+            for (int u = lane; u < a.Wb; u += 32) tspan[u] = __ldg(sp_row + u);
+            __syncwarp();
+            c.loaded = 1;
+            c.u = 0;
+            c.started = 0;
+        }
+        const int u = w_next_u(tspan, a.Wb, c.u, lane);
+        if (u < 0) { c.t += gridDim.x; c.loaded = 0; continue; }
+        const bool last = w_next_u(tspan, a.Wb, u + 1, lane) < 0;
+        if (lane == 0) {
+            const int2 sp = tspan[u];
+            hdr[s].tile = c.t;
+            hdr[s].flags = (c.started ? 0 : 1) | (last ? 2 : 0);
+            const int nb = (sp.y - sp.x + kWBox) / kWBox;
+            mbar_expect_tx(&full[s], nb * kWBox * kWRowBytes + kWEBytes);
+            uint8_t* dst = smem + s * kWStageBytes;
+            for (int b = 0; b < nb; ++b)
+                tma_load_4d(dst + b * kWBox * kWRowBytes, tm_g, &full[s], w.vb * kWV, u, sp.x + b * kWBox, w.ml);
+            tma_load_3d(dst + kWGBytes, tm_e, &full[s], 2 * w.xt * kWX, u, w.g * kWF);
+            c.u = u + 1;
+            c.started = 1;
+            if (last) { c.t += gridDim.x; c.loaded = 0; }
+            *cur = c;
+        }
+        __syncwarp();
         return;
     }
-    const WTile w = w_tile(a, c.t);
-    const bool last = !w_more_in_tile(a, c.t, c.u);
-    hdr[s].tile = c.t;
-    hdr[s].flags = (first ? 1 : 0) | (last ? 2 : 0);
-    const int nb = (sp.y - sp.x + kWBox) / kWBox;
-    mbar_expect_tx(&full[s], nb * kWBox * kWRowBytes + kWEBytes);
-    uint8_t* dst = smem + s * kWStageBytes;
-    for (int b = 0; b < nb; ++b)
-        tma_load_4d(dst + b * kWBox * kWRowBytes, tm_g, &full[s], w.vb * kWV, c.u, sp.x + b * kWBox, w.ml);
-    tma_load_3d(dst + kWGBytes, tm_e, &full[s], 2 * w.xt * kWX, c.u, w.g * kWF);
-    ++c.u;
-    if (last) { c.t += gridDim.x; c.u = 0; c.tile_started = 0; }
-    *cur = c;
 }
 
 // fp64 accumulators of a warp in TMEM: plane pl (of the warp's 2), output i, v slot k (of the
@@ -268,7 +259,7 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
     uint64_t* full = reinterpret_cast<uint64_t*>(w_smem + kWOffBar);
     WHeader* hdr = reinterpret_cast<WHeader*>(w_smem + kWOffHdr);
     WCursor* cur = reinterpret_cast<WCursor*>(w_smem + kWOffCur);
-    WCursor* pcur = reinterpret_cast<WCursor*>(w_smem + kWOffPre);
+    int2* tspan = reinterpret_cast<int2*>(w_smem + kWOffSpan);
     int* rel = reinterpret_cast<int*>(w_smem + kWOffRel);
     uint32_t* tslot = reinterpret_cast<uint32_t*>(w_smem + kWOffTmem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -280,12 +271,12 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
         }
         fence_mbar_init();
         *cur = WCursor{static_cast<int>(blockIdx.x), 0, 0, 0};
-        *pcur = WCursor{static_cast<int>(blockIdx.x), 0, 0, 0};
         tma_prefetch_desc(&tm_g);
         tma_prefetch_desc(&tm_e);
-        for (int s = 0; s < kWStages; ++s) w_issue(cur, hdr, s, a, n_tiles, &tm_g, &tm_e, w_smem, full);
-        if (kWPrefetch > 0)
-            for (int s = 0; s < kWStages + kWPrefetch; ++s) w_prefetch_next(pcur, a, n_tiles, &tm_g);
+    }
+    if (warp == 0) {   // fill the ring
+        __syncwarp();
+        for (int s = 0; s < kWStages; ++s) w_issue(cur, tspan, hdr, s, a, n_tiles, &tm_g, &tm_e, w_smem, full, lane);
     }
     if (warp == 0) tmem_alloc(tslot, kWTmemCols);
     tc_fence_before();
@@ -349,15 +340,15 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
         // last warp to release it issues the refill
         fence_proxy_async_smem();
         __syncwarp();
+        int last_rel = 0;
         if (lane == 0) {
             __threadfence_block();
-            if (atomicAdd(&rel[stage], 1) == kWWarps - 1) {
-                rel[stage] = 0;
-                __threadfence_block();
-                w_issue(cur, hdr, stage, a, n_tiles, &tm_g, &tm_e, w_smem, full);
-                if (kWPrefetch > 0) w_prefetch_next(pcur, a, n_tiles, &tm_g);
-            }
+            last_rel = atomicAdd(&rel[stage], 1) == kWWarps - 1;
+            if (last_rel) rel[stage] = 0;
+            __threadfence_block();
         }
+        if (__shfl_sync(0xffffffffu, last_rel, 0))
+            w_issue(cur, tspan, hdr, stage, a, n_tiles, &tm_g, &tm_e, w_smem, full, lane);
         __syncwarp();
         const int this_stage = stage;
         if (++stage == kWStages) { stage = 0; phase ^= 1; }
