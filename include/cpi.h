@@ -81,14 +81,16 @@ typedef int32_t cpi_status;
                                  refocusing stages, each 8 u x 8 v block as one contiguous 256-B
                                  segment (faster refocus, same arithmetic).  Needs
                                  roi_b.width % 8 == 0. */
-#define CPI_GAMMA_VMAJOR  16u /* B pixels are ordered v-major everywhere in this context: B pixel
-                                 q = v*W_b + u has index u*H_b + v in S_b, in the columns of S_ab
+#define CPI_GAMMA_VMAJOR  16u /* B pixels are ordered v-major in blocks of VB = min(H_b, 128) rows
+                                 everywhere in this context: B pixel q = v*W_b + u has index
+                                 (v / VB)*(W_b*VB) + u*VB + v % VB in S_b, in the columns of S_ab
                                  and of every Gamma it writes or cpi_refocus reads.  For one A
-                                 pixel and one B column u the H_b values are contiguous, which is
-                                 what the window stage 1 (KB5w) stages: all lanes of a
-                                 warp share one (x, u) sample and reuse the two Gamma rows of
-                                 neighbouring outputs from registers.  Needs roi_b.height % 4 == 0;
-                                 exclusive with CPI_GAMMA_UBLOCKED.  Refocusing spans longer than
+                                 pixel, one v block and one B column u the VB values are
+                                 contiguous (and consecutive u adjacent), which is what the window
+                                 stage 1 (KB5w) stages: all lanes of a warp share one
+                                 (x, u) sample and reuse the two Gamma rows of neighbouring outputs
+                                 from registers.  Needs roi_b.height % 4 == 0 and, above 128, a
+                                 multiple of 128; exclusive with CPI_GAMMA_UBLOCKED.  Refocusing spans longer than
                                  the kernel's stage (A-axis map slopes above ~2.2) and W_a > 256 run
                                  a plain staged stage 1 (contiguous row shards only). */
 

@@ -282,8 +282,9 @@ class Context:
         if self.gamma_order == "rowmajor":
             return q
         v, u = q // Wb, q % Wb
-        if self.gamma_order == "vmajor":
-            return u * Hb + v
+        if self.gamma_order == "vmajor":   # include/cpi.h: blocks of 128 B rows (kernels.h vmajor_slot)
+            vb = min(Hb, 128)
+            return (v // vb) * (Wb * vb) + u * vb + v % vb
         return (u // 8) * (8 * Hb) + 8 * v + (u % 8)
 
     def new_gamma(self):

@@ -426,11 +426,15 @@ cpi_status refocus_vmajor(cpi_ctx* c, const cpi_refocus_spec* spec, float* plane
                 cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
                 if (!enc) return fail(c, CPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
                 CUtensorMap tg, te;
-                const cuuint64_t gd[4] = {cuuint64_t(Hb), cuuint64_t(Wb), cuuint64_t(Wa), cuuint64_t(m_count)};
-                const cuuint64_t gs[3] = {cuuint64_t(Hb) * 4, cuuint64_t(c->p_b) * 4, cuuint64_t(Wa) * c->p_b * 4};
-                const cuuint32_t gb[4] = {cuuint32_t(cpi::stage1_w_vblock()), 1u, cuuint32_t(cpi::stage1_w_jbox()), 1u};
-                const cuuint32_t es4[4] = {1u, 1u, 1u, 1u};
-                CUresult r = enc(&tg, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(gsrc), gd, gs, gb, es4,
+                // (v % VB, u, v / VB, j, local m) over the blocked v-major columns (kernels.h vmajor_slot)
+                const int vbs = cpi::vmajor_block(Hb);
+                const cuuint64_t gd[5] = {cuuint64_t(vbs), cuuint64_t(Wb), cuuint64_t(Hb / vbs), cuuint64_t(Wa),
+                                          cuuint64_t(m_count)};
+                const cuuint64_t gs[4] = {cuuint64_t(vbs) * 4, cuuint64_t(Wb) * vbs * 4, cuuint64_t(c->p_b) * 4,
+                                          cuuint64_t(Wa) * c->p_b * 4};
+                const cuuint32_t gb[5] = {cuuint32_t(cpi::stage1_w_vblock()), 1u, 1u, cuuint32_t(cpi::stage1_w_jbox()), 1u};
+                const cuuint32_t es4[5] = {1u, 1u, 1u, 1u, 1u};
+                CUresult r = enc(&tg, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(gsrc), gd, gs, gb, es4,
                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
                 if (r != CUDA_SUCCESS) return fail(c, CPI_ERR_CUDA, "Gamma tensor map (v-major) failed (%d)", int(r));
@@ -446,6 +450,7 @@ cpi_status refocus_vmajor(cpi_ctx* c, const cpi_refocus_spec* spec, float* plane
                 a.Wa = Wa; a.Ha = Ha; a.Wb = Wb; a.Hb = Hb;
                 a.m_base = m_base; a.m_count = m_count; a.m_block = m_block; a.m_stride = m_stride;
                 a.n_planes = nb; a.span = c->w_span; a.mband = c->w_mband; a.T = c->w_T; a.t_plane = t_plane;
+                if (const char* ev = getenv("CPI_S1W_PROBE")) a.probe = atoi(ev);   // timing probe only
                 e = cpi::launch_refocus_stage1_w(&tg, &te, a, c->num_sms, st);
                 c->launches += 1;
             } else {
@@ -535,8 +540,10 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
         return fail(nullptr, CPI_ERR_UNSUPPORTED, "CPI_GAMMA_UBLOCKED needs roi_b.width %% 8 == 0");
     if ((cfg->flags & CPI_GAMMA_VMAJOR) && (cfg->flags & CPI_GAMMA_UBLOCKED))
         return fail(nullptr, CPI_ERR_INVALID_ARG, "CPI_GAMMA_VMAJOR and CPI_GAMMA_UBLOCKED are exclusive");
-    if ((cfg->flags & CPI_GAMMA_VMAJOR) && cfg->roi_b.height % 4)
-        return fail(nullptr, CPI_ERR_UNSUPPORTED, "CPI_GAMMA_VMAJOR needs roi_b.height %% 4 == 0");
+    if ((cfg->flags & CPI_GAMMA_VMAJOR) &&
+        (cfg->roi_b.height % 4 || (cfg->roi_b.height > cpi::kVMajorBlock && cfg->roi_b.height % cpi::kVMajorBlock)))
+        return fail(nullptr, CPI_ERR_UNSUPPORTED, "CPI_GAMMA_VMAJOR needs roi_b.height %% 4 == 0 and, above %d, a "
+                                                  "multiple of %d", cpi::kVMajorBlock, cpi::kVMajorBlock);
     if (cfg->flags & ~(CPI_VARIANT_POPC | CPI_KEEP_COUNTS | CPI_VARIANT_FP4 | CPI_GAMMA_UBLOCKED | CPI_GAMMA_VMAJOR))
         return fail(nullptr, CPI_ERR_INVALID_ARG, "unknown flags 0x%x", cfg->flags);
     if ((cfg->flags & CPI_VARIANT_POPC) && (cfg->flags & CPI_VARIANT_FP4))

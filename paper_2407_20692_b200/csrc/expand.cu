@@ -20,10 +20,10 @@ namespace {
 constexpr int kThreads = 256;
 
 // operand row / sum slot of RoI pixel (m, j) (include/cpi.h B pixel orders): row-major m * w + j,
-// u-blocked (j / 8) * (8 h) + 8 m + j % 8 (CPI_GAMMA_UBLOCKED), v-major j * h + m (CPI_GAMMA_VMAJOR)
+// u-blocked (j / 8) * (8 h) + 8 m + j % 8 (CPI_GAMMA_UBLOCKED), v-major vmajor_slot (CPI_GAMMA_VMAJOR)
 __device__ __forceinline__ int64_t pixel_slot(int order, int m, int j, const RoiDev& roi) {
     if (order == kOrderUBlocked) return static_cast<int64_t>(j >> 3) * (8 * roi.h) + 8 * m + (j & 7);
-    if (order == kOrderVMajor) return static_cast<int64_t>(j) * roi.h + m;
+    if (order == kOrderVMajor) return vmajor_slot(j, m, roi.w, roi.h);
     return static_cast<int64_t>(m) * roi.w + j;
 }
 constexpr int kSub = 128;       // frames per staged sub-block

@@ -37,6 +37,16 @@ enum { kExpandU8 = 0, kExpandBits = 1, kExpandE2M1 = 2 };
 // (j / 8) * (8 * roi.h) + 8 * m + j % 8 (CPI_GAMMA_UBLOCKED), kOrderVMajor j * roi.h + m
 // (CPI_GAMMA_VMAJOR); the B arm follows the context's order, the A arm is always row-major.
 enum { kOrderRowMajor = 0, kOrderUBlocked = 1, kOrderVMajor = 2 };
+// v-major order (CPI_GAMMA_VMAJOR): B rows in blocks of kVMajorBlock (all H_b rows if H_b <= 128):
+// pixel (u, v) -> (v / VB) * (W_b * VB) + u * VB + v % VB, VB = min(H_b, kVMajorBlock).  For one A
+// pixel and one v block, every column u is one contiguous VB-row segment, and consecutive u are
+// adjacent (DRAM pages stay open across consecutive refocus stages).
+constexpr int kVMajorBlock = 128;
+__host__ __device__ inline int vmajor_block(int Hb) { return Hb < kVMajorBlock ? Hb : kVMajorBlock; }
+__host__ __device__ inline int64_t vmajor_slot(int u, int v, int Wb, int Hb) {
+    const int vb = vmajor_block(Hb);
+    return static_cast<int64_t>(v / vb) * Wb * vb + static_cast<int64_t>(u) * vb + v % vb;
+}
 void launch_expand(const uint8_t* frames, int64_t n, int row_bytes, int frame_h, int msb,
                    RoiDev roi, void* op, int64_t ld, int64_t k_pad, int32_t* s, int mode,
                    int order, cudaStream_t st);
@@ -158,6 +168,8 @@ struct S1WArgs {
     const int2* mband;                        // [n_groups][n_vb] union A-row band read by stage 2
     float* T;                                 // plane p at T + p * t_plane: [W_a][H_a][H_b]
     int64_t t_plane;
+    int probe;                                // timing probes (CPI_S1W_PROBE): 1 = no Gamma loads (wrong
+                                              // values), 2 = load both rows of every sample (no reuse)
 };
 bool stage1_w_supported(int Wa, int Hb);
 int stage1_w_xtile();      // outputs x per tile (entry table x padding)

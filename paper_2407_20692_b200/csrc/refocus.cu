@@ -165,9 +165,9 @@ stage1_kernel(const float* __restrict__ gamma, int64_t ldg, int Wa, int Ha, int 
         for (int rr = threadIdx.x; rr < nv * nj; rr += kS1Threads) {
             const int v = rr / nj, jj = rr - v * nj;
             float* dst = sm + (v * nj + jj) * kPad;
-            if (vmajor) {   // B pixel (u, v) at column u * H_b + v (CPI_GAMMA_VMAJOR)
-                const float* col = g_m + static_cast<int64_t>(jlo + jj) * ldg + static_cast<int64_t>(u0) * Hb + v0 + v;
-                for (int k = 0; k < nu; ++k) dst[k] = __ldg(col + static_cast<int64_t>(k) * Hb);
+            if (vmajor) {   // B pixel (u, v) at column vmajor_slot(u, v) (CPI_GAMMA_VMAJOR)
+                const float* row = g_m + static_cast<int64_t>(jlo + jj) * ldg;
+                for (int k = 0; k < nu; ++k) dst[k] = __ldg(row + vmajor_slot(u0 + k, v0 + v, Wb, Hb));
                 continue;
             }
             const float* src = g_m + static_cast<int64_t>(jlo + jj) * ldg + static_cast<int64_t>(v0 + v) * Wb + u0;
@@ -870,9 +870,9 @@ resample_b_kernel(const float* __restrict__ src, float* __restrict__ dst, int Wb
     }
 }
 
-// v-major B order (CPI_GAMMA_VMAJOR, slot q = u * H_b + v): thread = one slot; consecutive threads
-// take consecutive v of one u, so the corner reads (n(v), n(v) + 1 of columns k(u), k(u) + 1) and
-// the stores are coalesced.
+// v-major B order (CPI_GAMMA_VMAJOR, slot q = vmajor_slot(u, v)): thread = one slot; consecutive
+// threads take consecutive v of one u and v block, so the corner reads (rows n(v), n(v) + 1 of
+// columns k(u), k(u) + 1) and the stores are coalesced.
 __global__ void __launch_bounds__(256)
 resample_b_vmajor_kernel(const float* __restrict__ src, float* __restrict__ dst, int Wb, int Hb,
                          const int32_t* __restrict__ bxi, const double* __restrict__ bxt,
@@ -881,14 +881,17 @@ resample_b_vmajor_kernel(const float* __restrict__ src, float* __restrict__ dst,
     const int64_t q = static_cast<int64_t>(blockIdx.y) * 256 + threadIdx.x;
     if (q >= pb) return;
     const int64_t p = blockIdx.x;
-    const int u = static_cast<int>(q / Hb), v = static_cast<int>(q - static_cast<int64_t>(u) * Hb);
+    const int vbs = vmajor_block(Hb);
+    const int64_t blk = q / (static_cast<int64_t>(Wb) * vbs), r = q - blk * Wb * vbs;
+    const int u = static_cast<int>(r / vbs), v = static_cast<int>(blk * vbs + r % vbs);
     const float* s = src + p * pb;
     const int n = __ldg(byi + v), k = __ldg(bxi + u);
     const double tv = __ldg(byt + v), wv = __dadd_rn(1.0, -tv);
     const double tu = __ldg(bxt + u), wu = __dadd_rn(1.0, -tu);
-    const int64_t c0 = static_cast<int64_t>(k) * Hb, c1 = c0 + Hb;
-    const double lo = wu * static_cast<double>(__ldg(s + c0 + n)) + tu * static_cast<double>(__ldg(s + c1 + n));
-    const double hi = wu * static_cast<double>(__ldg(s + c0 + n + 1)) + tu * static_cast<double>(__ldg(s + c1 + n + 1));
+    const double lo = wu * static_cast<double>(__ldg(s + vmajor_slot(k, n, Wb, Hb))) +
+                      tu * static_cast<double>(__ldg(s + vmajor_slot(k + 1, n, Wb, Hb)));
+    const double hi = wu * static_cast<double>(__ldg(s + vmajor_slot(k, n + 1, Wb, Hb))) +
+                      tu * static_cast<double>(__ldg(s + vmajor_slot(k + 1, n + 1, Wb, Hb)));
     __stcs(dst + p * pb + q, static_cast<float>(wv * lo + tv * hi));
 }
 

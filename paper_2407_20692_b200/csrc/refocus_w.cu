@@ -103,6 +103,21 @@ __device__ __forceinline__ void w_lds_if(uint4& g, uint32_t addr, uint32_t flag)
         : "memory");
 }
 
+// 16 bytes of shared memory (generic-pointer-free: the stage address is a shared-window offset)
+__device__ __forceinline__ uint4 w_lds(uint32_t addr) {
+    uint4 g;
+    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w) : "r"(addr) : "memory");
+    return g;
+}
+// part (4 v as two fp32 pairs) += wa * ga + wb * gb, in that order (FFMA2)
+__device__ __forceinline__ void w_taps(uint64_t (&pp)[2], float wa, const uint4& ga, float wb, const uint4& gb) {
+    const uint64_t wa2 = pk2(wa, wa), wb2 = pk2(wb, wb);
+    pp[0] = fma2(wb2, pk2(__uint_as_float(gb.x), __uint_as_float(gb.y)),
+                 fma2(wa2, pk2(__uint_as_float(ga.x), __uint_as_float(ga.y)), pp[0]));
+    pp[1] = fma2(wb2, pk2(__uint_as_float(gb.z), __uint_as_float(gb.w)),
+                 fma2(wa2, pk2(__uint_as_float(ga.z), __uint_as_float(ga.w)), pp[1]));
+}
+
 __device__ __forceinline__ int w_shard_row(const S1WArgs& a, int l) {
     return a.m_base + (l / a.m_block) * a.m_stride + l % a.m_block;
 }
@@ -194,11 +209,11 @@ __device__ __forceinline__ void w_issue(WCursor* cur, int2* tspan, WHeader* hdr,
             const int2 sp = tspan[u];
             hdr[s].tile = c.t;
             hdr[s].flags = (c.started ? 0 : 1) | (last ? 2 : 0);
-            const int nb = (sp.y - sp.x + kWBox) / kWBox;
+            const int nb = a.probe & 1 ? 0 : (sp.y - sp.x + kWBox) / kWBox;
             mbar_expect_tx(&full[s], nb * kWBox * kWRowBytes + kWEBytes);
             uint8_t* dst = smem + s * kWStageBytes;
             for (int b = 0; b < nb; ++b)
-                tma_load_4d(dst + b * kWBox * kWRowBytes, tm_g, &full[s], w.vb * kWV, u, sp.x + b * kWBox, w.ml);
+                tma_load_5d(dst + b * kWBox * kWRowBytes, tm_g, &full[s], 0, u, w.vb, sp.x + b * kWBox, w.ml);
             tma_load_3d(dst + kWGBytes, tm_e, &full[s], 2 * w.xt * kWX, u, w.g * kWF);
             c.u = u + 1;
             c.started = 1;
@@ -311,29 +326,48 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
         const uint8_t* sbase = w_smem + stage * kWStageBytes;
         const uint4* E = reinterpret_cast<const uint4*>(sbase + kWGBytes);
         const uint32_t gaddr = smem_u32(sbase) + lane16;   // this lane's 16 bytes (4 v) of row 0
+        // the warp's two planes walk interleaved (independent load -> FMA chains); entries of planes
+        // past the batch are the TMA's zero fill: zero weights (exact zero taps)
+        const uint4* Ep = E + (kWFW * wp * kWX + wx * kWXW) / 2;
+        if (!(a.probe & 2)) {   // window reuse (rows kept in registers, loads only when they change)
+            uint4 ga[kWFW], gb[kWFW];   // even / odd row of each plane's window
 #pragma unroll
-        for (int pl = 0; pl < kWFW; ++pl) {
-            if (pl < nfw) {
-                const uint4* Ep = E + ((kWFW * wp + pl) * kWX + wx * kWXW) / 2;
-                uint4 ga = make_uint4(0u, 0u, 0u, 0u), gb = ga;   // even / odd row of the window
+            for (int pl = 0; pl < kWFW; ++pl) ga[pl] = gb[pl] = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-                for (int i = 0; i < kWXW; i += 2) {
-                    const uint4 e2 = Ep[i / 2];   // entries of outputs i, i + 1 (broadcast)
+            for (int i = 0; i < kWXW; i += 2) {
+                uint4 e2[kWFW];
 #pragma unroll
-                    for (int k = 0; k < 2; ++k) {
-                        const uint32_t lo = k ? e2.z : e2.x, hi = k ? e2.w : e2.y;
-                        w_lds_if(ga, gaddr + ((hi & 0xFFu) << 9), hi & 0x10000u);
-                        w_lds_if(gb, gaddr + ((hi >> 8 & 0xFFu) << 9), hi & 0x20000u);
+                for (int pl = 0; pl < kWFW; ++pl) e2[pl] = Ep[pl * (kWX / 2) + i / 2];
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+#pragma unroll
+                    for (int pl = 0; pl < kWFW; ++pl) {
+                        const uint32_t lo = k ? e2[pl].z : e2[pl].x, hi = k ? e2[pl].w : e2[pl].y;
+                        w_lds_if(ga[pl], gaddr + ((hi & 0xFFu) << 9), hi & 0x10000u);
+                        w_lds_if(gb[pl], gaddr + ((hi >> 8 & 0xFFu) << 9), hi & 0x20000u);
                         const float wa = __uint_as_float(lo);
                         const float wb = __uint_as_float(hi & kWOne) - wa;
-                        const uint64_t wa2 = pk2(wa, wa), wb2 = pk2(wb, wb);
-                        uint64_t* pp = part[pl][i + k];
-                        pp[0] = fma2(wb2, pk2(__uint_as_float(gb.x), __uint_as_float(gb.y)),
-                                     fma2(wa2, pk2(__uint_as_float(ga.x), __uint_as_float(ga.y)), pp[0]));
-                        pp[1] = fma2(wb2, pk2(__uint_as_float(gb.z), __uint_as_float(gb.w)),
-                                     fma2(wa2, pk2(__uint_as_float(ga.z), __uint_as_float(ga.w)), pp[1]));
+                        w_taps(part[pl][i + k], wa, ga[pl], wb, gb[pl]);
                     }
-                }
+            }
+        } else {   // probe 2: both rows of every sample loaded (no cross-step register dependencies; slower)
+#pragma unroll
+            for (int i = 0; i < kWXW; i += 2) {
+                uint4 e2[kWFW];
+#pragma unroll
+                for (int pl = 0; pl < kWFW; ++pl) e2[pl] = Ep[pl * (kWX / 2) + i / 2];
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+#pragma unroll
+                    for (int pl = 0; pl < kWFW; ++pl) {
+                        const uint32_t lo = k ? e2[pl].z : e2[pl].x, hi = k ? e2[pl].w : e2[pl].y;
+                        // lo = weight of the even row, hi = even / odd row (bits 0-7 / 8-15), 1.0f bits
+                        const uint4 ga = w_lds(gaddr + ((hi & 0xFFu) << 9));
+                        const uint4 gb = w_lds(gaddr + ((hi >> 8 & 0xFFu) << 9));
+                        const float wa = __uint_as_float(lo);
+                        const float wb = __uint_as_float(hi & kWOne) - wa;
+                        w_taps(part[pl][i + k], wa, ga, wb, gb);
+                    }
             }
         }
         // release the slot (generic-proxy reads before the async-proxy refill); the
@@ -510,7 +544,10 @@ int stage1_w_vblock() { return kWV; }
 int stage1_w_group() { return kWF; }
 int stage1_w_jbox() { return kWBox; }
 int stage1_w_max_span() { return kWRows; }
-bool stage1_w_supported(int Wa, int Hb) { return Wa >= 2 && Wa <= 256 && Hb >= 4 && Hb % 4 == 0; }
+// the v-major block must be the kernel's v block (128 rows, or all of H_b <= 128)
+bool stage1_w_supported(int Wa, int Hb) {
+    return Wa >= 2 && Wa <= 256 && Hb >= 4 && Hb % 4 == 0 && (Hb <= kWV || Hb % kWV == 0) && kVMajorBlock == kWV;
+}
 
 cudaError_t launch_pack_w(const int32_t* const* i0s_dev, const double* const* ts_dev, const int32_t* const* ylo_dev,
                           const int32_t* const* yhi_dev, int n_planes, int Wa, int Wb, int Hb, uint32_t* ent,

@@ -55,7 +55,7 @@ ALPHAS = [0.5, 0.61, 0.75, 0.93, 1.0, 1.07, 1.3, 1.52, 1.77, 2.0, -0.6]
 
 
 @pytest.mark.parametrize("dims", [(24, 20, 16, 12), (7, 5, 9, 4), (40, 33, 37, 8), (64, 10, 20, 128),
-                                  (130, 6, 12, 132), (256, 4, 9, 20), (96, 7, 256, 8)])
+                                  (130, 6, 12, 256), (256, 4, 9, 20), (96, 7, 256, 8)])
 @pytest.mark.parametrize("boundary", [0, 1])
 def test_vmajor_refocus_random_gamma(dims, boundary):
     """Random Gamma, 11 planes (two full groups of 4 and a ragged group of 3, one negative
