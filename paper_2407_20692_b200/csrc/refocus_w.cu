@@ -95,19 +95,28 @@ __device__ __forceinline__ uint64_t fma2(uint64_t w, uint64_t g, uint64_t c) {
 
 // g = 16 bytes of shared memory at addr if flag != 0 (a warp-uniform predicate: no wavefront
 // when off), else unchanged
+// No "memory" clobber: the compiler may schedule these loads freely among the stage's other
+// shared loads; they cannot move above the stage's full-barrier wait (their addresses come from
+// entries loaded after it) and w_pin keeps them before the stage release.
 __device__ __forceinline__ void w_lds_if(uint4& g, uint32_t addr, uint32_t flag) {
     asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %4, 0;\n\t"
         "@p ld.shared.v4.u32 {%0, %1, %2, %3}, [%5];\n\t}"
         : "+r"(g.x), "+r"(g.y), "+r"(g.z), "+r"(g.w)
-        : "r"(flag), "r"(addr)
-        : "memory");
+        : "r"(flag), "r"(addr));
 }
 
 // 16 bytes of shared memory (generic-pointer-free: the stage address is a shared-window offset)
 __device__ __forceinline__ uint4 w_lds(uint32_t addr) {
     uint4 g;
-    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w) : "r"(addr) : "memory");
+    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w) : "r"(addr));
     return g;
+}
+// Compiler-level pin: every partial (hence every load feeding it) is computed before this point.
+__device__ __forceinline__ void w_pin(const uint64_t (&part)[kWFW][kWXW][2]) {
+#pragma unroll
+    for (int pl = 0; pl < kWFW; ++pl)
+#pragma unroll
+        for (int i = 0; i < kWXW; ++i) asm volatile("" ::"l"(part[pl][i][0]), "l"(part[pl][i][1]) : "memory");
 }
 // part (4 v as two fp32 pairs) += wa * ga + wb * gb, in that order (FFMA2)
 __device__ __forceinline__ void w_taps(uint64_t (&pp)[2], float wa, const uint4& ga, float wb, const uint4& gb) {
@@ -372,6 +381,7 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
         }
         // release the slot (generic-proxy reads before the async-proxy refill); the
         // last warp to release it issues the refill
+        w_pin(part);
         fence_proxy_async_smem();
         __syncwarp();
         int last_rel = 0;
@@ -419,7 +429,7 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
                     }
                 }
             }
-        } else if (++nst == kWFlush) {
+        } else if (++nst == kWFlush && !(a.probe & 4)) {   // probe 4: no flushes (wrong values)
             w_flush(part, tbase, first);
             first = false;
             nst = 0;
