@@ -64,6 +64,9 @@ def parse():
                         "(parallel.py); auto = tiles when all-gathering the packed frames moves fewer bytes than "
                         "reduce-scattering the int32 partial S_ab (N * 16 KB < 4 P_a P_b), else lib; tiles = "
                         "all-gather of frames + each rank's own Gamma rows (SURVEY §8(e) control)")
+    p.add_argument("--no-fused-reduce", action="store_true",
+                   help="lib mode: reduce-scatter the partial pair sums with NCCL instead of adding them into the "
+                        "owners' shards from the GEMM epilogue (CPI_FUSED_REDUCE, default)")
     p.add_argument("--sharded", action="store_true",
                    help="run the frame-sharded multi-GPU pipeline (NCCL) even at one rank (tests its code path)")
     p.add_argument("--no-e2e", action="store_true")
@@ -378,8 +381,9 @@ def main():
             from paper_2407_20692_b200 import nccl_unique_id
             box = [nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(box, src=0)
+            fused = not args.no_fused_reduce and args.variant != "popc"
             ctx = Context(roi_a, roi_b, n, device=local, variant=args.variant, gamma_order=args.gamma_order,
-                          keep_counts=True, rank=rank, world=world, nccl_id=box[0])
+                          keep_counts=not fused, rank=rank, world=world, nccl_id=box[0], fused_reduce=fused)
             planes = ctx.new_planes(args.planes)
         else:
             # torch.distributed orchestration (parallel.py): rows = GEMM row panels reduce-scattered as
@@ -563,7 +567,10 @@ def main():
                                 f"refocus stack"),
                    "frames_per_step": n_total, "frames_per_step_per_rank": n, "planes_per_step": args.planes,
                    "alphas": "linspace(0.5, 2.0, P)", "variant": args.variant, "gamma_order": args.gamma_order,
-                   "parallelism": (f"frame-sharded x{world} (" + {"lib": "library NCCL reduce-scatter",
+                   "parallelism": (f"frame-sharded x{world} (" + {"lib": "library: GEMM-epilogue reduction into the "
+                                                                          "owners' shards over peer memory"
+                                                                   if not args.no_fused_reduce else
+                                                                   "library NCCL reduce-scatter",
                                                                    "rows": "torch.distributed panelised reduce-scatter",
                                                                    "tiles": "output-tile sharding"}[mode] + ")")
                    if use_dist else "single GPU",

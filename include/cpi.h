@@ -93,6 +93,21 @@ typedef int32_t cpi_status;
                                  multiple of 128; exclusive with CPI_GAMMA_UBLOCKED.  Refocusing spans longer than
                                  the kernel's stage (A-axis map slopes above ~2.2) and W_a > 256 run
                                  a plain staged stage 1 (contiguous row shards only). */
+#define CPI_FUSED_REDUCE 32u /* multi-GPU only: the pair-sum GEMM epilogue adds each
+                                 finished partial tile straight into the shard of the rank that owns
+                                 its A rows (red.global.add.s32 into peer memory mapped with CUDA IPC;
+                                 NVLink between GPUs), instead of writing a full-size local partial
+                                 and reduce-scattering it: no 4 P_a P_b-byte local partial, no
+                                 separate reduction pass, the exchange overlaps the GEMM tile by
+                                 tile.  Exact: integer adds.  CTA-pair tensor-core variants only.
+                                 With nccl_id the library maps the peers itself (handles
+                                 all-gathered over its communicator) and cpi_reset / cpi_finalize
+                                 order the ranks; without nccl_id (external mode) the caller
+                                 exchanges cpi_shard_ipc_handle bytes, calls cpi_open_peer_shards,
+                                 and orders the ranks itself (all shards zeroed by cpi_reset before
+                                 any rank correlates; all correlates done before the shard,
+                                 cpi_counts_dev's s_ab, is read). */
+#define CPI_SHARD_HANDLE_BYTES 64
 
 /* Boundary policy of refocusing. */
 #define CPI_SKIP_RENORMALIZE 0  /* sample counts only if 0 <= c_A <= W-1 on both axes; mean */
@@ -239,7 +254,8 @@ int64_t cpi_row_align(const cpi_ctx *ctx);
 
 /* Borrow the device pointers of the accumulated sums (valid until cpi_destroy; contents
  * change with every correlate / reset): s_ab int32 [P_a][P_b] (NULL without
- * CPI_KEEP_COUNTS), s_a int32 [P_a], s_b int32 [P_b].  Lets a caller run collectives on the
+ * CPI_KEEP_COUNTS; with CPI_FUSED_REDUCE this rank's reduced shard [owned A pixels][P_b], see
+ * cpi_finalize for the row layout), s_a int32 [P_a], s_b int32 [P_b] (this rank's frames).  Lets a caller run collectives on the
  * library's buffers without copies.  Any out pointer may be NULL.  Errors: INVALID_ARG. */
 cpi_status cpi_counts_dev(cpi_ctx *ctx, int32_t **s_ab, int32_t **s_a, int32_t **s_b);
 
@@ -267,6 +283,16 @@ cpi_status cpi_finalize(cpi_ctx *ctx, float *gamma_dev, int64_t *n_tot, int64_t 
  * every row_stride A rows, starting at A row row0 / W_a.  Single GPU: row_block = row_stride = H_a.
  * Either pointer may be NULL.  Errors: INVALID_ARG. */
 cpi_status cpi_shard_layout(const cpi_ctx *ctx, int32_t *row_block, int32_t *row_stride);
+
+/* CPI_FUSED_REDUCE: the CUDA IPC handle (CPI_SHARD_HANDLE_BYTES bytes) of this rank's shard of
+ * the pair sums ([owned A pixels][P_b] int32), for cpi_open_peer_shards on the other ranks.
+ * Errors: INVALID_ARG, STATE (not fused), CUDA. */
+cpi_status cpi_shard_ipc_handle(cpi_ctx *ctx, uint8_t *handle);
+
+/* CPI_FUSED_REDUCE, external mode: map every rank's shard (handles[r * CPI_SHARD_HANDLE_BYTES ..]
+ * from cpi_shard_ipc_handle of rank r; this rank's own entry is ignored) so that the GEMM
+ * epilogue can add into it.  Once per context.  Errors: INVALID_ARG, STATE, CUDA. */
+cpi_status cpi_open_peer_shards(cpi_ctx *ctx, const uint8_t *handles);
 
 /* A new NCCL unique id (CPI_NCCL_ID_BYTES bytes into id) for the cpi_config.nccl_id of a
  * multi-GPU group: call on one rank, share the bytes with the others (any out-of-band channel).

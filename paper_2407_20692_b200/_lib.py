@@ -20,6 +20,8 @@ CPI_LSB_FIRST, CPI_MSB_FIRST = 0, 1
 CPI_HOST, CPI_DEVICE = 0, 1
 CPI_VARIANT_TC, CPI_VARIANT_POPC, CPI_KEEP_COUNTS, CPI_VARIANT_FP4, CPI_GAMMA_UBLOCKED = 0, 1, 2, 4, 8
 CPI_GAMMA_VMAJOR = 16
+CPI_FUSED_REDUCE = 32
+CPI_SHARD_HANDLE_BYTES = 64
 CPI_SKIP_RENORMALIZE, CPI_CLAMP = 0, 1
 KC_GEMM, KC_EXPAND, KC_STAGE1, KC_STAGE2, KC_FINALIZE, KC_COORDS, KC_RESAMPLE = range(7)
 
@@ -28,7 +30,7 @@ EXPORTS = ["cpi_create", "cpi_destroy", "cpi_last_error", "cpi_status_string", "
            "cpi_correlate", "cpi_finalize", "cpi_finalize_counts", "cpi_get_counts", "cpi_reset",
            "cpi_refocus", "cpi_launch_count", "cpi_set_timing", "cpi_kernel_time_ms",
            "cpi_abi_version", "cpi_correlate_rows", "cpi_row_align", "cpi_counts_dev", "cpi_correlate_rows_to",
-           "cpi_shard_layout", "cpi_nccl_unique_id"]
+           "cpi_shard_layout", "cpi_nccl_unique_id", "cpi_shard_ipc_handle", "cpi_open_peer_shards"]
 
 
 class CpiError(RuntimeError):
@@ -93,6 +95,8 @@ def load():
         "cpi_finalize": ([P, P, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64), P], i32),
         "cpi_shard_layout": ([P, ctypes.POINTER(i32), ctypes.POINTER(i32)], i32),
         "cpi_nccl_unique_id": ([P], i32),
+        "cpi_shard_ipc_handle": ([P, P], i32),
+        "cpi_open_peer_shards": ([P, P], i32),
         "cpi_finalize_counts": ([P, P, i64, i64, P, P, i64, P, P], i32),
         "cpi_get_counts": ([P, P, P, P, ctypes.POINTER(i64), P], i32),
         "cpi_reset": ([P, P], i32),

@@ -31,26 +31,31 @@ class Context:
     def __init__(self, roi_a, roi_b, max_frames: int, *, width: int = FRAME_W, height: int = FRAME_H,
                  bit_order: int = _lib.CPI_LSB_FIRST, device: int = 0, variant: str = "tc",
                  keep_counts: bool = False, gamma_blocked: bool = False, gamma_order: Optional[str] = None,
-                 rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None):
+                 rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, fused_reduce: bool = False):
         """rank / world / nccl_id: frame-sharded multi-GPU mode (include/cpi.h cpi_config; world >= 2
         needs keep_counts and the same nccl_unique_id() bytes on every rank; cpi_create is
-        collective)."""
+        collective).  fused_reduce: CPI_FUSED_REDUCE (the GEMM epilogue adds into the owners'
+        shards; without nccl_id the caller maps the peers with open_peer_shards)."""
         self._lib = _lib.load()
         if variant not in ("tc", "popc", "fp4"):
             raise ValueError("variant must be 'tc', 'popc' or 'fp4'")
         flags = {"tc": _lib.CPI_VARIANT_TC, "popc": _lib.CPI_VARIANT_POPC, "fp4": _lib.CPI_VARIANT_FP4}[variant]
         if keep_counts:
             flags |= _lib.CPI_KEEP_COUNTS
+        if fused_reduce:
+            flags |= _lib.CPI_FUSED_REDUCE
         if gamma_order is None:
             gamma_order = "ublocked" if gamma_blocked else "rowmajor"
         if gamma_order not in GAMMA_ORDERS:
             raise ValueError(f"gamma_order must be one of {sorted(GAMMA_ORDERS)}")
         flags |= GAMMA_ORDERS[gamma_order]   # B pixel (Gamma column) order, include/cpi.h
         self._id_buf = None
-        if world > 1 or nccl_id is not None:
-            if nccl_id is None or len(nccl_id) != _lib.CPI_NCCL_ID_BYTES:
-                raise ValueError(f"world > 1 needs nccl_id of {_lib.CPI_NCCL_ID_BYTES} bytes (nccl_unique_id())")
+        if nccl_id is not None:
+            if len(nccl_id) != _lib.CPI_NCCL_ID_BYTES:
+                raise ValueError(f"nccl_id must be {_lib.CPI_NCCL_ID_BYTES} bytes (nccl_unique_id())")
             self._id_buf = ctypes.create_string_buffer(bytes(nccl_id), _lib.CPI_NCCL_ID_BYTES)
+        elif world > 1 and not fused_reduce:
+            raise ValueError("world > 1 needs nccl_id (nccl_unique_id()), or fused_reduce=True (external mode)")
         cfg = _lib.Config(_lib.Layout(width, height, bit_order), _lib.Roi(*roi_a), _lib.Roi(*roi_b),
                           int(max_frames), int(device), flags, int(rank), int(world),
                           ctypes.cast(self._id_buf, ctypes.c_void_p) if self._id_buf is not None else None)
@@ -69,7 +74,8 @@ class Context:
         self.variant = variant
         self.keep_counts = keep_counts
         self.rank, self.world = (int(rank), int(world)) if world > 1 else (0, 1)
-        self.sharded = self._id_buf is not None
+        self.sharded = self._id_buf is not None or (world > 1 and fused_reduce)
+        self.fused_reduce = fused_reduce
         self.shard_rows = (0, self.p_a)    # owned Gamma rows (A pixels) of the last finalize
         self.gamma_order = gamma_order
         self.gamma_blocked = gamma_order == "ublocked"
@@ -182,7 +188,8 @@ class Context:
             t = torch.as_tensor(_Arr(), device=f"cuda:{self.device}")
             assert t.numel() == n and t.data_ptr() == ptr.value
             return t
-        return view(pab, (self.p_a, self.p_b)), view(pa, (self.p_a,)), view(pb, (self.p_b,))
+        rows_ab = self.p_a // self.world if self.fused_reduce else self.p_a   # fused: this rank's shard
+        return view(pab, (rows_ab, self.p_b)), view(pa, (self.p_a,)), view(pb, (self.p_b,))
 
     def finalize(self, gamma=None, stream=None) -> int:
         """cpi_finalize: Gamma from the accumulated sums; returns N_TOT.  Multi-GPU: the cross-rank
@@ -196,6 +203,18 @@ class Context:
         self.shard_rows = (r0.value, rows.value)
         return n.value
 
+    def shard_ipc_handle(self) -> bytes:
+        """cpi_shard_ipc_handle (CPI_FUSED_REDUCE): this rank's shard handle for the other ranks."""
+        buf = ctypes.create_string_buffer(_lib.CPI_SHARD_HANDLE_BYTES)
+        self._check(self._lib.cpi_shard_ipc_handle(self._h, buf))
+        return buf.raw
+
+    def open_peer_shards(self, handles):
+        """cpi_open_peer_shards: handles[r] = shard_ipc_handle() bytes of rank r."""
+        blob = b"".join(bytes(h) for h in handles)
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        self._check(self._lib.cpi_open_peer_shards(self._h, buf))
+
     def shard_layout(self):
         """cpi_shard_layout: (row_block, row_stride) of this rank's block-cyclic A rows."""
         b, st = ctypes.c_int32(0), ctypes.c_int32(0)
@@ -204,9 +223,11 @@ class Context:
 
     def shard_pixel_rows(self):
         """Global A pixel of each local Gamma row owned by this rank (include/cpi.h cpi_finalize)."""
-        row0, rows = self.shard_rows
         block, stride = self.shard_layout()
-        Wa = self.roi_a[2]
+        Wa, Ha = self.roi_a[2], self.roi_a[3]
+        row0, rows = self.shard_rows
+        if self.sharded:   # include/cpi.h cpi_finalize: rank r owns blocks r of every panel
+            row0, rows = self.rank * block * Wa, (Ha // self.world) * Wa
         lr = np.arange(rows // Wa)
         m = row0 // Wa + (lr // block) * stride + lr % block
         return (m[:, None] * Wa + np.arange(Wa)[None, :]).reshape(-1)

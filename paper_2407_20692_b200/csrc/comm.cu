@@ -32,7 +32,8 @@ const NcclApi* nccl_api() {
         if (!h) return;
         g_ok = sym(h, "ncclGetUniqueId", g_api.get_unique_id) && sym(h, "ncclCommInitRank", g_api.comm_init_rank) &&
                sym(h, "ncclCommDestroy", g_api.comm_destroy) && sym(h, "ncclAllReduce", g_api.all_reduce) &&
-               sym(h, "ncclReduceScatter", g_api.reduce_scatter) && sym(h, "ncclGroupStart", g_api.group_start) &&
+               sym(h, "ncclReduceScatter", g_api.reduce_scatter) && sym(h, "ncclAllGather", g_api.all_gather) &&
+               sym(h, "ncclGroupStart", g_api.group_start) &&
                sym(h, "ncclGroupEnd", g_api.group_end) && sym(h, "ncclGetErrorString", g_api.error_string);
     });
     return g_ok ? &g_api : nullptr;

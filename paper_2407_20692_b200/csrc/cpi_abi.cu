@@ -100,7 +100,12 @@ struct cpi_ctx {
     cpi::TElem* w_T = nullptr;             // [batch][W_a][H_a][H_b]
     // frame-sharded multi-GPU mode (cfg.world >= 2): library-owned NCCL communicator and shard plan
     int world = 1, rank = 0;
+    bool sharded = false;                  // multi-GPU mode (shard plan); comm may be null (external mode)
+    bool fused = false;                    // CPI_FUSED_REDUCE: GEMM epilogue reduces into the owners' shards
     ncclComm_t comm = nullptr;
+    int32_t** d_peers = nullptr;           // [world] device pointers of every rank's shard (own: local)
+    std::vector<void*> peer_open;          // IPC-opened peer shard pointers (closed at destroy)
+    bool peers_ready = false;
     int sh_block = 0, sh_panels = 1, sh_m_base = 0, sh_m_count = 0, sh_stride = 0;   // A rows
     int32_t* sh_counts = nullptr;          // [m_count * W_a][P_b] reduced pair sums of the owned rows
     int32_t* sh_marg = nullptr;            // [P_a + P_b + 1] all-reduced S_a | S_b | N
@@ -249,6 +254,9 @@ void free_all(cpi_ctx* c) {
     cudaFree(c->w_i0s); cudaFree(c->w_ts); cudaFree(c->w_ylo); cudaFree(c->w_yhi);
     cudaFree(c->w_ent); cudaFree(c->w_steps); cudaFree(c->w_span); cudaFree(c->w_mband);
     cudaFree(c->w_ypack); cudaFree(c->w_T);
+    for (void* p : c->peer_open) cudaIpcCloseMemHandle(p);
+    c->peer_open.clear();
+    cudaFree(c->d_peers);
     cudaFree(c->sh_counts); cudaFree(c->sh_marg); cudaFree(c->sh_gamma_ws); cudaFree(c->planes64);
     if (c->comm) {
         if (const cpi::NcclApi* api = cpi::nccl_api()) api->comm_destroy(c->comm);
@@ -544,7 +552,8 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
         (cfg->roi_b.height % 4 || (cfg->roi_b.height > cpi::kVMajorBlock && cfg->roi_b.height % cpi::kVMajorBlock)))
         return fail(nullptr, CPI_ERR_UNSUPPORTED, "CPI_GAMMA_VMAJOR needs roi_b.height %% 4 == 0 and, above %d, a "
                                                   "multiple of %d", cpi::kVMajorBlock, cpi::kVMajorBlock);
-    if (cfg->flags & ~(CPI_VARIANT_POPC | CPI_KEEP_COUNTS | CPI_VARIANT_FP4 | CPI_GAMMA_UBLOCKED | CPI_GAMMA_VMAJOR))
+    if (cfg->flags & ~(CPI_VARIANT_POPC | CPI_KEEP_COUNTS | CPI_VARIANT_FP4 | CPI_GAMMA_UBLOCKED | CPI_GAMMA_VMAJOR |
+                       CPI_FUSED_REDUCE))
         return fail(nullptr, CPI_ERR_INVALID_ARG, "unknown flags 0x%x", cfg->flags);
     if ((cfg->flags & CPI_VARIANT_POPC) && (cfg->flags & CPI_VARIANT_FP4))
         return fail(nullptr, CPI_ERR_INVALID_ARG, "CPI_VARIANT_POPC and CPI_VARIANT_FP4 are exclusive");
@@ -554,16 +563,21 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
     // multi-GPU mode: world >= 2, or world == 1 with an nccl_id (the same code path as a one-rank group)
     const int world = cfg->world > 1 ? cfg->world : 1;
     const bool sharded = cfg->world > 1 || (cfg->world == 1 && cfg->nccl_id);
+    const bool fused = (cfg->flags & CPI_FUSED_REDUCE) != 0;
+    if (fused && !sharded) return fail(nullptr, CPI_ERR_INVALID_ARG, "CPI_FUSED_REDUCE needs a multi-GPU config");
+    if (fused && ((cfg->flags & CPI_VARIANT_POPC) || getenv("CPI_GEMM_1CTA")))
+        return fail(nullptr, CPI_ERR_UNSUPPORTED, "CPI_FUSED_REDUCE runs in the CTA-pair tensor-core GEMM epilogue");
     if (sharded) {
         if (cfg->rank < 0 || cfg->rank >= world)
             return fail(nullptr, CPI_ERR_INVALID_ARG, "rank %d outside [0, world = %d)", cfg->rank, world);
-        if (!cfg->nccl_id) return fail(nullptr, CPI_ERR_INVALID_ARG, "multi-GPU config needs nccl_id");
-        if (!(cfg->flags & CPI_KEEP_COUNTS))
+        if (!cfg->nccl_id && !fused)
+            return fail(nullptr, CPI_ERR_INVALID_ARG, "multi-GPU config needs nccl_id (or CPI_FUSED_REDUCE)");
+        if (!(cfg->flags & CPI_KEEP_COUNTS) && !fused)
             return fail(nullptr, CPI_ERR_INVALID_ARG, "multi-GPU config needs CPI_KEEP_COUNTS (partial pair sums)");
         if (cfg->roi_a.height % world)
             return fail(nullptr, CPI_ERR_INVALID_ARG, "H_a = %d must be divisible by world = %d", cfg->roi_a.height,
                         world);
-        if (!cpi::nccl_api()) return fail(nullptr, CPI_ERR_NCCL, "libnccl.so.2 could not be loaded");
+        if (cfg->nccl_id && !cpi::nccl_api()) return fail(nullptr, CPI_ERR_NCCL, "libnccl.so.2 could not be loaded");
     }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -640,6 +654,8 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
         // blocks) holds >= 8192 A pixels, so each reduce-scatter call moves >= 32 KB per B pixel row
         c->world = world;
         c->rank = cfg->rank;
+        c->sharded = true;
+        c->fused = fused;
         const int Wa = cfg->roi_a.width, m_per = cfg->roi_a.height / world;
         int block = m_per;
         for (int b = 1; b <= m_per; ++b)
@@ -651,22 +667,50 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
         c->sh_stride = world * block;
         cudaError_t ea = cudaMalloc(&c->sh_counts, sizeof(int32_t) * size_t(m_per) * Wa * c->p_b);
         if (ea == cudaSuccess) ea = cudaMalloc(&c->sh_marg, sizeof(int32_t) * size_t(c->p_a + c->p_b + 1));
+        if (ea == cudaSuccess) ea = cudaMalloc(&c->d_peers, sizeof(int32_t*) * world);
+        if (ea == cudaSuccess) ea = cudaMemset(c->sh_counts, 0, sizeof(int32_t) * size_t(m_per) * Wa * c->p_b);
         if (ea != cudaSuccess) {
             cpi_status s = cuda_fail(nullptr, ea, "cpi_create shard workspaces");
             free_all(c);
             delete c;
             return s;
         }
-        ncclUniqueId id;
-        static_assert(sizeof(id) == CPI_NCCL_ID_BYTES, "NCCL unique id size");
-        std::memcpy(&id, cfg->nccl_id, sizeof(id));
-        const ncclResult_t r = cpi::nccl_api()->comm_init_rank(&c->comm, world, id, c->rank);
-        if (r != ncclSuccess) {
-            c->comm = nullptr;
-            const cpi_status s = fail(nullptr, CPI_ERR_NCCL, "ncclCommInitRank: %s", cpi::nccl_api()->error_string(r));
-            free_all(c);
-            delete c;
-            return s;
+        if (cfg->nccl_id) {
+            ncclUniqueId id;
+            static_assert(sizeof(id) == CPI_NCCL_ID_BYTES, "NCCL unique id size");
+            std::memcpy(&id, cfg->nccl_id, sizeof(id));
+            const ncclResult_t r = cpi::nccl_api()->comm_init_rank(&c->comm, world, id, c->rank);
+            if (r != ncclSuccess) {
+                c->comm = nullptr;
+                const cpi_status s = fail(nullptr, CPI_ERR_NCCL, "ncclCommInitRank: %s", cpi::nccl_api()->error_string(r));
+                free_all(c);
+                delete c;
+                return s;
+            }
+            if (fused) {   // exchange the shard IPC handles over the communicator and map the peers
+                std::vector<uint8_t> hs(size_t(world) * CPI_SHARD_HANDLE_BYTES);
+                cpi_status s = cpi_shard_ipc_handle(c, hs.data() + size_t(c->rank) * CPI_SHARD_HANDLE_BYTES);
+                uint8_t* d_hs = nullptr;
+                if (s == CPI_OK && cudaMalloc(&d_hs, hs.size()) != cudaSuccess) s = fail(c, CPI_ERR_OOM, "handle buffer");
+                if (s == CPI_OK) {
+                    cudaMemcpy(d_hs + size_t(c->rank) * CPI_SHARD_HANDLE_BYTES, hs.data() + size_t(c->rank) * CPI_SHARD_HANDLE_BYTES,
+                               CPI_SHARD_HANDLE_BYTES, cudaMemcpyHostToDevice);
+                    const ncclResult_t rg = cpi::nccl_api()->all_gather(d_hs + size_t(c->rank) * CPI_SHARD_HANDLE_BYTES, d_hs,
+                                                                        CPI_SHARD_HANDLE_BYTES, ncclUint8, c->comm, nullptr);
+                    if (rg != ncclSuccess || cudaDeviceSynchronize() != cudaSuccess)
+                        s = fail(c, CPI_ERR_NCCL, "shard handle all-gather failed");
+                    else if (cudaMemcpy(hs.data(), d_hs, hs.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+                        s = fail(c, CPI_ERR_CUDA, "shard handle copy failed");
+                }
+                cudaFree(d_hs);
+                if (s == CPI_OK) s = cpi_open_peer_shards(c, hs.data());
+                if (s != CPI_OK) {
+                    g_create_error = c->err;
+                    free_all(c);
+                    delete c;
+                    return s;
+                }
+            }
         }
     }
     c->cfg.nccl_id = nullptr;   // the caller's buffer is not kept
@@ -783,8 +827,14 @@ cpi_status gemm_rows(cpi_ctx* c, int64_t row0, int64_t rows, float* gamma, cudaS
     epi.s_b = c->s_b;
     epi.gamma = gamma;
     epi.ldg = c->p_b;
-    epi.counts = c->keep ? c->counts : nullptr;
+    epi.counts = c->keep && !c->fused ? c->counts : nullptr;
     epi.ldc = c->p_b;
+    if (c->fused) {
+        epi.peers = c->d_peers;
+        epi.world = c->world;
+        epi.chunk_rows = int64_t(c->sh_block) * c->cfg.roi_a.width;
+        epi.panel_rows = epi.chunk_rows * c->world;
+    }
     epi.accumulate = c->accumulate;
     epi.p_a = static_cast<int>(std::min(c->p_a, row0 + rows));
     epi.p_b = static_cast<int>(c->p_b);
@@ -838,12 +888,14 @@ cpi_status cpi_correlate(cpi_ctx* c, float* gamma, void* stream) {
     if (!c) return CPI_ERR_INVALID_ARG;
     if (!c->loaded || c->consumed || c->expanded)
         return fail(c, CPI_ERR_STATE, "cpi_correlate needs a freshly loaded batch (cpi_load_frames)");
-    if (!c->keep && c->batches > 0)
+    if (!c->keep && !c->fused && c->batches > 0)
         return fail(c, CPI_ERR_STATE, "second batch needs CPI_KEEP_COUNTS (or cpi_reset)");
-    if (!c->keep && !gamma)
+    if (!c->keep && !c->fused && !gamma)
         return fail(c, CPI_ERR_STATE, "gamma_dev is NULL and CPI_KEEP_COUNTS is off: pair sums would be lost");
-    if (c->comm && gamma)
+    if (c->sharded && gamma)
         return fail(c, CPI_ERR_STATE, "multi-GPU context: the pair sums are partial; Gamma comes from cpi_finalize");
+    if (c->fused && !c->peers_ready)
+        return fail(c, CPI_ERR_STATE, "CPI_FUSED_REDUCE: the peer shards are not mapped (cpi_open_peer_shards)");
     const int64_t n = c->n_cur;
     if (gamma && c->n_tot + n == 0) return fail(c, CPI_ERR_ZERO_FRAMES, "Gamma needs N_TOT >= 1");
     CK(c, cudaSetDevice(c->dev));
@@ -885,10 +937,11 @@ cpi_status cpi_correlate_rows(cpi_ctx* c, int64_t row0, int64_t rows, float* gam
     if (!c) return CPI_ERR_INVALID_ARG;
     if (!c->loaded || c->consumed)
         return fail(c, CPI_ERR_STATE, "cpi_correlate_rows needs a loaded batch not consumed by cpi_correlate");
-    if (!c->expanded && !c->keep && c->batches > 0)
+    if (!c->expanded && !c->keep && !c->fused && c->batches > 0)
         return fail(c, CPI_ERR_STATE, "second batch needs CPI_KEEP_COUNTS (or cpi_reset)");
-    if (!c->keep && !gamma)
+    if (!c->keep && !c->fused && !gamma)
         return fail(c, CPI_ERR_STATE, "gamma_dev is NULL and CPI_KEEP_COUNTS is off: pair sums would be lost");
+    if (c->fused && gamma) return fail(c, CPI_ERR_STATE, "multi-GPU context: Gamma comes from the finalisation");
     const int64_t align = cpi_row_align(c);
     if (row0 < 0 || rows <= 0 || row0 + rows > c->p_a || row0 % align || (rows % align && row0 + rows != c->p_a))
         return fail(c, CPI_ERR_INVALID_ARG, "rows [%lld, +%lld) must lie in [0, P_a) on multiples of %lld",
@@ -926,7 +979,7 @@ cpi_status cpi_counts_dev(cpi_ctx* c, int32_t** s_ab, int32_t** s_a, int32_t** s
         if (s != CPI_OK) return s;
         CK(c, cudaDeviceSynchronize());
     }
-    if (s_ab) *s_ab = c->keep ? c->counts : nullptr;
+    if (s_ab) *s_ab = c->fused ? c->sh_counts : c->keep ? c->counts : nullptr;   // fused: this rank's shard rows
     if (s_a) *s_a = c->s_a;
     if (s_b) *s_b = c->s_b;
     return CPI_OK;
@@ -957,9 +1010,10 @@ cpi_status finalize_sharded(cpi_ctx* c, float* gamma, int64_t* n_tot, cudaStream
     const int64_t chunk = int64_t(c->sh_block) * Wa, panel = chunk * c->world;
     NK(c, api->group_start());
     NK(c, api->all_reduce(c->sh_marg, c->sh_marg, size_t(c->p_a + c->p_b + 1), ncclInt32, ncclSum, c->comm, st));
-    for (int k = 0; k < c->sh_panels; ++k)
-        NK(c, api->reduce_scatter(c->counts + k * panel * c->p_b, c->sh_counts + k * chunk * c->p_b,
-                                  size_t(chunk * c->p_b), ncclInt32, ncclSum, c->comm, st));
+    if (!c->fused)   // fused: the GEMM epilogues already reduced into the shards (f2)
+        for (int k = 0; k < c->sh_panels; ++k)
+            NK(c, api->reduce_scatter(c->counts + k * panel * c->p_b, c->sh_counts + k * chunk * c->p_b,
+                                      size_t(chunk * c->p_b), ncclInt32, ncclSum, c->comm, st));
     NK(c, api->group_end());
     int32_t n_glob = 0;
     CK(c, cudaMemcpyAsync(&n_glob, c->sh_marg + c->p_a + c->p_b, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -988,7 +1042,10 @@ cpi_status cpi_finalize(cpi_ctx* c, float* gamma, int64_t* n_tot, int64_t* row0,
     if (!c) return CPI_ERR_INVALID_ARG;
     CK(c, cudaSetDevice(c->dev));
     auto st = static_cast<cudaStream_t>(stream);
-    if (c->comm) {
+    if (c->sharded) {
+        if (!c->comm)
+            return fail(c, CPI_ERR_STATE, "external multi-GPU mode (no nccl_id): reduce S_a, S_b, N across ranks and "
+                                          "finalise the shard (cpi_counts_dev) with cpi_finalize_counts");
         cpi_status s = finalize_sharded(c, gamma, n_tot, st);
         if (s != CPI_OK) return s;
         if (row0) *row0 = int64_t(c->sh_m_base) * c->cfg.roi_a.width;
@@ -1016,8 +1073,40 @@ cpi_status cpi_finalize(cpi_ctx* c, float* gamma, int64_t* n_tot, int64_t* row0,
 cpi_status cpi_shard_layout(const cpi_ctx* c, int32_t* row_block, int32_t* row_stride) {
     if (!c) return CPI_ERR_INVALID_ARG;
     const int ha = c->cfg.roi_a.height;
-    if (row_block) *row_block = c->comm ? c->sh_block : ha;
-    if (row_stride) *row_stride = c->comm ? c->sh_stride : ha;
+    if (row_block) *row_block = c->sharded ? c->sh_block : ha;
+    if (row_stride) *row_stride = c->sharded ? c->sh_stride : ha;
+    return CPI_OK;
+}
+
+cpi_status cpi_shard_ipc_handle(cpi_ctx* c, uint8_t* handle) {
+    if (!c || !handle) return CPI_ERR_INVALID_ARG;
+    if (!c->fused) return fail(c, CPI_ERR_STATE, "CPI_FUSED_REDUCE is off");
+    CK(c, cudaSetDevice(c->dev));
+    cudaIpcMemHandle_t h;
+    static_assert(sizeof(h) == CPI_SHARD_HANDLE_BYTES, "IPC handle size");
+    CK(c, cudaIpcGetMemHandle(&h, c->sh_counts));
+    std::memcpy(handle, &h, sizeof(h));
+    return CPI_OK;
+}
+
+cpi_status cpi_open_peer_shards(cpi_ctx* c, const uint8_t* handles) {
+    if (!c || !handles) return CPI_ERR_INVALID_ARG;
+    if (!c->fused) return fail(c, CPI_ERR_STATE, "CPI_FUSED_REDUCE is off");
+    if (c->peers_ready) return fail(c, CPI_ERR_STATE, "peer shards already mapped");
+    CK(c, cudaSetDevice(c->dev));
+    std::vector<int32_t*> ptrs(c->world, nullptr);
+    for (int r = 0; r < c->world; ++r) {
+        if (r == c->rank) { ptrs[r] = c->sh_counts; continue; }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handles + size_t(r) * CPI_SHARD_HANDLE_BYTES, sizeof(h));
+        void* p = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return cuda_fail(c, e, "cudaIpcOpenMemHandle (peer shard)");
+        c->peer_open.push_back(p);
+        ptrs[r] = static_cast<int32_t*>(p);
+    }
+    CK(c, cudaMemcpy(c->d_peers, ptrs.data(), sizeof(int32_t*) * c->world, cudaMemcpyHostToDevice));
+    c->peers_ready = true;
     return CPI_OK;
 }
 
@@ -1072,6 +1161,14 @@ cpi_status cpi_reset(cpi_ctx* c, void* stream) {
     CK(c, cudaMemsetAsync(c->s_a, 0, sizeof(int32_t) * c->p_a, st));
     CK(c, cudaMemsetAsync(c->s_b, 0, sizeof(int32_t) * c->p_b, st));
     c->counts_stale = true;                  // zeroed lazily: the next batch overwrites them
+    if (c->fused) {
+        // every rank's GEMM adds into every shard: all shards must be zero before any rank's next GEMM
+        // (the NCCL barrier below; in external mode the caller synchronises the ranks)
+        CK(c, cudaMemsetAsync(c->sh_counts, 0, sizeof(int32_t) * size_t(c->sh_m_count) * c->cfg.roi_a.width * c->p_b, st));
+        if (c->comm) {
+            NK(c, cpi::nccl_api()->all_reduce(c->sh_marg, c->sh_marg, 1, ncclInt32, ncclSum, c->comm, st));
+        }
+    }
     c->n_tot = 0;
     c->batches = 0;
     c->gemm_batches = 0;
@@ -1085,7 +1182,8 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
     if (!spec_in || !planes) return fail(c, CPI_ERR_INVALID_ARG, "spec and planes_dev must be non-NULL");
     cpi_refocus_spec spec_local = *spec_in;
     const cpi_refocus_spec* spec = &spec_local;
-    if (!spec_local.gamma_dev && c->comm) {
+    if (!spec_local.gamma_dev && c->sharded) {
+        if (!c->comm) return fail(c, CPI_ERR_STATE, "external multi-GPU mode: refocus the shard rows explicitly");
         // this rank's Gamma rows of the last cpi_finalize, then the fp64 plane all-reduce (C3)
         if (!c->sh_gamma_cur) return fail(c, CPI_ERR_STATE, "multi-GPU refocus from the totals needs cpi_finalize first");
         const int Wa = c->cfg.roi_a.width, Ha = c->cfg.roi_a.height;

@@ -195,7 +195,17 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
                     for (int e = 0; e < 32; ++e) r[e] = static_cast<uint32_t>(__float2int_rn(__uint_as_float(r[e])));
                 }
                 const int col0 = tn * BN + 32 * c;
-                if (row_ok && col0 < epi.p_b) {
+                if (epi.peers && row_ok && col0 < epi.p_b) {
+                    // f2: this tile row's partial sums go straight to the owning rank's shard
+                    const int64_t ch = row / epi.chunk_rows;
+                    const int owner = static_cast<int>(ch % epi.world);
+                    const int64_t lrow = (row / epi.panel_rows) * epi.chunk_rows + row % epi.chunk_rows;
+                    int32_t* dp = epi.peers[owner] + lrow * epi.ldc + col0;
+                    const int nc = min(32, epi.p_b - col0);
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (e < nc && r[e] != 0u) atomicAdd(dp + e, static_cast<int>(r[e]));   // RED.ADD (no return)
+                } else if (row_ok && col0 < epi.p_b) {
                     int32_t* cp = epi.counts ? epi.counts + static_cast<int64_t>(row) * epi.ldc + col0 : nullptr;
                     float* gp = epi.gamma ? epi.gamma + static_cast<int64_t>(row) * epi.ldg + col0 : nullptr;
                     const int32_t* sbc = sbs + 32 * c;
@@ -217,6 +227,7 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
         }
+        if (epi.peers) __threadfence_system();   // peer-memory reductions visible beyond this GPU
     }
     __syncwarp();
     tc_fence_before();

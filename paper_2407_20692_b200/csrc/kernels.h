@@ -26,6 +26,14 @@ struct Epilogue {
     double inv_n2;        // 1 / N_TOT^2 (kept for reference; kernels use make_gamma_scale(n))
     int cache;            // bit 0: Gamma stores evict-first (st.global.cs); bit 1: operand loads L2 evict_last
     int m_tile0;          // first M tile of this launch (row panels: cpi_correlate_rows)
+    // fused cross-rank reduction (CPI_FUSED_REDUCE): when peers != nullptr the
+    // epilogue adds each partial pair sum into the shard of the rank that owns its A row (peer
+    // memory, red.global.add.s32) instead of writing local counts: A pixel row is owned by rank
+    // (row / chunk_rows) % world, at local row (row / panel_rows) * chunk_rows + row % chunk_rows
+    // of that rank's shard [rows][ldc].
+    int32_t* const* peers;
+    int world;
+    int64_t chunk_rows, panel_rows;
 };
 
 // KB1: expand one RoI of packed frames into a K-major operand, zero-filling frames [n, k_pad),
@@ -210,6 +218,7 @@ struct NcclApi {
     ncclResult_t (*comm_destroy)(ncclComm_t);
     ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
     ncclResult_t (*reduce_scatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
     ncclResult_t (*group_start)();
     ncclResult_t (*group_end)();
     const char* (*error_string)(ncclResult_t);

@@ -22,8 +22,9 @@ def main():
     dist.broadcast_object_list(box, src=0)
     frames = synth.bernoulli_frames(N, 0.2, seed=101)
     lo, hi = rank * N // world, (rank + 1) * N // world
-    c = Context(ROI_A, ROI_B, N, keep_counts=True, gamma_order="vmajor", device=int(os.environ["LOCAL_RANK"]),
-                rank=rank, world=world, nccl_id=box[0])
+    fused = os.environ.get("CPI_ABI_FUSED", "0") == "1"
+    c = Context(ROI_A, ROI_B, N, keep_counts=not fused, gamma_order="vmajor", device=int(os.environ["LOCAL_RANK"]),
+                rank=rank, world=world, nccl_id=box[0], fused_reduce=fused)
     c.load_frames(np.ascontiguousarray(frames[lo:hi]))
     c.correlate(None)
     rows = c.shard_pixel_rows()

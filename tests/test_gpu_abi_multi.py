@@ -103,13 +103,16 @@ print("ok")
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
                     reason="needs >= 2 GPUs (one rank per GPU)")
-def test_abi_multi_gpu_matches_single_gpu(tmp_path):
+@pytest.mark.parametrize("fused", [False, True])
+def test_abi_multi_gpu_matches_single_gpu(tmp_path, fused):
+    """One rank per GPU: library NCCL reduce-scatter (fused = False) or the GEMM epilogue adding into
+    the owners' shards over NVLink peer memory (CPI_FUSED_REDUCE, f2)."""
     world = min(torch.cuda.device_count(), 8)
     out = tmp_path / "abi_mgpu.npz"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(29800 + os.getpid() % 100),
            os.path.join(HERE, "_abi_mgpu_worker.py"), str(out)]
-    subprocess.run(cmd, check=True, timeout=900)
+    subprocess.run(cmd, check=True, timeout=900, env=dict(os.environ, CPI_ABI_FUSED="1" if fused else "0"))
     got = np.load(out)
     frames = synth.bernoulli_frames(int(got["n"]), 0.2, seed=101)
     _, G, P = _single(frames, "vmajor")
