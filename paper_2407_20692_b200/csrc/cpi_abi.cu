@@ -37,6 +37,7 @@ struct cpi_ctx {
     bool popc = false, keep = false, pair = true;   // pair: cta_group::2 GEMM
     bool fp4 = false;                      // kind::mxf4 GEMM on E2M1 operands (2 frames per byte)
     bool ublocked = false;                 // B pixels in u-blocked order (CPI_GAMMA_UBLOCKED)
+    bool symmetric = false;                // roi_a == roi_b: one operand, SYRK GEMM (upper tiles, mirrored)
     int order = cpi::kOrderRowMajor;       // B pixel order (row-major / u-blocked / v-major)
     int64_t k_align = 128;                 // frames per GEMM K block
     int64_t p_a = 0, p_b = 0;
@@ -232,8 +233,8 @@ void free_all(cpi_ctx* c) {
         if (c->ev_consumed[b]) cudaEventDestroy(c->ev_consumed[b]);
     }
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->op_b != c->op_a) cudaFree(c->op_b);
     cudaFree(c->op_a);
-    cudaFree(c->op_b);
     cudaFree(c->s_a);
     cudaFree(c->s_b);
     cudaFree(c->counts);
@@ -623,6 +624,15 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
         c->ld_op = c->k_cap;        // bytes
     }
     const size_t op_elem = c->popc ? 4 : 1;
+    // roi_a == roi_b (e.g. the whole frame as both arms): S_ab is symmetric, so one
+    // operand serves both arms and the CTA-pair GEMM computes only tiles touching the upper triangle
+    // (SYRK), mirroring them in the epilogue; row-major B order only (the other
+    // orders permute the B index), single GPU only (knob CPI_NO_SYRK=1 turns it off)
+    const cpi_roi& ra_ = cfg->roi_a;
+    const cpi_roi& rb_ = cfg->roi_b;
+    c->symmetric = ra_.x0 == rb_.x0 && ra_.y0 == rb_.y0 && ra_.width == rb_.width && ra_.height == rb_.height &&
+                   c->order == cpi::kOrderRowMajor && !c->popc && c->pair && !(cfg->world > 1 || cfg->nccl_id) &&
+                   getenv("CPI_NO_SYRK") == nullptr;
     cudaError_t e = cudaSuccess;
     auto chk = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
     chk(cudaMalloc(&c->frames_dev[0], size_t(c->frame_bytes) * cfg->max_frames));
@@ -633,12 +643,14 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
         chk(cudaEventCreateWithFlags(&c->ev_consumed[b], cudaEventDisableTiming));
     }
     chk(cudaMalloc(&c->op_a, size_t(c->rows_a) * c->ld_op * op_elem));
-    chk(cudaMalloc(&c->op_b, size_t(c->rows_b) * c->ld_op * op_elem));
+    if (c->symmetric) c->op_b = nullptr;
+    else chk(cudaMalloc(&c->op_b, size_t(c->rows_b) * c->ld_op * op_elem));
     chk(cudaMalloc(&c->s_a, sizeof(int32_t) * c->p_a));
     chk(cudaMalloc(&c->s_b, sizeof(int32_t) * c->p_b));
     if (c->keep) chk(cudaMalloc(&c->counts, sizeof(int32_t) * size_t(c->p_a) * c->p_b));
     if (e == cudaSuccess) chk(cudaMemset(c->op_a, 0, size_t(c->rows_a) * c->ld_op * op_elem));
-    if (e == cudaSuccess) chk(cudaMemset(c->op_b, 0, size_t(c->rows_b) * c->ld_op * op_elem));
+    if (e == cudaSuccess && !c->symmetric) chk(cudaMemset(c->op_b, 0, size_t(c->rows_b) * c->ld_op * op_elem));
+    if (c->symmetric) c->op_b = c->op_a;
     if (e == cudaSuccess) chk(cudaMemset(c->s_a, 0, sizeof(int32_t) * c->p_a));
     if (e == cudaSuccess) chk(cudaMemset(c->s_b, 0, sizeof(int32_t) * c->p_b));
     if (e == cudaSuccess && c->keep) chk(cudaMemset(c->counts, 0, sizeof(int32_t) * size_t(c->p_a) * c->p_b));
@@ -719,7 +731,8 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
         const uint32_t box_b = c->fp4 ? cpi::gemm_f4_box_rows_b() : c->pair ? cpi::gemm_tc2_box_rows()
                                                                             : cpi::gemm_tc_block_n();
         cpi_status s = make_tmap(c, &c->tm_a, c->op_a, c->rows_a, c->ld_op, box_a);
-        if (s == CPI_OK) s = make_tmap(c, &c->tm_b, c->op_b, c->rows_b, c->ld_op, box_b);
+        if (s == CPI_OK)   // symmetric: the B map reads the A operand (rows past it are TMA zero fill)
+            s = make_tmap(c, &c->tm_b, c->op_b, c->symmetric ? c->rows_a : c->rows_b, c->ld_op, box_b);
         if (s != CPI_OK) {
             g_create_error = c->err;
             free_all(c);
@@ -792,9 +805,12 @@ cpi_status expand_batch(cpi_ctx* c, cudaStream_t st) {
     if (n > 0) {
         cpi::launch_expand(c->frames_cur, n, L.width_px / 8, L.height_px, L.bit_order, ra, c->op_a,
                            c->ld_op, k_pad, c->s_a, mode, cpi::kOrderRowMajor, st);
-        cpi::launch_expand(c->frames_cur, n, L.width_px / 8, L.height_px, L.bit_order, rb, c->op_b,
-                           c->ld_op, k_pad, c->s_b, mode, c->order, st);
-        c->launches += 2;
+        if (c->symmetric)   // one operand for both arms; S_b = S_a (running totals)
+            CK(c, cudaMemcpyAsync(c->s_b, c->s_a, sizeof(int32_t) * c->p_a, cudaMemcpyDeviceToDevice, st));
+        else
+            cpi::launch_expand(c->frames_cur, n, L.width_px / 8, L.height_px, L.bit_order, rb, c->op_b,
+                               c->ld_op, k_pad, c->s_b, mode, c->order, st);
+        c->launches += c->symmetric ? 1 : 2;
         CK(c, cudaGetLastError());
     }
     if (c->cur_buf >= 0) {
@@ -829,6 +845,7 @@ cpi_status gemm_rows(cpi_ctx* c, int64_t row0, int64_t rows, float* gamma, cudaS
     epi.ldg = c->p_b;
     epi.counts = c->keep && !c->fused ? c->counts : nullptr;
     epi.ldc = c->p_b;
+    epi.symmetric = c->symmetric && row0 == 0 && rows == c->p_a ? 1 : 0;   // SYRK on full launches only
     if (c->fused) {
         epi.peers = c->d_peers;
         epi.world = c->world;

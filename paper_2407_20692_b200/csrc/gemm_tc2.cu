@@ -51,6 +51,11 @@ __device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int
     tn = r / gm;
 }
 
+// SYRK: a tile with no element on or above the diagonal (every column < every row) is not computed
+__device__ __forceinline__ bool below_diagonal(const Epilogue& epi, int tm, int tn, int bn) {
+    return epi.symmetric && (tn + 1) * bn - 1 < tm * BM;
+}
+
 template <bool kF4>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
@@ -113,6 +118,7 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
                 int tm, tn;
                 tile_coords(t, m_tiles, n_tiles, tm, tn);
                 tm += epi.m_tile0;
+                if (below_diagonal(epi, tm, tn, BN)) continue;
                 for (int kb = 0; kb < k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_expect_tx(&full[stage], 2 * kStageBytes);
@@ -134,9 +140,15 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
-            for (int t = pair; t < num_tiles; t += num_pairs, ++local) {
+            for (int t = pair; t < num_tiles; t += num_pairs) {
+                {
+                    int tm, tn;
+                    tile_coords(t, m_tiles, n_tiles, tm, tn);
+                    if (below_diagonal(epi, tm + epi.m_tile0, tn, BN)) continue;
+                }
                 const int acc = local & 1;
                 const uint32_t acc_phase = (local >> 1) & 1;
+                ++local;
                 mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
@@ -166,12 +178,14 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
         const GammaScale gs = make_gamma_scale(epi.n);
         const uint32_t tempty_leader0 = leader_addr(&tempty[0]), tempty_leader1 = leader_addr(&tempty[1]);
         int local = 0;
-        for (int t = pair; t < num_tiles; t += num_pairs, ++local) {
+        for (int t = pair; t < num_tiles; t += num_pairs) {
             int tm, tn;
             tile_coords(t, m_tiles, n_tiles, tm, tn);
             tm += epi.m_tile0;
+            if (below_diagonal(epi, tm, tn, BN)) continue;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
+            ++local;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             // this tile's S_b slice -> smem once (coalesced), read back as broadcast LDS
@@ -205,6 +219,42 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
 #pragma unroll
                     for (int e = 0; e < 32; ++e)
                         if (e < nc && r[e] != 0u) atomicAdd(dp + e, static_cast<int>(r[e]));   // RED.ADD (no return)
+                } else if (epi.symmetric) {
+                  if (row_ok && col0 < epi.p_b && col0 + 31 >= row) {   // chunks below the diagonal: mirrored elsewhere
+                    // SYRK: element (row, col) for col >= row, mirrored to (col, row) for col > row;
+                    // per column the warp's 32 rows are consecutive, so the mirrored stores coalesce
+                    const int nc = min(32, epi.p_b - col0);
+                    if (col0 > row && epi.vec && nc == 32) {   // whole chunk above the diagonal
+                        int32_t* cp = epi.counts ? epi.counts + static_cast<int64_t>(row) * epi.ldc + col0 : nullptr;
+                        float* gp = epi.gamma ? epi.gamma + static_cast<int64_t>(row) * epi.ldg + col0 : nullptr;
+                        const int32_t* sbc = sbs + 32 * c;
+                        if (gs.small) epilogue_chunk_vec<true>(r, cp, epi.accumulate, gp, sbc, sa, gs);
+                        else epilogue_chunk_vec<false>(r, cp, epi.accumulate, gp, sbc, sa, gs);
+#pragma unroll 4
+                        for (int e = 0; e < 32; ++e) {   // r[] now holds the accumulated sums
+                            const int64_t mi = static_cast<int64_t>(col0 + e);
+                            if (epi.counts) epi.counts[mi * epi.ldc + row] = static_cast<int>(r[e]);
+                            if (epi.gamma) epi.gamma[mi * epi.ldg + row] = gamma_entry(static_cast<int>(r[e]), sa, sbc[e], gs);
+                        }
+                    } else
+#pragma unroll 4
+                    for (int e = 0; e < 32; ++e) {
+                        const int col = col0 + e;
+                        if (e >= nc || col < row) continue;
+                        int v = static_cast<int>(r[e]);
+                        if (epi.counts) {
+                            int32_t* cp = epi.counts + static_cast<int64_t>(row) * epi.ldc + col;
+                            if (epi.accumulate) v += *cp;
+                            *cp = v;
+                            if (col != row) epi.counts[static_cast<int64_t>(col) * epi.ldc + row] = v;
+                        }
+                        if (epi.gamma) {
+                            const float gv = gamma_entry(v, sa, sbs[32 * c + e], gs);
+                            epi.gamma[static_cast<int64_t>(row) * epi.ldg + col] = gv;
+                            if (col != row) epi.gamma[static_cast<int64_t>(col) * epi.ldg + row] = gv;
+                        }
+                    }
+                  }
                 } else if (row_ok && col0 < epi.p_b) {
                     int32_t* cp = epi.counts ? epi.counts + static_cast<int64_t>(row) * epi.ldc + col0 : nullptr;
                     float* gp = epi.gamma ? epi.gamma + static_cast<int64_t>(row) * epi.ldg + col0 : nullptr;

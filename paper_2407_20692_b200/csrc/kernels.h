@@ -34,6 +34,9 @@ struct Epilogue {
     int32_t* const* peers;
     int world;
     int64_t chunk_rows, panel_rows;
+    // symmetric pair sums (SYRK, roi_a == roi_b): tiles entirely below the diagonal
+    // are skipped; a computed element (r, c) with c > r is written at (r, c) and (c, r), c < r not
+    int symmetric;
 };
 
 // KB1: expand one RoI of packed frames into a K-major operand, zero-filling frames [n, k_pad),
