@@ -627,12 +627,14 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
     // roi_a == roi_b (e.g. the whole frame as both arms): S_ab is symmetric, so one
     // operand serves both arms and the CTA-pair GEMM computes only tiles touching the upper triangle
     // (SYRK), mirroring them in the epilogue; row-major B order only (the other
-    // orders permute the B index), single GPU only (knob CPI_NO_SYRK=1 turns it off)
+    // orders permute the B index), single GPU only.  Opt-in (CPI_SYRK=1): measured on the whole
+    // frame (P = 131072, 10^4 frames) the mirrored epilogue stores cost more than the half of the
+    // MMAs they save (GEMM 77.5 ms vs 70.8 ms)
     const cpi_roi& ra_ = cfg->roi_a;
     const cpi_roi& rb_ = cfg->roi_b;
     c->symmetric = ra_.x0 == rb_.x0 && ra_.y0 == rb_.y0 && ra_.width == rb_.width && ra_.height == rb_.height &&
                    c->order == cpi::kOrderRowMajor && !c->popc && c->pair && !(cfg->world > 1 || cfg->nccl_id) &&
-                   getenv("CPI_NO_SYRK") == nullptr;
+                   getenv("CPI_SYRK") != nullptr && atoi(getenv("CPI_SYRK")) != 0;
     cudaError_t e = cudaSuccess;
     auto chk = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
     chk(cudaMalloc(&c->frames_dev[0], size_t(c->frame_bytes) * cfg->max_frames));

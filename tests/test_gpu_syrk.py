@@ -12,6 +12,11 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
+@pytest.fixture(autouse=True)
+def _syrk_on(monkeypatch):
+    monkeypatch.setenv("CPI_SYRK", "1")   # opt-in knob
+
+
 def _run(roi, frames, variant, batches=1, env=None, monkeypatch=None, rows_panels=None):
     from paper_2407_20692_b200 import Context
     if env and monkeypatch:
@@ -56,13 +61,13 @@ def test_syrk_matches_oracle(roi, variant):
 
 
 def test_syrk_equals_full_gemm_and_panels(monkeypatch):
-    """The same context without SYRK (CPI_NO_SYRK=1), and row panels (which run the plain GEMM on the
+    """The same context without SYRK (CPI_SYRK=0), and row panels (which run the plain GEMM on the
     shared operand), give bit-identical counts and Gamma."""
     roi = (0, 0, 48, 32)
     frames = synth.bernoulli_frames(900, 0.3, seed=5)
     a = _run(roi, frames, "fp4")
     b = _run(roi, frames, "fp4", rows_panels=512)
-    c = _run(roi, frames, "fp4", env={"CPI_NO_SYRK": "1"}, monkeypatch=monkeypatch)
+    c = _run(roi, frames, "fp4", env={"CPI_SYRK": "0"}, monkeypatch=monkeypatch)
     for x, y in ((a, b), (a, c)):
         for u, v in zip(x, y):
             np.testing.assert_array_equal(u, v)
