@@ -131,16 +131,18 @@ __device__ __forceinline__ int w_shard_row(const S1WArgs& a, int l) {
     return a.m_base + (l / a.m_block) * a.m_stride + l % a.m_block;
 }
 
-// tile t -> (local A row, v block) outer, (plane group, x tile) inner
+// tile t -> (local A row, v block, x tile) outer, plane group inner: the groups of one (m, v block,
+// x tile) run on neighbouring CTAs at the same time and walk u in near lockstep, so the Gamma rows
+// their spans share are read from L2
 struct WTile { int ml, vb, g, xt; };
 __device__ __forceinline__ WTile w_tile(const S1WArgs& a, int t) {
-    const int inner = a.n_groups * a.n_xt;
-    const int o = t / inner, i = t - o * inner;
+    const int o = t / a.n_groups;
     WTile w;
-    w.ml = o / a.n_vb;
-    w.vb = o - w.ml * a.n_vb;
-    w.g = i / a.n_xt;
-    w.xt = i - w.g * a.n_xt;
+    w.g = t - o * a.n_groups;
+    const int o2 = o / a.n_xt;
+    w.xt = o - o2 * a.n_xt;
+    w.ml = o2 / a.n_vb;
+    w.vb = o2 - w.ml * a.n_vb;
     return w;
 }
 __device__ __forceinline__ bool w_needed(const S1WArgs& a, const WTile& w, int m) {
@@ -319,7 +321,8 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
     int stage = 0;
     uint32_t phase = 0;
     for (;;) {
-        mbar_wait(&full[stage], phase);
+        if (a.probe & 8) mbar_wait_spin(&full[stage], phase);   // probe 8: non-suspending wait
+        else mbar_wait(&full[stage], phase);
         const WHeader h = hdr[stage];
         if (h.tile < 0) break;
         if (h.flags & 1) {   // first stage of a tile
@@ -338,7 +341,8 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
         // the warp's two planes walk interleaved (independent load -> FMA chains); entries of planes
         // past the batch are the TMA's zero fill: zero weights (exact zero taps)
         const uint4* Ep = E + (kWFW * wp * kWX + wx * kWXW) / 2;
-        if (!(a.probe & 2)) {   // window reuse (rows kept in registers, loads only when they change)
+        if (a.probe & 16) {     // probe 16: no step work (ring / barrier / issue cost only)
+        } else if (!(a.probe & 2)) {   // window reuse (rows kept in registers, loads only when they change)
             uint4 ga[kWFW], gb[kWFW];   // even / odd row of each plane's window
 #pragma unroll
             for (int pl = 0; pl < kWFW; ++pl) ga[pl] = gb[pl] = make_uint4(0u, 0u, 0u, 0u);
