@@ -215,6 +215,23 @@ const char *cpi_status_string(cpi_status s);
 cpi_status cpi_load_frames(cpi_ctx *ctx, const void *packed, int64_t n_frames, int32_t where,
                            void *stream);
 
+/* Dataset files ("Input Dataset": sets of headerless .bin files, 8 MiB = 512 frames
+ * each; S:57-64 parse_bin_file, S:91-100 scan_dataset).  Host-only: these two need no device
+ * and no context.  A file is a whole number of packed frames of `layout`
+ * (width_px/8 * height_px bytes each) and nothing else.
+ *   cpi_bin_frames: *n_frames = file size / frame bytes.  Errors: INVALID_ARG (NULL, bad
+ *     layout -> LAYOUT), SIZE_MISMATCH (size not a multiple of the frame bytes), CUDA is
+ *     never returned; an unreadable file is INVALID_ARG with the errno text in
+ *     cpi_last_error(NULL).  An empty file has 0 frames.
+ *   cpi_read_bin: copies frames [frame0, frame0 + n_frames) of the file, bit for bit, into
+ *     the caller's host buffer `dst` (n_frames * frame bytes; pinned memory can then go straight
+ *     to cpi_load_frames).  Errors: INVALID_ARG (NULL, negative range, range past the end of
+ *     the file, read failure), LAYOUT, SIZE_MISMATCH.
+ * Ordering of a dataset's files (SPEC scan_dataset: lexicographic) is the caller's; the Python
+ * binding's scan_dataset sorts names and checks that every file has the same frame count. */
+cpi_status cpi_bin_frames(const char *path, const cpi_layout *layout, int64_t *n_frames);
+cpi_status cpi_read_bin(const char *path, const cpi_layout *layout, int64_t frame0, int64_t n_frames, void *dst);
+
 /* Accumulate the loaded batch into the context's sums (Eq. (1) numerators):
  *   S_a[p] += sum_i A^i_p,  S_b[q] += sum_i B^i_q,  N_TOT += n_frames,
  *   S_ab[p][q] += sum_i A^i_p B^i_q   (int32, exact; N_TOT < 2^31)

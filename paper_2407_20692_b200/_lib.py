@@ -30,7 +30,8 @@ EXPORTS = ["cpi_create", "cpi_destroy", "cpi_last_error", "cpi_status_string", "
            "cpi_correlate", "cpi_finalize", "cpi_finalize_counts", "cpi_get_counts", "cpi_reset",
            "cpi_refocus", "cpi_launch_count", "cpi_set_timing", "cpi_kernel_time_ms",
            "cpi_abi_version", "cpi_correlate_rows", "cpi_row_align", "cpi_counts_dev", "cpi_correlate_rows_to",
-           "cpi_shard_layout", "cpi_nccl_unique_id", "cpi_shard_ipc_handle", "cpi_open_peer_shards"]
+           "cpi_shard_layout", "cpi_nccl_unique_id", "cpi_shard_ipc_handle", "cpi_open_peer_shards",
+           "cpi_bin_frames", "cpi_read_bin"]
 
 
 class CpiError(RuntimeError):
@@ -109,6 +110,8 @@ def load():
         "cpi_correlate_rows_to": ([P, i64, i64, P, P], i32),
         "cpi_row_align": ([P], i64),
         "cpi_counts_dev": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)], i32),
+        "cpi_bin_frames": ([ctypes.c_char_p, ctypes.POINTER(Layout), ctypes.POINTER(i64)], i32),
+        "cpi_read_bin": ([ctypes.c_char_p, ctypes.POINTER(Layout), i64, i64, P], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <cerrno>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -527,6 +528,69 @@ const char* cpi_status_string(cpi_status s) {
 
 const char* cpi_last_error(const cpi_ctx* c) {
     return c ? c->err.c_str() : g_create_error.c_str();
+}
+
+// ---- dataset files (S:57-64 parse_bin_file) -- host only, no context ----------------
+namespace {
+cpi_status bin_open(const char* path, const cpi_layout* L, FILE** f, int64_t* frame_bytes, int64_t* n_frames) {
+    g_create_error.clear();
+    if (!path || !L || !n_frames) return fail(nullptr, CPI_ERR_INVALID_ARG, "path, layout and n_frames must be non-NULL");
+    if (L->width_px <= 0 || L->height_px <= 0 || L->width_px % 8 || L->height_px % 8)
+        return fail(nullptr, CPI_ERR_LAYOUT, "frame %dx%d: width and height must be positive multiples of 8",
+                    L->width_px, L->height_px);
+    *frame_bytes = int64_t(L->width_px / 8) * L->height_px;
+    FILE* fp = fopen(path, "rb");
+    if (!fp) return fail(nullptr, CPI_ERR_INVALID_ARG, "%s: %s", path, strerror(errno));
+    if (fseeko(fp, 0, SEEK_END) != 0) {
+        fclose(fp);
+        return fail(nullptr, CPI_ERR_INVALID_ARG, "%s: %s", path, strerror(errno));
+    }
+    const int64_t size = ftello(fp);
+    if (size < 0) {
+        fclose(fp);
+        return fail(nullptr, CPI_ERR_INVALID_ARG, "%s: %s", path, strerror(errno));
+    }
+    if (size % *frame_bytes) {
+        fclose(fp);
+        return fail(nullptr, CPI_ERR_SIZE_MISMATCH, "%s: %lld bytes is not a whole number of %lld-byte frames", path,
+                    static_cast<long long>(size), static_cast<long long>(*frame_bytes));
+    }
+    *n_frames = size / *frame_bytes;
+    if (f) *f = fp; else fclose(fp);
+    return CPI_OK;
+}
+}  // namespace
+
+cpi_status cpi_bin_frames(const char* path, const cpi_layout* layout, int64_t* n_frames) {
+    int64_t fb = 0;
+    return bin_open(path, layout, nullptr, &fb, n_frames);
+}
+
+cpi_status cpi_read_bin(const char* path, const cpi_layout* layout, int64_t frame0, int64_t n_frames, void* dst) {
+    if (!dst && n_frames > 0) {
+        g_create_error.clear();
+        return fail(nullptr, CPI_ERR_INVALID_ARG, "dst must be non-NULL");
+    }
+    FILE* fp = nullptr;
+    int64_t fb = 0, total = 0;
+    const cpi_status st = bin_open(path, layout, &fp, &fb, &total);
+    if (st != CPI_OK) return st;
+    if (frame0 < 0 || n_frames < 0 || frame0 > total || n_frames > total - frame0) {
+        fclose(fp);
+        return fail(nullptr, CPI_ERR_INVALID_ARG, "%s: frames [%lld, %lld) outside the file's %lld frames", path,
+                    static_cast<long long>(frame0), static_cast<long long>(frame0 + n_frames),
+                    static_cast<long long>(total));
+    }
+    const int64_t bytes = n_frames * fb;
+    if (bytes > 0) {
+        if (fseeko(fp, frame0 * fb, SEEK_SET) != 0 || fread(dst, 1, static_cast<size_t>(bytes), fp) != size_t(bytes)) {
+            const int e = errno;
+            fclose(fp);
+            return fail(nullptr, CPI_ERR_INVALID_ARG, "%s: short read (%s)", path, e ? strerror(e) : "end of file");
+        }
+    }
+    fclose(fp);
+    return CPI_OK;
 }
 
 cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
