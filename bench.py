@@ -39,7 +39,7 @@ import synth  # noqa: E402
 METRIC = "frames/s into Gamma (and % int8 TC peak); refocused planes/s (% HBM BW)"
 # the step's default configuration (tests/test_gpu_fullsize.py runs exactly this against the oracle)
 STEP_VARIANT = "fp4"
-STEP_GAMMA_ORDER = "ublocked"
+STEP_GAMMA_ORDER = "vmajor"
 
 
 def parse():
@@ -88,11 +88,13 @@ def rois(name):
 
 
 def load_traffic():
-    """ncu DRAM bytes per launch of the dominant kernels (profiles/r01_traffic.json)."""
-    try:
-        return json.loads((ROOT / "profiles" / "r01_traffic.json").read_text())
-    except Exception:
-        return {}
+    """ncu DRAM bytes per launch of the dominant kernels (profiles/r02_traffic.json, else r01's)."""
+    for name in ("r02_traffic.json", "r01_traffic.json"):
+        try:
+            return json.loads((ROOT / "profiles" / name).read_text())
+        except Exception:
+            pass
+    return {}
 
 
 def load_peaks():
@@ -516,19 +518,29 @@ def main():
                  "traffic": traffic.get("gemm_i8_tc2_kernel<fp4>" if args.variant == "fp4" else
                                         "gemm_i8_tc2_kernel<i8>", {}).get("bytes_per_launch")
                  if args.variant != "popc" else None,
-                 "traffic_note": "ncu dram read + write bytes per launch (profiles/r01_traffic.json)"}
-    roof_s1 = {"kernel": "refocus_stage1_tma (KB5, 4 planes per pass)", "bound": "alu",
+                 "traffic_note": "ncu dram read + write bytes per launch (profiles/r02_traffic.json)"}
+    fma_peak_gtaps = 148 * 128 * f_clk / 1e9         # 128 fp32 FMA lanes per clock per SM
+    vm = args.gamma_order == "vmajor"
+    s1_key = "stage1_w_kernel" if vm else "stage1_tma_kernel<1,4,1,256>"
+    roof_s1 = {"kernel": ("refocus_stage1_w (KB5w, v-major window stage 1: 8 planes per staged slab, one launch "
+                          "per 64 planes)" if vm else "refocus_stage1_tma (KB5, 4 planes per pass)"),
+               "bound": "alu",
                "achieved": s1_gtaps, "peak": lds_peak_gtaps, "unit": "Gtap/s",
                "frac": s1_gtaps / lds_peak_gtaps if s1_gtaps else None,
-               "peak_note": ("one fp32 tap = one 4-byte shared-memory load (+1 FFMA); peak = 148 SMs x 32 "
-                             "LDS lanes/clk x median SM clock of this run (DESIGN.md §5)"),
+               "peak_note": ("taps per second at one 4-byte shared-memory load per tap (+1 FFMA): 148 SMs x 32 "
+                             "LDS lanes/clk x median SM clock of this run (DESIGN.md §5)" +
+                             ("; KB5w loads alpha/2 bytes per tap (rows reused from registers), so this is the "
+                              "one-load-per-tap design's roof kept across rounds; fma_view is the FP32 FMA-lane "
+                              "roof" if vm else "")),
+               "fma_view": {"peak": fma_peak_gtaps, "frac": s1_gtaps / fma_peak_gtaps if s1_gtaps else None,
+                            "note": "one FFMA lane per tap: 148 SMs x 128 FP32 lanes/clk x median SM clock"},
                "taps_per_step": taps, "ms_per_step": s1_ms / args.steps,
                "hbm_view": {"algorithmic_bytes_per_step": span, "achieved_gbs": s1_gbs, "peak_gbs": hbm,
                             "frac": s1_gbs / hbm if s1_gbs else None,
-                            "note": "per-plane span bytes / time; > 1 possible because 4 planes share one HBM pass"},
-               "traffic": traffic.get("stage1_tma_kernel<1,4,1,256>", {}).get("bytes_per_launch"),
-               "traffic_note": ("ncu dram read + write bytes of one 4-plane launch (profiles/r01_traffic.json); "
-                                "achieved is per step (16 launches)")}
+                            "note": "per-plane span bytes / time; > 1 possible because planes share HBM passes"},
+               "traffic": traffic.get(s1_key, {}).get("bytes_per_launch"),
+               "traffic_note": (f"ncu dram read + write bytes per launch of {s1_key} (profiles/r02_traffic.json); "
+                                + ("one launch per step" if vm else "achieved is per step (16 launches)"))}
     dominant = roof_s1 if (s1_ms > gemm_ms) else roof_gemm
     # north_star's correlation metric is the kind::i8 kernel's fraction of the int8 peak: when
     # the step runs the FP4 GEMM, time the kind::i8 GEMM on the same frames too (after the timed

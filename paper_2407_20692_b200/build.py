@@ -13,7 +13,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libcpi.so"
-SOURCES = ["cpi_abi.cu", "expand.cu", "gemm_tc.cu", "gemm_tc2.cu", "gemm_popc.cu", "refocus.cu", "refocus_w.cu", "comm.cu"]
+SOURCES = ["cpi_abi.cu", "expand.cu", "gemm_tc.cu", "gemm_tc2.cu", "gemm_popc.cu", "refocus.cu", "refocus_w.cu", "refocus_gen.cu", "comm.cu"]
 HEADERS = ["common.cuh", "kernels.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -10,6 +10,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include <cuda.h>
@@ -72,16 +73,19 @@ struct cpi_ctx {
     float* gamma_ws = nullptr;             // library Gamma for cpi_refocus from counts (lazy)
     CUtensorMap tm_a{}, tm_b{};
     // refocus workspaces
-    cpi::AxisTables xs[cpi::kRefocusMaxFuse]{}, ys[cpi::kRefocusMaxFuse]{};
+    static constexpr int kS1Planes = cpi::kRefocusMaxFuse;   // planes per KB5 launch
+    cpi::AxisTables xs[kS1Planes]{}, ys[kS1Planes]{};
+    int n_plane_ws = 0;                    // planes whose xs / ys / T are allocated (grown on demand)
+    cpi::GenTables gen_x{}, gen_y{};       // general maps (d != 0): per-axis supports (lazy)
     cpi::AxisTables bxs{}, bys{};          // fractional-B path: B supports per u / v
     float* bws = nullptr;                  // fractional-B path: Gamma resampled onto the B lattice (lazy)
     size_t bws_bytes = 0;
-    cpi::TElem* T[cpi::kRefocusMaxFuse]{};
+    cpi::TElem* T[kS1Planes]{};
     bool refocus_ready = false;
     int fuse = 4;                          // planes per Gamma pass in the TMA stage 1 (CPI_REFOCUS_FUSE)
-    uint32_t* xpack = nullptr;             // packed x-tables [kRefocusMaxFuse][W_b][W_a]
+    uint32_t* xpack = nullptr;             // packed x-tables [kS1Planes][W_b][W_a]
     uint32_t* ypack = nullptr;             // packed y-tables [kRefocusMaxFuse][H_b][H_a]
-    uint32_t* xblk = nullptr;              // x-block masks [kRefocusMaxFuse][W_b / 8]
+    uint32_t* xblk = nullptr;              // x-block masks [kS1Planes][W_b / 8]
     bool use_s2_staged = false;
     cpi::Stage1Maps s1maps{};
     bool use_s1_tma = false;
@@ -239,13 +243,14 @@ void free_all(cpi_ctx* c) {
     cudaFree(c->s_a);
     cudaFree(c->s_b);
     cudaFree(c->counts);
-    for (int f = 0; f < cpi::kRefocusMaxFuse; ++f) {
+    for (int f = 0; f < cpi_ctx::kS1Planes; ++f) {
         cpi::AxisTables* t2[2] = {&c->xs[f], &c->ys[f]};
         for (auto* t : t2) { cudaFree(t->i0); cudaFree(t->t); cudaFree(t->cnt); cudaFree(t->lo); cudaFree(t->hi); }
         if (f == 0)
             for (auto* t : {&c->bxs, &c->bys}) { cudaFree(t->i0); cudaFree(t->t); cudaFree(t->cnt); cudaFree(t->lo); cudaFree(t->hi); }
         cudaFree(c->T[f]);
     }
+    for (auto* t : {&c->gen_x, &c->gen_y}) { cudaFree(t->a0); cudaFree(t->at); cudaFree(t->b0); cudaFree(t->bt); cudaFree(t->cnt); }
     cudaFree(c->xpack);
     cudaFree(c->ypack);
     cudaFree(c->xblk);
@@ -274,6 +279,19 @@ cpi_status alloc_axis(cpi_ctx* c, cpi::AxisTables& t, int W, int Wb) {
     CK(c, cudaMalloc(&t.cnt, sizeof(int32_t) * W));
     CK(c, cudaMalloc(&t.lo, sizeof(int32_t) * Wb));
     CK(c, cudaMalloc(&t.hi, sizeof(int32_t) * Wb));
+    return CPI_OK;
+}
+
+// Coordinate tables and stage-1 output T of planes [0, n) of a refocus batch (grown on demand:
+// T is W_a H_a H_b fp32 per plane).
+cpi_status ensure_planes(cpi_ctx* c, int n, int Wa, int Ha, int Wb, int Hb) {
+    for (int p = c->n_plane_ws; p < n; ++p) {
+        cpi_status s = alloc_axis(c, c->xs[p], Wa, Wb);
+        if (s == CPI_OK) s = alloc_axis(c, c->ys[p], Ha, Hb);
+        if (s != CPI_OK) return s;
+        CK(c, cudaMalloc(&c->T[p], sizeof(cpi::TElem) * size_t(Wa) * Ha * Hb));
+        c->n_plane_ws = p + 1;
+    }
     return CPI_OK;
 }
 
@@ -309,6 +327,62 @@ int w_max_span(const double (*maps)[6], int n, int Wa, int Wb) {
 // batch the coordinate tables of every plane, one pack_w, one launch of the window stage 1 (KB5w)
 // and the staged stage 2 per group of 4.  Planes of one batch share one Gamma source (the
 // caller's Gamma, or one B-resampled Gamma for a fractional B map).
+// General maps whose B coordinates depend on the output pixel (dx or dy != 0; refocus_gen.cu):
+// per plane, the two axes' support tables, then the two image-sampling stages.
+cpi_status refocus_general(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, cudaStream_t st) {
+    const int Wa = c->cfg.roi_a.width, Ha = c->cfg.roi_a.height;
+    const int Wb = c->cfg.roi_b.width, Hb = c->cfg.roi_b.height;
+    if (c->order != cpi::kOrderRowMajor)
+        return fail(c, CPI_ERR_UNSUPPORTED, "maps with output-dependent B coordinates need the row-major B order");
+    if (!cpi::refocus_gen_supported(Wa, Ha, Wb, Hb))
+        return fail(c, CPI_ERR_UNSUPPORTED, "maps with output-dependent B coordinates need A RoIs of 2..256 px per side "
+                                            "and B RoIs of 2..512");
+    const int m_count = static_cast<int>(spec->rows / Wa);
+    if (spec->row_block > 0 && spec->row_block < m_count)
+        return fail(c, CPI_ERR_UNSUPPORTED, "maps with output-dependent B coordinates need contiguous row shards");
+    if (!c->gen_x.a0) {
+        const int64_t nx = int64_t(Wa) * Wb, ny = int64_t(Ha) * Hb;
+        for (auto [t, n, no] : {std::tuple<cpi::GenTables*, int64_t, int>{&c->gen_x, nx, Wa}, {&c->gen_y, ny, Ha}}) {
+            CK(c, cudaMalloc(&t->a0, sizeof(int32_t) * n));
+            CK(c, cudaMalloc(&t->at, sizeof(float) * n));
+            CK(c, cudaMalloc(&t->b0, sizeof(int32_t) * n));
+            CK(c, cudaMalloc(&t->bt, sizeof(float) * n));
+            CK(c, cudaMalloc(&t->cnt, sizeof(int32_t) * no));
+        }
+    }
+    cpi_status s = ensure_planes(c, 1, Wa, Ha, Wb, Hb);
+    if (s != CPI_OK) return s;
+    const int m_base = static_cast<int>(spec->row0 / Wa);
+    for (int p = 0; p < spec->n_planes; ++p) {
+        double mp[12];
+        if (spec->affine) {
+            for (int i = 0; i < 12; ++i) mp[i] = spec->affine[12 * p + i];
+        } else {
+            const double al = spec->alphas[p];
+            const double d[12] = {al, 1.0 - al, 0.0, 0.0, 1.0, 0.0, al, 1.0 - al, 0.0, 0.0, 1.0, 0.0};
+            for (int i = 0; i < 12; ++i) mp[i] = d[i];
+        }
+        {
+            TimedScope ts(c, KC_COORDS, st);
+            cudaError_t e = cpi::launch_gen_axis(cpi::GenMap{mp[0], mp[1], mp[2], mp[3], mp[4], mp[5]}, Wa, Wb,
+                                                 spec->boundary, c->gen_x, st);
+            if (e == cudaSuccess)
+                e = cpi::launch_gen_axis(cpi::GenMap{mp[6], mp[7], mp[8], mp[9], mp[10], mp[11]}, Ha, Hb,
+                                         spec->boundary, c->gen_y, st);
+            c->launches += 2;
+            if (e != cudaSuccess) return cuda_fail(c, e, "general-map tables launch");
+        }
+        {
+            TimedScope ts(c, KC_STAGE1, st);
+            cudaError_t e = cpi::launch_refocus_gen(spec->gamma_dev, c->p_b, Wa, Ha, Wb, Hb, m_base, m_count, c->gen_x,
+                                                    c->gen_y, c->T[0], planes + int64_t(p) * Ha * Wa, st);
+            c->launches += 2 + (m_count < Ha ? 1 : 0);
+            if (e != cudaSuccess) return cuda_fail(c, e, "general-map refocus launch");
+        }
+    }
+    return CPI_OK;
+}
+
 cpi_status refocus_vmajor(cpi_ctx* c, const cpi_refocus_spec* spec, float* planes, cudaStream_t st, bool resample) {
     const int Wa = c->cfg.roi_a.width, Ha = c->cfg.roi_a.height;
     const int Wb = c->cfg.roi_b.width, Hb = c->cfg.roi_b.height;
@@ -1312,14 +1386,13 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
     if (spec->boundary != CPI_SKIP_RENORMALIZE && spec->boundary != CPI_CLAMP)
         return fail(c, CPI_ERR_INVALID_ARG, "unknown boundary policy %d", spec->boundary);
     bool genb = false;   // some plane has fractional B coordinates -> general-B kernels
+    bool gen_xy = false; // some plane's B coordinates depend on the output pixel (dx, dy != 0)
     if (spec->affine) {
         for (int p = 0; p < spec->n_planes; ++p) {
             const double* mp = spec->affine + 12 * p;
             for (int i = 0; i < 12; ++i)
                 if (!std::isfinite(mp[i])) return fail(c, CPI_ERR_INVALID_ARG, "affine[%d][%d] is not finite", p, i);
-            if (mp[3] != 0.0 || mp[9] != 0.0)
-                return fail(c, CPI_ERR_UNSUPPORTED, "affine[%d]: B coordinates depending on x / y (dx, dy != 0) "
-                                                    "are not supported on the GPU", p);
+            if (mp[3] != 0.0 || mp[9] != 0.0) gen_xy = true;
             if (mp[4] != 1.0 || mp[5] != 0.0 || mp[10] != 1.0 || mp[11] != 0.0) genb = true;
         }
     } else {
@@ -1337,28 +1410,23 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
                     (long long)spec->row0, (long long)spec->rows);
     CK(c, cudaSetDevice(c->dev));
     auto st = static_cast<cudaStream_t>(stream);
+    if (gen_xy) return refocus_general(c, spec, planes, st);
     if (!c->refocus_ready && c->order != cpi::kOrderVMajor) {
         c->use_s1_tma = cpi::stage1_tma_supported(Wa, Wb, Hb) && getenv("CPI_STAGE1_SIMPLE") == nullptr;
         if (const char* ev = getenv("CPI_REFOCUS_FUSE")) c->fuse = atoi(ev);
         if (c->fuse < 1) c->fuse = 1;
         if (c->fuse > cpi::kRefocusMaxFuse) c->fuse = cpi::kRefocusMaxFuse;
         c->use_s2_staged = cpi::stage2_staged_supported(Ha) && getenv("CPI_STAGE2_SIMPLE") == nullptr;
-        const int nbuf = c->use_s1_tma ? c->fuse : 1;
         if (c->use_s2_staged)
             CK(c, cudaMalloc(&c->ypack, sizeof(uint32_t) * size_t(Ha) * Hb * cpi::kRefocusMaxFuse));
-        for (int f = 0; f < nbuf; ++f) {
-            cpi_status s = alloc_axis(c, c->xs[f], Wa, Wb);
-            if (s == CPI_OK) s = alloc_axis(c, c->ys[f], Ha, Hb);
-            if (s != CPI_OK) return s;
-            CK(c, cudaMalloc(&c->T[f], sizeof(cpi::TElem) * size_t(Wa) * Ha * Hb));
-        }
         if (c->use_s1_tma) {
-            CK(c, cudaMalloc(&c->xpack, sizeof(uint32_t) * size_t(Wa) * Wb * cpi::kRefocusMaxFuse));
-            CK(c, cudaMemset(c->xpack, 0, sizeof(uint32_t) * size_t(Wa) * Wb * cpi::kRefocusMaxFuse));
-            CK(c, cudaMalloc(&c->xblk, sizeof(uint32_t) * size_t((Wb + 7) / 8) * cpi::kRefocusMaxFuse));
+            constexpr int kP = cpi_ctx::kS1Planes;
+            CK(c, cudaMalloc(&c->xpack, sizeof(uint32_t) * size_t(Wa) * Wb * kP));
+            CK(c, cudaMemset(c->xpack, 0, sizeof(uint32_t) * size_t(Wa) * Wb * kP));
+            CK(c, cudaMalloc(&c->xblk, sizeof(uint32_t) * size_t((Wb + 7) / 8) * kP));
             cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
             if (!enc) return fail(c, CPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
-            const cuuint64_t dims[3] = {cuuint64_t(Wa), cuuint64_t(Wb), cuuint64_t(cpi::kRefocusMaxFuse)};
+            const cuuint64_t dims[3] = {cuuint64_t(Wa), cuuint64_t(Wb), cuuint64_t(kP)};
             const cuuint64_t strides[2] = {cuuint64_t(Wa) * 4, cuuint64_t(Wa) * Wb * 4};
             const cuuint32_t box[3] = {cuuint32_t(Wa), 8u, 1u};
             const cuuint32_t es[3] = {1u, 1u, 1u};
@@ -1478,45 +1546,53 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
                                                         "need contiguous row shards");
     }
     const int group = tma_now ? c->fuse : 1;
+    // one fused group per KB5 launch (16 groups per launch in slab-major tile order, sharing each
+    // Gamma slab through L2, measured 80 vs 76 ms: DESIGN §17)
+    const int batch_cap = group;
+    const int64_t nch = (Wb + 7) / 8;
     int resampled = -1;   // plane whose B map the workspace currently holds
     for (int p0 = 0; p0 < spec->n_planes;) {
-        // a fused group: consecutive planes sharing one Gamma source (one B map when resampling)
-        int nf = 1;
-        while (nf < group && p0 + nf < spec->n_planes && (!resample || same_b(p0, p0 + nf))) ++nf;
+        int nb = 1;
+        while (nb < batch_cap && p0 + nb < spec->n_planes && (!resample || same_b(p0, p0 + nb))) ++nb;
+        {
+            cpi_status s = ensure_planes(c, nb, Wa, Ha, Wb, Hb);
+            if (s != CPI_OK) return s;
+        }
         const bool from_ws = resample && frac_b(p0);
         const float* gsrc = from_ws ? c->bws : spec->gamma_dev;
         {
             TimedScope ts(c, KC_COORDS, st);
             cudaError_t e = cudaSuccess;
-            cpi::CoordsGroupArgs cg{};
-            cg.Wa = Wa; cg.Ha = Ha; cg.Wb = Wb; cg.Hb = Hb; cg.boundary = spec->boundary;
-            for (int f = 0; f < nf; ++f) {   // (a, b, c) of the A-axis maps of plane p0 + f
-                if (spec->affine) {
-                    const double* mp = spec->affine + 12 * (p0 + f);
-                    const double m6[6] = {mp[0], mp[1], mp[2], mp[6], mp[7], mp[8]};
-                    for (int i = 0; i < 6; ++i) cg.map[f][i] = m6[i];
-                } else {
-                    const double alpha = spec->alphas[p0 + f];
-                    cg.map[f][0] = cg.map[f][3] = alpha;
-                    cg.map[f][1] = cg.map[f][4] = 1.0 - alpha;
-                    cg.map[f][2] = cg.map[f][5] = 0.0;
+            for (int g0 = 0; g0 < nb && e == cudaSuccess; g0 += group) {
+                const int nf = std::min(group, nb - g0);
+                cpi::CoordsGroupArgs cg{};
+                cg.Wa = Wa; cg.Ha = Ha; cg.Wb = Wb; cg.Hb = Hb; cg.boundary = spec->boundary;
+                for (int f = 0; f < nf; ++f) {   // (a, b, c) of the A-axis maps of plane p0 + g0 + f
+                    const int p = p0 + g0 + f;
+                    if (spec->affine) {
+                        const double* mp = spec->affine + 12 * p;
+                        const double m6[6] = {mp[0], mp[1], mp[2], mp[6], mp[7], mp[8]};
+                        for (int i = 0; i < 6; ++i) cg.map[f][i] = m6[i];
+                    } else {
+                        const double alpha = spec->alphas[p];
+                        cg.map[f][0] = cg.map[f][3] = alpha;
+                        cg.map[f][1] = cg.map[f][4] = 1.0 - alpha;
+                        cg.map[f][2] = cg.map[f][5] = 0.0;
+                    }
+                    cg.xs[f] = c->xs[g0 + f];
+                    cg.ys[f] = c->ys[g0 + f];
+                    bkey(p, cg.bmap[f]);
+                    cg.bx[f] = c->bxs;   // one B map per batch: every f writes the same supports
+                    cg.by[f] = c->bys;
                 }
-                cg.xs[f] = c->xs[f];
-                cg.ys[f] = c->ys[f];
-                bkey(p0 + f, cg.bmap[f]);
-                cg.bx[f] = c->bxs;   // one B map per group: every f writes the same supports
-                cg.by[f] = c->bys;
-            }
-            cg.genb = direct || from_ws ? 1 : 0;   // B supports for the direct kernels / the resample
-            e = cpi::launch_refocus_coords_group(cg, nf, st);
-            c->launches += 2;
-            if (e == cudaSuccess && tma_now) {
-                e = cpi::launch_pack_xtable_group(c->xs, nf, Wa, Wb, c->xpack, c->xblk, st);
-                c->launches += 1;
-            }
-            if (e == cudaSuccess && c->use_s2_staged) {
-                e = cpi::launch_pack_ytable_group(c->ys, nf, Ha, Hb, c->ypack, st);
-                c->launches += 1;
+                cg.genb = direct || from_ws ? 1 : 0;   // B supports for the direct kernels / the resample
+                e = cpi::launch_refocus_coords_group(cg, nf, st);
+                c->launches += 2;
+                if (e == cudaSuccess && tma_now) {
+                    e = cpi::launch_pack_xtable_group(c->xs + g0, nf, Wa, Wb, c->xpack + int64_t(g0) * Wa * Wb,
+                                                      c->xblk + g0 * nch, st);
+                    c->launches += 1;
+                }
             }
             if (e != cudaSuccess) return cuda_fail(c, e, "refocus coords launch");
         }
@@ -1534,45 +1610,54 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
         }
         {
             TimedScope ts(c, KC_STAGE1, st);
-            cudaError_t e;
-            if (direct)
+            cudaError_t e = cudaSuccess;
+            if (direct) {
                 e = cpi::launch_refocus_stage1_genb(spec->gamma_dev, c->p_b, Wa, Ha, Wb, Hb, m_base, m_count, c->xs[0],
                                                     c->bxs, c->T[0], st);
-            else if (tma_now)
-                e = cpi::launch_refocus_stage1_tma(&c->s1maps, nf, Wa, Ha, Wb, Hb, m_base, m_count, m_block, m_stride,
+                c->launches += 1;
+            } else if (tma_now) {
+                e = cpi::launch_refocus_stage1_tma(&c->s1maps, nb, Wa, Ha, Wb, Hb, m_base, m_count, m_block, m_stride,
                                                    c->xs, c->ys, c->T, c->xblk, c->num_sms, st);
-            else if (!cyclic)
-                e = cpi::launch_refocus_stage1(gsrc, c->p_b, Wa, Ha, Wb, Hb, m_base, m_count,
-                                               c->xs[0], c->ys[0], c->T[0], st);
-            else
+                c->launches += 1;
+            } else if (!cyclic) {
+                e = cpi::launch_refocus_stage1(gsrc, c->p_b, Wa, Ha, Wb, Hb, m_base, m_count, c->xs[0], c->ys[0],
+                                               c->T[0], st);
+                c->launches += 1;
+            } else {
                 return fail(c, CPI_ERR_UNSUPPORTED, "block-cyclic shards need the TMA stage 1 (W_a <= 256, W_b %% 4 == 0, "
                                                     "16-byte aligned Gamma)");
-            c->launches += 1;
+            }
             if (e != cudaSuccess) return cuda_fail(c, e, "refocus stage-1 launch");
         }
         {
             TimedScope ts(c, KC_STAGE2, st);
             cudaError_t e = cudaSuccess;
-            if (direct) {
-                e = cpi::launch_refocus_stage2_genb(c->T[0], Wa, Ha, Hb, m_base, m_count, c->xs[0], c->ys[0], c->bys,
-                                                    planes + int64_t(p0) * Ha * Wa, st);
-                c->launches += 1;
-            } else if (c->use_s2_staged) {
-                e = cpi::launch_refocus_stage2_group(c->T, nf, Wa, Ha, Hb, m_base, m_count, m_block, m_stride, c->xs,
-                                                     c->ys, c->ypack, planes + int64_t(p0) * Ha * Wa, st);
-                c->launches += 1;
-            } else if (cyclic) {
-                return fail(c, CPI_ERR_UNSUPPORTED, "block-cyclic shards need H_a <= 256");
-            } else {
-                for (int f = 0; f < nf && e == cudaSuccess; ++f) {
-                    e = cpi::launch_refocus_stage2(c->T[f], Wa, Ha, Hb, m_base, m_count, c->xs[f], c->ys[f],
-                                                   planes + int64_t(p0 + f) * Ha * Wa, st);
+            for (int g0 = 0; g0 < nb && e == cudaSuccess; g0 += group) {
+                const int nf = std::min(group, nb - g0);
+                float* pl = planes + int64_t(p0 + g0) * Ha * Wa;
+                if (direct) {
+                    e = cpi::launch_refocus_stage2_genb(c->T[0], Wa, Ha, Hb, m_base, m_count, c->xs[0], c->ys[0], c->bys,
+                                                        pl, st);
                     c->launches += 1;
+                } else if (c->use_s2_staged) {
+                    e = cpi::launch_pack_ytable_group(c->ys + g0, nf, Ha, Hb, c->ypack, st);
+                    if (e == cudaSuccess)
+                        e = cpi::launch_refocus_stage2_group(c->T + g0, nf, Wa, Ha, Hb, m_base, m_count, m_block,
+                                                             m_stride, c->xs + g0, c->ys + g0, c->ypack, pl, st);
+                    c->launches += 2;
+                } else if (cyclic) {
+                    return fail(c, CPI_ERR_UNSUPPORTED, "block-cyclic shards need H_a <= 256");
+                } else {
+                    for (int f = 0; f < nf && e == cudaSuccess; ++f) {
+                        e = cpi::launch_refocus_stage2(c->T[g0 + f], Wa, Ha, Hb, m_base, m_count, c->xs[g0 + f],
+                                                       c->ys[g0 + f], pl + int64_t(f) * Ha * Wa, st);
+                        c->launches += 1;
+                    }
                 }
             }
             if (e != cudaSuccess) return cuda_fail(c, e, "refocus stage-2 launch");
         }
-        p0 += nf;
+        p0 += nb;
     }
     return CPI_OK;
 }

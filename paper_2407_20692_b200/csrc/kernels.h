@@ -164,6 +164,22 @@ struct PackGroupArgs {
 };
 cudaError_t launch_pack_xtable_group(const AxisTables* xs, int n_fuse, int Wa, int Wb, uint32_t* xpack,
                                      uint32_t* xblk, cudaStream_t st);
+// General maps with output-dependent B coordinates (refocus_gen.cu, SPEC.md:273 with d != 0):
+// per-axis tables [n_out][n_samp] of both supports, then two image-sampling stages.
+struct GenMap { double a, b, c, d, e, f; };   // c_A = a (o - c) + b (s - c') + c ..., c_B = d (o - c) + e (s - c') + f ...
+struct GenTables {
+    int32_t* a0;   // A-lattice support (-1: sample skipped)
+    float* at;
+    int32_t* b0;   // B-lattice support
+    float* bt;
+    int32_t* cnt;  // [n_out] used samples
+};
+bool refocus_gen_supported(int Wa, int Ha, int Wb, int Hb);
+cudaError_t launch_gen_axis(const GenMap& mp, int WA, int WB, int boundary, const GenTables& tab, cudaStream_t st);
+// one plane: T (W_a H_a H_b fp32 workspace) from Gamma rows [m_base, m_base + m_count) (row-major B
+// order, gamma points at the shard's first row), then the plane [H_a][W_a]
+cudaError_t launch_refocus_gen(const float* gamma, int64_t pb, int Wa, int Ha, int Wb, int Hb, int m_base, int m_count,
+                               const GenTables& xt, const GenTables& yt, TElem* T, float* plane, cudaStream_t st);
 // KB5w (refocus_w.cu): stage 1 with window reuse along x, for Gamma in the v-major B order
 // (CPI_GAMMA_VMAJOR).  One launch refocuses a batch of n_planes planes (groups of 4 share each
 // staged slab); fp64 accumulators in TMEM.  Tensor maps: Gamma 4D (v, u, j, local m) with box

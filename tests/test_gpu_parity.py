@@ -302,6 +302,23 @@ def test_refocus_fused_plane_groups(fuse, monkeypatch):
     _assert_planes(R, G, dims, alphas)
 
 
+@pytest.mark.parametrize("fuse,n_planes", [(4, 70), (3, 50), (1, 9)])
+def test_refocus_many_planes_fused_groups(fuse, n_planes, monkeypatch):
+    """Long stacks in fused groups of F planes (ragged last group): every plane matches the
+    oracle and equals the same plane refocused alone, bit for bit (a plane's taps, their order
+    and its fp32 / fp64 sums do not depend on the planes it shares a pass over Gamma with)."""
+    monkeypatch.setenv("CPI_REFOCUS_FUSE", str(fuse))
+    dims = (48, 20, 32, 16)
+    Wa, Ha, Wb, Hb = dims
+    G = synth.random_gamma(Wa * Ha, Wb * Hb, seed=70 + fuse)
+    alphas = list(np.linspace(0.5, 2.0, n_planes))
+    R = _refocus_gpu(G, dims, alphas)
+    _assert_planes(R, G, dims, alphas)
+    monkeypatch.setenv("CPI_REFOCUS_FUSE", "1")
+    for p in (0, n_planes // 2, n_planes - 1):
+        np.testing.assert_array_equal(_refocus_gpu(G, dims, [alphas[p]])[0], R[p])
+
+
 @pytest.mark.parametrize("knobs", [{"CPI_STAGE1_SIMPLE": "1"}, {"CPI_STAGE2_SIMPLE": "1"},
                                    {"CPI_STAGE1_SIMPLE": "1", "CPI_STAGE2_SIMPLE": "1"}, {"CPI_S1_NOSKIP": "1"},
                                    {"CPI_S1_L2PROMO": "0"}, {"CPI_S1_L2PROMO": "128"}, {"CPI_REFOCUS_FUSE": "3"}])
@@ -481,9 +498,45 @@ def test_refocus_affine_maps(boundary):
     ctx.refocus(None, g, p2, boundary=boundary, affine=[oracle.default_map(a) for a in al])
     torch.cuda.synchronize()
     np.testing.assert_array_equal(p2.cpu().numpy(), p1.cpu().numpy())
-    from paper_2407_20692_b200 import CpiError
-    with pytest.raises(CpiError, match="UNSUPPORTED"):      # B coordinate depending on x
-        ctx.refocus(None, g, p1, affine=[[1.0, 0.0, 0.0, 0.1, 1.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0, 0.0]])
+
+
+@pytest.mark.parametrize("boundary", [0, 1])
+@pytest.mark.parametrize("dims", [(24, 20, 16, 12), (40, 12, 170, 9), (9, 33, 6, 200)])
+def test_refocus_output_dependent_b(boundary, dims):
+    """General maps whose B coordinates depend on the output pixel (dx, dy != 0, all
+    twelve coefficients free) through refocus_gen.cu vs the oracle's 16-corner refocus, incl.
+    B RoIs wider than one shared-memory column window (170, 200 > 160) and mixed stacks (a
+    default-map plane evaluated by the same route); row shards; the u-blocked order refuses."""
+    Wa, Ha, Wb, Hb = dims
+    G = synth.random_gamma(Wa * Ha, Wb * Hb, seed=sum(dims))
+    maps = [[1.0, 0.0, 0.0, 0.1, 1.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0, 0.0],
+            [0.7, 0.3, 0.25, -0.2, 0.9, 0.4, 1.3, -0.3, -0.4, 0.35, 1.1, -0.6],
+            [1.6, -0.45, -1.5, 0.5, 0.5, 0.0, 0.55, 0.5, 2.0, -0.5, 0.75, 1.5],
+            oracle.default_map(1.2),
+            [-0.8, 1.2, 3.0, 1.0, 0.0, 0.0, 2.0, -1.0, 0.5, 0.05, 1.0, 0.0]]
+    ctx = _ctx((0, 0, Wa, Ha), (0, 0, Wb, Hb), 1)
+    g = torch.from_numpy(np.ascontiguousarray(G, dtype=np.float32)).cuda()
+    planes = ctx.new_planes(len(maps))
+    ctx.refocus(None, g, planes, boundary=boundary, affine=maps)
+    torch.cuda.synchronize()
+    R = planes.cpu().numpy().astype(np.float64)
+    Ro = oracle.refocus_affine(G, dims, maps, boundary=boundary)
+    M = oracle.refocus_affine(np.abs(G.astype(np.float64)), dims, maps, boundary=boundary)
+    assert np.all(np.abs(R - Ro) <= 1e-6 * M + 1e-30), np.max(np.abs(R - Ro) / np.maximum(M, 1e-300))
+    # contiguous row shards sum to the whole
+    r1 = Ha // 3
+    parts = np.zeros_like(R)
+    for a, b in [(0, r1), (r1, Ha)]:
+        pp = ctx.new_planes(len(maps))
+        ctx.refocus(None, g[a * Wa:], pp, row0=a * Wa, rows=(b - a) * Wa, boundary=boundary, affine=maps)
+        torch.cuda.synchronize()
+        parts += pp.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(parts - Ro) <= 1e-6 * M + 1e-30)   # M is additive over row shards
+    if Wb % 8 == 0:
+        from paper_2407_20692_b200 import CpiError
+        ub = _ctx((0, 0, Wa, Ha), (0, 0, Wb, Hb), 1, gamma_order="ublocked")
+        with pytest.raises(CpiError, match="UNSUPPORTED"):
+            ub.refocus(None, g, planes, affine=maps)
 
 
 @pytest.mark.parametrize("boundary", [0, 1])
