@@ -196,9 +196,8 @@ struct S1WArgs {
     float* T;                                 // plane p at T + p * t_plane: [W_a][H_a][H_b]
     int64_t t_plane;
     int probe;                                // timing probes (CPI_S1W_PROBE; 1/4/16 give wrong
-                                              // values): 1 = no Gamma loads, 2 = load both rows of every
-                                              // sample (no reuse), 4 = no fp64 flushes, 8 = non-suspending
-                                              // barrier waits, 16 = no step work
+                                              // values): 1 = no Gamma loads, 4 = no fp64 flushes,
+                                              // 8 = non-suspending barrier waits, 16 = no step work
 };
 bool stage1_w_supported(int Wa, int Hb);
 int stage1_w_xtile();      // outputs x per tile (entry table x padding)

@@ -4,13 +4,14 @@
 //   T_p[x][m][v] = sum_u [(1 - t(x,u)) Gamma(m, j0(x,u); v, u) + t(x,u) Gamma(m, j0(x,u) + 1; v, u)]
 //
 // The TMA stage 1 of refocus.cu gives every lane its own (x, v) samples, so every tap costs one
-// 4-byte shared-memory load and the shared-memory pipe bounds it.  Here all 32 lanes
-// of a warp work on the SAME (plane, x, u) sample and on 128 different B rows v (four per lane),
-// so the support (j0, t) is warp-uniform, and a warp walks 8 consecutive outputs x for one u: the
-// lower tap row of output x + 1 is j0(x) + d with d = 0 or 1 for alpha <= 1 (1 or 2 for
-// 1 < alpha <= 2), so the two rows (j0, j0 + 1) of consecutive outputs overlap and stay in
-// registers.  A warp-step is 128 v x 2 corners = 256 taps for d loads of 512 B (16 B per lane,
-// conflict-free), i.e. alpha / 2 shared-memory bytes per tap instead of 4 on average.  Skipped
+// 4-byte shared-memory load and the shared-memory pipe bounds it.  Here the 16
+// lanes of a half-warp work on the SAME (plane, x, u) sample and on 128 different B rows v (eight
+// per lane), so the support (j0, t) is uniform across the half (one entry decode per 8 v), and a
+// warp walks 8 consecutive outputs x for one u (its two halves: two planes): the lower tap row of
+// output x + 1 is j0(x) + d with d = 0 or 1 for alpha <= 1 (1 or 2 for 1 < alpha <= 2), so the
+// two rows (j0, j0 + 1) of consecutive outputs overlap and stay in registers.  A half-step is
+// 128 v x 2 corners = 256 taps for d loads of 512 B (two 16-B loads per lane, each half reading
+// 256 contiguous bytes: conflict-free), i.e. alpha / 2 shared-memory bytes per tap instead of 4.  Skipped
 // samples and outputs outside the RoI add exact zeros without loads.
 //
 // The per-step logic is precomputed (pack_w_steps_kernel): a 64-bit step entry per (plane, u, x)
@@ -107,12 +108,6 @@ __device__ __forceinline__ void w_lds_if(uint4& g, uint32_t addr, uint32_t flag)
         : "r"(flag), "r"(addr));
 }
 
-// 16 bytes of shared memory (generic-pointer-free: the stage address is a shared-window offset)
-__device__ __forceinline__ uint4 w_lds(uint32_t addr) {
-    uint4 g;
-    asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w) : "r"(addr));
-    return g;
-}
 // Compiler-level pin: every partial (hence every load feeding it) is computed before this point.
 __device__ __forceinline__ void w_pin(const uint64_t (&part)[kWFW][kWXW][2]) {
 #pragma unroll
@@ -239,9 +234,9 @@ __device__ __forceinline__ bool w_issue(WCursor* cur, int2* tspan, WHeader* hdr,
     }
 }
 
-// fp64 accumulators of a warp in TMEM: plane pl (of the warp's 2), output i, v slot k (of the
-// lane's 4) at columns 64 pl + 8 i + 2 k (+1: high word).  r holds columns [32 half, +32) of one
-// plane (outputs 4 half .. 4 half + 3); adds the fp32 partials (r ignored when first).
+// fp64 accumulators of a lane in TMEM: v half h (of the lane's two 4-v groups), output i, v slot
+// k at columns 64 h + 8 i + 2 k (+1: high word).  r holds columns [32 half, +32) of one v half
+// (outputs 4 half .. 4 half + 3); adds the fp32 partials (r ignored when first).
 __device__ __forceinline__ void w_combine(const uint64_t (&pp)[kWXW][2], uint32_t (&r)[32], int half, bool first) {
 #pragma unroll
     for (int ii = 0; ii < 4; ++ii) {
@@ -325,10 +320,11 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
     const uint32_t tmem = *tslot;
 
     // warp: planes 2 (warp / 4) + {0, 1} of the group, outputs x = x tile + 8 (warp % 4) + i;
-    // lane: B rows v = v block + 4 lane + {0..3}
-    const int wp = warp >> 2, wx = warp & 3;
+    // lane: plane 2 (warp / 4) + lane / 16, B rows v = v block + 64 h + 4 (lane % 16) + {0..3} for
+    // h = 0, 1 (each 16-lane half reads 256 contiguous bytes of a row per load: conflict-free)
+    const int wp = warp >> 2, wx = warp & 3, lpl = lane >> 4;
     const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + static_cast<uint32_t>(warp >> 2) * 128u;
-    const uint32_t lane16 = 16u * lane;
+    const uint32_t lane16 = 16u * (lane & 15);
     uint64_t part[kWFW][kWXW][2];
     bool first = true;   // no fp64 partial in TMEM yet for this tile
     int nst = 0, nfw = 0;
@@ -351,50 +347,31 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
         }
         const uint8_t* sbase = w_smem + stage * kWStageBytes;
         const uint4* E = reinterpret_cast<const uint4*>(sbase + kWGBytes);
-        const uint32_t gaddr = smem_u32(sbase) + lane16;   // this lane's 16 bytes (4 v) of row 0
-        // the warp's two planes walk interleaved (independent load -> FMA chains); entries of planes
-        // past the batch are the TMA's zero fill: zero weights (exact zero taps)
-        const uint4* Ep = E + (kWFW * wp * kWX + wx * kWXW) / 2;
+        const uint32_t gaddr = smem_u32(sbase) + lane16;   // this lane's 16 bytes (4 v) of row 0, half 0
+        // each 16-lane half walks its own plane; entries of planes past the batch are the TMA's zero
+        // fill: zero weights (exact zero taps)
+        const uint4* Ep = E + (kWFW * wp * kWX + wx * kWXW) / 2 + lpl * (kWX / 2);
         if (a.probe & 16) {     // probe 16: no step work (ring / barrier / issue cost only)
-        } else if (!(a.probe & 2)) {   // window reuse (rows kept in registers, loads only when they change)
-            uint4 ga[kWFW], gb[kWFW];   // even / odd row of each plane's window
-#pragma unroll
-            for (int pl = 0; pl < kWFW; ++pl) ga[pl] = gb[pl] = make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-            for (int i = 0; i < kWXW; i += 2) {
-                uint4 e2[kWFW];
-#pragma unroll
-                for (int pl = 0; pl < kWFW; ++pl) e2[pl] = Ep[pl * (kWX / 2) + i / 2];
-#pragma unroll
-                for (int k = 0; k < 2; ++k)
-#pragma unroll
-                    for (int pl = 0; pl < kWFW; ++pl) {
-                        const uint32_t lo = k ? e2[pl].z : e2[pl].x, hi = k ? e2[pl].w : e2[pl].y;
-                        w_lds_if(ga[pl], gaddr + ((hi & 0xFFu) << 9), hi & 0x10000u);
-                        w_lds_if(gb[pl], gaddr + ((hi >> 8 & 0xFFu) << 9), hi & 0x20000u);
-                        const float wa = __uint_as_float(lo);
-                        const float wb = __uint_as_float(hi & kWOne) - wa;
-                        w_taps(part[pl][i + k], wa, ga[pl], wb, gb[pl]);
-                    }
-            }
-        } else {   // probe 2: both rows of every sample loaded (no cross-step register dependencies; slower)
+        } else {   // window reuse (rows kept in registers, loads only when they change)
+            uint4 ga[2], gb[2];   // even / odd row of the window, v halves h = 0, 1
+            ga[0] = ga[1] = gb[0] = gb[1] = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
             for (int i = 0; i < kWXW; i += 2) {
-                uint4 e2[kWFW];
+                const uint4 e2 = Ep[i / 2];
 #pragma unroll
-                for (int pl = 0; pl < kWFW; ++pl) e2[pl] = Ep[pl * (kWX / 2) + i / 2];
-#pragma unroll
-                for (int k = 0; k < 2; ++k)
-#pragma unroll
-                    for (int pl = 0; pl < kWFW; ++pl) {
-                        const uint32_t lo = k ? e2[pl].z : e2[pl].x, hi = k ? e2[pl].w : e2[pl].y;
-                        // lo = weight of the even row, hi = even / odd row (bits 0-7 / 8-15), 1.0f bits
-                        const uint4 ga = w_lds(gaddr + ((hi & 0xFFu) << 9));
-                        const uint4 gb = w_lds(gaddr + ((hi >> 8 & 0xFFu) << 9));
-                        const float wa = __uint_as_float(lo);
-                        const float wb = __uint_as_float(hi & kWOne) - wa;
-                        w_taps(part[pl][i + k], wa, ga, wb, gb);
-                    }
+                for (int k = 0; k < 2; ++k) {
+                    // lo = weight of the even row, hi = even / odd row (bits 0-7 / 8-15), load flags, 1.0f bits
+                    const uint32_t lo = k ? e2.z : e2.x, hi = k ? e2.w : e2.y;
+                    const uint32_t ra = gaddr + ((hi & 0xFFu) << 9), rb = gaddr + ((hi >> 8 & 0xFFu) << 9);
+                    w_lds_if(ga[0], ra, hi & 0x10000u);
+                    w_lds_if(ga[1], ra + 256u, hi & 0x10000u);
+                    w_lds_if(gb[0], rb, hi & 0x20000u);
+                    w_lds_if(gb[1], rb + 256u, hi & 0x20000u);
+                    const float wa = __uint_as_float(lo);
+                    const float wb = __uint_as_float(hi & kWOne) - wa;
+                    w_taps(part[0][i + k], wa, ga[0], wb, gb[0]);
+                    w_taps(part[1][i + k], wa, ga[1], wb, gb[1]);
+                }
             }
         }
         // release the slot to the producer (generic-proxy reads before the async-proxy refill,
@@ -407,32 +384,31 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
         if (h.flags & 2) {   // last stage of the tile: fp64 sum (TMEM + partial) -> fp32 T
             const WTile w = w_tile(a, h.tile);
             const int m = w_shard_row(a, w.ml);
-            const int v = w.vb * kWV + 4 * lane;
             const int x0 = w.xt * kWX + wx * kWXW;
+            const bool lane_ok = lpl < nfw;   // this lane's plane is in the batch
+            float* Tf = a.T + static_cast<int64_t>(w.g * kWF + kWFW * wp + (lane_ok ? lpl : 0)) * a.t_plane;
 #pragma unroll
-            for (int pl = 0; pl < kWFW; ++pl) {
-                if (pl < nfw) {
-                    float* Tf = a.T + static_cast<int64_t>(w.g * kWF + kWFW * wp + pl) * a.t_plane;
+            for (int hv = 0; hv < 2; ++hv) {   // v half (the accumulators' first index)
+                const int v = w.vb * kWV + 64 * hv + 4 * (lane & 15);
 #pragma unroll
-                    for (int half = 0; half < 2; ++half) {
-                        uint32_t r[32];
-                        if (!first) {
-                            tmem_ld_32x32b_x32(tbase + 64 * pl + 32 * half, r);
-                            tmem_wait_ld();
-                        }
-                        w_combine(part[pl], r, half, first);
+                for (int half = 0; half < 2; ++half) {   // outputs 4 half .. 4 half + 3
+                    uint32_t r[32];
+                    if (!first) {   // warp-collective TMEM load (every lane, valid plane or not)
+                        tmem_ld_32x32b_x32(tbase + 64 * hv + 32 * half, r);
+                        tmem_wait_ld();
+                    }
+                    w_combine(part[hv], r, half, first);
 #pragma unroll
-                        for (int ii = 0; ii < 4; ++ii) {
-                            const int x = x0 + 4 * half + ii;
-                            float o[4];
+                    for (int ii = 0; ii < 4; ++ii) {
+                        const int x = x0 + 4 * half + ii;
+                        float o[4];
 #pragma unroll
-                            for (int k = 0; k < 4; ++k)
-                                o[k] = static_cast<float>(__hiloint2double(static_cast<int>(r[8 * ii + 2 * k + 1]),
-                                                                           static_cast<int>(r[8 * ii + 2 * k])));
-                            if (x < a.Wa && v < a.Hb)
-                                *reinterpret_cast<float4*>(Tf + (static_cast<int64_t>(x) * a.Ha + m) * a.Hb + v) =
-                                    make_float4(o[0], o[1], o[2], o[3]);
-                        }
+                        for (int k = 0; k < 4; ++k)
+                            o[k] = static_cast<float>(__hiloint2double(static_cast<int>(r[8 * ii + 2 * k + 1]),
+                                                                       static_cast<int>(r[8 * ii + 2 * k])));
+                        if (lane_ok && x < a.Wa && v < a.Hb)
+                            *reinterpret_cast<float4*>(Tf + (static_cast<int64_t>(x) * a.Ha + m) * a.Hb + v) =
+                                make_float4(o[0], o[1], o[2], o[3]);
                     }
                 }
             }
