@@ -51,12 +51,17 @@ __device__ __forceinline__ void tile_coords(int t, int m_tiles, int n_tiles, int
     tn = r / gm;
 }
 
+// Epilogue modes, compiled separately so the plain kernel carries none of the others' code:
+// plain (counts / fused Gamma), f2 peer reduction (epi.peers), SYRK (epi.symmetric).
+enum EpiMode { kEpiPlain = 0, kEpiPeers = 1, kEpiSyrk = 2 };
+
 // SYRK: a tile with no element on or above the diagonal (every column < every row) is not computed
-__device__ __forceinline__ bool below_diagonal(const Epilogue& epi, int tm, int tn, int bn) {
-    return epi.symmetric && (tn + 1) * bn - 1 < tm * BM;
+template <int kMode>
+__device__ __forceinline__ bool below_diagonal(int tm, int tn, int bn) {
+    return kMode == kEpiSyrk && (tn + 1) * bn - 1 < tm * BM;
 }
 
-template <bool kF4>
+template <bool kF4, int kMode>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                    int m_tiles, int n_tiles, int k_blocks, Epilogue epi) {
@@ -118,7 +123,7 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
                 int tm, tn;
                 tile_coords(t, m_tiles, n_tiles, tm, tn);
                 tm += epi.m_tile0;
-                if (below_diagonal(epi, tm, tn, BN)) continue;
+                if (below_diagonal<kMode>(tm, tn, BN)) continue;
                 for (int kb = 0; kb < k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_expect_tx(&full[stage], 2 * kStageBytes);
@@ -144,7 +149,7 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
                 {
                     int tm, tn;
                     tile_coords(t, m_tiles, n_tiles, tm, tn);
-                    if (below_diagonal(epi, tm + epi.m_tile0, tn, BN)) continue;
+                    if (below_diagonal<kMode>(tm + epi.m_tile0, tn, BN)) continue;
                 }
                 const int acc = local & 1;
                 const uint32_t acc_phase = (local >> 1) & 1;
@@ -182,7 +187,7 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
             int tm, tn;
             tile_coords(t, m_tiles, n_tiles, tm, tn);
             tm += epi.m_tile0;
-            if (below_diagonal(epi, tm, tn, BN)) continue;
+            if (below_diagonal<kMode>(tm, tn, BN)) continue;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             ++local;
@@ -209,7 +214,8 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
                     for (int e = 0; e < 32; ++e) r[e] = static_cast<uint32_t>(__float2int_rn(__uint_as_float(r[e])));
                 }
                 const int col0 = tn * BN + 32 * c;
-                if (epi.peers && row_ok && col0 < epi.p_b) {
+                if (kMode == kEpiPeers) {
+                  if (row_ok && col0 < epi.p_b) {
                     // f2: this tile row's partial sums go straight to the owning rank's shard
                     const int64_t ch = row / epi.chunk_rows;
                     const int owner = static_cast<int>(ch % epi.world);
@@ -219,7 +225,8 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
 #pragma unroll
                     for (int e = 0; e < 32; ++e)
                         if (e < nc && r[e] != 0u) atomicAdd(dp + e, static_cast<int>(r[e]));   // RED.ADD (no return)
-                } else if (epi.symmetric) {
+                  }
+                } else if (kMode == kEpiSyrk) {
                   if (row_ok && col0 < epi.p_b && col0 + 31 >= row) {   // chunks below the diagonal: mirrored elsewhere
                     // SYRK: element (row, col) for col >= row, mirrored to (col, row) for col > row;
                     // per column the warp's 32 rows are consecutive, so the mirrored stores coalesce
@@ -277,7 +284,7 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
         }
-        if (epi.peers) __threadfence_system();   // peer-memory reductions visible beyond this GPU
+        if (kMode == kEpiPeers) __threadfence_system();   // peer-memory reductions visible beyond this GPU
     }
     __syncwarp();
     tc_fence_before();
@@ -296,19 +303,27 @@ int gemm_tc2_box_rows() { return Tc2<false>::HM; }
 int gemm_f4_block_n() { return Tc2<true>::BN; }
 int gemm_f4_box_rows_b() { return Tc2<true>::HN; }
 
-template <bool kF4>
-static cudaError_t launch_tc2(const CUtensorMap* tma_a, const CUtensorMap* tma_b, int m_tiles, int n_tiles,
-                              int k_blocks, const Epilogue& epi, int num_sms, cudaStream_t st) {
+template <bool kF4, int kMode>
+static cudaError_t launch_tc2_mode(const CUtensorMap* tma_a, const CUtensorMap* tma_b, int m_tiles, int n_tiles,
+                                   int k_blocks, const Epilogue& epi, int num_sms, cudaStream_t st) {
     // the attribute is per device: set it before every launch (a host-side call, negligible)
-    cudaError_t e = cudaFuncSetAttribute(gemm_i8_tc2_kernel<kF4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(gemm_i8_tc2_kernel<kF4, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Tc2<kF4>::kSmemBytes);
     if (e != cudaSuccess) return e;
     const int tiles = m_tiles * n_tiles;
     int pairs = num_sms / 2;
     if (tiles < pairs) pairs = tiles;
-    gemm_i8_tc2_kernel<kF4><<<2 * pairs, kThreads, Tc2<kF4>::kSmemBytes, st>>>(*tma_a, *tma_b, m_tiles, n_tiles,
-                                                                             k_blocks, epi);
+    gemm_i8_tc2_kernel<kF4, kMode><<<2 * pairs, kThreads, Tc2<kF4>::kSmemBytes, st>>>(*tma_a, *tma_b, m_tiles,
+                                                                                    n_tiles, k_blocks, epi);
     return cudaGetLastError();
+}
+template <bool kF4>
+static cudaError_t launch_tc2(const CUtensorMap* tma_a, const CUtensorMap* tma_b, int m_tiles, int n_tiles,
+                              int k_blocks, const Epilogue& epi, int num_sms, cudaStream_t st) {
+    if (epi.peers) return launch_tc2_mode<kF4, kEpiPeers>(tma_a, tma_b, m_tiles, n_tiles, k_blocks, epi, num_sms, st);
+    if (epi.symmetric)
+        return launch_tc2_mode<kF4, kEpiSyrk>(tma_a, tma_b, m_tiles, n_tiles, k_blocks, epi, num_sms, st);
+    return launch_tc2_mode<kF4, kEpiPlain>(tma_a, tma_b, m_tiles, n_tiles, k_blocks, epi, num_sms, st);
 }
 
 cudaError_t launch_gemm_tc2(const CUtensorMap* tma_a, const CUtensorMap* tma_b, int m_tiles,
