@@ -58,11 +58,11 @@ constexpr int kWEBytes = kWF * kWX * 8;            // 2 KB of step entries per s
 constexpr int kWStageBytes = kWGBytes + kWEBytes;
 constexpr int kWOffBar = kWStages * kWStageBytes;              // full barriers, then empty barriers
 constexpr int kWOffHdr = kWOffBar + 2 * kWStages * 8;           // stage headers (16 B each)
-constexpr int kWOffCur = kWOffHdr + kWStages * 16;              // issue cursor (16 B)
-constexpr int kWOffTmem = kWOffCur + 16;                        // TMEM base slot
+constexpr int kWOffTmem = kWOffHdr + kWStages * 16;             // TMEM base slot
 constexpr int kWMaxWb = 512;                                    // B columns (tile span row copy)
 constexpr int kWOffSpan = (kWOffTmem + 16 + 15) / 16 * 16;      // the issuing cursor's tile span row
-constexpr int kWSmem = kWOffSpan + kWMaxWb * 8;
+constexpr int kWOffUList = kWOffSpan + kWMaxWb * 8;                // the tile's used u, in order
+constexpr int kWSmem = kWOffUList + kWMaxWb * 4;
 constexpr uint32_t kWInvalid = 0xFFFFFFFFu;        // 32-bit (j0 | t) table: skipped sample / padding x
 // 64-bit step entry of (plane, u, x) for a warp walking its 8 outputs x in order.  The warp keeps
 // two row registers, slot A for the even and slot B for the odd stage row of the pair (j0, j0 + 1):
@@ -155,82 +155,70 @@ __device__ __forceinline__ bool w_needed(const S1WArgs& a, const WTile& w, int m
 // version had no producer warp: the last warp to release a slot issued its refill, and that warp,
 // late by the issue, tended to be the last releaser again, serialising issue and compute: 90.6 ms
 // vs 66.9 ms with the producer warp.)
-struct WCursor {   // the next (tile, u) stage to load (shared memory, producer warp only)
-    int t, u;
-    int started;   // the current tile has issued a stage
-    int loaded;    // the current tile's span row is in the shared-memory copy
-};
 struct WHeader {
     int tile;    // -1: no more stages
     int flags;   // bit 0: first stage of the tile, bit 1: last stage of the tile
     int pad[2];
 };
 
-// First u >= u0 of the cursor tile with a non-empty span (-1: none); warp-collective (ballots
-// over 32 columns of the shared-memory span row).
-__device__ __forceinline__ int w_next_u(const int2* tspan, int Wb, int u0, int lane) {
-    for (int base = u0; base < Wb; base += 32) {
-        const int u = base + lane;
-        bool ne = false;
-        if (u < Wb) {
-            const int2 sp = tspan[u];
-            ne = sp.y >= sp.x;
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, ne);
-        if (m) return base + __ffs(m) - 1;
-    }
-    return -1;
-}
-
-// Issue the next stage into ring slot s; warp-collective (the producer warp); true: end marker issued.
-// When the cursor moves to a new tile the warp copies that tile's span row into shared memory
-// (one coalesced pass), so an issue costs shared-memory scans and lane 0's TMA instructions.
-__device__ __forceinline__ bool w_issue(WCursor* cur, int2* tspan, WHeader* hdr, int s, const S1WArgs& a,
-                                        int n_tiles, const CUtensorMap* tm_g, const CUtensorMap* tm_e,
-                                        uint8_t* smem, uint64_t* full, int lane) {
-    WCursor c = *cur;
-    for (;;) {
-        if (c.t >= n_tiles) {
-            if (lane == 0) {
-                hdr[s].tile = -1;
-                hdr[s].flags = 0;
-                *cur = c;
-                mbar_arrive(&full[s]);   // release: consumers see the end marker
-            }
-            __syncwarp();
-            return true;
-        }
-        const WTile w = w_tile(a, c.t);
-        if (!c.loaded) {
-            if (!w_needed(a, w, w_shard_row(a, w.ml))) { c.t += gridDim.x; continue; }
+// Producer loop (warp 16).  Per tile the warp copies the tile's span row and compacts its used u
+// (non-empty spans) into a list with ballots; lane 0 then issues the tile's stages straight from
+// the list, so a stage costs lane 0 two shared loads, the header and the TMA instructions.
+__device__ __forceinline__ void w_produce(int2* tspan, int* ulist, WHeader* hdr, const S1WArgs& a, int n_tiles,
+                                          const CUtensorMap* tm_g, const CUtensorMap* tm_e, uint8_t* smem,
+                                          uint64_t* full, uint64_t* empty, int lane) {
+    int s = 0, k = 0;
+    uint32_t ph = 0;
+    for (int t = blockIdx.x;; t += gridDim.x) {
+        int cnt = 0;
+        WTile w{};
+        for (; t < n_tiles; t += gridDim.x) {
+            w = w_tile(a, t);
+            if (!w_needed(a, w, w_shard_row(a, w.ml))) continue;
             const int2* sp_row = a.span + static_cast<int64_t>(w.g * a.n_xt + w.xt) * a.Wb;
             __syncwarp();
-            for (int u = lane; u < a.Wb; u += 32) tspan[u] = __ldg(sp_row + u);
+            for (int base = 0; base < a.Wb; base += 32) {
+                const int u = base + lane;
+                int2 sp = make_int2(1, 0);
+                if (u < a.Wb) sp = __ldg(sp_row + u);
+                const bool ne = sp.y >= sp.x;
+                const unsigned m = __ballot_sync(0xffffffffu, ne);
+                if (ne) {
+                    const int pos = cnt + __popc(m & ((1u << lane) - 1u));
+                    ulist[pos] = u;
+                    tspan[pos] = sp;
+                }
+                cnt += __popc(m);
+            }
             __syncwarp();
-            c.loaded = 1;
-            c.u = 0;
-            c.started = 0;
+            if (cnt > 0) break;
         }
-        const int u = w_next_u(tspan, a.Wb, c.u, lane);
-        if (u < 0) { c.t += gridDim.x; c.loaded = 0; continue; }
-        const bool last = w_next_u(tspan, a.Wb, u + 1, lane) < 0;
         if (lane == 0) {
-            const int2 sp = tspan[u];
-            hdr[s].tile = c.t;
-            hdr[s].flags = (c.started ? 0 : 1) | (last ? 2 : 0);
-            const int nb = a.probe & 1 ? 0 : (sp.y - sp.x + kWBox) / kWBox;
-            mbar_expect_tx(&full[s], nb * kWBox * kWRowBytes + kWEBytes);
-            uint8_t* dst = smem + s * kWStageBytes;
-            for (int b = 0; b < nb; ++b)
-                tma_load_5d(dst + b * kWBox * kWRowBytes, tm_g, &full[s], 0, u, w.vb, sp.x + b * kWBox, w.ml);
-            tma_load_3d(dst + kWGBytes, tm_e, &full[s], 2 * w.xt * kWX, u, w.g * kWF);
-            c.u = u + 1;
-            c.started = 1;
-            if (last) { c.t += gridDim.x; c.loaded = 0; }
-            *cur = c;
+            if (t >= n_tiles) {   // end marker
+                if (k >= kWStages) mbar_wait(&empty[s], ph ^ 1);
+                hdr[s].tile = -1;
+                hdr[s].flags = 0;
+                mbar_arrive(&full[s]);
+            } else {
+                for (int i = 0; i < cnt; ++i) {
+                    if (k >= kWStages) mbar_wait(&empty[s], ph ^ 1);
+                    const int u = ulist[i];
+                    const int2 sp = tspan[i];
+                    hdr[s].tile = t;
+                    hdr[s].flags = (i == 0 ? 1 : 0) | (i == cnt - 1 ? 2 : 0);
+                    const int nb = a.probe & 1 ? 0 : (sp.y - sp.x + kWBox) / kWBox;
+                    mbar_expect_tx(&full[s], nb * kWBox * kWRowBytes + kWEBytes);
+                    uint8_t* dst = smem + s * kWStageBytes;
+                    for (int b = 0; b < nb; ++b)
+                        tma_load_5d(dst + b * kWBox * kWRowBytes, tm_g, &full[s], 0, u, w.vb, sp.x + b * kWBox, w.ml);
+                    tma_load_3d(dst + kWGBytes, tm_e, &full[s], 2 * w.xt * kWX, u, w.g * kWF);
+                    ++k;
+                    if (++s == kWStages) { s = 0; ph ^= 1; }
+                }
+            }
         }
         __syncwarp();
-        return false;
+        if (t >= n_tiles) return;
     }
 }
 
@@ -282,7 +270,6 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
     extern __shared__ __align__(1024) uint8_t w_smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(w_smem + kWOffBar);
     WHeader* hdr = reinterpret_cast<WHeader*>(w_smem + kWOffHdr);
-    WCursor* cur = reinterpret_cast<WCursor*>(w_smem + kWOffCur);
     int2* tspan = reinterpret_cast<int2*>(w_smem + kWOffSpan);
     uint64_t* empty = full + kWStages;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(w_smem + kWOffTmem);
@@ -294,7 +281,6 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
             mbar_init(&empty[s], kWWarps);   // lane 0 of every consumer warp
         }
         fence_mbar_init();
-        *cur = WCursor{static_cast<int>(blockIdx.x), 0, 0, 0};
         tma_prefetch_desc(&tm_g);
         tma_prefetch_desc(&tm_e);
     }
@@ -307,13 +293,8 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kWProdRegs));
         if (warp != kWWarps) return;
         // stages in order; slot s is refilled once all consumer warps released it
-        int s = 0;
-        uint32_t ph = 0;
-        for (int k = 0;; ++k) {
-            if (k >= kWStages) mbar_wait(&empty[s], ph ^ 1);
-            if (w_issue(cur, tspan, hdr, s, a, n_tiles, &tm_g, &tm_e, w_smem, full, lane)) break;
-            if (++s == kWStages) { s = 0; ph ^= 1; }
-        }
+        w_produce(tspan, reinterpret_cast<int*>(w_smem + kWOffUList), hdr, a, n_tiles, &tm_g, &tm_e, w_smem, full,
+                  empty, lane);
         return;
     }
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kWConsRegs));
