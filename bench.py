@@ -514,6 +514,12 @@ def main():
                  "frac_of_sustained": gemm_tops / tc_sustained if gemm_tops else None,
                  "frac_of_clock_peak": gemm_tops / clock_peak_tops if gemm_tops else None,
                  "clock_peak_tops": clock_peak_tops,
+                 "smem_view": ({"ceiling_tops": 448.0 / 578.0 * clock_peak_tops,
+                                "frac": gemm_tops / (448.0 / 578.0 * clock_peak_tops) if gemm_tops else None,
+                                "note": ("shared-memory roof of the CTA-pair FP4 tile: 74 KB of operand traffic "
+                                         "(TMA writes + tensor-core reads) per 256-frame k-block at 128 B/clk = 578 "
+                                         "clocks vs 448 clocks of MMAs (DESIGN.md §17.2)")}
+                               if args.variant == "fp4" else None),
                  "ops_per_launch": ops, "ms_per_launch": gemm_ms / gemm_n if gemm_n else None,
                  "traffic": traffic.get("gemm_i8_tc2_kernel<fp4>" if args.variant == "fp4" else
                                         "gemm_i8_tc2_kernel<i8>", {}).get("bytes_per_launch")
