@@ -307,24 +307,25 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
     const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + static_cast<uint32_t>(warp >> 2) * 128u;
     const uint32_t lane16 = 16u * (lane & 15);
     uint64_t part[kWFW][kWXW][2];
-    bool first = true;   // no fp64 partial in TMEM yet for this tile
-    int nst = 0, nfw = 0;
-    int stage = 0;
-    uint32_t phase = 0;
+    // loop state kept small (the consumers run at the 112-register cap): kst = stages of the current
+    // tile so far (a flush every kWFlush; no fp64 partial in TMEM while kst < kWFlush), ring position
+    // sp = slot | phase << 2
+    int kst = 0;
+    uint32_t sp = 0;
+    static_assert(kWStages == 4, "ring position packing assumes 4 slots");
     for (;;) {
+        const int stage = static_cast<int>(sp & 3u);
+        const uint32_t phase = sp >> 2;
         if (a.probe & 8) mbar_wait_spin(&full[stage], phase);   // probe 8: non-suspending wait
         else mbar_wait(&full[stage], phase);
         const WHeader h = hdr[stage];
         if (h.tile < 0) break;
         if (h.flags & 1) {   // first stage of a tile
-            const WTile w = w_tile(a, h.tile);
-            nfw = min(kWFW, a.n_planes - w.g * kWF - kWFW * wp);   // this warp's planes (may be <= 0)
 #pragma unroll
             for (int pl = 0; pl < kWFW; ++pl)
 #pragma unroll
                 for (int i = 0; i < kWXW; ++i) part[pl][i][0] = part[pl][i][1] = 0ull;
-            first = true;
-            nst = 0;
+            kst = 0;
         }
         const uint8_t* sbase = w_smem + stage * kWStageBytes;
         const uint4* E = reinterpret_cast<const uint4*>(sbase + kWGBytes);
@@ -361,12 +362,13 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
-        if (++stage == kWStages) { stage = 0; phase ^= 1; }
+        sp = (sp + 1u) & 7u;
         if (h.flags & 2) {   // last stage of the tile: fp64 sum (TMEM + partial) -> fp32 T
             const WTile w = w_tile(a, h.tile);
             const int m = w_shard_row(a, w.ml);
             const int x0 = w.xt * kWX + wx * kWXW;
-            const bool lane_ok = lpl < nfw;   // this lane's plane is in the batch
+            const bool first = kst < kWFlush;   // no fp64 partial in TMEM yet
+            const bool lane_ok = kWFW * wp + lpl < a.n_planes - w.g * kWF;   // this lane's plane is in the batch
             float* Tf = a.T + static_cast<int64_t>(w.g * kWF + kWFW * wp + (lane_ok ? lpl : 0)) * a.t_plane;
 #pragma unroll
             for (int hv = 0; hv < 2; ++hv) {   // v half (the accumulators' first index)
@@ -393,10 +395,8 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
                     }
                 }
             }
-        } else if (++nst == kWFlush && !(a.probe & 4)) {   // probe 4: no flushes (wrong values)
-            w_flush(part, tbase, first);
-            first = false;
-            nst = 0;
+        } else if ((++kst & (kWFlush - 1)) == 0 && !(a.probe & 4)) {   // probe 4: no flushes (wrong values)
+            w_flush(part, tbase, kst == kWFlush);
         }
     }
     // all consumer warps done with TMEM before warp 0 frees it (the producers have exited)
