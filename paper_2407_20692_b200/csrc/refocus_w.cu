@@ -223,12 +223,13 @@ __device__ __forceinline__ void w_produce(int2* tspan, int* ulist, WHeader* hdr,
 }
 
 // fp64 accumulators of a lane in TMEM: v half h (of the lane's two 4-v groups), output i, v slot
-// k at columns 64 h + 8 i + 2 k (+1: high word).  r holds columns [32 half, +32) of one v half
-// (outputs 4 half .. 4 half + 3); adds the fp32 partials (r ignored when first).
-__device__ __forceinline__ void w_combine(const uint64_t (&pp)[kWXW][2], uint32_t (&r)[32], int half, bool first) {
+// k at columns 64 h + 8 i + 2 k (+1: high word).  r holds columns [16 qt, +16) of one v half
+// (outputs 2 qt, 2 qt + 1); adds the fp32 partials (r ignored when first).  16 columns at a time
+// keep the temporaries small (the consumers run at the 112-register cap).
+__device__ __forceinline__ void w_combine(const uint64_t (&pp)[kWXW][2], uint32_t (&r)[16], int qt, bool first) {
 #pragma unroll
-    for (int ii = 0; ii < 4; ++ii) {
-        const int i = 4 * half + ii;
+    for (int ii = 0; ii < 2; ++ii) {
+        const int i = 2 * qt + ii;
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
             const float2 p = upk2(pp[i][q]);
@@ -248,15 +249,15 @@ __device__ __forceinline__ void w_flush(uint64_t (&part)[kWFW][kWXW][2], uint32_
 #pragma unroll
     for (int pl = 0; pl < kWFW; ++pl)
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            uint32_t r[32];
-            const uint32_t col = tbase + 64 * pl + 32 * half;
+        for (int qt = 0; qt < 4; ++qt) {
+            uint32_t r[16];
+            const uint32_t col = tbase + 64 * pl + 16 * qt;
             if (!first) {
-                tmem_ld_32x32b_x32(col, r);
+                tmem_ld_32x32b_x16(col, r);
                 tmem_wait_ld();
             }
-            w_combine(part[pl], r, half, first);
-            tmem_st_32x32b_x32(col, r);
+            w_combine(part[pl], r, qt, first);
+            tmem_st_32x32b_x16(col, r);
         }
     tmem_wait_st();
 #pragma unroll
@@ -374,16 +375,16 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
             for (int hv = 0; hv < 2; ++hv) {   // v half (the accumulators' first index)
                 const int v = w.vb * kWV + 64 * hv + 4 * (lane & 15);
 #pragma unroll
-                for (int half = 0; half < 2; ++half) {   // outputs 4 half .. 4 half + 3
-                    uint32_t r[32];
+                for (int qt = 0; qt < 4; ++qt) {   // outputs 2 qt, 2 qt + 1
+                    uint32_t r[16];
                     if (!first) {   // warp-collective TMEM load (every lane, valid plane or not)
-                        tmem_ld_32x32b_x32(tbase + 64 * hv + 32 * half, r);
+                        tmem_ld_32x32b_x16(tbase + 64 * hv + 16 * qt, r);
                         tmem_wait_ld();
                     }
-                    w_combine(part[hv], r, half, first);
+                    w_combine(part[hv], r, qt, first);
 #pragma unroll
-                    for (int ii = 0; ii < 4; ++ii) {
-                        const int x = x0 + 4 * half + ii;
+                    for (int ii = 0; ii < 2; ++ii) {
+                        const int x = x0 + 2 * qt + ii;
                         float o[4];
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
