@@ -130,11 +130,17 @@ def correlate_files(ctx, manifest: Manifest, batch_frames: Optional[int] = None,
     if (manifest.width, manifest.height) != (ctx.width, ctx.height):
         raise ValueError("manifest layout differs from the context's")
     batch_frames = int(batch_frames or ctx.max_frames)
+    if batch_frames > ctx.max_frames:
+        raise ValueError(f"batch_frames {batch_frames} exceeds the context's max_frames {ctx.max_frames}")
+    batches = list(_batches(manifest, batch_frames))
+    if len(batches) > 1 and not ctx.keep_counts:
+        raise ValueError("more than one batch needs a context with keep_counts=True (CPI_KEEP_COUNTS)")
+    if not ctx.keep_counts and gamma is None:
+        raise ValueError("a context without kept counts needs a gamma output")
     fb = ctx.frame_bytes
     bufs = [torch.empty(batch_frames * fb, dtype=torch.uint8).pin_memory() for _ in range(2)]
     done: list = [None, None]
     st = stream if stream is not None else torch.cuda.current_stream(ctx.device)
-    batches = list(_batches(manifest, batch_frames))
     total = 0
     for b, (pieces, n) in enumerate(batches):
         k = b & 1

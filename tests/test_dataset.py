@@ -84,3 +84,17 @@ def test_batches_cover_every_frame_once():
             off += cnt
             got += [(path, f0 + k) for k in range(cnt)]
     assert got == [(f"f{i}", k) for i in range(3) for k in range(5)]
+
+
+def test_correlate_files_argument_checks(tmp_path):
+    class _Ctx:   # host-side checks run before any device work
+        width, height, frame_bytes, max_frames, keep_counts, device = 512, 256, 16384, 4, False, 0
+    m = dataset.Manifest(["f0", "f1"], 5)
+    with pytest.raises(ValueError, match="max_frames"):
+        dataset.correlate_files(_Ctx(), m, batch_frames=8)
+    with pytest.raises(ValueError, match="keep_counts"):
+        dataset.correlate_files(_Ctx(), m)
+    c = _Ctx()
+    c.max_frames = 10
+    with pytest.raises(ValueError, match="gamma"):
+        dataset.correlate_files(c, m)
