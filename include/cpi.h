@@ -172,17 +172,20 @@ typedef struct {
                                  c_Bx = dx (x - c_ax) + ex (u - c_bx) + fx + c_bx
                                (y, v likewise; evaluated left to right in fp64).  A sample counts
                                only if all four coordinates lie on their lattices (skip policy).
-                               GPU support: B coordinates independent of the output pixel
-                               (dx = dy = 0).  Integral B (ex = ey = 1, fx = fy = 0) runs the
+                               B coordinates independent of the output pixel (dx = dy = 0):
+                               integral B (ex = ey = 1, fx = fy = 0) runs the
                                fast separable kernels directly.  Any other (ex, fx, ey, fy):
                                the library resamples Gamma onto the B lattice once per distinct
                                B map (a rows x P_b fp32 workspace, allocated on first use and
                                kept) and runs the same fast kernels, consecutive planes with
                                one B map fused; if that workspace cannot be allocated it falls
                                back to general-B kernels (2 x 2 corners per stage, row-major B
-                               order, contiguous row shards only).  dx or dy != 0 ->
-                               CPI_ERR_UNSUPPORTED.  The default map is {a, 1 - a, 0, 0, 1, 0}
-                               on both axes. */
+                               order, contiguous row shards only).  dx or dy != 0 (B
+                               coordinates depending on the output pixel): per-axis support
+                               tables and two image-sampling stages (refocus_gen.cu; row-major
+                               B order, A RoIs up to 256 px per side, contiguous row shards;
+                               otherwise CPI_ERR_UNSUPPORTED).  The default map is
+                               {a, 1 - a, 0, 0, 1, 0} on both axes. */
 } cpi_refocus_spec;
 
 typedef struct cpi_ctx cpi_ctx;   /* opaque, owned by the library */
