@@ -41,7 +41,7 @@ constexpr int kWWarps = 16;
 constexpr int kWXW = 8;                            // outputs x per warp
 constexpr int kWF = 8;                             // planes per group
 constexpr int kWFW = 2;                            // planes per warp
-constexpr int kWBox = 16;                          // j rows per Gamma TMA box
+constexpr int kWBox = 8;                           // j rows per Gamma TMA box
 constexpr int kWRows = 96;                         // staged j rows (6 boxes); larger spans -> plain stage 1
 constexpr int kWStages = 4;
 constexpr int kWFlush = 8;                         // u per fp32 partial before the fp64 flush
