@@ -549,10 +549,11 @@ cpi_status refocus_vmajor(cpi_ctx* c, const cpi_refocus_spec* spec, float* plane
         {
             TimedScope ts(c, KC_STAGE2, st);
             cudaError_t e = cudaSuccess;
-            for (int g0 = 0; g0 < nb && e == cudaSuccess; g0 += gf) {
-                const int nf = std::min(gf, nb - g0);
+            const int gf2 = cpi::stage2_staged_supported(Ha) ? cpi::kS2MaxPlanes : gf;   // planes per stage-2 launch
+            for (int g0 = 0; g0 < nb && e == cudaSuccess; g0 += gf2) {
+                const int nf = std::min(gf2, nb - g0);
                 if (cpi::stage2_staged_supported(Ha)) {
-                    cpi::TElem* Tp[cpi::kRefocusMaxFuse];
+                    cpi::TElem* Tp[cpi::kS2MaxPlanes];
                     for (int f = 0; f < nf; ++f) Tp[f] = c->w_T + (g0 + f) * t_plane;
                     e = cpi::launch_refocus_stage2_group(Tp, nf, Wa, Ha, Hb, m_base, m_count, m_block, m_stride,
                                                          c->wxs + g0, c->wys + g0, c->w_ypack + int64_t(g0) * Hb * Ha,

@@ -142,6 +142,7 @@ cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int H
 // sharing one pass over Gamma.  Needs W_a <= 256 with W_a % 4 == 0, W_b % 4 == 0, W_b <= 512, H_b <= 256, the tensor maps of
 // Gamma (4D: u, v, j, m) and of the packed x-tables (3D uint32: x, u, plane slot).
 constexpr int kRefocusMaxFuse = 4;
+constexpr int kS2MaxPlanes = 16;   // planes per staged stage-2 launch (more CTAs in flight over T)
 struct Stage1Maps {
     CUtensorMap gamma;       // 4D (u, v, j, m) row-major Gamma, or 5D (u%8, v, u/8, j, m) u-blocked
     CUtensorMap xtab;

@@ -590,13 +590,13 @@ constexpr int kS2VC = 16, kS2XB = 2, kS2Threads = 256, kS2MI = 256 / (kS2Threads
 struct S2Args {
     int Wa, Ha, Hb;
     int m_base, m_count, m_block, m_stride;      // rows of T present: the shard's A rows (see S1Args)
-    const TElem* T[kRefocusMaxFuse];
-    const int32_t* xcnt[kRefocusMaxFuse];
-    const int32_t* ycnt[kRefocusMaxFuse];
-    const int32_t* ylo[kRefocusMaxFuse];
-    const int32_t* yhi[kRefocusMaxFuse];
+    const TElem* T[kS2MaxPlanes];
+    const int32_t* xcnt[kS2MaxPlanes];
+    const int32_t* ycnt[kS2MaxPlanes];
+    const int32_t* ylo[kS2MaxPlanes];
+    const int32_t* yhi[kS2MaxPlanes];
     const uint32_t* ypack;                       // [F][H_b][H_a]
-    float* plane[kRefocusMaxFuse];
+    float* plane[kS2MaxPlanes];
 };
 
 __global__ void __launch_bounds__(kS2Threads, 3)
@@ -1033,7 +1033,7 @@ cudaError_t launch_pack_ytable_group(const AxisTables* ys, int n_fuse, int Ha, i
 cudaError_t launch_refocus_stage2_group(TElem* const* T, int n_fuse, int Wa, int Ha, int Hb, int m_base, int m_count,
                                         int m_block, int m_stride, const AxisTables* xs, const AxisTables* ys,
                                         const uint32_t* ypack, float* planes, cudaStream_t st) {
-    if (n_fuse < 1 || n_fuse > kRefocusMaxFuse || !stage2_staged_supported(Ha)) return cudaErrorInvalidValue;
+    if (n_fuse < 1 || n_fuse > kS2MaxPlanes || !stage2_staged_supported(Ha)) return cudaErrorInvalidValue;
     S2Args a{};
     a.Wa = Wa; a.Ha = Ha; a.Hb = Hb; a.ypack = ypack;
     a.m_base = m_base; a.m_count = m_count;
