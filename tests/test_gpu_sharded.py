@@ -31,7 +31,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, mode="rows", affine=False):
+def _worker(rank, world, port, q, mode="rows", affine=False, order="rowmajor", variant="tc"):
     import torch.distributed as dist
     import synth
     from paper_2407_20692_b200 import parallel
@@ -42,7 +42,7 @@ def _worker(rank, world, port, q, mode="rows", affine=False):
         frames = synth.bernoulli_frames(N, 0.2, seed=77)
         lo, hi = parallel.frame_slice(N, rank, world)
         be = parallel.CudaBackend(ROI_A, ROI_B, N if mode == "tiles" else hi - lo, device=0,
-                                  keep_counts=mode != "tiles")
+                                  keep_counts=mode != "tiles", gamma_order=order, variant=variant)
 
         class GlooCuda:
             """gloo collectives need host tensors: stage through the host (plumbing only)."""
@@ -79,8 +79,11 @@ def _worker(rank, world, port, q, mode="rows", affine=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode,affine", [("rows", False), ("tiles", False), ("rows", True)])
-def test_two_ranks_on_one_gpu_match_single_context(mode, affine):
+@pytest.mark.parametrize("mode,affine,order,variant", [("rows", False, "rowmajor", "tc"), ("tiles", False, "rowmajor", "tc"),
+                                                       ("rows", True, "rowmajor", "tc"),
+                                                       ("tiles", False, "vmajor", "fp4"),   # bench.py's --gpus N step
+                                                       ("rows", False, "vmajor", "fp4")])
+def test_two_ranks_on_one_gpu_match_single_context(mode, affine, order, variant):
     import torch.multiprocessing as mp
     import synth
     from paper_2407_20692_b200 import Context
@@ -88,7 +91,7 @@ def test_two_ranks_on_one_gpu_match_single_context(mode, affine):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, mode, affine)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, mode, affine, order, variant)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=600) for _ in range(world)]
@@ -96,7 +99,7 @@ def test_two_ranks_on_one_gpu_match_single_context(mode, affine):
         p.join(timeout=120)
         assert p.exitcode == 0
     frames = synth.bernoulli_frames(N, 0.2, seed=77)
-    c = Context(ROI_A, ROI_B, N)
+    c = Context(ROI_A, ROI_B, N, gamma_order=order, variant=variant)
     c.load_frames(frames)
     g = c.correlate(c.new_gamma())
     planes = c.new_planes(len(MAPS) if affine else len(ALPHAS))
@@ -108,8 +111,9 @@ def test_two_ranks_on_one_gpu_match_single_context(mode, affine):
     G = g.cpu().numpy()
     P = planes.cpu().numpy()
     dims = (ROI_A[2], ROI_A[3], ROI_B[2], ROI_B[3])
-    Gabs = np.abs(G.astype(np.float64))
-    R = oracle.refocus_affine(G, dims, MAPS) if affine else oracle.refocus(G, dims, ALPHAS)
+    G_rm = G[:, c.b_index()]                        # the oracle reads row-major B columns
+    Gabs = np.abs(G_rm.astype(np.float64))
+    R = oracle.refocus_affine(G_rm, dims, MAPS) if affine else oracle.refocus(G_rm, dims, ALPHAS)
     M = oracle.refocus_affine(Gabs, dims, MAPS) if affine else oracle.refocus(Gabs, dims, ALPHAS)
     for rank, n_tot, rows, panels, g_rows, pl in out:
         assert n_tot == N and panels > 1           # several row panels, block-cyclic ownership
