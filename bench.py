@@ -52,9 +52,10 @@ def parse():
                    help="frames per step, split across the ranks (strong scaling of the configs[1] step)")
     p.add_argument("--planes", type=int, default=64, help="refocus planes per step")
     p.add_argument("--occupancy", type=float, default=0.05, help="Bernoulli f of the synthetic bits")
-    p.add_argument("--variant", default=STEP_VARIANT, choices=["tc", "popc", "fp4"],
+    p.add_argument("--variant", default=STEP_VARIANT, choices=["tc", "popc", "fp4", "bits"],
                    help="pair-sum GEMM: fp4 = tcgen05 kind::mxf4 on E2M1 0/1 (default, exact), "
-                        "tc = kind::i8, popc = popcount(AND)")
+                        "tc = kind::i8, popc = popcount(AND), bits = kind::i8 on bit streams unpacked in "
+                        "shared memory (f1)")
     p.add_argument("--roi", default="full", choices=["full", "128", "tiny"])
     p.add_argument("--gamma-order", default=STEP_GAMMA_ORDER, choices=["ublocked", "rowmajor", "vmajor"],
                    help="column order of the step's Gamma (include/cpi.h CPI_GAMMA_UBLOCKED)")
@@ -383,7 +384,7 @@ def main():
             from paper_2407_20692_b200 import nccl_unique_id
             box = [nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(box, src=0)
-            fused = not args.no_fused_reduce and args.variant != "popc"
+            fused = not args.no_fused_reduce and args.variant in ("tc", "fp4")
             ctx = Context(roi_a, roi_b, n, device=local, variant=args.variant, gamma_order=args.gamma_order,
                           keep_counts=not fused, rank=rank, world=world, nccl_id=box[0], fused_reduce=fused)
             planes = ctx.new_planes(args.planes)
@@ -504,6 +505,7 @@ def main():
     if args.variant == "fp4":
         clock_peak_tops *= 2.0                        # 16384 e2m1 MAC/clk/SM
     roof_gemm = {"kernel": {"tc": "gemm_i8_tc2 (KB2, cta_group::2, kind::i8)", "popc": "gemm_popc (KB3)",
+                            "bits": "gemm_i8_tc2<bits> (f1: bit streams unpacked in shared memory, kind::i8)",
                             "fp4": "gemm_i8_tc2<fp4> (KB2, cta_group::2, kind::mxf4)"}[args.variant],
                  "bound": "tensor", "achieved": gemm_tops, "peak": tc_burst, "unit": "TOPS",
                  "frac": gemm_tops / tc_burst if gemm_tops else None,
@@ -523,7 +525,7 @@ def main():
                  "ops_per_launch": ops, "ms_per_launch": gemm_ms / gemm_n if gemm_n else None,
                  "traffic": traffic.get("gemm_i8_tc2_kernel<fp4>" if args.variant == "fp4" else
                                         "gemm_i8_tc2_kernel<i8>", {}).get("bytes_per_launch")
-                 if args.variant != "popc" else None,
+                 if args.variant in ("tc", "fp4") else None,
                  "traffic_note": "ncu dram read + write bytes per launch (profiles/r02_traffic.json)"}
     fma_peak_gtaps = 148 * 128 * f_clk / 1e9         # 128 fp32 FMA lanes per clock per SM
     vm = args.gamma_order == "vmajor"
@@ -576,6 +578,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None,
         "dtype": {"tc": "u8 x u8 -> s32 (S_ab)", "popc": "u32 popc(and) -> s32 (S_ab)",
+                  "bits": "1-bit streams -> u8 in smem, u8 x u8 -> s32 (S_ab)",
                   "fp4": "e2m1 {0,1} x e2m1 -> f32 exact integers -> s32 (S_ab)"}[args.variant]
                  + ", f64 -> f32 (Gamma), f32/f64 (refocus)",
         "data": "synthetic",

@@ -74,6 +74,14 @@ typedef int32_t cpi_status;
                                  2^0, fp32 accumulation -- every partial sum is an integer
                                  < 2^24, so S_ab is exact for batches of < 2^24 frames; twice the
                                  int8 MMA rate.  Exclusive with CPI_VARIANT_POPC. */
+#define CPI_VARIANT_TC_BITS 64u /* SURVEY f1 ("bit unpacking and cross-correlation calculation
+                                 occur jointly in the same kernel"): the expansion writes pixel-major
+                                 bit streams (1 bit per frame, 1/8 of the u8 operand bytes) and the
+                                 CTA-pair kind::i8 GEMM TMA-loads them and unpacks each stage into
+                                 the swizzled u8 operand tiles in shared memory (expansion warps,
+                                 fence.proxy.async, then the MMA).  Same exact int32 S_ab.
+                                 Exclusive with CPI_VARIANT_POPC / CPI_VARIANT_FP4; plain epilogue
+                                 (no CPI_FUSED_REDUCE, no SYRK). */
 #define CPI_GAMMA_UBLOCKED 8u /* B pixels are ordered u-blocked everywhere in this context: B pixel
                                  q = v*W_b + u has index (u/8)*(8*H_b) + 8*v + u%8 in S_b, in the
                                  columns of S_ab and of every Gamma it writes or cpi_refocus reads

@@ -19,6 +19,7 @@ CPI_NCCL_ID_BYTES = 128
 CPI_LSB_FIRST, CPI_MSB_FIRST = 0, 1
 CPI_HOST, CPI_DEVICE = 0, 1
 CPI_VARIANT_TC, CPI_VARIANT_POPC, CPI_KEEP_COUNTS, CPI_VARIANT_FP4, CPI_GAMMA_UBLOCKED = 0, 1, 2, 4, 8
+CPI_VARIANT_TC_BITS = 64   # f1: bit-stream operands unpacked inside the CTA-pair kind::i8 GEMM
 CPI_GAMMA_VMAJOR = 16
 CPI_FUSED_REDUCE = 32
 CPI_SHARD_HANDLE_BYTES = 64

@@ -37,9 +37,10 @@ class Context:
         collective).  fused_reduce: CPI_FUSED_REDUCE (the GEMM epilogue adds into the owners'
         shards; without nccl_id the caller maps the peers with open_peer_shards)."""
         self._lib = _lib.load()
-        if variant not in ("tc", "popc", "fp4"):
-            raise ValueError("variant must be 'tc', 'popc' or 'fp4'")
-        flags = {"tc": _lib.CPI_VARIANT_TC, "popc": _lib.CPI_VARIANT_POPC, "fp4": _lib.CPI_VARIANT_FP4}[variant]
+        if variant not in ("tc", "popc", "fp4", "bits"):
+            raise ValueError("variant must be 'tc', 'popc', 'fp4' or 'bits'")
+        flags = {"tc": _lib.CPI_VARIANT_TC, "popc": _lib.CPI_VARIANT_POPC, "fp4": _lib.CPI_VARIANT_FP4,
+                 "bits": _lib.CPI_VARIANT_TC_BITS}[variant]
         if keep_counts:
             flags |= _lib.CPI_KEEP_COUNTS
         if fused_reduce:

@@ -38,6 +38,7 @@ struct cpi_ctx {
     int num_sms = 148;
     bool popc = false, keep = false, pair = true;   // pair: cta_group::2 GEMM
     bool fp4 = false;                      // kind::mxf4 GEMM on E2M1 operands (2 frames per byte)
+    bool bits = false;                     // f1: kind::i8 GEMM unpacking bit-stream operands in shared memory
     bool ublocked = false;                 // B pixels in u-blocked order (CPI_GAMMA_UBLOCKED)
     bool symmetric = false;                // roi_a == roi_b: one operand, SYRK GEMM (upper tiles, mirrored)
     int order = cpi::kOrderRowMajor;       // B pixel order (row-major / u-blocked / v-major)
@@ -693,10 +694,12 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
         return fail(nullptr, CPI_ERR_UNSUPPORTED, "CPI_GAMMA_VMAJOR needs roi_b.height %% 4 == 0 and, above %d, a "
                                                   "multiple of %d", cpi::kVMajorBlock, cpi::kVMajorBlock);
     if (cfg->flags & ~(CPI_VARIANT_POPC | CPI_KEEP_COUNTS | CPI_VARIANT_FP4 | CPI_GAMMA_UBLOCKED | CPI_GAMMA_VMAJOR |
-                       CPI_FUSED_REDUCE))
+                       CPI_FUSED_REDUCE | CPI_VARIANT_TC_BITS))
         return fail(nullptr, CPI_ERR_INVALID_ARG, "unknown flags 0x%x", cfg->flags);
-    if ((cfg->flags & CPI_VARIANT_POPC) && (cfg->flags & CPI_VARIANT_FP4))
-        return fail(nullptr, CPI_ERR_INVALID_ARG, "CPI_VARIANT_POPC and CPI_VARIANT_FP4 are exclusive");
+    if (__builtin_popcount(cfg->flags & (CPI_VARIANT_POPC | CPI_VARIANT_FP4 | CPI_VARIANT_TC_BITS)) > 1)
+        return fail(nullptr, CPI_ERR_INVALID_ARG, "CPI_VARIANT_POPC, CPI_VARIANT_FP4 and CPI_VARIANT_TC_BITS are exclusive");
+    if ((cfg->flags & CPI_VARIANT_TC_BITS) && (cfg->flags & CPI_FUSED_REDUCE))
+        return fail(nullptr, CPI_ERR_UNSUPPORTED, "CPI_VARIANT_TC_BITS runs the plain GEMM epilogue (no CPI_FUSED_REDUCE)");
     if ((cfg->flags & CPI_VARIANT_FP4) && cfg->max_frames >= (int64_t(1) << 24))
         return fail(nullptr, CPI_ERR_INVALID_ARG, "CPI_VARIANT_FP4 needs max_frames < 2^24 (exact fp32 sums)");
 
@@ -738,6 +741,7 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
     c->num_sms = prop.multiProcessorCount;
     c->popc = (cfg->flags & CPI_VARIANT_POPC) != 0;
     c->fp4 = (cfg->flags & CPI_VARIANT_FP4) != 0;
+    c->bits = (cfg->flags & CPI_VARIANT_TC_BITS) != 0;
     c->keep = (cfg->flags & CPI_KEEP_COUNTS) != 0;
     c->p_a = int64_t(cfg->roi_a.width) * cfg->roi_a.height;
     c->p_b = int64_t(cfg->roi_b.width) * cfg->roi_b.height;
@@ -751,6 +755,11 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
         c->rows_a = round_up(c->p_a, cpi::gemm_popc_block());
         c->rows_b = round_up(c->p_b, cpi::gemm_popc_block());
         c->ld_op = c->k_cap / 32;   // 32-bit words
+    } else if (c->bits) {           // bit streams (as popc) padded to the CTA-pair tiles
+        c->pair = true;
+        c->rows_a = round_up(c->p_a, cpi::gemm_tc2_block_m());
+        c->rows_b = round_up(c->p_b, cpi::gemm_tc2_block_n());
+        c->ld_op = c->k_cap / 32;   // 32-bit words
     } else if (c->fp4) {
         c->pair = true;
         c->rows_a = round_up(c->p_a, cpi::gemm_tc2_block_m());
@@ -762,7 +771,7 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
         c->rows_b = round_up(c->p_b, c->pair ? cpi::gemm_tc2_block_n() : cpi::gemm_tc_block_n());
         c->ld_op = c->k_cap;        // bytes
     }
-    const size_t op_elem = c->popc ? 4 : 1;
+    const size_t op_elem = c->popc || c->bits ? 4 : 1;
     // roi_a == roi_b (e.g. the whole frame as both arms): S_ab is symmetric, so one
     // operand serves both arms and the CTA-pair GEMM computes only tiles touching the upper triangle
     // (SYRK), mirroring them in the epilogue; row-major B order only (the other
@@ -772,7 +781,7 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
     const cpi_roi& ra_ = cfg->roi_a;
     const cpi_roi& rb_ = cfg->roi_b;
     c->symmetric = ra_.x0 == rb_.x0 && ra_.y0 == rb_.y0 && ra_.width == rb_.width && ra_.height == rb_.height &&
-                   c->order == cpi::kOrderRowMajor && !c->popc && c->pair && !(cfg->world > 1 || cfg->nccl_id) &&
+                   c->order == cpi::kOrderRowMajor && !c->popc && !c->bits && c->pair && !(cfg->world > 1 || cfg->nccl_id) &&
                    getenv("CPI_SYRK") != nullptr && atoi(getenv("CPI_SYRK")) != 0;
     cudaError_t e = cudaSuccess;
     auto chk = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
@@ -867,7 +876,28 @@ cpi_status cpi_create(const cpi_config* cfg, cpi_ctx** out) {
         }
     }
     c->cfg.nccl_id = nullptr;   // the caller's buffer is not kept
-    if (!c->popc) {
+    if (c->bits) {   // 2D uint32 (words, rows), box 4 words (128 frames) x 128 rows, no swizzle
+        cpi_status s = CPI_OK;
+        for (int arm = 0; arm < 2 && s == CPI_OK; ++arm) {
+            cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
+            if (!enc) { s = fail(c, CPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver"); break; }
+            const int64_t rows = arm ? c->rows_b : c->rows_a;
+            const cuuint64_t dims[2] = {cuuint64_t(c->ld_op), cuuint64_t(rows)};
+            const cuuint64_t strides[1] = {cuuint64_t(c->ld_op) * 4};
+            const cuuint32_t box[2] = {4u, cuuint32_t(cpi::gemm_tc2_box_rows())};
+            const cuuint32_t estr[2] = {1u, 1u};
+            CUresult r = enc(arm ? &c->tm_b : &c->tm_a, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, arm ? c->op_b : c->op_a, dims,
+                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) s = fail(c, CPI_ERR_CUDA, "bit-stream tensor map failed (%d)", int(r));
+        }
+        if (s != CPI_OK) {
+            g_create_error = c->err;
+            free_all(c);
+            delete c;
+            return s;
+        }
+    } else if (!c->popc) {
         const uint32_t box_a = c->pair ? cpi::gemm_tc2_box_rows() : cpi::gemm_tc_block_m();
         const uint32_t box_b = c->fp4 ? cpi::gemm_f4_box_rows_b() : c->pair ? cpi::gemm_tc2_box_rows()
                                                                             : cpi::gemm_tc_block_n();
@@ -938,7 +968,7 @@ cpi_status expand_batch(cpi_ctx* c, cudaStream_t st) {
         return fail(c, CPI_ERR_CAPACITY, "N_TOT would reach %lld >= 2^31 (int32 sums)", (long long)(c->n_tot + n));
     const cpi_layout& L = c->cfg.layout;
     const int64_t k_pad = round_up(n, c->k_align);
-    const int mode = c->popc ? cpi::kExpandBits : c->fp4 ? cpi::kExpandE2M1 : cpi::kExpandU8;
+    const int mode = c->popc || c->bits ? cpi::kExpandBits : c->fp4 ? cpi::kExpandE2M1 : cpi::kExpandU8;
     TimedScope ts(c, KC_EXPAND, st);
     const cpi::RoiDev ra{c->cfg.roi_a.x0, c->cfg.roi_a.y0, c->cfg.roi_a.width, c->cfg.roi_a.height};
     const cpi::RoiDev rb{c->cfg.roi_b.x0, c->cfg.roi_b.y0, c->cfg.roi_b.width, c->cfg.roi_b.height};
@@ -1010,6 +1040,12 @@ cpi_status gemm_rows(cpi_ctx* c, int64_t row0, int64_t rows, float* gamma, cudaS
         epi.m_tile0 = static_cast<int>(row0 / T);
         e = cpi::launch_gemm_popc(static_cast<const uint32_t*>(c->op_a), static_cast<const uint32_t*>(c->op_b),
                                   c->ld_op, k_pad / 32, epi, st);
+    } else if (c->bits) {
+        const int64_t bm = cpi::gemm_tc2_block_m();
+        epi.m_tile0 = static_cast<int>(row0 / bm);
+        e = cpi::launch_gemm_bits(&c->tm_a, &c->tm_b, static_cast<int>((rows + bm - 1) / bm),
+                                  static_cast<int>(c->rows_b / cpi::gemm_tc2_block_n()),
+                                  static_cast<int>(k_pad / kKAlign), epi, c->num_sms, st);
     } else if (c->fp4) {
         const int64_t bm = cpi::gemm_tc2_block_m();
         epi.m_tile0 = static_cast<int>(row0 / bm);

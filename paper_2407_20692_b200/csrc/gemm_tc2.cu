@@ -35,9 +35,17 @@ struct Tc2 {
     static constexpr int kStageBytes = kABytes + kBBytes;   // per CTA
     static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256 + 2 * BN * 4;
     static constexpr uint32_t kSfCol = 448;                 // fp4: SFA at 448, SFB at 464
+    // f1 (bits mode, kind::i8 only): the packed bit streams of a stage (16 B per operand row) land
+    // by TMA in a small ring after the S_b staging; expansion warps write the u8 operand stage
+    static constexpr int kOffBits = kStages * kStageBytes + 256 + 2 * BN * 4;
+    static constexpr int kBitsStage = (HM + HN) * 16;       // 4 KB
+    static constexpr int kBitsSmem = kSmemBytes + kStages * kBitsStage;
 };
 constexpr int BM = 256, BK = 128;
 constexpr int kThreads = 192;
+constexpr int kExpGroups = 4;                     // f1: groups of 4 expansion warps, stage s to group s % kExpGroups
+constexpr int kExpWarps = 4 * kExpGroups;
+constexpr int kThreadsBits = kThreads + 32 * kExpWarps;
 constexpr int kTmemCols = 512;
 constexpr int kGroupM = 8;                        // pair-tile rows per raster group
 
@@ -61,8 +69,21 @@ __device__ __forceinline__ bool below_diagonal(int tm, int tn, int bn) {
     return kMode == kEpiSyrk && (tn + 1) * bn - 1 < tm * BM;
 }
 
-template <bool kF4, int kMode>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+// f1: 16 packed frames (16 bits) of one operand row -> 16 u8 bytes (0 / 1), frame f in byte f
+__device__ __forceinline__ uint4 bits_to_u8(uint32_t b16) {
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[q] = (((b16 >> (4 * q)) & 0xFu) * 0x00204081u) & 0x01010101u;   // bit k -> byte k
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// kBits (f1, SURVEY §8(f) "unpack fused into the GEMM producer"): the operands arrive as
+// pixel-major bit streams (bit f % 32 of word f / 32 = frame f, KB1's popcount layout); per stage
+// the producer TMA-loads 16 B of bits per operand row and kExpWarps expansion warps write the
+// 128-B swizzled u8 rows the MMA reads (fence.proxy.async, then an arrive on the leader's stage
+// barrier: 2 CTAs x kExpWarps arrivals instead of TMA transaction bytes).
+template <bool kF4, int kMode, bool kBits = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBits ? kThreadsBits : kThreads, 1)
 gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                    int m_tiles, int n_tiles, int k_blocks, Epilogue epi) {
     using P = Tc2<kF4>;
@@ -76,7 +97,9 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
     uint64_t* tfull = empty + kStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* bfull = reinterpret_cast<uint64_t*>(tmem_slot + 2);   // f1: bits stage landed (this CTA)
     int32_t* sb_stage = reinterpret_cast<int32_t*>(smem + kStages * kStageBytes + 256);   // [2][BN]
+    uint8_t* sbits = smem + P::kOffBits;                             // f1: [kStages][HM + HN][16 B]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -86,8 +109,9 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
         tma_prefetch_desc(&tma_a);
         tma_prefetch_desc(&tma_b);
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);      // leader: one arrive.expect_tx per stage
+            mbar_init(&full[s], kBits ? 8 : 1);   // leader: arrive.expect_tx (TMA), or 4 expansion warps x 2 CTAs
             mbar_init(&empty[s], 1);     // one multicast commit per stage
+            if (kBits) mbar_init(&bfull[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);     // one multicast commit per tile
@@ -126,6 +150,14 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
                 if (below_diagonal<kMode>(tm, tn, BN)) continue;
                 for (int kb = 0; kb < k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
+                    if constexpr (kBits) {   // this CTA's rows of the packed bits (4 words = 128 frames each)
+                        uint8_t* dst = sbits + stage * P::kBitsStage;
+                        mbar_expect_tx(&bfull[stage], P::kBitsStage);
+                        tma_load_2d(dst, &tma_a, &bfull[stage], kb * 4, tm * BM + rank * HM);
+                        tma_load_2d(dst + HM * 16, &tma_b, &bfull[stage], kb * 4, tn * BN + rank * HN);
+                        if (++stage == kStages) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
                     if (leader) mbar_expect_tx(&full[stage], 2 * kStageBytes);
                     if (epi.cache & 2) {
                         tma_load_2d_2sm_hint(sA + stage * kABytes, &tma_a, &full[stage], kb * BK, tm * BM + rank * HM, pol);
@@ -175,6 +207,35 @@ gemm_i8_tc2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_const
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
                 mma_commit_2sm(&tfull[acc]);
+            }
+        }
+    } else if (kBits && warp >= kThreads / 32) {
+        // f1 expansion warps: kExpGroups groups of 4 take stages in turn (several stages expanded at once);
+        // thread t of a group expands row t of this CTA's A half and of its B half
+        const int t = (threadIdx.x - kThreads) & 127, grp = (threadIdx.x - kThreads) >> 7;
+        const uint32_t full_leader0 = leader_addr(&full[0]);
+        int stage = 0, seq = 0;
+        uint32_t phase = 0;
+        for (int tt = pair; tt < num_tiles; tt += num_pairs) {
+            for (int kb = 0; kb < k_blocks; ++kb, ++seq) {
+                if (seq % kExpGroups == grp) {
+                    mbar_wait(&bfull[stage], phase);
+                    const uint8_t* src = sbits + stage * P::kBitsStage;
+#pragma unroll
+                    for (int op = 0; op < 2; ++op) {
+                        const uint4 b = *reinterpret_cast<const uint4*>(src + (op ? HM * 16 : 0) + t * 16);
+                        uint8_t* row = (op ? sB + stage * kBBytes : sA + stage * kABytes) + (t >> 3) * 1024 + (t & 7) * 128;
+                        const uint32_t wv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                        for (int c = 0; c < 8; ++c)   // 16-B chunk c = frames 16 c .. 16 c + 15, 128-B swizzle
+                            *reinterpret_cast<uint4*>(row + ((c ^ (t & 7)) << 4)) =
+                                bits_to_u8(wv[c >> 1] >> (16 * (c & 1)));
+                    }
+                    fence_proxy_async_smem();   // generic-proxy writes -> the tensor cores' async-proxy reads
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(full_leader0 + stage * 8);
+                }
+                if (++stage == kStages) { stage = 0; phase ^= 1; }
             }
         }
     } else {
@@ -336,6 +397,19 @@ cudaError_t launch_gemm_f4(const CUtensorMap* tma_a, const CUtensorMap* tma_b, i
                            int n_tiles, int k_blocks, const Epilogue& epi, int num_sms,
                            cudaStream_t st) {
     return launch_tc2<true>(tma_a, tma_b, m_tiles, n_tiles, k_blocks, epi, num_sms, st);
+}
+
+cudaError_t launch_gemm_bits(const CUtensorMap* tma_a, const CUtensorMap* tma_b, int m_tiles, int n_tiles,
+                             int k_blocks, const Epilogue& epi, int num_sms, cudaStream_t st) {
+    if (epi.peers || epi.symmetric) return cudaErrorInvalidValue;   // plain epilogue only
+    auto kern = gemm_i8_tc2_kernel<false, kEpiPlain, true>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc2<false>::kBitsSmem);
+    if (e != cudaSuccess) return e;
+    const int tiles = m_tiles * n_tiles;
+    int pairs = num_sms / 2;
+    if (tiles < pairs) pairs = tiles;
+    kern<<<2 * pairs, kThreadsBits, Tc2<false>::kBitsSmem, st>>>(*tma_a, *tma_b, m_tiles, n_tiles, k_blocks, epi);
+    return cudaGetLastError();
 }
 
 }  // namespace cpi

@@ -83,6 +83,11 @@ cudaError_t launch_gemm_f4(const CUtensorMap* tma_a, const CUtensorMap* tma_b, i
                            int n_tiles, int k_blocks, const Epilogue& epi, int num_sms,
                            cudaStream_t st);
 int gemm_f4_block_n();
+// f1: the CTA-pair kind::i8 GEMM fed with packed bit streams (uint32 [rows][k_pad / 32], KB1's
+// popcount layout) that expansion warps unpack into the swizzled u8 stages in shared memory.
+// Tensor maps: 2D uint32 (k_pad / 32 words, rows) with box (4, 128).  Plain epilogue only.
+cudaError_t launch_gemm_bits(const CUtensorMap* tma_a, const CUtensorMap* tma_b, int m_tiles, int n_tiles,
+                             int k_blocks, const Epilogue& epi, int num_sms, cudaStream_t st);
 int gemm_f4_box_rows_b();
 
 // KB3: popcount(AND) GEMM on CUDA cores over 32-bit bit streams [rows][ldw].

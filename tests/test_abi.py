@@ -66,6 +66,7 @@ def _cfg(lib_mod, roi_a=(0, 0, 256, 256), roi_b=(256, 0, 256, 256), w=512, h=256
     (dict(max_frames=0), -1),                       # CPI_ERR_INVALID_ARG
     (dict(flags=0x80), -1),
     (dict(flags=0x1 | 0x4), -1),                    # POPC and FP4 are exclusive
+    (dict(flags=0x40 | 0x4), -1),                   # f1 (TC_BITS) and FP4 are exclusive
     (dict(flags=0x4, max_frames=1 << 24), -1),      # FP4: exact fp32 sums need N < 2^24
     (dict(flags=0x8, roi_b=(256, 0, 12, 8)), -12),  # u-blocked Gamma needs W_b % 8 == 0
     (dict(order=5), -1),

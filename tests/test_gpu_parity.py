@@ -68,7 +68,7 @@ def _check_sums(got, want):
     assert got["n"] == want["n"]
 
 
-@pytest.mark.parametrize("variant", ["tc", "popc", "fp4"])
+@pytest.mark.parametrize("variant", ["tc", "popc", "fp4", "bits"])
 def test_tiny_config_bit_exact(variant):
     """BASELINE configs[0]: 8x8 rho_a x 4x4 rho_b (non byte-aligned), 1000 frames."""
     fr = synth.bernoulli_frames(1000, 0.05, seed=synth.SEED_ARMS)
@@ -78,7 +78,7 @@ def test_tiny_config_bit_exact(variant):
     _assert_gamma(got["gamma"], want["gamma"])
 
 
-@pytest.mark.parametrize("variant", ["tc", "popc", "fp4"])
+@pytest.mark.parametrize("variant", ["tc", "popc", "fp4", "bits"])
 @pytest.mark.parametrize("n", [1, 31, 127, 129, 255, 257, 1000, 2600, 12500])
 def test_ragged_tiles_and_k_tails(variant, n):
     """Several M/N tiles with ragged edges (P_a = 1500, P_b = 380) and K tails (N not a
@@ -131,6 +131,9 @@ def test_multi_batch_accumulation_and_virtual_ranks():
     three_f4 = _gpu_sums(fr, roi_a, roi_b, "fp4", batches=[1000, 1, 1999])
     _check_sums(three_f4, one)
     np.testing.assert_array_equal(three_f4["gamma"], one["gamma"])
+    three_bits = _gpu_sums(fr, roi_a, roi_b, "bits", batches=[1000, 1, 1999])   # f1: unpacked inside the GEMM
+    _check_sums(three_bits, one)
+    np.testing.assert_array_equal(three_bits["gamma"], one["gamma"])
     _check_sums(three, one)
     np.testing.assert_array_equal(three["gamma"], one["gamma"])
     parts = [_gpu_sums(fr[a:b], roi_a, roi_b, "tc", gamma=False) for a, b in [(0, 700), (700, 2048), (2048, 3000)]]
