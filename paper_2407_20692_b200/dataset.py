@@ -120,12 +120,15 @@ def _batches(manifest: Manifest, batch_frames: int):
         yield pieces, filled
 
 
-def correlate_files(ctx, manifest: Manifest, batch_frames: Optional[int] = None, gamma=None, stream=None) -> int:
+def correlate_files(ctx, manifest: Manifest, batch_frames: Optional[int] = None, gamma=None, stream=None,
+                    threads: Optional[int] = None) -> int:
     """Stream a dataset through a context: batches of up to ctx.max_frames frames are read into
     two pinned host buffers (the next batch is read while the GPU correlates the current one),
     loaded (cpi_load_frames, asynchronous from pinned memory) and accumulated (cpi_correlate).
     The context needs CPI_KEEP_COUNTS for more than one batch; `gamma`, if given, receives Gamma
-    of the totals from the last batch's fused epilogue.  Returns the number of frames."""
+    of the totals from the last batch's fused epilogue.  A batch's file pieces are read by
+    `threads` host threads at once (cpi_read_bin releases the GIL).  Returns the number of frames."""
+    from concurrent.futures import ThreadPoolExecutor
     import torch
     if (manifest.width, manifest.height) != (ctx.width, ctx.height):
         raise ValueError("manifest layout differs from the context's")
@@ -142,17 +145,19 @@ def correlate_files(ctx, manifest: Manifest, batch_frames: Optional[int] = None,
     done: list = [None, None]
     st = stream if stream is not None else torch.cuda.current_stream(ctx.device)
     total = 0
-    for b, (pieces, n) in enumerate(batches):
-        k = b & 1
-        if done[k] is not None:
-            done[k].synchronize()   # the GPU finished with this buffer's previous batch
-        for path, f0, cnt, off in pieces:
-            read_bin(path, f0, cnt, bufs[k][off * fb:(off + cnt) * fb], width=manifest.width,
-                     height=manifest.height, bit_order=manifest.bit_order)
-        ctx.load_frames(bufs[k][:n * fb], n, stream=st)
-        ctx.correlate(gamma if b == len(batches) - 1 else None, stream=st)
-        ev = torch.cuda.Event()
-        ev.record(st)
-        done[k] = ev
-        total += n
+    with ThreadPoolExecutor(max(1, threads or min(8, os.cpu_count() or 1))) as pool:
+        for b, (pieces, n) in enumerate(batches):
+            k = b & 1
+            if done[k] is not None:
+                done[k].synchronize()   # the GPU finished with this buffer's previous batch
+            buf = bufs[k]
+            list(pool.map(lambda pc: read_bin(pc[0], pc[1], pc[2], buf[pc[3] * fb:(pc[3] + pc[2]) * fb],
+                                              width=manifest.width, height=manifest.height,
+                                              bit_order=manifest.bit_order), pieces))
+            ctx.load_frames(buf[:n * fb], n, stream=st)
+            ctx.correlate(gamma if b == len(batches) - 1 else None, stream=st)
+            ev = torch.cuda.Event()
+            ev.record(st)
+            done[k] = ev
+            total += n
     return total
