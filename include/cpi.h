@@ -379,7 +379,8 @@ int64_t cpi_launch_count(const cpi_ctx *ctx);
 cpi_status cpi_set_timing(cpi_ctx *ctx, int32_t enable);
 cpi_status cpi_kernel_time_ms(cpi_ctx *ctx, int32_t kernel_class, double *ms, int64_t *launches);
 
-/* ABI version (major * 100 + minor). */
+/* ABI version (major * 100 + minor): 201 = 2.01 (2.00 + cpi_bin_frames / cpi_read_bin and
+ * CPI_VARIANT_TC_BITS). */
 int32_t cpi_abi_version(void);
 
 #ifdef __cplusplus

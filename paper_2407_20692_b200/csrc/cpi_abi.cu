@@ -580,7 +580,7 @@ cpi_status refocus_vmajor(cpi_ctx* c, const cpi_refocus_spec* spec, float* plane
 
 extern "C" {
 
-int32_t cpi_abi_version(void) { return 200; }
+int32_t cpi_abi_version(void) { return 201; }
 
 const char* cpi_status_string(cpi_status s) {
     switch (s) {

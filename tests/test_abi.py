@@ -33,7 +33,7 @@ def test_header_symbols_exported(lib):
 
 
 def test_abi_version_and_status_names(lib):
-    assert lib.cpi_abi_version() == 200
+    assert lib.cpi_abi_version() == 201
     assert lib.cpi_status_string(0) == b"CPI_OK"
     assert lib.cpi_status_string(-7) == b"CPI_ERR_DEGENERATE_ALPHA"
     assert lib.cpi_status_string(-12) == b"CPI_ERR_UNSUPPORTED"
