@@ -19,6 +19,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+# extra nvcc flags for experiments, e.g. CPI_NVCC_EXTRA=-DCPI_S1W_PROBES (KB5w timing probes);
+# a changed value does not mark the library stale: build with --force
+FLAGS += os.environ.get("CPI_NVCC_EXTRA", "").split()
 
 
 def _stale() -> bool:

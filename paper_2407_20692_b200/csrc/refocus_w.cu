@@ -45,6 +45,13 @@ constexpr int kWBox = 8;                           // j rows per Gamma TMA box
 constexpr int kWRows = 96;                         // staged j rows (6 boxes); larger spans -> plain stage 1
 constexpr int kWStages = 4;
 constexpr int kWFlush = 8;                         // u per fp32 partial before the fp64 flush
+// Timing probes (CPI_S1W_PROBE) are compiled in only with -DCPI_S1W_PROBES: the
+// consumer loop of the product kernel carries no probe tests.
+#ifdef CPI_S1W_PROBES
+#define W_PROBE(a, bit) (((a).probe & (bit)) != 0)
+#else
+#define W_PROBE(a, bit) false
+#endif
 // A producer warpgroup (warps 16-19; warp 16 issues, the others exit) next to the 16 consumer
 // warps: a 17th warp alone would put 5 warps on one SM sub-partition and cap the registers at 96,
 // so the producers drop to kWProdRegs with setmaxnreg and the consumers rise to kWConsRegs
@@ -206,7 +213,7 @@ __device__ __forceinline__ void w_produce(int2* tspan, int* ulist, WHeader* hdr,
                     const int2 sp = tspan[i];
                     hdr[s].tile = t;
                     hdr[s].flags = (i == 0 ? 1 : 0) | (i == cnt - 1 ? 2 : 0);
-                    const int nb = a.probe & 1 ? 0 : (sp.y - sp.x + kWBox) / kWBox;
+                    const int nb = W_PROBE(a, 1) ? 0 : (sp.y - sp.x + kWBox) / kWBox;
                     mbar_expect_tx(&full[s], nb * kWBox * kWRowBytes + kWEBytes);
                     uint8_t* dst = smem + s * kWStageBytes;
                     for (int b = 0; b < nb; ++b)
@@ -317,7 +324,7 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
     for (;;) {
         const int stage = static_cast<int>(sp & 3u);
         const uint32_t phase = sp >> 2;
-        if (a.probe & 8) mbar_wait_spin(&full[stage], phase);   // probe 8: non-suspending wait
+        if (W_PROBE(a, 8)) mbar_wait_spin(&full[stage], phase);   // probe 8: non-suspending wait
         else mbar_wait(&full[stage], phase);
         const WHeader h = hdr[stage];
         if (h.tile < 0) break;
@@ -334,7 +341,7 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
         // each 16-lane half walks its own plane; entries of planes past the batch are the TMA's zero
         // fill: zero weights (exact zero taps)
         const uint4* Ep = E + (kWFW * wp * kWX + wx * kWXW) / 2 + lpl * (kWX / 2);
-        if (a.probe & 16) {     // probe 16: no step work (ring / barrier / issue cost only)
+        if (W_PROBE(a, 16)) {     // probe 16: no step work (ring / barrier / issue cost only)
         } else {   // window reuse (rows kept in registers, loads only when they change)
             uint4 ga[2], gb[2];   // even / odd row of the window, v halves h = 0, 1
             ga[0] = ga[1] = gb[0] = gb[1] = make_uint4(0u, 0u, 0u, 0u);
@@ -396,7 +403,7 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
                     }
                 }
             }
-        } else if ((++kst & (kWFlush - 1)) == 0 && !(a.probe & 4)) {   // probe 4: no flushes (wrong values)
+        } else if ((++kst & (kWFlush - 1)) == 0 && !W_PROBE(a, 4)) {   // probe 4: no flushes (wrong values)
             w_flush(part, tbase, kst == kWFlush);
         }
     }
