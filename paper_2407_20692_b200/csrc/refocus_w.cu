@@ -114,6 +114,14 @@ __device__ __forceinline__ void w_lds_if(uint4& g, uint32_t addr, uint32_t flag)
         : "+r"(g.x), "+r"(g.y), "+r"(g.z), "+r"(g.w)
         : "r"(flag), "r"(addr));
 }
+// Both 16-byte halves of one staged row (addr, addr + 256) if flag != 0, one predicate for the pair
+__device__ __forceinline__ void w_lds2_if(uint4& g0, uint4& g1, uint32_t addr, uint32_t flag) {
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %8, 0;\n\t"
+        "@p ld.shared.v4.u32 {%0, %1, %2, %3}, [%9];\n\t"
+        "@p ld.shared.v4.u32 {%4, %5, %6, %7}, [%9+256];\n\t}"
+        : "+r"(g0.x), "+r"(g0.y), "+r"(g0.z), "+r"(g0.w), "+r"(g1.x), "+r"(g1.y), "+r"(g1.z), "+r"(g1.w)
+        : "r"(flag), "r"(addr));
+}
 
 // Compiler-level pin: every partial (hence every load feeding it) is computed before this point.
 __device__ __forceinline__ void w_pin(const uint64_t (&part)[kWFW][kWXW][2]) {
@@ -353,10 +361,8 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
                     // lo = weight of the even row, hi = even / odd row (bits 0-7 / 8-15), load flags, 1.0f bits
                     const uint32_t lo = k ? e2.z : e2.x, hi = k ? e2.w : e2.y;
                     const uint32_t ra = gaddr + ((hi & 0xFFu) << 9), rb = gaddr + ((hi >> 8 & 0xFFu) << 9);
-                    w_lds_if(ga[0], ra, hi & 0x10000u);
-                    w_lds_if(ga[1], ra + 256u, hi & 0x10000u);
-                    w_lds_if(gb[0], rb, hi & 0x20000u);
-                    w_lds_if(gb[1], rb + 256u, hi & 0x20000u);
+                    w_lds2_if(ga[0], ga[1], ra, hi & 0x10000u);
+                    w_lds2_if(gb[0], gb[1], rb, hi & 0x20000u);
                     const float wa = __uint_as_float(lo);
                     const float wb = __uint_as_float(hi & kWOne) - wa;
                     w_taps(part[0][i + k], wa, ga[0], wb, gb[0]);
