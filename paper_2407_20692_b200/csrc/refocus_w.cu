@@ -75,7 +75,7 @@ constexpr uint32_t kWInvalid = 0xFFFFFFFFu;        // 32-bit (j0 | t) table: ski
 // two row registers, slot A for the even and slot B for the odd stage row of the pair (j0, j0 + 1):
 //   lo = weight of the even row (1 - t if j0 - span_lo is even, else t; fp32, exact), 0 for a
 //        skipped sample;
-//   hi = even row (bits 0-7) | odd row (bits 8-15) | load slot A (bit 16) | load slot B (bit 17) |
+//   hi = 2 x even row (byte 0) | 2 x odd row (byte 1) | load slot A (bit 16) | load slot B (bit 17) |
 //        the bits of 1.0f (0x3F800000, bits 23-29) for a used sample, so the odd row's weight is
 //        float(hi & 0x3F800000) - lo, exactly (and 0 - 0 = 0 for a skipped sample: its taps add
 //        exact zeros).  A row already in its slot is not reloaded.
@@ -83,6 +83,8 @@ constexpr uint32_t kWOne = 0x3F800000u;
 constexpr uint32_t kWTmemCols = 512;
 
 static_assert(kWSmem <= 232448, "stage-1 window kernel exceeds the 227 KB shared-memory limit");
+static_assert(2 * (kWRows - 1) < 256, "step entries keep 2 x row in one byte");
+static_assert(kWRowBytes == 512, "step entries encode a row's offset as 2 x row << 8");
 static_assert(kWWarps * kWXW == kWX * (kWF / kWFW), "warps x outputs x planes must cover the tile");
 static_assert(kWWarps * kWFW * kWXW * 4 * 2 <= 4 * 128 * 32 * 4, "fp64 accumulators exceed TMEM");
 
@@ -360,7 +362,8 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
                 for (int k = 0; k < 2; ++k) {
                     // lo = weight of the even row, hi = even / odd row (bits 0-7 / 8-15), load flags, 1.0f bits
                     const uint32_t lo = k ? e2.z : e2.x, hi = k ? e2.w : e2.y;
-                    const uint32_t ra = gaddr + ((hi & 0xFFu) << 9), rb = gaddr + ((hi >> 8 & 0xFFu) << 9);
+                    // byte k of hi (2 x row) moved to byte 1 = the row's 512-B offset (one PRMT each)
+                    const uint32_t ra = gaddr + __byte_perm(hi, 0u, 0x4404u), rb = gaddr + __byte_perm(hi, 0u, 0x4414u);
                     w_lds2_if(ga[0], ga[1], ra, hi & 0x10000u);
                     w_lds2_if(gb[0], gb[1], rb, hi & 0x20000u);
                     const float wa = __uint_as_float(lo);
@@ -494,7 +497,7 @@ __global__ void pack_w_steps_kernel(const uint32_t* __restrict__ ent, const int2
             ra = re;
             rb = ro;
             s2.x = __float_as_uint(ev ? 1.f - t : t);                     // exact
-            s2.y = static_cast<uint32_t>(re) | (static_cast<uint32_t>(ro) << 8) | (la << 16) | (lb << 17) | kWOne;
+            s2.y = static_cast<uint32_t>(2 * re) | (static_cast<uint32_t>(2 * ro) << 8) | (la << 16) | (lb << 17) | kWOne;
         }
         steps[base + i] = s2;
     }
