@@ -98,6 +98,20 @@ def load_traffic():
     return {}
 
 
+def issue_view(prof, ms_per_launch, f_clk):
+    """Issue-slot and shared-memory views of a kernel from its committed ncu capture: the capture's
+    warp instructions and shared-memory wavefronts per launch over this run's live launch time,
+    against 4 warp instructions and 1 wavefront per clock per SM (148 SMs, this run's median clock)."""
+    inst, wav = prof.get("warp_instructions_per_launch"), prof.get("smem_wavefronts_per_launch")
+    if not inst or not ms_per_launch:
+        return None
+    slots = 148 * f_clk * ms_per_launch / 1e3
+    return {"issue_frac": inst / (4 * slots), "smem_wavefront_frac": wav / slots if wav else None,
+            "warp_instructions_per_launch": inst, "smem_wavefronts_per_launch": wav,
+            "source": prof.get("source"),
+            "note": "counts from the ncu capture named in source, time from this run"}
+
+
 def load_peaks():
     try:
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
@@ -546,6 +560,7 @@ def main():
                "hbm_view": {"algorithmic_bytes_per_step": span, "achieved_gbs": s1_gbs, "peak_gbs": hbm,
                             "frac": s1_gbs / hbm if s1_gbs else None,
                             "note": "per-plane span bytes / time; > 1 possible because planes share HBM passes"},
+               "issue_view": issue_view(traffic.get(s1_key, {}), s1_ms / args.steps, f_clk),
                "traffic": traffic.get(s1_key, {}).get("bytes_per_launch"),
                "traffic_note": (f"ncu dram read + write bytes per launch of {s1_key} (profiles/r02_traffic.json); "
                                 + ("one launch per step" if vm else "achieved is per step (16 launches)"))}

@@ -85,7 +85,8 @@ struct cpi_ctx {
     bool refocus_ready = false;
     int fuse = 4;                          // planes per Gamma pass in the TMA stage 1 (CPI_REFOCUS_FUSE)
     uint32_t* xpack = nullptr;             // packed x-tables [kS1Planes][W_b][W_a]
-    uint32_t* ypack = nullptr;             // packed y-tables [kRefocusMaxFuse][H_b][H_a]
+    float* xwpack = nullptr;               // their near-t corner offsets [kS1Planes][W_b][W_a]
+    uint2* ypack = nullptr;                // packed y-tables [kRefocusMaxFuse][H_b][H_a]
     uint32_t* xblk = nullptr;              // x-block masks [kS1Planes][W_b / 8]
     bool use_s2_staged = false;
     cpi::Stage1Maps s1maps{};
@@ -100,10 +101,10 @@ struct cpi_ctx {
     const int32_t** w_ylo = nullptr;
     const int32_t** w_yhi = nullptr;
     uint32_t* w_ent = nullptr;             // [batch][W_b][x_pad] (j0 | t)
-    uint2* w_steps = nullptr;              // [batch][W_b][x_pad] step entries
+    uint4* w_steps = nullptr;              // [batch][W_b][x_pad / 8] walk entries (80 B; 16 B per x allocated)
     int2* w_span = nullptr;                // [groups][x tiles][W_b]
     int2* w_mband = nullptr;               // [groups][v blocks]
-    uint32_t* w_ypack = nullptr;           // [batch][H_b][H_a]
+    uint2* w_ypack = nullptr;              // [batch][H_b][H_a]
     cpi::TElem* w_T = nullptr;             // [batch][W_a][H_a][H_b]
     // frame-sharded multi-GPU mode (cfg.world >= 2): library-owned NCCL communicator and shard plan
     int world = 1, rank = 0;
@@ -253,6 +254,7 @@ void free_all(cpi_ctx* c) {
     }
     for (auto* t : {&c->gen_x, &c->gen_y}) { cudaFree(t->a0); cudaFree(t->at); cudaFree(t->b0); cudaFree(t->bt); cudaFree(t->cnt); }
     cudaFree(c->xpack);
+    cudaFree(c->xwpack);
     cudaFree(c->ypack);
     cudaFree(c->xblk);
     cudaFree(c->gamma_ws);
@@ -418,10 +420,10 @@ cpi_status refocus_vmajor(cpi_ctx* c, const cpi_refocus_spec* spec, float* plane
         CK(c, cudaMemcpy(c->w_ylo, h.data() + 2 * nb, sizeof(void*) * nb, cudaMemcpyHostToDevice));
         CK(c, cudaMemcpy(c->w_yhi, h.data() + 3 * nb, sizeof(void*) * nb, cudaMemcpyHostToDevice));
         CK(c, cudaMalloc(&c->w_ent, sizeof(uint32_t) * nb * Wb * xpad));
-        CK(c, cudaMalloc(&c->w_steps, sizeof(uint2) * nb * Wb * xpad));
+        CK(c, cudaMalloc(&c->w_steps, sizeof(uint4) * nb * Wb * xpad));
         CK(c, cudaMalloc(&c->w_span, sizeof(int2) * n_g * n_xt * Wb));
         CK(c, cudaMalloc(&c->w_mband, sizeof(int2) * n_g * n_vb));
-        CK(c, cudaMalloc(&c->w_ypack, sizeof(uint32_t) * size_t(nb) * Hb * Ha));
+        CK(c, cudaMalloc(&c->w_ypack, sizeof(uint2) * size_t(nb) * Hb * Ha));
         CK(c, cudaMalloc(&c->w_T, sizeof(cpi::TElem) * size_t(nb) * Wa * Ha * Hb));
         c->w_batch = nb;
         c->w_ready = true;
@@ -524,9 +526,10 @@ cpi_status refocus_vmajor(cpi_ctx* c, const cpi_refocus_spec* spec, float* plane
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
                 if (r != CUDA_SUCCESS) return fail(c, CPI_ERR_CUDA, "Gamma tensor map (v-major) failed (%d)", int(r));
                 const int64_t xpad = (Wa + cpi::stage1_w_xtile() - 1) / cpi::stage1_w_xtile() * cpi::stage1_w_xtile();
-                const cuuint64_t ed[3] = {cuuint64_t(2 * xpad), cuuint64_t(Wb), cuuint64_t(nb)};
-                const cuuint64_t est[2] = {cuuint64_t(2 * xpad) * 4, cuuint64_t(2 * xpad) * Wb * 4};
-                const cuuint32_t eb[3] = {cuuint32_t(2 * cpi::stage1_w_xtile()), 1u, cuuint32_t(cpi::stage1_w_group())};
+                // walk entries: 20 words per 8 outputs (refocus_w.cu)
+                const cuuint64_t ed[3] = {cuuint64_t(xpad / 8 * 20), cuuint64_t(Wb), cuuint64_t(nb)};
+                const cuuint64_t est[2] = {cuuint64_t(xpad / 8 * 20) * 4, cuuint64_t(xpad / 8 * 20) * Wb * 4};
+                const cuuint32_t eb[3] = {cuuint32_t(cpi::stage1_w_xtile() / 8 * 20), 1u, cuuint32_t(cpi::stage1_w_group())};
                 const cuuint32_t es3[3] = {1u, 1u, 1u};
                 r = enc(&te, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, c->w_steps, ed, est, eb, es3, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1455,11 +1458,13 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
         if (c->fuse > cpi::kRefocusMaxFuse) c->fuse = cpi::kRefocusMaxFuse;
         c->use_s2_staged = cpi::stage2_staged_supported(Ha) && getenv("CPI_STAGE2_SIMPLE") == nullptr;
         if (c->use_s2_staged)
-            CK(c, cudaMalloc(&c->ypack, sizeof(uint32_t) * size_t(Ha) * Hb * cpi::kRefocusMaxFuse));
+            CK(c, cudaMalloc(&c->ypack, sizeof(uint2) * size_t(Ha) * Hb * cpi::kRefocusMaxFuse));
         if (c->use_s1_tma) {
             constexpr int kP = cpi_ctx::kS1Planes;
             CK(c, cudaMalloc(&c->xpack, sizeof(uint32_t) * size_t(Wa) * Wb * kP));
             CK(c, cudaMemset(c->xpack, 0, sizeof(uint32_t) * size_t(Wa) * Wb * kP));
+            CK(c, cudaMalloc(&c->xwpack, sizeof(float) * size_t(Wa) * Wb * kP));
+            CK(c, cudaMemset(c->xwpack, 0, sizeof(float) * size_t(Wa) * Wb * kP));
             CK(c, cudaMalloc(&c->xblk, sizeof(uint32_t) * size_t((Wb + 7) / 8) * kP));
             cpi::EncodeTiledFn enc = cpi::encode_tiled_fn();
             if (!enc) return fail(c, CPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
@@ -1627,7 +1632,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
                 c->launches += 2;
                 if (e == cudaSuccess && tma_now) {
                     e = cpi::launch_pack_xtable_group(c->xs + g0, nf, Wa, Wb, c->xpack + int64_t(g0) * Wa * Wb,
-                                                      c->xblk + g0 * nch, st);
+                                                      c->xwpack + int64_t(g0) * Wa * Wb, c->xblk + g0 * nch, st);
                     c->launches += 1;
                 }
             }
@@ -1654,7 +1659,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
                 c->launches += 1;
             } else if (tma_now) {
                 e = cpi::launch_refocus_stage1_tma(&c->s1maps, nb, Wa, Ha, Wb, Hb, m_base, m_count, m_block, m_stride,
-                                                   c->xs, c->ys, c->T, c->xblk, c->num_sms, st);
+                                                   c->xs, c->ys, c->T, c->xblk, c->xwpack, c->num_sms, st);
                 c->launches += 1;
             } else if (!cyclic) {
                 e = cpi::launch_refocus_stage1(gsrc, c->p_b, Wa, Ha, Wb, Hb, m_base, m_count, c->xs[0], c->ys[0],

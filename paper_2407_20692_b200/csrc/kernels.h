@@ -157,8 +157,8 @@ bool stage1_tma_supported(int Wa, int Wb, int Hb);
 int stage1_vgroup(int Wa);   // B rows v per stage-1 tile (Gamma tensor-map box height)
 cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa, int Ha, int Wb, int Hb,
                                       int m_base, int m_count, int m_block, int m_stride, const AxisTables* xs,
-                                      const AxisTables* ys, TElem* const* T, const uint32_t* xblk, int num_sms,
-                                      cudaStream_t st);
+                                      const AxisTables* ys, TElem* const* T, const uint32_t* xblk, const float* xw,
+                                      int num_sms, cudaStream_t st);
 // x-tables of a fused group packed for the TMA stage 1: uint32 j_rel << 23 | round(t * 2^23),
 // [n_fuse][Wb][Wa] (see refocus.cu), and xblk[n_fuse][ceil(Wb / 8)]: bit b set if some
 // x in [16 b, 16 b + 16) has a used sample for some u of the 8-column chunk.
@@ -168,7 +168,7 @@ struct PackGroupArgs {
     const double* t[kRefocusMaxFuse];
     const int32_t* lo[kRefocusMaxFuse];
 };
-cudaError_t launch_pack_xtable_group(const AxisTables* xs, int n_fuse, int Wa, int Wb, uint32_t* xpack,
+cudaError_t launch_pack_xtable_group(const AxisTables* xs, int n_fuse, int Wa, int Wb, uint32_t* xpack, float* xwpack,
                                      uint32_t* xblk, cudaStream_t st);
 // General maps with output-dependent B coordinates (refocus_gen.cu, SPEC.md:273 with d != 0):
 // per-axis tables [n_out][n_samp] of both supports, then two image-sampling stages.
@@ -213,7 +213,7 @@ int stage1_w_jbox();       // j rows per Gamma box
 int stage1_w_max_span();   // staged j rows per stage (plane groups with a longer span use refocus.cu)
 cudaError_t launch_pack_w(const int32_t* const* i0s_dev, const double* const* ts_dev, const int32_t* const* ylo_dev,
                           const int32_t* const* yhi_dev, int n_planes, int Wa, int Wb, int Hb, uint32_t* ent,
-                          uint2* steps, int2* span, int2* mband, cudaStream_t st);
+                          uint4* steps, int2* span, int2* mband, cudaStream_t st);
 cudaError_t launch_refocus_stage1_w(const CUtensorMap* tm_gamma, const CUtensorMap* tm_ent, const S1WArgs& a,
                                     int num_sms, cudaStream_t st);
 // driver entry point cuTensorMapEncodeTiled (nullptr if unavailable)
@@ -231,11 +231,11 @@ cudaError_t launch_refocus_stage2(const TElem* T, int Wa, int Ha, int Hb, int m_
 // staged stage 2 (KB6'): one launch for n_fuse planes written to planes[f * Ha * Wa]; rows of
 // T outside the shard count as 0.  Needs the packed y-tables [n_fuse][Hb][Ha] (H_a <= 256).
 bool stage2_staged_supported(int Ha);
-cudaError_t launch_pack_ytable_group(const AxisTables* ys, int n_fuse, int Ha, int Hb, uint32_t* ypack,
+cudaError_t launch_pack_ytable_group(const AxisTables* ys, int n_fuse, int Ha, int Hb, uint2* ypack,
                                      cudaStream_t st);
 cudaError_t launch_refocus_stage2_group(TElem* const* T, int n_fuse, int Wa, int Ha, int Hb, int m_base, int m_count,
                                         int m_block, int m_stride, const AxisTables* xs, const AxisTables* ys,
-                                        const uint32_t* ypack, float* planes, cudaStream_t st);
+                                        const uint2* ypack, float* planes, cudaStream_t st);
 
 // NCCL entry points, resolved from libnccl.so.2 at run time (comm.cu); nullptr if unavailable.
 struct NcclApi {

@@ -189,8 +189,11 @@ stage1_kernel(const float* __restrict__ gamma, int64_t ldg, int Wa, int Ha, int 
                 const int64_t ti = static_cast<int64_t>(u0 + k) * Wa + x;
                 const int j0 = __ldg(xs.i0 + ti);
                 if (j0 < 0) continue;
-                const float t = static_cast<float>(__ldg(xs.t + ti));
-                const float w0 = 1.f - t;
+                // both corner weights rounded once from fp64 (the small one keeps its relative
+                // precision)
+                const double td = __ldg(xs.t + ti);
+                const float t = __double2float_rn(td);
+                const float w0 = __double2float_rn(1.0 - td);
                 const float* s0 = sm + (j0 - jlo) * kPad + k;
 #pragma unroll
                 for (int v = 0; v < kVG; ++v) {
@@ -281,13 +284,17 @@ __device__ __forceinline__ uint64_t ffma2(float, uint64_t g, uint64_t c, uint64_
 }
 
 // The 8 taps of one packed x-table entry for one lane: 4 v slots x 2 corners, as FFMA2 pairs
-// (lane-wise identical to scalar fmaf in the same order).  entry = j_rel << 23 | round(t * 2^23),
-// j_rel = smem row of j0 relative to the chunk's staged span (256 = zero rows: skipped, t = 0).
+// (lane-wise identical to scalar fmaf in the same order).  entry = j_rel << 23 (| a 2^-23 t the
+// taps do not use), j_rel = smem row of j0 relative to the chunk's staged span (the zero rows for
+// a skipped sample); sn = the sample's corner offset in the near-t form of the weight table
+// (t for t <= 1/2, -(1 - t) above, 0 for a skipped sample), so both weights keep their relative
+// precision (a t on the 2^-23 grid erred by up to 2^-24 |Gamma(j0 + 1) - Gamma(j0)|).
 template <int NS, int kRow>
-__device__ __forceinline__ void s1_taps(uint64_t (&part)[NS / 2], uint32_t e, const float* Gu, const int (&voff)[NS]) {
-    const float one_t = __int_as_float((e & 0x7FFFFFu) | 0x3F800000u);   // 1 + t
-    const float t = one_t - 1.f;
-    const float w0 = 2.f - one_t;
+__device__ __forceinline__ void s1_taps(uint64_t (&part)[NS / 2], uint32_t e, float sn, const float* Gu,
+                                        const int (&voff)[NS]) {
+    const bool up = signbit(sn);
+    const float w0 = up ? -sn : 1.f - sn;
+    const float t = up ? 1.f + sn : sn;
     const float* gp = Gu + (e >> 23) * kRow;
     const uint64_t t2 = pack_f32x2(t, t), w2 = pack_f32x2(w0, w0);
 #pragma unroll
@@ -327,6 +334,7 @@ struct S1Args {
     const int32_t* yhi[kRefocusMaxFuse];
     TElem* T[kRefocusMaxFuse];
     const uint32_t* xblk;                    // [F][n_chunks] x-block masks (OR-ed over F in smem)
+    const float* xw;                         // [F][W_b][W_a] near-t corner offsets (s1_taps)
     int gamma_5d;                            // Gamma map is 5D u-blocked (u%8, v, u/8, j, m)
 };
 
@@ -485,29 +493,40 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                     if (!kFullX && xbase + 128 * i >= a.Wa) continue;
                     // all x-table entries of this x block first, so entry decode overlaps taps
                     uint32_t ent[kTUC][F];
+                    float sn[kTUC][F];
 #pragma unroll
-                    for (int k = 0; k < kTUC; ++k)
+                    for (int k = 0; k < kTUC; ++k) {
+                        const int uu = (k + xl) & (kTUC - 1), u = c * kTUC + uu;
 #pragma unroll
-                        for (int f = 0; f < F; ++f)
-                            ent[k][f] = sxs[f * C::kXEntries + ((k + xl) & (kTUC - 1)) * a.Wa + 128 * i];
+                        for (int f = 0; f < F; ++f) {
+                            ent[k][f] = sxs[f * C::kXEntries + uu * a.Wa + 128 * i];
+                            sn[k][f] = u < a.Wb && xbase + 128 * i < a.Wa
+                                           ? __ldg(a.xw + (static_cast<int64_t>(f) * a.Wb + u) * a.Wa + xbase + 128 * i)
+                                           : 0.f;
+                        }
+                    }
 #pragma unroll
                     for (int k = 0; k < kTUC; ++k) {
                         const int uu = (k + xl) & (kTUC - 1);
 #pragma unroll
-                        for (int f = 0; f < F; ++f) s1_taps<NS, C::kRow>(part[f][i], ent[k][f], G + uu, voff);
+                        for (int f = 0; f < F; ++f) s1_taps<NS, C::kRow>(part[f][i], ent[k][f], sn[k][f], G + uu, voff);
                     }
                 }
             } else {
 #pragma unroll
                 for (int k = 0; k < kTUC; ++k) {
-                    const int uu = (k + xl) & (kTUC - 1);
+                    const int uu = (k + xl) & (kTUC - 1), u = c * kTUC + uu;
 #pragma unroll
                     for (int f = 0; f < F; ++f)
 #pragma unroll
                         for (int i = 0; i < NI; ++i)
-                            if (kFullX || xbase + 128 * i < a.Wa)
-                                s1_taps<NS, C::kRow>(part[f][i], sxs[f * C::kXEntries + uu * a.Wa + 128 * i], G + uu,
-                                                     voff);
+                            if (kFullX || xbase + 128 * i < a.Wa) {
+                                const float sn = u < a.Wb ? __ldg(a.xw + (static_cast<int64_t>(f) * a.Wb + u) * a.Wa +
+                                                                  xbase + 128 * i)
+                                                          : 0.f;
+                                s1_taps<NS, C::kRow>(part[f][i], sxs[f * C::kXEntries + uu * a.Wa + 128 * i], sn,
+                                                     G + uu, voff);
+                            }
                 }
             }
             // Release the stage to the TMA producer.  The reads above are generic-proxy loads and
@@ -547,7 +566,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
 // 1 moves to the next row with t = 0), and skipped samples point at the zero rows
 // (j_rel = zrow = the stage's row capacity, t = 0).  t keeps 2^-23 resolution; t = 0 stays exact.
 __global__ void pack_xtable_group_kernel(PackGroupArgs g, int Wa, int Wb, uint32_t zrow, uint32_t* __restrict__ out,
-                                         uint32_t* __restrict__ xblk) {
+                                         float* __restrict__ outw, uint32_t* __restrict__ xblk) {
     const int c = blockIdx.x, f = blockIdx.y, c0 = c * 8, n_chunks = gridDim.x;
     __shared__ uint32_t sblk;
     if (threadIdx.x == 0) sblk = 0;
@@ -561,14 +580,16 @@ __global__ void pack_xtable_group_kernel(PackGroupArgs g, int Wa, int Wb, uint32
             const int64_t idx = static_cast<int64_t>(u) * Wa + x;
             const int j = __ldg(g.i0[f] + idx);
             uint32_t e = zrow << 23;
+            float sn = 0.f;
             if (j >= 0) {
-                uint32_t tq = static_cast<uint32_t>(__double2uint_rn(__ldg(g.t[f] + idx) * 8388608.0));
-                int jr = j - jlo;
-                if (tq >= 8388608u) { tq = 0; jr += 1; }
-                e = (static_cast<uint32_t>(jr) << 23) | tq;
+                const double t = __ldg(g.t[f] + idx);
+                e = static_cast<uint32_t>(j - jlo) << 23;
+                // near-t form (s1_taps): -(1 - t) is exact in fp64 for t > 1/2; t = 1 -> -0.0
+                sn = __double2float_rn(t > 0.5 ? -(1.0 - t) : t);
                 used = true;
             }
             out[(static_cast<int64_t>(f) * Wb + u) * Wa + x] = e;
+            outw[(static_cast<int64_t>(f) * Wb + u) * Wa + x] = sn;
         }
         if (used) atomicOr(&sblk, 1u << (x >> 4));
     }
@@ -595,7 +616,7 @@ struct S2Args {
     const int32_t* ycnt[kS2MaxPlanes];
     const int32_t* ylo[kS2MaxPlanes];
     const int32_t* yhi[kS2MaxPlanes];
-    const uint32_t* ypack;                       // [F][H_b][H_a]
+    const uint2* ypack;                          // [F][H_b][H_a] (m_near, delta) entries
     float* plane[kS2MaxPlanes];
 };
 
@@ -605,16 +626,16 @@ stage2_staged_kernel(S2Args a) {
     const int f = blockIdx.y, x0 = blockIdx.x * kS2XB;
     const int Ha = a.Ha, Hb = a.Hb, P = Ha + 2;           // staged row pitch (rows Ha, Ha+1 = 0)
     TElem* ts = reinterpret_cast<TElem*>(s2_smem);                       // [kS2XB][kS2VC][P]
-    uint32_t* tab = reinterpret_cast<uint32_t*>(ts + kS2XB * kS2VC * P);  // [kS2VC][Ha]
+    uint2* tab = reinterpret_cast<uint2*>(ts + kS2XB * kS2VC * P);        // [kS2VC][Ha]
     const TElem* T = a.T[f];
-    const uint32_t* yp = a.ypack + static_cast<int64_t>(f) * Hb * Ha;
+    const uint2* yp = a.ypack + static_cast<int64_t>(f) * Hb * Ha;
     const int32_t* ylo = a.ylo[f];
     const int32_t* yhi = a.yhi[f];
     for (int i = threadIdx.x; i < kS2XB * kS2VC * 2; i += blockDim.x) ts[(i >> 1) * P + Ha + (i & 1)] = 0.f;
     // loader role: thread = (vv = tid % 8, m = tid / 8 + 32 k), both x of the CTA
     const int vl = threadIdx.x & (kS2VC - 1), ml = threadIdx.x / kS2VC;
     TElem pre[kS2XB][kS2MI];
-    uint32_t ptab[kS2MI];
+    uint2 ptab[kS2MI];
     uint32_t present = 0;                          // bit k: this thread's row m = ml + 32 k is in the shard
 #pragma unroll
     for (int k = 0; k < kS2MI; ++k) {
@@ -638,7 +659,7 @@ stage2_staged_kernel(S2Args a) {
                 pre[xb][k] = ok && x < a.Wa ? __ldg(T + (static_cast<int64_t>(x) * Ha + m) * Hb + v) : 0.f;
             }
             const int i = threadIdx.x + k * kS2Threads;               // table entry (vv, y)
-            ptab[k] = i < nvalid ? __ldg(yp + static_cast<int64_t>(v0) * Ha + i) : (static_cast<uint32_t>(Ha) << 23);
+            ptab[k] = i < nvalid ? __ldg(yp + static_cast<int64_t>(v0) * Ha + i) : make_uint2(static_cast<uint32_t>(Ha), 0u);
         }
     };
     double sum[kS2XB];
@@ -663,13 +684,18 @@ stage2_staged_kernel(S2Args a) {
         if (y < Ha) {
 #pragma unroll
             for (int vv = 0; vv < kS2VC; ++vv) {
-                const uint32_t e = tab[vv * Ha + y];
-                const int m0 = static_cast<int>(e >> 23);
-                const float t = static_cast<float>(e & 0x7FFFFFu) * (1.f / 8388608.f);   // exact
+                // entry = (nearest row m_near, delta = c - m_near in fp32): the small weight |delta|
+                // is exact to 2^-24 relative, the large one 1 - |delta| >= 1/2 likewise, so each
+                // corner's weight carries a relative error <= 2^-24
+                const uint2 e = tab[vv * Ha + y];
+                const float d = __uint_as_float(e.y), s = fabsf(d), big = 1.f - s;
+                const bool below = d < 0.f;   // c lies in [m_near - 1, m_near]
+                const int m0 = static_cast<int>(e.x) - (below ? 1 : 0);
+                const float w0 = below ? s : big, w1 = below ? big : s;
 #pragma unroll
                 for (int xb = 0; xb < kS2XB; ++xb) {
                     const TElem* row = ts + (xb * kS2VC + vv) * P + m0;
-                    sum[xb] += static_cast<double>(fmaf(t, row[1] - row[0], row[0]));
+                    sum[xb] += static_cast<double>(fmaf(w1, row[1], w0 * row[0]));
                 }
             }
         }
@@ -686,19 +712,22 @@ stage2_staged_kernel(S2Args a) {
     }
 }
 
-// Packed y-tables of a group: entry(f, v, y) = m0 << 23 | round(t * 2^23); skipped samples
-// point at the zero rows (m0 = H_a, t = 0); a t that rounds to 1 moves to m0 + 1 with t = 0.
-__global__ void pack_ytable_kernel(PackGroupArgs g, int Ha, int Hb, uint32_t* __restrict__ out) {
+// Packed y-tables of a group: entry(f, v, y) = (m_near, delta) with c = i0 + t, m_near = i0 and
+// delta = t for t <= 1/2, else m_near = i0 + 1 and delta = t - 1 (exact in fp64), delta rounded
+// once to fp32 -- relative, not absolute, precision for the small corner weight (a fixed-point t
+// on a 2^-23 grid loses it when t or 1 - t is tiny: |error| up to 2^-24 |T(i0 + 1) - T(i0)|,
+// beyond 1e-6 M when the two corners differ widely).  Skipped samples point at the zero rows
+// (m_near = H_a, delta = 0).
+__global__ void pack_ytable_kernel(PackGroupArgs g, int Ha, int Hb, uint2* __restrict__ out) {
     const int v = blockIdx.x, f = blockIdx.y;
     for (int y = threadIdx.x; y < Ha; y += blockDim.x) {
         const int64_t idx = static_cast<int64_t>(v) * Ha + y;
         const int m0 = __ldg(g.i0[f] + idx);
-        uint32_t e = static_cast<uint32_t>(Ha) << 23;
+        uint2 e = make_uint2(static_cast<uint32_t>(Ha), 0u);
         if (m0 >= 0) {
-            uint32_t tq = static_cast<uint32_t>(__double2uint_rn(__ldg(g.t[f] + idx) * 8388608.0));
-            int mr = m0;
-            if (tq >= 8388608u) { tq = 0; mr += 1; }
-            e = (static_cast<uint32_t>(mr) << 23) | tq;
+            const double t = __ldg(g.t[f] + idx);
+            const bool up = t > 0.5;
+            e = make_uint2(static_cast<uint32_t>(m0 + (up ? 1 : 0)), __float_as_uint(__double2float_rn(up ? t - 1.0 : t)));
         }
         out[(static_cast<int64_t>(f) * Hb + v) * Ha + y] = e;
     }
@@ -754,8 +783,9 @@ stage1_genb_kernel(const float* __restrict__ gamma, int64_t ldg, int Wa, int Ha,
                     const int64_t ti = static_cast<int64_t>(u) * Wa + x;
                     const int j0 = __ldg(xs.i0 + ti);
                     if (j0 < 0) continue;
-                    const float t = static_cast<float>(__ldg(xs.t + ti)), w0 = 1.f - t;
-                    const float tk = static_cast<float>(__ldg(bx.t + u)), wk0 = 1.f - tk;
+                    const double td = __ldg(xs.t + ti), tkd = __ldg(bx.t + u);
+                    const float t = __double2float_rn(td), w0 = __double2float_rn(1.0 - td);
+                    const float tk = __double2float_rn(tkd), wk0 = __double2float_rn(1.0 - tkd);
                     const int kk = __ldg(bx.i0 + u) - klo;
                     const float* s0 = sgb + (j0 - jlo) * kGbPad + kk;
 #pragma unroll
@@ -913,7 +943,7 @@ resample_b_band_kernel(const float* __restrict__ src, float* __restrict__ dst, i
     extern __shared__ float4 rs_sm4[];
     float* s_g = reinterpret_cast<float*>(rs_sm4);   // [kRsCap][pitch]
     __shared__ int s_vr[kRsV];                       // support row of v0 + i, relative to lo
-    __shared__ float s_vt[kRsV];
+    __shared__ float s_vt[kRsV], s_vw[kRsV];         // its weights t and 1 - t (each rounded once)
     const int pitch = rs_pitch(Wb);
     const int64_t pb = static_cast<int64_t>(Wb) * Hb;
     const int64_t p = blockIdx.x;
@@ -922,22 +952,26 @@ resample_b_band_kernel(const float* __restrict__ src, float* __restrict__ dst, i
     const int lo = min(na, nz), rows = max(na, nz) + 2 - lo;   // support rows [lo, lo + rows)
     if (threadIdx.x < nv) {
         s_vr[threadIdx.x] = (__ldg(byi + v0 + threadIdx.x) - lo) * pitch;
-        s_vt[threadIdx.x] = static_cast<float>(__ldg(byt + v0 + threadIdx.x));
+        const double tvd = __ldg(byt + v0 + threadIdx.x);
+        s_vt[threadIdx.x] = __double2float_rn(tvd);
+        s_vw[threadIdx.x] = __double2float_rn(1.0 - tvd);
     }
     const float* s = src + p * pb;
     if (rows > cap) {   // cannot happen for the host's cap; kept as a safe global-memory path
         for (int w = threadIdx.x; w < nv * Wb; w += 256) {
             const int v = v0 + w / Wb, u = w % Wb;
             const int n = __ldg(byi + v), k = __ldg(bxi + u);
-            const float tu = static_cast<float>(__ldg(bxt + u)), tv = static_cast<float>(__ldg(byt + v));
+            const double tud = __ldg(bxt + u), tvd = __ldg(byt + v);
+            const float tu = __double2float_rn(tud), wu = __double2float_rn(1.0 - tud);
+            const float tv = __double2float_rn(tvd), wv = __double2float_rn(1.0 - tvd);
             auto at = [&](int nn, int kk) {
                 return __ldg(s + (kUB ? static_cast<int64_t>(kk >> 3) * 8 * Hb + 8 * nn + (kk & 7)
                                       : static_cast<int64_t>(nn) * Wb + kk));
             };
-            const float a = fmaf(tu, at(n, k + 1), (1.f - tu) * at(n, k));
-            const float b = fmaf(tu, at(n + 1, k + 1), (1.f - tu) * at(n + 1, k));
+            const float a = fmaf(tu, at(n, k + 1), wu * at(n, k));
+            const float b = fmaf(tu, at(n + 1, k + 1), wu * at(n + 1, k));
             dst[p * pb + (kUB ? static_cast<int64_t>(u >> 3) * 8 * Hb + 8 * v + (u & 7) : static_cast<int64_t>(v) * Wb + u)] =
-                fmaf(tv, b - a, a);
+                fmaf(tv, b, wv * a);
         }
         return;
     }
@@ -961,17 +995,18 @@ resample_b_band_kernel(const float* __restrict__ src, float* __restrict__ dst, i
     float* d = dst + p * pb;
     for (int u = threadIdx.x; u < Wb; u += 256) {
         const int k = __ldg(bxi + u);
-        const float tu = static_cast<float>(__ldg(bxt + u)), wu = 1.f - tu;
+        const double tud = __ldg(bxt + u);
+        const float tu = __double2float_rn(tud), wu = __double2float_rn(1.0 - tud);
         const float* col = s_g + k;
         float* o = d + (kUB ? static_cast<int64_t>(u >> 3) * 8 * Hb + 8 * v0 + (u & 7) : static_cast<int64_t>(v0) * Wb + u);
         const int ostep = kUB ? 8 : Wb;
 #pragma unroll 4
         for (int i = 0; i < nv; ++i) {
             const float* r0 = col + s_vr[i];
-            const float tv = s_vt[i];
+            const float tv = s_vt[i], wv = s_vw[i];
             const float a = fmaf(tu, r0[1], wu * r0[0]);
             const float b = fmaf(tu, r0[pitch + 1], wu * r0[pitch]);
-            __stcs(o + i * ostep, fmaf(tv, b - a, a));
+            __stcs(o + i * ostep, fmaf(tv, b, wv * a));
         }
     }
 }
@@ -1021,7 +1056,7 @@ cudaError_t launch_resample_b(const float* src, float* dst, int64_t rows, int Wb
 
 bool stage2_staged_supported(int Ha) { return Ha >= 2 && Ha <= kS2Threads; }
 
-cudaError_t launch_pack_ytable_group(const AxisTables* ys, int n_fuse, int Ha, int Hb, uint32_t* ypack,
+cudaError_t launch_pack_ytable_group(const AxisTables* ys, int n_fuse, int Ha, int Hb, uint2* ypack,
                                      cudaStream_t st) {
     PackGroupArgs g{};
     g.n = n_fuse;
@@ -1032,7 +1067,7 @@ cudaError_t launch_pack_ytable_group(const AxisTables* ys, int n_fuse, int Ha, i
 
 cudaError_t launch_refocus_stage2_group(TElem* const* T, int n_fuse, int Wa, int Ha, int Hb, int m_base, int m_count,
                                         int m_block, int m_stride, const AxisTables* xs, const AxisTables* ys,
-                                        const uint32_t* ypack, float* planes, cudaStream_t st) {
+                                        const uint2* ypack, float* planes, cudaStream_t st) {
     if (n_fuse < 1 || n_fuse > kS2MaxPlanes || !stage2_staged_supported(Ha)) return cudaErrorInvalidValue;
     S2Args a{};
     a.Wa = Wa; a.Ha = Ha; a.Hb = Hb; a.ypack = ypack;
@@ -1043,7 +1078,7 @@ cudaError_t launch_refocus_stage2_group(TElem* const* T, int n_fuse, int Wa, int
         a.T[f] = T[f]; a.xcnt[f] = xs[f].cnt; a.ycnt[f] = ys[f].cnt; a.ylo[f] = ys[f].lo; a.yhi[f] = ys[f].hi;
         a.plane[f] = planes + static_cast<int64_t>(f) * Ha * Wa;
     }
-    const size_t smem = sizeof(TElem) * kS2XB * kS2VC * (Ha + 2) + sizeof(uint32_t) * kS2VC * Ha;
+    const size_t smem = sizeof(TElem) * kS2XB * kS2VC * (Ha + 2) + sizeof(uint2) * kS2VC * Ha;
     if (smem > 48 * 1024) {   // per-device attribute: set before every launch
         cudaError_t e = cudaFuncSetAttribute(stage2_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
@@ -1085,13 +1120,13 @@ bool stage1_tma_supported(int Wa, int Wb, int Hb) {
     return Wa <= 256 && Wa >= 4 && (Wa % 4) == 0 && (Wb % 4) == 0 && Wb <= 8 * kTMaxChunks && Hb <= 256;
 }
 
-cudaError_t launch_pack_xtable_group(const AxisTables* xs, int n_fuse, int Wa, int Wb, uint32_t* xpack,
+cudaError_t launch_pack_xtable_group(const AxisTables* xs, int n_fuse, int Wa, int Wb, uint32_t* xpack, float* xwpack,
                                      uint32_t* xblk, cudaStream_t st) {
     PackGroupArgs g{};
     g.n = n_fuse;
     for (int f = 0; f < n_fuse; ++f) { g.i0[f] = xs[f].i0; g.t[f] = xs[f].t; g.lo[f] = xs[f].lo; }
     pack_xtable_group_kernel<<<dim3((Wb + 7) / 8, n_fuse), Wa >= 256 ? 256 : ((Wa + 31) / 32) * 32, 0, st>>>(
-        g, Wa, Wb, static_cast<uint32_t>(stage1_rows(Wa)), xpack, xblk);
+        g, Wa, Wb, static_cast<uint32_t>(stage1_rows(Wa)), xpack, xwpack, xblk);
     return cudaGetLastError();
 }
 
@@ -1118,8 +1153,8 @@ static cudaError_t launch_s1_f(int F, const Stage1Maps* maps, const S1Args& a, i
 
 cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa, int Ha, int Wb, int Hb,
                                       int m_base, int m_count, int m_block, int m_stride, const AxisTables* xs,
-                                      const AxisTables* ys, TElem* const* T, const uint32_t* xblk, int num_sms,
-                                      cudaStream_t st) {
+                                      const AxisTables* ys, TElem* const* T, const uint32_t* xblk, const float* xw,
+                                      int num_sms, cudaStream_t st) {
     if (n_fuse < 1 || n_fuse > kRefocusMaxFuse) return cudaErrorInvalidValue;
     S1Args a{};
     a.Wa = Wa; a.Ha = Ha; a.Wb = Wb; a.Hb = Hb; a.m_base = m_base; a.m_count = m_count;
@@ -1128,6 +1163,7 @@ cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa
     a.n_vg = (Hb + stage1_vg(stage1_rows(Wa)) - 1) / stage1_vg(stage1_rows(Wa));
     a.n_chunks = (Wb + kTUC - 1) / kTUC;
     a.xblk = xblk;
+    a.xw = xw;
     a.gamma_5d = maps->gamma_5d;
     for (int f = 0; f < n_fuse; ++f) {
         a.xlo[f] = xs[f].lo; a.xhi[f] = xs[f].hi; a.ylo[f] = ys[f].lo; a.yhi[f] = ys[f].hi; a.T[f] = T[f];

@@ -22,6 +22,17 @@
 namespace cpi {
 namespace {
 
+// A corner offset t in [0, 1] is stored in fp32 as t (t <= 1/2) or -(1 - t) (exact in fp64), so
+// the smaller corner weight keeps its relative precision when rounded; gen_weights recovers
+// (1 - t, t) with each weight's relative error <= 2^-24.
+// (t = 1 is stored as -0.0: the sign bit, not the value, says which corner s belongs to.)
+__device__ __forceinline__ float gen_near_t(double t) { return __double2float_rn(t > 0.5 ? -(1.0 - t) : t); }
+__device__ __forceinline__ void gen_weights(float s, float& w0, float& w1) {
+    const bool up = signbit(s);
+    w0 = up ? -s : 1.f - s;
+    w1 = up ? 1.f + s : s;
+}
+
 constexpr int kGenMaxR = 256, kGenWin = 128, kGenPitch = kGenWin + 1;   // staged columns per window (+1 overlap)
 constexpr int kGenThreads = 256;
 
@@ -53,9 +64,9 @@ __global__ void gen_axis_kernel(GenMap mp, int WA, int WB, int boundary, GenTabl
             if (fa > static_cast<double>(WA - 2)) fa = static_cast<double>(WA - 2);
             if (fb > static_cast<double>(WB - 2)) fb = static_cast<double>(WB - 2);
             tab.a0[idx] = static_cast<int>(fa);
-            tab.at[idx] = static_cast<float>(__dadd_rn(cA, -fa));
+            tab.at[idx] = gen_near_t(__dadd_rn(cA, -fa));
             tab.b0[idx] = static_cast<int>(fb);
-            tab.bt[idx] = static_cast<float>(__dadd_rn(cB, -fb));
+            tab.bt[idx] = gen_near_t(__dadd_rn(cB, -fb));
             ++used;
         } else {
             tab.a0[idx] = -1;
@@ -124,9 +135,12 @@ __global__ void __launch_bounds__(kGenThreads) gen_sum_kernel(GenSumArgs g) {
                 if (n_win > 1 && min(b0 / kGenWin, n_win - 1) != w) continue;   // sample's window
                 const float ta = __ldg(g.tab.at + t0 + s), tb = __ldg(g.tab.bt + t0 + s);
                 const float* p = simg + a0 * pitch + (b0 - c_lo);
-                const float lo = fmaf(tb, p[1], (1.f - tb) * p[0]);
-                const float hi = fmaf(tb, p[pitch + 1], (1.f - tb) * p[pitch]);
-                sum += static_cast<double>(fmaf(ta, hi, (1.f - ta) * lo));
+                float wa0, wa1, wb0, wb1;
+                gen_weights(ta, wa0, wa1);
+                gen_weights(tb, wb0, wb1);
+                const float lo = fmaf(wb1, p[1], wb0 * p[0]);
+                const float hi = fmaf(wb1, p[pitch + 1], wb0 * p[pitch]);
+                sum += static_cast<double>(fmaf(wa1, hi, wa0 * lo));
             }
         }
     }

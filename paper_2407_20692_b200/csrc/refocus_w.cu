@@ -61,7 +61,8 @@ constexpr int kWProdRegs = 32, kWConsRegs = 112;
 constexpr int kWThreads = 32 * (kWWarps + kWProdWarps);
 constexpr int kWRowBytes = kWV * 4;                // 512 B per staged row
 constexpr int kWGBytes = kWRows * kWRowBytes;      // 72 KB of Gamma per stage
-constexpr int kWEBytes = kWF * kWX * 8;            // 2 KB of step entries per stage
+constexpr int kWWalkU4 = 5;                        // uint4 per walk: a row header + 4 x 2 steps' weights
+constexpr int kWEBytes = kWF * (kWX / kWXW) * kWWalkU4 * 16;   // 2.5 KB of walk entries per stage
 constexpr int kWStageBytes = kWGBytes + kWEBytes;
 constexpr int kWOffBar = kWStages * kWStageBytes;              // full barriers, then empty barriers
 constexpr int kWOffHdr = kWOffBar + 2 * kWStages * 8;           // stage headers (16 B each)
@@ -71,15 +72,18 @@ constexpr int kWOffSpan = (kWOffTmem + 16 + 15) / 16 * 16;      // the issuing c
 constexpr int kWOffUList = kWOffSpan + kWMaxWb * 8;                // the tile's used u, in order
 constexpr int kWSmem = kWOffUList + kWMaxWb * 4;
 constexpr uint32_t kWInvalid = 0xFFFFFFFFu;        // 32-bit (j0 | t) table: skipped sample / padding x
-// 64-bit step entry of (plane, u, x) for a warp walking its 8 outputs x in order.  The warp keeps
-// two row registers, slot A for the even and slot B for the odd stage row of the pair (j0, j0 + 1):
-//   lo = weight of the even row (1 - t if j0 - span_lo is even, else t; fp32, exact), 0 for a
-//        skipped sample;
-//   hi = 2 x even row (byte 0) | 2 x odd row (byte 1) | load slot A (bit 16) | load slot B (bit 17) |
-//        the bits of 1.0f (0x3F800000, bits 23-29) for a used sample, so the odd row's weight is
-//        float(hi & 0x3F800000) - lo, exactly (and 0 - 0 = 0 for a skipped sample: its taps add
-//        exact zeros).  A row already in its slot is not reloaded.
-constexpr uint32_t kWOne = 0x3F800000u;
+// Walk entry of (plane, u, block of 8 outputs x) for a warp walking its 8 outputs in order: 80 B.
+// The warp keeps two row registers, slot A for the even and slot B for the odd stage row of the
+// pair (j0, j0 + 1).
+//   uint4 0 (header): byte 2k = 2 x the even row of step k, byte 2k + 1 = 2 x its odd row; a
+//       row equal to the previous step's is not reloaded (a skipped sample repeats the previous
+//       rows, 0xFF before the first used one: no load);
+//   uint4 1 + q: (even weight, odd weight) of steps 2q and 2q + 1 (fp32, each rounded once from
+//       its fp64 value 1 - t or t, so the small one keeps its relative precision; 0, 0 for a
+//       skipped sample: its taps add exact zeros).
+// (A 64-bit step entry with t on a 2^-23 grid and the odd weight derived as 1 - even lost the
+// small weight's relative precision: an error up to 2^-24 |Gamma(j0 + 1) - Gamma(j0)|, beyond
+// 1e-6 M when t or 1 - t is tiny.)
 constexpr uint32_t kWTmemCols = 512;
 
 static_assert(kWSmem <= 232448, "stage-1 window kernel exceeds the 227 KB shared-memory limit");
@@ -105,17 +109,6 @@ __device__ __forceinline__ uint64_t fma2(uint64_t w, uint64_t g, uint64_t c) {
     return d;
 }
 
-// g = 16 bytes of shared memory at addr if flag != 0 (a warp-uniform predicate: no wavefront
-// when off), else unchanged
-// No "memory" clobber: the compiler may schedule these loads freely among the stage's other
-// shared loads; they cannot move above the stage's full-barrier wait (their addresses come from
-// entries loaded after it) and w_pin keeps them before the stage release.
-__device__ __forceinline__ void w_lds_if(uint4& g, uint32_t addr, uint32_t flag) {
-    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %4, 0;\n\t"
-        "@p ld.shared.v4.u32 {%0, %1, %2, %3}, [%5];\n\t}"
-        : "+r"(g.x), "+r"(g.y), "+r"(g.z), "+r"(g.w)
-        : "r"(flag), "r"(addr));
-}
 // Both 16-byte halves of one staged row (addr, addr + 256) if flag != 0, one predicate for the pair
 __device__ __forceinline__ void w_lds2_if(uint4& g0, uint4& g1, uint32_t addr, uint32_t flag) {
     asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %8, 0;\n\t"
@@ -123,6 +116,15 @@ __device__ __forceinline__ void w_lds2_if(uint4& g0, uint4& g1, uint32_t addr, u
         "@p ld.shared.v4.u32 {%4, %5, %6, %7}, [%9+256];\n\t}"
         : "+r"(g0.x), "+r"(g0.y), "+r"(g0.z), "+r"(g0.w), "+r"(g1.x), "+r"(g1.y), "+r"(g1.z), "+r"(g1.w)
         : "r"(flag), "r"(addr));
+}
+
+// The same pair load if x != y (the row offset changed since the previous step)
+__device__ __forceinline__ void w_lds2_ifne(uint4& g0, uint4& g1, uint32_t addr, uint32_t x, uint32_t y) {
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %8, %9;\n\t"
+        "@p ld.shared.v4.u32 {%0, %1, %2, %3}, [%10];\n\t"
+        "@p ld.shared.v4.u32 {%4, %5, %6, %7}, [%10+256];\n\t}"
+        : "+r"(g0.x), "+r"(g0.y), "+r"(g0.z), "+r"(g0.w), "+r"(g1.x), "+r"(g1.y), "+r"(g1.z), "+r"(g1.w)
+        : "r"(x), "r"(y), "r"(addr));
 }
 
 // Compiler-level pin: every partial (hence every load feeding it) is computed before this point.
@@ -228,7 +230,7 @@ __device__ __forceinline__ void w_produce(int2* tspan, int* ulist, WHeader* hdr,
                     uint8_t* dst = smem + s * kWStageBytes;
                     for (int b = 0; b < nb; ++b)
                         tma_load_5d(dst + b * kWBox * kWRowBytes, tm_g, &full[s], 0, u, w.vb, sp.x + b * kWBox, w.ml);
-                    tma_load_3d(dst + kWGBytes, tm_e, &full[s], 2 * w.xt * kWX, u, w.g * kWF);
+                    tma_load_3d(dst + kWGBytes, tm_e, &full[s], w.xt * (kWX / kWXW) * kWWalkU4 * 4, u, w.g * kWF);
                     ++k;
                     if (++s == kWStages) { s = 0; ph ^= 1; }
                 }
@@ -350,26 +352,29 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
         const uint32_t gaddr = smem_u32(sbase) + lane16;   // this lane's 16 bytes (4 v) of row 0, half 0
         // each 16-lane half walks its own plane; entries of planes past the batch are the TMA's zero
         // fill: zero weights (exact zero taps)
-        const uint4* Ep = E + (kWFW * wp * kWX + wx * kWXW) / 2 + lpl * (kWX / 2);
+        const uint4* Wk = E + ((kWFW * wp + lpl) * (kWX / kWXW) + wx) * kWWalkU4;   // this half's walk
         if (W_PROBE(a, 16)) {     // probe 16: no step work (ring / barrier / issue cost only)
         } else {   // window reuse (rows kept in registers, loads only when they change)
             uint4 ga[2], gb[2];   // even / odd row of the window, v halves h = 0, 1
             ga[0] = ga[1] = gb[0] = gb[1] = make_uint4(0u, 0u, 0u, 0u);
+            const uint4 hd = Wk[0];
+            uint32_t oa_prev = 0xFF00u, ob_prev = 0xFF00u;   // no rows in the slots yet
 #pragma unroll
-            for (int i = 0; i < kWXW; i += 2) {
-                const uint4 e2 = Ep[i / 2];
+            for (int q = 0; q < kWXW / 2; ++q) {
+                const uint32_t hw = q == 0 ? hd.x : q == 1 ? hd.y : q == 2 ? hd.z : hd.w;
+                const uint4 wt = Wk[1 + q];
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
-                    // lo = weight of the even row, hi = even / odd row (bits 0-7 / 8-15), load flags, 1.0f bits
-                    const uint32_t lo = k ? e2.z : e2.x, hi = k ? e2.w : e2.y;
-                    // byte k of hi (2 x row) moved to byte 1 = the row's 512-B offset (one PRMT each)
-                    const uint32_t ra = gaddr + __byte_perm(hi, 0u, 0x4404u), rb = gaddr + __byte_perm(hi, 0u, 0x4414u);
-                    w_lds2_if(ga[0], ga[1], ra, hi & 0x10000u);
-                    w_lds2_if(gb[0], gb[1], rb, hi & 0x20000u);
-                    const float wa = __uint_as_float(lo);
-                    const float wb = __uint_as_float(hi & kWOne) - wa;
-                    w_taps(part[0][i + k], wa, ga[0], wb, gb[0]);
-                    w_taps(part[1][i + k], wa, ga[1], wb, gb[1]);
+                    // byte 2k / 2k + 1 of hw (2 x row) moved to byte 1 = the row's 512-B offset
+                    const uint32_t oa = __byte_perm(hw, 0u, k ? 0x4424u : 0x4404u);
+                    const uint32_t ob = __byte_perm(hw, 0u, k ? 0x4434u : 0x4414u);
+                    w_lds2_ifne(ga[0], ga[1], gaddr + oa, oa, oa_prev);
+                    w_lds2_ifne(gb[0], gb[1], gaddr + ob, ob, ob_prev);
+                    oa_prev = oa;
+                    ob_prev = ob;
+                    const float wa = __uint_as_float(k ? wt.z : wt.x), wb = __uint_as_float(k ? wt.w : wt.y);
+                    w_taps(part[0][2 * q + k], wa, ga[0], wb, gb[0]);
+                    w_taps(part[1][2 * q + k], wa, ga[1], wb, gb[1]);
                 }
             }
         }
@@ -426,7 +431,7 @@ stage1_w_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant_
 }
 
 // ---- pack: per-plane entries, per-(group, x tile, u) spans, step entries, m bands ----------
-// entry(f, u, x) = j0 << 23 | round(t * 2^23) (a t that rounds to 1 moves to j0 + 1 with t = 0),
+// entry(f, u, x) = j0 << 23 | min(round(t * 2^23), 2^23 - 1),
 // kWInvalid for skipped samples and for the padding columns x >= W_a.
 __global__ void pack_w_entries_kernel(const int32_t* const* i0s, const double* const* ts, int Wa, int Wb, int xpad,
                                       uint32_t* __restrict__ ent) {
@@ -439,10 +444,9 @@ __global__ void pack_w_entries_kernel(const int32_t* const* i0s, const double* c
             const int64_t idx = static_cast<int64_t>(u) * Wa + x;
             const int j = __ldg(i0 + idx);
             if (j >= 0) {
-                uint32_t tq = static_cast<uint32_t>(__double2uint_rn(__ldg(tt + idx) * 8388608.0));
-                int jj = j;
-                if (tq >= 8388608u) { tq = 0; jj += 1; }
-                e = (static_cast<uint32_t>(jj) << 23) | tq;
+                // t on a 2^-23 grid for the span logic only (the step weights come from the fp64 t)
+                const uint32_t tq = min(static_cast<uint32_t>(__double2uint_rn(__ldg(tt + idx) * 8388608.0)), 8388607u);
+                e = (static_cast<uint32_t>(j) << 23) | tq;
             }
         }
         ent[(static_cast<int64_t>(f) * Wb + u) * xpad + x] = e;
@@ -474,33 +478,37 @@ __global__ void pack_w_span_kernel(const uint32_t* __restrict__ ent, int n_plane
         span[(static_cast<int64_t>(g) * n_xt + xt) * Wb + u] = hi >= lo ? make_int2(lo, hi) : make_int2(1, 0);
     }
 }
-// step entries (see kWOne): one thread per (plane, u, warp block of 8 outputs x) scans the block
-// in the warp's walk order, tracking which stage row each slot holds; rows are relative to the
-// span of (group, x tile, u).
-__global__ void pack_w_steps_kernel(const uint32_t* __restrict__ ent, const int2* __restrict__ span, int Wb, int xpad,
-                                    int n_xt, uint2* __restrict__ steps) {
+// walk entries (see the layout above): one thread per (plane, u, warp block of 8 outputs x) scans
+// the block in the warp's walk order, tracking which stage row each slot holds; rows are relative
+// to the span of (group, x tile, u).
+__global__ void pack_w_steps_kernel(const uint32_t* __restrict__ ent, const double* const* ts, const int2* __restrict__ span,
+                                    int Wa, int Wb, int xpad, int n_xt, uint4* __restrict__ steps) {
     const int u = blockIdx.x, f = blockIdx.y, blk = threadIdx.x;
     if (blk >= xpad / kWXW) return;
     const int x0 = blk * kWXW, xt = x0 / kWX, g = f / kWF;
     const int2 sp = __ldg(span + (static_cast<int64_t>(g) * n_xt + xt) * Wb + u);
     const int64_t base = (static_cast<int64_t>(f) * Wb + u) * xpad + x0;
-    int ra = -1, rb = -1;   // stage rows in slots A (even) and B (odd)
+    uint32_t ra = 0xFFu, rb = 0xFFu;   // 2 x stage row in slots A (even) and B (odd); 0xFF: none yet
+    uint32_t hdr[4] = {0u, 0u, 0u, 0u};
+    uint32_t w[kWXW][2];
     for (int i = 0; i < kWXW; ++i) {
         const uint32_t e = __ldg(ent + base + i);
-        uint2 s2 = make_uint2(0u, 0u);
+        w[i][0] = w[i][1] = 0u;
         if (e != kWInvalid) {
             const int r0 = static_cast<int>(e >> 23) - sp.x;               // stage row of j0 (< kWRows - 1)
-            const float t = static_cast<float>(e & 0x7FFFFFu) * (1.f / 8388608.f);   // exact
+            const double t = __ldg(ts[f] + static_cast<int64_t>(u) * Wa + x0 + i);
+            const float w0 = __double2float_rn(1.0 - t), w1 = __double2float_rn(t);   // each rounded once
             const bool ev = (r0 & 1) == 0;
-            const int re = ev ? r0 : r0 + 1, ro = ev ? r0 + 1 : r0;
-            const uint32_t la = ra != re, lb = rb != ro;
-            ra = re;
-            rb = ro;
-            s2.x = __float_as_uint(ev ? 1.f - t : t);                     // exact
-            s2.y = static_cast<uint32_t>(2 * re) | (static_cast<uint32_t>(2 * ro) << 8) | (la << 16) | (lb << 17) | kWOne;
+            ra = static_cast<uint32_t>(2 * (ev ? r0 : r0 + 1));
+            rb = static_cast<uint32_t>(2 * (ev ? r0 + 1 : r0));
+            w[i][0] = __float_as_uint(ev ? w0 : w1);
+            w[i][1] = __float_as_uint(ev ? w1 : w0);
         }
-        steps[base + i] = s2;
+        hdr[i / 2] |= (ra | (rb << 8)) << (16 * (i & 1));
     }
+    uint4* out = steps + (static_cast<int64_t>(f) * Wb + u) * (xpad / kWXW) * kWWalkU4 + static_cast<int64_t>(blk) * kWWalkU4;
+    out[0] = make_uint4(hdr[0], hdr[1], hdr[2], hdr[3]);
+    for (int q = 0; q < kWXW / 2; ++q) out[1 + q] = make_uint4(w[2 * q][0], w[2 * q][1], w[2 * q + 1][0], w[2 * q + 1][1]);
 }
 // mband(g, vb) = union over the group's planes and the block's B rows v of the A rows stage 2
 // reads, [lo_y(v), hi_y(v)] (tiles outside it are not computed)
@@ -542,7 +550,7 @@ bool stage1_w_supported(int Wa, int Hb) {
 
 cudaError_t launch_pack_w(const int32_t* const* i0s_dev, const double* const* ts_dev, const int32_t* const* ylo_dev,
                           const int32_t* const* yhi_dev, int n_planes, int Wa, int Wb, int Hb, uint32_t* ent,
-                          uint2* steps, int2* span, int2* mband, cudaStream_t st) {
+                          uint4* steps, int2* span, int2* mband, cudaStream_t st) {
     const int xpad = ((Wa + kWX - 1) / kWX) * kWX, n_xt = xpad / kWX;
     const int n_groups = (n_planes + kWF - 1) / kWF, n_vb = (Hb + kWV - 1) / kWV;
     pack_w_entries_kernel<<<dim3(Wb, n_planes), 128, 0, st>>>(i0s_dev, ts_dev, Wa, Wb, xpad, ent);
@@ -551,7 +559,8 @@ cudaError_t launch_pack_w(const int32_t* const* i0s_dev, const double* const* ts
     pack_w_span_kernel<<<dim3(Wb, n_groups, n_xt), kWX, 0, st>>>(ent, n_planes, Wb, xpad, n_xt, span);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    pack_w_steps_kernel<<<dim3(Wb, n_planes), ((xpad / kWXW + 31) / 32) * 32, 0, st>>>(ent, span, Wb, xpad, n_xt, steps);
+    pack_w_steps_kernel<<<dim3(Wb, n_planes), ((xpad / kWXW + 31) / 32) * 32, 0, st>>>(ent, ts_dev, span, Wa, Wb, xpad,
+                                                                                     n_xt, steps);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     pack_w_mband_kernel<<<dim3(n_vb, n_groups), kWV, 0, st>>>(ylo_dev, yhi_dev, n_planes, Hb, n_vb, mband);
