@@ -14,8 +14,9 @@
 // 256 contiguous bytes: conflict-free), i.e. alpha / 2 shared-memory bytes per tap instead of 4.  Skipped
 // samples and outputs outside the RoI add exact zeros without loads.
 //
-// The per-step logic is precomputed (pack_w_steps_kernel): a 64-bit step entry per (plane, u, x)
-// holds t, the byte offset of row j0 in the stage and the load action in the warp's walk order.
+// The per-step logic is precomputed (pack_w_steps_kernel): an 80-byte walk entry per (plane, u,
+// 8 outputs x) holds the stage rows of every step (a slot reloads when its row changes) and both
+// corner weights in fp32, each rounded once from fp64 (relative precision).
 //
 // Layout: Gamma with the B pixels in v-major order (include/cpi.h CPI_GAMMA_VMAJOR): column
 // q = u * H_b + v, so for one (A pixel (m, j), u) the v are contiguous.  A tile = (A row m, 128 B
