@@ -620,7 +620,7 @@ struct S2Args {
     float* plane[kS2MaxPlanes];
 };
 
-__global__ void __launch_bounds__(kS2Threads, 3)
+__global__ void __launch_bounds__(kS2Threads, 2)
 stage2_staged_kernel(S2Args a) {
     extern __shared__ __align__(16) uint8_t s2_smem[];
     const int f = blockIdx.y, x0 = blockIdx.x * kS2XB;
