@@ -83,7 +83,7 @@ struct cpi_ctx {
     size_t bws_bytes = 0;
     cpi::TElem* T[kS1Planes]{};
     bool refocus_ready = false;
-    int fuse = 4;                          // planes per Gamma pass in the TMA stage 1 (CPI_REFOCUS_FUSE)
+    int fuse = cpi::kStage1MaxFuse;        // planes per Gamma pass in the TMA stage 1 (CPI_REFOCUS_FUSE)
     uint32_t* xpack = nullptr;             // packed x-tables [kS1Planes][W_b][W_a]
     float* xwpack = nullptr;               // their near-t corner offsets [kS1Planes][W_b][W_a]
     uint2* ypack = nullptr;                // packed y-tables [kRefocusMaxFuse][H_b][H_a]
@@ -1455,7 +1455,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
         c->use_s1_tma = cpi::stage1_tma_supported(Wa, Wb, Hb) && getenv("CPI_STAGE1_SIMPLE") == nullptr;
         if (const char* ev = getenv("CPI_REFOCUS_FUSE")) c->fuse = atoi(ev);
         if (c->fuse < 1) c->fuse = 1;
-        if (c->fuse > cpi::kRefocusMaxFuse) c->fuse = cpi::kRefocusMaxFuse;
+        if (c->fuse > cpi::kStage1MaxFuse) c->fuse = cpi::kStage1MaxFuse;
         c->use_s2_staged = cpi::stage2_staged_supported(Ha) && getenv("CPI_STAGE2_SIMPLE") == nullptr;
         if (c->use_s2_staged)
             CK(c, cudaMalloc(&c->ypack, sizeof(uint2) * size_t(Ha) * Hb * cpi::kRefocusMaxFuse));
@@ -1476,6 +1476,10 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) return fail(c, CPI_ERR_CUDA, "x-table tensor map failed (%d)", int(r));
+            r = enc(&c->s1maps.xwtab, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, c->xwpack, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return fail(c, CPI_ERR_CUDA, "x-weight tensor map failed (%d)", int(r));
         }
         c->refocus_ready = true;
     }
@@ -1659,7 +1663,7 @@ cpi_status cpi_refocus(cpi_ctx* c, const cpi_refocus_spec* spec_in, float* plane
                 c->launches += 1;
             } else if (tma_now) {
                 e = cpi::launch_refocus_stage1_tma(&c->s1maps, nb, Wa, Ha, Wb, Hb, m_base, m_count, m_block, m_stride,
-                                                   c->xs, c->ys, c->T, c->xblk, c->xwpack, c->num_sms, st);
+                                                   c->xs, c->ys, c->T, c->xblk, c->num_sms, st);
                 c->launches += 1;
             } else if (!cyclic) {
                 e = cpi::launch_refocus_stage1(gsrc, c->p_b, Wa, Ha, Wb, Hb, m_base, m_count, c->xs[0], c->ys[0],

@@ -147,18 +147,20 @@ cudaError_t launch_refocus_stage1(const float* gamma, int64_t ldg, int Wa, int H
 // sharing one pass over Gamma.  Needs W_a <= 256 with W_a % 4 == 0, W_b % 4 == 0, W_b <= 512, H_b <= 256, the tensor maps of
 // Gamma (4D: u, v, j, m) and of the packed x-tables (3D uint32: x, u, plane slot).
 constexpr int kRefocusMaxFuse = 4;
+constexpr int kStage1MaxFuse = 2;   // planes per KB5 launch: x-tables and their fp32 weights share the ring
 constexpr int kS2MaxPlanes = 16;   // planes per staged stage-2 launch (more CTAs in flight over T)
 struct Stage1Maps {
     CUtensorMap gamma;       // 4D (u, v, j, m) row-major Gamma, or 5D (u%8, v, u/8, j, m) u-blocked
     CUtensorMap xtab;
+    CUtensorMap xwtab;       // the x-tables' fp32 near-t weights (same shape)
     int gamma_5d = 0;
 };
 bool stage1_tma_supported(int Wa, int Wb, int Hb);
 int stage1_vgroup(int Wa);   // B rows v per stage-1 tile (Gamma tensor-map box height)
 cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa, int Ha, int Wb, int Hb,
                                       int m_base, int m_count, int m_block, int m_stride, const AxisTables* xs,
-                                      const AxisTables* ys, TElem* const* T, const uint32_t* xblk, const float* xw,
-                                      int num_sms, cudaStream_t st);
+                                      const AxisTables* ys, TElem* const* T, const uint32_t* xblk, int num_sms,
+                                      cudaStream_t st);
 // x-tables of a fused group packed for the TMA stage 1: uint32 j_rel << 23 | round(t * 2^23),
 // [n_fuse][Wb][Wa] (see refocus.cu), and xblk[n_fuse][ceil(Wb / 8)]: bit b set if some
 // x in [16 b, 16 b + 16) has a used sample for some u of the 8-column chunk.

@@ -313,12 +313,13 @@ struct S1Cfg {
     static constexpr int kGFloats = (kJ + 2) * kRow;
     // both row capacities: ~66 KB Gamma stages (three fit next to one plane's x-tables, two next
     // to 2-4 planes' tables)
-    static constexpr int kStages = F == 1 ? 3 : 2;
+    static constexpr int kStages = 2;   // (3 for F = 1 before the weight tables joined the ring)
     // smem map (bytes): [Gamma stages (258 rows each)][x-table stages x F][span table]
     //                   [x-block masks][barriers]
     static constexpr int kOffX = kStages * kGFloats * 4;
     static constexpr int kXEntries = kTUC * kJ;             // x-table entries per (stage, plane) slot
-    static constexpr int kOffSpan = kOffX + kStages * F * kXEntries * 4;
+    static constexpr int kOffW = kOffX + kStages * F * kXEntries * 4;    // the x-tables' near-t weights
+    static constexpr int kOffSpan = kOffW + kStages * F * kXEntries * 4;
     static constexpr int kOffXblk = kOffSpan + kTMaxChunks * 8;
     static constexpr int kOffYb = kOffXblk + kTMaxChunks * 4;   // int2 [F][H_b <= 256] y bands
     static constexpr int kOffBar = kOffYb + F * 256 * 8;
@@ -334,7 +335,6 @@ struct S1Args {
     const int32_t* yhi[kRefocusMaxFuse];
     TElem* T[kRefocusMaxFuse];
     const uint32_t* xblk;                    // [F][n_chunks] x-block masks (OR-ed over F in smem)
-    const float* xw;                         // [F][W_b][W_a] near-t corner offsets (s1_taps)
     int gamma_5d;                            // Gamma map is 5D u-blocked (u%8, v, u/8, j, m)
 };
 
@@ -355,13 +355,17 @@ __device__ __forceinline__ unsigned tile_mask(const int2* yband, int Hb, int m, 
     return need;
 }
 
+#define C_SMEM_OK(F, kJ) (S1Cfg<F, kJ>::kSmem <= 232448)
 template <bool kFullX, int F, bool kSkip, int kJ>
 __global__ void __launch_bounds__(kTThreads, 1)
-stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_x, S1Args a) {
+stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_x,
+                  const __grid_constant__ CUtensorMap tm_w, S1Args a) {
+    static_assert(C_SMEM_OK(F, kJ), "stage-1 shared memory exceeds 227 KB");
     using C = S1Cfg<F, kJ>;
     extern __shared__ __align__(1024) uint8_t s1_smem[];
     float* sg = reinterpret_cast<float*>(s1_smem);
     const uint32_t* sx = reinterpret_cast<const uint32_t*>(s1_smem + C::kOffX);
+    const float* swt = reinterpret_cast<const float*>(s1_smem + C::kOffW);
     int2* span = reinterpret_cast<int2*>(s1_smem + C::kOffSpan);
     uint64_t* full = reinterpret_cast<uint64_t*>(s1_smem + C::kOffBar);
     uint64_t* empty = full + C::kStages;
@@ -409,6 +413,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
         if (lane == 0) {
             tma_prefetch_desc(&tm_g);
             tma_prefetch_desc(&tm_x);
+            tma_prefetch_desc(&tm_w);
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = t_first; tile < t_end; tile += t_step) {
@@ -422,7 +427,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                     if (sp.y < sp.x) continue;
                     const int nb = (sp.y - sp.x + kTJBox) / kTJBox;
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], nb * kTJBox * C::kRow * 4 + F * kTUC * a.Wa * 4);
+                    mbar_expect_tx(&full[stage], nb * kTJBox * C::kRow * 4 + 2 * F * kTUC * a.Wa * 4);
                     float* dst = sg + stage * C::kGFloats;
                     for (int b = 0; b < nb; ++b) {
                         if (a.gamma_5d)   // u-blocked Gamma: one 256-B segment per (j, chunk)
@@ -435,6 +440,10 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
 #pragma unroll
                     for (int f = 0; f < F; ++f)
                             tma_load_3d(s1_smem + C::kOffX + (stage * F + f) * C::kXEntries * 4, &tm_x, &full[stage], 0,
+                                        c * kTUC, f);
+#pragma unroll
+                    for (int f = 0; f < F; ++f)
+                            tma_load_3d(s1_smem + C::kOffW + (stage * F + f) * C::kXEntries * 4, &tm_w, &full[stage], 0,
                                         c * kTUC, f);
                     if (++stage == C::kStages) { stage = 0; phase ^= 1; }
                 }
@@ -483,6 +492,7 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
 #pragma unroll
                     for (int p = 0; p < NS / 2; ++p) part[f][i][p] = 0ull;
             const uint32_t* sxs = sx + stage * F * C::kXEntries + xbase;
+            const float* swx = swt + stage * F * C::kXEntries + xbase;   // the same entries' weights
             if constexpr (kSkip) {
                 // i-outer order with a warp-uniform skip of a 16-wide x block that has no used
                 // sample in this chunk for any plane of the group
@@ -496,13 +506,11 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
                     float sn[kTUC][F];
 #pragma unroll
                     for (int k = 0; k < kTUC; ++k) {
-                        const int uu = (k + xl) & (kTUC - 1), u = c * kTUC + uu;
+                        const int uu = (k + xl) & (kTUC - 1);
 #pragma unroll
                         for (int f = 0; f < F; ++f) {
                             ent[k][f] = sxs[f * C::kXEntries + uu * a.Wa + 128 * i];
-                            sn[k][f] = u < a.Wb && xbase + 128 * i < a.Wa
-                                           ? __ldg(a.xw + (static_cast<int64_t>(f) * a.Wb + u) * a.Wa + xbase + 128 * i)
-                                           : 0.f;
+                            sn[k][f] = swx[f * C::kXEntries + uu * a.Wa + 128 * i];
                         }
                     }
 #pragma unroll
@@ -515,15 +523,13 @@ stage1_tma_kernel(const __grid_constant__ CUtensorMap tm_g, const __grid_constan
             } else {
 #pragma unroll
                 for (int k = 0; k < kTUC; ++k) {
-                    const int uu = (k + xl) & (kTUC - 1), u = c * kTUC + uu;
+                    const int uu = (k + xl) & (kTUC - 1);
 #pragma unroll
                     for (int f = 0; f < F; ++f)
 #pragma unroll
                         for (int i = 0; i < NI; ++i)
                             if (kFullX || xbase + 128 * i < a.Wa) {
-                                const float sn = u < a.Wb ? __ldg(a.xw + (static_cast<int64_t>(f) * a.Wb + u) * a.Wa +
-                                                                  xbase + 128 * i)
-                                                          : 0.f;
+                                const float sn = swx[f * C::kXEntries + uu * a.Wa + 128 * i];
                                 s1_taps<NS, C::kRow>(part[f][i], sxs[f * C::kXEntries + uu * a.Wa + 128 * i], sn,
                                                      G + uu, voff);
                             }
@@ -1137,7 +1143,7 @@ static cudaError_t launch_s1(const Stage1Maps* maps, const S1Args& a, int grid, 
     // the attribute is per device: set it before every launch (a host-side call, negligible)
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, kTThreads, C::kSmem, st>>>(maps->gamma, maps->xtab, a);
+    kern<<<grid, kTThreads, C::kSmem, st>>>(maps->gamma, maps->xtab, maps->xwtab, a);
     return cudaGetLastError();
 }
 
@@ -1146,15 +1152,14 @@ static cudaError_t launch_s1_f(int F, const Stage1Maps* maps, const S1Args& a, i
     switch (F) {
         case 1: return launch_s1<kFullX, 1, kSkip, kJ>(maps, a, grid, st);
         case 2: return launch_s1<kFullX, 2, kSkip, kJ>(maps, a, grid, st);
-        case 3: return launch_s1<kFullX, 3, kSkip, kJ>(maps, a, grid, st);
-        default: return launch_s1<kFullX, 4, kSkip, kJ>(maps, a, grid, st);
+        default: return launch_s1<kFullX, 2, kSkip, kJ>(maps, a, grid, st);   // F <= 2 (kStage1MaxFuse)
     }
 }
 
 cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa, int Ha, int Wb, int Hb,
                                       int m_base, int m_count, int m_block, int m_stride, const AxisTables* xs,
-                                      const AxisTables* ys, TElem* const* T, const uint32_t* xblk, const float* xw,
-                                      int num_sms, cudaStream_t st) {
+                                      const AxisTables* ys, TElem* const* T, const uint32_t* xblk, int num_sms,
+                                      cudaStream_t st) {
     if (n_fuse < 1 || n_fuse > kRefocusMaxFuse) return cudaErrorInvalidValue;
     S1Args a{};
     a.Wa = Wa; a.Ha = Ha; a.Wb = Wb; a.Hb = Hb; a.m_base = m_base; a.m_count = m_count;
@@ -1163,7 +1168,6 @@ cudaError_t launch_refocus_stage1_tma(const Stage1Maps* maps, int n_fuse, int Wa
     a.n_vg = (Hb + stage1_vg(stage1_rows(Wa)) - 1) / stage1_vg(stage1_rows(Wa));
     a.n_chunks = (Wb + kTUC - 1) / kTUC;
     a.xblk = xblk;
-    a.xw = xw;
     a.gamma_5d = maps->gamma_5d;
     for (int f = 0; f < n_fuse; ++f) {
         a.xlo[f] = xs[f].lo; a.xhi[f] = xs[f].hi; a.ylo[f] = ys[f].lo; a.yhi[f] = ys[f].hi; a.T[f] = T[f];
